@@ -1,0 +1,233 @@
+/*
+ * h2.h -- C ABI of libh2: B200-native (sm_100a) bottom-up adaptive-sketching construction of
+ * symmetric H^2 matrices (Boukaram, Liu, Ghysels, Li, "Adaptive Sketching Based Construction of
+ * H2 Matrices on GPUs", arXiv 2506.16759; cited below as PAPER.md L<line>).
+ *
+ * The calls follow the paper's problem statement (Algorithm 1):
+ *   Input : sample block size d, a hierarchical partitioning, a relative tolerance eps,
+ *           a black-box sketch Y = K_blk(Omega) and a (batched) entry evaluator.
+ *   Output: skeleton indices I~_tau, leaf bases U_tau, transfer matrices E, dense blocks D,
+ *           coupling blocks B.
+ *
+ * Conventions (all entry points):
+ *   - Every index is a TREE-ORDER index (position after the KD-tree permutation) unless named
+ *     "original".  int64 for sizes/offsets, int32 for cluster-local quantities.
+ *   - Dense blocks are row-major.  Y and Omega are row-major N x ncols with a leading dimension.
+ *   - "dev" pointers are CUDA device memory of the current device, "host" pointers host memory.
+ *   - Every call returns h2_status; on failure h2_last_error() gives a thread-local message.
+ *     On failure nothing is leaked and any *out handle is set to NULL.
+ *   - Handles are owned by the library; free them with the matching *_free call.  A built
+ *     h2_matrix is immutable; h2_matvec may be called concurrently on different streams.
+ *     An h2_matrix references the h2_tree it was built on: free the tree last.
+ *   - stream arguments are cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are stream-ordered; h2_build synchronises the stream internally (it reads ranks
+ *     back to size the next level, "prefix sum ... single allocation").
+ */
+#ifndef H2_H
+#define H2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  H2_OK = 0,
+  H2_ERR_INVALID_ARG = -1,
+  H2_ERR_OOM = -2,
+  H2_ERR_CUDA = -3,
+  H2_ERR_CALLBACK = -5,      /* a user sketch/entry callback returned non-zero             */
+  H2_ERR_NOT_CONVERGED = -6, /* adaptive sampling hit d_max; stats.failed_depth says where */
+  H2_ERR_NONFINITE = -7      /* the sketch produced a non-finite sample                    */
+} h2_status;
+
+typedef struct h2_tree h2_tree;
+typedef struct h2_matrix h2_matrix;
+
+/* ---------------------------------------------------------------------------------------
+ * Partition (§II-A; Algorithm 1 input "a hierarchical partitioning", L200)
+ * KD-tree: complete binary tree, all leaves at depth Dl = min{D : ceil(n/2^D) <= leaf_size};
+ * split the longest bbox axis (ties -> lowest axis) at the median of the stable order
+ * (coordinate, original index), lower half ceil(m/2) points (R4).
+ * Admissibility Eq.(1): adm(s,t) = s != t and (D(s)+D(t))/2 <= eta * Dist(s,t), D = bbox
+ * diagonal, Dist = distance of bbox centres (H2_DIST_CENTER, R1) or minimum box-box
+ * distance (H2_DIST_BOX).  Dual traversal from (root, root) (L127).
+ * ------------------------------------------------------------------------------------- */
+enum { H2_DIST_CENTER = 0, H2_DIST_BOX = 1 };
+
+/* coords_host: n x dim row-major float64 in ORIGINAL order (1 <= dim <= 3, finite).
+ * leaf_size >= 2, eta > 0.  The tree keeps a host copy and uploads tree-ordered coordinates
+ * to the current device (used by the built-in kernels).  Errors: INVALID_ARG, OOM, CUDA. */
+h2_status h2_tree_build(const double* coords_host, int64_t n, int32_t dim, int32_t leaf_size,
+                        double eta, int32_t dist_rule, h2_tree** out);
+
+typedef struct {
+  int64_t n;
+  int32_t dim, leaf_size, leaf_depth; /* depth 0 = root; paper level l = leaf_depth - depth + 1 */
+  int32_t top_depth;                  /* coarsest depth with an admissible pair, -1 if none     */
+  int64_t near_nnz;                   /* ordered inadmissible leaf pairs (incl. (tau,tau))      */
+  int64_t far_nnz_total;              /* ordered admissible pairs over all depths               */
+  int32_t csp;                        /* sparsity constant C_sp (max blocks per block row)      */
+} h2_tree_info;
+h2_status h2_tree_get_info(const h2_tree* tree, h2_tree_info* info);
+
+/* Host copies of the partition.  perm[n] (tree index -> original index), begin/end of every
+ * cluster in heap order (node (depth t, index c) at position 2^t - 1 + c; total 2^(Dl+1)-1
+ * entries each), near pairs (near_nnz x 2, sorted), far pairs of one depth (sorted).
+ * Any output pointer may be NULL to skip it. */
+h2_status h2_tree_export(const h2_tree* tree, int64_t* perm, int64_t* begin, int64_t* end,
+                         int32_t* near_pairs);
+h2_status h2_tree_far_count(const h2_tree* tree, int32_t depth, int64_t* nnz);
+h2_status h2_tree_export_far(const h2_tree* tree, int32_t depth, int32_t* far_pairs);
+void h2_tree_free(h2_tree* tree);
+
+/* ---------------------------------------------------------------------------------------
+ * Operators.  Built-in kernels (§V-A) enable the fused device paths:
+ *   H2_K_EXP       K(x,y) = exp(-|x-y|/param)                (Eq. cov, l = 0.2 in L431)
+ *   H2_K_HELMHOLTZ K(x,y) = cos(param |x-y|)/|x-y|, 0 at x=y (Eq. ie, k = 3 in L439)
+ * ------------------------------------------------------------------------------------- */
+enum { H2_K_EXP = 0, H2_K_HELMHOLTZ = 1 };
+typedef struct {
+  int32_t kind;
+  double param;
+} h2_kernel;
+
+/* Sketch request handed to a callback sampler (Algorithm 1 line 1, "Y = K_blk(Omega)",
+ * PAPER.md L203/L216/L246).  Rows [row_begin,row_end) of Y for sample columns
+ * [col0, col0+ncols) must be written: y[(i-row_begin)*ld_y + j] = sum_k K(i,k) omega[k*ld_omega+j]
+ * for i in the row range (tree order).  omega holds ALL n rows.  Enqueue work on `stream`;
+ * do not synchronise it.  Return 0 on success, anything else aborts h2_build with
+ * H2_ERR_CALLBACK. */
+typedef struct {
+  int64_t n, row_begin, row_end;
+  int32_t col0, ncols;
+  const double* omega; /* dev */
+  int64_t ld_omega;
+  double* y;           /* dev */
+  int64_t ld_y;
+  void* stream;
+} h2_sketch_req;
+typedef int (*h2_sketch_fn)(void* ctx, const h2_sketch_req* req);
+
+enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1 };
+typedef struct {
+  int32_t kind;       /* H2_S_DENSE_KERNEL: Y = K Omega with the built-in kernel below (O(N^2)) */
+  h2_kernel kern;     /*                    H2_S_CALLBACK: fn(ctx, req)                          */
+  h2_sketch_fn fn;
+  void* ctx;
+} h2_sketch;
+
+/* Batched entry evaluator ("batched entry generator ... evaluate all D or B at a
+ * given level with a single kernel launch").  Block q: out[q][i*ld[q] + j] = K(row_idx[row_off[q]+i],
+ * col_idx[col_off[q]+j]) for i < m[q], j < nc[q] (tree-order indices).  All arrays are device
+ * arrays; `out` is a device array of device pointers.  Return 0 on success. */
+typedef struct {
+  int64_t nblocks;
+  const int32_t* m;
+  const int32_t* nc;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  const int32_t* row_idx;
+  const int32_t* col_idx;
+  double* const* out;
+  const int32_t* ld;
+  void* stream;
+} h2_block_batch;
+typedef int (*h2_entry_fn)(void* ctx, const h2_block_batch* batch);
+
+enum { H2_E_BUILTIN = 0, H2_E_CALLBACK = 1 };
+typedef struct {
+  int32_t kind;       /* H2_E_BUILTIN: entries of `kern` at the tree's coordinates              */
+  h2_kernel kern;
+  h2_entry_fn fn;
+  void* ctx;
+} h2_entry;
+
+/* ---------------------------------------------------------------------------------------
+ * Build options (R9-R13, R26)
+ * ------------------------------------------------------------------------------------- */
+enum { H2_TOL_RMS = 0, H2_TOL_LITERAL = 1 };
+typedef struct {
+  int32_t d_init;      /* initial samples (Algorithm 1 line 1)                          [32]  */
+  int32_t d_blk;       /* adaptive block: samples added per round (line 216/246)       [32]  */
+  int32_t d_max;       /* sample cap; reaching it -> H2_ERR_NOT_CONVERGED              [512] */
+  int32_t adaptive;    /* 1: §III-B convergence loop; 0: fixed sample size §III-A      [1]   */
+  int32_t tol_rule;    /* H2_TOL_RMS: eps_l = s*tol*||Y||_F/sqrt(N)  (R10/R11)         [RMS] */
+                       /* H2_TOL_LITERAL: eps_l = tol*norm (p_os = 0)          */
+  double tol_safety;   /* s                                                            [0.1] */
+  int32_t p_os;        /* oversampling margin: converged iff m<=d or k<=d-1-p_os (R12) [10]  */
+  double norm;         /* nu for H2_TOL_LITERAL                                        [0]   */
+  int32_t max_rank;    /* cap on every rank, <=0: none                                 [0]   */
+  uint64_t seed;       /* Omega stream key (Philox4x32-10, R8)               [1]   */
+  uint32_t stream_id;  /* Omega stream id (counter word 2)                             [0]   */
+} h2_build_opts;
+void h2_build_opts_default(h2_build_opts* opts);
+
+enum {
+  H2_PH_RAND = 0, H2_PH_SKETCH, H2_PH_GEN, H2_PH_BSR, H2_PH_CPQR, H2_PH_ID, H2_PH_MISC, H2_NPHASE
+};
+typedef struct {
+  int32_t samples;            /* d at exit                                                  */
+  int32_t failed_depth;       /* depth that hit d_max (H2_ERR_NOT_CONVERGED), else -1       */
+  int32_t top_depth, leaf_depth;
+  int32_t rounds[64];         /* convergence tests per depth                                */
+  int32_t rank_min[64], rank_max[64];
+  double rank_mean[64];
+  double eps;                 /* final eps_l                                                */
+  int64_t entries_D, entries_B; /* unique entries evaluated and stored                       */
+  int64_t entries_sketch;     /* kernel entries evaluated by the built-in dense sketch      */
+  int64_t bytes_U, bytes_E, bytes_B, bytes_D;
+  int64_t launches;           /* device kernel launches issued by h2_build                  */
+  double t_phase_ms[H2_NPHASE];
+  double t_total_ms;
+} h2_build_stats;
+
+/* Algorithm 1 on the current device.  tree: from h2_tree_build.  tol >= 0.
+ * sketch/entry: operators (see above).  stats may be NULL.  Errors: INVALID_ARG, OOM, CUDA,
+ * CALLBACK, NOT_CONVERGED, NONFINITE; *out = NULL on error. */
+h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                   const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats);
+
+/* y = alpha * K_H * x + beta * y for ncols right-hand sides (H^2 matvec: upward pass, couplings,
+ * downward pass, dense leaves).  x, y: dev, tree-order rows, row-major with leading dims
+ * ldx, ldy >= ncols.  1 <= ncols <= 64. */
+h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y, int64_t ldy,
+                    int32_t ncols, double alpha, double beta, void* stream);
+
+/* Built-in dense operator product, rows [row_begin,row_end): y = K(rows,:) * omega (the dense
+ * sketch of BASELINE configs[1], also the multi-GPU row shard).  omega: dev, all n rows. */
+h2_status h2_dense_sketch(const h2_tree* tree, h2_kernel kern, int64_t row_begin, int64_t row_end,
+                          const double* omega, int64_t ld_omega, int32_t ncols, double* y,
+                          int64_t ld_y, void* stream);
+
+/* Omega stream (Philox4x32-10 + Box-Muller, R8): rows [row0,row0+nrows) x sample
+ * columns [col0,col0+ncols) into out (dev, row-major, leading dim ld). */
+h2_status h2_omega(uint64_t seed, uint32_t stream_id, int64_t row0, int64_t nrows, int32_t col0,
+                   int32_t ncols, double* out, int64_t ld, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Inspection (tests, verification).  Sizes first, then copies into caller buffers (host or
+ * device: the copy kind is inferred).  Layouts:
+ *   rank[t]   : int32 per cluster of depth t, for top_depth <= t <= leaf_depth
+ *   skel[t]   : int32, concatenated I~_tau in pivot order (offsets = prefix sum of rank)
+ *   basis[t]  : float64, concatenated row-major X_tau (m_tau x k_tau): U_tau at the leaf depth,
+ *               [E_nu1; E_nu2] above (m_tau = k_nu1 + k_nu2), offsets = prefix sum m*k
+ *   D         : float64, unique near pairs (s <= b) in sorted order, each m_s x m_b row-major
+ *   B[t]      : float64, unique far pairs (s < b) of depth t in sorted order, k_s x k_b
+ *   cert[t]   : float64 pairs (min pivot gap, stop margin) per cluster (CPQR certification)
+ * ------------------------------------------------------------------------------------- */
+enum { H2_X_RANK = 0, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT };
+h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_t* count);
+h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst);
+h2_status h2_matrix_get_stats(const h2_matrix* H, h2_build_stats* stats);
+int64_t h2_matrix_device_bytes(const h2_matrix* H);
+void h2_free(h2_matrix* H);
+
+const char* h2_last_error(void);
+const char* h2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2_H */

@@ -47,6 +47,7 @@ class H2Matrix:
     skel: dict = field(default_factory=dict)     # depth -> list of int64 arrays
     X: dict = field(default_factory=dict)        # depth -> list of bases (U at leaves, [E1;E2] above)
     ids: dict = field(default_factory=dict)      # depth -> list of RowID (certification data)
+    panels: dict = field(default_factory=dict)   # depth -> list of Y^loc_tau (m x d) at commit
     D: dict = field(default_factory=dict)        # (s, b) -> block, leaf depth
     B: dict = field(default_factory=dict)        # depth -> {(s, b): block}
     samples: int = 0
@@ -166,6 +167,7 @@ def build(tree, part, sampler, entry, omega, tol, opts: BuildOpts = None) -> H2M
         H.eps = eps
         # lines 221-224 / 250-253: ID, skeletons
         H.ids[t] = ids
+        H.panels[t] = Yl                          # Y^loc_tau at the final d (verification data)
         H.X[t] = [i.X for i in ids]
         H.rank[t] = np.array([i.k for i in ids], np.int64)
         if t == Dl:

@@ -1,0 +1,904 @@
+// libh2 C ABI + host driver of Algorithm 1: the level loop, the adaptive
+// sample controller (§III-B, updateSamples L386) and the marshaling of per-level
+// batch descriptors (§IV-A).  Every arithmetic step runs in the sm_100a kernels of
+// sketch.cu / gen_bsr.cu / cpqr.cu / matvec.cu; the host only sizes levels (prefix sums of
+// ranks read back once per convergence test) and launches.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.hpp"
+#include "tree.hpp"
+
+namespace h2 {
+thread_local int64_t g_launches = 0;
+void count_launch() { ++g_launches; }
+}  // namespace h2
+
+namespace {
+
+thread_local std::string g_err;
+
+// Stream-ordered device array from the device's default memory pool.  The pool keeps freed
+// memory mapped (release threshold = max, set once per device), so the per-level "single
+// allocation per operation" of PAPER.md L384 costs no page mapping after the first build.
+void retain_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  int64_t n = 0;
+  cudaStream_t st = 0;     // stream the array is freed on (stream order)
+  DArr() = default;
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+  DArr(DArr&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+  DArr& operator=(DArr&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      st = o.st;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DArr() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    n = 0;
+  }
+  // arrays that outlive the build (the H^2 matrix) are freed on the legacy default stream
+  void detach() { st = 0; }
+  void alloc(int64_t cnt, cudaStream_t stream) {
+    release();
+    n = cnt;
+    st = stream;
+    H2_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * std::max<int64_t>(cnt, 1), stream));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc((int64_t)v.size(), st);
+    if (!v.empty()) H2_CUDA(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  }
+  int64_t bytes() const { return p ? (int64_t)sizeof(T) * std::max<int64_t>(n, 1) : 0; }
+};
+
+// one processed depth t of the basis tree
+struct Level {
+  int t = 0;
+  int32_t nclus = 0;
+  std::vector<int32_t> m, k;
+  std::vector<int64_t> poff, roff, xoff;
+  int64_t rows = 0, rtot = 0, xtot = 0;
+  int32_t max_m = 0, max_k = 0;
+  DArr<int32_t> d_m, d_k, d_perm, d_skel;
+  DArr<int64_t> d_poff, d_roff, d_xoff;
+  DArr<double> X, cert;
+  // couplings of this depth (unique far pairs, s < b)
+  std::vector<int64_t> B_off;
+  DArr<int64_t> d_B_off;
+  DArr<double> B;
+  // panels of this depth: Y^loc / Omega^l (rows x LD); leaf depth aliases the sketch buffers
+  DArr<double> Yl, Ol;
+};
+
+}  // namespace
+
+struct h2_matrix {
+  std::shared_ptr<h2_tree> tree;
+  int top = 0, Dl = 0;
+  int64_t n = 0;
+  std::vector<Level> lv;   // index t - top
+  DArr<double> D;
+  h2_build_stats stats{};
+  Level& L(int t) { return lv[t - top]; }
+  const Level& L(int t) const { return lv[t - top]; }
+};
+
+namespace {
+
+using namespace h2;
+
+struct PhaseTimer {
+  cudaStream_t st;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  int cur = -1;
+  cudaEvent_t cur_ev{};
+  explicit PhaseTimer(cudaStream_t s) : st(s) {}
+  void begin(int ph) {
+    cudaEvent_t e;
+    H2_CUDA(cudaEventCreate(&e));
+    H2_CUDA(cudaEventRecord(e, st));
+    cur = ph;
+    cur_ev = e;
+  }
+  void end() {
+    cudaEvent_t e;
+    H2_CUDA(cudaEventCreate(&e));
+    H2_CUDA(cudaEventRecord(e, st));
+    ev.push_back({cur, {cur_ev, e}});
+  }
+  void collect(double* out) {
+    for (auto& x : ev) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, x.second.first, x.second.second);
+      out[x.first] += ms;
+    }
+  }
+  ~PhaseTimer() {
+    for (auto& x : ev) {
+      cudaEventDestroy(x.second.first);
+      cudaEventDestroy(x.second.second);
+    }
+  }
+};
+
+template <class T>
+std::vector<T> download(const DArr<T>& a, int64_t n, cudaStream_t st) {
+  std::vector<T> v(n);
+  if (n) H2_CUDA(cudaMemcpyAsync(v.data(), a.p, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+  H2_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+struct Builder {
+  const h2_tree& T;
+  const h2_sketch& S;
+  const h2_entry& E;
+  double tol;
+  h2_build_opts o;
+  cudaStream_t st;
+  h2_matrix& H;
+  KernelParams ekp{}, skp{};
+  int64_t LD = 0;
+  int d = 0;
+  DArr<double> Y, Om;           // leaf-level sketch / random vectors (N x LD)
+  DArr<double> sumsq_scratch, sumsq_acc;
+  DArr<int> nonfinite;
+  DArr<double> W;               // CPQR workspace
+  DArr<int32_t> d_leaf_cnt32;   // leaf sizes as int32
+  PhaseTimer timer;
+  int64_t entries_sketch = 0;
+
+  Builder(const h2_tree& t, const h2_sketch& s, const h2_entry& e, double tl, const h2_build_opts& op,
+          cudaStream_t stream, h2_matrix& h)
+      : T(t), S(s), E(e), tol(tl), o(op), st(stream), H(h), timer(stream) {}
+
+  // ---------------------------------------------------------------- sketch of columns [c0, c1)
+  void draw(int c0, int c1) {
+    timer.begin(H2_PH_RAND);
+    launch_omega(o.seed, o.stream_id, 0, T.n, c0, c1 - c0, Om.p + c0, LD, st);
+    timer.end();
+    timer.begin(H2_PH_SKETCH);
+    if (S.kind == H2_S_DENSE_KERNEL) {
+      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om.p + c0, LD, c1 - c0, Y.p + c0, LD, st);
+      entries_sketch += T.n * T.n;
+    } else {
+      h2_sketch_req rq{};
+      rq.n = T.n;
+      rq.row_begin = 0;
+      rq.row_end = T.n;
+      rq.col0 = c0;
+      rq.ncols = c1 - c0;
+      rq.omega = Om.p + c0;
+      rq.ld_omega = LD;
+      rq.y = Y.p + c0;
+      rq.ld_y = LD;
+      rq.stream = st;
+      int rc = S.fn(S.ctx, &rq);
+      if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+    }
+    timer.end();
+    timer.begin(H2_PH_MISC);
+    launch_sumsq(Y.p, T.n, LD, c0, c1, sumsq_scratch.p, sumsq_acc.p, nonfinite.p, st);
+    timer.end();
+  }
+
+  double eps_now() {
+    double acc = 0;
+    int nf = 0;
+    H2_CUDA(cudaMemcpyAsync(&acc, sumsq_acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaMemcpyAsync(&nf, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaStreamSynchronize(st));
+    if (nf) throw Error(H2_ERR_NONFINITE, "the sketch produced a non-finite sample");
+    if (o.tol_rule == H2_TOL_RMS) return o.tol_safety * tol * std::sqrt(acc / (double)T.n);
+    return tol * o.norm;
+  }
+
+  // ---------------------------------------------------------------- batched entry generation
+  void gen(const GenArgs& g) {
+    if (g.nblocks == 0) return;
+    timer.begin(H2_PH_GEN);
+    if (E.kind == H2_E_BUILTIN) {
+      launch_gen(ekp, T.d_x, T.d_y, T.d_z, g, st);
+    } else {
+      DArr<int32_t> m, nc, ld;
+      DArr<int64_t> ro, co;
+      DArr<double*> outp;
+      m.alloc(g.nblocks, st);
+      nc.alloc(g.nblocks, st);
+      ld.alloc(g.nblocks, st);
+      ro.alloc(g.nblocks, st);
+      co.alloc(g.nblocks, st);
+      outp.alloc(g.nblocks, st);
+      launch_gen_batch_desc(g, m.p, nc.p, ro.p, co.p, outp.p, ld.p, st);
+      h2_block_batch bb{g.nblocks, m.p, nc.p, ro.p, co.p, g.idx, g.idx, outp.p, ld.p, st};
+      int rc = E.fn(E.ctx, &bb);
+      if (rc != 0) throw Error(H2_ERR_CALLBACK, "entry callback returned " + std::to_string(rc));
+      H2_CUDA(cudaStreamSynchronize(st));
+    }
+    timer.end();
+  }
+
+  // ---------------------------------------------------------------- BSR subtraction at depth t
+  // leaf (t == Dl): Y(I_tau) -= sum_{b in N_tau} D Om(I_b)   (L213)
+  // inner: Yl_t(rows of child nu) -= sum_{b in F_nu} B_{nu,b} Ol_t(rows of b)   (L240-243)
+  void bsr(int t, int c0, int c1) {
+    timer.begin(H2_PH_BSR);
+    BsrArgs a{};
+    a.c0 = c0;
+    a.ncols = c1 - c0;
+    if (t == T.Dl) {
+      a.nclusters = 1 << T.Dl;
+      a.max_rows = H.L(T.Dl).max_m;
+      a.yoff = a.ooff = T.d_leaf_begin;
+      a.cnt = T.d_leaf_size;
+      a.ptr = T.d_near.ptr;
+      a.idx = T.d_near.idx;
+      a.uidx = T.d_near.uidx;
+      a.us = T.d_near.us;
+      a.blk_off = T.d_D_off;
+      a.blk = H.D.p;
+      a.Y = Y.p;
+      a.Om = Om.p;
+    } else {
+      Level& C = H.L(t + 1);
+      Level& P = H.L(t);
+      a.nclusters = C.nclus;
+      a.max_rows = C.max_k;
+      a.yoff = a.ooff = C.d_roff.p;
+      a.cnt = C.d_k.p;
+      a.ptr = T.d_far[t + 1].ptr;
+      a.idx = T.d_far[t + 1].idx;
+      a.uidx = T.d_far[t + 1].uidx;
+      a.us = T.d_far[t + 1].us;
+      a.blk_off = C.d_B_off.p;
+      a.blk = C.B.p;
+      a.Y = P.Yl.p;
+      a.Om = P.Ol.p;
+    }
+    a.ldy = a.ldo = LD;
+    launch_bsr(a, st);
+    timer.end();
+  }
+
+  // ---------------------------------------------------------------- level set-up
+  void setup_level(int t) {
+    Level& L = H.L(t);
+    L.t = t;
+    L.nclus = 1 << t;
+    L.m.resize(L.nclus);
+    L.poff.resize(L.nclus);
+    if (t == T.Dl) {
+      for (int c = 0; c < L.nclus; ++c) {
+        L.m[c] = (int32_t)(T.end[t][c] - T.begin[t][c]);
+        L.poff[c] = T.begin[t][c];
+      }
+    } else {
+      const Level& C = H.L(t + 1);
+      for (int c = 0; c < L.nclus; ++c) {
+        L.m[c] = C.k[2 * c] + C.k[2 * c + 1];
+        L.poff[c] = C.roff[2 * c];
+      }
+    }
+    L.rows = 0;
+    L.max_m = 0;
+    for (int c = 0; c < L.nclus; ++c) {
+      L.rows += L.m[c];
+      L.max_m = std::max(L.max_m, L.m[c]);
+    }
+    L.d_m.upload(L.m, st);
+    L.d_poff.upload(L.poff, st);
+    L.d_k.alloc(L.nclus, st);
+    L.d_perm.alloc(std::max<int64_t>(L.rows, 1), st);
+    L.cert.alloc(2 * L.nclus, st);
+  }
+
+  // CPQR of every panel of depth t with the current d; returns host ranks
+  void cpqr(int t, double eps) {
+    Level& L = H.L(t);
+    int64_t need = std::max<int64_t>(L.rows * d, 1);
+    if (W.n < need) W.alloc(need, st);
+    timer.begin(H2_PH_CPQR);
+    CpqrArgs a{};
+    a.nclusters = L.nclus;
+    a.max_m = std::max(L.max_m, 1);
+    a.Y = (t == T.Dl) ? Y.p : L.Yl.p;
+    a.ldy = LD;
+    a.poff = L.d_poff.p;
+    a.m = L.d_m.p;
+    a.d = d;
+    a.eps = eps;
+    a.kmax = o.max_rank;
+    a.W = W.p;
+    a.k = L.d_k.p;
+    a.perm = L.d_perm.p;
+    a.cert = L.cert.p;
+    launch_cpqr(a, st);
+    timer.end();
+    L.k = download(L.d_k, L.nclus, st);
+  }
+
+  void commit(int t) {
+    Level& L = H.L(t);
+    L.roff.assign(L.nclus, 0);
+    L.xoff.assign(L.nclus, 0);
+    L.rtot = L.xtot = 0;
+    L.max_k = 0;
+    for (int c = 0; c < L.nclus; ++c) {
+      L.roff[c] = L.rtot;
+      L.xoff[c] = L.xtot;
+      L.rtot += L.k[c];
+      L.xtot += (int64_t)L.m[c] * L.k[c];
+      L.max_k = std::max(L.max_k, L.k[c]);
+    }
+    L.d_roff.upload(L.roff, st);
+    L.d_xoff.upload(L.xoff, st);
+    L.X.alloc(L.xtot, st);
+    L.d_skel.alloc(L.rtot, st);
+    timer.begin(H2_PH_ID);
+    IdArgs a{};
+    a.nclusters = L.nclus;
+    a.W = W.p;
+    a.d = d;
+    a.poff = L.d_poff.p;
+    a.m = L.d_m.p;
+    a.k = L.d_k.p;
+    a.perm = L.d_perm.p;
+    a.xoff = L.d_xoff.p;
+    a.X = L.X.p;
+    a.ibar = (t == T.Dl) ? T.d_iota : H.L(t + 1).d_skel.p;
+    a.roff = L.d_roff.p;
+    a.skel = L.d_skel.p;
+    launch_id(a, st);
+    timer.end();
+  }
+
+  // shrink + project committed depth u for columns [c0,c1) into the panels of depth u-1
+  void shrink(int u, int c0, int c1) {
+    Level& L = H.L(u);
+    Level& P = H.L(u - 1);
+    timer.begin(H2_PH_ID);
+    ShrinkArgs a{};
+    a.nclusters = L.nclus;
+    a.poff = L.d_poff.p;
+    a.m = L.d_m.p;
+    a.k = L.d_k.p;
+    a.perm = L.d_perm.p;
+    a.xoff = L.d_xoff.p;
+    a.X = L.X.p;
+    a.roff = L.d_roff.p;
+    a.Yl = (u == T.Dl) ? Y.p : L.Yl.p;
+    a.Ol = (u == T.Dl) ? Om.p : L.Ol.p;
+    a.ld = LD;
+    a.Yp = P.Yl.p;
+    a.Op = P.Ol.p;
+    a.ldp = LD;
+    a.c0 = c0;
+    a.c1 = c1;
+    launch_shrink_project(a, st);
+    timer.end();
+  }
+
+  void gen_B(int t) {
+    Level& L = H.L(t);
+    const PairCSR& F = T.far[t];
+    L.B_off.assign(F.nuniq() + 1, 0);
+    for (int64_t u = 0; u < F.nuniq(); ++u)
+      L.B_off[u + 1] = L.B_off[u] + (int64_t)L.k[F.us[u]] * L.k[F.ub[u]];
+    L.d_B_off.upload(L.B_off, st);
+    L.B.alloc(L.B_off.back(), st);
+    GenArgs g{};
+    g.nblocks = F.nuniq();
+    g.us = T.d_far[t].us;
+    g.ub = T.d_far[t].ub;
+    g.cnt = L.d_k.p;
+    g.off = L.d_roff.p;
+    g.idx = L.d_skel.p;
+    g.out_off = L.d_B_off.p;
+    g.out = L.B.p;
+    gen(g);
+  }
+
+  void run() {
+    const int Dl = T.Dl;
+    const int top = T.top < 0 ? Dl : T.top;
+    H.top = top;
+    H.Dl = Dl;
+    H.n = T.n;
+    H.lv.resize(Dl - top + 1);
+    if (S.kind == H2_S_DENSE_KERNEL) skp = make_kernel(S.kern);
+    if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
+    LD = o.d_max;
+    d = std::min(o.d_init, o.d_max);
+    Y.alloc(T.n * LD, st);
+    Om.alloc(T.n * LD, st);
+    sumsq_scratch.alloc(div_up(T.n, 1024), st);
+    sumsq_acc.alloc(1, st);
+    nonfinite.alloc(1, st);
+    H2_CUDA(cudaMemsetAsync(sumsq_acc.p, 0, sizeof(double), st));
+    H2_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+
+    // line 1: Y = K_blk(Omega)
+    draw(0, d);
+    // line 212: D_{tau,b} = K(I_tau, I_b), one unique block per unordered pair
+    H.D.alloc(T.D_off.back(), st);
+    {
+      GenArgs g{};
+      g.nblocks = T.near.nuniq();
+      g.us = T.d_near.us;
+      g.ub = T.d_near.ub;
+      g.cnt = T.d_leaf_size;
+      g.off = T.d_leaf_begin;
+      g.idx = T.d_iota;
+      g.out_off = T.d_D_off;
+      g.out = H.D.p;
+      gen(g);
+    }
+    setup_level(Dl);
+    bsr(Dl, 0, d);   // line 213
+    for (int t = Dl; t >= top; --t) {
+      if (t < Dl) {
+        setup_level(t);
+        bsr(t, 0, d);   // lines 240-243
+      }
+      Level& L = H.L(t);
+      int rounds = 0;
+      double eps = 0;
+      while (true) {
+        eps = eps_now();
+        cpqr(t, eps);
+        ++rounds;
+        if (!o.adaptive) break;
+        bool conv = true;
+        const int pos = (o.tol_rule == H2_TOL_RMS) ? o.p_os : 0;
+        for (int c = 0; c < L.nclus && conv; ++c) conv = (L.m[c] <= d) || (L.k[c] <= d - 1 - pos);
+        if (conv) break;
+        if (d + o.d_blk > o.d_max) {
+          H.stats.failed_depth = t;
+          throw Error(H2_ERR_NOT_CONVERGED, "adaptive sampling reached d_max=" + std::to_string(o.d_max) +
+                                                " at depth " + std::to_string(t));
+        }
+        // updateSamples (L216-217, L246-247, L386): new block, swept up to depth t
+        const int c0 = d, c1 = d + o.d_blk;
+        draw(c0, c1);
+        bsr(Dl, c0, c1);
+        for (int u = Dl; u > t; --u) {
+          shrink(u, c0, c1);
+          bsr(u - 1, c0, c1);
+        }
+        d = c1;
+      }
+      H.stats.rounds[t] = rounds;
+      H.stats.eps = eps;
+      commit(t);                                    // lines 221-224 / 250-253
+      if (t > top) {
+        Level& P = H.L(t - 1);
+        P.Yl.alloc(std::max<int64_t>(L.rtot, 1) * LD, st);
+        P.Ol.alloc(std::max<int64_t>(L.rtot, 1) * LD, st);
+        shrink(t, 0, d);
+      }
+      gen_B(t);                                     // line 258
+    }
+    H2_CUDA(cudaStreamSynchronize(st));
+    for (auto& L : H.lv) {   // sample panels are build scratch, not part of the H^2 matrix
+      L.Yl.release();
+      L.Ol.release();
+      for (auto* a : {&L.d_m, &L.d_k, &L.d_perm, &L.d_skel}) a->detach();
+      for (auto* a : {&L.d_poff, &L.d_roff, &L.d_xoff, &L.d_B_off}) a->detach();
+      for (auto* a : {&L.X, &L.cert, &L.B}) a->detach();
+    }
+    H.D.detach();
+    // stats
+    h2_build_stats& s = H.stats;
+    s.samples = d;
+    s.top_depth = top;
+    s.leaf_depth = Dl;
+    s.entries_D = T.D_off.back();
+    s.entries_sketch = entries_sketch;
+    s.bytes_D = H.D.bytes();
+    for (int t = top; t <= Dl; ++t) {
+      const Level& L = H.L(t);
+      int mn = INT32_MAX, mx = 0;
+      double sum = 0;
+      for (int c = 0; c < L.nclus; ++c) {
+        mn = std::min(mn, L.k[c]);
+        mx = std::max(mx, L.k[c]);
+        sum += L.k[c];
+      }
+      s.rank_min[t] = mn;
+      s.rank_max[t] = mx;
+      s.rank_mean[t] = sum / L.nclus;
+      s.entries_B += L.B_off.back();
+      s.bytes_B += L.B.bytes();
+      if (t == Dl) s.bytes_U += L.X.bytes();
+      else s.bytes_E += L.X.bytes();
+    }
+    timer.collect(s.t_phase_ms);
+  }
+};
+
+// the tree is built on the host; its device mirror is created on first use (current device)
+void ensure_uploaded(const h2_tree* tree) {
+  h2_tree* T = const_cast<h2_tree*>(tree);
+  int dev = 0;
+  H2_CUDA(cudaGetDevice(&dev));
+  if (T->device < 0) tree_upload(*T);
+  H2_REQUIRE(dev == T->device, "libh2: the tree was uploaded to another device");
+}
+
+h2_status fail(const Error& e) {
+  g_err = e.what();
+  return e.status;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+const char* h2_last_error(void) { return g_err.c_str(); }
+const char* h2_version(void) { return "libh2 0.1 (sm_100a)"; }
+
+h2_status h2_tree_build(const double* coords_host, int64_t n, int32_t dim, int32_t leaf_size, double eta,
+                        int32_t dist_rule, h2_tree** out) {
+  if (!out) return (g_err = "h2_tree_build: out is NULL", H2_ERR_INVALID_ARG);
+  *out = nullptr;
+  try {
+    H2_REQUIRE(coords_host != nullptr, "h2_tree_build: coords is NULL");
+    auto* T = new h2_tree();
+    std::unique_ptr<h2_tree> guard(T);
+    tree_build_host(*T, coords_host, n, dim, leaf_size, eta, dist_rule);   // device upload is lazy
+    *out = guard.release();
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    g_err = "h2_tree_build: host out of memory";
+    return H2_ERR_OOM;
+  }
+}
+
+h2_status h2_tree_get_info(const h2_tree* T, h2_tree_info* info) {
+  if (!T || !info) return (g_err = "h2_tree_get_info: NULL argument", H2_ERR_INVALID_ARG);
+  info->n = T->n;
+  info->dim = T->dim;
+  info->leaf_size = T->leaf_size;
+  info->leaf_depth = T->Dl;
+  info->top_depth = T->top;
+  info->near_nnz = T->near.nnz();
+  info->far_nnz_total = 0;
+  for (auto& f : T->far) info->far_nnz_total += f.nnz();
+  info->csp = T->csp;
+  return H2_OK;
+}
+
+h2_status h2_tree_export(const h2_tree* T, int64_t* perm, int64_t* begin, int64_t* end, int32_t* near_pairs) {
+  if (!T) return (g_err = "h2_tree_export: NULL tree", H2_ERR_INVALID_ARG);
+  if (perm) std::memcpy(perm, T->perm.data(), sizeof(int64_t) * T->n);
+  int64_t pos = 0;
+  for (int t = 0; t <= T->Dl; ++t)
+    for (size_t c = 0; c < T->begin[t].size(); ++c, ++pos) {
+      if (begin) begin[pos] = T->begin[t][c];
+      if (end) end[pos] = T->end[t][c];
+    }
+  if (near_pairs) {
+    for (int64_t s = 0; s < (int64_t)T->near.ptr.size() - 1; ++s)
+      for (int e = T->near.ptr[s]; e < T->near.ptr[s + 1]; ++e) {
+        near_pairs[2 * e] = (int32_t)s;
+        near_pairs[2 * e + 1] = T->near.idx[e];
+      }
+  }
+  return H2_OK;
+}
+
+h2_status h2_tree_far_count(const h2_tree* T, int32_t depth, int64_t* nnz) {
+  if (!T || !nnz || depth < 0 || depth > T->Dl) return (g_err = "h2_tree_far_count: bad argument", H2_ERR_INVALID_ARG);
+  *nnz = T->far[depth].nnz();
+  return H2_OK;
+}
+
+h2_status h2_tree_export_far(const h2_tree* T, int32_t depth, int32_t* far_pairs) {
+  if (!T || !far_pairs || depth < 0 || depth > T->Dl)
+    return (g_err = "h2_tree_export_far: bad argument", H2_ERR_INVALID_ARG);
+  const PairCSR& F = T->far[depth];
+  for (int64_t s = 0; s < (int64_t)F.ptr.size() - 1; ++s)
+    for (int e = F.ptr[s]; e < F.ptr[s + 1]; ++e) {
+      far_pairs[2 * e] = (int32_t)s;
+      far_pairs[2 * e + 1] = F.idx[e];
+    }
+  return H2_OK;
+}
+
+void h2_tree_free(h2_tree* T) { delete T; }
+
+void h2_build_opts_default(h2_build_opts* o) {
+  if (!o) return;
+  o->d_init = 32;
+  o->d_blk = 32;
+  o->d_max = 512;
+  o->adaptive = 1;
+  o->tol_rule = H2_TOL_RMS;
+  o->tol_safety = 0.1;
+  o->p_os = 10;
+  o->norm = 0.0;
+  o->max_rank = 0;
+  o->seed = 1;
+  o->stream_id = 0;
+}
+
+h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                   const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats) {
+  if (!out) return (g_err = "h2_build: out is NULL", H2_ERR_INVALID_ARG);
+  *out = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  h2_build_opts o;
+  h2_build_opts_default(&o);
+  if (opts) o = *opts;
+  auto* H = new h2_matrix();
+  std::memset(&H->stats, 0, sizeof(H->stats));
+  H->stats.failed_depth = -1;
+  int64_t launches0 = h2::g_launches;
+  auto t0 = std::chrono::steady_clock::now();
+  retain_pool_memory();
+  try {
+    H2_REQUIRE(tree && sketch && entry, "h2_build: NULL tree/sketch/entry");
+    H2_REQUIRE(tol >= 0 && std::isfinite(tol), "h2_build: tol must be finite and >= 0");
+    H2_REQUIRE(o.d_init >= 1 && o.d_blk >= 1 && o.d_max >= o.d_init, "h2_build: need 1 <= d_init <= d_max, d_blk >= 1");
+    H2_REQUIRE(o.tol_rule == H2_TOL_RMS || o.tol_rule == H2_TOL_LITERAL, "h2_build: bad tol_rule");
+    H2_REQUIRE(o.tol_rule != H2_TOL_LITERAL || o.norm > 0, "h2_build: literal tolerance needs opts.norm > 0");
+    H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn),
+               "h2_build: bad sketch");
+    H2_REQUIRE(entry->kind == H2_E_BUILTIN || (entry->kind == H2_E_CALLBACK && entry->fn), "h2_build: bad entry");
+    for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
+                               entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
+      if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
+    ensure_uploaded(tree);
+    // the tree is owned by the caller; share it without taking ownership
+    H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
+    {
+      Builder B(*tree, *sketch, *entry, tol, o, st, *H);
+      B.run();
+    }
+    H->stats.launches = h2::g_launches - launches0;
+    H->stats.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = H->stats;
+    *out = H;
+    return H2_OK;
+  } catch (const Error& e) {
+    if (stats) {
+      *stats = H->stats;
+    }
+    cudaStreamSynchronize(st);
+    delete H;
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    delete H;
+    g_err = "h2_build: host out of memory";
+    return H2_ERR_OOM;
+  }
+}
+
+h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
+                    double beta, void* stream) {
+  try {
+    H2_REQUIRE(H && x && y, "h2_matvec: NULL argument");
+    H2_REQUIRE(q >= 1 && q <= 64 && ldx >= q && ldy >= q, "h2_matvec: need 1 <= ncols <= 64, ld >= ncols");
+    cudaStream_t st = (cudaStream_t)stream;
+    const h2_tree& T = *H->tree;
+    const int Dl = H->Dl, top = H->top;
+    std::vector<DArr<double>> xh(Dl + 1), yh(Dl + 1);
+    for (int t = top; t <= Dl; ++t) {
+      const Level& L = H->L(t);
+      xh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
+      yh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
+      H2_CUDA(cudaMemsetAsync(yh[t].p, 0, sizeof(double) * std::max<int64_t>(L.rtot, 1) * q, st));
+    }
+    if (beta != 1.0) launch_scale(y, T.n, ldy, q, beta, st);
+    // upward pass
+    for (int t = Dl; t >= top; --t) {
+      const Level& L = H->L(t);
+      UpArgs a{};
+      a.nclusters = L.nclus;
+      a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
+      a.m = L.d_m.p;
+      a.k = L.d_k.p;
+      a.xoff = L.d_xoff.p;
+      a.X = L.X.p;
+      a.roff = L.d_roff.p;
+      a.xin = (t == Dl) ? x : xh[t + 1].p;
+      a.ldi = (t == Dl) ? ldx : q;
+      a.xh = xh[t].p;
+      a.ldh = q;
+      a.q = q;
+      launch_upward(a, st);
+    }
+    // couplings  y^_s += sum_{b in F_s} B_{s,b} x^_b
+    for (int t = top; t <= Dl; ++t) {
+      const Level& L = H->L(t);
+      if (T.far[t].nnz() == 0) continue;
+      SpmmArgs s{};
+      s.nclusters = L.nclus;
+      s.max_rows = L.max_k;
+      s.yoff = s.xoff = L.d_roff.p;
+      s.cnt = L.d_k.p;
+      s.ptr = T.d_far[t].ptr;
+      s.idx = T.d_far[t].idx;
+      s.uidx = T.d_far[t].uidx;
+      s.us = T.d_far[t].us;
+      s.blk_off = L.d_B_off.p;
+      s.blk = L.B.p;
+      s.x = xh[t].p;
+      s.ldx = q;
+      s.y = yh[t].p;
+      s.ldy = q;
+      s.q = q;
+      s.alpha = 1.0;
+      launch_spmm(s, st);
+    }
+    // downward pass
+    for (int t = top; t <= Dl; ++t) {
+      const Level& L = H->L(t);
+      DownArgs a{};
+      a.nclusters = L.nclus;
+      a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
+      a.m = L.d_m.p;
+      a.k = L.d_k.p;
+      a.xoff = L.d_xoff.p;
+      a.X = L.X.p;
+      a.roff = L.d_roff.p;
+      a.yh = yh[t].p;
+      a.ldh = q;
+      a.yout = (t == Dl) ? y : yh[t + 1].p;
+      a.ldo = (t == Dl) ? ldy : q;
+      a.q = q;
+      a.alpha = (t == Dl) ? alpha : 1.0;
+      a.accumulate = 1;
+      launch_downward(a, st);
+    }
+    // dense leaves  y += alpha sum_{b in N} D x
+    {
+      SpmmArgs s{};
+      s.nclusters = 1 << Dl;
+      s.max_rows = H->L(Dl).max_m;
+      s.yoff = s.xoff = T.d_leaf_begin;
+      s.cnt = T.d_leaf_size;
+      s.ptr = T.d_near.ptr;
+      s.idx = T.d_near.idx;
+      s.uidx = T.d_near.uidx;
+      s.us = T.d_near.us;
+      s.blk_off = T.d_D_off;
+      s.blk = H->D.p;
+      s.x = x;
+      s.ldx = ldx;
+      s.y = y;
+      s.ldy = ldy;
+      s.q = q;
+      s.alpha = alpha;
+      launch_spmm(s, st);
+    }
+    // workspaces are released stream-ordered (cudaFreeAsync on st) when they go out of scope
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, int64_t row_end, const double* omega,
+                          int64_t ld_omega, int32_t ncols, double* y, int64_t ld_y, void* stream) {
+  try {
+    H2_REQUIRE(T && omega && y, "h2_dense_sketch: NULL argument");
+    H2_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= T->n, "h2_dense_sketch: bad row range");
+    H2_REQUIRE(ncols >= 0 && ld_omega >= ncols && ld_y >= ncols, "h2_dense_sketch: bad ncols / leading dims");
+    H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ) && kern.param > 0, "h2_dense_sketch: bad kernel");
+    ensure_uploaded(T);
+    launch_dense_sketch(make_kernel(kern), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
+                        ld_y, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_omega(uint64_t seed, uint32_t stream_id, int64_t row0, int64_t nrows, int32_t col0, int32_t ncols,
+                   double* out, int64_t ld, void* stream) {
+  try {
+    H2_REQUIRE(out && row0 >= 0 && nrows >= 0 && col0 >= 0 && ncols >= 0 && ld >= ncols, "h2_omega: bad argument");
+    launch_omega(seed, stream_id, row0, nrows, col0, ncols, out, ld, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_t* count) {
+  if (!H || !count) return (g_err = "h2_export_size: NULL argument", H2_ERR_INVALID_ARG);
+  if (what == H2_X_D) {
+    *count = H->D.n;
+    return H2_OK;
+  }
+  if (depth < H->top || depth > H->Dl) return (g_err = "h2_export_size: depth outside [top, leaf]", H2_ERR_INVALID_ARG);
+  const Level& L = H->L(depth);
+  switch (what) {
+    case H2_X_RANK: *count = L.nclus; break;
+    case H2_X_SKEL: *count = L.rtot; break;
+    case H2_X_BASIS: *count = L.xtot; break;
+    case H2_X_B: *count = L.B_off.empty() ? 0 : L.B_off.back(); break;
+    case H2_X_CERT: *count = 2 * (int64_t)L.nclus; break;
+    default: return (g_err = "h2_export_size: bad `what`", H2_ERR_INVALID_ARG);
+  }
+  return H2_OK;
+}
+
+h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst) {
+  int64_t cnt = 0;
+  h2_status s = h2_export_size(H, what, depth, &cnt);
+  if (s != H2_OK) return s;
+  if (!dst) return (g_err = "h2_export: NULL dst", H2_ERR_INVALID_ARG);
+  if (cnt == 0) return H2_OK;
+  const void* src = nullptr;
+  size_t el = 8;
+  if (what == H2_X_D) src = H->D.p;
+  else {
+    const Level& L = H->L(depth);
+    switch (what) {
+      case H2_X_RANK: src = L.d_k.p; el = 4; break;
+      case H2_X_SKEL: src = L.d_skel.p; el = 4; break;
+      case H2_X_BASIS: src = L.X.p; break;
+      case H2_X_B: src = L.B.p; break;
+      case H2_X_CERT: src = L.cert.p; break;
+    }
+  }
+  cudaError_t e = cudaMemcpy(dst, src, el * cnt, cudaMemcpyDefault);
+  if (e != cudaSuccess) return (g_err = std::string("h2_export: ") + cudaGetErrorString(e), H2_ERR_CUDA);
+  return H2_OK;
+}
+
+h2_status h2_matrix_get_stats(const h2_matrix* H, h2_build_stats* stats) {
+  if (!H || !stats) return (g_err = "h2_matrix_get_stats: NULL argument", H2_ERR_INVALID_ARG);
+  *stats = H->stats;
+  return H2_OK;
+}
+
+int64_t h2_matrix_device_bytes(const h2_matrix* H) {
+  if (!H) return 0;
+  int64_t b = H->D.bytes();
+  for (auto& L : H->lv)
+    b += L.X.bytes() + L.B.bytes() + L.d_skel.bytes() + L.d_perm.bytes() + L.Yl.bytes() + L.Ol.bytes();
+  return b;
+}
+
+void h2_free(h2_matrix* H) { delete H; }
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Internal helpers of libh2 (CUDA path only; never shared with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/h2.h"
+
+namespace h2 {
+
+// ---------------------------------------------------------------------------------------
+// error plumbing: internal code throws h2::Error, the C ABI converts it to a status code
+// ---------------------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  h2_status status;
+  Error(h2_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define H2_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::h2::Error(e_ == cudaErrorMemoryAllocation ? H2_ERR_OOM : H2_ERR_CUDA,         \
+                        std::string(#call) + ": " + cudaGetErrorString(e_) + " @" __FILE__ \
+                        ":" + std::to_string(__LINE__));                                   \
+  } while (0)
+
+void count_launch();  // api.cpp: per-thread kernel launch counter (h2_build_stats.launches)
+#define H2_CHECK_LAUNCH()     \
+  do {                        \
+    ::h2::count_launch();     \
+    H2_CUDA(cudaGetLastError()); \
+  } while (0)
+
+#define H2_REQUIRE(cond, msg) \
+  do {                        \
+    if (!(cond)) throw ::h2::Error(H2_ERR_INVALID_ARG, msg); \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// built-in kernels (§V-A): K(x,y) as a function of r^2 = |x-y|^2
+// ---------------------------------------------------------------------------------------
+struct KernelParams {
+  int kind;
+  double param;   // l (exp) or k (helmholtz)
+  double inv;     // 1/l for exp
+};
+
+inline KernelParams make_kernel(const h2_kernel& k) {
+  KernelParams p;
+  p.kind = k.kind;
+  p.param = k.param;
+  p.inv = 1.0 / k.param;
+  return p;
+}
+
+// exp(x) for x <= 0 in ~10 FP64 pipe operations (libdevice exp costs ~2.5x more, measured):
+// x = (n/64) ln2 + g with n = rint(64 x / ln2) (shifter trick), Cody-Waite 2-term reduction
+// (fdlibm ln2 split; |n| < 2^17 keeps kf*hi exact), |g| <= ln2/128, e^g by the degree-5 Taylor
+// polynomial (truncation 3.5e-17 relative), 2^(j/64) from a 64-entry table `tab`, 2^(n>>6) by
+// exponent arithmetic.  Max error ~1.5 ulp.  x < -700 -> 0 (true value < 1e-304).
+__device__ __forceinline__ double exp_neg(double x, const double* __restrict__ tab) {
+  const double SH = 6755399441055744.0;                 // 1.5 * 2^52
+  double t = fma(x, 92.332482616893656, SH);            // 64/ln2
+  double kf = t - SH;
+  int n = __double2loint(t);
+  double g = fma(kf, -0.01083042469326756, x);          // ln2_hi/64 (fdlibm 0x3fe62e42fee00000)
+  g = fma(kf, -2.9815858269852933e-12, g);              // ln2_lo/64 (fdlibm 0x3dea39ef35793c76)
+  double p = fma(g, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, g, 1.0 / 6.0);
+  p = fma(p, g, 0.5);
+  p = fma(p, g, 1.0);
+  p = fma(p, g, 1.0);
+  double r = tab[n & 63] * p;
+  r = __hiloint2double(__double2hiint(r) + ((n >> 6) << 20), __double2loint(r));
+  return x < -700.0 ? 0.0 : r;
+}
+
+// 2^(j/64), j < 64, filled once per CTA (libdevice exp2, < 1 ulp)
+__device__ __forceinline__ void fill_exp_table(double* tab) {
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = exp2((double)j * (1.0 / 64.0));
+}
+
+template <int KIND>
+__device__ __forceinline__ double kernel_of_r2(double r2, double param, double inv, const double* tab) {
+  if (KIND == H2_K_EXP) {
+    // exp(-|x-y|/l)  (PAPER.md Eq. cov)
+    return exp_neg(-sqrt(r2) * inv, tab);
+  } else {
+    double r = sqrt(r2);
+    return r2 > 0.0 ? cos(param * r) / r : 0.0;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ double kernel_of_r2(double r2, double param, double inv) {
+  if (KIND == H2_K_EXP) {
+    // exp(-|x-y|/l)  (PAPER.md Eq. cov)
+    return exp(-sqrt(r2) * inv);
+  } else {
+    // cos(k|x-y|)/|x-y|, 0 at x = y  (PAPER.md Eq. ie; R20)
+    double r = sqrt(r2);
+    return r2 > 0.0 ? cos(param * r) / r : 0.0;
+  }
+}
+
+__device__ __forceinline__ double dist2(double xi, double yi, double zi, double xj, double yj, double zj) {
+  double dx = xi - xj, dy = yi - yj, dz = zi - zj;
+  return fma(dz, dz, fma(dy, dy, dx * dx));
+}
+
+// ---------------------------------------------------------------------------------------
+// FP64 tensor-core MMA (DMMA.8x8x4 on sm_100a; no tcgen05 .kind::f64 exists)
+// A: 8x4 row, one element per lane: A[lane>>2][lane&3]
+// B: 4x8 col, one element per lane: B[lane&3][lane>>2]
+// C: 8x8, two elements per lane: C[lane>>2][2*(lane&3) + {0,1}]
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace h2

@@ -1,0 +1,264 @@
+// batchedID: column-pivoted QR of every panel A_c = (Y^loc_c)^T,
+// which is also the convergence test of §III-B (L361, "QR decomposition ... smallest absolute
+// value of the diagonal"; reading R12), the ID epilogue (T = R11^{-1} R12, Eq.(3)) and the
+// shrink / Omega upsweep (batchedShrink L222/L251, batchedGemm L223/L252).
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace h2 {
+
+// (best value, index, second-best value) reduction: ties -> lowest index (R14)
+struct Top2 {
+  double v;
+  int i;
+  double s;
+};
+
+__device__ __forceinline__ Top2 top2_merge(Top2 a, Top2 b) {
+  Top2 r;
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) {
+    r.v = b.v;
+    r.i = b.i;
+    r.s = fmax(b.s, a.v);
+  } else {
+    r.v = a.v;
+    r.i = a.i;
+    r.s = fmax(a.s, b.v);
+  }
+  return r;
+}
+
+__device__ __forceinline__ Top2 warp_top2(Top2 t) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Top2 u;
+    u.v = __shfl_xor_sync(0xffffffffu, t.v, o);
+    u.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+    u.s = __shfl_xor_sync(0xffffffffu, t.s, o);
+    t = top2_merge(t, u);
+  }
+  return t;
+}
+
+constexpr int CQ_THREADS = 256;
+constexpr int CQ_WARPS = CQ_THREADS / 32;
+
+// One CTA per cluster.  The panel lives in W (global, L1/L2 resident), row j = column j of A
+// (a point's d samples, contiguous).  Residual column norms are RECOMPUTED from the updated
+// trailing rows every step (R14); the norm for step i+1 is fused into the reflector update of
+// step i (one pass over the trailing panel per step).
+__global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
+  extern __shared__ double smem[];
+  const int c = blockIdx.x;
+  const int m = a.m[c];
+  const int d = a.d;
+  double* v = smem;                       // d
+  double* nrm = v + d;                    // m
+  int* perm = (int*)(nrm + a.max_m);      // m
+  __shared__ Top2 red[CQ_WARPS];
+  __shared__ double redd[CQ_WARPS];
+  __shared__ double s_tau, s_beta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t off = a.poff[c];
+  double* A = a.W + off * d;
+  // copy panel rows (Y^loc rows) into the work panel
+  for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
+    int64_t j = e / d;
+    A[e] = a.Y[(off + j) * a.ldy + (e - j * d)];
+  }
+  __syncthreads();
+  for (int j = warp; j < m; j += CQ_WARPS) {
+    double s = 0.0;
+    for (int r = lane; r < d; r += 32) s = fma(A[(int64_t)j * d + r], A[(int64_t)j * d + r], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      nrm[j] = sqrt(s);
+      perm[j] = j;
+    }
+  }
+  __syncthreads();
+  const int kfull = min(d, m);
+  const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
+  double min_gap = INFINITY, margin = INFINITY;
+  int k = 0;
+  for (int i = 0;; ++i) {
+    // ---- pivot: largest recomputed residual norm among columns i..m-1
+    Top2 t{-1.0, 0x7fffffff, -1.0};
+    for (int j = i + threadIdx.x; j < m; j += CQ_THREADS) t = top2_merge(t, Top2{nrm[j], j, -1.0});
+    t = warp_top2(t);
+    if (lane == 0) red[warp] = t;
+    __syncthreads();
+    if (warp == 0) {
+      Top2 u = lane < CQ_WARPS ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
+      u = warp_top2(u);
+      if (lane == 0) red[0] = u;
+    }
+    __syncthreads();
+    t = red[0];
+    if (i >= m) break;
+    // truncation margin of every decision taken (R13); no decision exists at i = min(d, m)
+    if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    if (i == kcap || !(t.v > a.eps)) {
+      k = i;
+      break;
+    }
+    if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    const int p = t.i;
+    __syncthreads();
+    // ---- swap rows i and p of the panel (columns of A)
+    if (p != i) {
+      for (int r = threadIdx.x; r < d; r += CQ_THREADS) {
+        double x = A[(int64_t)i * d + r];
+        A[(int64_t)i * d + r] = A[(int64_t)p * d + r];
+        A[(int64_t)p * d + r] = x;
+      }
+      if (threadIdx.x == 0) {
+        int q = perm[i];
+        perm[i] = perm[p];
+        perm[p] = q;
+        double x = nrm[i];
+        nrm[i] = nrm[p];
+        nrm[p] = x;
+      }
+    }
+    __syncthreads();
+    // ---- Householder reflector of A(i:d, i), LAPACK dlarfg convention
+    double* Ai = A + (int64_t)i * d;
+    double s = 0.0;
+    for (int r = i + 1 + threadIdx.x; r < d; r += CQ_THREADS) s = fma(Ai[r], Ai[r], s);
+    s = warp_sum(s);
+    if (lane == 0) redd[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x2 = 0.0;
+      for (int w = 0; w < CQ_WARPS; ++w) x2 += redd[w];
+      double alpha = Ai[i];
+      double xnorm = sqrt(x2);
+      double tau, beta;
+      if (xnorm == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+      } else {
+        double h = hypot(alpha, xnorm);
+        beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
+        tau = (beta - alpha) / beta;
+      }
+      s_tau = tau;
+      s_beta = beta;
+      v[i] = alpha - beta;   // scale denominator, replaced by 1 below
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    {
+      const double den = v[i];
+      for (int r = i + 1 + threadIdx.x; r < d; r += CQ_THREADS) {
+        v[r] = tau != 0.0 ? Ai[r] / den : 0.0;
+        Ai[r] = 0.0;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      v[i] = 1.0;
+      Ai[i] = s_beta;
+    }
+    __syncthreads();
+    // ---- trailing update of rows j > i (columns of A) + next residual norms
+    for (int j = i + 1 + warp; j < m; j += CQ_WARPS) {
+      double* Aj = A + (int64_t)j * d;
+      double w = 0.0;
+      for (int r = i + lane; r < d; r += 32) w = fma(v[r], Aj[r], w);
+      w = warp_sum(w) * tau;
+      double q = 0.0;
+      for (int r = i + lane; r < d; r += 32) {
+        double x = fma(-w, v[r], Aj[r]);
+        Aj[r] = x;
+        if (r > i) q = fma(x, x, q);
+      }
+      q = warp_sum(q);
+      if (lane == 0) nrm[j] = sqrt(q);
+    }
+    __syncthreads();
+    k = i + 1;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += CQ_THREADS) a.perm[off + j] = perm[j];
+  if (threadIdx.x == 0) {
+    a.k[c] = k;
+    a.cert[2 * c] = min_gap;
+    a.cert[2 * c + 1] = margin;
+  }
+}
+
+void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
+  if (a.nclusters <= 0) return;
+  size_t sm = sizeof(double) * (a.d + a.max_m) + sizeof(int) * a.max_m;
+  if (sm > 48 * 1024) H2_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr_kernel<<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+  H2_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------------------------------
+// ID epilogue.  W row j holds column j of the factored A: R(0:k, j) in its first k entries.
+// X (m x k row-major): X(J[i], :) = e_i, X(Rhat[c], :) = T(:, c)^T, T = R11^{-1} R12 by back
+// substitution (rows k-1 -> 0, ascending inner sums, R15).  One thread per redundant column.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) id_kernel(IdArgs a) {
+  const int c = blockIdx.x;
+  const int m = a.m[c], k = a.k[c], d = a.d;
+  const int64_t off = a.poff[c];
+  const double* A = a.W + off * d;
+  const int* perm = a.perm + off;
+  double* X = a.X + a.xoff[c];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    double* row = X + (int64_t)perm[i] * k;
+    for (int q = 0; q < k; ++q) row[q] = (q == i) ? 1.0 : 0.0;
+    a.skel[a.roff[c] + i] = a.ibar[off + perm[i]];
+  }
+  for (int cc = threadIdx.x; cc < m - k; cc += blockDim.x) {
+    const double* r12 = A + (int64_t)(k + cc) * d;     // column k+cc of R
+    double* t = X + (int64_t)perm[k + cc] * k;          // T(:, cc) stored as a row of X
+    for (int i = k - 1; i >= 0; --i) {
+      double s = r12[i];
+      for (int j = i + 1; j < k; ++j) s -= A[(int64_t)j * d + i] * t[j];
+      t[i] = s / A[(int64_t)i * d + i];
+    }
+  }
+}
+
+void launch_id(const IdArgs& a, cudaStream_t st) {
+  if (a.nclusters <= 0) return;
+  id_kernel<<<a.nclusters, 128, 0, st>>>(a);
+  H2_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------------------------------
+// shrink + project for columns [c0, c1):  Yp(roff+i) = Yl(poff+J[i]),
+// Op(roff+i) = Ol(poff+J[i]) + sum_cc T(i,cc) Ol(poff+Rhat[cc])   (= X^T Ol, identity rows exact)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) shrink_project_kernel(ShrinkArgs a) {
+  const int c = blockIdx.x;
+  const int m = a.m[c], k = a.k[c];
+  const int64_t off = a.poff[c];
+  const int* perm = a.perm + off;
+  const double* X = a.X + a.xoff[c];
+  const int nc = a.c1 - a.c0;
+  for (int e = threadIdx.x; e < k * nc; e += blockDim.x) {
+    const int i = e / nc, col = a.c0 + e % nc;
+    const int64_t src = off + perm[i];
+    a.Yp[(a.roff[c] + i) * a.ldp + col] = a.Yl[src * a.ld + col];
+    double s = a.Ol[src * a.ld + col];
+    for (int cc = 0; cc < m - k; ++cc) {
+      const int rr = perm[k + cc];
+      s = fma(X[(int64_t)rr * k + i], a.Ol[(off + rr) * a.ld + col], s);
+    }
+    a.Op[(a.roff[c] + i) * a.ldp + col] = s;
+  }
+}
+
+void launch_shrink_project(const ShrinkArgs& a, cudaStream_t st) {
+  if (a.nclusters <= 0 || a.c1 <= a.c0) return;
+  shrink_project_kernel<<<a.nclusters, 256, 0, st>>>(a);
+  H2_CHECK_LAUNCH();
+}
+
+}  // namespace h2

@@ -1,0 +1,176 @@
+// Launch wrappers of the sm_100a kernels of libh2 (one line each says which Algorithm-1 step).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace h2 {
+
+// batchedRand: Omega rows [row0,row0+nrows) x cols [col0,col0+ncols)          (L203, L384)
+void launch_omega(uint64_t seed, uint32_t sid, int64_t row0, int64_t nrows, int col0, int ncols, double* out,
+                  int64_t ld, cudaStream_t st);
+// built-in dense sketch Y(rows,:) = K(rows,:) Omega                              (L203 with K_blk = K)
+void launch_dense_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                         int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
+                         int64_t ldy, cudaStream_t st);
+// accum += ||Y(:, c0:c1)||_F^2 (deterministic)                                   (R10 tolerance scale)
+void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum,
+                  int* nonfinite, cudaStream_t st);
+
+// batchedGen over unique pairs u: out[out_off[u] + i*nc + j] = K(idx[off[us]+i], idx[off[ub]+j])
+// (L212 for D with idx = iota, off = cluster begin; L258 for B with idx = skeletons)
+struct GenArgs {
+  int64_t nblocks;
+  const int32_t* us;
+  const int32_t* ub;
+  const int32_t* cnt;     // per cluster rows
+  const int64_t* off;     // per cluster offset into idx
+  const int32_t* idx;     // tree-order point indices
+  const int64_t* out_off; // per unique pair
+  double* out;
+};
+void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, const GenArgs& a,
+                cudaStream_t st);
+// fill the pointer / size arrays of an h2_block_batch for a user entry callback
+void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* roff, int64_t* coff, double** outp,
+                           int32_t* ld, cudaStream_t st);
+
+// batchedBSRGemm: Y(rows of s, c0:c0+nc) -= sum_{b in CSR row s} Blk(s,b) Om(rows of b, c0:c0+nc)
+// (L213 leaf with D, L240-243 inner with B); partners ascending, no atomics (L385)
+struct BsrArgs {
+  int32_t nclusters;
+  int32_t max_rows;
+  const int64_t* yoff;    // per cluster: first row in Y
+  const int64_t* ooff;    // per cluster: first row in Om
+  const int32_t* cnt;     // per cluster: rows
+  const int32_t* ptr;
+  const int32_t* idx;
+  const int32_t* uidx;
+  const int32_t* us;      // stored orientation of unique pair u: rows = cluster us[u]
+  const int64_t* blk_off;
+  const double* blk;
+  double* Y;
+  int64_t ldy;
+  const double* Om;
+  int64_t ldo;
+  int c0, ncols;
+};
+void launch_bsr(const BsrArgs& a, cudaStream_t st);
+
+// CPQR of every panel A_c = Y(poff[c] : poff[c]+m[c], 0:d)^T (row ID via column ID, L173, L387)
+// with threshold eps (R13/R14); W receives the factored panels (packed, ld = d).
+struct CpqrArgs {
+  int32_t nclusters;
+  int32_t max_m;
+  const double* Y;
+  int64_t ldy;
+  const int64_t* poff;
+  const int32_t* m;
+  int d;
+  double eps;
+  int kmax;
+  double* W;
+  int32_t* k;
+  int32_t* perm;          // at poff[c]
+  double* cert;           // 2 per cluster (min gap, stop margin)
+};
+void launch_cpqr(const CpqrArgs& a, cudaStream_t st);
+
+// ID epilogue: X_c (m x k, U or [E1;E2]) from T = R11^{-1} R12 (R15); skeletons I~ (L224, L253)
+struct IdArgs {
+  int32_t nclusters;
+  const double* W;
+  int d;
+  const int64_t* poff;
+  const int32_t* m;
+  const int32_t* k;
+  const int32_t* perm;
+  const int64_t* xoff;
+  double* X;
+  const int32_t* ibar;    // Ibar_c = ibar + poff[c]
+  const int64_t* roff;    // rank prefix sum of this depth
+  int32_t* skel;
+};
+void launch_id(const IdArgs& a, cudaStream_t st);
+
+// batchedShrink + batchedGemm upsweep for columns [c0,c1) (L222-223, L251-252):
+// Yp(roff[c]+i) = Yl(poff[c] + J[i]);  Op(roff[c]+i) = sum_j X(j,i) Ol(poff[c]+j)
+struct ShrinkArgs {
+  int32_t nclusters;
+  const int64_t* poff;
+  const int32_t* m;
+  const int32_t* k;
+  const int32_t* perm;
+  const int64_t* xoff;
+  const double* X;
+  const int64_t* roff;
+  const double* Yl;
+  const double* Ol;
+  int64_t ld;
+  double* Yp;
+  double* Op;
+  int64_t ldp;
+  int c0, c1;
+};
+void launch_shrink_project(const ShrinkArgs& a, cudaStream_t st);
+
+// ---- H^2 matvec pieces (CS4)
+// xh(roff[c]+i, :) = sum_j X_c(j,i) xin(ioff[c]+j, :)       (upward; leaf: xin = x, ioff = begin)
+struct UpArgs {
+  int32_t nclusters;
+  const int64_t* ioff;
+  const int32_t* m;
+  const int32_t* k;
+  const int64_t* xoff;
+  const double* X;
+  const int64_t* roff;
+  const double* xin;
+  int64_t ldi;
+  double* xh;
+  int64_t ldh;
+  int q;
+};
+void launch_upward(const UpArgs& a, cudaStream_t st);
+// yout(ioff[c]+j, :) = beta_in*yout + alpha * sum_i X_c(j,i) yh(roff[c]+i, :)     (downward / leaf out)
+struct DownArgs {
+  int32_t nclusters;
+  const int64_t* ioff;
+  const int32_t* m;
+  const int32_t* k;
+  const int64_t* xoff;
+  const double* X;
+  const int64_t* roff;
+  const double* yh;
+  int64_t ldh;
+  double* yout;
+  int64_t ldo;
+  int q;
+  double alpha;
+  int accumulate;          // 1: yout += ..., 0: yout = ...
+};
+void launch_downward(const DownArgs& a, cudaStream_t st);
+// y(rows of s) += alpha * sum_b Blk(s,b) x(rows of b)   (coupling B / dense D products)
+struct SpmmArgs {
+  int32_t nclusters;
+  int32_t max_rows;
+  const int64_t* yoff;
+  const int64_t* xoff;
+  const int32_t* cnt;
+  const int32_t* ptr;
+  const int32_t* idx;
+  const int32_t* uidx;
+  const int32_t* us;
+  const int64_t* blk_off;
+  const double* blk;
+  const double* x;
+  int64_t ldx;
+  double* y;
+  int64_t ldy;
+  int q;
+  double alpha;
+};
+void launch_spmm(const SpmmArgs& a, cudaStream_t st);
+void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStream_t st);
+
+}  // namespace h2

@@ -1,0 +1,329 @@
+// batchedRand (PAPER.md L203/L216/L246, L384 "generated in a single kernel") and the built-in
+// dense-kernel sketch Y = K Omega (Algorithm 1 line 1 with K_blk = the dense kernel matrix,
+// BASELINE configs[1]); plus the sketch-norm reduction used by the tolerance rule (R10).
+#include "common.cuh"
+#include "kernels.hpp"
+
+#include <cstdlib>
+
+namespace h2 {
+
+// ------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11) -> two 53-bit uniforms -> Box-Muller pair (R8)
+// counter = (row, column pair q, stream id, 0), key = (seed lo, seed hi)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+__device__ __forceinline__ double u53(uint32_t lo, uint32_t hi) {
+  uint64_t v = ((uint64_t)hi << 32) | lo;
+  return ((double)(v >> 11) + 0.5) * 0x1.0p-53;
+}
+
+__global__ void omega_kernel(uint2 key, uint32_t sid, int64_t row0, int64_t nrows, int col0, int ncols,
+                             double* __restrict__ out, int64_t ld) {
+  const int q0 = col0 >> 1;
+  const int nq = ((col0 + ncols + 1) >> 1) - q0;
+  const int64_t total = nrows * nq;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / nq;
+    int q = q0 + (int)(t - r * nq);
+    uint4 w = philox4x32_10(make_uint4((uint32_t)(row0 + r), (uint32_t)q, sid, 0u), key);
+    double u1 = u53(w.x, w.y), u2 = u53(w.z, w.w);
+    double rad = sqrt(-2.0 * log(u1));
+    double s, c;
+    sincospi(2.0 * u2, &s, &c);
+    int j0 = 2 * q - col0;  // column within the output block
+    double* o = out + r * ld;
+    if (j0 >= 0 && j0 < ncols) o[j0] = rad * c;
+    if (j0 + 1 >= 0 && j0 + 1 < ncols) o[j0 + 1] = rad * s;
+  }
+}
+
+void launch_omega(uint64_t seed, uint32_t sid, int64_t row0, int64_t nrows, int col0, int ncols, double* out,
+                  int64_t ld, cudaStream_t st) {
+  if (nrows <= 0 || ncols <= 0) return;
+  uint2 key = make_uint2((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  int64_t work = nrows * ((ncols + 2) / 2);
+  int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
+  omega_kernel<<<grid, 256, 0, st>>>(key, sid, row0, nrows, col0, ncols, out, ld);
+  H2_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------------------------------
+// Dense sketch: Y(i, c0:c0+32) = sum_{j in [jb,je)} K(x_i, x_j) Omega(j, c0:c0+32)
+// CTA = 4 warps x (8 MB) rows; columns in one 32-wide chunk (4 DMMA n-blocks).  K entries are
+// generated in registers directly in the DMMA A-fragment layout (each lane evaluates exactly
+// the entries it contributes: no K tile ever touches shared memory or HBM); Omega rows and
+// the x_j coordinates are staged in shared memory per 32-row j-chunk (cp.async double buffer).
+// The j range may be split over gridDim.y slices (partial sums combined in a fixed order by
+// sketch_combine_kernel) to fill the last wave; accumulation order is fixed -> deterministic.
+// ------------------------------------------------------------------------------------------
+constexpr int SK_JT = 32;       // j rows per smem stage
+constexpr int SK_LD = 36;       // padded Omega row stride (doubles), conflict-free B fragments
+
+template <int KIND, int MB, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    dense_sketch_kernel(const double* __restrict__ X, const double* __restrict__ Yc, const double* __restrict__ Zc,
+                        int64_t n, int64_t row0, int64_t row1, const double* __restrict__ Om, int64_t ldo, int ncols,
+                        double* __restrict__ Yout, int64_t ldy, int64_t split_stride, double param, double inv,
+                        bool aligned) {
+  constexpr int WR = 8 * MB;                       // rows per warp
+  __shared__ __align__(16) double sOm[2][SK_JT * SK_LD];
+  __shared__ double sx[2][SK_JT], sy[2][SK_JT], sz[2][SK_JT];
+  __shared__ double tab[64];
+  fill_exp_table(tab);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rbase = row0 + (int64_t)blockIdx.x * (4 * WR) + warp * WR;
+  // j slice of this CTA
+  const int64_t nch_all = (n + SK_JT - 1) / SK_JT;
+  const int64_t ch_b = nch_all * blockIdx.y / gridDim.y, ch_e = nch_all * (blockIdx.y + 1) / gridDim.y;
+  double xi[MB], yi[MB], zi[MB];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    int64_t i = rbase + mb * 8 + (lane >> 2);
+    if (i < row1) {
+      xi[mb] = X[i];
+      yi[mb] = Yc[i];
+      zi[mb] = Zc[i];
+    } else {
+      xi[mb] = yi[mb] = zi[mb] = 0.0;
+    }
+  }
+  double acc[MB][4][2];
+#pragma unroll
+  for (int a = 0; a < MB; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto stage = [&](int64_t ch, int buf) {
+    int64_t j0 = ch * SK_JT;
+    for (int e = threadIdx.x; e < SK_JT * 16; e += 128) {
+      int r = e >> 4, c2 = (e & 15) * 2;
+      double* dst = &sOm[buf][r * SK_LD + c2];
+      int64_t j = j0 + r;
+      if (aligned && j < n && c2 + 1 < ncols) {
+        const double* src = Om + j * ldo + c2;
+        unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(src));
+      } else {
+        dst[0] = (j < n && c2 < ncols) ? Om[j * ldo + c2] : 0.0;
+        dst[1] = (j < n && c2 + 1 < ncols) ? Om[j * ldo + c2 + 1] : 0.0;
+      }
+    }
+    if (threadIdx.x < SK_JT) {
+      int64_t j = j0 + threadIdx.x;
+      sx[buf][threadIdx.x] = j < n ? X[j] : 0.0;
+      sy[buf][threadIdx.x] = j < n ? Yc[j] : 0.0;
+      sz[buf][threadIdx.x] = j < n ? Zc[j] : 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  if (ch_b < ch_e) stage(ch_b, 0);
+  for (int64_t ch = ch_b; ch < ch_e; ++ch) {
+    const int buf = (int)((ch - ch_b) & 1);
+    if (ch + 1 < ch_e) {
+      stage(ch + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const int64_t j0 = ch * SK_JT;
+    const bool full = j0 + SK_JT <= n;
+#pragma unroll 2
+    for (int ks = 0; ks < SK_JT / 4; ++ks) {
+      const int jl = ks * 4 + (lane & 3);
+      const double xj = sx[buf][jl], yj = sy[buf][jl], zj = sz[buf][jl];
+      const bool jvalid = full || (j0 + jl) < n;
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        double r2 = dist2(xi[mb], yi[mb], zi[mb], xj, yj, zj);
+        double v = kernel_of_r2<KIND>(r2, param, inv, tab);
+        a[mb] = jvalid ? v : 0.0;
+      }
+      double b[4];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) b[nb] = sOm[buf][(ks * 4 + (lane & 3)) * SK_LD + nb * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], b[nb]);
+    }
+    __syncthreads();
+  }
+  double* Yo = Yout + blockIdx.y * split_stride;
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    int64_t i = rbase + mb * 8 + (lane >> 2);
+    if (i >= row1) continue;
+    double* y = Yo + (i - row0) * ldy;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      int c = nb * 8 + 2 * (lane & 3);
+      if (c < ncols) y[c] = acc[mb][nb][0];
+      if (c + 1 < ncols) y[c + 1] = acc[mb][nb][1];
+    }
+  }
+}
+
+// Y(i, c) = sum_{s < S} P_s(i, c), s ascending (fixed order)
+__global__ void sketch_combine_kernel(const double* __restrict__ P, int S, int64_t rows, int ncols,
+                                      double* __restrict__ Y, int64_t ldy) {
+  const int64_t total = rows * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / ncols;
+    int c = (int)(e - r * ncols);
+    double s = P[e];
+    for (int q = 1; q < S; ++q) s += P[q * total + e];
+    Y[r * ldy + c] = s;
+  }
+}
+
+namespace {
+int env_int(const char* name, int def) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : def;
+}
+
+template <int KIND, int MB, int MINB>
+void sketch_variant(dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc, int64_t n,
+                    int64_t row0, int64_t row1, const double* Om, int64_t ldo, int nc, double* Yo, int64_t ldy,
+                    int64_t sstride, const KernelParams& kp, bool aligned) {
+  dense_sketch_kernel<KIND, MB, MINB><<<grid, 128, 0, st>>>(X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride,
+                                                            kp.param, kp.inv, aligned);
+}
+
+template <int KIND>
+void sketch_dispatch(int mb, dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc,
+                     int64_t n, int64_t row0, int64_t row1, const double* Om, int64_t ldo, int nc, double* Yo,
+                     int64_t ldy, int64_t sstride, const KernelParams& kp, bool aligned) {
+  if (mb == 2)
+    sketch_variant<KIND, 2, 4>(grid, st, X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride, kp, aligned);
+  else
+    sketch_variant<KIND, 4, 3>(grid, st, X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride, kp, aligned);
+}
+}  // namespace
+
+void launch_dense_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                         int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
+                         int64_t ldy, cudaStream_t st) {
+  if (row1 <= row0 || ncols <= 0) return;
+  const int mb = env_int("H2_SK_MB", 4) == 2 ? 2 : 4;
+  const int occ = mb == 2 ? 4 : 3;                 // resident CTAs / SM (registers)
+  const int64_t rows = row1 - row0;
+  const int tiles = div_up(rows, 4 * 8 * mb);
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // j-split S: fill the last wave (efficiency = units / (slots * ceil(units / slots)))
+  int S = env_int("H2_SK_SPLIT", 0);
+  if (S <= 0) {
+    const int slots = sms * occ;
+    double best = 0;
+    S = 1;
+    for (int s = 1; s <= 4; ++s) {
+      int64_t units = (int64_t)tiles * s;
+      if (n / s < 4096 && s > 1) break;
+      double eff = (double)units / ((double)slots * ((units + slots - 1) / slots)) - 0.01 * (s - 1);
+      if (eff > best + 1e-9) {
+        best = eff;
+        S = s;
+      }
+    }
+  }
+  double* part = nullptr;
+  if (S > 1) H2_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * rows * 32 * S, st));
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    int nc = std::min(32, ncols - c0);
+    // 16-byte cp.async staging needs 16-byte aligned Omega rows
+    const bool aligned = ((uintptr_t)(Om + c0) % 16 == 0) && (ldo % 2 == 0);
+    dim3 grid(tiles, S);
+    double* yo = S > 1 ? part : Yout + c0;
+    const int64_t ld = S > 1 ? nc : ldy;
+    const int64_t sstride = S > 1 ? rows * nc : 0;
+    if (kp.kind == H2_K_EXP)
+      sketch_dispatch<H2_K_EXP>(mb, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp, aligned);
+    else
+      sketch_dispatch<H2_K_HELMHOLTZ>(mb, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp,
+                                      aligned);
+    H2_CHECK_LAUNCH();
+    if (S > 1) {
+      int g = (int)std::min<int64_t>((rows * nc + 255) / 256, (int64_t)sms * 16);
+      sketch_combine_kernel<<<g, 256, 0, st>>>(part, S, rows, nc, Yout + c0, ldy);
+      H2_CHECK_LAUNCH();
+    }
+  }
+  if (part) H2_CUDA(cudaFreeAsync(part, st));
+}
+
+// ------------------------------------------------------------------------------------------
+// sum of squares of Y(:, c0:c1): fixed 1024-row chunks, fixed-order combination -> bitwise
+// reproducible for a given n (R10: rho^2 N = ||Y||_F^2, accumulated over rounds).
+// ------------------------------------------------------------------------------------------
+__global__ void sumsq_partial_kernel(const double* __restrict__ Y, int64_t n, int64_t ld, int c0, int c1,
+                                     double* __restrict__ part) {
+  __shared__ double red[32];
+  int64_t r0 = (int64_t)blockIdx.x * 1024;
+  double s = 0.0;
+  const int w = c1 - c0;
+  for (int e = threadIdx.x; e < 1024 * w; e += blockDim.x) {
+    int64_t r = r0 + e / w;
+    if (r < n) {
+      double v = Y[r * ld + c0 + e % w];
+      s = fma(v, v, s);
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+__global__ void sumsq_final_kernel(const double* __restrict__ part, int np, double* __restrict__ out, int* flag) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      out[0] += v;
+      if (!isfinite(v)) *flag = 1;
+    }
+  }
+}
+
+void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum, int* nonfinite,
+                  cudaStream_t st) {
+  int np = div_up(n, 1024);
+  sumsq_partial_kernel<<<np, 256, 0, st>>>(Y, n, ld, c0, c1, scratch);
+  H2_CHECK_LAUNCH();
+  sumsq_final_kernel<<<1, 1024, 0, st>>>(scratch, np, accum, nonfinite);
+  H2_CHECK_LAUNCH();
+}
+
+}  // namespace h2

@@ -1,0 +1,48 @@
+// Host-side cluster tree + block partition (§II-A) and their flattened
+// per-level CSR batch descriptors (§IV-A "stored contiguously level by level").
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/h2.h"
+
+struct PairCSR {
+  // ordered pairs (row s, col b) of one depth, sorted (s, b); symmetric set
+  std::vector<int32_t> ptr;    // 2^t + 1
+  std::vector<int32_t> idx;    // partner b per ordered pair
+  std::vector<int32_t> uidx;   // index of {min(s,b), max(s,b)} in the unique list
+  std::vector<int32_t> us, ub; // unique pairs (s <= b for near, s < b for far), sorted
+  int64_t nnz() const { return (int64_t)idx.size(); }
+  int64_t nuniq() const { return (int64_t)us.size(); }
+};
+
+struct DeviceCSR {
+  int32_t *ptr = nullptr, *idx = nullptr, *uidx = nullptr, *us = nullptr, *ub = nullptr;
+};
+
+struct h2_tree {
+  int64_t n = 0;
+  int32_t dim = 0, leaf_size = 0, Dl = 0, top = -1, rule = 0, csp = 0;
+  double eta = 0;
+  std::vector<int64_t> perm;                       // tree index -> original index
+  std::vector<std::vector<int64_t>> begin, end;    // per depth
+  std::vector<double> xt, yt, zt;                  // tree-order coordinates (zero padded to 3D)
+  PairCSR near;                                    // leaf depth
+  std::vector<PairCSR> far;                        // per depth
+  std::vector<int64_t> D_off;                      // unique near pair offsets (m_s*m_b prefix)
+
+  // device mirrors (current device at build time)
+  int device = -1;
+  double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr;
+  int32_t* d_iota = nullptr;                       // 0..n-1
+  int64_t* d_leaf_begin = nullptr;                 // 2^Dl + 1 (last = n)
+  int32_t* d_leaf_size = nullptr;
+  int64_t* d_D_off = nullptr;
+  DeviceCSR d_near;
+  std::vector<DeviceCSR> d_far;
+
+  ~h2_tree();
+};
+
+void tree_build_host(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+void tree_upload(h2_tree& T);

@@ -1,0 +1,306 @@
+"""Thin Python binding of libh2 (include/h2.h): argument marshalling only.
+
+PyTorch provides device memory, streams and process groups; every step of Algorithm 1
+ runs in the sm_100a kernels of libh2.so.  Names follow the paper:
+``Tree`` (cluster tree + block partition, §II-A), ``build`` (Algorithm 1, returns an
+``H2Matrix`` holding U, E, B, D and the skeletons I~), ``H2Matrix.matvec``.
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+
+KERNELS = {"exp": L.H2_K_EXP, "helmholtz": L.H2_K_HELMHOLTZ}
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class _CudaView:
+    """__cuda_array_interface__ wrapper so torch can view a libh2-owned / callback buffer."""
+
+    def __init__(self, ptr, shape, strides_elems, typestr="<f8", itemsize=8):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False), "version": 3,
+            "strides": tuple(s * itemsize for s in strides_elems)}
+
+
+def device_view(ptr, shape, strides, dtype=torch.float64):
+    typestr, size = {torch.float64: ("<f8", 8), torch.int32: ("<i4", 4), torch.int64: ("<i8", 8)}[dtype]
+    return torch.as_tensor(_CudaView(ptr, shape, strides, typestr, size), device="cuda")
+
+
+class Tree:
+    """KD-tree cluster tree + dual-traversal partition (§II-A; R1-R6).
+
+    points: n x dim float64 in original order (host).  The tree keeps tree-ordered
+    coordinates on the current CUDA device for the built-in kernels."""
+
+    def __init__(self, points, leaf_size=64, eta=0.7, dist_rule="center"):
+        P = np.ascontiguousarray(points, dtype=np.float64)
+        if P.ndim == 1:
+            P = P[:, None]
+        self.points = P
+        h = C.c_void_p()
+        check(lib.h2_tree_build(P.ctypes.data_as(C.c_void_p), P.shape[0], P.shape[1], leaf_size, float(eta),
+                                L.H2_DIST_CENTER if dist_rule == "center" else L.H2_DIST_BOX, C.byref(h)))
+        self._h = h
+        info = L.h2_tree_info()
+        check(lib.h2_tree_get_info(h, C.byref(info)))
+        self.n, self.dim, self.leaf_size = info.n, info.dim, info.leaf_size
+        self.leaf_depth = info.leaf_depth
+        self.top_depth = info.top_depth
+        self.near_nnz, self.far_nnz_total, self.csp = info.near_nnz, info.far_nnz_total, info.csp
+        nnodes = (1 << (self.leaf_depth + 1)) - 1
+        self.perm = np.empty(self.n, np.int64)
+        b = np.empty(nnodes, np.int64)
+        e = np.empty(nnodes, np.int64)
+        near = np.empty((self.near_nnz, 2), np.int32)
+        check(lib.h2_tree_export(h, self.perm.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                 e.ctypes.data_as(C.c_void_p), near.ctypes.data_as(C.c_void_p)))
+        self.begin = [b[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
+        self.end = [e[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
+        self.near = near.astype(np.int64)
+        self.far = []
+        for t in range(self.leaf_depth + 1):
+            cnt = C.c_int64()
+            check(lib.h2_tree_far_count(h, t, C.byref(cnt)))
+            f = np.empty((cnt.value, 2), np.int32)
+            if cnt.value:
+                check(lib.h2_tree_export_far(h, t, f.ctypes.data_as(C.c_void_p)))
+            self.far.append(f.astype(np.int64))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.h2_tree_free(h)
+            self._h = None
+
+
+def build_opts(**kw):
+    o = L.h2_build_opts()
+    lib.h2_build_opts_default(C.byref(o))
+    names = {"tol_rule": None}
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if k == "tol_rule":
+            v = {"rms": L.H2_TOL_RMS, "literal": L.H2_TOL_LITERAL}[v] if isinstance(v, str) else v
+        if k == "adaptive":
+            v = int(bool(v))
+        if not hasattr(o, k) and k not in names:
+            raise TypeError(f"unknown build option {k}")
+        setattr(o, k, v)
+    return o
+
+
+def _kernel(kind, param):
+    return L.h2_kernel(KERNELS[kind], float(param))
+
+
+class H2Matrix:
+    """Result of Algorithm 1: U (leaves), E (transfer), B (couplings), D (dense), I~ (skeletons)."""
+
+    def __init__(self, handle, tree, stats, keep=()):
+        self._h = handle
+        self.tree = tree          # the matrix references the tree: keep it alive
+        self.stats = stats
+        self._keep = keep
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.h2_free(h)
+            self._h = None
+
+    # ---- inspection (copies to host numpy)
+    def _export(self, what, depth=0, dtype=np.float64):
+        cnt = C.c_int64()
+        check(lib.h2_export_size(self._h, what, depth, C.byref(cnt)))
+        out = np.empty(cnt.value, dtype)
+        if cnt.value:
+            check(lib.h2_export(self._h, what, depth, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    @property
+    def top_depth(self):
+        return self.stats["top_depth"]
+
+    @property
+    def samples(self):
+        return self.stats["samples"]
+
+    def rank(self, t):
+        return self._export(L.H2_X_RANK, t, np.int32).astype(np.int64)
+
+    def skel(self, t):
+        r = self.rank(t)
+        s = self._export(L.H2_X_SKEL, t, np.int32).astype(np.int64)
+        return np.split(s, np.cumsum(r)[:-1])
+
+    def panel_rows(self, t):
+        if t == self.tree.leaf_depth:
+            return (self.tree.end[t] - self.tree.begin[t]).astype(np.int64)
+        rc = self.rank(t + 1)
+        return rc[0::2] + rc[1::2]
+
+    def basis(self, t):
+        """X_tau per cluster of depth t (m x k): U_tau at the leaves, [E_nu1; E_nu2] above."""
+        r = self.rank(t)
+        m = self.panel_rows(t)
+        x = self._export(L.H2_X_BASIS, t)
+        out, o = [], 0
+        for mi, ki in zip(m, r):
+            out.append(x[o:o + mi * ki].reshape(mi, ki))
+            o += mi * ki
+        return out
+
+    def cert(self, t):
+        return self._export(L.H2_X_CERT, t).reshape(-1, 2)
+
+    def D_blocks(self):
+        """dict (s, b) -> m_s x m_b for unique near pairs s <= b."""
+        Dl = self.tree.leaf_depth
+        raw = self._export(L.H2_X_D)
+        sz = self.tree.end[Dl] - self.tree.begin[Dl]
+        out, o = {}, 0
+        for s, b in self.tree.near:
+            if s <= b:
+                n = sz[s] * sz[b]
+                out[(int(s), int(b))] = raw[o:o + n].reshape(sz[s], sz[b])
+                o += n
+        return out
+
+    def B_blocks(self, t):
+        """dict (s, b) -> k_s x k_b for unique far pairs s < b of depth t."""
+        r = self.rank(t)
+        raw = self._export(L.H2_X_B, t)
+        out, o = {}, 0
+        for s, b in self.tree.far[t]:
+            if s < b:
+                n = r[s] * r[b]
+                out[(int(s), int(b))] = raw[o:o + n].reshape(r[s], r[b])
+                o += n
+        return out
+
+    def device_bytes(self):
+        return int(lib.h2_matrix_device_bytes(self._h))
+
+    # ---- H^2 matvec (tree-order rows)
+    def matvec(self, x, alpha=1.0, beta=0.0, y=None, stream=None):
+        """y = alpha K_H x + beta y for x: (n, q) float64 CUDA tensor (q <= 64)."""
+        vec = x.dim() == 1
+        X = x.reshape(x.shape[0], -1).contiguous()
+        assert X.is_cuda and X.dtype == torch.float64 and X.shape[0] == self.tree.n
+        q = X.shape[1]
+        if y is None:
+            y = torch.zeros_like(X)
+            beta = 0.0
+        check(lib.h2_matvec(self._h, _ptr(X), X.stride(0), _ptr(y), y.stride(0), q, float(alpha), float(beta),
+                            _stream(stream)))
+        return y[:, 0] if vec else y
+
+
+def _stats_dict(s):
+    d = {k: getattr(s, k) for k in ("samples", "failed_depth", "top_depth", "leaf_depth", "eps", "entries_D",
+                                    "entries_B", "entries_sketch", "bytes_U", "bytes_E", "bytes_B", "bytes_D",
+                                    "launches", "t_total_ms")}
+    lo, hi = s.top_depth, s.leaf_depth
+    d["rounds"] = {t: s.rounds[t] for t in range(lo, hi + 1)}
+    d["rank_min"] = {t: s.rank_min[t] for t in range(lo, hi + 1)}
+    d["rank_max"] = {t: s.rank_max[t] for t in range(lo, hi + 1)}
+    d["rank_mean"] = {t: s.rank_mean[t] for t in range(lo, hi + 1)}
+    d["t_phase_ms"] = {L.PHASES[i]: s.t_phase_ms[i] for i in range(L.H2_NPHASE)}
+    return d
+
+
+def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, **opts):
+    """Algorithm 1 on the current device.
+
+    kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
+    unless ``sketch`` is given).  sketch: optional callable sketch(omega, y, col0, row_begin,
+    row_end) filling y (tree-order rows) for a black-box K_blk; entry: optional callable
+    entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  opts: h2_build_opts
+    fields (d_init, d_blk, d_max, adaptive, tol_rule, tol_safety, p_os, norm, max_rank, seed,
+    stream_id)."""
+    o = build_opts(**opts)
+    kern = _kernel(*kernel)
+    keep = []
+    sk = L.h2_sketch()
+    sk.kern = kern
+    if sketch is None:
+        sk.kind = L.H2_S_DENSE_KERNEL
+    else:
+        sk.kind = L.H2_S_CALLBACK
+
+        def _sk(ctx, req):
+            try:
+                r = req.contents
+                n, nr, nc = r.n, r.row_end - r.row_begin, r.ncols
+                om = device_view(r.omega, (n, nc), (r.ld_omega, 1))
+                y = device_view(r.y, (nr, nc), (r.ld_y, 1))
+                sketch(om, y, r.col0, r.row_begin, r.row_end)
+                return 0
+            except Exception as exc:  # reported as H2_ERR_CALLBACK
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb = L.SKETCH_FN(_sk)
+        keep.append(cb)
+        sk.fn = cb
+    en = L.h2_entry()
+    en.kern = kern
+    if entry is None:
+        en.kind = L.H2_E_BUILTIN
+    else:
+        en.kind = L.H2_E_CALLBACK
+
+        def _en(ctx, batch):
+            try:
+                b = batch.contents
+                entry(b)
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+        cb2 = L.ENTRY_FN(_en)
+        keep.append(cb2)
+        en.fn = cb2
+    h = C.c_void_p()
+    st = L.h2_build_stats()
+    check(lib.h2_build(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o), _stream(stream), C.byref(h),
+                       C.byref(st)))
+    return H2Matrix(h, tree, _stats_dict(st), keep)
+
+
+def dense_sketch(tree: Tree, omega, kernel=("exp", 0.2), row_begin=0, row_end=None, out=None, stream=None):
+    """Y(rows, :) = K(rows, :) Omega with the built-in kernel (DMMA tile kernel)."""
+    row_end = tree.n if row_end is None else row_end
+    assert omega.is_cuda and omega.dtype == torch.float64 and omega.shape[0] == tree.n
+    nc = omega.shape[1]
+    if out is None:
+        out = torch.empty((row_end - row_begin, nc), dtype=torch.float64, device=omega.device)
+    check(lib.h2_dense_sketch(tree.handle, _kernel(*kernel), row_begin, row_end, _ptr(omega), omega.stride(0), nc,
+                              _ptr(out), out.stride(0), _stream(stream)))
+    return out
+
+
+def omega(nrows, ncols, seed=1, stream_id=0, row0=0, col0=0, device="cuda", stream=None):
+    """Rows [row0,row0+nrows) x columns [col0,col0+ncols) of the Omega stream (Philox4x32-10)."""
+    out = torch.empty((nrows, ncols), dtype=torch.float64, device=device)
+    check(lib.h2_omega(seed, stream_id, row0, nrows, col0, ncols, _ptr(out), out.stride(0), _stream(stream)))
+    return out
