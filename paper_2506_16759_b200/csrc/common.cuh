@@ -78,6 +78,57 @@ __device__ __forceinline__ double exp_neg(double x, const double* __restrict__ t
   return x < -700.0 ? 0.0 : r;
 }
 
+// ---------------------------------------------------------------------------------------
+// Sketch-path evaluation in SCALED coordinates x' = x*cs (cs = 1/l for exp, k for Helmholtz),
+// so r' = |x'-y'| is the kernel argument directly.  FP64-pipe cost per entry (SASS):
+//   r'^2: 6 (3 DADD, DMUL, 2 DFMA);  1/r' : MUFU.RSQ64H + 4 (one cubic correction, ~1 ulp,
+//   as libdevice rsqrt);  r' = r'^2/r': 1;  exp(-r'): 7 (shifter, 1-term Cody-Waite, degree-4
+//   polynomial on |g| <= ln2/512, 256-entry table, exponent arithmetic).
+// Absolute error <= ~2e-16 for exp entries (the 1-term reduction error kf*d(ln2/256) is damped
+// by e^{-r'}); the sketch only needs rounding-level accuracy in absolute terms.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y * y, 1.0);
+  double p = fma(e, 0.375, 0.5);
+  return fma(p, y * e, y);
+}
+
+// exp(-r) for r >= 0 with a 256-entry table of 2^(j/256)
+__device__ __forceinline__ double exp_neg256(double r, const double* __restrict__ tab) {
+  const double SH = 6755399441055744.0;                  // 1.5 * 2^52
+  double t = fma(r, -369.32993046757464, SH);            // -256/ln2
+  double kf = t - SH;
+  int n = __double2loint(t);                             // n = rint(-256 r / ln2) <= 0
+  double g = fma(kf, -0.0027076061740622863, -r);        // -r - kf ln2/256, |g| <= ln2/512
+  double p = fma(g, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(p, g, 0.5);
+  p = fma(p, g, 1.0);
+  p = fma(p, g, 1.0);
+  double v = tab[n & 255] * p;
+  v = __hiloint2double(__double2hiint(v) + ((n >> 8) << 20), __double2loint(v));
+  return n < -256 * 1000 ? 0.0 : v;
+}
+
+__device__ __forceinline__ void fill_exp_table256(double* tab) {
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) tab[j] = exp2((double)j * (1.0 / 256.0));
+}
+
+// K(r') in scaled coordinates; r2 = r'^2.  exp: e^{-r'};  Helmholtz: k cos(r')/r' (0 at r' = 0)
+template <int KIND>
+__device__ __forceinline__ double kernel_scaled(double r2, double k, const double* __restrict__ tab) {
+  const bool zero = __double2hiint(r2) < 0x00100000;     // r2 < 2^-1022 (incl. 0): integer test
+  double y = rsqrt_fast(zero ? 1.0 : r2);
+  if (KIND == H2_K_EXP) {
+    double r = zero ? 0.0 : r2 * y;
+    return exp_neg256(r, tab);
+  } else {
+    double r = r2 * y;
+    return zero ? 0.0 : k * cos(r) * y;
+  }
+}
+
 // 2^(j/64), j < 64, filled once per CTA (libdevice exp2, < 1 ulp)
 __device__ __forceinline__ void fill_exp_table(double* tab) {
   for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = exp2((double)j * (1.0 / 64.0));

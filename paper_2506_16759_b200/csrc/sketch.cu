@@ -73,7 +73,7 @@ void launch_omega(uint64_t seed, uint32_t sid, int64_t row0, int64_t nrows, int 
 constexpr int SK_JT = 32;       // j rows per smem stage
 constexpr int SK_LD = 36;       // padded Omega row stride (doubles), conflict-free B fragments
 
-template <int KIND, int MB, int MINB>
+template <int KIND, int MB, int MINB, int UNR>
 __global__ void __launch_bounds__(128, MINB)
     dense_sketch_kernel(const double* __restrict__ X, const double* __restrict__ Yc, const double* __restrict__ Zc,
                         int64_t n, int64_t row0, int64_t row1, const double* __restrict__ Om, int64_t ldo, int ncols,
@@ -82,8 +82,10 @@ __global__ void __launch_bounds__(128, MINB)
   constexpr int WR = 8 * MB;                       // rows per warp
   __shared__ __align__(16) double sOm[2][SK_JT * SK_LD];
   __shared__ double sx[2][SK_JT], sy[2][SK_JT], sz[2][SK_JT];
-  __shared__ double tab[64];
-  fill_exp_table(tab);
+  __shared__ double tab[256];
+  fill_exp_table256(tab);
+  // scaled coordinates x' = cs x: the kernel argument is |x'-y'| directly (cs = 1/l or k)
+  const double cs = KIND == H2_K_EXP ? inv : param;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rbase = row0 + (int64_t)blockIdx.x * (4 * WR) + warp * WR;
   // j slice of this CTA
@@ -94,9 +96,9 @@ __global__ void __launch_bounds__(128, MINB)
   for (int mb = 0; mb < MB; ++mb) {
     int64_t i = rbase + mb * 8 + (lane >> 2);
     if (i < row1) {
-      xi[mb] = X[i];
-      yi[mb] = Yc[i];
-      zi[mb] = Zc[i];
+      xi[mb] = X[i] * cs;
+      yi[mb] = Yc[i] * cs;
+      zi[mb] = Zc[i] * cs;
     } else {
       xi[mb] = yi[mb] = zi[mb] = 0.0;
     }
@@ -124,9 +126,9 @@ __global__ void __launch_bounds__(128, MINB)
     }
     if (threadIdx.x < SK_JT) {
       int64_t j = j0 + threadIdx.x;
-      sx[buf][threadIdx.x] = j < n ? X[j] : 0.0;
-      sy[buf][threadIdx.x] = j < n ? Yc[j] : 0.0;
-      sz[buf][threadIdx.x] = j < n ? Zc[j] : 0.0;
+      sx[buf][threadIdx.x] = j < n ? X[j] * cs : 0.0;
+      sy[buf][threadIdx.x] = j < n ? Yc[j] * cs : 0.0;
+      sz[buf][threadIdx.x] = j < n ? Zc[j] * cs : 0.0;
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(128, MINB)
     __syncthreads();
     const int64_t j0 = ch * SK_JT;
     const bool full = j0 + SK_JT <= n;
-#pragma unroll 2
+#pragma unroll UNR
     for (int ks = 0; ks < SK_JT / 4; ++ks) {
       const int jl = ks * 4 + (lane & 3);
       const double xj = sx[buf][jl], yj = sy[buf][jl], zj = sz[buf][jl];
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb) {
         double r2 = dist2(xi[mb], yi[mb], zi[mb], xj, yj, zj);
-        double v = kernel_of_r2<KIND>(r2, param, inv, tab);
+        double v = kernel_scaled<KIND>(r2, param, tab);
         a[mb] = jvalid ? v : 0.0;
       }
       double b[4];
@@ -199,22 +201,37 @@ int env_int(const char* name, int def) {
   return v ? atoi(v) : def;
 }
 
-template <int KIND, int MB, int MINB>
+template <int KIND, int MB, int MINB, int UNR>
 void sketch_variant(dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc, int64_t n,
                     int64_t row0, int64_t row1, const double* Om, int64_t ldo, int nc, double* Yo, int64_t ldy,
                     int64_t sstride, const KernelParams& kp, bool aligned) {
-  dense_sketch_kernel<KIND, MB, MINB><<<grid, 128, 0, st>>>(X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride,
-                                                            kp.param, kp.inv, aligned);
+  dense_sketch_kernel<KIND, MB, MINB, UNR><<<grid, 128, 0, st>>>(X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy,
+                                                                 sstride, kp.param, kp.inv, aligned);
 }
 
+// (rows-per-lane MB, min CTAs/SM, k-step unroll) variants; index from H2_SK_VAR (tuning)
+struct SkVar {
+  int rows, occ;   // rows per CTA, resident CTAs per SM
+};
+constexpr SkVar SK_VARS[] = {{128, 3}, {128, 3}, {128, 4}, {128, 4}, {64, 4}, {64, 5}, {64, 6}};
+constexpr int SK_DEFAULT_VAR = 1;
+
 template <int KIND>
-void sketch_dispatch(int mb, dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc,
+void sketch_dispatch(int var, dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc,
                      int64_t n, int64_t row0, int64_t row1, const double* Om, int64_t ldo, int nc, double* Yo,
                      int64_t ldy, int64_t sstride, const KernelParams& kp, bool aligned) {
-  if (mb == 2)
-    sketch_variant<KIND, 2, 4>(grid, st, X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride, kp, aligned);
-  else
-    sketch_variant<KIND, 4, 3>(grid, st, X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride, kp, aligned);
+#define H2_SKV(MB, MINB, UNR) \
+  sketch_variant<KIND, MB, MINB, UNR>(grid, st, X, Yc, Zc, n, row0, row1, Om, ldo, nc, Yo, ldy, sstride, kp, aligned)
+  switch (var) {
+    case 1: H2_SKV(4, 3, 1); break;
+    case 2: H2_SKV(4, 4, 1); break;
+    case 3: H2_SKV(4, 4, 2); break;
+    case 4: H2_SKV(2, 4, 2); break;
+    case 5: H2_SKV(2, 5, 1); break;
+    case 6: H2_SKV(2, 6, 1); break;
+    default: H2_SKV(4, 3, 2); break;
+  }
+#undef H2_SKV
 }
 }  // namespace
 
@@ -222,10 +239,11 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
                          int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                          int64_t ldy, cudaStream_t st) {
   if (row1 <= row0 || ncols <= 0) return;
-  const int mb = env_int("H2_SK_MB", 4) == 2 ? 2 : 4;
-  const int occ = mb == 2 ? 4 : 3;                 // resident CTAs / SM (registers)
+  int var = env_int("H2_SK_VAR", SK_DEFAULT_VAR);
+  if (var < 0 || var > 6) var = SK_DEFAULT_VAR;
+  const int occ = SK_VARS[var].occ;               // resident CTAs / SM (registers)
   const int64_t rows = row1 - row0;
-  const int tiles = div_up(rows, 4 * 8 * mb);
+  const int tiles = div_up(rows, SK_VARS[var].rows);
   int sms = 148;
   {
     int dev = 0;
@@ -259,9 +277,9 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
     const int64_t ld = S > 1 ? nc : ldy;
     const int64_t sstride = S > 1 ? rows * nc : 0;
     if (kp.kind == H2_K_EXP)
-      sketch_dispatch<H2_K_EXP>(mb, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp, aligned);
+      sketch_dispatch<H2_K_EXP>(var, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp, aligned);
     else
-      sketch_dispatch<H2_K_HELMHOLTZ>(mb, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp,
+      sketch_dispatch<H2_K_HELMHOLTZ>(var, grid, st, X, Yc, Zc, n, row0, row1, Om + c0, ldo, nc, yo, ld, sstride, kp,
                                       aligned);
     H2_CHECK_LAUNCH();
     if (S > 1) {

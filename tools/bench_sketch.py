@@ -9,9 +9,11 @@ X = uniform_points(n, 3, 0)
 T = g.Tree(X, 64)
 Om = g.omega(n, 32)
 ref = None
-for mb in ("4", "2"):
-    for sp in ("1", "2", "3", "0"):
-        os.environ["H2_SK_MB"], os.environ["H2_SK_SPLIT"] = mb, sp
+variants = sys.argv[2].split(",") if len(sys.argv) > 2 else [str(v) for v in range(7)]
+splits = sys.argv[3].split(",") if len(sys.argv) > 3 else ["0"]
+for mb in variants:
+    for sp in splits:
+        os.environ["H2_SK_VAR"], os.environ["H2_SK_SPLIT"] = mb, sp
         y = g.dense_sketch(T, Om)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -23,5 +25,5 @@ for mb in ("4", "2"):
         if ref is None:
             ref = y.clone()
         dev = (y - ref).abs().max().item() / ref.abs().max().item()
-        print(f"MB={mb} split={sp}: {ms:8.2f} ms  {2*n*n*32/ms/1e9:6.2f} TFLOP/s contraction  "
+        print(f"var={mb} split={sp}: {ms:8.2f} ms  {2*n*n*32/ms/1e9:6.2f} TFLOP/s contraction  "
               f"{n*n/ms/1e9:6.2f} Gentries/ms  rel-dev {dev:.1e}", flush=True)
