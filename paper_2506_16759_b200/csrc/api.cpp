@@ -97,8 +97,6 @@ struct Level {
   std::vector<int64_t> B_off;
   DArr<int64_t> d_B_off;
   DArr<double> B;
-  // panels of this depth: Y^loc / Omega^l (rows x LD); leaf depth aliases the sketch buffers
-  DArr<double> Yl, Ol;
 };
 
 }  // namespace
@@ -160,6 +158,24 @@ std::vector<T> download(const DArr<T>& a, int64_t n, cudaStream_t st) {
   return v;
 }
 
+// Sample panel of one depth: Y^l / Omega^l rows x ld, row-major (a point's samples contiguous,
+// the CPQR column of A = (Y^loc)^T).  Columns are appended in place; ld grows on demand.
+struct Panel {
+  DArr<double> Y, O;
+  int64_t rows = 0, ld = 0;
+  void alloc(int64_t r, int64_t l, cudaStream_t st) {
+    rows = r;
+    ld = l;
+    Y.alloc(std::max<int64_t>(r, 1) * l, st);
+    O.alloc(std::max<int64_t>(r, 1) * l, st);
+  }
+  void release() {
+    Y.release();
+    O.release();
+    rows = ld = 0;
+  }
+};
+
 struct Builder {
   const h2_tree& T;
   const h2_sketch& S;
@@ -169,13 +185,11 @@ struct Builder {
   cudaStream_t st;
   h2_matrix& H;
   KernelParams ekp{}, skp{};
-  int64_t LD = 0;
   int d = 0;
-  DArr<double> Y, Om;           // leaf-level sketch / random vectors (N x LD)
+  Panel cur;                    // full-width panel of the depth being processed
   DArr<double> sumsq_scratch, sumsq_acc;
   DArr<int> nonfinite;
   DArr<double> W;               // CPQR workspace
-  DArr<int32_t> d_leaf_cnt32;   // leaf sizes as int32
   PhaseTimer timer;
   int64_t entries_sketch = 0;
 
@@ -183,14 +197,34 @@ struct Builder {
           cudaStream_t stream, h2_matrix& h)
       : T(t), S(s), E(e), tol(tl), o(op), st(stream), H(h), timer(stream) {}
 
-  // ---------------------------------------------------------------- sketch of columns [c0, c1)
-  void draw(int c0, int c1) {
+  // panel leading dimension: d_max when the panel is small, else the needed width + 2 blocks
+  int64_t ld_for(int64_t rows, int dneed) const {
+    const int64_t full = o.d_max;
+    if (rows * full * 16 <= (int64_t(1) << 30)) return full;
+    int64_t l = ((dneed + 2 * (int64_t)o.d_blk + 31) / 32) * 32;
+    return std::min<int64_t>(std::max<int64_t>(l, dneed), full);
+  }
+
+  void grow(Panel& P, int dneed) {
+    if (dneed <= P.ld) return;
+    Panel Q;
+    Q.alloc(P.rows, ld_for(P.rows, dneed), st);
+    if (P.rows > 0 && d > 0) {
+      H2_CUDA(cudaMemcpy2DAsync(Q.Y.p, Q.ld * 8, P.Y.p, P.ld * 8, (size_t)d * 8, P.rows, cudaMemcpyDeviceToDevice, st));
+      H2_CUDA(cudaMemcpy2DAsync(Q.O.p, Q.ld * 8, P.O.p, P.ld * 8, (size_t)d * 8, P.rows, cudaMemcpyDeviceToDevice, st));
+    }
+    P = std::move(Q);
+  }
+
+  // ---------------------------------------------------------------- sketch of stream columns
+  // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
+  void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
     timer.begin(H2_PH_RAND);
-    launch_omega(o.seed, o.stream_id, 0, T.n, c0, c1 - c0, Om.p + c0, LD, st);
+    launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
     timer.end();
     timer.begin(H2_PH_SKETCH);
     if (S.kind == H2_S_DENSE_KERNEL) {
-      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om.p + c0, LD, c1 - c0, Y.p + c0, LD, st);
+      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, st);
       entries_sketch += T.n * T.n;
     } else {
       h2_sketch_req rq{};
@@ -198,18 +232,18 @@ struct Builder {
       rq.row_begin = 0;
       rq.row_end = T.n;
       rq.col0 = c0;
-      rq.ncols = c1 - c0;
-      rq.omega = Om.p + c0;
-      rq.ld_omega = LD;
-      rq.y = Y.p + c0;
-      rq.ld_y = LD;
+      rq.ncols = nc;
+      rq.omega = Od;
+      rq.ld_omega = ld;
+      rq.y = Yd;
+      rq.ld_y = ld;
       rq.stream = st;
       int rc = S.fn(S.ctx, &rq);
       if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
     }
     timer.end();
     timer.begin(H2_PH_MISC);
-    launch_sumsq(Y.p, T.n, LD, c0, c1, sumsq_scratch.p, sumsq_acc.p, nonfinite.p, st);
+    launch_sumsq(Yd, T.n, ld, 0, nc, sumsq_scratch.p, sumsq_acc.p, nonfinite.p, st);
     timer.end();
   }
 
@@ -249,14 +283,15 @@ struct Builder {
     timer.end();
   }
 
-  // ---------------------------------------------------------------- BSR subtraction at depth t
+  // ---------------------------------------------------------------- BSR subtraction on a panel of depth t
   // leaf (t == Dl): Y(I_tau) -= sum_{b in N_tau} D Om(I_b)   (L213)
-  // inner: Yl_t(rows of child nu) -= sum_{b in F_nu} B_{nu,b} Ol_t(rows of b)   (L240-243)
-  void bsr(int t, int c0, int c1) {
+  // inner: Y^l_t(rows of child nu) -= sum_{b in F_nu} B_{nu,b} Om^l_t(rows of b)   (L240-243)
+  // Y, O point at the first column to update; nc columns.
+  void bsr(int t, double* Yp, const double* Op, int64_t ld, int nc) {
     timer.begin(H2_PH_BSR);
     BsrArgs a{};
-    a.c0 = c0;
-    a.ncols = c1 - c0;
+    a.c0 = 0;
+    a.ncols = nc;
     if (t == T.Dl) {
       a.nclusters = 1 << T.Dl;
       a.max_rows = H.L(T.Dl).max_m;
@@ -268,11 +303,8 @@ struct Builder {
       a.us = T.d_near.us;
       a.blk_off = T.d_D_off;
       a.blk = H.D.p;
-      a.Y = Y.p;
-      a.Om = Om.p;
     } else {
       Level& C = H.L(t + 1);
-      Level& P = H.L(t);
       a.nclusters = C.nclus;
       a.max_rows = C.max_k;
       a.yoff = a.ooff = C.d_roff.p;
@@ -283,10 +315,10 @@ struct Builder {
       a.us = T.d_far[t + 1].us;
       a.blk_off = C.d_B_off.p;
       a.blk = C.B.p;
-      a.Y = P.Yl.p;
-      a.Om = P.Ol.p;
     }
-    a.ldy = a.ldo = LD;
+    a.Y = Yp;
+    a.Om = Op;
+    a.ldy = a.ldo = ld;
     launch_bsr(a, st);
     timer.end();
   }
@@ -323,7 +355,7 @@ struct Builder {
     L.cert.alloc(2 * L.nclus, st);
   }
 
-  // CPQR of every panel of depth t with the current d; returns host ranks
+  // CPQR of every panel of depth t (current panel, d columns); returns host ranks
   void cpqr(int t, double eps) {
     Level& L = H.L(t);
     int64_t need = std::max<int64_t>(L.rows * d, 1);
@@ -332,8 +364,8 @@ struct Builder {
     CpqrArgs a{};
     a.nclusters = L.nclus;
     a.max_m = std::max(L.max_m, 1);
-    a.Y = (t == T.Dl) ? Y.p : L.Yl.p;
-    a.ldy = LD;
+    a.Y = cur.Y.p;
+    a.ldy = cur.ld;
     a.poff = L.d_poff.p;
     a.m = L.d_m.p;
     a.d = d;
@@ -383,10 +415,10 @@ struct Builder {
     timer.end();
   }
 
-  // shrink + project committed depth u for columns [c0,c1) into the panels of depth u-1
-  void shrink(int u, int c0, int c1) {
+  // batchedShrink + Omega upsweep of committed depth u, nc columns: source panel (depth u)
+  // -> destination panel (depth u-1); pointers at the first column of each.
+  void shrink(int u, const double* Ys, const double* Os, int64_t lds, double* Yd, double* Od, int64_t ldd, int nc) {
     Level& L = H.L(u);
-    Level& P = H.L(u - 1);
     timer.begin(H2_PH_ID);
     ShrinkArgs a{};
     a.nclusters = L.nclus;
@@ -397,14 +429,14 @@ struct Builder {
     a.xoff = L.d_xoff.p;
     a.X = L.X.p;
     a.roff = L.d_roff.p;
-    a.Yl = (u == T.Dl) ? Y.p : L.Yl.p;
-    a.Ol = (u == T.Dl) ? Om.p : L.Ol.p;
-    a.ld = LD;
-    a.Yp = P.Yl.p;
-    a.Op = P.Ol.p;
-    a.ldp = LD;
-    a.c0 = c0;
-    a.c1 = c1;
+    a.Yl = Ys;
+    a.Ol = Os;
+    a.ld = lds;
+    a.Yp = Yd;
+    a.Op = Od;
+    a.ldp = ldd;
+    a.c0 = 0;
+    a.c1 = nc;
     launch_shrink_project(a, st);
     timer.end();
   }
@@ -429,6 +461,35 @@ struct Builder {
     gen(g);
   }
 
+  // updateSamples (L216-217, L246-247, L386): one new block of b stream columns, swept up through
+  // the committed depths Dl..t+1 with the stored D/B/J/U/E, appended to the panel of depth t.
+  // Intermediate depths use b-wide scratch panels; only depth t holds all d columns.
+  void update_samples(int t, int b) {
+    const int c0 = d;
+    grow(cur, d + b);
+    if (t == T.Dl) {
+      draw(cur.Y.p + c0, cur.O.p + c0, cur.ld, c0, b);
+      bsr(T.Dl, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
+      return;
+    }
+    Panel src;
+    src.alloc(T.n, b, st);
+    draw(src.Y.p, src.O.p, b, c0, b);
+    bsr(T.Dl, src.Y.p, src.O.p, b, b);
+    for (int u = T.Dl; u > t; --u) {
+      if (u - 1 == t) {
+        shrink(u, src.Y.p, src.O.p, src.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
+        bsr(t, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
+      } else {
+        Panel dst;
+        dst.alloc(H.L(u).rtot, b, st);
+        shrink(u, src.Y.p, src.O.p, src.ld, dst.Y.p, dst.O.p, dst.ld, b);
+        bsr(u - 1, dst.Y.p, dst.O.p, dst.ld, b);
+        src = std::move(dst);
+      }
+    }
+  }
+
   void run() {
     const int Dl = T.Dl;
     const int top = T.top < 0 ? Dl : T.top;
@@ -438,18 +499,16 @@ struct Builder {
     H.lv.resize(Dl - top + 1);
     if (S.kind == H2_S_DENSE_KERNEL) skp = make_kernel(S.kern);
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
-    LD = o.d_max;
     d = std::min(o.d_init, o.d_max);
-    Y.alloc(T.n * LD, st);
-    Om.alloc(T.n * LD, st);
     sumsq_scratch.alloc(div_up(T.n, 1024), st);
     sumsq_acc.alloc(1, st);
     nonfinite.alloc(1, st);
     H2_CUDA(cudaMemsetAsync(sumsq_acc.p, 0, sizeof(double), st));
     H2_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
 
-    // line 1: Y = K_blk(Omega)
-    draw(0, d);
+    // line 1: Y = K_blk(Omega) into the leaf panel (leaf Y^loc is computed in place)
+    cur.alloc(T.n, ld_for(T.n, d), st);
+    draw(cur.Y.p, cur.O.p, cur.ld, 0, d);
     // line 212: D_{tau,b} = K(I_tau, I_b), one unique block per unordered pair
     H.D.alloc(T.D_off.back(), st);
     {
@@ -465,11 +524,11 @@ struct Builder {
       gen(g);
     }
     setup_level(Dl);
-    bsr(Dl, 0, d);   // line 213
+    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
     for (int t = Dl; t >= top; --t) {
       if (t < Dl) {
         setup_level(t);
-        bsr(t, 0, d);   // lines 240-243
+        bsr(t, cur.Y.p, cur.O.p, cur.ld, d);   // lines 240-243
       }
       Level& L = H.L(t);
       int rounds = 0;
@@ -488,31 +547,24 @@ struct Builder {
           throw Error(H2_ERR_NOT_CONVERGED, "adaptive sampling reached d_max=" + std::to_string(o.d_max) +
                                                 " at depth " + std::to_string(t));
         }
-        // updateSamples (L216-217, L246-247, L386): new block, swept up to depth t
-        const int c0 = d, c1 = d + o.d_blk;
-        draw(c0, c1);
-        bsr(Dl, c0, c1);
-        for (int u = Dl; u > t; --u) {
-          shrink(u, c0, c1);
-          bsr(u - 1, c0, c1);
-        }
-        d = c1;
+        update_samples(t, o.d_blk);
+        d += o.d_blk;
       }
       H.stats.rounds[t] = rounds;
       H.stats.eps = eps;
       commit(t);                                    // lines 221-224 / 250-253
-      if (t > top) {
-        Level& P = H.L(t - 1);
-        P.Yl.alloc(std::max<int64_t>(L.rtot, 1) * LD, st);
-        P.Ol.alloc(std::max<int64_t>(L.rtot, 1) * LD, st);
-        shrink(t, 0, d);
+      Panel next;
+      if (t > top) {                                // lines 222-223 / 251-252 into the parent panel
+        next.alloc(L.rtot, ld_for(L.rtot, d), st);
+        shrink(t, cur.Y.p, cur.O.p, cur.ld, next.Y.p, next.O.p, next.ld, d);
       }
       gen_B(t);                                     // line 258
+      cur = std::move(next);
     }
     H2_CUDA(cudaStreamSynchronize(st));
-    for (auto& L : H.lv) {   // sample panels are build scratch, not part of the H^2 matrix
-      L.Yl.release();
-      L.Ol.release();
+    cur.release();
+    W.release();
+    for (auto& L : H.lv) {
       for (auto* a : {&L.d_m, &L.d_k, &L.d_perm, &L.d_skel}) a->detach();
       for (auto* a : {&L.d_poff, &L.d_roff, &L.d_xoff, &L.d_B_off}) a->detach();
       for (auto* a : {&L.X, &L.cert, &L.B}) a->detach();
@@ -895,7 +947,7 @@ int64_t h2_matrix_device_bytes(const h2_matrix* H) {
   if (!H) return 0;
   int64_t b = H->D.bytes();
   for (auto& L : H->lv)
-    b += L.X.bytes() + L.B.bytes() + L.d_skel.bytes() + L.d_perm.bytes() + L.Yl.bytes() + L.Ol.bytes();
+    b += L.X.bytes() + L.B.bytes() + L.d_skel.bytes() + L.d_perm.bytes();
   return b;
 }
 
