@@ -166,19 +166,8 @@ def run_ours(args, w, rank, world, local_rank):
     sketch = None
     if world > 1:
         import torch.distributed as dist
-        bounds = [n * r // world for r in range(world + 1)]
-        r0, r1 = bounds[rank], bounds[rank + 1]
-        maxrows = max(bounds[i + 1] - bounds[i] for i in range(world))
-
-        def sketch(om, y, col0, rb, re):
-            nc = om.shape[1]
-            part = torch.zeros((maxrows, nc), dtype=torch.float64, device=dev)
-            g.dense_sketch(T, om, kern, r0, r1, out=part[: r1 - r0])
-            gathered = torch.empty((world * maxrows, nc), dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(gathered, part)
-            for r in range(world):
-                a, b = bounds[r], bounds[r + 1]
-                y[a:b].copy_(gathered[r * maxrows: r * maxrows + (b - a)])
+        from paper_2506_16759_b200.dist import ShardedSketch, dense_shard_fn
+        sketch = ShardedSketch(n, dense_shard_fn(T, kern))
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream()
