@@ -229,7 +229,11 @@ def run_ours(args, w, rank, world, local_rank):
         for _ in range(max(1, min(args.steps, 3))):
             t0 = time.perf_counter()
             T2 = g.Tree(Xpin.numpy(), w["leaf"], 0.7)
-            H2 = g.build(T2, kern, w["tol"], sketch=None if world == 1 else sketch, **opts)
+            sk2 = None
+            if world > 1:
+                from paper_2506_16759_b200.dist import ShardedSketch, dense_shard_fn
+                sk2 = ShardedSketch(n, dense_shard_fn(T2, kern))
+            H2 = g.build(T2, kern, w["tol"], sketch=sk2, **opts)
             d2h = 0
             for t in range(H2.top_depth, T2.leaf_depth + 1):
                 d2h += H2.rank(t).nbytes // 2 + sum(s.nbytes // 2 for s in H2.skel(t))
@@ -261,6 +265,8 @@ def run_ours(args, w, rank, world, local_rank):
                    "parallelism": f"sketch rows x{world}" if world > 1 else "1 GPU",
                    "l2": "256 MiB flush before every timed step; working set (N x d_max x 16 B = 2 GiB) > L2"},
         "samples": st["samples"], "verified_error": verr,
+        "step_ms": [round(t, 2) for t in times],
+        "host_wall_ms": [round(s["t_total_ms"], 2) for s in stats],
         "ranks": {str(t): [st["rank_min"][t], st["rank_max"][t], round(st["rank_mean"][t], 1)]
                   for t in st["rank_min"]},
         "rounds": st["rounds"],

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -14,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "alloc.hpp"
 #include "kernels.hpp"
 #include "tree.hpp"
 
@@ -25,22 +27,10 @@ void count_launch() { ++g_launches; }
 namespace {
 
 thread_local std::string g_err;
+thread_local double g_alloc_ms = 0;   // host time inside cudaMallocAsync (H2_TRACE=1 diagnostics)
 
-// Stream-ordered device array from the device's default memory pool.  The pool keeps freed
-// memory mapped (release threshold = max, set once per device), so the per-level "single
-// allocation per operation" of PAPER.md L384 costs no page mapping after the first build.
-void retain_pool_memory() {
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
-}
-
+// Stream-ordered device array on the libh2 block cache (alloc.hpp): the per-level "single
+// allocation per operation" of PAPER.md L384 is a cache hit after the first build.
 template <class T>
 struct DArr {
   T* p = nullptr;
@@ -63,7 +53,7 @@ struct DArr {
   }
   ~DArr() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) h2::cache_free(p, st);
     p = nullptr;
     n = 0;
   }
@@ -73,7 +63,9 @@ struct DArr {
     release();
     n = cnt;
     st = stream;
-    H2_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * std::max<int64_t>(cnt, 1), stream));
+    auto t0 = std::chrono::steady_clock::now();
+    p = static_cast<T*>(h2::cache_alloc(sizeof(T) * std::max<int64_t>(cnt, 1), stream));
+    g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc((int64_t)v.size(), st);
@@ -121,8 +113,11 @@ struct PhaseTimer {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
   int cur = -1;
   cudaEvent_t cur_ev{};
+  double host_ms[H2_NPHASE] = {};   // host wall time spent issuing each phase (H2_TRACE=1)
+  std::chrono::steady_clock::time_point h0;
   explicit PhaseTimer(cudaStream_t s) : st(s) {}
   void begin(int ph) {
+    h0 = std::chrono::steady_clock::now();
     cudaEvent_t e;
     H2_CUDA(cudaEventCreate(&e));
     H2_CUDA(cudaEventRecord(e, st));
@@ -134,6 +129,7 @@ struct PhaseTimer {
     H2_CUDA(cudaEventCreate(&e));
     H2_CUDA(cudaEventRecord(e, st));
     ev.push_back({cur, {cur_ev, e}});
+    host_ms[cur] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   }
   void collect(double* out) {
     for (auto& x : ev) {
@@ -596,6 +592,11 @@ struct Builder {
       else s.bytes_E += L.X.bytes();
     }
     timer.collect(s.t_phase_ms);
+    if (getenv("H2_TRACE")) {
+      fprintf(stderr, "[h2 trace] host ms per phase:");
+      for (int p = 0; p < H2_NPHASE; ++p) fprintf(stderr, " %.1f", timer.host_ms[p]);
+      fprintf(stderr, " | alloc %.1f ms\n", g_alloc_ms);
+    }
   }
 };
 
@@ -723,7 +724,7 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
   H->stats.failed_depth = -1;
   int64_t launches0 = h2::g_launches;
   auto t0 = std::chrono::steady_clock::now();
-  retain_pool_memory();
+  g_alloc_ms = 0;
   try {
     H2_REQUIRE(tree && sketch && entry, "h2_build: NULL tree/sketch/entry");
     H2_REQUIRE(tol >= 0 && std::isfinite(tol), "h2_build: tol must be finite and >= 0");

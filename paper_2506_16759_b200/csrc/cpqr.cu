@@ -47,6 +47,9 @@ constexpr int CQ_WARPS = CQ_THREADS / 32;
 // (a point's d samples, contiguous).  Residual column norms are RECOMPUTED from the updated
 // trailing rows every step (R14); the norm for step i+1 is fused into the reflector update of
 // step i (one pass over the trailing panel per step).
+// SMEM: the panel is factored in shared memory (m*d*8 bytes fit) and written back to W for the
+// ID epilogue; otherwise it is factored in place in W (L1/L2 resident).
+template <bool SMEM>
 __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   extern __shared__ double smem[];
   const int c = blockIdx.x;
@@ -55,12 +58,13 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   double* v = smem;                       // d
   double* nrm = v + d;                    // m
   int* perm = (int*)(nrm + a.max_m);      // m
+  double* spanel = nrm + a.max_m + (a.max_m + 1) / 2;   // m*d (SMEM variant)
   __shared__ Top2 red[CQ_WARPS];
   __shared__ double redd[CQ_WARPS];
   __shared__ double s_tau, s_beta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t off = a.poff[c];
-  double* A = a.W + off * d;
+  double* A = SMEM ? spanel : a.W + off * d;
   // copy panel rows (Y^loc rows) into the work panel
   for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
     int64_t j = e / d;
@@ -182,6 +186,10 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   }
   __syncthreads();
   for (int j = threadIdx.x; j < m; j += CQ_THREADS) a.perm[off + j] = perm[j];
+  if (SMEM) {
+    double* Wc = a.W + off * d;
+    for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) Wc[e] = A[e];
+  }
   if (threadIdx.x == 0) {
     a.k[c] = k;
     a.cert[2 * c] = min_gap;
@@ -191,9 +199,18 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
 
 void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
-  size_t sm = sizeof(double) * (a.d + a.max_m) + sizeof(int) * a.max_m;
-  if (sm > 48 * 1024) H2_CUDA(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  cpqr_kernel<<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+  size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
+  size_t panel = sizeof(double) * (size_t)a.max_m * a.d;
+  if (sm + panel <= 200 * 1024) {
+    sm += panel;
+    if (sm > 48 * 1024)
+      H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    cpqr_kernel<true><<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+  } else {
+    if (sm > 48 * 1024)
+      H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    cpqr_kernel<false><<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+  }
   H2_CHECK_LAUNCH();
 }
 

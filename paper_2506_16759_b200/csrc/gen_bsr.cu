@@ -80,21 +80,26 @@ void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* r
 // inside a block: the accumulation order is fixed -> deterministic, no atomics (L385).
 // Blocks are stored once per unordered pair; (s,b) with s != us[u] reads the transpose.
 // ------------------------------------------------------------------------------------------
-// DMMA tiling: CTA = 4 warps = 64 rows x 32 columns; warp w owns rows 16w..16w+15 (2 m-blocks)
-// x all 4 n-blocks (16 accumulators / lane).  Partner blocks stream through shared memory in
-// 32-deep k-slabs; row stride 36 doubles makes the A/B fragment loads bank-conflict free.
-constexpr int BT_R = 64, BT_K = 32, BT_C = 32, BT_LD = 36;
+// DMMA tiling: CTA = 4*(CW/32) warps = 64 rows x CW columns; warp (wr, wc) owns rows
+// 16wr..16wr+15 (2 m-blocks) x columns 32wc..32wc+31 (4 n-blocks): 16 accumulators / lane.
+// Partner blocks stream through shared memory in 32-deep k-slabs (each block entry is read
+// once per CW columns); row strides = 4 mod 16 doubles keep the fragment loads conflict free.
+constexpr int BT_R = 64, BT_K = 32, BT_LD = 36;
 
-__global__ void __launch_bounds__(128) bsr_kernel(BsrArgs a, double alpha) {
+template <int CW>
+__global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
+  constexpr int NT = 4 * CW;           // threads
+  constexpr int LDB = CW + 4;
   __shared__ __align__(16) double sA[BT_R * BT_LD];
-  __shared__ __align__(16) double sB[BT_K * BT_LD];
+  __shared__ __align__(16) double sB[BT_K * LDB];
   const int s = blockIdx.x;
   const int ms = a.cnt[s];
   const int r0 = blockIdx.y * BT_R;
-  const int cb = a.c0 + blockIdx.z * BT_C;
-  const int nc = min(BT_C, a.c0 + a.ncols - cb);
+  const int cb = a.c0 + blockIdx.z * CW;
+  const int nc = min(CW, a.c0 + a.ncols - cb);
   if (r0 >= ms || nc <= 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wr = warp & 3, wc = warp >> 2;
   double acc[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -111,19 +116,19 @@ __global__ void __launch_bounds__(128) bsr_kernel(BsrArgs a, double alpha) {
       const int nk = min(BT_K, mb - k0);
       __syncthreads();
       if (direct) {   // stored (s, b): rows of s contiguous along k
-        for (int t = threadIdx.x; t < BT_R * BT_K; t += 128) {
+        for (int t = threadIdx.x; t < BT_R * BT_K; t += NT) {
           int r = t >> 5, kk = t & 31;
           sA[r * BT_LD + kk] = (r0 + r < ms && kk < nk) ? blk[(int64_t)(r0 + r) * mb + k0 + kk] : 0.0;
         }
       } else {        // stored (b, s): read the transpose, coalesced along the rows of s
-        for (int t = threadIdx.x; t < BT_R * BT_K; t += 128) {
+        for (int t = threadIdx.x; t < BT_R * BT_K; t += NT) {
           int kk = t >> 6, r = t & 63;
           sA[r * BT_LD + kk] = (r0 + r < ms && kk < nk) ? blk[(int64_t)(k0 + kk) * ms + r0 + r] : 0.0;
         }
       }
-      for (int t = threadIdx.x; t < BT_K * BT_C; t += 128) {
-        int kk = t >> 5, c = t & 31;
-        sB[kk * BT_LD + c] = (kk < nk && c < nc) ? om[(int64_t)(k0 + kk) * a.ldo + c] : 0.0;
+      for (int t = threadIdx.x; t < BT_K * CW; t += NT) {
+        int kk = t / CW, c = t % CW;
+        sB[kk * LDB + c] = (kk < nk && c < nc) ? om[(int64_t)(k0 + kk) * a.ldo + c] : 0.0;
       }
       __syncthreads();
       const int ksteps = (nk + 3) >> 2;
@@ -131,9 +136,9 @@ __global__ void __launch_bounds__(128) bsr_kernel(BsrArgs a, double alpha) {
         const int kk = ks * 4 + (lane & 3);
         double af[2], bf[4];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) af[i] = sA[(warp * 16 + i * 8 + (lane >> 2)) * BT_LD + kk];
+        for (int i = 0; i < 2; ++i) af[i] = sA[(wr * 16 + i * 8 + (lane >> 2)) * BT_LD + kk];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = sB[kk * BT_LD + j * 8 + (lane >> 2)];
+        for (int j = 0; j < 4; ++j) bf[j] = sB[kk * LDB + wc * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -143,12 +148,12 @@ __global__ void __launch_bounds__(128) bsr_kernel(BsrArgs a, double alpha) {
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const int r = r0 + warp * 16 + i * 8 + (lane >> 2);
+    const int r = r0 + wr * 16 + i * 8 + (lane >> 2);
     if (r >= ms) continue;
     double* y = a.Y + (a.yoff[s] + r) * a.ldy + cb;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int c = j * 8 + 2 * (lane & 3);
+      const int c = wc * 32 + j * 8 + 2 * (lane & 3);
       if (c < nc) y[c] = fma(alpha, acc[i][j][0], y[c]);
       if (c + 1 < nc) y[c + 1] = fma(alpha, acc[i][j][1], y[c + 1]);
     }
@@ -157,8 +162,13 @@ __global__ void __launch_bounds__(128) bsr_kernel(BsrArgs a, double alpha) {
 
 static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
-  dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, BT_C));
-  bsr_kernel<<<grid, 128, 0, st>>>(a, alpha);
+  if (a.ncols > 32) {
+    dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 64));
+    bsr_kernel<64><<<grid, 256, 0, st>>>(a, alpha);
+  } else {
+    dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 32));
+    bsr_kernel<32><<<grid, 128, 0, st>>>(a, alpha);
+  }
   H2_CHECK_LAUNCH();
 }
 

@@ -2,6 +2,7 @@
 // dense-kernel sketch Y = K Omega (Algorithm 1 line 1 with K_blk = the dense kernel matrix,
 // BASELINE configs[1]); plus the sketch-norm reduction used by the tolerance rule (R10).
 #include "common.cuh"
+#include "alloc.hpp"
 #include "kernels.hpp"
 
 #include <cstdlib>
@@ -267,7 +268,7 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
     }
   }
   double* part = nullptr;
-  if (S > 1) H2_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * rows * 32 * S, st));
+  if (S > 1) part = static_cast<double*>(cache_alloc(sizeof(double) * rows * 32 * S, st));
   for (int c0 = 0; c0 < ncols; c0 += 32) {
     int nc = std::min(32, ncols - c0);
     // 16-byte cp.async staging needs 16-byte aligned Omega rows
@@ -288,7 +289,7 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
       H2_CHECK_LAUNCH();
     }
   }
-  if (part) H2_CUDA(cudaFreeAsync(part, st));
+  if (part) cache_free(part, st);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -1,0 +1,62 @@
+"""One-off run of a BASELINE workload at full size on one GPU (no oracle): build time per phase,
+samples, ranks, memory, and the dense-probe error ||H X - K X||_F / ||K X||_F (16 probes, the
+products K X computed by the GPU dense-sketch kernel).
+
+  python tools/run_config.py cov3d_2m [--reps 1] [--s 0.1]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2506_16759_b200 as g
+from synth import WORKLOADS
+
+p = argparse.ArgumentParser()
+p.add_argument("workload")
+p.add_argument("--reps", type=int, default=1)
+p.add_argument("--s", type=float, default=0.1)
+p.add_argument("--d-blk", type=int, default=32)
+p.add_argument("--probes", type=int, default=16)
+a = p.parse_args()
+w = dict(WORKLOADS[a.workload])
+X = w["points"]()
+n = X.shape[0]
+kern = (w["kernel"], w["param"])
+t0 = time.perf_counter()
+T = g.Tree(X, w["leaf"], 0.7)
+t_tree = time.perf_counter() - t0
+out = {"workload": a.workload, "n": n, "leaf": w["leaf"], "tol": w["tol"], "tree_s": t_tree,
+       "leaf_depth": T.leaf_depth, "top_depth": T.top_depth, "near_nnz": T.near_nnz, "far_nnz": T.far_nnz_total,
+       "csp": T.csp}
+times = []
+for r in range(a.reps):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s)
+    e1.record()
+    e1.synchronize()
+    times.append(e0.elapsed_time(e1) / 1e3)
+    if r < a.reps - 1:
+        del H
+st = H.stats
+out.update({"build_s": times, "samples": st["samples"], "phase_ms": st["t_phase_ms"], "rounds": st["rounds"],
+            "ranks": {t: [st["rank_min"][t], st["rank_max"][t], round(st["rank_mean"][t], 1)] for t in st["rank_min"]},
+            "entries_D": st["entries_D"], "entries_B": st["entries_B"], "matrix_GB": H.device_bytes() / 1e9,
+            "peak_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "launches": st["launches"]})
+Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, a.probes))).cuda()
+t0 = time.perf_counter()
+KX = g.dense_sketch(T, Xp, kern)
+HX = H.matvec(Xp)
+torch.cuda.synchronize()
+out["probe_error"] = float(torch.linalg.norm(HX - KX) / torch.linalg.norm(KX))
+out["probe_s"] = time.perf_counter() - t0
+free, total = torch.cuda.mem_get_info()
+out["device_free_GB_after"] = free / 1e9
+print(json.dumps(out))
