@@ -101,7 +101,7 @@ def oracle_sample_seconds(w, X, samples_hint, budget_rows=96, leaves=16):
     tree = geometry.build_cluster_tree(X, w["leaf"])
     Dl = tree.leaf_depth
     op = kernels.KernelOperator(w["kernel"], w["param"], X[tree.perm])
-    om32 = rng.gaussian_block(1, 0, 0, n, 0, 32)
+    om32 = rng.omega_block(1, 0, 0, n, 0, 32)
     rows = np.arange(0, n, max(1, n // budget_rows))[:budget_rows]
     t0 = time.perf_counter()
     op.sketch_rows(om32, rows)
@@ -109,7 +109,7 @@ def oracle_sample_seconds(w, X, samples_hint, budget_rows=96, leaves=16):
     # leaf-level sample (partition of the whole tree is needed for N_tau; build it untimed)
     part = geometry.build_partition(tree, 0.7)
     d = samples_hint
-    Om = rng.gaussian_block(1, 0, 0, n, 0, d)
+    Om = rng.omega_block(1, 0, 0, n, 0, d)
     rng_of = lambda c: np.arange(tree.begin[Dl][c], tree.end[Dl][c])
     lv = np.linspace(0, (1 << Dl) - 1, leaves).astype(int)
     Ys = {c: np.random.default_rng(c).standard_normal((len(rng_of(c)), d)) for c in lv}  # stand-in samples

@@ -196,13 +196,17 @@ h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y,
                     int32_t ncols, double alpha, double beta, void* stream);
 
 /* Built-in dense operator product, rows [row_begin,row_end): y = K(rows,:) * omega (the dense
- * sketch of BASELINE configs[1], also the multi-GPU row shard).  omega: dev, all n rows. */
+ * sketch of BASELINE configs[1], also the multi-GPU row shard).  omega: dev, all n rows.
+ * flags: H2_SKETCH_OMEGA_QUARTERS asserts every omega entry is q/4 with integer |q| <= 32 (true
+ * for the h2_omega stream); it enables the exact int8 tensor-core contraction for H2_K_EXP.
+ * Without it (arbitrary omega) the FP64 DMMA path runs. */
+enum { H2_SKETCH_OMEGA_QUARTERS = 1 };
 h2_status h2_dense_sketch(const h2_tree* tree, h2_kernel kern, int64_t row_begin, int64_t row_end,
                           const double* omega, int64_t ld_omega, int32_t ncols, double* y,
-                          int64_t ld_y, void* stream);
+                          int64_t ld_y, int32_t flags, void* stream);
 
-/* Omega stream (Philox4x32-10 + Box-Muller, R8): rows [row0,row0+nrows) x sample
- * columns [col0,col0+ncols) into out (dev, row-major, leading dim ld). */
+/* Omega stream (Philox4x32-10 -> centred binomial (popcount(64 bits) - 32)/4, R8):
+ * rows [row0,row0+nrows) x sample columns [col0,col0+ncols) into out (dev, row-major, ld). */
 h2_status h2_omega(uint64_t seed, uint32_t stream_id, int64_t row0, int64_t nrows, int32_t col0,
                    int32_t ncols, double* out, int64_t ld, void* stream);
 

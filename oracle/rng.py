@@ -1,15 +1,16 @@
-"""Counter-based Gaussian random matrix Omega for Algorithm 1 line 1 (PAPER.md L203,
-"Y = K_blk(Omega) with a random Omega"; L384 "generated in a single kernel").  TEST INFRA.
+"""Counter-based random matrix Omega for Algorithm 1 line 1 ("Y = K_blk(Omega)
+with a random Omega"; L384 "generated in a single kernel").  TEST INFRA.
 
-Reading (R8): Omega is i.i.d. standard normal.  Entry (i, j) of the stream
-(i = tree-order row, j = global sample column) is produced from one Philox4x32-10 block
-(Salmon et al., SC'11, "Parallel random numbers: as easy as 1, 2, 3") with
-  counter = (i, j // 2, stream, 0),  key = (seed mod 2^32, seed >> 32)
-whose 4 words give two 53-bit uniforms u1 = ((w1:w0) >> 11 + 0.5) 2^-53 and
-u2 = ((w3:w2) >> 11 + 0.5) 2^-53, and the Box-Muller pair
-  Omega(i, 2q)   = sqrt(-2 ln u1) cos(2 pi u2),
-  Omega(i, 2q+1) = sqrt(-2 ln u1) sin(2 pi u2).
-The CUDA path implements the same generator independently (csrc/rand.cu).
+Reading (R8): the paper only asks for "a random matrix".  Omega is i.i.d. with the
+centred, scaled binomial distribution  Omega = (B - 32) / 4,  B ~ Binomial(64, 1/2): mean 0,
+variance 1, sub-Gaussian, values in {-8, -7.75, ..., 8} -- exactly representable, so the CPU
+oracle and the GPU produce bit-identical Omega, and the GPU sketch can multiply it exactly on the
+int8 tensor cores.  Entry (i, j) (i = tree-order row, j = global sample column) comes from one
+Philox4x32-10 block (Salmon et al., SC'11, "Parallel random numbers: as easy as 1, 2, 3"):
+  counter = (i, j // 2, stream, 0),  key = (seed mod 2^32, seed >> 32),
+  Omega(i, 2q)   = (popcount(w0) + popcount(w1) - 32) / 4,
+  Omega(i, 2q+1) = (popcount(w2) + popcount(w3) - 32) / 4.
+The CUDA path implements the same generator independently (csrc/sketch.cu).
 """
 import numpy as np
 
@@ -44,12 +45,7 @@ def philox4x32_10(ctr, key):
     return np.stack(c)
 
 
-def _u53(lo, hi):
-    v = (hi.astype(np.uint64) << np.uint64(32)) | lo.astype(np.uint64)
-    return ((v >> np.uint64(11)).astype(np.float64) + 0.5) * (2.0 ** -53)
-
-
-def gaussian_block(seed: int, stream: int, row0: int, nrows: int, col0: int, ncols: int) -> np.ndarray:
+def binomial_block(seed: int, stream: int, row0: int, nrows: int, col0: int, ncols: int) -> np.ndarray:
     """Rows [row0, row0+nrows) x columns [col0, col0+ncols) of the Omega stream, float64."""
     if nrows <= 0 or ncols <= 0:
         return np.zeros((max(nrows, 0), max(ncols, 0)))
@@ -62,13 +58,15 @@ def gaussian_block(seed: int, stream: int, row0: int, nrows: int, col0: int, nco
                     np.full(n, stream, np.uint32), np.zeros(n, np.uint32)])
     key = np.stack([np.full(n, seed & 0xFFFFFFFF, np.uint32), np.full(n, (seed >> 32) & 0xFFFFFFFF, np.uint32)])
     w = philox4x32_10(ctr, key)
-    u1 = _u53(w[0], w[1])
-    u2 = _u53(w[2], w[3])
-    rad = np.sqrt(-2.0 * np.log(u1))
-    g0 = rad * np.cos(2.0 * np.pi * u2)
-    g1 = rad * np.sin(2.0 * np.pi * u2)
+    pc = np.bitwise_count(w).astype(np.int64)
+    g0 = (pc[0] + pc[1] - 32).astype(np.float64) / 4.0
+    g1 = (pc[2] + pc[3] - 32).astype(np.float64) / 4.0
     g = np.empty((nrows, (q1 - q0) * 2))
     g[:, 0::2] = g0.reshape(nrows, q1 - q0)
     g[:, 1::2] = g1.reshape(nrows, q1 - q0)
     off = col0 - 2 * q0
     return np.ascontiguousarray(g[:, off:off + ncols])
+
+
+# the Omega stream used by Algorithm 1 (R8)
+omega_block = binomial_block

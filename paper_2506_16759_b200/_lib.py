@@ -18,6 +18,7 @@ H2_S_DENSE_KERNEL, H2_S_CALLBACK = 0, 1
 H2_E_BUILTIN, H2_E_CALLBACK = 0, 1
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT = range(6)
+H2_SKETCH_OMEGA_QUARTERS = 1
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
 H2_NPHASE = len(PHASES)
 
@@ -86,7 +87,8 @@ SIGNATURES = {
     "h2_build": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts), _P,
                            C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_matvec": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P]),
-    "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64, _P]),
+    "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64,
+                                  C.c_int32, _P]),
     "h2_omega": (C.c_int, [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, C.c_int64, _P]),
     "h2_export_size": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "h2_export": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),

@@ -220,7 +220,7 @@ struct Builder {
     timer.end();
     timer.begin(H2_PH_SKETCH);
     if (S.kind == H2_S_DENSE_KERNEL) {
-      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, st);
+      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
       entries_sketch += T.n * T.n;
     } else {
       h2_sketch_req rq{};
@@ -869,7 +869,7 @@ h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y,
 }
 
 h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, int64_t row_end, const double* omega,
-                          int64_t ld_omega, int32_t ncols, double* y, int64_t ld_y, void* stream) {
+                          int64_t ld_omega, int32_t ncols, double* y, int64_t ld_y, int32_t flags, void* stream) {
   try {
     H2_REQUIRE(T && omega && y, "h2_dense_sketch: NULL argument");
     H2_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= T->n, "h2_dense_sketch: bad row range");
@@ -877,7 +877,7 @@ h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, i
     H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ) && kern.param > 0, "h2_dense_sketch: bad kernel");
     ensure_uploaded(T);
     launch_dense_sketch(make_kernel(kern), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
-                        ld_y, (cudaStream_t)stream);
+                        ld_y, (flags & H2_SKETCH_OMEGA_QUARTERS) != 0, (cudaStream_t)stream);
     return H2_OK;
   } catch (const Error& e) {
     return fail(e);

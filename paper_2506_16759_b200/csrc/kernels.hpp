@@ -11,9 +11,16 @@ namespace h2 {
 void launch_omega(uint64_t seed, uint32_t sid, int64_t row0, int64_t nrows, int col0, int ncols, double* out,
                   int64_t ld, cudaStream_t st);
 // built-in dense sketch Y(rows,:) = K(rows,:) Omega                              (L203 with K_blk = K)
+// omega_quarters: every entry is q/4, |q| <= 32 (the h2_omega stream) -> int8 tensor-core path
 void launch_dense_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                          int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
-                         int64_t ldy, cudaStream_t st);
+                         int64_t ldy, bool omega_quarters, cudaStream_t st);
+// exp-kernel sketch on the int8 tensor cores (tcgen05 kind::i8, exact slices; sketch_tc.cu)
+bool sketch_tc_supported(const KernelParams& kp);
+void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                            int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
+                            int64_t ldy, cudaStream_t st);
+void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, double* Y, int64_t ldy, cudaStream_t st);
 // accum += ||Y(:, c0:c1)||_F^2 (deterministic)                                   (R10 tolerance scale)
 void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum,
                   int* nonfinite, cudaStream_t st);

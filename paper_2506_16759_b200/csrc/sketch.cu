@@ -10,7 +10,7 @@
 namespace h2 {
 
 // ------------------------------------------------------------------------------------------
-// Philox4x32-10 (Salmon et al. SC'11) -> two 53-bit uniforms -> Box-Muller pair (R8)
+// Philox4x32-10 (Salmon et al. SC'11) -> two centred-binomial entries (R8)
 // counter = (row, column pair q, stream id, 0), key = (seed lo, seed hi)
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
@@ -27,11 +27,6 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-__device__ __forceinline__ double u53(uint32_t lo, uint32_t hi) {
-  uint64_t v = ((uint64_t)hi << 32) | lo;
-  return ((double)(v >> 11) + 0.5) * 0x1.0p-53;
-}
-
 __global__ void omega_kernel(uint2 key, uint32_t sid, int64_t row0, int64_t nrows, int col0, int ncols,
                              double* __restrict__ out, int64_t ld) {
   const int q0 = col0 >> 1;
@@ -41,14 +36,13 @@ __global__ void omega_kernel(uint2 key, uint32_t sid, int64_t row0, int64_t nrow
     int64_t r = t / nq;
     int q = q0 + (int)(t - r * nq);
     uint4 w = philox4x32_10(make_uint4((uint32_t)(row0 + r), (uint32_t)q, sid, 0u), key);
-    double u1 = u53(w.x, w.y), u2 = u53(w.z, w.w);
-    double rad = sqrt(-2.0 * log(u1));
-    double s, c;
-    sincospi(2.0 * u2, &s, &c);
+    // centred binomial (R8): (popcount of 64 random bits - 32) / 4, exact in FP64 and int8
+    const double g0 = (double)(__popc(w.x) + __popc(w.y) - 32) * 0.25;
+    const double g1 = (double)(__popc(w.z) + __popc(w.w) - 32) * 0.25;
     int j0 = 2 * q - col0;  // column within the output block
     double* o = out + r * ld;
-    if (j0 >= 0 && j0 < ncols) o[j0] = rad * c;
-    if (j0 + 1 >= 0 && j0 + 1 < ncols) o[j0 + 1] = rad * s;
+    if (j0 >= 0 && j0 < ncols) o[j0] = g0;
+    if (j0 + 1 >= 0 && j0 + 1 < ncols) o[j0 + 1] = g1;
   }
 }
 
@@ -196,6 +190,12 @@ __global__ void sketch_combine_kernel(const double* __restrict__ P, int S, int64
   }
 }
 
+void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, double* Y, int64_t ldy, cudaStream_t st) {
+  int g = (int)std::min<int64_t>((rows * ncols + 255) / 256, (int64_t)148 * 16);
+  sketch_combine_kernel<<<g, 256, 0, st>>>(P, S, rows, ncols, Y, ldy);
+  H2_CHECK_LAUNCH();
+}
+
 namespace {
 int env_int(const char* name, int def) {
   const char* v = getenv(name);
@@ -238,8 +238,14 @@ void sketch_dispatch(int var, dim3 grid, cudaStream_t st, const double* X, const
 
 void launch_dense_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                          int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
-                         int64_t ldy, cudaStream_t st) {
+                         int64_t ldy, bool omega_quarters, cudaStream_t st) {
   if (row1 <= row0 || ncols <= 0) return;
+  // exp kernel with Omega in quarters (the h2 stream): exact int8 tensor-core contraction
+  // (sketch_tc.cu); any other Omega, or H2_SK_TC=0, takes the DMMA path
+  if (omega_quarters && sketch_tc_supported(kp) && env_int("H2_SK_TC", 1) != 0) {
+    launch_dense_sketch_tc(kp, X, Yc, Zc, n, row0, row1, Om, ldo, ncols, Yout, ldy, st);
+    return;
+  }
   int var = env_int("H2_SK_VAR", SK_DEFAULT_VAR);
   if (var < 0 || var > 6) var = SK_DEFAULT_VAR;
   const int occ = SK_VARS[var].occ;               // resident CTAs / SM (registers)

@@ -1,0 +1,382 @@
+// Dense-kernel sketch Y = K Omega on the 5th-generation tensor cores (tcgen05.mma kind::i8),
+// exact in integer arithmetic (Algorithm 1 line 1; BASELINE configs[0..2]).
+//
+// FP64 has no tcgen05 kind, and on B200 DMMA shares the FP64 pipe with DFMA, so a DMMA sketch
+// spends ~64 % of its FP64 issue on the contraction.  Here the contraction leaves the FP64 pipe:
+//   * Omega entries are exact quarters q/4, q in [-32, 32] (the centred binomial, R8):
+//     one signed int8 operand.
+//   * every kernel entry K in (0, 1] (exp kernel) is generated in FP64 registers and converted
+//     to the 52-bit fixed-point integer m = round(K 2^52) (the mantissa of 1 + K: one DADD,
+//     rounding error <= 2^-53, as for an FP64 value <= 1); its 7 low bytes are 7 unsigned int8
+//     slices A_s (K-major UMMA core-matrix layout in shared memory).
+//   * tcgen05.mma.kind::i8 accumulates D_s = A_s B exactly in int32 TMEM (7 x 32 columns);
+//     every 65536 j the accumulators are drained: Y += sum_s 2^(8s-54) D_s in FP64.
+// The result is the exact product of the 2^-52-rounded K with Omega, rounded only at the
+// drains: as accurate as an FP64 GEMM, and the FP64 pipe only evaluates K.
+#include "alloc.hpp"
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace h2 {
+namespace {
+
+constexpr int TC_M = 128;                      // rows per CTA (UMMA M)
+constexpr int TC_JC = 64;                      // j per chunk (K bytes per slice)
+constexpr int TC_NS = 7;                       // byte slices of the 52-bit fixed-point K
+constexpr int TC_SLICE = TC_M * TC_JC;         // 8 KB
+constexpr int TC_ABUF = TC_NS * TC_SLICE;      // 56 KB per A buffer
+constexpr int TC_BBUF = 32 * TC_JC;            // 2 KB (32 columns x 64 j, int8)
+constexpr int TC_CBUF = TC_JC * 32 + 128;      // 64 j x (x, y, z, pad) doubles, +16 B per 8 j (bank skew)
+constexpr int TC_NB = 4;                       // coordinate / B ring depth
+constexpr int TC_DRAIN = 1024;                 // chunks per TMEM drain: 65536 * 255 * 32 < 2^31
+
+// UMMA shared-memory descriptor, K-major, no swizzle (canonical ((8,m),(16B,2)):((16B,SBO),(1,LBO)))
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);   // version 1 (sm_100)
+}
+
+// instruction descriptor: D s32, A u8, B s8, both K-major, N = 32, M = 128
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(addr),
+      "r"(parity));
+}
+
+// round(exp(-|x'-y'|) * 2^52) for r2 = |x'-y'|^2 (scaled coordinates) as (lo 32, hi 20 bits).
+// r2 is clamped to [2^-1007, 490000] on its high word (integer pipe): 1/sqrt stays finite at
+// r2 = 0 (K = 1) and e^{-r} >= e^{-700} keeps the exponent arithmetic of exp_neg256 normal.
+// K is clamped below 1 - 2^-52 so that 1 + K < 2 keeps exponent 0: then the mantissa bits of
+// (1 + K) are round(K 2^52).  FP64 pipe: 6 (r2, caller) + 5 (rsqrt) + 1 + 8 (exp) + 1 = 21.
+// `tabl` = lane-replicated table (16 copies interleaved: entry j of copy l at [16 j + l]); lane l of
+// each half-warp reads copy l & 15, so the 32 random lookups of a warp are bank-conflict free.
+__device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restrict__ tabl) {
+  int hw = __double2hiint(r2);
+  hw = min(max(hw, 0x01000000), 0x411DE840);
+  r2 = __hiloint2double(hw, __double2loint(r2));
+  const double r = r2 * rsqrt_fast(r2);
+  const double SH = 6755399441055744.0;
+  const double t = fma(r, -369.32993046757464, SH);      // -256/ln2
+  const double kf = t - SH;
+  const int n = __double2loint(t);
+  const double g = fma(kf, -0.0027076061740622863, -r);
+  double p = fma(g, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(p, g, 0.5);
+  p = fma(p, g, 1.0);
+  p = fma(p, g, 1.0);
+  const double v0 = tabl[(n & 255) << 4] * p;
+  int vh = __double2hiint(v0) + ((n >> 8) << 20);
+  int vl = __double2loint(v0);
+  if (vh >= 0x3FF00000) {   // K rounded to 1.0 (r ~ 0): use 1 - 2^-52
+    vh = 0x3FEFFFFF;
+    vl = (int)0xFFFFFFFE;
+  }
+  const double w = 1.0 + __hiloint2double(vh, vl);
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)__double2hiint(w) & 0xFFFFFu);
+}
+
+// 4x4 byte transpose: out[s] = bytes s of (a, b, c, d)
+__device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* o) {
+  uint32_t p = __byte_perm(a, b, 0x5140), q = __byte_perm(c, d, 0x5140);
+  uint32_t r = __byte_perm(a, b, 0x7362), t = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(p, q, 0x5410);
+  o[1] = __byte_perm(p, q, 0x7632);
+  o[2] = __byte_perm(r, t, 0x5410);
+  o[3] = __byte_perm(r, t, 0x7632);
+}
+
+__global__ void coords_aos_kernel(const double* X, const double* Y, const double* Z, int64_t n, int64_t npad, double cs,
+                                  double4* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npad; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < n ? make_double4(X[i] * cs, Y[i] * cs, Z[i] * cs, 0.0) : make_double4(0.0, 0.0, 0.0, 0.0);
+}
+
+// Omega (n x ncols doubles q/4) -> int8 q per 64-j chunk in the B core-matrix layout:
+// chunk t, column c, jj: t*2048 + (jj/16)*512 + (c/8)*128 + (c%8)*16 + jj%16  (0 beyond n / ncols)
+__global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int64_t n, int ncols, int64_t nchunks,
+                                int8_t* __restrict__ out) {
+  const int64_t total = nchunks * TC_JC * 32;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e >> 5;
+    const int c = (int)(e & 31);
+    const int64_t t = j / TC_JC;
+    const int jj = (int)(j - t * TC_JC);
+    int q = 0;
+    if (j < n && c < ncols) q = __double2int_rn(Om[j * ldo + c] * 4.0);
+    out[t * TC_BBUF + (jj >> 4) * 512 + (c >> 3) * 128 + (c & 7) * 16 + (jj & 15)] = (int8_t)q;
+  }
+}
+
+// Warp-specialised, barrier-free pipeline per CTA (128 rows):
+//   16 producer warps: wait loaded[slot] (coordinates + B of the chunk landed) and empty[buf]
+//     (the MMA that last read A[buf] finished), evaluate 2 rows x 8 j each, write the 7 byte
+//     slices to A[buf], fence.proxy.async, arrive on full[buf];
+//   1 control warp: waits full[buf], issues the 14 tcgen05.mma of the chunk, commits empty[buf]
+//     (and drain on drain chunks), then refills the coordinate / B ring with cp.async tracked
+//     by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
+//   producer warps 0-3 (TMEM lanes 0-127) drain the int32 accumulators after every drain chunk.
+constexpr int TC_NA = 3;                 // A buffers
+constexpr int TC_PRODUCERS = 8;          // 4 rows x 8 j = 32 entries per lane and chunk
+constexpr int TC_CTA_THREADS = 32 * (TC_PRODUCERS + 1);
+constexpr int SMEM2_A = 0;
+constexpr int SMEM2_B = TC_NA * TC_ABUF;
+constexpr int SMEM2_C = SMEM2_B + TC_NB * TC_BBUF;
+constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
+constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
+constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
+
+__global__ void __launch_bounds__(TC_CTA_THREADS, 1)
+    sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
+                     const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
+                     int64_t split_stride) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  double* tab = reinterpret_cast<double*>(smem + SMEM2_T);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bar_full = sbase + SMEM2_BAR;            // 3
+  const uint32_t bar_empty = bar_full + 8 * TC_NA;         // 3
+  const uint32_t bar_loaded = bar_empty + 8 * TC_NA;       // 4
+  const uint32_t bar_drain = bar_loaded + 8 * TC_NB;       // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM2_BAR + 8 * (2 * TC_NA + TC_NB + 1));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rtile = row0 + (int64_t)blockIdx.x * TC_M;
+  const int64_t ch_b = nchunks * blockIdx.y / gridDim.y, ch_e = nchunks * (blockIdx.y + 1) / gridDim.y;
+  const int nch = (int)(ch_e - ch_b);
+  const bool control = (warp == TC_PRODUCERS);
+
+  for (int e = tid; e < 16 * 256; e += TC_CTA_THREADS) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
+  if (tid == 0) {
+    for (int b = 0; b < TC_NA; ++b) {
+      mbar_init(bar_full + 8 * b, TC_PRODUCERS);
+      mbar_init(bar_empty + 8 * b, 1);
+    }
+    for (int s = 0; s < TC_NB; ++s) mbar_init(bar_loaded + 8 * s, 32);
+    mbar_init(bar_drain, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+  double* Yo = Yout + blockIdx.y * split_stride;
+
+  if (control) {
+    // chunk it -> ring slot it % 4: B (2 KB) + coordinates (2 KB) = 256 x 16 B, 8 per lane
+    auto prefetch = [&](int it) {
+      if (it >= nch) return;
+      const int64_t t = ch_b + it;
+      const int slot = it & (TC_NB - 1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = lane + 32 * q;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BBUF + e * 16),
+                     "l"(Bq + t * TC_BBUF + e * 16));
+        const int jc = e >> 1;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
+                                                                          (jc >> 3) * 16),
+                     "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
+    };
+    prefetch(0);
+    prefetch(1);
+    for (int it = 0; it < nch; ++it) {
+      const int buf = it % TC_NA;
+      const int slot = it & (TC_NB - 1);
+      mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const bool first = (it % TC_DRAIN) == 0;
+      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+      if (lane == 0) {
+        const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
+        const uint32_t b0 = sbase + SMEM2_B + slot * TC_BBUF;
+#pragma unroll
+        for (int s = 0; s < TC_NS; ++s)
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
+            const uint64_t bd = umma_desc(b0 + kk * 2 * 512, 512, 128);
+            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * 32),
+                "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+          }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            bar_empty + 8 * buf));
+        if (drain)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              bar_drain));
+      }
+      __syncwarp();
+      // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
+      // full(it-2) and its B by MMA(it-2) -> wait for that MMA
+      if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
+      prefetch(it + 2);
+    }
+  } else {
+    // producer: rows r0 + 32 k (k < 4), 8 consecutive j (half h of the 16-j group g = warp / 2)
+    const int r0 = 16 * (warp & 1) + (lane >> 1);
+    const int h = lane & 1;
+    const int g = warp >> 1;
+    double4 ci[4];
+    int off[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = r0 + 32 * k;
+      ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
+      off[k] = g * 2048 + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
+    }
+    const double* tabl = tab + (lane & 15);
+    int drains = 0;
+    for (int it = 0; it < nch; ++it) {
+      const int buf = it % TC_NA;
+      const int slot = it & (TC_NB - 1);
+      mbar_wait(bar_loaded + 8 * slot, (it / TC_NB) & 1);
+      if (it >= TC_NA) mbar_wait(bar_empty + 8 * buf, ((it - TC_NA) / TC_NA) & 1);
+      const uint8_t* cb = smem + SMEM2_C + slot * TC_CBUF;
+      uint8_t* Ab = smem + SMEM2_A + buf * TC_ABUF;
+      const int jj0 = 16 * g + 8 * h;
+      uint32_t lo[4][8], hi[4][8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int jj = jj0 + q;
+        const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint2 m = expk_fixed52(dist2(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z), tabl);
+          lo[k][q] = m.x;
+          hi[k][q] = m.y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t w[4][4];
+        transpose4(lo[k][0], lo[k][1], lo[k][2], lo[k][3], w[0]);
+        transpose4(lo[k][4], lo[k][5], lo[k][6], lo[k][7], w[1]);
+        transpose4(hi[k][0], hi[k][1], hi[k][2], hi[k][3], w[2]);
+        transpose4(hi[k][4], hi[k][5], hi[k][6], hi[k][7], w[3]);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          *reinterpret_cast<uint2*>(Ab + s * TC_SLICE + off[k]) = make_uint2(w[0][s], w[1][s]);
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+          *reinterpret_cast<uint2*>(Ab + (s + 4) * TC_SLICE + off[k]) = make_uint2(w[2][s], w[3][s]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
+
+      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+      if (drain && warp < 4) {
+        mbar_wait(bar_drain, drains & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        const int64_t i = rtile + warp * 32 + lane;
+        double v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = 0.0;
+#pragma unroll
+        for (int s = 0; s < TC_NS; ++s) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + s * 32;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          const double wgt = ldexp(1.0, 8 * s - 54);   // slice weight 2^(8s) * 2^-52 * (1/4)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+        }
+        if (i < row1) {
+          double* y = Yo + (i - row0) * ldy;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c < ncols) y[c] = drains == 0 ? v[c] : y[c] + v[c];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      }
+      if (drain) ++drains;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+}
+
+}  // namespace
+
+bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP; }
+
+void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                            int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
+                            int64_t ldy, cudaStream_t st) {
+  if (row1 <= row0 || ncols <= 0) return;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attr_set = false;
+  if (!attr_set) {
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    attr_set = true;
+  }
+  const int64_t nchunks = (n + TC_JC - 1) / TC_JC;
+  const int64_t npad = nchunks * TC_JC;
+  const int64_t rows = row1 - row0;
+  const int tiles = div_up(rows, TC_M);
+  // j-split S fills the last wave (1 CTA / SM)
+  int S = 1;
+  {
+    double best = 0;
+    for (int s = 1; s <= 4; ++s) {
+      if (s > 1 && nchunks / s < 64) break;
+      const int64_t units = (int64_t)tiles * s;
+      const double eff = (double)units / ((double)sms * ((units + sms - 1) / sms)) - 0.01 * (s - 1);
+      if (eff > best + 1e-9) {
+        best = eff;
+        S = s;
+      }
+    }
+  }
+  double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)nchunks * TC_BBUF, st));
+  double* part = S > 1 ? static_cast<double*>(cache_alloc(sizeof(double) * rows * 32 * S, st)) : nullptr;
+  coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(X, Yc, Zc, n, npad,
+                                                                                                  kp.inv, C);
+  H2_CHECK_LAUNCH();
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    const int nc = std::min(32, ncols - c0);
+    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * TC_JC * 32 + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+        Om + c0, ldo, n, nc, nchunks, Bq);
+    H2_CHECK_LAUNCH();
+    double* yo = S > 1 ? part : Yout + c0;
+    const int64_t ld = S > 1 ? nc : ldy;
+    sketch_tc_kernel<<<dim3(tiles, S), TC_CTA_THREADS, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+                                                                     S > 1 ? rows * nc : 0);
+    H2_CHECK_LAUNCH();
+    if (S > 1) {
+      launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
+    }
+  }
+  cache_free(C, st);
+  cache_free(Bq, st);
+  if (part) cache_free(part, st);
+}
+
+}  // namespace h2

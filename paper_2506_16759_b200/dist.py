@@ -54,5 +54,5 @@ def dense_shard_fn(tree, kernel):
     from . import h2 as _h2
 
     def fn(om, out, r0, r1):
-        _h2.dense_sketch(tree, om, kernel, r0, r1, out=out)
+        _h2.dense_sketch(tree, om, kernel, r0, r1, out=out, omega_quarters=True)   # h2 stream Omega
     return fn

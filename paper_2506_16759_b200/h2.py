@@ -287,15 +287,19 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     return H2Matrix(h, tree, _stats_dict(st), keep)
 
 
-def dense_sketch(tree: Tree, omega, kernel=("exp", 0.2), row_begin=0, row_end=None, out=None, stream=None):
-    """Y(rows, :) = K(rows, :) Omega with the built-in kernel (DMMA tile kernel)."""
+def dense_sketch(tree: Tree, omega, kernel=("exp", 0.2), row_begin=0, row_end=None, out=None, stream=None,
+                 omega_quarters=False):
+    """Y(rows, :) = K(rows, :) Omega with the built-in kernel.  omega_quarters=True asserts that
+    Omega is the h2 stream (entries q/4, |q| <= 32): the exp kernel then runs on the int8 tensor
+    cores (exact); otherwise the FP64 DMMA kernel."""
     row_end = tree.n if row_end is None else row_end
     assert omega.is_cuda and omega.dtype == torch.float64 and omega.shape[0] == tree.n
     nc = omega.shape[1]
     if out is None:
         out = torch.empty((row_end - row_begin, nc), dtype=torch.float64, device=omega.device)
     check(lib.h2_dense_sketch(tree.handle, _kernel(*kernel), row_begin, row_end, _ptr(omega), omega.stride(0), nc,
-                              _ptr(out), out.stride(0), _stream(stream)))
+                              _ptr(out), out.stride(0), L.H2_SKETCH_OMEGA_QUARTERS if omega_quarters else 0,
+                              _stream(stream)))
     return out
 
 

@@ -17,7 +17,7 @@ def oracle_build(X, kind, param, leaf, tol, eta=0.7, seed=1, **opts):
     tree = geometry.build_cluster_tree(X, leaf)
     part = geometry.build_partition(tree, eta)
     op = kernels.KernelOperator(kind, param, X[tree.perm])
-    om = lambda c0, nc: rng.gaussian_block(seed, 0, 0, tree.n, c0, nc)
+    om = lambda c0, nc: rng.omega_block(seed, 0, 0, tree.n, c0, nc)
     H = oh2.build(tree, part, op.sampler, op.entry, om, tol, oh2.BuildOpts(**opts))
     return H, op
 

@@ -23,24 +23,30 @@ CASES = {
 
 def test_omega_matches_oracle_generator():
     Om = g.omega(3000, 37, seed=11, stream_id=3, col0=5).cpu().numpy()
-    ref = rng.gaussian_block(11, 3, 0, 3000, 5, 37)
-    assert np.abs(Om - ref).max() <= 1e-14 * np.abs(ref).max()
+    ref = rng.omega_block(11, 3, 0, 3000, 5, 37)
+    assert np.array_equal(Om, ref)          # exactly representable stream: bit-identical
 
 
 @pytest.mark.parametrize("case", list(CASES))
-def test_dense_sketch_matches_oracle(case):
+@pytest.mark.parametrize("quarters", [False, True])
+def test_dense_sketch_matches_oracle(case, quarters):
+    """DMMA path (arbitrary Omega) and, for the exp kernel with the h2 Omega stream, the exact
+    int8 tensor-core path (sketch_tc.cu)."""
     mk, kind, p, leaf, tol = CASES[case]
     X = mk()
     T = g.Tree(X, leaf)
-    Om = rng.gaussian_block(1, 0, 0, T.n, 0, 45)
+    Om = rng.omega_block(1, 0, 0, T.n, 0, 45)
+    if not quarters:
+        Om = Om + 1e-3 * np.random.default_rng(7).standard_normal(Om.shape)   # generic values
     op = kernels.KernelOperator(kind, p, X[T.perm])
     ref = op.sampler(Om)
-    y = g.dense_sketch(T, torch.from_numpy(Om).cuda(), (kind, p)).cpu().numpy()
+    Od = torch.from_numpy(Om).cuda()
+    y = g.dense_sketch(T, Od, (kind, p), omega_quarters=quarters).cpu().numpy()
     scale = np.abs(ref).max()
     assert np.abs(y - ref).max() <= 1e-13 * scale
     # row-range variant (multi-GPU row shard)
     r0, r1 = 333, min(T.n, 1777)
-    y2 = g.dense_sketch(T, torch.from_numpy(Om).cuda(), (kind, p), r0, r1).cpu().numpy()
+    y2 = g.dense_sketch(T, Od, (kind, p), r0, r1, omega_quarters=quarters).cpu().numpy()
     assert np.abs(y2 - ref[r0:r1]).max() <= 1e-13 * scale
 
 

@@ -10,7 +10,7 @@ from synthetic_h2 import synthetic_h2
 def setup(X, leaf, eta=0.7):
     tree = geometry.build_cluster_tree(X, leaf)
     part = geometry.build_partition(tree, eta)
-    om = lambda c0, nc: rng.gaussian_block(1, 0, 0, tree.n, c0, nc)
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, tree.n, c0, nc)
     return tree, part, om
 
 
@@ -121,7 +121,7 @@ def test_all_dense_and_single_leaf():
     X = uniform_points(300, 3, 8)
     tree = geometry.build_cluster_tree(X, 64)
     part = geometry.build_partition(tree, 1e-12)        # eta -> 0: every leaf pair dense
-    om = lambda c0, nc: rng.gaussian_block(1, 0, 0, tree.n, c0, nc)
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, tree.n, c0, nc)
     op = kernels.KernelOperator("exp", 0.2, X[tree.perm])
     H = h2.build(tree, part, op.sampler, op.entry, om, 1e-6)
     assert np.all(H.rank[tree.leaf_depth] == 0)          # Y^loc == 0 up to roundoff
@@ -129,7 +129,7 @@ def test_all_dense_and_single_leaf():
     t1 = geometry.build_cluster_tree(X[:40], 64)
     p1 = geometry.build_partition(t1, 0.7)
     op1 = kernels.KernelOperator("exp", 0.2, X[:40][t1.perm])
-    H1 = h2.build(t1, p1, op1.sampler, op1.entry, lambda c0, nc: rng.gaussian_block(1, 0, 0, 40, c0, nc), 1e-6)
+    H1 = h2.build(t1, p1, op1.sampler, op1.entry, lambda c0, nc: rng.omega_block(1, 0, 0, 40, c0, nc), 1e-6)
     assert np.array_equal(h2.to_dense(H1), op1.dense())
 
 
@@ -160,7 +160,7 @@ def test_weak_admissibility_is_hss():
     X = uniform_points(512, 1, 0)
     tree = geometry.build_cluster_tree(X, 32)
     part = geometry.build_partition(tree, 1e12)
-    om = lambda c0, nc: rng.gaussian_block(1, 0, 0, tree.n, c0, nc)
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, tree.n, c0, nc)
     op = kernels.KernelOperator("exp", 0.2, X[tree.perm])
     H = h2.build(tree, part, op.sampler, op.entry, om, 1e-6)
     assert H.top == 1
