@@ -28,6 +28,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "H2 build time (s) + samples used vs N at tol=1e-6"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 64 FP64 FMA/clk/SM (DFMA = DMMA pipe), 1965 MHz
+FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12          # FP64 pipe instructions (lane-ops) per second
+F_EVAL = 21          # FP64 pipe ops per exp-kernel entry in sketch_tc_kernel (SASS count)
+INT8_DENSE_TOPS = 4500.0                            # nominal dense int8 tensor ops/s (B200, guide)
 
 
 def parse():
@@ -127,7 +130,7 @@ def run_reference(args, w, rank):
     if rank != 0:
         return
     X = w["points"]()
-    samples_hint = 128   # GPU samples at configs[1] (BENCH); the oracle scales its sample by it
+    samples_hint = 224   # GPU samples at configs[1] (profiles/r1_bench_*.json); scales the oracle sample
     cores = len(os.sched_getaffinity(0))
     for _ in range(args.warmup):
         oracle_sample_seconds(w, X, samples_hint, budget_rows=8, leaves=2)
@@ -211,13 +214,20 @@ def run_ours(args, w, rank, world, local_rank):
     KX = g.dense_sketch(T, Xp, kern)
     HX = H.matvec(Xp)
     verr = float(torch.linalg.norm(HX - KX) / torch.linalg.norm(KX))
-    # roofline of the dominant kernel (dense sketch): contraction flops 2 N^2 b per launch
+    # roofline of the dominant kernel (sketch_tc_kernel, one launch per 32-sample round): the
+    # contraction runs exactly on the int8 tensor cores, so the bound is the FP64 pipe evaluating
+    # K: algorithmic work = N_rows * N entries x F_EVAL FP64 ops per launch
     sk_launches = st["samples"] // 32
     t_sk_ms = float(np.mean([s["t_phase_ms"]["sketch"] for s in stats]))
     per_launch_ms = t_sk_ms / max(sk_launches, 1)
     rows_local = n if world == 1 else (n // world)
-    flops_launch = 2.0 * rows_local * n * 32
-    achieved = flops_launch / (per_launch_ms * 1e-3) / 1e12
+    entries_launch = float(rows_local) * n
+    achieved = entries_launch * F_EVAL / (per_launch_ms * 1e-3) / 1e12
+    int8_ops = entries_launch * 32 * 7 * 2 / (per_launch_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1_sketch_tc_traffic.json")
+    if os.path.exists(tpath) and args.workload == "cov3d_256k" and world == 1:
+        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
     # e2e through the public API from host buffers: tree build + H2D + build + D2H of skeletons
     e2e = None
     if not args.no_e2e:
@@ -274,11 +284,15 @@ def run_ours(args, w, rank, world, local_rank):
         "entries_evaluated_per_s": (st["entries_D"] + st["entries_B"]) / (ms / 1e3),
         "sketch_entries_per_s": st["entries_sketch"] / (ms / 1e3),
         "gpu_launches": int(sum(s["launches"] for s in stats)),
-        "roofline": {"bound": "alu", "kernel": "dense_sketch_kernel (DMMA m8n8k4 + FP64 exp)",
-                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                     "note": "achieved = 2 N^2 32 contraction flops per launch / CUDA-event launch time; peak = "
-                             "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured DFMA 37.0, DMMA 32.9 TF/s)"},
+        "roofline": {"bound": "alu", "kernel": "sketch_tc_kernel (FP64 K evaluation + tcgen05 kind::i8 contraction)",
+                     "achieved": achieved, "peak": FP64_PIPE_TOPS, "unit": "TOP/s (FP64 pipe ops)",
+                     "frac": achieved / FP64_PIPE_TOPS, "traffic": traffic,
+                     "entries_per_s": entries_launch / (per_launch_ms * 1e-3),
+                     "int8_tensor_tops": int8_ops, "int8_tensor_frac": int8_ops / INT8_DENSE_TOPS,
+                     "per_launch_ms": per_launch_ms,
+                     "note": f"achieved = N^2 entries x {F_EVAL} FP64 ops (SASS) per launch / CUDA-event time of the "
+                             "sketch phase per 32-sample launch; peak = 148 SM x 64 FP64 lanes/clk x 1.965 GHz "
+                             "(microbenchmarked DFMA 37.0 TF/s = 99.5 %); traffic = ncu dram bytes per launch"},
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -13,6 +13,8 @@
 //     every 65536 j the accumulators are drained: Y += sum_s 2^(8s-54) D_s in FP64.
 // The result is the exact product of the 2^-52-rounded K with Omega, rounded only at the
 // drains: as accurate as an FP64 GEMM, and the FP64 pipe only evaluates K.
+#include <cstdlib>
+
 #include "alloc.hpp"
 #include "common.cuh"
 #include "kernels.hpp"
@@ -123,8 +125,7 @@ __global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int6
 //     by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
 //   producer warps 0-3 (TMEM lanes 0-127) drain the int32 accumulators after every drain chunk.
 constexpr int TC_NA = 3;                 // A buffers
-constexpr int TC_PRODUCERS = 8;          // 4 rows x 8 j = 32 entries per lane and chunk
-constexpr int TC_CTA_THREADS = 32 * (TC_PRODUCERS + 1);
+// NPW producer warps (8: 4 rows x 8 j = 32 entries per lane and chunk; 16: 2 rows x 8 j)
 constexpr int SMEM2_A = 0;
 constexpr int SMEM2_B = TC_NA * TC_ABUF;
 constexpr int SMEM2_C = SMEM2_B + TC_NB * TC_BBUF;
@@ -132,7 +133,8 @@ constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
 constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
 constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
 
-__global__ void __launch_bounds__(TC_CTA_THREADS, 1)
+template <int NPW>
+__global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride) {
@@ -148,6 +150,9 @@ __global__ void __launch_bounds__(TC_CTA_THREADS, 1)
   const int64_t rtile = row0 + (int64_t)blockIdx.x * TC_M;
   const int64_t ch_b = nchunks * blockIdx.y / gridDim.y, ch_e = nchunks * (blockIdx.y + 1) / gridDim.y;
   const int nch = (int)(ch_e - ch_b);
+  constexpr int TC_PRODUCERS = NPW;
+  constexpr int TC_CTA_THREADS = 32 * (NPW + 1);
+  constexpr int RPT = 32 / NPW;            // rows per producer thread (128 rows x 64 j / (32 NPW lanes x 8 j))
   const bool control = (warp == TC_PRODUCERS);
 
   for (int e = tid; e < 16 * 256; e += TC_CTA_THREADS) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
@@ -226,15 +231,16 @@ __global__ void __launch_bounds__(TC_CTA_THREADS, 1)
       prefetch(it + 2);
     }
   } else {
-    // producer: rows r0 + 32 k (k < 4), 8 consecutive j (half h of the 16-j group g = warp / 2)
-    const int r0 = 16 * (warp & 1) + (lane >> 1);
+    // producer: rows rs*16 + pair + k*16*NPW/4 (k < RPT), 8 consecutive j (half h of 16-j group g)
+    const int g = warp & 3;
+    const int rs = warp >> 2;
     const int h = lane & 1;
-    const int g = warp >> 1;
-    double4 ci[4];
-    int off[4];
+    const int r0 = 16 * rs + (lane >> 1);
+    double4 ci[RPT];
+    int off[RPT];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = r0 + 32 * k;
+    for (int k = 0; k < RPT; ++k) {
+      const int r = r0 + k * 4 * NPW;
       ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
       off[k] = g * 2048 + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
@@ -248,20 +254,20 @@ __global__ void __launch_bounds__(TC_CTA_THREADS, 1)
       const uint8_t* cb = smem + SMEM2_C + slot * TC_CBUF;
       uint8_t* Ab = smem + SMEM2_A + buf * TC_ABUF;
       const int jj0 = 16 * g + 8 * h;
-      uint32_t lo[4][8], hi[4][8];
+      uint32_t lo[RPT][8], hi[RPT][8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int jj = jj0 + q;
         const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < RPT; ++k) {
           const uint2 m = expk_fixed52(dist2(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z), tabl);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < RPT; ++k) {
         uint32_t w[4][4];
         transpose4(lo[k][0], lo[k][1], lo[k][2], lo[k][3], w[0]);
         transpose4(lo[k][4], lo[k][5], lo[k][6], lo[k][7], w[1]);
@@ -333,9 +339,12 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static bool attr_set = false;
   if (!attr_set) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
     attr_set = true;
   }
+  const char* npw_env = getenv("H2_TC_NPW");
+  const int npw = (npw_env && atoi(npw_env) == 8) ? 8 : 16;   // 16 producer warps (measured 163 vs 170 ms)
   const int64_t nchunks = (n + TC_JC - 1) / TC_JC;
   const int64_t npad = nchunks * TC_JC;
   const int64_t rows = row1 - row0;
@@ -367,7 +376,11 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     H2_CHECK_LAUNCH();
     double* yo = S > 1 ? part : Yout + c0;
     const int64_t ld = S > 1 ? nc : ldy;
-    sketch_tc_kernel<<<dim3(tiles, S), TC_CTA_THREADS, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+    if (npw == 16)
+      sketch_tc_kernel<16><<<dim3(tiles, S), 32 * 17, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+                                                                      S > 1 ? rows * nc : 0);
+    else
+      sketch_tc_kernel<8><<<dim3(tiles, S), 32 * 9, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
                                                                      S > 1 ? rows * nc : 0);
     H2_CHECK_LAUNCH();
     if (S > 1) {

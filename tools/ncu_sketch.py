@@ -6,5 +6,5 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 18
 T = g.Tree(uniform_points(n, 3, 0), 64)
 Om = g.omega(n, 32)
 for _ in range(2):
-    y = g.dense_sketch(T, Om)
+    y = g.dense_sketch(T, Om, omega_quarters=True)
 torch.cuda.synchronize()
