@@ -110,12 +110,20 @@ typedef struct {
 } h2_sketch_req;
 typedef int (*h2_sketch_fn)(void* ctx, const h2_sketch_req* req);
 
-enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1 };
+/* H^2 + low-rank operator M = A_H + U U^T (BASELINE configs[4]): `base` is an
+ * h2_matrix built on the SAME h2_tree, U is dev n x rank row-major (tree-order rows, leading dim
+ * ld_U).  As a sketch: Y = A_H Omega (h2_matvec) + U (U^T Omega).  As an entry evaluator:
+ * D / B blocks of M extracted from A_H's D / B and expanded bases plus U U^T. */
+enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1, H2_S_H2_LOWRANK = 2 };
 typedef struct {
   int32_t kind;       /* H2_S_DENSE_KERNEL: Y = K Omega with the built-in kernel below (O(N^2)) */
-  h2_kernel kern;     /*                    H2_S_CALLBACK: fn(ctx, req)                          */
+  h2_kernel kern;     /* H2_S_CALLBACK: fn(ctx, req);  H2_S_H2_LOWRANK: base + U                 */
   h2_sketch_fn fn;
   void* ctx;
+  const h2_matrix* base;
+  const double* U;
+  int64_t ld_U;
+  int32_t rank;
 } h2_sketch;
 
 /* Batched entry evaluator ("batched entry generator ... evaluate all D or B at a
@@ -136,12 +144,16 @@ typedef struct {
 } h2_block_batch;
 typedef int (*h2_entry_fn)(void* ctx, const h2_block_batch* batch);
 
-enum { H2_E_BUILTIN = 0, H2_E_CALLBACK = 1 };
+enum { H2_E_BUILTIN = 0, H2_E_CALLBACK = 1, H2_E_H2_LOWRANK = 2 };
 typedef struct {
   int32_t kind;       /* H2_E_BUILTIN: entries of `kern` at the tree's coordinates              */
-  h2_kernel kern;
+  h2_kernel kern;     /* H2_E_H2_LOWRANK: entries of base + U U^T (see h2_sketch)               */
   h2_entry_fn fn;
   void* ctx;
+  const h2_matrix* base;
+  const double* U;
+  int64_t ld_U;
+  int32_t rank;
 } h2_entry;
 
 /* ---------------------------------------------------------------------------------------

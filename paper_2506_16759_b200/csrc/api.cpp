@@ -172,6 +172,9 @@ struct Panel {
   }
 };
 
+void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
+                 double beta, cudaStream_t st);
+
 struct Builder {
   const h2_tree& T;
   const h2_sketch& S;
@@ -222,6 +225,12 @@ struct Builder {
     if (S.kind == H2_S_DENSE_KERNEL) {
       launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
       entries_sketch += T.n * T.n;
+    } else if (S.kind == H2_S_H2_LOWRANK) {
+      // K_blk = A_H Omega + U (U^T Omega)
+      matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
+      DArr<double> scr;
+      scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
+      launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
     } else {
       h2_sketch_req rq{};
       rq.n = T.n;
@@ -454,7 +463,93 @@ struct Builder {
     g.idx = L.d_skel.p;
     g.out_off = L.d_B_off.p;
     g.out = L.B.p;
-    gen(g);
+    if (E.kind == H2_E_H2_LOWRANK) update_B(t);
+    else gen(g);
+  }
+
+  // B blocks of M = A_H + U U^T at depth t (PAPER.md L445 entry extraction; h2update.cu)
+  DArr<const int32_t*> base_k;
+  DArr<const int64_t*> base_xoff;
+  DArr<const double*> base_X;
+  void update_B(int t) {
+    Level& L = H.L(t);
+    const h2_matrix& A = *E.base;
+    const Level& La = A.L(t);
+    const PairCSR& F = T.far[t];
+    if (F.nuniq() == 0) return;
+    timer.begin(H2_PH_GEN);
+    if (!base_k.p) {   // per-depth device pointers of A's levels
+      std::vector<const int32_t*> kk(T.Dl + 1, nullptr);
+      std::vector<const int64_t*> xo(T.Dl + 1, nullptr);
+      std::vector<const double*> xx(T.Dl + 1, nullptr);
+      for (int u = A.top; u <= A.Dl; ++u) {
+        kk[u] = A.L(u).d_k.p;
+        xo[u] = A.L(u).d_xoff.p;
+        xx[u] = A.L(u).X.p;
+      }
+      base_k.upload(kk, st);
+      base_xoff.upload(xo, st);
+      base_X.upload(xx, st);
+    }
+    // R_s = A's expanded basis rows at the new skeletons of depth t (kn_s x kb_s)
+    std::vector<int64_t> rowoff(L.nclus + 1, 0);
+    std::vector<int32_t> ptc(std::max<int64_t>(L.rtot, 1), 0);
+    int kmax = 1;
+    for (int c = 0; c < L.nclus; ++c) {
+      rowoff[c + 1] = rowoff[c] + (int64_t)L.k[c] * La.k[c];
+      for (int i = 0; i < L.k[c]; ++i) ptc[L.roff[c] + i] = c;
+    }
+    for (int u = t; u <= T.Dl; ++u)
+      for (int32_t kv : A.L(u).k) kmax = std::max(kmax, kv);
+    DArr<int64_t> d_rowoff;
+    DArr<int32_t> d_ptc;
+    DArr<double> R;
+    d_rowoff.upload(rowoff, st);
+    d_ptc.upload(ptc, st);
+    R.alloc(std::max<int64_t>(rowoff.back(), 1), st);
+    ExpandArgs ea{};
+    ea.npoints = L.rtot;
+    ea.pt_cluster = d_ptc.p;
+    ea.roff_new = L.d_roff.p;
+    ea.skel_new = L.d_skel.p;
+    ea.nleaf = 1 << T.Dl;
+    ea.leaf_begin = T.d_leaf_begin;
+    ea.Dl = T.Dl;
+    ea.t = t;
+    ea.kb = base_k.p;
+    ea.xoff = base_xoff.p;
+    ea.X = base_X.p;
+    ea.kmax = kmax;
+    ea.R = R.p;
+    ea.rowoff = d_rowoff.p;
+    launch_expand_rows(ea, st);
+    int64_t gmax = 1;
+    for (int64_t u = 0; u < F.nuniq(); ++u)
+      gmax = std::max<int64_t>(gmax, (int64_t)La.k[F.us[u]] * L.k[F.ub[u]]);
+    const int grid = (int)std::min<int64_t>(F.nuniq(), 148 * 4);
+    DArr<double> scratch;
+    scratch.alloc(gmax * grid, st);
+    UpdateBArgs ba{};
+    ba.nblocks = F.nuniq();
+    ba.us = T.d_far[t].us;
+    ba.ub = T.d_far[t].ub;
+    ba.kn = L.d_k.p;
+    ba.kb = La.d_k.p;
+    ba.out = L.B.p;
+    ba.out_off = L.d_B_off.p;
+    ba.R = R.p;
+    ba.rowoff = d_rowoff.p;
+    ba.Bbase = La.B.p;
+    ba.Boff = La.d_B_off.p;
+    ba.U = E.U;
+    ba.ldu = E.ld_U;
+    ba.r = E.rank;
+    ba.skel = L.d_skel.p;
+    ba.roff_new = L.d_roff.p;
+    ba.scratch = scratch.p;
+    ba.gmax = gmax;
+    launch_update_B(ba, grid, st);
+    timer.end();
   }
 
   // updateSamples (L216-217, L246-247, L386): one new block of b stream columns, swept up through
@@ -517,7 +612,25 @@ struct Builder {
       g.idx = T.d_iota;
       g.out_off = T.d_D_off;
       g.out = H.D.p;
-      gen(g);
+      if (E.kind == H2_E_H2_LOWRANK) {
+        timer.begin(H2_PH_GEN);
+        UpdateDArgs a{};
+        a.nblocks = g.nblocks;
+        a.us = g.us;
+        a.ub = g.ub;
+        a.cnt = T.d_leaf_size;
+        a.begin = T.d_leaf_begin;
+        a.off = T.d_D_off;
+        a.Dbase = E.base->D.p;
+        a.out = H.D.p;
+        a.U = E.U;
+        a.ldu = E.ld_U;
+        a.r = E.rank;
+        launch_update_D(a, st);
+        timer.end();
+      } else {
+        gen(g);
+      }
     }
     setup_level(Dl);
     bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
@@ -599,6 +712,105 @@ struct Builder {
     }
   }
 };
+
+// y = alpha K_H x + beta y (CS4: upward pass, couplings, downward pass, dense leaves); stream-ordered,
+// workspaces released stream-ordered on return
+void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
+                 double beta, cudaStream_t st) {
+  const h2_matrix* H = &Hm;
+    const h2_tree& T = *H->tree;
+  const int Dl = H->Dl, top = H->top;
+  std::vector<DArr<double>> xh(Dl + 1), yh(Dl + 1);
+  for (int t = top; t <= Dl; ++t) {
+    const Level& L = H->L(t);
+    xh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
+    yh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
+    H2_CUDA(cudaMemsetAsync(yh[t].p, 0, sizeof(double) * std::max<int64_t>(L.rtot, 1) * q, st));
+  }
+  if (beta != 1.0) launch_scale(y, T.n, ldy, q, beta, st);
+  // upward pass
+  for (int t = Dl; t >= top; --t) {
+    const Level& L = H->L(t);
+    UpArgs a{};
+    a.nclusters = L.nclus;
+    a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
+    a.m = L.d_m.p;
+    a.k = L.d_k.p;
+    a.xoff = L.d_xoff.p;
+    a.X = L.X.p;
+    a.roff = L.d_roff.p;
+    a.xin = (t == Dl) ? x : xh[t + 1].p;
+    a.ldi = (t == Dl) ? ldx : q;
+    a.xh = xh[t].p;
+    a.ldh = q;
+    a.q = q;
+    launch_upward(a, st);
+  }
+  // couplings  y^_s += sum_{b in F_s} B_{s,b} x^_b
+  for (int t = top; t <= Dl; ++t) {
+    const Level& L = H->L(t);
+    if (T.far[t].nnz() == 0) continue;
+    SpmmArgs s{};
+    s.nclusters = L.nclus;
+    s.max_rows = L.max_k;
+    s.yoff = s.xoff = L.d_roff.p;
+    s.cnt = L.d_k.p;
+    s.ptr = T.d_far[t].ptr;
+    s.idx = T.d_far[t].idx;
+    s.uidx = T.d_far[t].uidx;
+    s.us = T.d_far[t].us;
+    s.blk_off = L.d_B_off.p;
+    s.blk = L.B.p;
+    s.x = xh[t].p;
+    s.ldx = q;
+    s.y = yh[t].p;
+    s.ldy = q;
+    s.q = q;
+    s.alpha = 1.0;
+    launch_spmm(s, st);
+  }
+  // downward pass
+  for (int t = top; t <= Dl; ++t) {
+    const Level& L = H->L(t);
+    DownArgs a{};
+    a.nclusters = L.nclus;
+    a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
+    a.m = L.d_m.p;
+    a.k = L.d_k.p;
+    a.xoff = L.d_xoff.p;
+    a.X = L.X.p;
+    a.roff = L.d_roff.p;
+    a.yh = yh[t].p;
+    a.ldh = q;
+    a.yout = (t == Dl) ? y : yh[t + 1].p;
+    a.ldo = (t == Dl) ? ldy : q;
+    a.q = q;
+    a.alpha = (t == Dl) ? alpha : 1.0;
+    a.accumulate = 1;
+    launch_downward(a, st);
+  }
+  // dense leaves  y += alpha sum_{b in N} D x
+  {
+    SpmmArgs s{};
+    s.nclusters = 1 << Dl;
+    s.max_rows = H->L(Dl).max_m;
+    s.yoff = s.xoff = T.d_leaf_begin;
+    s.cnt = T.d_leaf_size;
+    s.ptr = T.d_near.ptr;
+    s.idx = T.d_near.idx;
+    s.uidx = T.d_near.uidx;
+    s.us = T.d_near.us;
+    s.blk_off = T.d_D_off;
+    s.blk = H->D.p;
+    s.x = x;
+    s.ldx = ldx;
+    s.y = y;
+    s.ldy = ldy;
+    s.q = q;
+    s.alpha = alpha;
+    launch_spmm(s, st);
+  }
+}
 
 // the tree is built on the host; its device mirror is created on first use (current device)
 void ensure_uploaded(const h2_tree* tree) {
@@ -731,9 +943,22 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
     H2_REQUIRE(o.d_init >= 1 && o.d_blk >= 1 && o.d_max >= o.d_init, "h2_build: need 1 <= d_init <= d_max, d_blk >= 1");
     H2_REQUIRE(o.tol_rule == H2_TOL_RMS || o.tol_rule == H2_TOL_LITERAL, "h2_build: bad tol_rule");
     H2_REQUIRE(o.tol_rule != H2_TOL_LITERAL || o.norm > 0, "h2_build: literal tolerance needs opts.norm > 0");
-    H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn),
+    H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
+                   sketch->kind == H2_S_H2_LOWRANK,
                "h2_build: bad sketch");
-    H2_REQUIRE(entry->kind == H2_E_BUILTIN || (entry->kind == H2_E_CALLBACK && entry->fn), "h2_build: bad entry");
+    H2_REQUIRE(entry->kind == H2_E_BUILTIN || (entry->kind == H2_E_CALLBACK && entry->fn) ||
+                   entry->kind == H2_E_H2_LOWRANK,
+               "h2_build: bad entry");
+    for (int which = 0; which < 2; ++which) {
+      const bool upd = which == 0 ? sketch->kind == H2_S_H2_LOWRANK : entry->kind == H2_E_H2_LOWRANK;
+      if (!upd) continue;
+      const h2_matrix* base = which == 0 ? sketch->base : entry->base;
+      const double* U = which == 0 ? sketch->U : entry->U;
+      const int32_t r = which == 0 ? sketch->rank : entry->rank;
+      const int64_t ldu = which == 0 ? sketch->ld_U : entry->ld_U;
+      H2_REQUIRE(base && base->tree.get() == tree, "h2_build: the H2+low-rank operator needs a base built on this tree");
+      H2_REQUIRE(U && r >= 1 && r <= 1024 && ldu >= r, "h2_build: H2+low-rank operator needs U (n x rank, ld >= rank)");
+    }
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
       if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
@@ -768,100 +993,7 @@ h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y,
   try {
     H2_REQUIRE(H && x && y, "h2_matvec: NULL argument");
     H2_REQUIRE(q >= 1 && q <= 64 && ldx >= q && ldy >= q, "h2_matvec: need 1 <= ncols <= 64, ld >= ncols");
-    cudaStream_t st = (cudaStream_t)stream;
-    const h2_tree& T = *H->tree;
-    const int Dl = H->Dl, top = H->top;
-    std::vector<DArr<double>> xh(Dl + 1), yh(Dl + 1);
-    for (int t = top; t <= Dl; ++t) {
-      const Level& L = H->L(t);
-      xh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
-      yh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
-      H2_CUDA(cudaMemsetAsync(yh[t].p, 0, sizeof(double) * std::max<int64_t>(L.rtot, 1) * q, st));
-    }
-    if (beta != 1.0) launch_scale(y, T.n, ldy, q, beta, st);
-    // upward pass
-    for (int t = Dl; t >= top; --t) {
-      const Level& L = H->L(t);
-      UpArgs a{};
-      a.nclusters = L.nclus;
-      a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
-      a.m = L.d_m.p;
-      a.k = L.d_k.p;
-      a.xoff = L.d_xoff.p;
-      a.X = L.X.p;
-      a.roff = L.d_roff.p;
-      a.xin = (t == Dl) ? x : xh[t + 1].p;
-      a.ldi = (t == Dl) ? ldx : q;
-      a.xh = xh[t].p;
-      a.ldh = q;
-      a.q = q;
-      launch_upward(a, st);
-    }
-    // couplings  y^_s += sum_{b in F_s} B_{s,b} x^_b
-    for (int t = top; t <= Dl; ++t) {
-      const Level& L = H->L(t);
-      if (T.far[t].nnz() == 0) continue;
-      SpmmArgs s{};
-      s.nclusters = L.nclus;
-      s.max_rows = L.max_k;
-      s.yoff = s.xoff = L.d_roff.p;
-      s.cnt = L.d_k.p;
-      s.ptr = T.d_far[t].ptr;
-      s.idx = T.d_far[t].idx;
-      s.uidx = T.d_far[t].uidx;
-      s.us = T.d_far[t].us;
-      s.blk_off = L.d_B_off.p;
-      s.blk = L.B.p;
-      s.x = xh[t].p;
-      s.ldx = q;
-      s.y = yh[t].p;
-      s.ldy = q;
-      s.q = q;
-      s.alpha = 1.0;
-      launch_spmm(s, st);
-    }
-    // downward pass
-    for (int t = top; t <= Dl; ++t) {
-      const Level& L = H->L(t);
-      DownArgs a{};
-      a.nclusters = L.nclus;
-      a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
-      a.m = L.d_m.p;
-      a.k = L.d_k.p;
-      a.xoff = L.d_xoff.p;
-      a.X = L.X.p;
-      a.roff = L.d_roff.p;
-      a.yh = yh[t].p;
-      a.ldh = q;
-      a.yout = (t == Dl) ? y : yh[t + 1].p;
-      a.ldo = (t == Dl) ? ldy : q;
-      a.q = q;
-      a.alpha = (t == Dl) ? alpha : 1.0;
-      a.accumulate = 1;
-      launch_downward(a, st);
-    }
-    // dense leaves  y += alpha sum_{b in N} D x
-    {
-      SpmmArgs s{};
-      s.nclusters = 1 << Dl;
-      s.max_rows = H->L(Dl).max_m;
-      s.yoff = s.xoff = T.d_leaf_begin;
-      s.cnt = T.d_leaf_size;
-      s.ptr = T.d_near.ptr;
-      s.idx = T.d_near.idx;
-      s.uidx = T.d_near.uidx;
-      s.us = T.d_near.us;
-      s.blk_off = T.d_D_off;
-      s.blk = H->D.p;
-      s.x = x;
-      s.ldx = ldx;
-      s.y = y;
-      s.ldy = ldy;
-      s.q = q;
-      s.alpha = alpha;
-      launch_spmm(s, st);
-    }
-    // workspaces are released stream-ordered (cudaFreeAsync on st) when they go out of scope
+    matvec_impl(*H, x, ldx, y, ldy, q, alpha, beta, (cudaStream_t)stream);
     return H2_OK;
   } catch (const Error& e) {
     return fail(e);

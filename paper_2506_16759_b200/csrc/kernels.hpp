@@ -178,6 +178,56 @@ struct SpmmArgs {
   double alpha;
 };
 void launch_spmm(const SpmmArgs& a, cudaStream_t st);
+
+// ---- H^2 + low-rank update operators (h2update.cu, BASELINE configs[4])
+// Y += U (U^T Omega): scratch >= (ceil(n/1024) + 1) * r * nc doubles
+void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om, int64_t ldo, int nc, int64_t n,
+                           double* Y, int64_t ldy, double* scratch, cudaStream_t st);
+struct UpdateDArgs {            // D_new = D_A + U(I_s) U(I_b)^T over unique near pairs
+  int64_t nblocks;
+  const int32_t *us, *ub, *cnt;
+  const int64_t *begin, *off;
+  const double* Dbase;
+  double* out;
+  const double* U;
+  int64_t ldu;
+  int r;
+};
+void launch_update_D(const UpdateDArgs& a, cudaStream_t st);
+struct ExpandArgs {             // rows of A's expanded basis at the new skeletons of depth t
+  int64_t npoints;
+  const int32_t* pt_cluster;
+  const int64_t* roff_new;
+  const int32_t* skel_new;
+  int nleaf;
+  const int64_t* leaf_begin;
+  int Dl, t;
+  const int32_t* const* kb;     // per depth: base ranks
+  const int64_t* const* xoff;   // per depth: base basis offsets
+  const double* const* X;       // per depth: base bases
+  int kmax;
+  double* R;
+  const int64_t* rowoff;        // per cluster of depth t: offset of R_s (kn_s x kb_s)
+};
+void launch_expand_rows(const ExpandArgs& a, cudaStream_t st);
+struct UpdateBArgs {            // B_new = R_s B_A R_b^T + U(I~_s) U(I~_b)^T over unique far pairs
+  int64_t nblocks;
+  const int32_t *us, *ub, *kn, *kb;
+  double* out;
+  const int64_t* out_off;
+  const double* R;
+  const int64_t* rowoff;
+  const double* Bbase;
+  const int64_t* Boff;
+  const double* U;
+  int64_t ldu;
+  int r;
+  const int32_t* skel;
+  const int64_t* roff_new;
+  double* scratch;
+  int64_t gmax;                 // scratch doubles per CTA (>= max kb_s * kn_b)
+};
+void launch_update_B(const UpdateBArgs& a, int grid, cudaStream_t st);
 void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStream_t st);
 
 }  // namespace h2

@@ -227,21 +227,31 @@ def _stats_dict(s):
     return d
 
 
-def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, **opts):
+def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
     unless ``sketch`` is given).  sketch: optional callable sketch(omega, y, col0, row_begin,
     row_end) filling y (tree-order rows) for a black-box K_blk; entry: optional callable
-    entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  opts: h2_build_opts
-    fields (d_init, d_blk, d_max, adaptive, tol_rule, tol_safety, p_os, norm, max_rank, seed,
-    stream_id)."""
+    entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  update=(H_base, U):
+    recompress M = H_base + U U^T (H_base built on this tree, U a (n, r) float64
+    CUDA tensor in tree order) with the library's H^2-matvec + low-rank sketch and entry
+    extraction.  opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
+    tol_safety, p_os, norm, max_rank, seed, stream_id)."""
     o = build_opts(**opts)
     kern = _kernel(*kernel)
     keep = []
     sk = L.h2_sketch()
     sk.kern = kern
-    if sketch is None:
+    if update is not None:
+        Hb, U = update
+        assert Hb.tree is tree, "update: the base H^2 must be built on the same Tree"
+        U = U.contiguous()
+        assert U.is_cuda and U.dtype == torch.float64 and U.shape[0] == tree.n
+        keep += [Hb, U]
+        sk.kind = L.H2_S_H2_LOWRANK
+        sk.base, sk.U, sk.ld_U, sk.rank = Hb._h, U.data_ptr(), U.stride(0), U.shape[1]
+    elif sketch is None:
         sk.kind = L.H2_S_DENSE_KERNEL
     else:
         sk.kind = L.H2_S_CALLBACK
@@ -263,7 +273,10 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         sk.fn = cb
     en = L.h2_entry()
     en.kern = kern
-    if entry is None:
+    if update is not None:
+        en.kind = L.H2_E_H2_LOWRANK
+        en.base, en.U, en.ld_U, en.rank = sk.base, sk.U, sk.ld_U, sk.rank
+    elif entry is None:
         en.kind = L.H2_E_BUILTIN
     else:
         en.kind = L.H2_E_CALLBACK

@@ -7,4 +7,4 @@ BASELINE.json configs).  The random matrix Omega that Algorithm 1 draws (PAPER.m
 "batchedRand") is NOT produced here: the oracle (oracle/rng.py) and the CUDA path
 (csrc/rand.cu) each implement the same counter-based Philox4x32-10 generator.
 """
-from .inputs import uniform_points, grid_points, probe_vectors, workload, WORKLOADS  # noqa: F401
+from .inputs import uniform_points, grid_points, probe_vectors, lowrank_factor, workload, WORKLOADS  # noqa: F401

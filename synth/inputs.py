@@ -7,7 +7,7 @@
 """
 import numpy as np
 
-__all__ = ["uniform_points", "grid_points", "probe_vectors", "workload", "WORKLOADS"]
+__all__ = ["uniform_points", "grid_points", "probe_vectors", "lowrank_factor", "workload", "WORKLOADS"]
 
 
 def uniform_points(n: int, dim: int = 3, seed: int = 0) -> np.ndarray:
@@ -32,6 +32,12 @@ def probe_vectors(n: int, q: int = 16, seed: int = 2) -> np.ndarray:
     return np.random.default_rng(seed).standard_normal((n, q))
 
 
+def lowrank_factor(n: int, r: int = 64, seed: int = 3) -> np.ndarray:
+    """n x r float64 factor U of the symmetric update U U^T (BASELINE configs[4], R24):
+    i.i.d. N(0, 1/r), so diag(U U^T) ~ 1 like the covariance diagonal."""
+    return np.random.default_rng(seed).standard_normal((n, r)) / np.sqrt(r)
+
+
 # name -> (points factory, kernel kind, kernel parameter, leaf size, tol)
 # kernel kinds: "exp" = e^{-r/l} (PAPER.md Eq. cov, L433), "helmholtz" = cos(k r)/r, 0 on the
 # diagonal (PAPER.md Eq. ie, L437).
@@ -45,6 +51,9 @@ WORKLOADS = {
     # BASELINE.json configs[3]: volume IE cos(3r)/r on a 128x128x64 grid (N=2^20), tol 1e-4
     "ie3d_1m": dict(points=lambda: grid_points((128, 128, 64), 1.0 / 128), kernel="helmholtz", param=3.0,
                     leaf=64, tol=1e-4),
+    # BASELINE configs[4]: recompress H2(A) + U U^T, A = exp covariance H^2 (tol 1e-6), rank-64 update
+    "h2update_1m": dict(points=lambda: uniform_points(1 << 20, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6,
+                        update_rank=64),
     # small parity cases (ragged sizes, several tiles)
     "cov3d_5k": dict(points=lambda: uniform_points(5000, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     "ie3d_4k": dict(points=lambda: grid_points((16, 16, 16), 1.0 / 16), kernel="helmholtz", param=3.0,

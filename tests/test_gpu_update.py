@@ -1,0 +1,84 @@
+"""GPU tests of the H^2 + low-rank update path (BASELINE configs[4]): M = A_H + U U^T
+recompressed with the library's black-box H^2-matvec + low-rank sketch and entry extraction."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import geometry, kernels, rng, h2 as oh2
+from synth import uniform_points
+import paper_2506_16759_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_of(H, n):
+    """Dense K_H by matvecs with identity blocks (test utility, small n)."""
+    out = np.empty((n, n))
+    for c0 in range(0, n, 64):
+        nc = min(64, n - c0)
+        E = torch.zeros((n, nc), dtype=torch.float64, device="cuda")
+        E[torch.arange(c0, c0 + nc), torch.arange(nc)] = 1.0
+        out[:, c0:c0 + nc] = H.matvec(E).cpu().numpy()
+    return out
+
+
+@pytest.fixture(scope="module")
+def setup():
+    n, tol, r = 2048, 1e-6, 8
+    X = uniform_points(n, 3, 21)
+    T = g.Tree(X, 64)
+    Hb = g.build(T, ("exp", 0.2), tol)
+    Ul = np.random.default_rng(5).standard_normal((n, r)) / np.sqrt(r)
+    U = torch.from_numpy(Ul).cuda()
+    return dict(n=n, tol=tol, X=X, T=T, Hb=Hb, Ul=Ul, U=U)
+
+
+def test_update_entry_extraction(setup):
+    """K14: D_new = D_A + U U^T exactly (same near pairs); B_new = M(I~_s, I~_b) where M's far
+    blocks are A's U_s B U_b^T (Eq.(2) expanded bases) plus U U^T."""
+    s = setup
+    T, Hb, Ul = s["T"], s["Hb"], s["Ul"]
+    Hu = g.build(T, ("exp", 0.2), s["tol"], update=(Hb, s["U"]))
+    Dl = T.leaf_depth
+    Db, Du = Hb.D_blocks(), Hu.D_blocks()
+    for (a, b), blk in Du.items():
+        Ia = np.arange(T.begin[Dl][a], T.end[Dl][a])
+        Ib = np.arange(T.begin[Dl][b], T.end[Dl][b])
+        ref = Db[(a, b)] + Ul[Ia] @ Ul[Ib].T
+        assert np.abs(blk - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
+    M = dense_of(Hb, s["n"]) + Ul @ Ul.T
+    for t in range(Hu.top_depth, Dl + 1):
+        sk = Hu.skel(t)
+        for (a, b), blk in Hu.B_blocks(t).items():
+            ref = M[np.ix_(sk[a], sk[b])]
+            assert np.abs(blk - ref).max() <= 1e-11 * max(1.0, np.abs(M).max()), (t, a, b)
+
+
+def test_update_accuracy_vs_oracle_operator(setup):
+    """The recompressed matrix approximates the oracle's own M = A_H(oracle) + U U^T to the
+    tolerance (two independent A_H of accuracy tol each: bound 4 tol)."""
+    s = setup
+    T, Hb, Ul, X, tol, n = s["T"], s["Hb"], s["Ul"], s["X"], s["tol"], s["n"]
+    Hu = g.build(T, ("exp", 0.2), tol, update=(Hb, s["U"]))
+    tree = geometry.build_cluster_tree(X, 64)
+    part = geometry.build_partition(tree, 0.7)
+    op = kernels.KernelOperator("exp", 0.2, X[tree.perm])
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, tree.n, c0, nc)
+    Ho = oh2.build(tree, part, op.sampler, op.entry, om, tol)
+    Mo = oh2.to_dense(Ho) + Ul @ Ul.T
+    Mu = dense_of(Hu, n)
+    assert np.linalg.norm(Mu - Mo) <= 4 * tol * np.linalg.norm(Mo)
+    # and against its own operator M_gpu to 2 tol (BASELINE north_star adaptive bar)
+    Mg = dense_of(Hb, n) + Ul @ Ul.T
+    assert np.linalg.norm(Mu - Mg) <= 2 * tol * np.linalg.norm(Mg)
+
+
+def test_update_zero_lowrank_reproduces_base_ranks(setup):
+    """U = 0: M = A_H; the recompression keeps A_H to the tolerance."""
+    s = setup
+    T, Hb = s["T"], s["Hb"]
+    Z = torch.zeros_like(s["U"])
+    Hu = g.build(T, ("exp", 0.2), s["tol"], update=(Hb, Z))
+    x = torch.randn(s["n"], 4, dtype=torch.float64, device="cuda")
+    yb, yu = Hb.matvec(x), Hu.matvec(x)
+    assert (torch.linalg.norm(yu - yb) / torch.linalg.norm(yb)).item() <= 2 * s["tol"]

@@ -35,11 +35,21 @@ out = {"workload": a.workload, "n": n, "leaf": w["leaf"], "tol": w["tol"], "tree
        "leaf_depth": T.leaf_depth, "top_depth": T.top_depth, "near_nnz": T.near_nnz, "far_nnz": T.far_nnz_total,
        "csp": T.csp}
 times = []
+update = None
+if "update_rank" in w:      # configs[4]: base H^2 of A (untimed setup, like PAPER.md L479), then M = A_H + U U^T
+    from synth import lowrank_factor
+    t0 = time.perf_counter()
+    Hbase = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s)
+    torch.cuda.synchronize()
+    out["base_build_s"] = time.perf_counter() - t0
+    out["base_samples"] = Hbase.samples
+    U = torch.from_numpy(lowrank_factor(n, w["update_rank"])).cuda()
+    update = (Hbase, U)
 for r in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s)
+    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, update=update)
     e1.record()
     e1.synchronize()
     times.append(e0.elapsed_time(e1) / 1e3)
@@ -52,7 +62,10 @@ out.update({"build_s": times, "samples": st["samples"], "phase_ms": st["t_phase_
             "peak_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "launches": st["launches"]})
 Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, a.probes))).cuda()
 t0 = time.perf_counter()
-KX = g.dense_sketch(T, Xp, kern)
+if update is not None:      # M X = A_H X + U (U^T X): the operator the update build compresses
+    KX = update[0].matvec(Xp) + update[1] @ (update[1].T @ Xp)
+else:
+    KX = g.dense_sketch(T, Xp, kern)
 HX = H.matvec(Xp)
 torch.cuda.synchronize()
 out["probe_error"] = float(torch.linalg.norm(HX - KX) / torch.linalg.norm(KX))
