@@ -40,8 +40,6 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
   return t;
 }
 
-constexpr int CQ_THREADS = 256;
-constexpr int CQ_WARPS = CQ_THREADS / 32;
 
 // One CTA per cluster.  The panel lives in W (global, L1/L2 resident), row j = column j of A
 // (a point's d samples, contiguous).  Residual column norms are RECOMPUTED from the updated
@@ -49,8 +47,9 @@ constexpr int CQ_WARPS = CQ_THREADS / 32;
 // step i (one pass over the trailing panel per step).
 // SMEM: the panel is factored in shared memory (m*d*8 bytes fit) and written back to W for the
 // ID epilogue; otherwise it is factored in place in W (L1/L2 resident).
-template <bool SMEM>
+template <bool SMEM, int CQ_THREADS>
 __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
+  constexpr int CQ_WARPS = CQ_THREADS / 32;
   extern __shared__ double smem[];
   const int c = blockIdx.x;
   const int m = a.m[c];
@@ -197,19 +196,26 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   }
 }
 
+template <bool SMEM, int NT>
+static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024)
+    H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<SMEM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a);
+}
+
 void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
   size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
   size_t panel = sizeof(double) * (size_t)a.max_m * a.d;
+  // large panels (upper levels: few clusters, m up to ~1000) get 1024 threads per panel
+  const bool big = (size_t)a.max_m * a.d >= 32768;
   if (sm + panel <= 200 * 1024) {
     sm += panel;
-    if (sm > 48 * 1024)
-      H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    cpqr_kernel<true><<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+    if (big) cpqr_launch<true, 1024>(a, sm, st);
+    else cpqr_launch<true, 256>(a, sm, st);
   } else {
-    if (sm > 48 * 1024)
-      H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    cpqr_kernel<false><<<a.nclusters, CQ_THREADS, sm, st>>>(a);
+    if (big) cpqr_launch<false, 1024>(a, sm, st);
+    else cpqr_launch<false, 256>(a, sm, st);
   }
   H2_CHECK_LAUNCH();
 }

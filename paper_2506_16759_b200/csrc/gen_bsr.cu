@@ -90,6 +90,8 @@ template <int CW>
 __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
   constexpr int NT = 4 * CW;           // threads
   constexpr int LDB = CW + 4;
+  constexpr int AE = BT_R * BT_K / NT; // A-slab elements per thread
+  constexpr int BE = BT_K * CW / NT;   // B-slab elements per thread
   __shared__ __align__(16) double sA[BT_R * BT_LD];
   __shared__ __align__(16) double sB[BT_K * LDB];
   const int s = blockIdx.x;
@@ -105,46 +107,87 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int e = a.ptr[s]; e < a.ptr[s + 1]; ++e) {
-    const int b = a.idx[e];
-    const int u = a.uidx[e];
+  // the (partner, k-slab) sequence, with the next slab prefetched into registers while the
+  // current one is multiplied (global loads overlap the DMMAs)
+  const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
+  if (e0 == e1) return;
+  int e = e0, k0 = 0;
+  double ra[AE], rb[BE];
+  int nk_cur = 0;
+  auto load = [&](int ee, int kk0, double* xa, double* xb) -> int {
+    const int b = a.idx[ee];
+    const int u = a.uidx[ee];
     const int mb = a.cnt[b];
     const bool direct = (a.us[u] == s);
     const double* blk = a.blk + a.blk_off[u];
     const double* om = a.Om + a.ooff[b] * a.ldo + cb;
-    for (int k0 = 0; k0 < mb; k0 += BT_K) {
-      const int nk = min(BT_K, mb - k0);
-      __syncthreads();
-      if (direct) {   // stored (s, b): rows of s contiguous along k
-        for (int t = threadIdx.x; t < BT_R * BT_K; t += NT) {
-          int r = t >> 5, kk = t & 31;
-          sA[r * BT_LD + kk] = (r0 + r < ms && kk < nk) ? blk[(int64_t)(r0 + r) * mb + k0 + kk] : 0.0;
-        }
-      } else {        // stored (b, s): read the transpose, coalesced along the rows of s
-        for (int t = threadIdx.x; t < BT_R * BT_K; t += NT) {
-          int kk = t >> 6, r = t & 63;
-          sA[r * BT_LD + kk] = (r0 + r < ms && kk < nk) ? blk[(int64_t)(k0 + kk) * ms + r0 + r] : 0.0;
-        }
+    const int nk = min(BT_K, mb - kk0);
+#pragma unroll
+    for (int q = 0; q < AE; ++q) {
+      const int t = threadIdx.x + q * NT;
+      int r, kk;
+      if (direct) {
+        r = t >> 5;
+        kk = t & 31;
+      } else {
+        kk = t >> 6;
+        r = t & 63;
       }
-      for (int t = threadIdx.x; t < BT_K * CW; t += NT) {
-        int kk = t / CW, c = t % CW;
-        sB[kk * LDB + c] = (kk < nk && c < nc) ? om[(int64_t)(k0 + kk) * a.ldo + c] : 0.0;
-      }
-      __syncthreads();
-      const int ksteps = (nk + 3) >> 2;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const int kk = ks * 4 + (lane & 3);
-        double af[2], bf[4];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) af[i] = sA[(wr * 16 + i * 8 + (lane >> 2)) * BT_LD + kk];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = sB[kk * LDB + wc * 32 + j * 8 + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      }
+      xa[q] = (r0 + r < ms && kk < nk)
+                  ? (direct ? blk[(int64_t)(r0 + r) * mb + kk0 + kk] : blk[(int64_t)(kk0 + kk) * ms + r0 + r])
+                  : 0.0;
     }
+#pragma unroll
+    for (int q = 0; q < BE; ++q) {
+      const int t = threadIdx.x + q * NT;
+      const int kk = t / CW, c = t % CW;
+      xb[q] = (kk < nk && c < nc) ? om[(int64_t)(kk0 + kk) * a.ldo + c] : 0.0;
+    }
+    return nk;
+  };
+  bool cur_direct = (a.us[a.uidx[e]] == s);
+  nk_cur = load(e, k0, ra, rb);
+  while (true) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < AE; ++q) {
+      const int t = threadIdx.x + q * NT;
+      const int r = cur_direct ? (t >> 5) : (t & 63);
+      const int kk = cur_direct ? (t & 31) : (t >> 6);
+      sA[r * BT_LD + kk] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < BE; ++q) {
+      const int t = threadIdx.x + q * NT;
+      sB[(t / CW) * LDB + (t % CW)] = rb[q];
+    }
+    __syncthreads();
+    const int nk = nk_cur;
+    // advance to the next slab and prefetch it
+    k0 += BT_K;
+    if (k0 >= a.cnt[a.idx[e]]) {
+      ++e;
+      k0 = 0;
+    }
+    const bool more = e < e1;
+    if (more) {
+      cur_direct = (a.us[a.uidx[e]] == s);
+      nk_cur = load(e, k0, ra, rb);
+    }
+    const int ksteps = (nk + 3) >> 2;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int kk = ks * 4 + (lane & 3);
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = sA[(wr * 16 + i * 8 + (lane >> 2)) * BT_LD + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = sB[kk * LDB + wc * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (!more) break;
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {

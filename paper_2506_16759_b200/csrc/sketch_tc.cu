@@ -133,8 +133,8 @@ constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
 constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
 constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
 
-template <int NPW>
-__global__ void __launch_bounds__(32 * (NPW + 1), 1)
+template <int NPW, bool CTRL0>
+__global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride) {
@@ -151,9 +151,10 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const int64_t ch_b = nchunks * blockIdx.y / gridDim.y, ch_e = nchunks * (blockIdx.y + 1) / gridDim.y;
   const int nch = (int)(ch_e - ch_b);
   constexpr int TC_PRODUCERS = NPW;
-  constexpr int TC_CTA_THREADS = 32 * (NPW + 1);
+  // CTRL0: producer warp 0 also issues the MMAs and refills the ring (no dedicated control warp)
+  constexpr int TC_CTA_THREADS = 32 * (NPW + (CTRL0 ? 0 : 1));
   constexpr int RPT = 32 / NPW;            // rows per producer thread (128 rows x 64 j / (32 NPW lanes x 8 j))
-  const bool control = (warp == TC_PRODUCERS);
+  const bool control = CTRL0 ? (warp == 0) : (warp == TC_PRODUCERS);
 
   for (int e = tid; e < 16 * 256; e += TC_CTA_THREADS) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
   if (tid == 0) {
@@ -176,60 +177,64 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const uint32_t tmem = *tmem_slot;
   double* Yo = Yout + blockIdx.y * split_stride;
 
-  if (control) {
-    // chunk it -> ring slot it % 4: B (2 KB) + coordinates (2 KB) = 256 x 16 B, 8 per lane
-    auto prefetch = [&](int it) {
-      if (it >= nch) return;
-      const int64_t t = ch_b + it;
-      const int slot = it & (TC_NB - 1);
+  // chunk it -> ring slot it % 4: B (2 KB) + coordinates (2 KB) = 256 x 16 B, 8 per lane
+  auto prefetch = [&](int it) {
+    if (it >= nch) return;
+    const int64_t t = ch_b + it;
+    const int slot = it & (TC_NB - 1);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int e = lane + 32 * q;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BBUF + e * 16),
-                     "l"(Bq + t * TC_BBUF + e * 16));
-        const int jc = e >> 1;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
-                                                                          (jc >> 3) * 16),
-                     "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
-      }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
-    };
+    for (int q = 0; q < 4; ++q) {
+      const int e = lane + 32 * q;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BBUF + e * 16),
+                   "l"(Bq + t * TC_BBUF + e * 16));
+      const int jc = e >> 1;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
+                                                                        (jc >> 3) * 16),
+                   "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
+  };
+  // wait until every producer wrote A(it), issue its 14 MMAs, commit; then refill slot it+2
+  auto control_step = [&](int it) {
+    const int buf = it % TC_NA;
+    const int slot = it & (TC_NB - 1);
+    mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const bool first = (it % TC_DRAIN) == 0;
+    const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+    if (lane == 0) {
+      const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
+      const uint32_t b0 = sbase + SMEM2_B + slot * TC_BBUF;
+#pragma unroll
+      for (int s = 0; s < TC_NS; ++s)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
+          const uint64_t bd = umma_desc(b0 + kk * 2 * 512, 512, 128);
+          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * 32),
+              "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+        }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          bar_empty + 8 * buf));
+      if (drain)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            bar_drain));
+    }
+    __syncwarp();
+    // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
+    // full(it-2) and its B by MMA(it-2) -> wait for that MMA
+    if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
+    prefetch(it + 2);
+  };
+  if (control) {
     prefetch(0);
     prefetch(1);
-    for (int it = 0; it < nch; ++it) {
-      const int buf = it % TC_NA;
-      const int slot = it & (TC_NB - 1);
-      mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const bool first = (it % TC_DRAIN) == 0;
-      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
-      if (lane == 0) {
-        const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
-        const uint32_t b0 = sbase + SMEM2_B + slot * TC_BBUF;
-#pragma unroll
-        for (int s = 0; s < TC_NS; ++s)
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
-            const uint64_t bd = umma_desc(b0 + kk * 2 * 512, 512, 128);
-            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-            asm volatile(
-                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * 32),
-                "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
-          }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            bar_empty + 8 * buf));
-        if (drain)
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-              bar_drain));
-      }
-      __syncwarp();
-      // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
-      // full(it-2) and its B by MMA(it-2) -> wait for that MMA
-      if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
-      prefetch(it + 2);
-    }
+  }
+  if (!CTRL0 && control) {
+    for (int it = 0; it < nch; ++it) control_step(it);
   } else {
     // producer: rows rs*16 + pair + k*16*NPW/4 (k < RPT), 8 consecutive j (half h of 16-j group g)
     const int g = warp & 3;
@@ -283,6 +288,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
+      if (CTRL0 && control) control_step(it);
 
       const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
       if (drain && warp < 4) {
@@ -339,12 +345,15 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   static bool attr_set = false;
   if (!attr_set) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
     attr_set = true;
   }
   const char* npw_env = getenv("H2_TC_NPW");
-  const int npw = (npw_env && atoi(npw_env) == 8) ? 8 : 16;   // 16 producer warps (measured 163 vs 170 ms)
+  // 8: 8 producers + control warp; 17 (default): 16 producers + control warp; 16: 16 producers,
+  // warp 0 also controls (512 threads, 128 registers)
+  const int npw = npw_env ? atoi(npw_env) : 17;   // measured (N=2^18): 17 -> 163 ms, 8 -> 170, 16 -> 181
   const int64_t nchunks = (n + TC_JC - 1) / TC_JC;
   const int64_t npad = nchunks * TC_JC;
   const int64_t rows = row1 - row0;
@@ -376,11 +385,14 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     H2_CHECK_LAUNCH();
     double* yo = S > 1 ? part : Yout + c0;
     const int64_t ld = S > 1 ? nc : ldy;
-    if (npw == 16)
-      sketch_tc_kernel<16><<<dim3(tiles, S), 32 * 17, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
-                                                                      S > 1 ? rows * nc : 0);
+    if (npw == 17)
+      sketch_tc_kernel<16, false><<<dim3(tiles, S), 32 * 17, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
+                                                                             ld, S > 1 ? rows * nc : 0);
+    else if (npw == 16)
+      sketch_tc_kernel<16, true><<<dim3(tiles, S), 32 * 16, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
+                                                                            ld, S > 1 ? rows * nc : 0);
     else
-      sketch_tc_kernel<8><<<dim3(tiles, S), 32 * 9, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+      sketch_tc_kernel<8, false><<<dim3(tiles, S), 32 * 9, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
                                                                      S > 1 ? rows * nc : 0);
     H2_CHECK_LAUNCH();
     if (S > 1) {

@@ -49,7 +49,8 @@ for r in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, update=update)
+    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, update=update,
+                d_max=w.get("d_max", 512))
     e1.record()
     e1.synchronize()
     times.append(e0.elapsed_time(e1) / 1e3)
