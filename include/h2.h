@@ -189,6 +189,8 @@ typedef struct {
   double eps;                 /* final eps_l                                                */
   int64_t entries_D, entries_B; /* unique entries evaluated and stored                       */
   int64_t entries_sketch;     /* kernel entries evaluated by the built-in dense sketch      */
+  int64_t sketch_columns;     /* Omega columns pushed through the sketch operator (>= samples:
+                                 speculative 64-column tensor-core passes)       */
   int64_t bytes_U, bytes_E, bytes_B, bytes_D;
   int64_t launches;           /* device kernel launches issued by h2_build                  */
   double t_phase_ms[H2_NPHASE];

@@ -72,6 +72,7 @@ class h2_build_stats(C.Structure):
                 ("leaf_depth", C.c_int32), ("rounds", C.c_int32 * 64), ("rank_min", C.c_int32 * 64),
                 ("rank_max", C.c_int32 * 64), ("rank_mean", C.c_double * 64), ("eps", C.c_double),
                 ("entries_D", C.c_int64), ("entries_B", C.c_int64), ("entries_sketch", C.c_int64),
+                ("sketch_columns", C.c_int64),
                 ("bytes_U", C.c_int64), ("bytes_E", C.c_int64), ("bytes_B", C.c_int64), ("bytes_D", C.c_int64),
                 ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double)]
 

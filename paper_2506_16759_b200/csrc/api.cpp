@@ -217,34 +217,76 @@ struct Builder {
 
   // ---------------------------------------------------------------- sketch of stream columns
   // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
-  void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
-    timer.begin(H2_PH_RAND);
+  // Speculative sketch columns: the int8 tensor-core
+  // sketch is bound by the FP64 evaluation of K, and one pass contracts each K tile with up to 64
+  // Omega columns at the same cost as 32.  A draw of nc < 64 columns therefore computes the whole
+  // pass and keeps the extra columns c0+nc.. for the next updateSamples draw.  Omega columns are
+  // counter-based and every sketch column is computed independently (exact integer accumulation),
+  // so the samples consumed are bit-identical to unspeculated draws.
+  bool spec_on = false;
+  Panel spec;                   // n x 64: columns [spec_c0, spec_c0 + spec_n) at offset spec_off
+  int spec_c0 = -1, spec_n = 0, spec_off = 0;
+  int64_t sketch_columns = 0;
+
+  void sketch_cols(double* Yd, double* Od, int64_t ld, int c0, int nc) {
     launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
     timer.end();
     timer.begin(H2_PH_SKETCH);
-    if (S.kind == H2_S_DENSE_KERNEL) {
-      launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
-      entries_sketch += T.n * T.n;
-    } else if (S.kind == H2_S_H2_LOWRANK) {
-      // K_blk = A_H Omega + U (U^T Omega)
-      matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
-      DArr<double> scr;
-      scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
-      launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
+    launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
+    entries_sketch += T.n * T.n * (int64_t)div_up(nc, 64);
+    sketch_columns += nc;
+  }
+
+  // ---------------------------------------------------------------- sketch of stream columns
+  // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
+  void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
+    timer.begin(H2_PH_RAND);
+    if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < 64 && c0 == spec_c0 && nc <= spec_n) {
+      H2_CUDA(cudaMemcpy2DAsync(Yd, ld * 8, spec.Y.p + spec_off, spec.ld * 8, (size_t)nc * 8, T.n,
+                                cudaMemcpyDeviceToDevice, st));
+      H2_CUDA(cudaMemcpy2DAsync(Od, ld * 8, spec.O.p + spec_off, spec.ld * 8, (size_t)nc * 8, T.n,
+                                cudaMemcpyDeviceToDevice, st));
+      spec_c0 += nc;
+      spec_n -= nc;
+      spec_off += nc;
+      timer.end();
+      timer.begin(H2_PH_SKETCH);
+    } else if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < 64 && c0 + 64 <= o.d_max) {
+      if (spec.rows == 0) spec.alloc(T.n, 64, st);
+      sketch_cols(spec.Y.p, spec.O.p, spec.ld, c0, 64);
+      H2_CUDA(cudaMemcpy2DAsync(Yd, ld * 8, spec.Y.p, spec.ld * 8, (size_t)nc * 8, T.n, cudaMemcpyDeviceToDevice, st));
+      H2_CUDA(cudaMemcpy2DAsync(Od, ld * 8, spec.O.p, spec.ld * 8, (size_t)nc * 8, T.n, cudaMemcpyDeviceToDevice, st));
+      spec_c0 = c0 + nc;
+      spec_n = 64 - nc;
+      spec_off = nc;
+    } else if (S.kind == H2_S_DENSE_KERNEL) {
+      sketch_cols(Yd, Od, ld, c0, nc);
     } else {
-      h2_sketch_req rq{};
-      rq.n = T.n;
-      rq.row_begin = 0;
-      rq.row_end = T.n;
-      rq.col0 = c0;
-      rq.ncols = nc;
-      rq.omega = Od;
-      rq.ld_omega = ld;
-      rq.y = Yd;
-      rq.ld_y = ld;
-      rq.stream = st;
-      int rc = S.fn(S.ctx, &rq);
-      if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+      launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
+      timer.end();
+      timer.begin(H2_PH_SKETCH);
+      sketch_columns += nc;
+      if (S.kind == H2_S_H2_LOWRANK) {
+        // K_blk = A_H Omega + U (U^T Omega)
+        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
+        DArr<double> scr;
+        scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
+        launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
+      } else {
+        h2_sketch_req rq{};
+        rq.n = T.n;
+        rq.row_begin = 0;
+        rq.row_end = T.n;
+        rq.col0 = c0;
+        rq.ncols = nc;
+        rq.omega = Od;
+        rq.ld_omega = ld;
+        rq.y = Yd;
+        rq.ld_y = ld;
+        rq.stream = st;
+        int rc = S.fn(S.ctx, &rq);
+        if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+      }
     }
     timer.end();
     timer.begin(H2_PH_MISC);
@@ -588,7 +630,10 @@ struct Builder {
     H.Dl = Dl;
     H.n = T.n;
     H.lv.resize(Dl - top + 1);
-    if (S.kind == H2_S_DENSE_KERNEL) skp = make_kernel(S.kern);
+    if (S.kind == H2_S_DENSE_KERNEL) {
+      skp = make_kernel(S.kern);
+      spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
+    }
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
     d = std::min(o.d_init, o.d_max);
     sumsq_scratch.alloc(div_up(T.n, 1024), st);
@@ -686,6 +731,7 @@ struct Builder {
     s.leaf_depth = Dl;
     s.entries_D = T.D_off.back();
     s.entries_sketch = entries_sketch;
+    s.sketch_columns = sketch_columns;
     s.bytes_D = H.D.bytes();
     for (int t = top; t <= Dl; ++t) {
       const Level& L = H.L(t);

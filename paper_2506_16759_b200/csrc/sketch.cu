@@ -196,11 +196,12 @@ void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, doub
   H2_CHECK_LAUNCH();
 }
 
-namespace {
 int env_int(const char* name, int def) {
   const char* v = getenv(name);
   return v ? atoi(v) : def;
 }
+
+namespace {
 
 template <int KIND, int MB, int MINB, int UNR>
 void sketch_variant(dim3 grid, cudaStream_t st, const double* X, const double* Yc, const double* Zc, int64_t n,

@@ -22,15 +22,23 @@
 namespace h2 {
 namespace {
 
+
 constexpr int TC_M = 128;                      // rows per CTA (UMMA M)
 constexpr int TC_JC = 64;                      // j per chunk (K bytes per slice)
 constexpr int TC_NS = 7;                       // byte slices of the 52-bit fixed-point K
 constexpr int TC_SLICE = TC_M * TC_JC;         // 8 KB
 constexpr int TC_ABUF = TC_NS * TC_SLICE;      // 56 KB per A buffer
-constexpr int TC_BBUF = 32 * TC_JC;            // 2 KB (32 columns x 64 j, int8)
+constexpr int TC_BMAX = 64 * TC_JC;            // B chunk bytes for 64 columns (int8)
 constexpr int TC_CBUF = TC_JC * 32 + 128;      // 64 j x (x, y, z, pad) doubles, +16 B per 8 j (bank skew)
 constexpr int TC_NB = 4;                       // coordinate / B ring depth
+constexpr int TC_NA = 3;                       // A buffers
 constexpr int TC_DRAIN = 1024;                 // chunks per TMEM drain: 65536 * 255 * 32 < 2^31
+constexpr int SMEM2_A = 0;
+constexpr int SMEM2_B = TC_NA * TC_ABUF;
+constexpr int SMEM2_C = SMEM2_B + TC_NB * TC_BMAX;
+constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
+constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
+constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
 
 // UMMA shared-memory descriptor, K-major, no swizzle (canonical ((8,m),(16B,2)):((16B,SBO),(1,LBO)))
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -38,8 +46,11 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);   // version 1 (sm_100)
 }
 
-// instruction descriptor: D s32, A u8, B s8, both K-major, N = 32, M = 128
-constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// instruction descriptor: D s32, A u8, B s8, both K-major, N = NCOL, M = 128
+template <int NCOL>
+__host__ __device__ constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((128u >> 4) << 24);
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count));
@@ -51,6 +62,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(addr),
       "r"(parity));
 }
+
 
 // round(exp(-|x'-y'|) * 2^52) for r2 = |x'-y'|^2 (scaled coordinates) as (lo 32, hi 20 bits).
 // r2 is clamped to [2^-1007, 490000] on its high word (integer pipe): 1/sqrt stays finite at
@@ -100,44 +112,42 @@ __global__ void coords_aos_kernel(const double* X, const double* Y, const double
     out[i] = i < n ? make_double4(X[i] * cs, Y[i] * cs, Z[i] * cs, 0.0) : make_double4(0.0, 0.0, 0.0, 0.0);
 }
 
-// Omega (n x ncols doubles q/4) -> int8 q per 64-j chunk in the B core-matrix layout:
-// chunk t, column c, jj: t*2048 + (jj/16)*512 + (c/8)*128 + (c%8)*16 + jj%16  (0 beyond n / ncols)
-__global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int64_t n, int ncols, int64_t nchunks,
-                                int8_t* __restrict__ out) {
-  const int64_t total = nchunks * TC_JC * 32;
+// Omega (n x ncols doubles q/4) -> int8 q per 64-j chunk in the B core-matrix layout for NCOL
+// columns: chunk t, column c, jj: t*NCOL*64 + (jj/16)*(NCOL*16) + (c/8)*128 + (c%8)*16 + jj%16
+// (0 beyond n / ncols).  The K-direction core stride (LBO) is NCOL*16 bytes.
+__global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int64_t n, int ncols, int NCOL,
+                                int64_t nchunks, int8_t* __restrict__ out) {
+  const int64_t total = nchunks * TC_JC * NCOL;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e >> 5;
-    const int c = (int)(e & 31);
+    const int64_t j = e / NCOL;
+    const int c = (int)(e - j * NCOL);
     const int64_t t = j / TC_JC;
     const int jj = (int)(j - t * TC_JC);
     int q = 0;
     if (j < n && c < ncols) q = __double2int_rn(Om[j * ldo + c] * 4.0);
-    out[t * TC_BBUF + (jj >> 4) * 512 + (c >> 3) * 128 + (c & 7) * 16 + (jj & 15)] = (int8_t)q;
+    out[t * (NCOL * TC_JC) + (jj >> 4) * (NCOL * 16) + (c >> 3) * 128 + (c & 7) * 16 + (jj & 15)] = (int8_t)q;
   }
 }
 
-// Warp-specialised, barrier-free pipeline per CTA (128 rows):
-//   16 producer warps: wait loaded[slot] (coordinates + B of the chunk landed) and empty[buf]
-//     (the MMA that last read A[buf] finished), evaluate 2 rows x 8 j each, write the 7 byte
-//     slices to A[buf], fence.proxy.async, arrive on full[buf];
-//   1 control warp: waits full[buf], issues the 14 tcgen05.mma of the chunk, commits empty[buf]
-//     (and drain on drain chunks), then refills the coordinate / B ring with cp.async tracked
-//     by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
+// Warp-specialised, barrier-free pipeline per CTA (128 rows x NCOL sample columns):
+//   NPW producer warps: wait loaded[slot] (coordinates + B of the chunk landed) and empty[buf]
+//     (the MMA that last read A[buf] finished), evaluate 32/NPW rows x 8 j each, write the 7
+//     byte slices to A[buf], fence.proxy.async, arrive on full[buf];
+//   1 control warp: waits full[buf], issues the 14 tcgen05.mma (M 128, N NCOL, K 32) of the
+//     chunk, commits empty[buf] (and drain on drain chunks), then refills the coordinate / B ring
+//     with cp.async tracked by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
 //   producer warps 0-3 (TMEM lanes 0-127) drain the int32 accumulators after every drain chunk.
-constexpr int TC_NA = 3;                 // A buffers
-// NPW producer warps (8: 4 rows x 8 j = 32 entries per lane and chunk; 16: 2 rows x 8 j)
-constexpr int SMEM2_A = 0;
-constexpr int SMEM2_B = TC_NA * TC_ABUF;
-constexpr int SMEM2_C = SMEM2_B + TC_NB * TC_BBUF;
-constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
-constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
-constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
-
-template <int NPW, bool CTRL0>
-__global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
+template <int NPW, int NCOL>
+__global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride) {
+  constexpr int NTH = 32 * (NPW + 1);
+  constexpr int RPT = 32 / NPW;            // rows per producer thread (128 rows x 64 j / (32 NPW lanes x 8 j))
+  constexpr int BBUF = NCOL * TC_JC;       // B chunk bytes
+  constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
+  constexpr uint32_t TMEM_COLS = NCOL == 32 ? 256 : 512;
+  constexpr uint32_t IDESC = idesc_i8<NCOL>();
   extern __shared__ __align__(1024) uint8_t smem[];
   double* tab = reinterpret_cast<double*>(smem + SMEM2_T);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
@@ -150,16 +160,12 @@ __global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
   const int64_t rtile = row0 + (int64_t)blockIdx.x * TC_M;
   const int64_t ch_b = nchunks * blockIdx.y / gridDim.y, ch_e = nchunks * (blockIdx.y + 1) / gridDim.y;
   const int nch = (int)(ch_e - ch_b);
-  constexpr int TC_PRODUCERS = NPW;
-  // CTRL0: producer warp 0 also issues the MMAs and refills the ring (no dedicated control warp)
-  constexpr int TC_CTA_THREADS = 32 * (NPW + (CTRL0 ? 0 : 1));
-  constexpr int RPT = 32 / NPW;            // rows per producer thread (128 rows x 64 j / (32 NPW lanes x 8 j))
-  const bool control = CTRL0 ? (warp == 0) : (warp == TC_PRODUCERS);
+  const bool control = (warp == NPW);
 
-  for (int e = tid; e < 16 * 256; e += TC_CTA_THREADS) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
+  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
   if (tid == 0) {
     for (int b = 0; b < TC_NA; ++b) {
-      mbar_init(bar_full + 8 * b, TC_PRODUCERS);
+      mbar_init(bar_full + 8 * b, NPW);
       mbar_init(bar_empty + 8 * b, 1);
     }
     for (int s = 0; s < TC_NB; ++s) mbar_init(bar_loaded + 8 * s, 32);
@@ -167,8 +173,9 @@ __global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
-        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(tmem_slot)),
+                 "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -177,66 +184,66 @@ __global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
   const uint32_t tmem = *tmem_slot;
   double* Yo = Yout + blockIdx.y * split_stride;
 
-  // chunk it -> ring slot it % 4: B (2 KB) + coordinates (2 KB) = 256 x 16 B, 8 per lane
-  auto prefetch = [&](int it) {
-    if (it >= nch) return;
-    const int64_t t = ch_b + it;
-    const int slot = it & (TC_NB - 1);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = lane + 32 * q;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BBUF + e * 16),
-                   "l"(Bq + t * TC_BBUF + e * 16));
-      const int jc = e >> 1;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
-                                                                        (jc >> 3) * 16),
-                   "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
-    }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
-  };
-  // wait until every producer wrote A(it), issue its 14 MMAs, commit; then refill slot it+2
-  auto control_step = [&](int it) {
-    const int buf = it % TC_NA;
-    const int slot = it & (TC_NB - 1);
-    mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    const bool first = (it % TC_DRAIN) == 0;
-    const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
-    if (lane == 0) {
-      const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
-      const uint32_t b0 = sbase + SMEM2_B + slot * TC_BBUF;
-#pragma unroll
-      for (int s = 0; s < TC_NS; ++s)
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
-          const uint64_t bd = umma_desc(b0 + kk * 2 * 512, 512, 128);
-          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * 32),
-              "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
-        }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-          bar_empty + 8 * buf));
-      if (drain)
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            bar_drain));
-    }
-    __syncwarp();
-    // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
-    // full(it-2) and its B by MMA(it-2) -> wait for that MMA
-    if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
-    prefetch(it + 2);
-  };
   if (control) {
+    // chunk it -> ring slot it % 4: B (NCOL x 64 bytes) + coordinates (2 KB) in 16 B pieces
+    auto prefetch = [&](int it) {
+      if (it >= nch) return;
+      const int64_t t = ch_b + it;
+      const int slot = it & (TC_NB - 1);
+#pragma unroll
+      for (int q = 0; q < BBUF / 16 / 32; ++q) {
+        const int e = lane + 32 * q;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BMAX + e * 16),
+                     "l"(Bq + t * BBUF + e * 16));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = lane + 32 * q;
+        const int jc = e >> 1;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
+                                                                          (jc >> 3) * 16),
+                     "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
+    };
     prefetch(0);
     prefetch(1);
-  }
-  if (!CTRL0 && control) {
-    for (int it = 0; it < nch; ++it) control_step(it);
+    for (int it = 0; it < nch; ++it) {
+      const int buf = it % TC_NA;
+      const int slot = it & (TC_NB - 1);
+      mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const bool first = (it % TC_DRAIN) == 0;
+      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+      if (lane == 0) {
+        const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
+        const uint32_t b0 = sbase + SMEM2_B + slot * TC_BMAX;
+#pragma unroll
+        for (int s = 0; s < TC_NS; ++s)
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
+            const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
+            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * NCOL),
+                "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+          }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            bar_empty + 8 * buf));
+        if (drain)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              bar_drain));
+      }
+      __syncwarp();
+      // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
+      // full(it-2) and its B by MMA(it-2) -> wait for that MMA
+      if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
+      prefetch(it + 2);
+    }
   } else {
-    // producer: rows rs*16 + pair + k*16*NPW/4 (k < RPT), 8 consecutive j (half h of 16-j group g)
+    // producer: rows rs*16 + pair + k*4*NPW (k < RPT), 8 consecutive j (half h of 16-j group g)
     const int g = warp & 3;
     const int rs = warp >> 2;
     const int h = lane & 1;
@@ -288,39 +295,41 @@ __global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
-      if (CTRL0 && control) control_step(it);
 
       const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
       if (drain && warp < 4) {
         mbar_wait(bar_drain, drains & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const int64_t i = rtile + warp * 32 + lane;
-        double v[32];
+        double* y = Yo + (i - row0) * ldy;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NCOL; c0 += 32) {   // 32 columns at a time (register budget)
+          double v[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = 0.0;
+          for (int c = 0; c < 32; ++c) v[c] = 0.0;
 #pragma unroll
-        for (int s = 0; s < TC_NS; ++s) {
-          uint32_t r[32];
-          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + s * 32;
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-          const double wgt = ldexp(1.0, 8 * s - 54);   // slice weight 2^(8s) * 2^-52 * (1/4)
+          for (int s = 0; s < TC_NS; ++s) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + s * NCOL + c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const double wgt = ldexp(1.0, 8 * s - 54);   // slice weight 2^(8s) * 2^-52 * (1/4)
 #pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
-        }
-        if (i < row1) {
-          double* y = Yo + (i - row0) * ldy;
+            for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+          }
+          if (i < row1) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c < ncols) y[c] = drains == 0 ? v[c] : y[c] + v[c];
+            for (int c = 0; c < 32; ++c)
+              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? v[c] : y[c0 + c] + v[c];
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       }
@@ -329,13 +338,29 @@ __global__ void __launch_bounds__(32 * (NPW + (CTRL0 ? 0 : 1)), 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
 }  // namespace
 
 bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP; }
 
+namespace {
+template <int NPW, int NCOL>
+void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
+               int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride) {
+  static bool attr = false;
+  if (!attr) {
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<NPW, NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    attr = true;
+  }
+  sketch_tc_kernel<NPW, NCOL><<<grid, 32 * (NPW + 1), SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+                                                                        sstride);
+}
+}  // namespace
+
+// Omega columns are processed 64 at a time (one pass evaluates K once for up to 64 columns);
+// H2_TC_NPW selects 8 or 16 producer warps (default 16).
 void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st) {
@@ -343,17 +368,8 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static bool attr_set = false;
-  if (!attr_set) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
-    attr_set = true;
-  }
   const char* npw_env = getenv("H2_TC_NPW");
-  // 8: 8 producers + control warp; 17 (default): 16 producers + control warp; 16: 16 producers,
-  // warp 0 also controls (512 threads, 128 registers)
-  const int npw = npw_env ? atoi(npw_env) : 17;   // measured (N=2^18): 17 -> 163 ms, 8 -> 170, 16 -> 181
+  const int npw = (npw_env && atoi(npw_env) == 8) ? 8 : 16;   // measured (N=2^18, 32 cols): 16 -> 163 ms, 8 -> 170
   const int64_t nchunks = (n + TC_JC - 1) / TC_JC;
   const int64_t npad = nchunks * TC_JC;
   const int64_t rows = row1 - row0;
@@ -373,31 +389,30 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     }
   }
   double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
-  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)nchunks * TC_BBUF, st));
-  double* part = S > 1 ? static_cast<double*>(cache_alloc(sizeof(double) * rows * 32 * S, st)) : nullptr;
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)nchunks * TC_BMAX, st));
+  double* part = S > 1 ? static_cast<double*>(cache_alloc(sizeof(double) * rows * 64 * S, st)) : nullptr;
   coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(X, Yc, Zc, n, npad,
                                                                                                   kp.inv, C);
   H2_CHECK_LAUNCH();
-  for (int c0 = 0; c0 < ncols; c0 += 32) {
-    const int nc = std::min(32, ncols - c0);
-    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * TC_JC * 32 + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
-        Om + c0, ldo, n, nc, nchunks, Bq);
+  for (int c0 = 0; c0 < ncols; c0 += 64) {
+    const int nc = std::min(64, ncols - c0);
+    const int NCOL = nc > 32 ? 64 : 32;
+    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * TC_JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+        Om + c0, ldo, n, nc, NCOL, nchunks, Bq);
     H2_CHECK_LAUNCH();
     double* yo = S > 1 ? part : Yout + c0;
     const int64_t ld = S > 1 ? nc : ldy;
-    if (npw == 17)
-      sketch_tc_kernel<16, false><<<dim3(tiles, S), 32 * 17, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
-                                                                             ld, S > 1 ? rows * nc : 0);
-    else if (npw == 16)
-      sketch_tc_kernel<16, true><<<dim3(tiles, S), 32 * 16, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
-                                                                            ld, S > 1 ? rows * nc : 0);
-    else
-      sketch_tc_kernel<8, false><<<dim3(tiles, S), 32 * 9, SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
-                                                                     S > 1 ? rows * nc : 0);
-    H2_CHECK_LAUNCH();
-    if (S > 1) {
-      launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
+    const int64_t ss = S > 1 ? rows * nc : 0;
+    const dim3 grid(tiles, S);
+    if (NCOL == 64) {
+      if (npw == 8) tc_launch<8, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      else tc_launch<16, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+    } else {
+      if (npw == 8) tc_launch<8, 32>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      else tc_launch<16, 32>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
     }
+    H2_CHECK_LAUNCH();
+    if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
   }
   cache_free(C, st);
   cache_free(Bq, st);

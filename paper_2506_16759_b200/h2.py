@@ -216,7 +216,7 @@ class H2Matrix:
 
 def _stats_dict(s):
     d = {k: getattr(s, k) for k in ("samples", "failed_depth", "top_depth", "leaf_depth", "eps", "entries_D",
-                                    "entries_B", "entries_sketch", "bytes_U", "bytes_E", "bytes_B", "bytes_D",
+                                    "entries_B", "entries_sketch", "sketch_columns", "bytes_U", "bytes_E", "bytes_B", "bytes_D",
                                     "launches", "t_total_ms")}
     lo, hi = s.top_depth, s.leaf_depth
     d["rounds"] = {t: s.rounds[t] for t in range(lo, hi + 1)}

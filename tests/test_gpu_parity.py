@@ -185,3 +185,24 @@ def test_deterministic_bitwise():
         assert np.array_equal(H1._export(g._lib.H2_X_BASIS, t), H2._export(g._lib.H2_X_BASIS, t))
         assert np.array_equal(H1._export(g._lib.H2_X_B, t), H2._export(g._lib.H2_X_B, t))
     assert np.array_equal(H1._export(g._lib.H2_X_D), H2._export(g._lib.H2_X_D))
+
+
+def test_speculative_sketch_columns_bitwise(monkeypatch):
+    """Speculative 64-column tensor-core passes change how many Omega columns are
+    pushed through the sketch, never the samples consumed: the build is bit-identical to one
+    drawing exactly d_blk columns per updateSamples."""
+    X = uniform_points(5000, 3, 0)
+    T = g.Tree(X, 64)
+    monkeypatch.setenv("H2_SPEC", "0")
+    H0 = g.build(T, ("exp", 0.2), 1e-6, d_init=16, d_blk=16)
+    monkeypatch.setenv("H2_SPEC", "1")
+    H1 = g.build(T, ("exp", 0.2), 1e-6, d_init=16, d_blk=16)
+    assert H0.samples == H1.samples
+    assert H0.stats["sketch_columns"] == H0.samples
+    assert H1.samples <= H1.stats["sketch_columns"] < H1.samples + 64
+    assert H1.stats["entries_sketch"] < H0.stats["entries_sketch"]
+    for t in range(H0.top_depth, T.leaf_depth + 1):
+        assert np.array_equal(H0.rank(t), H1.rank(t))
+        assert all(np.array_equal(a, b) for a, b in zip(H0.skel(t), H1.skel(t)))
+        assert np.array_equal(H0._export(g._lib.H2_X_BASIS, t), H1._export(g._lib.H2_X_BASIS, t))
+        assert np.array_equal(H0._export(g._lib.H2_X_B, t), H1._export(g._lib.H2_X_B, t))
