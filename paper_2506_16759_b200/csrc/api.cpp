@@ -218,13 +218,15 @@ struct Builder {
   // ---------------------------------------------------------------- sketch of stream columns
   // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
   // Speculative sketch columns: the int8 tensor-core
-  // sketch is bound by the FP64 evaluation of K, and one pass contracts each K tile with up to 64
-  // Omega columns at the same cost as 32.  A draw of nc < 64 columns therefore computes the whole
-  // pass and keeps the extra columns c0+nc.. for the next updateSamples draw.  Omega columns are
-  // counter-based and every sketch column is computed independently (exact integer accumulation),
-  // so the samples consumed are bit-identical to unspeculated draws.
+  // sketch is bound by the FP64 evaluation of K, and one pass contracts each K tile with up to
+  // W = sketch_tc_pass_cols() (128) Omega columns at the same evaluation cost as 32.  A draw of
+  // nc < W columns therefore computes the whole pass and keeps the extra columns c0+nc.. for the
+  // next updateSamples draws.  Omega columns are counter-based and every sketch column is computed
+  // independently (exact integer accumulation), so the samples consumed are bit-identical to
+  // unspeculated draws.
   bool spec_on = false;
-  Panel spec;                   // n x 64: columns [spec_c0, spec_c0 + spec_n) at offset spec_off
+  int spec_w = 64;              // pass width W
+  Panel spec;                   // n x W: columns [spec_c0, spec_c0 + spec_n) at offset spec_off
   int spec_c0 = -1, spec_n = 0, spec_off = 0;
   int64_t sketch_columns = 0;
 
@@ -233,7 +235,7 @@ struct Builder {
     timer.end();
     timer.begin(H2_PH_SKETCH);
     launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
-    entries_sketch += T.n * T.n * (int64_t)div_up(nc, 64);
+    entries_sketch += T.n * T.n * (int64_t)div_up(nc, spec_on ? spec_w : 64);
     sketch_columns += nc;
   }
 
@@ -241,7 +243,7 @@ struct Builder {
   // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
   void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
     timer.begin(H2_PH_RAND);
-    if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < 64 && c0 == spec_c0 && nc <= spec_n) {
+    if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < spec_w && c0 == spec_c0 && nc <= spec_n) {
       H2_CUDA(cudaMemcpy2DAsync(Yd, ld * 8, spec.Y.p + spec_off, spec.ld * 8, (size_t)nc * 8, T.n,
                                 cudaMemcpyDeviceToDevice, st));
       H2_CUDA(cudaMemcpy2DAsync(Od, ld * 8, spec.O.p + spec_off, spec.ld * 8, (size_t)nc * 8, T.n,
@@ -251,13 +253,13 @@ struct Builder {
       spec_off += nc;
       timer.end();
       timer.begin(H2_PH_SKETCH);
-    } else if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < 64 && c0 + 64 <= o.d_max) {
-      if (spec.rows == 0) spec.alloc(T.n, 64, st);
-      sketch_cols(spec.Y.p, spec.O.p, spec.ld, c0, 64);
+    } else if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < spec_w && c0 + spec_w <= o.d_max) {
+      if (spec.rows == 0) spec.alloc(T.n, spec_w, st);
+      sketch_cols(spec.Y.p, spec.O.p, spec.ld, c0, spec_w);
       H2_CUDA(cudaMemcpy2DAsync(Yd, ld * 8, spec.Y.p, spec.ld * 8, (size_t)nc * 8, T.n, cudaMemcpyDeviceToDevice, st));
       H2_CUDA(cudaMemcpy2DAsync(Od, ld * 8, spec.O.p, spec.ld * 8, (size_t)nc * 8, T.n, cudaMemcpyDeviceToDevice, st));
       spec_c0 = c0 + nc;
-      spec_n = 64 - nc;
+      spec_n = spec_w - nc;
       spec_off = nc;
     } else if (S.kind == H2_S_DENSE_KERNEL) {
       sketch_cols(Yd, Od, ld, c0, nc);
@@ -633,6 +635,7 @@ struct Builder {
     if (S.kind == H2_S_DENSE_KERNEL) {
       skp = make_kernel(S.kern);
       spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
+      spec_w = sketch_tc_pass_cols();
     }
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
     d = std::min(o.d_init, o.d_max);

@@ -23,22 +23,29 @@ namespace h2 {
 namespace {
 
 
-constexpr int TC_M = 128;                      // rows per CTA (UMMA M)
-constexpr int TC_JC = 64;                      // j per chunk (K bytes per slice)
 constexpr int TC_NS = 7;                       // byte slices of the 52-bit fixed-point K
-constexpr int TC_SLICE = TC_M * TC_JC;         // 8 KB
-constexpr int TC_ABUF = TC_NS * TC_SLICE;      // 56 KB per A buffer
-constexpr int TC_BMAX = 64 * TC_JC;            // B chunk bytes for 64 columns (int8)
-constexpr int TC_CBUF = TC_JC * 32 + 128;      // 64 j x (x, y, z, pad) doubles, +16 B per 8 j (bank skew)
 constexpr int TC_NB = 4;                       // coordinate / B ring depth
-constexpr int TC_NA = 3;                       // A buffers
-constexpr int TC_DRAIN = 1024;                 // chunks per TMEM drain: 65536 * 255 * 32 < 2^31
-constexpr int SMEM2_A = 0;
-constexpr int SMEM2_B = TC_NA * TC_ABUF;
-constexpr int SMEM2_C = SMEM2_B + TC_NB * TC_BMAX;
-constexpr int SMEM2_T = SMEM2_C + TC_NB * TC_CBUF;
-constexpr int SMEM2_BAR = SMEM2_T + 16 * 256 * 8;   // full[3], empty[3], loaded[4], drain: 11 x 8 B
-constexpr int SMEM2_TOTAL = SMEM2_BAR + 128;
+constexpr int TC_DRAIN_J = 65536;              // j per TMEM drain: 65536 * 255 * 32 < 2^31
+
+// Shared-memory plan of one (TM rows x NCOL columns x JC j per chunk) configuration:
+//   A: NA buffers of 7 byte slices (TM x JC each), B ring: NB x (NCOL x JC) int8,
+//   coordinate ring NB x CBUF, lane-replicated exp table (32 KB), mbarriers.
+template <int TM, int NCOL, int JC>
+struct TcPlan {
+  static constexpr int SLICE = TM * JC;                    // bytes of one slice
+  static constexpr int ABUF = TC_NS * SLICE;               // 56 KB (TM x JC = 8192) / 28 KB (4096)
+  static constexpr int NA = ABUF > 32768 ? (NCOL > 64 ? 2 : 3) : 4;   // A buffers
+  static constexpr int BBUF = NCOL * JC;
+  static constexpr int CBUF = JC * 32 + JC * 2;            // JC x (x, y, z, pad) doubles, +16 B per 8 j (bank skew)
+  static constexpr int DRAIN = TC_DRAIN_J / JC;            // chunks per TMEM drain
+  static constexpr int A0 = 0;
+  static constexpr int B0 = NA * ABUF;
+  static constexpr int C0 = B0 + TC_NB * BBUF;
+  static constexpr int T0 = C0 + TC_NB * CBUF;
+  static constexpr int BAR = T0 + 16 * 256 * 8;          // full[NA], empty[NA], loaded[NB], drain
+  static constexpr int TOTAL = BAR + 8 * (2 * NA + TC_NB + 1) + 16;
+  static_assert(TOTAL <= 227 * 1024, "shared memory plan exceeds 227 KB");
+};
 
 // UMMA shared-memory descriptor, K-major, no swizzle (canonical ((8,m),(16B,2)):((16B,SBO),(1,LBO)))
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -46,10 +53,22 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);   // version 1 (sm_100)
 }
 
-// instruction descriptor: D s32, A u8, B s8, both K-major, N = NCOL, M = 128
-template <int NCOL>
+// instruction descriptor: D s32, A u8, B s8, both K-major, N = NCOL, M = TM
+template <int TM, int NCOL>
 __host__ __device__ constexpr uint32_t idesc_i8() {
-  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((128u >> 4) << 24);
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NCOL >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+
+// TMEM address offset of the int32 accumulator of byte slice s.
+//   TM = 128: all 128 lanes, slice s at columns [s NCOL, (s+1) NCOL).
+//   TM = 64 : an M = 64 accumulator occupies lanes 0-15 of each 32-lane sub-partition (row
+//             16 q + l -> lane 32 q + l); a second one interleaves in lanes 16-31 at the same
+//             columns.  Slices 0-3 take the low half at columns s*NCOL, slices 4-6 the high
+//             half (lane offset 16) at columns (s-4)*NCOL: 7 x 128 columns in 4 x 128.
+template <int TM, int NCOL>
+__device__ __forceinline__ uint32_t tmem_slice(int s) {
+  if constexpr (TM == 128) return (uint32_t)(s * NCOL);
+  else return (s < 4) ? (uint32_t)(s * NCOL) : ((16u << 16) | (uint32_t)((s - 4) * NCOL));
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -115,56 +134,70 @@ __global__ void coords_aos_kernel(const double* X, const double* Y, const double
 // Omega (n x ncols doubles q/4) -> int8 q per 64-j chunk in the B core-matrix layout for NCOL
 // columns: chunk t, column c, jj: t*NCOL*64 + (jj/16)*(NCOL*16) + (c/8)*128 + (c%8)*16 + jj%16
 // (0 beyond n / ncols).  The K-direction core stride (LBO) is NCOL*16 bytes.
-__global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int64_t n, int ncols, int NCOL,
+__global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int64_t n, int ncols, int NCOL, int JC,
                                 int64_t nchunks, int8_t* __restrict__ out) {
-  const int64_t total = nchunks * TC_JC * NCOL;
+  const int64_t total = nchunks * JC * NCOL;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / NCOL;
     const int c = (int)(e - j * NCOL);
-    const int64_t t = j / TC_JC;
-    const int jj = (int)(j - t * TC_JC);
+    const int64_t t = j / JC;
+    const int jj = (int)(j - t * JC);
     int q = 0;
     if (j < n && c < ncols) q = __double2int_rn(Om[j * ldo + c] * 4.0);
-    out[t * (NCOL * TC_JC) + (jj >> 4) * (NCOL * 16) + (c >> 3) * 128 + (c & 7) * 16 + (jj & 15)] = (int8_t)q;
+    out[t * (NCOL * JC) + (jj >> 4) * (NCOL * 16) + (c >> 3) * 128 + (c & 7) * 16 + (jj & 15)] = (int8_t)q;
   }
 }
 
-// Warp-specialised, barrier-free pipeline per CTA (128 rows x NCOL sample columns):
+// Warp-specialised, barrier-free pipeline per CTA (TM rows x NCOL sample columns):
 //   NPW producer warps: wait loaded[slot] (coordinates + B of the chunk landed) and empty[buf]
-//     (the MMA that last read A[buf] finished), evaluate 32/NPW rows x 8 j each, write the 7
+//     (the MMA that last read A[buf] finished), evaluate TM/(4 NPW) rows x 8 j each, write the 7
 //     byte slices to A[buf], fence.proxy.async, arrive on full[buf];
-//   1 control warp: waits full[buf], issues the 14 tcgen05.mma (M 128, N NCOL, K 32) of the
+//   1 control warp: waits full[buf], issues the 14 tcgen05.mma (M TM, N NCOL, K 32) of the
 //     chunk, commits empty[buf] (and drain on drain chunks), then refills the coordinate / B ring
 //     with cp.async tracked by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
-//   producer warps 0-3 (TMEM lanes 0-127) drain the int32 accumulators after every drain chunk.
-template <int NPW, int NCOL>
+//   producer warps 0-3 (TMEM sub-partitions 0-3) drain the int32 accumulators after every drain
+//     chunk.
+// TM = 128, NCOL <= 64 : 7 x NCOL TMEM columns.  TM = 64, NCOL = 128 : the M = 64 accumulators
+// pack two slices per TMEM column (tmem_slice), so one evaluation of K feeds 128 columns.
+template <int TM, int NPW, int NCOL, int JC>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride) {
+  using P = TcPlan<TM, NCOL, JC>;
+  constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
+  constexpr int CBUF = P::CBUF;
   constexpr int NTH = 32 * (NPW + 1);
-  constexpr int RPT = 32 / NPW;            // rows per producer thread (128 rows x 64 j / (32 NPW lanes x 8 j))
-  constexpr int BBUF = NCOL * TC_JC;       // B chunk bytes
+  constexpr int NA = P::NA;
+  constexpr int RPT = TM * G / (16 * NPW); // rows per producer thread (TM rows x JC j / (32 NPW lanes x 8 j))
+  constexpr int BBUF = P::BBUF;            // B chunk bytes
+  constexpr int LBO_A = TM * 16;           // K-direction core-matrix stride of A
   constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
-  constexpr uint32_t TMEM_COLS = NCOL == 32 ? 256 : 512;
-  constexpr uint32_t IDESC = idesc_i8<NCOL>();
+  constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL == 32) ? 256 : 512;
+  constexpr uint32_t IDESC = idesc_i8<TM, NCOL>();
+  static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
+  static_assert((TM == 128 && NCOL <= 64) || (TM == 64 && NCOL == 128), "TMEM plan");
   extern __shared__ __align__(1024) uint8_t smem[];
-  double* tab = reinterpret_cast<double*>(smem + SMEM2_T);
+  double* tab = reinterpret_cast<double*>(smem + P::T0);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t bar_full = sbase + SMEM2_BAR;            // 3
-  const uint32_t bar_empty = bar_full + 8 * TC_NA;         // 3
-  const uint32_t bar_loaded = bar_empty + 8 * TC_NA;       // 4
+  const uint32_t bar_full = sbase + P::BAR;                // NA
+  const uint32_t bar_empty = bar_full + 8 * NA;            // NA
+  const uint32_t bar_loaded = bar_empty + 8 * NA;          // NB
   const uint32_t bar_drain = bar_loaded + 8 * TC_NB;       // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SMEM2_BAR + 8 * (2 * TC_NA + TC_NB + 1));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::BAR + 8 * (2 * NA + TC_NB + 1));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t rtile = row0 + (int64_t)blockIdx.x * TC_M;
-  const int64_t ch_b = nchunks * blockIdx.y / gridDim.y, ch_e = nchunks * (blockIdx.y + 1) / gridDim.y;
+  const int64_t rtile = row0 + (int64_t)blockIdx.x * TM;
+  // j-split boundaries in 128-j units (independent of JC), so that every pass shape splits and
+  // drains at the same j and produces bit-identical sums
+  const int64_t nunits = nchunks / (128 / JC);
+  const int64_t ch_b = nunits * blockIdx.y / gridDim.y * (128 / JC);
+  const int64_t ch_e = nunits * (blockIdx.y + 1) / gridDim.y * (128 / JC);
   const int nch = (int)(ch_e - ch_b);
   const bool control = (warp == NPW);
 
   for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
   if (tid == 0) {
-    for (int b = 0; b < TC_NA; ++b) {
+    for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, NPW);
       mbar_init(bar_empty + 8 * b, 1);
     }
@@ -193,41 +226,41 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
       for (int q = 0; q < BBUF / 16 / 32; ++q) {
         const int e = lane + 32 * q;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_B + slot * TC_BMAX + e * 16),
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::B0 + slot * BBUF + e * 16),
                      "l"(Bq + t * BBUF + e * 16));
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < JC / 16; ++q) {
         const int e = lane + 32 * q;
         const int jc = e >> 1;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + SMEM2_C + slot * TC_CBUF + e * 16 +
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::C0 + slot * CBUF + e * 16 +
                                                                           (jc >> 3) * 16),
-                     "l"(reinterpret_cast<const char*>(C + t * TC_JC) + e * 16));
+                     "l"(reinterpret_cast<const char*>(C + t * JC) + e * 16));
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
     };
     prefetch(0);
     prefetch(1);
     for (int it = 0; it < nch; ++it) {
-      const int buf = it % TC_NA;
+      const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
-      mbar_wait(bar_full + 8 * buf, (it / TC_NA) & 1);
+      mbar_wait(bar_full + 8 * buf, (it / NA) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const bool first = (it % TC_DRAIN) == 0;
-      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+      const bool first = (it % P::DRAIN) == 0;
+      const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
       if (lane == 0) {
-        const uint32_t a0 = sbase + SMEM2_A + buf * TC_ABUF;
-        const uint32_t b0 = sbase + SMEM2_B + slot * TC_BMAX;
+        const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
+        const uint32_t b0 = sbase + P::B0 + slot * BBUF;
 #pragma unroll
         for (int s = 0; s < TC_NS; ++s)
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const uint64_t ad = umma_desc(a0 + s * TC_SLICE + kk * 2 * 2048, 2048, 128);
+          for (int kk = 0; kk < JC / 32; ++kk) {
+            const uint64_t ad = umma_desc(a0 + s * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
             const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + s * NCOL),
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + tmem_slice<TM, NCOL>(s)),
                 "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
           }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -238,33 +271,35 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       }
       __syncwarp();
       // slot of chunk it+2 was last used by chunk it-2: its coordinates were consumed before
-      // full(it-2) and its B by MMA(it-2) -> wait for that MMA
-      if (it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % TC_NA), ((it - 2) / TC_NA) & 1);
+      // full(it-2) and its B by MMA(it-2) -> wait for that MMA.  With NA <= 2 the producers of
+      // chunk it already waited for MMA(it-NA) before arriving on full(it), and waiting here
+      // could alias: MMA(it) commits to the same barrier and may complete its phase too.
+      if (NA > 2 && it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % NA), ((it - 2) / NA) & 1);
       prefetch(it + 2);
     }
   } else {
-    // producer: rows rs*16 + pair + k*4*NPW (k < RPT), 8 consecutive j (half h of 16-j group g)
-    const int g = warp & 3;
-    const int rs = warp >> 2;
+    // producer: rows rs*16 + pair + k*16*(NPW/G) (k < RPT), 8 consecutive j (half h of 16-j group g)
+    const int g = warp % G;
+    const int rs = warp / G;
     const int h = lane & 1;
     const int r0 = 16 * rs + (lane >> 1);
     double4 ci[RPT];
     int off[RPT];
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
-      const int r = r0 + k * 4 * NPW;
+      const int r = r0 + k * 16 * (NPW / G);
       ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
-      off[k] = g * 2048 + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
+      off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
     const double* tabl = tab + (lane & 15);
     int drains = 0;
     for (int it = 0; it < nch; ++it) {
-      const int buf = it % TC_NA;
+      const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
       mbar_wait(bar_loaded + 8 * slot, (it / TC_NB) & 1);
-      if (it >= TC_NA) mbar_wait(bar_empty + 8 * buf, ((it - TC_NA) / TC_NA) & 1);
-      const uint8_t* cb = smem + SMEM2_C + slot * TC_CBUF;
-      uint8_t* Ab = smem + SMEM2_A + buf * TC_ABUF;
+      if (it >= NA) mbar_wait(bar_empty + 8 * buf, ((it - NA) / NA) & 1);
+      const uint8_t* cb = smem + P::C0 + slot * CBUF;
+      uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
       const int jj0 = 16 * g + 8 * h;
       uint32_t lo[RPT][8], hi[RPT][8];
 #pragma unroll
@@ -287,47 +322,61 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         transpose4(hi[k][4], hi[k][5], hi[k][6], hi[k][7], w[3]);
 #pragma unroll
         for (int s = 0; s < 4; ++s)
-          *reinterpret_cast<uint2*>(Ab + s * TC_SLICE + off[k]) = make_uint2(w[0][s], w[1][s]);
+          *reinterpret_cast<uint2*>(Ab + s * P::SLICE + off[k]) = make_uint2(w[0][s], w[1][s]);
 #pragma unroll
         for (int s = 0; s < 3; ++s)
-          *reinterpret_cast<uint2*>(Ab + (s + 4) * TC_SLICE + off[k]) = make_uint2(w[2][s], w[3][s]);
+          *reinterpret_cast<uint2*>(Ab + (s + 4) * P::SLICE + off[k]) = make_uint2(w[2][s], w[3][s]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
 
-      const bool drain = ((it % TC_DRAIN) == TC_DRAIN - 1) || (it == nch - 1);
+      const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
       if (drain && warp < 4) {
         mbar_wait(bar_drain, drains & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        const int64_t i = rtile + warp * 32 + lane;
+        // TM = 128: lane l of warp w holds row 32 w + l, all 7 slices.
+        // TM = 64 : lanes l < 16 hold row 16 w + l (slices 0-3), lanes 16 + l the same row
+        //           (slices 4-6); the halves are summed with one shuffle.
+        // Both shapes sum the slices as (s0..s3 chain) + (s4..s6 chain), so the sketch is bitwise
+        // independent of the pass width.
+        const int64_t i = TM == 128 ? rtile + warp * 32 + lane : rtile + warp * 16 + (lane & 15);
+        const bool writer = TM == 128 || lane < 16;
         double* y = Yo + (i - row0) * ldy;
 #pragma unroll 1
-        for (int c0 = 0; c0 < NCOL; c0 += 32) {   // 32 columns at a time (register budget)
-          double v[32];
+        for (int c0 = 0; c0 < NCOL; c0 += 16) {   // 16 columns at a time (register budget)
+          double v[16], u[16];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = 0.0;
+          for (int c = 0; c < 16; ++c) v[c] = u[c] = 0.0;
 #pragma unroll
           for (int s = 0; s < TC_NS; ++s) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + s * NCOL + c0;
+            if (TM == 64 && s >= 4) break;
+            uint32_t r[16];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + tmem_slice<TM, NCOL>(s) + (uint32_t)c0;
             asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];\n"
                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                  "=r"(r[15])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-            const double wgt = ldexp(1.0, 8 * s - 54);   // slice weight 2^(8s) * 2^-52 * (1/4)
+            // slice weight 2^(8 sl) * 2^-52 * (1/4); at TM = 64 the high lanes hold slice s + 4
+            const int sl = (TM == 128 || lane < 16) ? s : s + 4;
+            const double wgt = sl < TC_NS ? ldexp(1.0, 8 * sl - 54) : 0.0;
+            if (TM == 128 && s >= 4) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+              for (int c = 0; c < 16; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+            }
           }
-          if (i < row1) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
+          for (int c = 0; c < 16; ++c) v[c] += (TM == 64) ? __shfl_xor_sync(0xffffffffu, v[c], 16) : u[c];
+          if (writer && i < row1) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
               if (c0 + c < ncols) y[c0 + c] = drains == 0 ? v[c] : y[c0 + c] + v[c];
           }
         }
@@ -345,22 +394,47 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 
 bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP; }
 
+int sketch_tc_pass_cols() {
+  const char* e = getenv("H2_TC_WIDE");
+  return (e && atoi(e) == 0) ? 64 : 128;
+}
+
 namespace {
-template <int NPW, int NCOL>
+template <int TM, int NPW, int NCOL, int JC>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride) {
   static bool attr = false;
+  constexpr int smem = TcPlan<TM, NCOL, JC>::TOTAL;
   if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<NPW, NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_TOTAL));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<TM, NPW, NCOL, JC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
     attr = true;
   }
-  sketch_tc_kernel<NPW, NCOL><<<grid, 32 * (NPW + 1), SMEM2_TOTAL, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
-                                                                        sstride);
+  sketch_tc_kernel<TM, NPW, NCOL, JC><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+                                                                         sstride);
+}
+
+// j-split S fills the last wave (1 CTA / SM)
+int pick_split(int tiles, int64_t nunits, int sms) {
+  int S = 1;
+  double best = 0;
+  for (int s = 1; s <= 4; ++s) {
+    if (s > 1 && nunits / s < 32) break;
+    const int64_t units = (int64_t)tiles * s;
+    const double eff = (double)units / ((double)sms * ((units + sms - 1) / sms)) - 0.01 * (s - 1);
+    if (eff > best + 1e-9) {
+      best = eff;
+      S = s;
+    }
+  }
+  return S;
 }
 }  // namespace
 
-// Omega columns are processed 64 at a time (one pass evaluates K once for up to 64 columns);
-// H2_TC_NPW selects 8 or 16 producer warps (default 16).
+// Omega columns are processed sketch_tc_pass_cols() at a time: a pass of more than 64 columns
+// runs the 64-row / 128-column kernel (K evaluated once per 128 columns), narrower passes the
+// 128-row kernel with 32 or 64 columns.  H2_TC_NPW selects 8 or 16 producer warps (default 16),
+// H2_TC_JC the j-chunk of the 128-column kernel (64 or 128, default 128).
 void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st) {
@@ -370,46 +444,54 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const char* npw_env = getenv("H2_TC_NPW");
   const int npw = (npw_env && atoi(npw_env) == 8) ? 8 : 16;   // measured (N=2^18, 32 cols): 16 -> 163 ms, 8 -> 170
-  const int64_t nchunks = (n + TC_JC - 1) / TC_JC;
-  const int64_t npad = nchunks * TC_JC;
+  const char* jc_env = getenv("H2_TC_JC");
+  const int jc_wide = (jc_env && atoi(jc_env) == 64) ? 64 : 128;
+  const int wmax = sketch_tc_pass_cols();
+  const int64_t npad = ((n + 127) / 128) * 128;   // 128-j units: every chunk shape tiles it
   const int64_t rows = row1 - row0;
-  const int tiles = div_up(rows, TC_M);
-  // j-split S fills the last wave (1 CTA / SM)
-  int S = 1;
-  {
-    double best = 0;
-    for (int s = 1; s <= 4; ++s) {
-      if (s > 1 && nchunks / s < 64) break;
-      const int64_t units = (int64_t)tiles * s;
-      const double eff = (double)units / ((double)sms * ((units + sms - 1) / sms)) - 0.01 * (s - 1);
-      if (eff > best + 1e-9) {
-        best = eff;
-        S = s;
-      }
-    }
-  }
   double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
-  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)nchunks * TC_BMAX, st));
-  double* part = S > 1 ? static_cast<double*>(cache_alloc(sizeof(double) * rows * 64 * S, st)) : nullptr;
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 128, st));
+  double* part = nullptr;
+  int64_t part_elems = 0;
   coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(X, Yc, Zc, n, npad,
                                                                                                   kp.inv, C);
   H2_CHECK_LAUNCH();
-  for (int c0 = 0; c0 < ncols; c0 += 64) {
-    const int nc = std::min(64, ncols - c0);
-    const int NCOL = nc > 32 ? 64 : 32;
-    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * TC_JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
-        Om + c0, ldo, n, nc, NCOL, nchunks, Bq);
+  for (int c0 = 0; c0 < ncols; c0 += wmax) {
+    const int nc = std::min(wmax, ncols - c0);
+    const int NCOL = nc > 64 ? 128 : nc > 32 ? 64 : 32;
+    const int TM = NCOL == 128 ? 64 : 128;
+    const int JC = NCOL == 128 ? jc_wide : 64;
+    const int64_t nchunks = npad / JC;
+    const int tiles = div_up(rows, TM);
+    // the split is chosen for the 64-row tiles of the default 128-column pass and shared by
+    // all pass shapes (bitwise identical sketches, test_tc_pass_width_bitwise)
+    const int S = pick_split(div_up(rows, 64), npad / 128, sms);
+    if (S > 1 && part_elems < rows * nc * S) {
+      if (part) cache_free(part, st);
+      part_elems = rows * nc * S;
+      part = static_cast<double*>(cache_alloc(sizeof(double) * part_elems, st));
+    }
+    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+        Om + c0, ldo, n, nc, NCOL, JC, nchunks, Bq);
     H2_CHECK_LAUNCH();
     double* yo = S > 1 ? part : Yout + c0;
     const int64_t ld = S > 1 ? nc : ldy;
     const int64_t ss = S > 1 ? rows * nc : 0;
     const dim3 grid(tiles, S);
-    if (NCOL == 64) {
-      if (npw == 8) tc_launch<8, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      else tc_launch<16, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+    if (NCOL == 128) {
+      if (JC == 64) {
+        if (npw == 8) tc_launch<64, 8, 128, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+        else tc_launch<64, 16, 128, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      } else {
+        if (npw == 8) tc_launch<64, 8, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+        else tc_launch<64, 16, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      }
+    } else if (NCOL == 64) {
+      if (npw == 8) tc_launch<128, 8, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      else tc_launch<128, 16, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
     } else {
-      if (npw == 8) tc_launch<8, 32>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      else tc_launch<16, 32>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      if (npw == 8) tc_launch<128, 8, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
+      else tc_launch<128, 16, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
     }
     H2_CHECK_LAUNCH();
     if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);

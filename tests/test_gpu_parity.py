@@ -29,13 +29,15 @@ def test_omega_matches_oracle_generator():
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("quarters", [False, True])
-def test_dense_sketch_matches_oracle(case, quarters):
+@pytest.mark.parametrize("ncols", [45, 128, 150])
+def test_dense_sketch_matches_oracle(case, quarters, ncols):
     """DMMA path (arbitrary Omega) and, for the exp kernel with the h2 Omega stream, the exact
-    int8 tensor-core path (sketch_tc.cu)."""
+    int8 tensor-core path (sketch_tc.cu): 45 columns = one 128-row / 64-column pass, 128 = one
+    64-row / 128-column pass, 150 = a 128-column pass + a ragged 22-column pass."""
     mk, kind, p, leaf, tol = CASES[case]
     X = mk()
     T = g.Tree(X, leaf)
-    Om = rng.omega_block(1, 0, 0, T.n, 0, 45)
+    Om = rng.omega_block(1, 0, 0, T.n, 0, ncols)
     if not quarters:
         Om = Om + 1e-3 * np.random.default_rng(7).standard_normal(Om.shape)   # generic values
     op = kernels.KernelOperator(kind, p, X[T.perm])
@@ -187,8 +189,21 @@ def test_deterministic_bitwise():
     assert np.array_equal(H1._export(g._lib.H2_X_D), H2._export(g._lib.H2_X_D))
 
 
+def test_tc_pass_width_bitwise(monkeypatch):
+    """The 128-column (M = 64) and 64-column (M = 128) tensor-core passes accumulate the same
+    exact integers and sum the byte slices in the same order: bit-identical sketches."""
+    X = uniform_points(20000, 3, 0)
+    T = g.Tree(X, 64)
+    Od = torch.from_numpy(rng.omega_block(1, 0, 0, T.n, 0, 128)).cuda()
+    monkeypatch.setenv("H2_TC_WIDE", "0")
+    y0 = g.dense_sketch(T, Od, ("exp", 0.2), omega_quarters=True)
+    monkeypatch.setenv("H2_TC_WIDE", "1")
+    y1 = g.dense_sketch(T, Od, ("exp", 0.2), omega_quarters=True)
+    assert torch.equal(y0, y1)
+
+
 def test_speculative_sketch_columns_bitwise(monkeypatch):
-    """Speculative 64-column tensor-core passes change how many Omega columns are
+    """Speculative 128-column tensor-core passes change how many Omega columns are
     pushed through the sketch, never the samples consumed: the build is bit-identical to one
     drawing exactly d_blk columns per updateSamples."""
     X = uniform_points(5000, 3, 0)
@@ -199,7 +214,7 @@ def test_speculative_sketch_columns_bitwise(monkeypatch):
     H1 = g.build(T, ("exp", 0.2), 1e-6, d_init=16, d_blk=16)
     assert H0.samples == H1.samples
     assert H0.stats["sketch_columns"] == H0.samples
-    assert H1.samples <= H1.stats["sketch_columns"] < H1.samples + 64
+    assert H1.samples <= H1.stats["sketch_columns"] < H1.samples + 128
     assert H1.stats["entries_sketch"] < H0.stats["entries_sketch"]
     for t in range(H0.top_depth, T.leaf_depth + 1):
         assert np.array_equal(H0.rank(t), H1.rank(t))
