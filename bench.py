@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 METRIC = "H2 build time (s) + samples used vs N at tol=1e-6"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 64 FP64 FMA/clk/SM (DFMA = DMMA pipe), 1965 MHz
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12          # FP64 pipe instructions (lane-ops) per second
-F_EVAL = 21          # FP64 pipe ops per exp-kernel entry in sketch_tc_kernel (SASS count)
+F_EVAL = 19   # FP64 pipe ops per kernel entry in sketch_tc_kernel (SASS: 6 r^2, 5 r, 7 exp, 1 fixed-point DFMA)
 INT8_DENSE_TOPS = 4500.0                            # nominal dense int8 tensor ops/s (B200, guide)
 
 

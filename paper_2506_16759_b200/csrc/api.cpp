@@ -633,7 +633,7 @@ struct Builder {
     H.n = T.n;
     H.lv.resize(Dl - top + 1);
     if (S.kind == H2_S_DENSE_KERNEL) {
-      skp = make_kernel(S.kern);
+      skp = make_kernel(S.kern, T.diam);
       spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
       spec_w = sketch_tc_pass_cols();
     }
@@ -1057,7 +1057,7 @@ h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, i
     H2_REQUIRE(ncols >= 0 && ld_omega >= ncols && ld_y >= ncols, "h2_dense_sketch: bad ncols / leading dims");
     H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ) && kern.param > 0, "h2_dense_sketch: bad kernel");
     ensure_uploaded(T);
-    launch_dense_sketch(make_kernel(kern), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
+    launch_dense_sketch(make_kernel(kern, T->diam), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
                         ld_y, (flags & H2_SKETCH_OMEGA_QUARTERS) != 0, (cudaStream_t)stream);
     return H2_OK;
   } catch (const Error& e) {

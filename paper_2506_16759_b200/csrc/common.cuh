@@ -46,13 +46,15 @@ struct KernelParams {
   int kind;
   double param;   // l (exp) or k (helmholtz)
   double inv;     // 1/l for exp
+  double rmax;    // upper bound of the scaled distance |x-y|/l over the point set (exp); 0 = unknown
 };
 
-inline KernelParams make_kernel(const h2_kernel& k) {
+inline KernelParams make_kernel(const h2_kernel& k, double diam = -1.0) {
   KernelParams p;
   p.kind = k.kind;
   p.param = k.param;
   p.inv = 1.0 / k.param;
+  p.rmax = diam >= 0 ? diam * p.inv : 0.0;
   return p;
 }
 

@@ -29,7 +29,8 @@ constexpr int TC_DRAIN_J = 65536;              // j per TMEM drain: 65536 * 255 
 
 // Shared-memory plan of one (TM rows x NCOL columns x JC j per chunk) configuration:
 //   A: NA buffers of 7 byte slices (TM x JC each), B ring: NB x (NCOL x JC) int8,
-//   coordinate ring NB x CBUF, lane-replicated exp table (32 KB), mbarriers.
+//   coordinate ring NB x CBUF, mbarriers (the 32 KB lane-replicated exp table is static shared
+//   memory: its address is an immediate of the table loads).
 template <int TM, int NCOL, int JC>
 struct TcPlan {
   static constexpr int SLICE = TM * JC;                    // bytes of one slice
@@ -42,9 +43,9 @@ struct TcPlan {
   static constexpr int B0 = NA * ABUF;
   static constexpr int C0 = B0 + TC_NB * BBUF;
   static constexpr int T0 = C0 + TC_NB * CBUF;
-  static constexpr int BAR = T0 + 16 * 256 * 8;          // full[NA], empty[NA], loaded[NB], drain
+  static constexpr int BAR = T0;                         // full[NA], empty[NA], loaded[NB], drain
   static constexpr int TOTAL = BAR + 8 * (2 * NA + TC_NB + 1) + 16;
-  static_assert(TOTAL <= 227 * 1024, "shared memory plan exceeds 227 KB");
+  static_assert(TOTAL + 16 * 256 * 8 <= 227 * 1024, "shared memory plan exceeds 227 KB");
 };
 
 // UMMA shared-memory descriptor, K-major, no swizzle (canonical ((8,m),(16B,2)):((16B,SBO),(1,LBO)))
@@ -83,18 +84,33 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
 }
 
 
-// round(exp(-|x'-y'|) * 2^52) for r2 = |x'-y'|^2 (scaled coordinates) as (lo 32, hi 20 bits).
-// r2 is clamped to [2^-1007, 490000] on its high word (integer pipe): 1/sqrt stays finite at
-// r2 = 0 (K = 1) and e^{-r} >= e^{-700} keeps the exponent arithmetic of exp_neg256 normal.
-// K is clamped below 1 - 2^-52 so that 1 + K < 2 keeps exponent 0: then the mantissa bits of
-// (1 + K) are round(K 2^52).  FP64 pipe: 6 (r2, caller) + 5 (rsqrt) + 1 + 8 (exp) + 1 = 21.
-// `tabl` = lane-replicated table (16 copies interleaved: entry j of copy l at [16 j + l]); lane l of
-// each half-warp reads copy l & 15, so the 32 random lookups of a warp are bank-conflict free.
-__device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restrict__ tabl) {
-  int hw = __double2hiint(r2);
-  hw = min(max(hw, 0x01000000), 0x411DE840);
-  r2 = __hiloint2double(hw, __double2loint(r2));
-  const double r = r2 * rsqrt_fast(r2);
+// r'^2 = |x'-y'|^2 + 2^-1000: the floor (folded into the first FMA, no extra operation) keeps
+// 1/sqrt finite at x' = y' and is below half an ulp of every r'^2 >= 2^-947.
+__device__ __forceinline__ double dist2_floor(double xi, double yi, double zi, double xj, double yj, double zj) {
+  const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
+  return fma(dz, dz, fma(dy, dy, fma(dx, dx, 9.332636185032189e-302)));   // 2^-1000
+}
+
+// m = round(exp(-r') 2^52) for r2 = r'^2 (scaled coordinates) as (lo 32, hi 21 bits).
+// Domain: r' <= 650 (host-checked: sketch_tc_supported), so n = rint(-256 r'/ln2) > -2^18 and the
+// exponent arithmetic below stays in the normal range.
+//   r' = r2 y0 (1 + e/2 + 3e^2/8), e = 1 - r2 y0^2, y0 = MUFU.RSQ64H(r2) (~2^-20): the cubic
+//       correction applied to r2 y0 directly (error 5e^3/16 ~ 2^-60);
+//   e^{-r'} = 2^(n/256) p(g), g = -r' - n ln2/256 (|g| <= ln2/512), p = degree-4 Taylor;
+//   w = T_n p + 2^52 with T_n = 2^(52 + n/256) (table 2^(52 + j/256), lane-replicated: entry j of
+//       copy l at byte 128 j + 8 l, so the 32 lookups of a warp are bank-conflict free; exponent
+//       n >> 8 added to its high word): one DFMA, one rounding = the fixed-point rounding of
+//       K 2^52;
+//   m = bits(w) - bits(2^52): the FP64 bit pattern is monotonic, so for w in [2^52, 2^53] this
+//       is exactly w - 2^52, including K -> 1 (w = 2^53, m = 2^52, slice 6 = 0x10).
+// FP64 pipe: 6 (r'^2, caller) + 5 (r') + 7 (g, p) + 1 (w) = 19.
+__device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restrict__ tab, uint32_t lane8) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double r0 = r2 * y0;
+  const double e = fma(-r0, y0, 1.0);
+  const double pc = fma(e, 0.375, 0.5);
+  const double r = fma(r0 * e, pc, r0);
   const double SH = 6755399441055744.0;
   const double t = fma(r, -369.32993046757464, SH);      // -256/ln2
   const double kf = t - SH;
@@ -104,15 +120,14 @@ __device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restric
   p = fma(p, g, 0.5);
   p = fma(p, g, 1.0);
   p = fma(p, g, 1.0);
-  const double v0 = tabl[(n & 255) << 4] * p;
-  int vh = __double2hiint(v0) + ((n >> 8) << 20);
-  int vl = __double2loint(v0);
-  if (vh >= 0x3FF00000) {   // K rounded to 1.0 (r ~ 0): use 1 - 2^-52
-    vh = 0x3FEFFFFF;
-    vl = (int)0xFFFFFFFE;
-  }
-  const double w = 1.0 + __hiloint2double(vh, vl);
-  return make_uint2((uint32_t)__double2loint(w), (uint32_t)__double2hiint(w) & 0xFFFFFu);
+  uint32_t idx;   // ((n & 255) << 7) | lane8 in one LOP3
+  asm("lop3.b32 %0, %1, 0x7F80, %2, 0xEA;" : "=r"(idx) : "r"((uint32_t)n << 7), "r"(lane8));
+  const double tv = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + idx);
+  int th;   // hi(T_j) + (n >> 8) 2^20 as SHF + LEA (the compiler's default is 3 integer operations)
+  asm("{\n .reg .s32 e;\n shr.s32 e, %1, 8;\n mad.lo.s32 %0, e, 1048576, %2;\n}\n"
+      : "=r"(th) : "r"(n), "r"(__double2hiint(tv)));
+  const double w = fma(__hiloint2double(th, __double2loint(tv)), p, 4503599627370496.0);
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)(__double2hiint(w) - 0x43300000));
 }
 
 // 4x4 byte transpose: out[s] = bytes s of (a, b, c, d)
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
   static_assert((TM == 128 && NCOL <= 64) || (TM == 64 && NCOL == 128), "TMEM plan");
   extern __shared__ __align__(1024) uint8_t smem[];
-  double* tab = reinterpret_cast<double*>(smem + P::T0);
+  __shared__ __align__(128) double tab[16 * 256];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t bar_full = sbase + P::BAR;                // NA
   const uint32_t bar_empty = bar_full + 8 * NA;            // NA
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const int nch = (int)(ch_e - ch_b);
   const bool control = (warp == NPW);
 
-  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0));
+  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + 52.0);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, NPW);
@@ -291,7 +306,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
       off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
-    const double* tabl = tab + (lane & 15);
+    const uint32_t lane8 = 8u * (lane & 15);
     int drains = 0;
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
@@ -308,7 +323,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-          const uint2 m = expk_fixed52(dist2(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z), tabl);
+          const uint2 m = expk_fixed52(dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z), tab, lane8);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
@@ -392,7 +407,9 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 
 }  // namespace
 
-bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP; }
+// exp kernel on a point set whose scaled diameter keeps n = rint(-256 r'/ln2) in the range of the
+// exponent arithmetic of expk_fixed52 (r' <= 650; K < 1e-282 there, far below the 2^-53 grid)
+bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP && kp.rmax > 0 && kp.rmax <= 650.0; }
 
 int sketch_tc_pass_cols() {
   const char* e = getenv("H2_TC_WIDE");

@@ -143,6 +143,19 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
     if (dim > 1) T.yt[i] = coord(T.perm[i], 1);
     if (dim > 2) T.zt[i] = coord(T.perm[i], 2);
   }
+  {
+    double lo[3] = {1e308, 1e308, 1e308}, hi[3] = {-1e308, -1e308, -1e308};
+    for (int64_t i = 0; i < n; ++i) {
+      const double v[3] = {T.xt[i], T.yt[i], T.zt[i]};
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], v[a]);
+        hi[a] = std::max(hi[a], v[a]);
+      }
+    }
+    T.diam = n > 0 ? std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                               (hi[2] - lo[2]) * (hi[2] - lo[2]))
+                   : 0.0;
+  }
 
   // ---- bounding boxes per depth (tree order, zero padded)
   std::vector<std::vector<BBox>> box(Dl + 1);

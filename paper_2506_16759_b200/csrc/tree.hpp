@@ -27,6 +27,7 @@ struct h2_tree {
   std::vector<int64_t> perm;                       // tree index -> original index
   std::vector<std::vector<int64_t>> begin, end;    // per depth
   std::vector<double> xt, yt, zt;                  // tree-order coordinates (zero padded to 3D)
+  double diam = 0;                                 // bounding-box diagonal of all points
   PairCSR near;                                    // leaf depth
   std::vector<PairCSR> far;                        // per depth
   std::vector<int64_t> D_off;                      // unique near pair offsets (m_s*m_b prefix)
