@@ -460,6 +460,9 @@ struct Builder {
     a.ibar = (t == T.Dl) ? T.d_iota : H.L(t + 1).d_skel.p;
     a.roff = L.d_roff.p;
     a.skel = L.d_skel.p;
+    a.max_k = L.max_k;
+    a.max_red = 0;
+    for (int c = 0; c < L.nclus; ++c) a.max_red = std::max(a.max_red, L.m[c] - L.k[c]);
     launch_id(a, st);
     timer.end();
   }

@@ -222,35 +222,86 @@ void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
 
 // ------------------------------------------------------------------------------------------
 // ID epilogue.  W row j holds column j of the factored A: R(0:k, j) in its first k entries.
-// X (m x k row-major): X(J[i], :) = e_i, X(Rhat[c], :) = T(:, c)^T, T = R11^{-1} R12 by back
-// substitution (rows k-1 -> 0, ascending inner sums, R15).  One thread per redundant column.
+// X (m x k row-major): X(J[i], :) = e_i, X(Rhat[c], :) = T(:, c)^T, T = R11^{-1} R12 (R15: back
+// substitution, rows k-1 -> 0).
+// CTA (cluster, 32 redundant columns), 256 threads; B = R12(:, cols) (k x 32) lives in shared
+// memory and is overwritten by T.  Blocked right-looking back substitution over 32-row blocks
+// (from the bottom): warp 0 solves the 32 x 32 diagonal block (lane = column, left-looking,
+// ascending j), then all threads apply the rank-32 update to the rows above.  The previous
+// version (one thread per column, serial k^2/2 loop reading T from global memory) took 5 ms
+// per launch at the top levels (32 clusters, k ~ 210).
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) id_kernel(IdArgs a) {
+constexpr int ID_CB = 32;
+__global__ void __launch_bounds__(256) id_kernel(IdArgs a) {
+  extern __shared__ double sB[];           // k x ID_CB, row stride ID_CB + 1
+  __shared__ double sD[ID_CB][ID_CB + 1];  // diagonal block R(i0:i1, i0:i1)
   const int c = blockIdx.x;
   const int m = a.m[c], k = a.k[c], d = a.d;
   const int64_t off = a.poff[c];
   const double* A = a.W + off * d;
   const int* perm = a.perm + off;
   double* X = a.X + a.xoff[c];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    double* row = X + (int64_t)perm[i] * k;
-    for (int q = 0; q < k; ++q) row[q] = (q == i) ? 1.0 : 0.0;
-    a.skel[a.roff[c] + i] = a.ibar[off + perm[i]];
-  }
-  for (int cc = threadIdx.x; cc < m - k; cc += blockDim.x) {
-    const double* r12 = A + (int64_t)(k + cc) * d;     // column k+cc of R
-    double* t = X + (int64_t)perm[k + cc] * k;          // T(:, cc) stored as a row of X
-    for (int i = k - 1; i >= 0; --i) {
-      double s = r12[i];
-      for (int j = i + 1; j < k; ++j) s -= A[(int64_t)j * d + i] * t[j];
-      t[i] = s / A[(int64_t)i * d + i];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.y == 0) {
+    for (int i = warp; i < k; i += 8) {
+      double* row = X + (int64_t)perm[i] * k;
+      for (int q = lane; q < k; q += 32) row[q] = (q == i) ? 1.0 : 0.0;
+      if (lane == 0) a.skel[a.roff[c] + i] = a.ibar[off + perm[i]];
     }
+  }
+  const int cc0 = blockIdx.y * ID_CB;
+  const int ncc = min(ID_CB, m - k - cc0);
+  if (ncc <= 0 || k == 0) return;
+  constexpr int LD = ID_CB + 1;
+  // B(i, cc) = R(i, k + cc0 + cc) = W row (k + cc0 + cc), entry i
+  for (int e = tid; e < k * ID_CB; e += 256) {
+    const int cc = e / k, i = e - cc * k;
+    sB[i * LD + cc] = cc < ncc ? A[(int64_t)(k + cc0 + cc) * d + i] : 0.0;
+  }
+  for (int i1 = k; i1 > 0; i1 -= ID_CB) {
+    const int i0 = max(0, i1 - ID_CB), nb = i1 - i0;
+    __syncthreads();
+    for (int e = tid; e < nb * nb; e += 256) {
+      const int jj = e / nb, ii = e - jj * nb;       // R(i0+ii, i0+jj) = W row i0+jj, entry i0+ii
+      sD[ii][jj] = A[(int64_t)(i0 + jj) * d + i0 + ii];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // column `lane`: t_i = (b_i - sum_{j>i, j<i1} R(i,j) t_j) / R(i,i), ascending j
+      for (int ii = nb - 1; ii >= 0; --ii) {
+        double s = sB[(i0 + ii) * LD + lane];
+        for (int jj = ii + 1; jj < nb; ++jj) s -= sD[ii][jj] * sB[(i0 + jj) * LD + lane];
+        sB[(i0 + ii) * LD + lane] = s / sD[ii][ii];
+      }
+    }
+    __syncthreads();
+    // rows r < i0: b_r -= sum_{j in [i0,i1)} R(r, j) t_j   (ascending j)
+    for (int e = tid; e < i0 * ID_CB; e += 256) {
+      const int r = e / ID_CB, cc = e - r * ID_CB;
+      double s = sB[r * LD + cc];
+      for (int jj = 0; jj < nb; ++jj) s -= A[(int64_t)(i0 + jj) * d + r] * sB[(i0 + jj) * LD + cc];
+      sB[r * LD + cc] = s;
+    }
+  }
+  __syncthreads();
+  // X(Rhat[cc0 + cc], :) = T(:, cc0 + cc)^T
+  for (int cc = warp; cc < ncc; cc += 8) {
+    double* row = X + (int64_t)perm[k + cc0 + cc] * k;
+    for (int i = lane; i < k; i += 32) row[i] = sB[i * LD + cc];
   }
 }
 
 void launch_id(const IdArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
-  id_kernel<<<a.nclusters, 128, 0, st>>>(a);
+  const int ny = std::max(1, div_up(a.max_red, ID_CB));
+  const size_t smem = sizeof(double) * (size_t)std::max(a.max_k, 1) * (ID_CB + 1);
+  H2_REQUIRE(smem <= 200 * 1024, "id_kernel: rank too large for the shared-memory T panel");
+  static bool attr = false;   // static sD + dynamic may exceed 48 KB for any k > 150
+  if (!attr) {
+    H2_CUDA(cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  id_kernel<<<dim3(a.nclusters, ny), 256, smem, st>>>(a);
   H2_CHECK_LAUNCH();
 }
 
@@ -258,15 +309,20 @@ void launch_id(const IdArgs& a, cudaStream_t st) {
 // shrink + project for columns [c0, c1):  Yp(roff+i) = Yl(poff+J[i]),
 // Op(roff+i) = Ol(poff+J[i]) + sum_cc T(i,cc) Ol(poff+Rhat[cc])   (= X^T Ol, identity rows exact)
 // ------------------------------------------------------------------------------------------
+// CTA = (cluster, 32-column block): the top levels have only 32-128 clusters, so the columns
+// are split over blockIdx.y to fill the GPU.
+constexpr int SP_CB = 32;
 __global__ void __launch_bounds__(256) shrink_project_kernel(ShrinkArgs a) {
   const int c = blockIdx.x;
   const int m = a.m[c], k = a.k[c];
   const int64_t off = a.poff[c];
   const int* perm = a.perm + off;
   const double* X = a.X + a.xoff[c];
-  const int nc = a.c1 - a.c0;
+  const int cb0 = a.c0 + blockIdx.y * SP_CB;
+  const int nc = min(SP_CB, a.c1 - cb0);
+  if (nc <= 0) return;
   for (int e = threadIdx.x; e < k * nc; e += blockDim.x) {
-    const int i = e / nc, col = a.c0 + e % nc;
+    const int i = e / nc, col = cb0 + e % nc;
     const int64_t src = off + perm[i];
     a.Yp[(a.roff[c] + i) * a.ldp + col] = a.Yl[src * a.ld + col];
     double s = a.Ol[src * a.ld + col];
@@ -280,7 +336,7 @@ __global__ void __launch_bounds__(256) shrink_project_kernel(ShrinkArgs a) {
 
 void launch_shrink_project(const ShrinkArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0 || a.c1 <= a.c0) return;
-  shrink_project_kernel<<<a.nclusters, 256, 0, st>>>(a);
+  shrink_project_kernel<<<dim3(a.nclusters, div_up(a.c1 - a.c0, SP_CB)), 256, 0, st>>>(a);
   H2_CHECK_LAUNCH();
 }
 

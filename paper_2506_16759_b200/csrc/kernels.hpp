@@ -100,6 +100,7 @@ struct IdArgs {
   const int32_t* ibar;    // Ibar_c = ibar + poff[c]
   const int64_t* roff;    // rank prefix sum of this depth
   int32_t* skel;
+  int32_t max_k, max_red; // max k, max (m - k) over the clusters (grid / shared-memory sizing)
 };
 void launch_id(const IdArgs& a, cudaStream_t st);
 

@@ -30,6 +30,57 @@ __device__ __forceinline__ uint2 expk(double r2, const double* __restrict__ tab,
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)(__double2hiint(w) - 0x43300000));
 }
 
+__device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* o) {
+  uint32_t p = __byte_perm(a, b, 0x5140), q = __byte_perm(c, d, 0x5140);
+  uint32_t r = __byte_perm(a, b, 0x7362), t = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(p, q, 0x5410);
+  o[1] = __byte_perm(p, q, 0x7632);
+  o[2] = __byte_perm(r, t, 0x5410);
+  o[3] = __byte_perm(r, t, 0x7632);
+}
+
+// evaluation + byte slicing + 7 STS.64 per 8 entries (the sketch_tc producer body, no barriers)
+template <int RPT>
+__global__ void ks(uint32_t* out, int iters, const double4* __restrict__ C) {
+  __shared__ __align__(128) double tab[16 * 256];
+  __shared__ double4 cs[128];
+  __shared__ __align__(16) uint8_t A[7 * 1024];
+  for (int e = threadIdx.x; e < 4096; e += blockDim.x) tab[e] = exp2((double)(e >> 4) / 256.0 + 52.0);
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) cs[e] = C[e];
+  __syncthreads();
+  const uint32_t lane8 = 8u * (threadIdx.x & 15);
+  double4 ci[RPT];
+  for (int k = 0; k < RPT; ++k) ci[k] = C[(threadIdx.x + 37 * k) & 127];
+  const int off = (threadIdx.x * 8) & 1023;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      uint32_t lo[8], hi[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double4 p = cs[(q + it * 8) & 127];
+        const double dx = ci[k].x - p.x, dy = ci[k].y - p.y, dz = ci[k].z - p.z;
+        const double r2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, 9.332636185032189e-302)));
+        const uint2 m = expk(r2, tab, lane8);
+        lo[q] = m.x; hi[q] = m.y;
+      }
+      uint32_t w[4][4];
+      transpose4(lo[0], lo[1], lo[2], lo[3], w[0]);
+      transpose4(lo[4], lo[5], lo[6], lo[7], w[1]);
+      transpose4(hi[0], hi[1], hi[2], hi[3], w[2]);
+      transpose4(hi[4], hi[5], hi[6], hi[7], w[3]);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) *reinterpret_cast<uint2*>(A + s * 1024 + ((off + k * 256 + it * 8) & 1023)) = make_uint2(w[0][s], w[1][s]);
+#pragma unroll
+      for (int s = 0; s < 3; ++s) *reinterpret_cast<uint2*>(A + (s + 4) * 1024 + ((off + k * 256 + it * 8) & 1023)) = make_uint2(w[2][s], w[3][s]);
+    }
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  for (int e = 0; e < 7 * 1024; e += 97) acc += A[(e + threadIdx.x) % (7 * 1024)];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 template <int ILP>
 __global__ void k(uint32_t* out, int iters, const double4* __restrict__ C) {
   __shared__ __align__(128) double tab[16 * 256];
@@ -70,6 +121,15 @@ int main() {
       printf("threads %4d ilp %2d: %.3f ms, %.1f Gentries/s, %.2f entries/clk/SM, FP64 pipe %.1f %%\n", threads, ilp, ms,
              ents / ms / 1e6, ents / (ms * 1e-3) / (148 * 1.965e9), 100.0 * 19 * ents / (ms * 1e-3) / (148 * 64 * 1.965e9));
     }
+  }
+  for (int threads : {256, 512, 1024}) {
+    const int iters = 1000;
+    ks<2><<<148, threads>>>(out, 10, C);
+    cudaEventRecord(a); ks<2><<<148, threads>>>(out, iters, C); cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    double ents = 148.0 * threads * iters * 16;
+    printf("with slicing+STS: threads %4d rpt 2: %.1f Gentries/s, %.2f entries/clk/SM, FP64 pipe %.1f %%\n", threads,
+           ents / ms / 1e6, ents / (ms * 1e-3) / (148 * 1.965e9), 100.0 * 19 * ents / (ms * 1e-3) / (148 * 64 * 1.965e9));
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
