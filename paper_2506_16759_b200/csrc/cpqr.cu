@@ -41,43 +41,79 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
 }
 
 
-// One CTA per cluster.  The panel lives in W (global, L1/L2 resident), row j = column j of A
-// (a point's d samples, contiguous).  Residual column norms are RECOMPUTED from the updated
-// trailing rows every step (R14); the norm for step i+1 is fused into the reflector update of
-// step i (one pass over the trailing panel per step).
-// SMEM: the panel is factored in shared memory (m*d*8 bytes fit) and written back to W for the
-// ID epilogue; otherwise it is factored in place in W (L1/L2 resident).
+// One CTA per cluster.  The panel lives in shared memory (rows padded to LD = d rounded up to
+// 8 doubles, LD = 8 mod 16: conflict-free) or, when too large, in W (global, L1/L2 resident).
+// Row j = column j of A (a point's d samples).  Residual column norms are RECOMPUTED from the
+// updated trailing rows every step (R14); the norm for step i+1 is fused into the reflector
+// update of step i (one pass over the trailing panel per step).
+// Work split: 8 threads per panel row (thread s of a row handles entries r = s mod 8, then a
+// 3-step shuffle reduction), NT/8 rows at a time: the dot / update / norm chains are short and
+// independent, instead of one warp per row with 5-step butterflies (latency bound: ~1 flop/clk
+// per SM).  Per step: pivot = Top2 over the per-warp candidates recorded by the previous
+// trailing update (merged by every thread in the same order); warp 0 swaps and builds the
+// reflector; barrier; trailing update; barrier.
+constexpr int CQ_TPR = 8;
+__host__ __device__ inline int cq_ld(int d) { return ((d + 7) / 8) * 8 + (((d + 7) / 8) % 2 == 0 ? 8 : 0); }
+
 template <bool SMEM, int CQ_THREADS>
 __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   constexpr int CQ_WARPS = CQ_THREADS / 32;
+  constexpr int RPP = CQ_THREADS / CQ_TPR;      // rows per pass
   extern __shared__ double smem[];
   const int c = blockIdx.x;
   const int m = a.m[c];
   const int d = a.d;
+  const int LD = SMEM ? cq_ld(d) : d;
   double* v = smem;                       // d
   double* nrm = v + d;                    // m
   int* perm = (int*)(nrm + a.max_m);      // m
-  double* spanel = nrm + a.max_m + (a.max_m + 1) / 2;   // m*d (SMEM variant)
+  double* spanel = nrm + a.max_m + (a.max_m + 1) / 2;   // m*LD (SMEM variant)
   __shared__ Top2 red[CQ_WARPS];
-  __shared__ double redd[CQ_WARPS];
-  __shared__ double s_tau, s_beta;
+  __shared__ double s_tau;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
   const int64_t off = a.poff[c];
   double* A = SMEM ? spanel : a.W + off * d;
   // copy panel rows (Y^loc rows) into the work panel
   for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
-    int64_t j = e / d;
-    A[e] = a.Y[(off + j) * a.ldy + (e - j * d)];
+    const int64_t j = e / d;
+    A[j * LD + (e - j * d)] = a.Y[(off + j) * a.ldy + (e - j * d)];
   }
+  for (int j = threadIdx.x; j < m; j += CQ_THREADS) perm[j] = j;
   __syncthreads();
-  for (int j = warp; j < m; j += CQ_WARPS) {
-    double s = 0.0;
-    for (int r = lane; r < d; r += 32) s = fma(A[(int64_t)j * d + r], A[(int64_t)j * d + r], s);
-    s = warp_sum(s);
-    if (lane == 0) {
-      nrm[j] = sqrt(s);
-      perm[j] = j;
+  auto row_sum = [&](double x) {   // sum over the 8 threads of a row (fixed order)
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    return x;
+  };
+  auto warp_best = [&](Top2 t) {    // Top2 over the 4 rows of a warp (lanes of a row agree)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      Top2 u;
+      u.v = __shfl_xor_sync(0xffffffffu, t.v, o);
+      u.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+      u.s = __shfl_xor_sync(0xffffffffu, t.s, o);
+      t = top2_merge(t, u);
     }
+    return t;
+  };
+  {
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    for (int j0 = 0; j0 < m; j0 += RPP) {
+      const int j = j0 + rloc;
+      double q = 0.0;
+      if (j < m)
+        for (int r = sub; r < d; r += CQ_TPR) q = fma(A[(int64_t)j * LD + r], A[(int64_t)j * LD + r], q);
+      q = row_sum(q);
+      if (j < m) {
+        const double nj = sqrt(q);
+        if (sub == 0) nrm[j] = nj;
+        loc = top2_merge(loc, Top2{nj, j, -1.0});
+      }
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red[warp] = loc;
   }
   __syncthreads();
   const int kfull = min(d, m);
@@ -85,19 +121,9 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   double min_gap = INFINITY, margin = INFINITY;
   int k = 0;
   for (int i = 0;; ++i) {
-    // ---- pivot: largest recomputed residual norm among columns i..m-1
-    Top2 t{-1.0, 0x7fffffff, -1.0};
-    for (int j = i + threadIdx.x; j < m; j += CQ_THREADS) t = top2_merge(t, Top2{nrm[j], j, -1.0});
+    // every warp merges the per-warp candidates with one butterfly (same result in all threads)
+    Top2 t = lane < CQ_WARPS ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
     t = warp_top2(t);
-    if (lane == 0) red[warp] = t;
-    __syncthreads();
-    if (warp == 0) {
-      Top2 u = lane < CQ_WARPS ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
-      u = warp_top2(u);
-      if (lane == 0) red[0] = u;
-    }
-    __syncthreads();
-    t = red[0];
     if (i >= m) break;
     // truncation margin of every decision taken (R13); no decision exists at i = min(d, m)
     if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
@@ -107,79 +133,82 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     }
     if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
     const int p = t.i;
-    __syncthreads();
-    // ---- swap rows i and p of the panel (columns of A)
-    if (p != i) {
-      for (int r = threadIdx.x; r < d; r += CQ_THREADS) {
-        double x = A[(int64_t)i * d + r];
-        A[(int64_t)i * d + r] = A[(int64_t)p * d + r];
-        A[(int64_t)p * d + r] = x;
+    double* Ai = A + (int64_t)i * LD;
+    if (warp == 0) {
+      // ---- swap rows i and p of the panel (columns of A)
+      if (p != i) {
+        double* Ap = A + (int64_t)p * LD;
+        for (int r = lane; r < d; r += 32) {
+          const double x = Ai[r];
+          Ai[r] = Ap[r];
+          Ap[r] = x;
+        }
+        if (lane == 0) {
+          const int q = perm[i];
+          perm[i] = perm[p];
+          perm[p] = q;
+          const double x = nrm[i];
+          nrm[i] = nrm[p];
+          nrm[p] = x;
+        }
+        __syncwarp();
       }
-      if (threadIdx.x == 0) {
-        int q = perm[i];
-        perm[i] = perm[p];
-        perm[p] = q;
-        double x = nrm[i];
-        nrm[i] = nrm[p];
-        nrm[p] = x;
-      }
-    }
-    __syncthreads();
-    // ---- Householder reflector of A(i:d, i), LAPACK dlarfg convention
-    double* Ai = A + (int64_t)i * d;
-    double s = 0.0;
-    for (int r = i + 1 + threadIdx.x; r < d; r += CQ_THREADS) s = fma(Ai[r], Ai[r], s);
-    s = warp_sum(s);
-    if (lane == 0) redd[warp] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+      // ---- Householder reflector of A(i:d, i), LAPACK dlarfg convention
       double x2 = 0.0;
-      for (int w = 0; w < CQ_WARPS; ++w) x2 += redd[w];
-      double alpha = Ai[i];
-      double xnorm = sqrt(x2);
+      for (int r = i + 1 + lane; r < d; r += 32) x2 = fma(Ai[r], Ai[r], x2);
+      x2 = warp_sum(x2);
+      const double alpha = Ai[i];
+      const double xnorm = sqrt(x2);
       double tau, beta;
       if (xnorm == 0.0) {
         tau = 0.0;
         beta = alpha;
       } else {
-        double h = hypot(alpha, xnorm);
+        const double h = hypot(alpha, xnorm);
         beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
         tau = (beta - alpha) / beta;
       }
-      s_tau = tau;
-      s_beta = beta;
-      v[i] = alpha - beta;   // scale denominator, replaced by 1 below
-    }
-    __syncthreads();
-    const double tau = s_tau;
-    {
-      const double den = v[i];
-      for (int r = i + 1 + threadIdx.x; r < d; r += CQ_THREADS) {
+      const double den = alpha - beta;
+      __syncwarp();
+      for (int r = i + 1 + lane; r < d; r += 32) {
         v[r] = tau != 0.0 ? Ai[r] / den : 0.0;
         Ai[r] = 0.0;
       }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      v[i] = 1.0;
-      Ai[i] = s_beta;
-    }
-    __syncthreads();
-    // ---- trailing update of rows j > i (columns of A) + next residual norms
-    for (int j = i + 1 + warp; j < m; j += CQ_WARPS) {
-      double* Aj = A + (int64_t)j * d;
-      double w = 0.0;
-      for (int r = i + lane; r < d; r += 32) w = fma(v[r], Aj[r], w);
-      w = warp_sum(w) * tau;
-      double q = 0.0;
-      for (int r = i + lane; r < d; r += 32) {
-        double x = fma(-w, v[r], Aj[r]);
-        Aj[r] = x;
-        if (r > i) q = fma(x, x, q);
+      if (lane == 0) {
+        v[i] = 1.0;
+        Ai[i] = beta;
+        s_tau = tau;
       }
-      q = warp_sum(q);
-      if (lane == 0) nrm[j] = sqrt(q);
     }
+    __syncthreads();
+    const double tau = s_tau;
+    // ---- trailing update of rows j > i (columns of A) + next residual norms + local pivot
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    const int r0 = i + ((sub - i) & (CQ_TPR - 1));   // first r >= i with r = sub mod 8
+    for (int j0 = i + 1; j0 < m; j0 += RPP) {
+      const int j = j0 + rloc;
+      const bool act = j < m;
+      double* Aj = A + (int64_t)(act ? j : i) * LD;
+      double w = 0.0;
+      if (act)
+        for (int r = r0; r < d; r += CQ_TPR) w = fma(v[r], Aj[r], w);
+      w = row_sum(w) * tau;
+      double q = 0.0;
+      if (act)
+        for (int r = r0; r < d; r += CQ_TPR) {
+          const double x = fma(-w, v[r], Aj[r]);
+          Aj[r] = x;
+          if (r > i) q = fma(x, x, q);
+        }
+      q = row_sum(q);
+      if (act) {
+        const double nj = sqrt(q);
+        if (sub == 0) nrm[j] = nj;
+        loc = top2_merge(loc, Top2{nj, j, -1.0});
+      }
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red[warp] = loc;
     __syncthreads();
     k = i + 1;
   }
@@ -187,7 +216,10 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   for (int j = threadIdx.x; j < m; j += CQ_THREADS) a.perm[off + j] = perm[j];
   if (SMEM) {
     double* Wc = a.W + off * d;
-    for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) Wc[e] = A[e];
+    for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
+      const int64_t j = e / d;
+      Wc[e] = A[j * LD + (e - j * d)];
+    }
   }
   if (threadIdx.x == 0) {
     a.k[c] = k;
@@ -206,15 +238,15 @@ static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
 void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
   size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
-  size_t panel = sizeof(double) * (size_t)a.max_m * a.d;
-  // large panels (upper levels: few clusters, m up to ~1000) get 1024 threads per panel
-  const bool big = (size_t)a.max_m * a.d >= 32768;
+  size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
+  // rows per pass = threads / 8 (32 or 64); 512 threads once a panel has more than 32 rows
+  const bool big = a.max_m > 32;
   if (sm + panel <= 200 * 1024) {
     sm += panel;
-    if (big) cpqr_launch<true, 1024>(a, sm, st);
+    if (big) cpqr_launch<true, 512>(a, sm, st);
     else cpqr_launch<true, 256>(a, sm, st);
   } else {
-    if (big) cpqr_launch<false, 1024>(a, sm, st);
+    if (big) cpqr_launch<false, 512>(a, sm, st);
     else cpqr_launch<false, 256>(a, sm, st);
   }
   H2_CHECK_LAUNCH();
