@@ -75,111 +75,122 @@ void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* r
 
 // ------------------------------------------------------------------------------------------
 // BSR product  Y(rows of s) += alpha * sum_{b} Blk(s,b) * Om(rows of b)
-// CTA = (row cluster s, 64-row tile, 32-column tile); 256 threads, each 8 accumulators
-// (row r = tid/4, columns 8*(tid%4)..+7).  Partners in CSR (ascending) order, k ascending
-// inside a block: the accumulation order is fixed -> deterministic, no atomics (L385).
-// Blocks are stored once per unordered pair; (s,b) with s != us[u] reads the transpose.
+// CTA = (row cluster s, 64-row tile, CW-column tile); warp (wr, wc) owns rows 16wr..16wr+15 x
+// columns 32wc..32wc+31 (2 x 4 DMMA m8n8k4 tiles, 16 accumulators per lane).  Partners in CSR
+// (ascending) order, k ascending inside a block: the accumulation order is fixed ->
+// deterministic, no atomics (L385).  Blocks are stored once per unordered pair; (s,b) with
+// s != us[u] reads the stored block transposed.
+// The (partner, 32-deep k-slab) sequence streams through a BSR_NS-stage cp.async ring in shared
+// memory (global -> shared without register staging, zero fill at ragged edges): the loads of
+// slab it+NS-1 are in flight while slab it is multiplied.  The block slab is stored in its
+// stored orientation (row-major [64][36] for direct, [32][68] for transposed: padded,
+// 16-byte rows) and the DMMA A fragments read it accordingly.
 // ------------------------------------------------------------------------------------------
-// DMMA tiling: CTA = 4*(CW/32) warps = 64 rows x CW columns; warp (wr, wc) owns rows
-// 16wr..16wr+15 (2 m-blocks) x columns 32wc..32wc+31 (4 n-blocks): 16 accumulators / lane.
-// Partner blocks stream through shared memory in 32-deep k-slabs (each block entry is read
-// once per CW columns); row strides = 4 mod 16 doubles keep the fragment loads conflict free.
-constexpr int BT_R = 64, BT_K = 32, BT_LD = 36;
+constexpr int BT_R = 64, BT_K = 32, BSR_NS = 2;
+constexpr int BT_LDD = 36;   // direct slab row stride (doubles)
+constexpr int BT_LDT = 68;   // transposed slab row stride
+constexpr int BT_ASZ = BT_R * BT_LDD > BT_K * BT_LDT ? BT_R * BT_LDD : BT_K * BT_LDT;
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
 
 template <int CW>
 __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
   constexpr int NT = 4 * CW;           // threads
   constexpr int LDB = CW + 4;
-  constexpr int AE = BT_R * BT_K / NT; // A-slab elements per thread
-  constexpr int BE = BT_K * CW / NT;   // B-slab elements per thread
-  __shared__ __align__(16) double sA[BT_R * BT_LD];
-  __shared__ __align__(16) double sB[BT_K * LDB];
+  constexpr int BSZ = BT_K * LDB;
+  extern __shared__ __align__(16) double bsm[];   // NS x (A slab + B slab)
+  __shared__ int st_nk[BSR_NS], st_dir[BSR_NS];
   const int s = blockIdx.x;
   const int ms = a.cnt[s];
   const int r0 = blockIdx.y * BT_R;
   const int cb = a.c0 + blockIdx.z * CW;
   const int nc = min(CW, a.c0 + a.ncols - cb);
   if (r0 >= ms || nc <= 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
+  if (e0 == e1) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 3, wc = warp >> 2;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bsm);
+  // loader state: next (partner, k0) to load
+  int le = e0, lk = 0;
+  auto load_next = [&](int buf) {
+    if (le >= e1) return;
+    const int b = a.idx[le];
+    const int u = a.uidx[le];
+    const int mb = a.cnt[b];
+    const bool direct = (a.us[u] == s);
+    const double* blk = a.blk + a.blk_off[u];
+    const double* om = a.Om + a.ooff[b] * a.ldo + cb;
+    const int nk = min(BT_K, mb - lk);
+    const uint32_t sa = sbase + (uint32_t)(buf * (BT_ASZ + BSZ)) * 8u;
+    const uint32_t sb = sa + (uint32_t)BT_ASZ * 8u;
+    if (direct) {
+      // rows r of s (r0 + r < ms), entries kk of the slab: blk[(r0 + r) * mb + lk + kk]
+#pragma unroll 4
+      for (int q = tid; q < BT_R * BT_K; q += NT) {
+        const int r = q >> 5, kk = q & 31;
+        const bool ok = (r0 + r < ms) && (kk < nk);
+        cp_async8(sa + (uint32_t)(r * BT_LDD + kk) * 8u, ok ? blk + (int64_t)(r0 + r) * mb + lk + kk : blk, ok);
+      }
+    } else {
+      // stored block is b x s: entry (kk, r) at blk[(lk + kk) * ms + r0 + r]
+#pragma unroll 4
+      for (int q = tid; q < BT_R * BT_K; q += NT) {
+        const int kk = q >> 6, r = q & 63;
+        const bool ok = (r0 + r < ms) && (kk < nk);
+        cp_async8(sa + (uint32_t)(kk * BT_LDT + r) * 8u, ok ? blk + (int64_t)(lk + kk) * ms + r0 + r : blk, ok);
+      }
+    }
+#pragma unroll 4
+    for (int q = tid; q < BT_K * CW; q += NT) {
+      const int kk = q / CW, c = q % CW;
+      const bool ok = (kk < nk) && (c < nc);
+      cp_async8(sb + (uint32_t)(kk * LDB + c) * 8u, ok ? om + (int64_t)(lk + kk) * a.ldo + c : om, ok);
+    }
+    if (tid == 0) {
+      st_nk[buf] = nk;
+      st_dir[buf] = direct ? 1 : 0;
+    }
+    lk += BT_K;
+    if (lk >= mb) {
+      ++le;
+      lk = 0;
+    }
+  };
   double acc[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // the (partner, k-slab) sequence, with the next slab prefetched into registers while the
-  // current one is multiplied (global loads overlap the DMMAs)
-  const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
-  if (e0 == e1) return;
-  int e = e0, k0 = 0;
-  double ra[AE], rb[BE];
-  int nk_cur = 0;
-  auto load = [&](int ee, int kk0, double* xa, double* xb) -> int {
-    const int b = a.idx[ee];
-    const int u = a.uidx[ee];
-    const int mb = a.cnt[b];
-    const bool direct = (a.us[u] == s);
-    const double* blk = a.blk + a.blk_off[u];
-    const double* om = a.Om + a.ooff[b] * a.ldo + cb;
-    const int nk = min(BT_K, mb - kk0);
+  int nitems = 0;
+  for (int e = e0; e < e1; ++e) nitems += (a.cnt[a.idx[e]] + BT_K - 1) / BT_K;
 #pragma unroll
-    for (int q = 0; q < AE; ++q) {
-      const int t = threadIdx.x + q * NT;
-      int r, kk;
-      if (direct) {
-        r = t >> 5;
-        kk = t & 31;
-      } else {
-        kk = t >> 6;
-        r = t & 63;
-      }
-      xa[q] = (r0 + r < ms && kk < nk)
-                  ? (direct ? blk[(int64_t)(r0 + r) * mb + kk0 + kk] : blk[(int64_t)(kk0 + kk) * ms + r0 + r])
-                  : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < BE; ++q) {
-      const int t = threadIdx.x + q * NT;
-      const int kk = t / CW, c = t % CW;
-      xb[q] = (kk < nk && c < nc) ? om[(int64_t)(kk0 + kk) * a.ldo + c] : 0.0;
-    }
-    return nk;
-  };
-  bool cur_direct = (a.us[a.uidx[e]] == s);
-  nk_cur = load(e, k0, ra, rb);
-  while (true) {
+  for (int q = 0; q < BSR_NS - 1; ++q) {
+    load_next(q);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int it = 0; it < nitems; ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(BSR_NS - 2));
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < AE; ++q) {
-      const int t = threadIdx.x + q * NT;
-      const int r = cur_direct ? (t >> 5) : (t & 63);
-      const int kk = cur_direct ? (t & 31) : (t >> 6);
-      sA[r * BT_LD + kk] = ra[q];
-    }
-#pragma unroll
-    for (int q = 0; q < BE; ++q) {
-      const int t = threadIdx.x + q * NT;
-      sB[(t / CW) * LDB + (t % CW)] = rb[q];
-    }
-    __syncthreads();
-    const int nk = nk_cur;
-    // advance to the next slab and prefetch it
-    k0 += BT_K;
-    if (k0 >= a.cnt[a.idx[e]]) {
-      ++e;
-      k0 = 0;
-    }
-    const bool more = e < e1;
-    if (more) {
-      cur_direct = (a.us[a.uidx[e]] == s);
-      nk_cur = load(e, k0, ra, rb);
-    }
+    // the buffer of slab it-1 was consumed before this barrier: refill it with slab it+NS-1
+    load_next((it + BSR_NS - 1) % BSR_NS);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int buf = it % BSR_NS;
+    const double* sA = bsm + buf * (BT_ASZ + BSZ);
+    const double* sB = sA + BT_ASZ;
+    const int nk = st_nk[buf];
+    const bool direct = st_dir[buf] != 0;
     const int ksteps = (nk + 3) >> 2;
     for (int ks = 0; ks < ksteps; ++ks) {
       const int kk = ks * 4 + (lane & 3);
       double af[2], bf[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = sA[(wr * 16 + i * 8 + (lane >> 2)) * BT_LD + kk];
+      for (int i = 0; i < 2; ++i) {
+        const int r = wr * 16 + i * 8 + (lane >> 2);
+        af[i] = direct ? sA[r * BT_LDD + kk] : sA[kk * BT_LDT + r];
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = sB[kk * LDB + wc * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
@@ -187,8 +198,8 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    if (!more) break;
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = r0 + wr * 16 + i * 8 + (lane >> 2);
@@ -205,12 +216,20 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
 
 static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
+  static bool attr = false;
+  constexpr size_t sm32 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (32 + 4));
+  constexpr size_t sm64 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (64 + 4));
+  if (!attr) {
+    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32));
+    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
+    attr = true;
+  }
   if (a.ncols > 32) {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 64));
-    bsr_kernel<64><<<grid, 256, 0, st>>>(a, alpha);
+    bsr_kernel<64><<<grid, 256, sm64, st>>>(a, alpha);
   } else {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 32));
-    bsr_kernel<32><<<grid, 128, 0, st>>>(a, alpha);
+    bsr_kernel<32><<<grid, 128, sm32, st>>>(a, alpha);
   }
   H2_CHECK_LAUNCH();
 }
