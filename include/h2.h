@@ -197,11 +197,51 @@ typedef struct {
   double t_total_ms;
 } h2_build_stats;
 
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU (§IV-B: "the batch count becomes roughly the number
+ * of nodes per level divided by the number of GPUs").  One process per GPU; every rank calls
+ * h2_build_dist collectively with the same tree, operators and options.  Cluster c of depth t
+ * (2^t clusters) is owned by rank floor(c * nranks / 2^t): contiguous, subtree-aligned ranges.
+ * A rank evaluates the sketch rows of its leaves (Omega is regenerated everywhere), the D / B
+ * blocks touching its clusters, and the BSR / CPQR-ID / shrink-upsweep of its clusters; per
+ * level it all-gathers ranks, skeleton indices I~ and the next level's Omega rows (the
+ * exchange step of the north star).  The result is bitwise the same as a one-GPU build.
+ * The communicator is supplied by the caller (torch.distributed / NCCL in the Python binding):
+ *   allgatherv(ctx, buf, counts, displs, stream): buf is device memory; on entry the byte
+ *   segment [displs[r], displs[r] + counts[r]) holds rank r's data on rank r; on return every
+ *   rank holds every segment.  counts/displs are host arrays of nranks entries.  Stream-ordered
+ *   on `stream`.  Return 0 on success (else the build fails with H2_ERR_CALLBACK).
+ * ------------------------------------------------------------------------------------- */
+typedef int (*h2_allgatherv_fn)(void* ctx, void* buf, const int64_t* counts, const int64_t* displs,
+                                void* stream);
+typedef struct {
+  int32_t rank, nranks;
+  h2_allgatherv_fn allgatherv;
+  void* ctx;
+} h2_comm;
+
+/* Owned cluster range [*begin, *end) of `rank` among `nranks` at a depth with n_clusters
+ * clusters (host logic, no device).  Errors: INVALID_ARG. */
+h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end);
+
 /* Algorithm 1 on the current device.  tree: from h2_tree_build.  tol >= 0.
  * sketch/entry: operators (see above).  stats may be NULL.  Errors: INVALID_ARG, OOM, CUDA,
  * CALLBACK, NOT_CONVERGED, NONFINITE; *out = NULL on error. */
 h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                    const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats);
+
+/* h2_build over a communicator (comm NULL or nranks 1: same as h2_build).  The returned matrix
+ * holds this rank's bases, the blocks touching its clusters, and every rank / skeleton index;
+ * h2_matrix_allgather completes it on every rank (needed before h2_matvec / h2_export of the
+ * bases and blocks, which fail with INVALID_ARG on a partial matrix).  nranks must be a power
+ * of two <= 2^top_depth (subtree-aligned ownership); H2 + low-rank operators are single-GPU
+ * only (INVALID_ARG). */
+h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                        const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                        h2_build_stats* stats);
+/* Collective: all-gather bases X, certificates, B and D so that every rank holds the full
+ * matrix (segments by owner of the cluster / of the stored block's row cluster). */
+h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream);
 
 /* y = alpha * K_H * x + beta * y for ncols right-hand sides (H^2 matvec: upward pass, couplings,
  * downward pass, dense leaves).  x, y: dev, tree-order rows, row-major with leading dims

@@ -77,6 +77,13 @@ class h2_build_stats(C.Structure):
                 ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double)]
 
 
+ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)
+
+
+class h2_comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("allgatherv", ALLGATHERV_FN), ("ctx", C.c_void_p)]
+
+
 # every symbol include/h2.h declares, with its ctypes signature
 _P = C.c_void_p
 SIGNATURES = {
@@ -89,6 +96,10 @@ SIGNATURES = {
     "h2_build_opts_default": (None, [C.POINTER(h2_build_opts)]),
     "h2_build": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts), _P,
                            C.POINTER(_P), C.POINTER(h2_build_stats)]),
+    "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
+                                C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
+    "h2_matrix_allgather": (C.c_int, [_P, C.POINTER(h2_comm), _P]),
+    "h2_dist_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "h2_matvec": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P]),
     "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64,
                                   C.c_int32, _P]),

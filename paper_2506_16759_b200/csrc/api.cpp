@@ -96,6 +96,8 @@ struct Level {
 struct h2_matrix {
   std::shared_ptr<h2_tree> tree;
   int top = 0, Dl = 0;
+  int nranks = 1, rank = 0;   // built with a communicator: rank owns a subtree range per depth
+  bool partial = false;       // true until h2_matrix_allgather completed every rank's copy
   int64_t n = 0;
   std::vector<Level> lv;   // index t - top
   DArr<double> D;
@@ -175,6 +177,38 @@ struct Panel {
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                  double beta, cudaStream_t st);
 
+// Cluster ownership under a communicator (S§8(e)): cluster c of depth t (2^t clusters) belongs
+// to rank floor(c P / 2^t).  Ranges are contiguous and subtree-aligned (the children of an owned
+// cluster are owned), so every per-cluster array in cluster order has one contiguous segment
+// per rank and all-gathers are single in-place allgatherv calls.
+inline int own_begin(int t, int r, int P) {
+  const int64_t n = int64_t(1) << t;
+  return (int)((r * n + P - 1) / P);
+}
+
+// in-place all-gather of per-rank byte segments through the caller's communicator
+void comm_allgather(const h2_comm* comm, void* base, const std::vector<int64_t>& counts,
+                    const std::vector<int64_t>& displs, cudaStream_t st) {
+  int64_t tot = 0;
+  for (int64_t c : counts) tot += c;
+  if (tot == 0) return;
+  const int rc = comm->allgatherv(comm->ctx, base, counts.data(), displs.data(), st);
+  if (rc != 0) throw Error(H2_ERR_CALLBACK, "communicator allgatherv returned " + std::to_string(rc));
+}
+
+// all-gather of a per-cluster array of depth t: element offsets off(c), c in [0, 2^t]
+template <class F>
+void comm_allgather_clusters(const h2_comm* comm, void* base, size_t es, int t, F off, cudaStream_t st) {
+  const int P = comm->nranks;
+  std::vector<int64_t> cnt(P), dsp(P);
+  for (int r = 0; r < P; ++r) {
+    const int64_t a = off(own_begin(t, r, P)), b = off(own_begin(t, r + 1, P));
+    dsp[r] = a * (int64_t)es;
+    cnt[r] = (b - a) * (int64_t)es;
+  }
+  comm_allgather(comm, base, cnt, dsp, st);
+}
+
 struct Builder {
   const h2_tree& T;
   const h2_sketch& S;
@@ -191,10 +225,75 @@ struct Builder {
   DArr<double> W;               // CPQR workspace
   PhaseTimer timer;
   int64_t entries_sketch = 0;
+  const h2_comm* comm = nullptr;   // NULL: one GPU
+  int P = 1, R = 0;
+  DArr<double> leaf_part;          // per-leaf sums of squares of the current draw
 
   Builder(const h2_tree& t, const h2_sketch& s, const h2_entry& e, double tl, const h2_build_opts& op,
-          cudaStream_t stream, h2_matrix& h)
-      : T(t), S(s), E(e), tol(tl), o(op), st(stream), H(h), timer(stream) {}
+          cudaStream_t stream, h2_matrix& h, const h2_comm* cm)
+      : T(t), S(s), E(e), tol(tl), o(op), st(stream), H(h), timer(stream), comm(cm) {
+    if (comm && comm->nranks > 1) {
+      P = comm->nranks;
+      R = comm->rank;
+    } else {
+      comm = nullptr;
+    }
+  }
+  // owned clusters [cb(t), ce(t)) of depth t; owned leaf rows [row_b, row_e)
+  int cb(int t) const { return own_begin(t, R, P); }
+  int ce(int t) const { return own_begin(t, R + 1, P); }
+  int64_t leaf_row(int c) const { return c < (1 << T.Dl) ? T.begin[T.Dl][c] : T.n; }
+  int64_t row_b() const { return leaf_row(cb(T.Dl)); }
+  int64_t row_e() const { return leaf_row(ce(T.Dl)); }
+
+  // unique pairs (us[u], ub[u]) with an owned endpoint (both orientations of every block a
+  // BSR row of this rank reads); NULL list = all pairs (one GPU)
+  std::vector<int32_t> owned_pairs(const PairCSR& F, int t) const {
+    std::vector<int32_t> l;
+    for (int64_t u = 0; u < F.nuniq(); ++u) {
+      const int a = F.us[u], b = F.ub[u];
+      if ((a >= cb(t) && a < ce(t)) || (b >= cb(t) && b < ce(t))) l.push_back((int32_t)u);
+    }
+    return l;
+  }
+
+  // all-gather rows [roff_r, roff_{r+1}) (per rank) of a row-major panel, columns [0, ncols)
+  void allgather_rows(double* p, int64_t ld, int ncols, const std::vector<int64_t>& rowb, int64_t nrows) {
+    if (!comm || ncols <= 0) return;
+    std::vector<int64_t> cnt(P), dsp(P);
+    if (ld == ncols) {
+      for (int r = 0; r < P; ++r) {
+        dsp[r] = rowb[r] * ld * 8;
+        cnt[r] = (rowb[r + 1] - rowb[r]) * ld * 8;
+      }
+      comm_allgather(comm, p, cnt, dsp, st);
+      return;
+    }
+    DArr<double> pk;   // packed rows x ncols
+    pk.alloc(std::max<int64_t>(nrows, 1) * ncols, st);
+    const int64_t r0 = rowb[R], r1 = rowb[R + 1];
+    if (r1 > r0)
+      H2_CUDA(cudaMemcpy2DAsync(pk.p + r0 * ncols, ncols * 8, p + r0 * ld, ld * 8, (size_t)ncols * 8, r1 - r0,
+                                cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < P; ++r) {
+      dsp[r] = rowb[r] * ncols * 8;
+      cnt[r] = (rowb[r + 1] - rowb[r]) * ncols * 8;
+    }
+    comm_allgather(comm, pk.p, cnt, dsp, st);
+    if (nrows > 0)
+      H2_CUDA(cudaMemcpy2DAsync(p, ld * 8, pk.p, ncols * 8, (size_t)ncols * 8, nrows, cudaMemcpyDeviceToDevice, st));
+  }
+  // rows of the panel built by shrink(u): skeleton rows of depth u in roff order
+  void allgather_skel_rows(int u, double* p, int64_t ld, int ncols) {
+    if (!comm) return;
+    const Level& L = H.L(u);
+    std::vector<int64_t> rowb(P + 1);
+    for (int r = 0; r <= P; ++r) {
+      const int c = own_begin(u, r, P);
+      rowb[r] = c < L.nclus ? L.roff[c] : L.rtot;
+    }
+    allgather_rows(p, ld, ncols, rowb, L.rtot);
+  }
 
   // panel leading dimension: d_max when the panel is small, else the needed width + 2 blocks
   int64_t ld_for(int64_t rows, int dneed) const {
@@ -234,7 +333,8 @@ struct Builder {
     launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
     timer.end();
     timer.begin(H2_PH_SKETCH);
-    launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Od, ld, nc, Yd, ld, true, st);
+    // this rank's leaf rows only (Omega is regenerated for all rows on every rank)
+    launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, true, st);
     entries_sketch += T.n * T.n * (int64_t)div_up(nc, spec_on ? spec_w : 64);
     sketch_columns += nc;
   }
@@ -277,13 +377,13 @@ struct Builder {
       } else {
         h2_sketch_req rq{};
         rq.n = T.n;
-        rq.row_begin = 0;
-        rq.row_end = T.n;
+        rq.row_begin = row_b();
+        rq.row_end = row_e();
         rq.col0 = c0;
         rq.ncols = nc;
         rq.omega = Od;
         rq.ld_omega = ld;
-        rq.y = Yd;
+        rq.y = Yd + row_b() * ld;
         rq.ld_y = ld;
         rq.stream = st;
         int rc = S.fn(S.ctx, &rq);
@@ -292,7 +392,13 @@ struct Builder {
     }
     timer.end();
     timer.begin(H2_PH_MISC);
-    launch_sumsq(Yd, T.n, ld, 0, nc, sumsq_scratch.p, sumsq_acc.p, nonfinite.p, st);
+    // R10: ||Y||_F^2 accumulated over the draws; per-leaf partials (owned leaves), all-gathered,
+    // summed in leaf order: bitwise the same for any number of GPUs
+    const int nleaf = 1 << T.Dl;
+    if (leaf_part.n < nleaf) leaf_part.alloc(nleaf, st);
+    launch_sumsq_leaf(Yd, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, nc, leaf_part.p, st);
+    if (comm) comm_allgather_clusters(comm, leaf_part.p, 8, T.Dl, [](int c) { return (int64_t)c; }, st);
+    launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
     timer.end();
   }
 
@@ -342,7 +448,8 @@ struct Builder {
     a.c0 = 0;
     a.ncols = nc;
     if (t == T.Dl) {
-      a.nclusters = 1 << T.Dl;
+      a.c_begin = cb(T.Dl);
+      a.nclusters = ce(T.Dl) - cb(T.Dl);
       a.max_rows = H.L(T.Dl).max_m;
       a.yoff = a.ooff = T.d_leaf_begin;
       a.cnt = T.d_leaf_size;
@@ -354,7 +461,8 @@ struct Builder {
       a.blk = H.D.p;
     } else {
       Level& C = H.L(t + 1);
-      a.nclusters = C.nclus;
+      a.c_begin = cb(t + 1);
+      a.nclusters = ce(t + 1) - cb(t + 1);
       a.max_rows = C.max_k;
       a.yoff = a.ooff = C.d_roff.p;
       a.cnt = C.d_k.p;
@@ -411,7 +519,8 @@ struct Builder {
     if (W.n < need) W.alloc(need, st);
     timer.begin(H2_PH_CPQR);
     CpqrArgs a{};
-    a.nclusters = L.nclus;
+    a.c_begin = cb(t);
+    a.nclusters = ce(t) - cb(t);
     a.max_m = std::max(L.max_m, 1);
     a.Y = cur.Y.p;
     a.ldy = cur.ld;
@@ -426,6 +535,7 @@ struct Builder {
     a.cert = L.cert.p;
     launch_cpqr(a, st);
     timer.end();
+    if (comm) comm_allgather_clusters(comm, L.d_k.p, 4, t, [](int c) { return (int64_t)c; }, st);
     L.k = download(L.d_k, L.nclus, st);
   }
 
@@ -448,7 +558,8 @@ struct Builder {
     L.d_skel.alloc(L.rtot, st);
     timer.begin(H2_PH_ID);
     IdArgs a{};
-    a.nclusters = L.nclus;
+    a.c_begin = cb(t);
+    a.nclusters = ce(t) - cb(t);
     a.W = W.p;
     a.d = d;
     a.poff = L.d_poff.p;
@@ -464,6 +575,9 @@ struct Builder {
     a.max_red = 0;
     for (int c = 0; c < L.nclus; ++c) a.max_red = std::max(a.max_red, L.m[c] - L.k[c]);
     launch_id(a, st);
+    if (comm)   // skeletons I~ of every cluster (B generation of cross-rank pairs, parent Ibar)
+      comm_allgather_clusters(comm, L.d_skel.p, 4, t,
+                              [&](int c) { return c < L.nclus ? L.roff[c] : L.rtot; }, st);
     timer.end();
   }
 
@@ -473,7 +587,8 @@ struct Builder {
     Level& L = H.L(u);
     timer.begin(H2_PH_ID);
     ShrinkArgs a{};
-    a.nclusters = L.nclus;
+    a.c_begin = cb(u);
+    a.nclusters = ce(u) - cb(u);
     a.poff = L.d_poff.p;
     a.m = L.d_m.p;
     a.k = L.d_k.p;
@@ -503,6 +618,13 @@ struct Builder {
     L.B.alloc(L.B_off.back(), st);
     GenArgs g{};
     g.nblocks = F.nuniq();
+    DArr<int32_t> ul;
+    if (comm) {
+      const std::vector<int32_t> l = owned_pairs(F, t);
+      ul.upload(l, st);
+      g.ulist = ul.p;
+      g.nblocks = (int64_t)l.size();
+    }
     g.us = T.d_far[t].us;
     g.ub = T.d_far[t].ub;
     g.cnt = L.d_k.p;
@@ -617,11 +739,13 @@ struct Builder {
     for (int u = T.Dl; u > t; --u) {
       if (u - 1 == t) {
         shrink(u, src.Y.p, src.O.p, src.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
+        allgather_skel_rows(u, cur.O.p + c0, cur.ld, b);   // partners' Omega^t rows (BSR)
         bsr(t, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
       } else {
         Panel dst;
         dst.alloc(H.L(u).rtot, b, st);
         shrink(u, src.Y.p, src.O.p, src.ld, dst.Y.p, dst.O.p, dst.ld, b);
+        allgather_skel_rows(u, dst.O.p, dst.ld, b);
         bsr(u - 1, dst.Y.p, dst.O.p, dst.ld, b);
         src = std::move(dst);
       }
@@ -656,6 +780,13 @@ struct Builder {
     {
       GenArgs g{};
       g.nblocks = T.near.nuniq();
+      DArr<int32_t> ul;
+      if (comm) {
+        const std::vector<int32_t> l = owned_pairs(T.near, T.Dl);
+        ul.upload(l, st);
+        g.ulist = ul.p;
+        g.nblocks = (int64_t)l.size();
+      }
       g.us = T.d_near.us;
       g.ub = T.d_near.ub;
       g.cnt = T.d_leaf_size;
@@ -717,6 +848,7 @@ struct Builder {
       if (t > top) {                                // lines 222-223 / 251-252 into the parent panel
         next.alloc(L.rtot, ld_for(L.rtot, d), st);
         shrink(t, cur.Y.p, cur.O.p, cur.ld, next.Y.p, next.O.p, next.ld, d);
+        allgather_skel_rows(t, next.O.p, next.ld, d);   // Omega^{l+1} of every cluster (S§8(e))
       }
       gen_B(t);                                     // line 258
       cur = std::move(next);
@@ -975,8 +1107,22 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->stream_id = 0;
 }
 
+h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end) {
+  if (!begin || !end || nranks < 1 || rank < 0 || rank >= nranks || n_clusters < 0)
+    return (g_err = "h2_dist_range: bad argument", H2_ERR_INVALID_ARG);
+  *begin = (rank * n_clusters + nranks - 1) / nranks;
+  *end = ((rank + 1) * n_clusters + nranks - 1) / nranks;
+  return H2_OK;
+}
+
 h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                    const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats) {
+  return h2_build_dist(tree, sketch, entry, tol, opts, nullptr, stream, out, stats);
+}
+
+h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                        const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                        h2_build_stats* stats) {
   if (!out) return (g_err = "h2_build: out is NULL", H2_ERR_INVALID_ARG);
   *out = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1014,12 +1160,28 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
       if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
+    const bool dist = comm && comm->nranks > 1;
+    if (comm)
+      H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks && (!dist || comm->allgatherv),
+                 "h2_build_dist: bad communicator");
+    H2_REQUIRE(!dist || (sketch->kind != H2_S_H2_LOWRANK && entry->kind != H2_E_H2_LOWRANK),
+               "h2_build_dist: H2 + low-rank operators are single-GPU only");
+    // subtree-aligned ownership at every processed depth: a power-of-two rank count with at
+    // least one cluster per rank at the coarsest processed depth
+    H2_REQUIRE(!dist || ((comm->nranks & (comm->nranks - 1)) == 0 && tree->top >= 0 &&
+                         (int64_t(1) << tree->top) >= comm->nranks),
+               "h2_build_dist: nranks must be a power of two <= 2^top_depth");
     ensure_uploaded(tree);
     // the tree is owned by the caller; share it without taking ownership
     H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
     {
-      Builder B(*tree, *sketch, *entry, tol, o, st, *H);
+      Builder B(*tree, *sketch, *entry, tol, o, st, *H, comm);
       B.run();
+    }
+    if (dist) {
+      H->nranks = comm->nranks;
+      H->rank = comm->rank;
+      H->partial = true;
     }
     H->stats.launches = h2::g_launches - launches0;
     H->stats.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1040,10 +1202,48 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
   }
 }
 
+h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream) {
+  try {
+    H2_REQUIRE(H, "h2_matrix_allgather: NULL matrix");
+    if (!H->partial) return H2_OK;
+    H2_REQUIRE(comm && comm->nranks == H->nranks && comm->rank == H->rank && comm->allgatherv,
+               "h2_matrix_allgather: communicator does not match the build");
+    cudaStream_t st = (cudaStream_t)stream;
+    const h2_tree& T = *H->tree;
+    const int P = comm->nranks;
+    // blocks stored once per unique pair (s, b), sorted by s: the pairs whose row cluster s is
+    // owned by rank r form one contiguous range of unique indices
+    auto block_ranges = [&](const PairCSR& F, int t, const std::vector<int64_t>& off, double* base) {
+      std::vector<int64_t> cnt(P), dsp(P);
+      for (int r = 0; r < P; ++r) {
+        const int a = own_begin(t, r, P), b = own_begin(t, r + 1, P);
+        const int64_t u0 = std::lower_bound(F.us.begin(), F.us.end(), a) - F.us.begin();
+        const int64_t u1 = std::lower_bound(F.us.begin(), F.us.end(), b) - F.us.begin();
+        dsp[r] = off[u0] * 8;
+        cnt[r] = (off[u1] - off[u0]) * 8;
+      }
+      comm_allgather(comm, base, cnt, dsp, st);
+    };
+    for (int t = H->top; t <= H->Dl; ++t) {
+      Level& L = H->L(t);
+      comm_allgather_clusters(comm, L.X.p, 8, t, [&](int c) { return c < L.nclus ? L.xoff[c] : L.xtot; }, st);
+      comm_allgather_clusters(comm, L.cert.p, 16, t, [](int c) { return (int64_t)c; }, st);
+      if (T.far[t].nuniq() > 0) block_ranges(T.far[t], t, L.B_off, L.B.p);
+    }
+    block_ranges(T.near, T.Dl, T.D_off, H->D.p);
+    H2_CUDA(cudaStreamSynchronize(st));
+    H->partial = false;
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
 h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                     double beta, void* stream) {
   try {
     H2_REQUIRE(H && x && y, "h2_matvec: NULL argument");
+    H2_REQUIRE(!H->partial, "h2_matvec: distributed matrix: call h2_matrix_allgather first");
     H2_REQUIRE(q >= 1 && q <= 64 && ldx >= q && ldy >= q, "h2_matvec: need 1 <= ncols <= 64, ld >= ncols");
     matvec_impl(*H, x, ldx, y, ldy, q, alpha, beta, (cudaStream_t)stream);
     return H2_OK;
@@ -1099,6 +1299,8 @@ h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_
 }
 
 h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst) {
+  if (H && H->partial && (what == H2_X_BASIS || what == H2_X_D || what == H2_X_B || what == H2_X_CERT))
+    return (g_err = "h2_export: distributed matrix: call h2_matrix_allgather first", H2_ERR_INVALID_ARG);
   int64_t cnt = 0;
   h2_status s = h2_export_size(H, what, depth, &cnt);
   if (s != H2_OK) return s;

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   constexpr int CQ_WARPS = CQ_THREADS / 32;
   constexpr int RPP = CQ_THREADS / CQ_TPR;      // rows per pass
   extern __shared__ double smem[];
-  const int c = blockIdx.x;
+  const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c];
   const int d = a.d;
   const int LD = SMEM ? cq_ld(d) : d;
@@ -267,7 +267,7 @@ constexpr int ID_CB = 32;
 __global__ void __launch_bounds__(256) id_kernel(IdArgs a) {
   extern __shared__ double sB[];           // k x ID_CB, row stride ID_CB + 1
   __shared__ double sD[ID_CB][ID_CB + 1];  // diagonal block R(i0:i1, i0:i1)
-  const int c = blockIdx.x;
+  const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c], k = a.k[c], d = a.d;
   const int64_t off = a.poff[c];
   const double* A = a.W + off * d;
@@ -345,7 +345,7 @@ void launch_id(const IdArgs& a, cudaStream_t st) {
 // are split over blockIdx.y to fill the GPU.
 constexpr int SP_CB = 32;
 __global__ void __launch_bounds__(256) shrink_project_kernel(ShrinkArgs a) {
-  const int c = blockIdx.x;
+  const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c], k = a.k[c];
   const int64_t off = a.poff[c];
   const int* perm = a.perm + off;

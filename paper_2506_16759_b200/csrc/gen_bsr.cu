@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
   __shared__ double cx[256], cy[256], cz[256];
   __shared__ double tab[64];
   fill_exp_table(tab);
-  for (int64_t u = blockIdx.x; u < a.nblocks; u += gridDim.x) {
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
     const int m = a.cnt[s], nc = a.cnt[b];
     const int32_t* ri = a.idx + a.off[s];
@@ -54,14 +55,15 @@ void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const
 
 __global__ void gen_desc_kernel(GenArgs a, int32_t* m, int32_t* nc, int64_t* roff, int64_t* coff, double** outp,
                                 int32_t* ld) {
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < a.nblocks; u += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nblocks; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = a.ulist ? a.ulist[q] : q;
     int s = a.us[u], b = a.ub[u];
-    m[u] = a.cnt[s];
-    nc[u] = a.cnt[b];
-    ld[u] = a.cnt[b];
-    roff[u] = a.off[s];
-    coff[u] = a.off[b];
-    outp[u] = a.out + a.out_off[u];
+    m[q] = a.cnt[s];
+    nc[q] = a.cnt[b];
+    ld[q] = a.cnt[b];
+    roff[q] = a.off[s];
+    coff[q] = a.off[b];
+    outp[q] = a.out + a.out_off[u];
   }
 }
 
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
   constexpr int BSZ = BT_K * LDB;
   extern __shared__ __align__(16) double bsm[];   // NS x (A slab + B slab)
   __shared__ int st_nk[BSR_NS], st_dir[BSR_NS];
-  const int s = blockIdx.x;
+  const int s = a.c_begin + blockIdx.x;
   const int ms = a.cnt[s];
   const int r0 = blockIdx.y * BT_R;
   const int cb = a.c0 + blockIdx.z * CW;

@@ -24,6 +24,11 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
                             int64_t ldy, cudaStream_t st);
 void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, double* Y, int64_t ldy, cudaStream_t st);
 // accum += ||Y(:, c0:c1)||_F^2 (deterministic)                                   (R10 tolerance scale)
+// per-leaf sums of squares of Y(rows of leaf c, c0:c1) for leaves [cb, ce) into part[c] (one CTA
+// per leaf), and the fixed-order total over all nleaf partials: accum += sum_c part[c]
+void launch_sumsq_leaf(const double* Y, const int64_t* leaf_begin, int cb, int ce, int64_t ld, int c0, int c1,
+                       double* part, cudaStream_t st);
+void launch_sumsq_total(const double* part, int nleaf, double* accum, int* nonfinite, cudaStream_t st);
 void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum,
                   int* nonfinite, cudaStream_t st);
 
@@ -31,6 +36,7 @@ void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double
 // (L212 for D with idx = iota, off = cluster begin; L258 for B with idx = skeletons)
 struct GenArgs {
   int64_t nblocks;
+  const int32_t* ulist;   // optional: block q is unique pair ulist[q] (multi-GPU subset), else q
   const int32_t* us;
   const int32_t* ub;
   const int32_t* cnt;     // per cluster rows
@@ -48,7 +54,8 @@ void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* r
 // batchedBSRGemm: Y(rows of s, c0:c0+nc) -= sum_{b in CSR row s} Blk(s,b) Om(rows of b, c0:c0+nc)
 // (L213 leaf with D, L240-243 inner with B); partners ascending, no atomics (L385)
 struct BsrArgs {
-  int32_t nclusters;
+  int32_t nclusters;      // clusters c_begin .. c_begin + nclusters - 1 (multi-GPU: the owned range)
+  int32_t c_begin;
   int32_t max_rows;
   const int64_t* yoff;    // per cluster: first row in Y
   const int64_t* ooff;    // per cluster: first row in Om
@@ -70,7 +77,8 @@ void launch_bsr(const BsrArgs& a, cudaStream_t st);
 // CPQR of every panel A_c = Y(poff[c] : poff[c]+m[c], 0:d)^T (row ID via column ID, L173, L387)
 // with threshold eps (R13/R14); W receives the factored panels (packed, ld = d).
 struct CpqrArgs {
-  int32_t nclusters;
+  int32_t nclusters;      // clusters c_begin .. c_begin + nclusters - 1
+  int32_t c_begin;
   int32_t max_m;
   const double* Y;
   int64_t ldy;
@@ -88,7 +96,8 @@ void launch_cpqr(const CpqrArgs& a, cudaStream_t st);
 
 // ID epilogue: X_c (m x k, U or [E1;E2]) from T = R11^{-1} R12 (R15); skeletons I~ (L224, L253)
 struct IdArgs {
-  int32_t nclusters;
+  int32_t nclusters;      // clusters c_begin .. c_begin + nclusters - 1
+  int32_t c_begin;
   const double* W;
   int d;
   const int64_t* poff;
@@ -107,7 +116,8 @@ void launch_id(const IdArgs& a, cudaStream_t st);
 // batchedShrink + batchedGemm upsweep for columns [c0,c1) (L222-223, L251-252):
 // Yp(roff[c]+i) = Yl(poff[c] + J[i]);  Op(roff[c]+i) = sum_j X(j,i) Ol(poff[c]+j)
 struct ShrinkArgs {
-  int32_t nclusters;
+  int32_t nclusters;      // clusters c_begin .. c_begin + nclusters - 1
+  int32_t c_begin;
   const int64_t* poff;
   const int32_t* m;
   const int32_t* k;

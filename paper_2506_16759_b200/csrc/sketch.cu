@@ -264,8 +264,11 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
     const int slots = sms * occ;
     double best = 0;
     S = 1;
+    // chosen from n only (as if all rows were computed): the row shards of a multi-GPU build
+    // then split j identically and produce bitwise the same rows as one GPU
+    const int64_t tiles_n = div_up(n, SK_VARS[var].rows);
     for (int s = 1; s <= 4; ++s) {
-      int64_t units = (int64_t)tiles * s;
+      int64_t units = tiles_n * s;
       if (n / s < 4096 && s > 1) break;
       double eff = (double)units / ((double)slots * ((units + slots - 1) / slots)) - 0.01 * (s - 1);
       if (eff > best + 1e-9) {
@@ -341,6 +344,41 @@ __global__ void sumsq_final_kernel(const double* __restrict__ part, int np, doub
       if (!isfinite(v)) *flag = 1;
     }
   }
+}
+
+// per-leaf partials: every leaf is summed by one CTA (its owner under multi-GPU), and the total
+// is taken over the leaves in order, so the result is bitwise independent of the GPU count.
+__global__ void sumsq_leaf_kernel(const double* __restrict__ Y, const int64_t* __restrict__ leaf_begin, int cb,
+                                  int64_t ld, int c0, int c1, double* __restrict__ part) {
+  __shared__ double red[32];
+  const int c = cb + blockIdx.x;
+  const int64_t r0 = leaf_begin[c], r1 = leaf_begin[c + 1];
+  const int w = c1 - c0;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < (r1 - r0) * w; e += blockDim.x) {
+    const double v = Y[(r0 + e / w) * ld + c0 + e % w];
+    s = fma(v, v, s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) part[c] = v;
+  }
+}
+
+void launch_sumsq_leaf(const double* Y, const int64_t* leaf_begin, int cb, int ce, int64_t ld, int c0, int c1,
+                       double* part, cudaStream_t st) {
+  if (ce <= cb || c1 <= c0) return;
+  sumsq_leaf_kernel<<<ce - cb, 256, 0, st>>>(Y, leaf_begin, cb, ld, c0, c1, part);
+  H2_CHECK_LAUNCH();
+}
+
+void launch_sumsq_total(const double* part, int nleaf, double* accum, int* nonfinite, cudaStream_t st) {
+  sumsq_final_kernel<<<1, 1024, 0, st>>>(part, nleaf, accum, nonfinite);
+  H2_CHECK_LAUNCH();
 }
 
 void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum, int* nonfinite,

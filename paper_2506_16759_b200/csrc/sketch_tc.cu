@@ -482,7 +482,7 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     const int tiles = div_up(rows, TM);
     // the split is chosen for the 64-row tiles of the default 128-column pass and shared by
     // all pass shapes (bitwise identical sketches, test_tc_pass_width_bitwise)
-    const int S = pick_split(div_up(rows, 64), npad / 128, sms);
+    const int S = pick_split(div_up(n, 64), npad / 128, sms);   // f(n) only: row shards of a multi-GPU build split j identically
     if (S > 1 && part_elems < rows * nc * S) {
       if (part) cache_free(part, st);
       part_elems = rows * nc * S;

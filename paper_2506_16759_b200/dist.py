@@ -4,9 +4,15 @@ The O(N^2) dense-kernel sketch Y = K Omega (Algorithm 1 line 1; B
 configs[1..2]) shards by rows with no communication of Omega (each rank regenerates the
 counter-based stream, R8): rank r computes Y(rows_r, :) and the shards are
 all-gathered so that every rank holds the full Y for the (replicated) construction proper.
-This is the path's one exchange step.  Arithmetic stays in libh2; this module
-only partitions rows and moves the shards.
+Arithmetic stays in libh2; this module only partitions rows and moves bytes.
+
+``Comm`` is the communicator of the sharded construction (h2_build_dist, include/h2.h; S§8(e)):
+libh2 calls its in-place ``allgatherv`` on device buffers once per level (ranks, skeleton
+indices I~, the next level's Omega rows) and torch.distributed moves the bytes: NCCL over
+NVLink on GPU tensors, or gloo through host staging (multi-process tests on one GPU / CPU).
 """
+import ctypes as C
+
 import torch
 import torch.distributed as dist
 
@@ -56,3 +62,61 @@ def dense_shard_fn(tree, kernel):
     def fn(om, out, r0, r1):
         _h2.dense_sketch(tree, om, kernel, r0, r1, out=out, omega_quarters=True)   # h2 stream Omega
     return fn
+
+
+def owned_range(n_clusters: int, rank: int, world: int):
+    """Clusters [b, e) of a depth with n_clusters clusters owned by `rank` (cluster c belongs to
+    rank floor(c * world / n_clusters); mirrors h2_dist_range)."""
+    return (rank * n_clusters + world - 1) // world, ((rank + 1) * n_clusters + world - 1) // world
+
+
+def allgatherv_(buf: torch.Tensor, counts, displs, group=None):
+    """In-place all-gather of byte segments of a 1-D uint8 tensor: segment r =
+    buf[displs[r] : displs[r] + counts[r]] is valid on rank r on entry and on every rank on
+    return.  One broadcast per non-empty segment (NCCL: on-device; gloo: host staging)."""
+    nccl = dist.get_backend(group) == "nccl"
+    me = dist.get_rank(group)
+    for r, (c, d) in enumerate(zip(counts, displs)):
+        if c == 0:
+            continue
+        seg = buf[d:d + c]
+        src = dist.get_global_rank(group, r) if group is not None else r
+        if nccl or not seg.is_cuda:
+            dist.broadcast(seg, src=src, group=group)
+        else:
+            host = seg.cpu() if r == me else torch.empty(c, dtype=torch.uint8)
+            dist.broadcast(host, src=src, group=group)
+            if r != me:
+                seg.copy_(host)
+
+
+class Comm:
+    """h2_comm over a torch.distributed process group (one process per GPU)."""
+
+    def __init__(self, group=None):
+        from . import _lib as L
+        from .h2 import device_view
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.calls = 0
+        self.bytes = 0
+
+        def _agv(ctx, buf, counts, displs, stream):
+            try:
+                P = self.world
+                cnt = [int(counts[i]) for i in range(P)]
+                dsp = [int(displs[i]) for i in range(P)]
+                end = max(d + c for c, d in zip(cnt, dsp))
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+                    view = device_view(buf, (end,), (1,), dtype=torch.uint8)
+                    allgatherv_(view, cnt, dsp, self.group)
+                self.calls += 1
+                self.bytes += sum(cnt) - cnt[self.rank]
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._cb = L.ALLGATHERV_FN(_agv)
+        self.struct = L.h2_comm(self.rank, self.world, self._cb, None)

@@ -35,7 +35,8 @@ class _CudaView:
 
 
 def device_view(ptr, shape, strides, dtype=torch.float64):
-    typestr, size = {torch.float64: ("<f8", 8), torch.int32: ("<i4", 4), torch.int64: ("<i8", 8)}[dtype]
+    typestr, size = {torch.float64: ("<f8", 8), torch.int32: ("<i4", 4), torch.int64: ("<i8", 8),
+                     torch.uint8: ("|u1", 1)}[dtype]
     return torch.as_tensor(_CudaView(ptr, shape, strides, typestr, size), device="cuda")
 
 
@@ -196,6 +197,11 @@ class H2Matrix:
                 o += n
         return out
 
+    def allgather(self, comm, stream=None):
+        """Complete a distributed build on every rank (h2_matrix_allgather; collective)."""
+        check(lib.h2_matrix_allgather(self._h, C.byref(comm.struct), _stream(stream)))
+        return self
+
     def device_bytes(self):
         return int(lib.h2_matrix_device_bytes(self._h))
 
@@ -227,7 +233,8 @@ def _stats_dict(s):
     return d
 
 
-def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, **opts):
+def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, comm=None,
+          **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
@@ -236,7 +243,9 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  update=(H_base, U):
     recompress M = H_base + U U^T (H_base built on this tree, U a (n, r) float64
     CUDA tensor in tree order) with the library's H^2-matvec + low-rank sketch and entry
-    extraction.  opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
+    extraction.  comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
+    by subtrees (h2_build_dist); call ``H.allgather(comm)`` before matvec / block export.
+    opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
     tol_safety, p_os, norm, max_rank, seed, stream_id)."""
     o = build_opts(**opts)
     kern = _kernel(*kernel)
@@ -295,8 +304,12 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         en.fn = cb2
     h = C.c_void_p()
     st = L.h2_build_stats()
-    check(lib.h2_build(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o), _stream(stream), C.byref(h),
-                       C.byref(st)))
+    cm = None
+    if comm is not None:
+        cm = C.byref(comm.struct)
+        keep.append(comm)
+    check(lib.h2_build_dist(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o), cm, _stream(stream),
+                            C.byref(h), C.byref(st)))
     return H2Matrix(h, tree, _stats_dict(st), keep)
 
 

@@ -1,0 +1,90 @@
+"""Sharded construction (h2_build_dist, S§8(e)) on one B200 with world_size 2 and 4: one process
+per rank on cuda:0, gloo communicator (host-staged allgatherv).  The distributed build,
+completed with h2_matrix_allgather, must be BITWISE identical to the one-GPU build: every
+cluster's arithmetic and every block's partner order are rank independent."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _snapshot(H, g):
+    out = {"samples": H.samples}
+    for t in range(H.top_depth, H.tree.leaf_depth + 1):
+        out[("k", t)] = H.rank(t).copy()
+        out[("skel", t)] = H._export(g._lib.H2_X_SKEL, t).copy()
+        out[("X", t)] = H._export(g._lib.H2_X_BASIS, t).copy()
+        out[("B", t)] = H._export(g._lib.H2_X_B, t).copy()
+        out[("cert", t)] = H._export(g._lib.H2_X_CERT, t).copy()
+    out["D"] = H._export(g._lib.H2_X_D).copy()
+    return out
+
+
+def _worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2506_16759_b200 as g
+        from paper_2506_16759_b200.dist import Comm
+        from synth import uniform_points
+        n, adaptive = case
+        X = uniform_points(n, 3, 0)
+        T = g.Tree(X, 64)
+        comm = Comm()
+        opts = dict(adaptive=True) if adaptive else dict(adaptive=False, d_init=96)
+        Hd = g.build(T, ("exp", 0.2), 1e-6, comm=comm, **opts)
+        partial_refused = False
+        try:
+            Hd.matvec(torch.zeros(T.n, 1, dtype=torch.float64, device="cuda"))
+        except g.H2Error:
+            partial_refused = True
+        Hd.allgather(comm)
+        H1 = g.build(T, ("exp", 0.2), 1e-6, **opts)
+        a, b = _snapshot(Hd, g), _snapshot(H1, g)
+        same = {str(k): bool(np.array_equal(a[k], b[k])) for k in b}
+        q.put((rank, same, partial_refused, comm.calls, comm.bytes))
+    except Exception as exc:
+        import traceback
+        traceback.print_exc()
+        q.put((rank, {"error": repr(exc)}, False, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", [(5000, True), (8192, False)])
+def test_distributed_build_bitwise(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, same, refused, calls, nbytes in res:
+        assert "error" not in same, same
+        bad = [k for k, v in same.items() if not v]
+        assert not bad, (rank, bad)
+        assert refused          # a partial matrix refuses matvec until allgather
+        assert calls > 0 and nbytes > 0
