@@ -192,6 +192,9 @@ void comm_allgather(const h2_comm* comm, void* base, const std::vector<int64_t>&
   int64_t tot = 0;
   for (int64_t c : counts) tot += c;
   if (tot == 0) return;
+  // the segments are produced by kernels on `st`; a host-staged communicator reads them on the
+  // host side, so complete them first (a few times per level)
+  H2_CUDA(cudaStreamSynchronize(st));
   const int rc = comm->allgatherv(comm->ctx, base, counts.data(), displs.data(), st);
   if (rc != 0) throw Error(H2_ERR_CALLBACK, "communicator allgatherv returned " + std::to_string(rc));
 }

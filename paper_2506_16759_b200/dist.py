@@ -12,6 +12,7 @@ indices I~, the next level's Omega rows) and torch.distributed moves the bytes: 
 NVLink on GPU tensors, or gloo through host staging (multi-process tests on one GPU / CPU).
 """
 import ctypes as C
+import os
 
 import torch
 import torch.distributed as dist
@@ -108,6 +109,8 @@ class Comm:
                 cnt = [int(counts[i]) for i in range(P)]
                 dsp = [int(displs[i]) for i in range(P)]
                 end = max(d + c for c, d in zip(cnt, dsp))
+                if os.environ.get("H2_COMM_TRACE"):
+                    print(f"[rank {self.rank}] allgatherv #{self.calls} counts {cnt} displs {dsp}", flush=True)
                 with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
                     view = device_view(buf, (end,), (1,), dtype=torch.uint8)
                     allgatherv_(view, cnt, dsp, self.group)

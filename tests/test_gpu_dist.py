@@ -25,7 +25,7 @@ def _snapshot(H, g):
     out = {"samples": H.samples}
     for t in range(H.top_depth, H.tree.leaf_depth + 1):
         out[("k", t)] = H.rank(t).copy()
-        out[("skel", t)] = H._export(g._lib.H2_X_SKEL, t).copy()
+        out[("skel", t)] = H._export(g._lib.H2_X_SKEL, t, dtype=np.int32).copy()
         out[("X", t)] = H._export(g._lib.H2_X_BASIS, t).copy()
         out[("B", t)] = H._export(g._lib.H2_X_B, t).copy()
         out[("cert", t)] = H._export(g._lib.H2_X_CERT, t).copy()
