@@ -166,17 +166,20 @@ def run_ours(args, w, rank, world, local_rank):
     T = g.Tree(X, w["leaf"], 0.7)
     opts = dict(adaptive=True, d_init=32, d_blk=32, d_max=512)
     dist = None
-    sketch = None
+    comm = None
     if world > 1:
+        # sharded construction (h2_build_dist, S§8(e)): every rank owns a subtree range per
+        # level, sketch rows of its leaves, its blocks; per-level NCCL all-gathers of ranks,
+        # skeleton indices and Omega rows
         import torch.distributed as dist
-        from paper_2506_16759_b200.dist import ShardedSketch, dense_shard_fn
-        sketch = ShardedSketch(n, dense_shard_fn(T, kern))
+        from paper_2506_16759_b200.dist import Comm
+        comm = Comm()
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream()
 
     def one():
-        return g.build(T, kern, w["tol"], sketch=sketch, **opts)
+        return g.build(T, kern, w["tol"], comm=comm, **opts)
 
     for _ in range(args.warmup):
         H = one()
@@ -209,6 +212,8 @@ def run_ours(args, w, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     st = stats[-1]
+    if comm is not None:
+        H.allgather(comm)   # untimed: complete every rank's copy for the verification matvec
     # verification (untimed): dense probes  ||H X - K X||_F / ||K X||_F
     Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, 16))).to(dev)
     KX = g.dense_sketch(T, Xp, kern)
@@ -217,12 +222,9 @@ def run_ours(args, w, rank, world, local_rank):
     # roofline of the dominant kernel (sketch_tc_kernel, one launch per 128-column pass): the
     # contraction runs exactly on the int8 tensor cores, so the bound is the FP64 pipe evaluating
     # K: algorithmic work = N_rows * N entries x F_EVAL FP64 ops per launch
-    if world == 1:
-        sk_launches = st["entries_sketch"] // (n * n)
-        ncol_launch = -(-st["sketch_columns"] // max(sk_launches, 1))
-        ncol_launch = min(128, -(-ncol_launch // 32) * 32)
-    else:
-        sk_launches, ncol_launch = st["samples"] // 32, 32
+    sk_launches = st["entries_sketch"] // (n * n)
+    ncol_launch = -(-st["sketch_columns"] // max(sk_launches, 1))
+    ncol_launch = min(128, -(-ncol_launch // 32) * 32)
     t_sk_ms = float(np.mean([s["t_phase_ms"]["sketch"] for s in stats]))
     per_launch_ms = t_sk_ms / max(sk_launches, 1)
     rows_local = n if world == 1 else (n // world)
@@ -244,11 +246,7 @@ def run_ours(args, w, rank, world, local_rank):
         for _ in range(max(1, min(args.steps, 3))):
             t0 = time.perf_counter()
             T2 = g.Tree(Xpin.numpy(), w["leaf"], 0.7)
-            sk2 = None
-            if world > 1:
-                from paper_2506_16759_b200.dist import ShardedSketch, dense_shard_fn
-                sk2 = ShardedSketch(n, dense_shard_fn(T2, kern))
-            H2 = g.build(T2, kern, w["tol"], sketch=sk2, **opts)
+            H2 = g.build(T2, kern, w["tol"], comm=comm, **opts)
             d2h = 0
             for t in range(H2.top_depth, T2.leaf_depth + 1):
                 d2h += H2.rank(t).nbytes // 2 + sum(s.nbytes // 2 for s in H2.skel(t))
@@ -275,9 +273,10 @@ def run_ours(args, w, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "n": n, "leaf": w["leaf"], "eta": 0.7, "tol": w["tol"],
-                   "kernel": f"{w['kernel']}({w['param']})", "sketch": "dense-kernel (row-sharded)" if world > 1
+                   "kernel": f"{w['kernel']}({w['param']})", "sketch": "dense-kernel (row shards)" if world > 1
                    else "dense-kernel", "d_init": 32, "d_blk": 32, "d_max": 512,
-                   "parallelism": f"sketch rows x{world}" if world > 1 else "1 GPU",
+                   "parallelism": f"subtree shards x{world} (sketch rows, clusters per level; NCCL all-gathers)"
+                   if world > 1 else "1 GPU",
                    "l2": "256 MiB flush before every timed step; working set (N x d_max x 16 B = 2 GiB) > L2"},
         "samples": st["samples"], "sketch_columns": st["sketch_columns"], "sketch_launches": sk_launches,
         "verified_error": verr,
@@ -318,8 +317,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ngpu = torch.cuda.device_count()
+        if ngpu >= world:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            # fewer GPUs than ranks (functional check of the multi-rank path on one GPU):
+            # ranks share the devices and the communicator stages through the host (gloo)
+            local_rank %= ngpu
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
     run_ours(args, w, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
