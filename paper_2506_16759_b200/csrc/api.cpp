@@ -176,6 +176,7 @@ struct Panel {
 
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                  double beta, cudaStream_t st);
+KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st);
 
 // Cluster ownership under a communicator (S§8(e)): cluster c of depth t (2^t clusters) belongs
 // to rank floor(c P / 2^t).  Ranges are contiguous and subtree-aligned (the children of an owned
@@ -763,7 +764,7 @@ struct Builder {
     H.n = T.n;
     H.lv.resize(Dl - top + 1);
     if (S.kind == H2_S_DENSE_KERNEL) {
-      skp = make_kernel(S.kern, T.diam);
+      skp = tree_kernel(&T, S.kern, st);
       spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
       spec_w = sketch_tc_pass_cols();
     }
@@ -1006,6 +1007,18 @@ void ensure_uploaded(const h2_tree* tree) {
   H2_CUDA(cudaGetDevice(&dev));
   if (T->device < 0) tree_upload(*T);
   H2_REQUIRE(dev == T->device, "libh2: the tree was uploaded to another device");
+}
+
+// built-in kernel parameters on a tree: diameter (exp / Helmholtz range guards) and, for the
+// Helmholtz tensor-core sketch, the minimum point distance (computed once per tree)
+KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st) {
+  h2_tree* T = const_cast<h2_tree*>(tree);
+  if (k.kind == H2_K_HELMHOLTZ && T->rmin < 0) {
+    const double d2 = min_near_dist2(T->d_x, T->d_y, T->d_z, T->d_leaf_begin, 1 << T->Dl, T->d_near.ptr,
+                                     T->d_near.idx, st);
+    T->rmin = (d2 > 0 && d2 < 1e300) ? std::sqrt(d2) : 0.0;
+  }
+  return make_kernel(k, T->diam, k.kind == H2_K_HELMHOLTZ ? T->rmin : 0.0);
 }
 
 h2_status fail(const Error& e) {
@@ -1263,7 +1276,7 @@ h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, i
     H2_REQUIRE(ncols >= 0 && ld_omega >= ncols && ld_y >= ncols, "h2_dense_sketch: bad ncols / leading dims");
     H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ) && kern.param > 0, "h2_dense_sketch: bad kernel");
     ensure_uploaded(T);
-    launch_dense_sketch(make_kernel(kern, T->diam), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
+    launch_dense_sketch(tree_kernel(T, kern, (cudaStream_t)stream), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
                         ld_y, (flags & H2_SKETCH_OMEGA_QUARTERS) != 0, (cudaStream_t)stream);
     return H2_OK;
   } catch (const Error& e) {

@@ -46,15 +46,17 @@ struct KernelParams {
   int kind;
   double param;   // l (exp) or k (helmholtz)
   double inv;     // 1/l for exp
-  double rmax;    // upper bound of the scaled distance |x-y|/l over the point set (exp); 0 = unknown
+  double rmax;    // upper bound of the scaled distance over the point set (|x-y|/l, k|x-y|); 0 = unknown
+  double rmin;    // minimum distance of distinct points (unscaled; Helmholtz fixed-point scale); 0 = unknown
 };
 
-inline KernelParams make_kernel(const h2_kernel& k, double diam = -1.0) {
+inline KernelParams make_kernel(const h2_kernel& k, double diam = -1.0, double rmin = 0.0) {
   KernelParams p;
   p.kind = k.kind;
   p.param = k.param;
   p.inv = 1.0 / k.param;
-  p.rmax = diam >= 0 ? diam * p.inv : 0.0;
+  p.rmax = diam >= 0 ? diam * (k.kind == H2_K_EXP ? p.inv : k.param) : 0.0;
+  p.rmin = rmin;
   return p;
 }
 

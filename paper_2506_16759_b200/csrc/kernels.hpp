@@ -19,9 +19,12 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
 bool sketch_tc_supported(const KernelParams& kp);
 int sketch_tc_pass_cols();   // Omega columns per tensor-core sketch pass (K evaluated once per pass)
 int env_int(const char* name, int def);
-void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st);
+// minimum squared distance of distinct points over the near-field leaf pairs (Helmholtz scale)
+double min_near_dist2(const double* X, const double* Y, const double* Z, const int64_t* leaf_begin, int nleaf,
+                      const int32_t* near_ptr, const int32_t* near_idx, cudaStream_t st);
 void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, double* Y, int64_t ldy, cudaStream_t st);
 // accum += ||Y(:, c0:c1)||_F^2 (deterministic)                                   (R10 tolerance scale)
 // per-leaf sums of squares of Y(rows of leaf c, c0:c1) for leaves [cb, ce) into part[c] (one CTA

@@ -244,8 +244,8 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
   // exp kernel with Omega in quarters (the h2 stream): exact int8 tensor-core contraction
   // (sketch_tc.cu); any other Omega, or H2_SK_TC=0, takes the DMMA path
   if (omega_quarters && sketch_tc_supported(kp) && env_int("H2_SK_TC", 1) != 0) {
-    launch_dense_sketch_tc(kp, X, Yc, Zc, n, row0, row1, Om, ldo, ncols, Yout, ldy, st);
-    return;
+    if (launch_dense_sketch_tc(kp, X, Yc, Zc, n, row0, row1, Om, ldo, ncols, Yout, ldy, st)) return;
+    // a Helmholtz entry exceeded the fixed-point scale: recompute on the FP64 DMMA path
   }
   int var = env_int("H2_SK_VAR", SK_DEFAULT_VAR);
   if (var < 0 || var > 6) var = SK_DEFAULT_VAR;

@@ -13,7 +13,9 @@
 //     every 65536 j the accumulators are drained: Y += sum_s 2^(8s-54) D_s in FP64.
 // The result is the exact product of the 2^-52-rounded K with Omega, rounded only at the
 // drains: as accurate as an FP64 GEMM, and the FP64 pipe only evaluates K.
+#include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "alloc.hpp"
 #include "common.cuh"
@@ -130,6 +132,61 @@ __device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restric
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)(__double2hiint(w) - 0x43300000));
 }
 
+// Helmholtz (PAPER.md Eq. ie, R20): K = cos(k r)/r, 0 at r = 0, in scaled coordinates
+// r' = k r: K = k cos(r')/r'.  Signed 53-bit fixed point with a power-of-two scale 2^E >= max|K|
+// (hs = k / 2^E): m = round(v 2^51), v = hs cos(r') / r' in (-1, 1):
+//   w = v 2^51 + 3 2^51 in (2^52, 2^53): one FMA, the fixed-point rounding;
+//   m = bits(w) - bits(2^52) - 2^51 (hi word - 0x43380000): the 64-bit two's complement of m,
+//       whose bytes 0..5 are the unsigned slices and byte 6 (bits 48-55, sign-extended) the
+//       signed top slice (tcgen05.mma a_format s8);
+//   |v| >= 1 (a pair closer than the scale assumed) is flagged: the caller redoes the pass on
+//       the FP64 DMMA path.
+// cos(r'): n = rint(2 r'/pi), x = r' - n pi/2 (fdlibm two-term Cody-Waite), cos / sin Taylor
+// polynomials on |x| <= pi/4 (to x^16 / x^17: truncation < 1e-16), quadrant by n & 3.
+// 1/r': the cubic-corrected rsqrt.  r' = 0 (the diagonal; r2 = the 2^-1000 floor) gives 0.
+// FP64 pipe: 6 (r'^2) + 5 (1/r') + 1 (r') + 4 (reduction) + 1 (x^2) + 8 (cos) + 9 (sin) + 2 + 1.
+__device__ __forceinline__ uint2 helm_fixed51(double r2, double hs, uint32_t& ovf) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double y = fma(fma(e, 0.375, 0.5), y0 * e, y0);            // 1/r'
+  const double r = r2 * y;
+  const double SH = 6755399441055744.0;
+  const double t = fma(r, 0.63661977236758134308, SH);             // 2/pi
+  const double nf = t - SH;
+  const int n = __double2loint(t);
+  double x = fma(nf, -1.57079632673412561417e+00, r);              // pio2_1
+  x = fma(nf, -6.07710050650619224932e-11, x);                     // pio2_1t
+  const double z = x * x;
+  double c = fma(z, 4.7794773323873852974e-14, -1.1470745597729724714e-11);   // 1/16!, -1/14!
+  c = fma(c, z, 2.0876756987868098979e-09);                        // 1/12!
+  c = fma(c, z, -2.7557319223985890653e-07);                       // -1/10!
+  c = fma(c, z, 2.4801587301587301587e-05);                        // 1/8!
+  c = fma(c, z, -1.3888888888888888889e-03);                       // -1/6!
+  c = fma(c, z, 4.1666666666666666667e-02);                        // 1/4!
+  c = fma(c, z, -0.5);
+  c = fma(c, z, 1.0);
+  double sn = fma(z, 2.8114572543455207632e-15, -7.6471637318198164759e-13);  // 1/17!, -1/15!
+  sn = fma(sn, z, 1.6059043836821614599e-10);                      // 1/13!
+  sn = fma(sn, z, -2.5052108385441718775e-08);                     // -1/11!
+  sn = fma(sn, z, 2.7557319223985890653e-06);                      // 1/9!
+  sn = fma(sn, z, -1.9841269841269841270e-04);                     // -1/7!
+  sn = fma(sn, z, 8.3333333333333333333e-03);                      // 1/5!
+  sn = fma(sn, z, -0.16666666666666666667);                        // -1/3!
+  sn = fma(sn * z, x, x);
+  // quadrant: 0 cos, 1 -sin, 2 -cos, 3 sin
+  const bool odd = n & 1;
+  const uint32_t neg = (uint32_t)((n + 1) & 2) << 30;              // sign for quadrants 1, 2
+  const double tr = __hiloint2double((int)((uint32_t)__double2hiint(odd ? sn : c) ^ neg),
+                                     __double2loint(odd ? sn : c));
+  double v = (hs * tr) * y;
+  if (__double2hiint(r2) < 0x03B00000) v = 0.0;                    // r2 < 2^-900: x' = y'
+  const double w = fma(v, 2251799813685248.0, 6755399441055744.0);  // v 2^51 + 3 2^51
+  const int mh = __double2hiint(w) - 0x43380000;
+  ovf |= (uint32_t)(mh + 0x80000) > 0x100000u;
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
+}
+
 // 4x4 byte transpose: out[s] = bytes s of (a, b, c, d)
 __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* o) {
   uint32_t p = __byte_perm(a, b, 0x5140), q = __byte_perm(c, d, 0x5140);
@@ -174,11 +231,11 @@ __global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int6
 //     chunk.
 // TM = 128, NCOL <= 64 : 7 x NCOL TMEM columns.  TM = 64, NCOL = 128 : the M = 64 accumulators
 // pack two slices per TMEM column (tmem_slice), so one evaluation of K feeds 128 columns.
-template <int TM, int NPW, int NCOL, int JC>
+template <int KIND, int TM, int NPW, int NCOL, int JC>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
-                     int64_t split_stride) {
+                     int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag) {
   using P = TcPlan<TM, NCOL, JC>;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
   constexpr int CBUF = P::CBUF;
@@ -190,6 +247,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
   constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL == 32) ? 256 : 512;
   constexpr uint32_t IDESC = idesc_i8<TM, NCOL>();
+  // Helmholtz: the top slice holds the sign (two's complement of the signed fixed point): s8
+  constexpr uint32_t IDESC6 = KIND == H2_K_EXP ? IDESC : (IDESC | (1u << 7));
   static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
   static_assert((TM == 128 && NCOL <= 64) || (TM == 64 && NCOL == 128), "TMEM plan");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -276,7 +335,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                 " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + tmem_slice<TM, NCOL>(s)),
-                "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+                "l"(ad), "l"(bd), "r"(s == TC_NS - 1 ? IDESC6 : IDESC), "r"(acc));
           }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             bar_empty + 8 * buf));
@@ -307,6 +366,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
     const uint32_t lane8 = 8u * (lane & 15);
+    uint32_t ovf = 0;
     int drains = 0;
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
@@ -323,7 +383,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-          const uint2 m = expk_fixed52(dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z), tab, lane8);
+          const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51(r2, hs, ovf);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
@@ -378,7 +439,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
             // slice weight 2^(8 sl) * 2^-52 * (1/4); at TM = 64 the high lanes hold slice s + 4
             const int sl = (TM == 128 || lane < 16) ? s : s + 4;
-            const double wgt = sl < TC_NS ? ldexp(1.0, 8 * sl - 54) : 0.0;
+            const double wgt = sl < TC_NS ? ldexp(1.0, 8 * sl + wshift) : 0.0;
             if (TM == 128 && s >= 4) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
@@ -399,6 +460,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       }
       if (drain) ++drains;
     }
+    if (KIND != H2_K_EXP && ovf) atomicOr(ovf_flag, 1u);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
@@ -407,9 +469,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 
 }  // namespace
 
-// exp kernel on a point set whose scaled diameter keeps n = rint(-256 r'/ln2) in the range of the
-// exponent arithmetic of expk_fixed52 (r' <= 650; K < 1e-282 there, far below the 2^-53 grid)
-bool sketch_tc_supported(const KernelParams& kp) { return kp.kind == H2_K_EXP && kp.rmax > 0 && kp.rmax <= 650.0; }
+// exp: a point set whose scaled diameter keeps n = rint(-256 r'/ln2) in the range of the exponent
+// arithmetic of expk_fixed52 (r' <= 650; K < 1e-282 there, far below the 2^-53 grid).
+// Helmholtz: a known minimum point distance (the fixed-point scale) and r' = k r <= 650.
+bool sketch_tc_supported(const KernelParams& kp) {
+  if (kp.kind == H2_K_EXP) return kp.rmax > 0 && kp.rmax <= 650.0;
+  return kp.kind == H2_K_HELMHOLTZ && kp.rmax > 0 && kp.rmax <= 650.0 && kp.rmin > 0;
+}
 
 int sketch_tc_pass_cols() {
   const char* e = getenv("H2_TC_WIDE");
@@ -417,18 +483,28 @@ int sketch_tc_pass_cols() {
 }
 
 namespace {
-template <int TM, int NPW, int NCOL, int JC>
+template <int KIND, int TM, int NCOL, int JC>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
-               int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride) {
+               int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
+  constexpr int NPW = 16;   // producer warps (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128)
   static bool attr = false;
   constexpr int smem = TcPlan<TM, NCOL, JC>::TOTAL;
   if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<TM, NPW, NCOL, JC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  sketch_tc_kernel<TM, NPW, NCOL, JC><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo, ld,
-                                                                         sstride);
+  sketch_tc_kernel<KIND, TM, NPW, NCOL, JC><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
+                                                                                ld, sstride, hs, wshift, ovf);
+}
+
+template <int KIND>
+void tc_dispatch(int NCOL, dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1,
+                 const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t ss, double hs, int wshift,
+                 uint32_t* ovf) {
+  if (NCOL == 128) tc_launch<KIND, 64, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  else if (NCOL == 64) tc_launch<KIND, 128, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  else tc_launch<KIND, 128, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
 }
 
 // j-split S fills the last wave (1 CTA / SM)
@@ -450,39 +526,43 @@ int pick_split(int tiles, int64_t nunits, int sms) {
 
 // Omega columns are processed sketch_tc_pass_cols() at a time: a pass of more than 64 columns
 // runs the 64-row / 128-column kernel (K evaluated once per 128 columns), narrower passes the
-// 128-row kernel with 32 or 64 columns.  H2_TC_NPW selects 8 or 16 producer warps (default 16),
-// H2_TC_JC the j-chunk of the 128-column kernel (64 or 128, default 128).
-void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+// 128-row kernel with 32 or 64 columns.  Returns false if a Helmholtz entry overflowed the
+// fixed-point scale (the caller then recomputes on the FP64 DMMA path).
+bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st) {
-  if (row1 <= row0 || ncols <= 0) return;
+  if (row1 <= row0 || ncols <= 0) return true;
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const char* npw_env = getenv("H2_TC_NPW");
-  const int npw = (npw_env && atoi(npw_env) == 8) ? 8 : 16;   // measured (N=2^18, 32 cols): 16 -> 163 ms, 8 -> 170
-  const char* jc_env = getenv("H2_TC_JC");
-  const int jc_wide = (jc_env && atoi(jc_env) == 64) ? 64 : 128;
   const int wmax = sketch_tc_pass_cols();
   const int64_t npad = ((n + 127) / 128) * 128;   // 128-j units: every chunk shape tiles it
   const int64_t rows = row1 - row0;
+  const bool helm = kp.kind == H2_K_HELMHOLTZ;
+  // Helmholtz scale 2^E >= 4 max|K| (max|K| <= 1 / r_min): hs = k / 2^E, slice weight
+  // 2^(8s) 2^E 2^-51 / 4; exp: K in (0, 1], weight 2^(8s) 2^-52 / 4
+  const int E = helm ? (int)std::ceil(std::log2(1.0 / kp.rmin)) + 2 : 0;
+  const double hs = helm ? std::ldexp(kp.param, -E) : 0.0;
+  const int wshift = helm ? E - 53 : -54;
   double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
   int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 128, st));
+  uint32_t* ovf = static_cast<uint32_t*>(cache_alloc(sizeof(uint32_t), st));
+  H2_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
   double* part = nullptr;
   int64_t part_elems = 0;
-  coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(X, Yc, Zc, n, npad,
-                                                                                                  kp.inv, C);
+  coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(
+      X, Yc, Zc, n, npad, helm ? kp.param : kp.inv, C);
   H2_CHECK_LAUNCH();
   for (int c0 = 0; c0 < ncols; c0 += wmax) {
     const int nc = std::min(wmax, ncols - c0);
     const int NCOL = nc > 64 ? 128 : nc > 32 ? 64 : 32;
     const int TM = NCOL == 128 ? 64 : 128;
-    const int JC = NCOL == 128 ? jc_wide : 64;
+    const int JC = NCOL == 128 ? 128 : 64;
     const int64_t nchunks = npad / JC;
     const int tiles = div_up(rows, TM);
-    // the split is chosen for the 64-row tiles of the default 128-column pass and shared by
-    // all pass shapes (bitwise identical sketches, test_tc_pass_width_bitwise)
-    const int S = pick_split(div_up(n, 64), npad / 128, sms);   // f(n) only: row shards of a multi-GPU build split j identically
+    // the split is chosen from n only (the 64-row tiles of the default 128-column pass over all
+    // rows) and shared by all pass shapes and row shards: bitwise identical sketches
+    const int S = pick_split(div_up(n, 64), npad / 128, sms);
     if (S > 1 && part_elems < rows * nc * S) {
       if (part) cache_free(part, st);
       part_elems = rows * nc * S;
@@ -495,27 +575,59 @@ void launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     const int64_t ld = S > 1 ? nc : ldy;
     const int64_t ss = S > 1 ? rows * nc : 0;
     const dim3 grid(tiles, S);
-    if (NCOL == 128) {
-      if (JC == 64) {
-        if (npw == 8) tc_launch<64, 8, 128, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-        else tc_launch<64, 16, 128, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      } else {
-        if (npw == 8) tc_launch<64, 8, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-        else tc_launch<64, 16, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      }
-    } else if (NCOL == 64) {
-      if (npw == 8) tc_launch<128, 8, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      else tc_launch<128, 16, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-    } else {
-      if (npw == 8) tc_launch<128, 8, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-      else tc_launch<128, 16, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss);
-    }
+    if (helm) tc_dispatch<H2_K_HELMHOLTZ>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+    else tc_dispatch<H2_K_EXP>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
     H2_CHECK_LAUNCH();
     if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
   }
+  uint32_t h_ovf = 0;
+  if (helm) {
+    H2_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaStreamSynchronize(st));
+  }
   cache_free(C, st);
   cache_free(Bq, st);
+  cache_free(ovf, st);
   if (part) cache_free(part, st);
+  return h_ovf == 0;
+}
+
+// minimum squared distance between distinct points over the near-field leaf pairs (the closest
+// pair of a point set lies in adjacent, hence inadmissible, leaves): one CTA per leaf
+__global__ void min_dist2_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+                                 const double* __restrict__ Z, const int64_t* __restrict__ lb,
+                                 const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                 unsigned long long* __restrict__ out) {
+  const int c = blockIdx.x;
+  double best = INFINITY;
+  for (int e = ptr[c]; e < ptr[c + 1]; ++e) {
+    const int b = idx[e];
+    const int64_t i0 = lb[c], i1 = lb[c + 1], j0 = lb[b], j1 = lb[b + 1];
+    const int64_t nj = j1 - j0;
+    for (int64_t q = threadIdx.x; q < (i1 - i0) * nj; q += blockDim.x) {
+      const int64_t i = i0 + q / nj, j = j0 + q % nj;
+      if (i == j) continue;
+      const double dx = X[i] - X[j], dy = Y[i] - Y[j], dz = Z[i] - Z[j];
+      best = fmin(best, fma(dz, dz, fma(dy, dy, dx * dx)));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best < INFINITY) atomicMin(out, (unsigned long long)__double_as_longlong(best));
+}
+
+double min_near_dist2(const double* X, const double* Y, const double* Z, const int64_t* leaf_begin, int nleaf,
+                      const int32_t* near_ptr, const int32_t* near_idx, cudaStream_t st) {
+  unsigned long long* d = static_cast<unsigned long long*>(cache_alloc(sizeof(unsigned long long), st));
+  H2_CUDA(cudaMemsetAsync(d, 0x7f, sizeof(unsigned long long), st));   // 0x7f7f.. = a huge positive double
+  min_dist2_kernel<<<nleaf, 256, 0, st>>>(X, Y, Z, leaf_begin, near_ptr, near_idx, d);
+  H2_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  H2_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  H2_CUDA(cudaStreamSynchronize(st));
+  cache_free(d, st);
+  double v;
+  std::memcpy(&v, &h, sizeof(v));
+  return v;
 }
 
 }  // namespace h2

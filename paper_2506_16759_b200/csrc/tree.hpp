@@ -28,6 +28,7 @@ struct h2_tree {
   std::vector<std::vector<int64_t>> begin, end;    // per depth
   std::vector<double> xt, yt, zt;                  // tree-order coordinates (zero padded to 3D)
   double diam = 0;                                 // bounding-box diagonal of all points
+  double rmin = -1;                                // min distance of distinct points (near pairs), -1 = not computed
   PairCSR near;                                    // leaf depth
   std::vector<PairCSR> far;                        // per depth
   std::vector<int64_t> D_off;                      // unique near pair offsets (m_s*m_b prefix)
