@@ -5,7 +5,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
+#include <thread>
 
 #include "common.cuh"
 #include "tree.hpp"
@@ -46,33 +50,43 @@ double distance(const BBox& s, const BBox& t, int rule) {  // R1
 }
 
 void make_csr(PairCSR& C, std::vector<std::pair<int32_t, int32_t>>& pairs, int32_t nrows, bool strict) {
-  std::sort(pairs.begin(), pairs.end());
+  // counting sort by row, then each (short) row sorted: O(nnz) instead of a global sort
   C.ptr.assign(nrows + 1, 0);
-  C.idx.resize(pairs.size());
-  for (size_t q = 0; q < pairs.size(); ++q) {
-    C.ptr[pairs[q].first + 1]++;
-    C.idx[q] = pairs[q].second;
-  }
+  for (auto& p : pairs) C.ptr[p.first + 1]++;
   for (int32_t r = 0; r < nrows; ++r) C.ptr[r + 1] += C.ptr[r];
-  C.us.clear();
-  C.ub.clear();
-  for (auto& p : pairs)
-    if (strict ? p.first < p.second : p.first <= p.second) {
-      C.us.push_back(p.first);
-      C.ub.push_back(p.second);
-    }
-  C.uidx.resize(pairs.size());
-  for (size_t q = 0; q < pairs.size(); ++q) {
-    int32_t a = std::min(pairs[q].first, pairs[q].second), b = std::max(pairs[q].first, pairs[q].second);
-    // unique list is sorted by (s, b): binary search
-    size_t lo = 0, hi = C.us.size();
-    while (lo < hi) {
-      size_t mid = (lo + hi) / 2;
-      if (C.us[mid] < a || (C.us[mid] == a && C.ub[mid] < b)) lo = mid + 1;
-      else hi = mid;
-    }
-    C.uidx[q] = (int32_t)lo;
+  C.idx.resize(pairs.size());
+  {
+    std::vector<int32_t> fill(C.ptr.begin(), C.ptr.end() - 1);
+    for (auto& p : pairs) C.idx[fill[p.first]++] = p.second;
   }
+  for (int32_t r = 0; r < nrows; ++r) std::sort(C.idx.begin() + C.ptr[r], C.idx.begin() + C.ptr[r + 1]);
+  // unique pairs (s, b), s <= b (s < b if strict), sorted by (s, b): row s's partners b >= s
+  std::vector<int64_t> uoff(nrows + 1, 0);
+  std::vector<int32_t> first(nrows);   // position in row s of its first partner b >= s (b > s)
+  for (int32_t r = 0; r < nrows; ++r) {
+    const int32_t* b0 = C.idx.data() + C.ptr[r];
+    const int32_t* b1 = C.idx.data() + C.ptr[r + 1];
+    const int32_t* f = strict ? std::upper_bound(b0, b1, r) : std::lower_bound(b0, b1, r);
+    first[r] = (int32_t)(f - b0);
+    uoff[r + 1] = uoff[r] + (b1 - f);
+  }
+  C.us.resize(uoff[nrows]);
+  C.ub.resize(uoff[nrows]);
+  C.uidx.resize(pairs.size());
+  for (int32_t r = 0; r < nrows; ++r)
+    for (int32_t e = C.ptr[r] + first[r], q = 0; e < C.ptr[r + 1]; ++e, ++q) {
+      C.us[uoff[r] + q] = r;
+      C.ub[uoff[r] + q] = C.idx[e];
+    }
+  for (int32_t r = 0; r < nrows; ++r)
+    for (int32_t e = C.ptr[r]; e < C.ptr[r + 1]; ++e) {
+      const int32_t b = C.idx[e];
+      const int32_t a = std::min(r, b), c = std::max(r, b);
+      // position of c among row a's partners >= a (rows are sorted; the symmetric set holds (a, c))
+      const int32_t* b0 = C.idx.data() + C.ptr[a] + first[a];
+      const int32_t* b1 = C.idx.data() + C.ptr[a + 1];
+      C.uidx[e] = (int32_t)(uoff[a] + (std::lower_bound(b0, b1, c) - b0));
+    }
 }
 
 }  // namespace
@@ -91,57 +105,89 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
   T.rule = rule;
   const int Dl = T.Dl = leaf_depth_for(n, leaf);
   auto coord = [&](int64_t orig, int ax) { return X[orig * dim + ax]; };
+  const bool trace = getenv("H2_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[h2 tree] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
 
-  // ---- KD-tree (R4): median split of the longest bbox axis, key (coordinate, original index)
-  T.perm.resize(n);
-  std::iota(T.perm.begin(), T.perm.end(), int64_t(0));
+  // ---- KD-tree (R4): median split of the longest bbox axis, key (coordinate, original index).
+  // The points move as 32-byte records (coordinates + original index): partitions stream through
+  // contiguous memory instead of gathering coordinates through the permutation.
+  struct Pt {
+    double c[3];
+    int64_t orig;
+  };
+  std::vector<Pt> pts(n);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int a = 0; a < 3; ++a) pts[i].c[a] = a < dim ? coord(i, a) : 0.0;
+    pts[i].orig = i;
+  }
+  lap("kd records");
   T.begin.assign(Dl + 1, {});
   T.end.assign(Dl + 1, {});
   T.begin[0] = {0};
   T.end[0] = {n};
+  const int nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   for (int t = 0; t < Dl; ++t) {
     const int64_t nn = int64_t(1) << t;
     T.begin[t + 1].resize(2 * nn);
     T.end[t + 1].resize(2 * nn);
-    for (int64_t c = 0; c < nn; ++c) {
-      int64_t b = T.begin[t][c], e = T.end[t][c], m = e - b;
-      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-      for (int64_t q = b; q < e; ++q)
-        for (int a = 0; a < dim; ++a) {
-          double v = coord(T.perm[q], a);
-          lo[a] = std::min(lo[a], v);
-          hi[a] = std::max(hi[a], v);
+    // the nodes of a depth own disjoint segments: split them over threads (deterministic)
+    auto nodes = [&](int64_t c0, int64_t c1) {
+      for (int64_t c = c0; c < c1; ++c) {
+        const int64_t b = T.begin[t][c], e = T.end[t][c], m = e - b;
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int64_t q = b; q < e; ++q)
+          for (int a = 0; a < dim; ++a) {
+            lo[a] = std::min(lo[a], pts[q].c[a]);
+            hi[a] = std::max(hi[a], pts[q].c[a]);
+          }
+        int axis = 0;
+        double best = hi[0] - lo[0];
+        for (int a = 1; a < dim; ++a)
+          if (hi[a] - lo[a] > best) {
+            best = hi[a] - lo[a];
+            axis = a;
+          }
+        auto less = [axis](const Pt& p, const Pt& q) {
+          return p.c[axis] < q.c[axis] || (p.c[axis] == q.c[axis] && p.orig < q.orig);
+        };
+        const int64_t left = (m + 1) / 2;
+        if (t == Dl - 1) {
+          std::sort(pts.begin() + b, pts.begin() + e, less);   // leaf order = sorted (R4)
+        } else if (m > 1) {
+          std::nth_element(pts.begin() + b, pts.begin() + b + left, pts.begin() + e, less);
         }
-      int axis = 0;
-      double best = hi[0] - lo[0];
-      for (int a = 1; a < dim; ++a)
-        if (hi[a] - lo[a] > best) {
-          best = hi[a] - lo[a];
-          axis = a;
-        }
-      auto less = [&](int64_t p, int64_t q) {
-        double cp = coord(p, axis), cq = coord(q, axis);
-        return cp < cq || (cp == cq && p < q);
-      };
-      int64_t left = (m + 1) / 2;
-      if (t == Dl - 1) {
-        std::sort(T.perm.begin() + b, T.perm.begin() + e, less);   // leaf order = sorted (R4)
-      } else if (m > 1) {
-        std::nth_element(T.perm.begin() + b, T.perm.begin() + b + left, T.perm.begin() + e, less);
+        T.begin[t + 1][2 * c] = b;
+        T.end[t + 1][2 * c] = b + left;
+        T.begin[t + 1][2 * c + 1] = b + left;
+        T.end[t + 1][2 * c + 1] = e;
       }
-      T.begin[t + 1][2 * c] = b;
-      T.end[t + 1][2 * c] = b + left;
-      T.begin[t + 1][2 * c + 1] = b + left;
-      T.end[t + 1][2 * c + 1] = e;
+    };
+    const int nt = (int)std::min<int64_t>(nthreads, nn);
+    if (nt <= 1) {
+      nodes(0, nn);
+    } else {
+      std::vector<std::thread> th;
+      for (int q = 0; q < nt; ++q) th.emplace_back(nodes, nn * q / nt, nn * (q + 1) / nt);
+      for (auto& x : th) x.join();
     }
+    if (trace && t < 4) lap("kd depth");
   }
-  T.xt.assign(n, 0.0);
-  T.yt.assign(n, 0.0);
-  T.zt.assign(n, 0.0);
+  T.perm.resize(n);
+  for (int64_t i = 0; i < n; ++i) T.perm[i] = pts[i].orig;
+  lap("kd-tree");
+  T.xt.resize(n);
+  T.yt.resize(n);
+  T.zt.resize(n);
   for (int64_t i = 0; i < n; ++i) {
-    T.xt[i] = coord(T.perm[i], 0);
-    if (dim > 1) T.yt[i] = coord(T.perm[i], 1);
-    if (dim > 2) T.zt[i] = coord(T.perm[i], 2);
+    T.xt[i] = pts[i].c[0];
+    T.yt[i] = pts[i].c[1];
+    T.zt[i] = pts[i].c[2];
   }
   {
     double lo[3] = {1e308, 1e308, 1e308}, hi[3] = {-1e308, -1e308, -1e308};
@@ -157,6 +203,7 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
                    : 0.0;
   }
 
+  lap("coords");
   // ---- bounding boxes per depth (tree order, zero padded)
   std::vector<std::vector<BBox>> box(Dl + 1);
   for (int t = Dl; t >= 0; --t) {
@@ -186,6 +233,7 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
     }
   }
 
+  lap("bboxes");
   // ---- dual-tree traversal (L127), depth by depth
   std::vector<std::pair<int32_t, int32_t>> cur{{0, 0}}, nxt, near;
   T.far.assign(Dl + 1, PairCSR{});
@@ -216,6 +264,7 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
     make_csr(T.far[t], far, 1 << t, true);
     cur.swap(nxt);
   }
+  lap("traversal");
   make_csr(T.near, near, 1 << Dl, false);
   for (int t = 0; t <= Dl; ++t)
     for (int64_t r = 0; r < (int64_t(1) << t); ++r) {
@@ -230,6 +279,7 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
     int64_t mb = T.end[Dl][T.near.ub[q]] - T.begin[Dl][T.near.ub[q]];
     T.D_off[q + 1] = T.D_off[q] + ms * mb;
   }
+  lap("near csr");
 }
 
 namespace {
