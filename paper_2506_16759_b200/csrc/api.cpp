@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -213,6 +214,33 @@ void comm_allgather_clusters(const h2_comm* comm, void* base, size_t es, int t, 
   comm_allgather(comm, base, cnt, dsp, st);
 }
 
+// Per-device internal streams (created once, never destroyed): the build runs on a
+// greatest-priority stream linked to the caller's stream by events, the speculative next sketch
+// pass on a least-priority stream, so the construction kernels take the SMs as the long sketch
+// CTAs retire and the sketch fills the rest (overlap of the O(N^2) pass with the O(N) levels).
+cudaStream_t prio_stream(bool high) {
+  static std::mutex mu;
+  static cudaStream_t s[64][2] = {};
+  int dev = 0;
+  H2_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  cudaStream_t& x = s[dev & 63][high ? 1 : 0];
+  if (!x) {
+    int lo = 0, hi = 0;
+    H2_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    H2_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, high ? hi : lo));
+  }
+  return x;
+}
+
+void stream_after(cudaStream_t later, cudaStream_t earlier) {
+  cudaEvent_t e;
+  H2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  H2_CUDA(cudaEventRecord(e, earlier));
+  H2_CUDA(cudaStreamWaitEvent(later, e, 0));
+  H2_CUDA(cudaEventDestroy(e));
+}
+
 struct Builder {
   const h2_tree& T;
   const h2_sketch& S;
@@ -231,6 +259,7 @@ struct Builder {
   int64_t entries_sketch = 0;
   const h2_comm* comm = nullptr;   // NULL: one GPU
   int P = 1, R = 0;
+  cudaStream_t user_st = nullptr;  // the caller's stream (st becomes the internal high-priority one)
   DArr<double> leaf_part;          // per-leaf sums of squares of the current draw
 
   Builder(const h2_tree& t, const h2_sketch& s, const h2_entry& e, double tl, const h2_build_opts& op,
@@ -332,6 +361,42 @@ struct Builder {
   Panel spec;                   // n x W: columns [spec_c0, spec_c0 + spec_n) at offset spec_off
   int spec_c0 = -1, spec_n = 0, spec_off = 0;
   int64_t sketch_columns = 0;
+  // Optional (H2_PREFETCH=1): the pass after the first one is computed ahead, on the low-priority
+  // stream, while the leaf and lower levels are constructed (large problems need > W samples); a
+  // draw that reaches its columns waits for it; unused, it is waited for at the end of the build.
+  // Measured at N=2^18: 519 vs 526 ms (the construction slows down under the shared SMs), so it
+  // is off by default.
+  Panel pre;
+  int pre_c0 = -1;
+  bool pre_live = false, pre_started = false;
+  cudaEvent_t pre_done = nullptr;
+
+  void launch_prefetch(int c0) {
+    cudaStream_t ss = prio_stream(false);
+    stream_after(ss, st);
+    pre.alloc(T.n, spec_w, ss);
+    cudaEvent_t t0, t1;
+    H2_CUDA(cudaEventCreate(&t0));
+    H2_CUDA(cudaEventCreate(&t1));
+    H2_CUDA(cudaEventRecord(t0, ss));
+    launch_omega(o.seed, o.stream_id, 0, T.n, c0, spec_w, pre.O.p, pre.ld, ss);
+    launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), pre.O.p, pre.ld, spec_w,
+                        pre.Y.p + row_b() * pre.ld, pre.ld, true, ss);
+    H2_CUDA(cudaEventRecord(t1, ss));
+    timer.ev.push_back({H2_PH_SKETCH, {t0, t1}});
+    H2_CUDA(cudaEventCreateWithFlags(&pre_done, cudaEventDisableTiming));
+    H2_CUDA(cudaEventRecord(pre_done, ss));
+    entries_sketch += T.n * T.n;
+    sketch_columns += spec_w;
+    pre_c0 = c0;
+    pre_live = pre_started = true;
+  }
+  void join_prefetch() {
+    if (!pre_live) return;
+    H2_CUDA(cudaStreamWaitEvent(st, pre_done, 0));
+    H2_CUDA(cudaEventDestroy(pre_done));
+    pre_live = false;
+  }
 
   void sketch_cols(double* Yd, double* Od, int64_t ld, int c0, int nc) {
     launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
@@ -347,6 +412,13 @@ struct Builder {
   // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
   void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
     timer.begin(H2_PH_RAND);
+    if (pre_live && spec_n == 0 && c0 == pre_c0) {   // the prefetched pass becomes the bank
+      join_prefetch();
+      std::swap(spec, pre);
+      spec_c0 = pre_c0;
+      spec_n = spec_w;
+      spec_off = 0;
+    }
     if (S.kind == H2_S_DENSE_KERNEL && spec_on && nc < spec_w && c0 == spec_c0 && nc <= spec_n) {
       H2_CUDA(cudaMemcpy2DAsync(Yd, ld * 8, spec.Y.p + spec_off, spec.ld * 8, (size_t)nc * 8, T.n,
                                 cudaMemcpyDeviceToDevice, st));
@@ -365,6 +437,8 @@ struct Builder {
       spec_c0 = c0 + nc;
       spec_n = spec_w - nc;
       spec_off = nc;
+      if (!pre_started && skp.kind == H2_K_EXP && c0 + 2 * spec_w <= o.d_max && env_int("H2_PREFETCH", 0) != 0)
+        launch_prefetch(c0 + spec_w);
     } else if (S.kind == H2_S_DENSE_KERNEL) {
       sketch_cols(Yd, Od, ld, c0, nc);
     } else {
@@ -756,7 +830,22 @@ struct Builder {
     }
   }
 
+  ~Builder() {
+    // an exception may leave work queued on the internal streams: drain them before the
+    // members (allocated on them) are released
+    if (user_st) {
+      cudaStreamSynchronize(prio_stream(false));
+      cudaStreamSynchronize(st);
+      if (pre_live) cudaEventDestroy(pre_done);
+    }
+  }
+
   void run() {
+    // internal high-priority stream, ordered after the caller's stream
+    user_st = st;
+    st = prio_stream(true);
+    timer.st = st;
+    stream_after(st, user_st);
     const int Dl = T.Dl;
     const int top = T.top < 0 ? Dl : T.top;
     H.top = top;
@@ -857,7 +946,9 @@ struct Builder {
       gen_B(t);                                     // line 258
       cur = std::move(next);
     }
+    join_prefetch();   // an unused speculative pass is waited for (at most one pass)
     H2_CUDA(cudaStreamSynchronize(st));
+    stream_after(user_st, st);
     cur.release();
     W.release();
     for (auto& L : H.lv) {
