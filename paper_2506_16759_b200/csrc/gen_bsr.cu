@@ -6,7 +6,9 @@
 namespace h2 {
 
 // ------------------------------------------------------------------------------------------
-// batchedGen: one CTA per unique block (grid-stride), entries written row-major, coalesced.
+// batchedGen: one CTA per unique block (grid-stride).  Warp w takes rows i = w, w+8, ...; its
+// lanes the columns (coalesced row-major writes); the column coordinates of a 256-column chunk
+// are staged in shared memory, the row point is a warp-uniform load.
 // ------------------------------------------------------------------------------------------
 template <int KIND>
 __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, const double* __restrict__ Yc,
@@ -15,6 +17,7 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
   __shared__ double cx[256], cy[256], cz[256];
   __shared__ double tab[64];
   fill_exp_table(tab);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
     const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
@@ -26,17 +29,18 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
       const int nj = min(256, nc - j0);
       __syncthreads();
       if (threadIdx.x < nj) {
-        int p = ci[j0 + threadIdx.x];
+        const int p = ci[j0 + threadIdx.x];
         cx[threadIdx.x] = X[p];
         cy[threadIdx.x] = Yc[p];
         cz[threadIdx.x] = Zc[p];
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < m * nj; e += blockDim.x) {
-        int i = e / nj, j = e - i * nj;
-        int p = ri[i];
-        double r2 = dist2(X[p], Yc[p], Zc[p], cx[j], cy[j], cz[j]);
-        out[(int64_t)i * nc + j0 + j] = kernel_of_r2<KIND>(r2, param, inv, tab);
+      for (int i = warp; i < m; i += 8) {
+        const int p = ri[i];
+        const double xi = X[p], yi = Yc[p], zi = Zc[p];
+        double* orow = out + (int64_t)i * nc + j0;
+        for (int j = lane; j < nj; j += 32)
+          orow[j] = kernel_of_r2<KIND>(dist2(xi, yi, zi, cx[j], cy[j], cz[j]), param, inv, tab);
       }
     }
   }

@@ -21,6 +21,7 @@ p = argparse.ArgumentParser()
 p.add_argument("workload")
 p.add_argument("--reps", type=int, default=1)
 p.add_argument("--s", type=float, default=0.1)
+p.add_argument("--s-update", type=float, default=None, help="tol_safety of the update build (configs[4]); default --s")
 p.add_argument("--d-blk", type=int, default=32)
 p.add_argument("--probes", type=int, default=16)
 a = p.parse_args()
@@ -49,7 +50,8 @@ for r in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, update=update,
+    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk,
+                tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update,
                 d_max=w.get("d_max", 512))
     e1.record()
     e1.synchronize()
