@@ -112,8 +112,10 @@ typedef int (*h2_sketch_fn)(void* ctx, const h2_sketch_req* req);
 
 /* H^2 + low-rank operator M = A_H + U U^T (BASELINE configs[4]): `base` is an
  * h2_matrix built on the SAME h2_tree, U is dev n x rank row-major (tree-order rows, leading dim
- * ld_U).  As a sketch: Y = A_H Omega (h2_matvec) + U (U^T Omega).  As an entry evaluator:
- * D / B blocks of M extracted from A_H's D / B and expanded bases plus U U^T. */
+ * ld_U).  As a sketch: Y = A_H Omega (h2_matvec) + U (U^T Omega); rank 0 (U NULL) gives the pure
+ * O(N) H^2-matvec sketch Y = A_H Omega (K_blk of an existing H^2, e.g. one of
+ * K at a tighter tolerance).  As an entry evaluator (rank >= 1): D / B
+ * blocks of M extracted from A_H's D / B and expanded bases plus U U^T. */
 enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1, H2_S_H2_LOWRANK = 2 };
 typedef struct {
   int32_t kind;       /* H2_S_DENSE_KERNEL: Y = K Omega with the built-in kernel below (O(N^2)) */

@@ -1262,7 +1262,10 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
       const int32_t r = which == 0 ? sketch->rank : entry->rank;
       const int64_t ldu = which == 0 ? sketch->ld_U : entry->ld_U;
       H2_REQUIRE(base && base->tree.get() == tree, "h2_build: the H2+low-rank operator needs a base built on this tree");
-      H2_REQUIRE(U && r >= 1 && r <= 1024 && ldu >= r, "h2_build: H2+low-rank operator needs U (n x rank, ld >= rank)");
+      // rank 0 (sketch only): Y = A_H Omega, the O(N) H^2-matvec sketch of an existing H^2 (S§8(f) NEXT #1)
+      const bool pure = which == 0 && r == 0;
+      H2_REQUIRE(pure || (U && r >= 1 && r <= 1024 && ldu >= r),
+                 "h2_build: H2+low-rank operator needs U (n x rank, ld >= rank)");
     }
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})

@@ -234,7 +234,7 @@ def _stats_dict(s):
 
 
 def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, comm=None,
-          **opts):
+          h2_sketch=None, **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
@@ -243,7 +243,9 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  update=(H_base, U):
     recompress M = H_base + U U^T (H_base built on this tree, U a (n, r) float64
     CUDA tensor in tree order) with the library's H^2-matvec + low-rank sketch and entry
-    extraction.  comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
+    extraction.  h2_sketch=H_base: the O(N) black-box sketch Y = A_H Omega of an existing H^2 on
+    this tree (e.g. K at a tighter tolerance), entries from ``kernel``.
+    comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
     by subtrees (h2_build_dist); call ``H.allgather(comm)`` before matvec / block export.
     opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
     tol_safety, p_os, norm, max_rank, seed, stream_id)."""
@@ -260,6 +262,11 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         keep += [Hb, U]
         sk.kind = L.H2_S_H2_LOWRANK
         sk.base, sk.U, sk.ld_U, sk.rank = Hb._h, U.data_ptr(), U.stride(0), U.shape[1]
+    elif h2_sketch is not None:
+        assert h2_sketch.tree is tree, "h2_sketch: the H^2 must be built on the same Tree"
+        keep.append(h2_sketch)
+        sk.kind = L.H2_S_H2_LOWRANK
+        sk.base, sk.U, sk.ld_U, sk.rank = h2_sketch._h, None, 0, 0
     elif sketch is None:
         sk.kind = L.H2_S_DENSE_KERNEL
     else:

@@ -82,3 +82,21 @@ def test_update_zero_lowrank_reproduces_base_ranks(setup):
     x = torch.randn(s["n"], 4, dtype=torch.float64, device="cuda")
     yb, yu = Hb.matvec(x), Hu.matvec(x)
     assert (torch.linalg.norm(yu - yb) / torch.linalg.norm(yb)).item() <= 2 * s["tol"]
+
+
+def test_h2_matvec_sketch_recompression():
+    """S§8(f) NEXT #1: the O(N) black-box sketch Y = A_H Omega of an H^2 of K built at a tighter
+    tolerance drives the construction at tol; entries from the kernel.  The
+    result meets 2 tol against dense K, with ranks close to the dense-sketch build."""
+    X = uniform_points(6000, 3, 4)
+    T = g.Tree(X, 64)
+    K = kernels.KernelOperator("exp", 0.2, X[T.perm]).dense()
+    Hb = g.build(T, ("exp", 0.2), 1e-9)
+    H = g.build(T, ("exp", 0.2), 1e-6, h2_sketch=Hb)
+    Hd = g.build(T, ("exp", 0.2), 1e-6)
+    P = np.random.default_rng(2).standard_normal((T.n, 8))
+    KP = K @ P
+    err = np.linalg.norm(H.matvec(torch.from_numpy(P).cuda()).cpu().numpy() - KP) / np.linalg.norm(KP)
+    assert err <= 2e-6, err
+    for t in range(H.top_depth, T.leaf_depth + 1):
+        assert abs(H.rank(t).mean() - Hd.rank(t).mean()) <= 0.1 * Hd.rank(t).mean() + 2

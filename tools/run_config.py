@@ -24,6 +24,9 @@ p.add_argument("--s", type=float, default=0.1)
 p.add_argument("--s-update", type=float, default=None, help="tol_safety of the update build (configs[4]); default --s")
 p.add_argument("--d-blk", type=int, default=32)
 p.add_argument("--probes", type=int, default=16)
+p.add_argument("--bootstrap", type=float, default=None,
+               help="S8(f) NEXT #1: build an H^2 of K at this tighter tol (dense sketch, timed separately), "
+                    "then the timed build at the workload tol with its O(N) H^2-matvec sketch")
 a = p.parse_args()
 w = dict(WORKLOADS[a.workload])
 X = w["points"]()
@@ -46,12 +49,20 @@ if "update_rank" in w:      # configs[4]: base H^2 of A (untimed setup, like PAP
     out["base_samples"] = Hbase.samples
     U = torch.from_numpy(lowrank_factor(n, w["update_rank"])).cuda()
     update = (Hbase, U)
+h2sk = None
+if a.bootstrap is not None:
+    t0 = time.perf_counter()
+    h2sk = g.build(T, kern, a.bootstrap, d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, d_max=1024)
+    torch.cuda.synchronize()
+    out["bootstrap_tol"] = a.bootstrap
+    out["bootstrap_build_s"] = time.perf_counter() - t0
+    out["bootstrap_samples"] = h2sk.samples
 for r in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk,
-                tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update,
+                tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk,
                 d_max=w.get("d_max", 512))
     e1.record()
     e1.synchronize()
