@@ -1023,6 +1023,7 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
     a.xh = xh[t].p;
     a.ldh = q;
     a.q = q;
+    a.max_out = L.max_k;
     launch_upward(a, st);
   }
   // couplings  y^_s += sum_{b in F_s} B_{s,b} x^_b
@@ -1066,6 +1067,7 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
     a.q = q;
     a.alpha = (t == Dl) ? alpha : 1.0;
     a.accumulate = 1;
+    a.max_out = L.max_m;
     launch_downward(a, st);
   }
   // dense leaves  y += alpha sum_{b in N} D x

@@ -2,6 +2,7 @@
 // which is also the convergence test of §III-B (L361, "QR decomposition ... smallest absolute
 // value of the diagonal"; reading R12), the ID epilogue (T = R11^{-1} R12, Eq.(3)) and the
 // shrink / Omega upsweep (batchedShrink L222/L251, batchedGemm L223/L252).
+#include "alloc.hpp"
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -264,8 +265,10 @@ void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
 // per launch at the top levels (32 clusters, k ~ 210).
 // ------------------------------------------------------------------------------------------
 constexpr int ID_CB = 32;
-__global__ void __launch_bounds__(256) id_kernel(IdArgs a) {
-  extern __shared__ double sB[];           // k x ID_CB, row stride ID_CB + 1
+__global__ void __launch_bounds__(256) id_kernel(IdArgs a, double* __restrict__ gpanel) {
+  extern __shared__ double smB[];          // k x ID_CB, row stride ID_CB + 1
+  // ranks beyond the shared-memory panel (k > ~770) use a per-CTA panel in global memory
+  double* sB = gpanel ? gpanel + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * a.max_k * (ID_CB + 1) : smB;
   __shared__ double sD[ID_CB][ID_CB + 1];  // diagonal block R(i0:i1, i0:i1)
   const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c], k = a.k[c], d = a.d;
@@ -327,14 +330,20 @@ void launch_id(const IdArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
   const int ny = std::max(1, div_up(a.max_red, ID_CB));
   const size_t smem = sizeof(double) * (size_t)std::max(a.max_k, 1) * (ID_CB + 1);
-  H2_REQUIRE(smem <= 200 * 1024, "id_kernel: rank too large for the shared-memory T panel");
   static bool attr = false;   // static sD + dynamic may exceed 48 KB for any k > 150
   if (!attr) {
     H2_CUDA(cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  id_kernel<<<dim3(a.nclusters, ny), 256, smem, st>>>(a);
-  H2_CHECK_LAUNCH();
+  if (smem <= 200 * 1024) {
+    id_kernel<<<dim3(a.nclusters, ny), 256, smem, st>>>(a, nullptr);
+    H2_CHECK_LAUNCH();
+  } else {
+    double* g = static_cast<double*>(cache_alloc(smem * (size_t)a.nclusters * ny, st));
+    id_kernel<<<dim3(a.nclusters, ny), 256, 0, st>>>(a, g);
+    H2_CHECK_LAUNCH();
+    cache_free(g, st);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -153,6 +153,7 @@ struct UpArgs {
   double* xh;
   int64_t ldh;
   int q;
+  int32_t max_out;        // max k over the clusters (grid sizing; 0: derived per launch as 1024)
 };
 void launch_upward(const UpArgs& a, cudaStream_t st);
 // yout(ioff[c]+j, :) = beta_in*yout + alpha * sum_i X_c(j,i) yh(roff[c]+i, :)     (downward / leaf out)
@@ -171,6 +172,7 @@ struct DownArgs {
   int q;
   double alpha;
   int accumulate;          // 1: yout += ..., 0: yout = ...
+  int32_t max_out;        // max m over the clusters (grid sizing)
 };
 void launch_downward(const DownArgs& a, cudaStream_t st);
 // y(rows of s) += alpha * sum_b Blk(s,b) x(rows of b)   (coupling B / dense D products)
