@@ -266,7 +266,7 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
     S = 1;
     // chosen from n only (as if all rows were computed): the row shards of a multi-GPU build
     // then split j identically and produce bitwise the same rows as one GPU
-    const int64_t tiles_n = div_up(n, SK_VARS[var].rows);
+    const int64_t tiles_n = div_up(n, SK_VARS[var].rows * 8);   // the 8-GPU row shard (as sketch_tc.cu)
     for (int s = 1; s <= 4; ++s) {
       int64_t units = tiles_n * s;
       if (n / s < 4096 && s > 1) break;

@@ -560,9 +560,10 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
     const int JC = NCOL == 128 ? 128 : 64;
     const int64_t nchunks = npad / JC;
     const int tiles = div_up(rows, TM);
-    // the split is chosen from n only (the 64-row tiles of the default 128-column pass over all
-    // rows) and shared by all pass shapes and row shards: bitwise identical sketches
-    const int S = pick_split(div_up(n, 64), npad / 128, sms);
+    // the split is chosen from n only -- for the row shard of the largest rank count of one box
+    // (8 GPUs: its 64-row tiles fill the waves there; one GPU just runs more waves) -- and shared
+    // by all pass shapes and row shards: bitwise identical sketches for any P <= 8
+    const int S = pick_split(div_up(n, 64 * 8), npad / 128, sms);
     if (S > 1 && part_elems < rows * nc * S) {
       if (part) cache_free(part, st);
       part_elems = rows * nc * S;
