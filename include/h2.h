@@ -116,7 +116,7 @@ typedef int (*h2_sketch_fn)(void* ctx, const h2_sketch_req* req);
  * O(N) H^2-matvec sketch Y = A_H Omega (K_blk of an existing H^2, e.g. one of
  * K at a tighter tolerance).  As an entry evaluator (rank >= 1): D / B
  * blocks of M extracted from A_H's D / B and expanded bases plus U U^T. */
-enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1, H2_S_H2_LOWRANK = 2 };
+enum { H2_S_DENSE_KERNEL = 0, H2_S_CALLBACK = 1, H2_S_H2_LOWRANK = 2, H2_S_DENSE_MATRIX = 3 };
 typedef struct {
   int32_t kind;       /* H2_S_DENSE_KERNEL: Y = K Omega with the built-in kernel below (O(N^2)) */
   h2_kernel kern;     /* H2_S_CALLBACK: fn(ctx, req);  H2_S_H2_LOWRANK: base + U                 */
@@ -126,6 +126,11 @@ typedef struct {
   const double* U;
   int64_t ld_U;
   int32_t rank;
+  /* H2_S_DENSE_MATRIX (an explicit operator such as a frontal matrix,
+   * PAPER.md L443/L487): Y = A Omega with A dev n x n row-major in TREE order (leading dim ld_A),
+   * one FP64 GEMM per draw (cuBLAS, the plain library GEMM). */
+  const double* A;
+  int64_t ld_A;
 } h2_sketch;
 
 /* Batched entry evaluator ("batched entry generator ... evaluate all D or B at a
@@ -146,7 +151,7 @@ typedef struct {
 } h2_block_batch;
 typedef int (*h2_entry_fn)(void* ctx, const h2_block_batch* batch);
 
-enum { H2_E_BUILTIN = 0, H2_E_CALLBACK = 1, H2_E_H2_LOWRANK = 2 };
+enum { H2_E_BUILTIN = 0, H2_E_CALLBACK = 1, H2_E_H2_LOWRANK = 2, H2_E_DENSE_MATRIX = 3 };
 typedef struct {
   int32_t kind;       /* H2_E_BUILTIN: entries of `kern` at the tree's coordinates              */
   h2_kernel kern;     /* H2_E_H2_LOWRANK: entries of base + U U^T (see h2_sketch)               */
@@ -156,6 +161,8 @@ typedef struct {
   const double* U;
   int64_t ld_U;
   int32_t rank;
+  const double* A;    /* H2_E_DENSE_MATRIX: entries A[i * ld_A + j] (tree-order, dev)           */
+  int64_t ld_A;
 } h2_entry;
 
 /* ---------------------------------------------------------------------------------------

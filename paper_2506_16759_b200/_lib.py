@@ -14,8 +14,8 @@ H2_OK, H2_ERR_INVALID_ARG, H2_ERR_OOM, H2_ERR_CUDA = 0, -1, -2, -3
 H2_ERR_CALLBACK, H2_ERR_NOT_CONVERGED, H2_ERR_NONFINITE = -5, -6, -7
 H2_DIST_CENTER, H2_DIST_BOX = 0, 1
 H2_K_EXP, H2_K_HELMHOLTZ = 0, 1
-H2_S_DENSE_KERNEL, H2_S_CALLBACK, H2_S_H2_LOWRANK = 0, 1, 2
-H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK = 0, 1, 2
+H2_S_DENSE_KERNEL, H2_S_CALLBACK, H2_S_H2_LOWRANK, H2_S_DENSE_MATRIX = 0, 1, 2, 3
+H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK, H2_E_DENSE_MATRIX = 0, 1, 2, 3
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT = range(6)
 H2_SKETCH_OMEGA_QUARTERS = 1
@@ -44,7 +44,8 @@ SKETCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(h2_sketch_req))
 
 class h2_sketch(C.Structure):
     _fields_ = [("kind", C.c_int32), ("kern", h2_kernel), ("fn", SKETCH_FN), ("ctx", C.c_void_p),
-                ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32)]
+                ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32),
+                ("A", C.c_void_p), ("ld_A", C.c_int64)]
 
 
 class h2_block_batch(C.Structure):
@@ -58,7 +59,8 @@ ENTRY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(h2_block_batch))
 
 class h2_entry(C.Structure):
     _fields_ = [("kind", C.c_int32), ("kern", h2_kernel), ("fn", ENTRY_FN), ("ctx", C.c_void_p),
-                ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32)]
+                ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32),
+                ("A", C.c_void_p), ("ld_A", C.c_int64)]
 
 
 class h2_build_opts(C.Structure):

@@ -446,7 +446,9 @@ struct Builder {
       timer.end();
       timer.begin(H2_PH_SKETCH);
       sketch_columns += nc;
-      if (S.kind == H2_S_H2_LOWRANK) {
+      if (S.kind == H2_S_DENSE_MATRIX) {
+        dense_matrix_sketch(S.A, S.ld_A, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, st);
+      } else if (S.kind == H2_S_H2_LOWRANK) {
         // K_blk = A_H Omega + U (U^T Omega)
         matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
         DArr<double> scr;
@@ -497,6 +499,8 @@ struct Builder {
     timer.begin(H2_PH_GEN);
     if (E.kind == H2_E_BUILTIN) {
       launch_gen(ekp, T.d_x, T.d_y, T.d_z, g, st);
+    } else if (E.kind == H2_E_DENSE_MATRIX) {
+      launch_gen_dense(E.A, E.ld_A, g, st);
     } else {
       DArr<int32_t> m, nc, ld;
       DArr<int64_t> ro, co;
@@ -1251,10 +1255,12 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
     H2_REQUIRE(o.tol_rule == H2_TOL_RMS || o.tol_rule == H2_TOL_LITERAL, "h2_build: bad tol_rule");
     H2_REQUIRE(o.tol_rule != H2_TOL_LITERAL || o.norm > 0, "h2_build: literal tolerance needs opts.norm > 0");
     H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
-                   sketch->kind == H2_S_H2_LOWRANK,
+                   sketch->kind == H2_S_H2_LOWRANK ||
+                   (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= tree->n),
                "h2_build: bad sketch");
     H2_REQUIRE(entry->kind == H2_E_BUILTIN || (entry->kind == H2_E_CALLBACK && entry->fn) ||
-                   entry->kind == H2_E_H2_LOWRANK,
+                   entry->kind == H2_E_H2_LOWRANK ||
+                   (entry->kind == H2_E_DENSE_MATRIX && entry->A && entry->ld_A >= tree->n),
                "h2_build: bad entry");
     for (int which = 0; which < 2; ++which) {
       const bool upd = which == 0 ? sketch->kind == H2_S_H2_LOWRANK : entry->kind == H2_E_H2_LOWRANK;

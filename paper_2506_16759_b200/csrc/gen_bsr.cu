@@ -46,6 +46,29 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
   }
 }
 
+// batchedGen from an explicit matrix (H2_E_DENSE_MATRIX): out(i, j) = A[ri[i] * lda + ci[j]]
+__global__ void __launch_bounds__(256) gen_dense_kernel(const double* __restrict__ A, int64_t lda, GenArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t u = a.ulist ? a.ulist[q] : q;
+    const int s = a.us[u], b = a.ub[u];
+    const int m = a.cnt[s], nc = a.cnt[b];
+    const int32_t* ri = a.idx + a.off[s];
+    const int32_t* ci = a.idx + a.off[b];
+    double* out = a.out + a.out_off[u];
+    for (int i = warp; i < m; i += 8) {
+      const double* arow = A + (int64_t)ri[i] * lda;
+      for (int j = lane; j < nc; j += 32) out[(int64_t)i * nc + j] = arow[ci[j]];
+    }
+  }
+}
+
+void launch_gen_dense(const double* A, int64_t lda, const GenArgs& a, cudaStream_t st) {
+  if (a.nblocks <= 0) return;
+  gen_dense_kernel<<<(int)std::min<int64_t>(a.nblocks, 148 * 32), 256, 0, st>>>(A, lda, a);
+  H2_CHECK_LAUNCH();
+}
+
 void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, const GenArgs& a,
                 cudaStream_t st) {
   if (a.nblocks <= 0) return;

@@ -50,6 +50,10 @@ struct GenArgs {
 };
 void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, const GenArgs& a,
                 cudaStream_t st);
+void launch_gen_dense(const double* A, int64_t lda, const GenArgs& a, cudaStream_t st);
+// Y(rows) = A(rows, :) Omega for a dense row-major operator (cuBLAS DGEMM, the plain library GEMM)
+void dense_matrix_sketch(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, const double* Om,
+                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st);
 // fill the pointer / size arrays of an h2_block_batch for a user entry callback
 void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* roff, int64_t* coff, double** outp,
                            int32_t* ld, cudaStream_t st);

@@ -1,6 +1,9 @@
 // batchedRand (PAPER.md L203/L216/L246, L384 "generated in a single kernel") and the built-in
 // dense-kernel sketch Y = K Omega (Algorithm 1 line 1 with K_blk = the dense kernel matrix,
 // BASELINE configs[1]); plus the sketch-norm reduction used by the tolerance rule (R10).
+#include <cublas_v2.h>
+#include <mutex>
+
 #include "common.cuh"
 #include "alloc.hpp"
 #include "kernels.hpp"
@@ -388,6 +391,26 @@ void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double
   H2_CHECK_LAUNCH();
   sumsq_final_kernel<<<1, 1024, 0, st>>>(scratch, np, accum, nonfinite);
   H2_CHECK_LAUNCH();
+}
+
+// Y (rows x ncols, row-major, ldy) = A(rows, :) (row-major, lda) Omega (n x ncols, row-major, ldo):
+// in column-major terms Y^T = Omega^T A(rows,:)^T, one DGEMM.
+void dense_matrix_sketch(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, const double* Om,
+                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st) {
+  if (row1 <= row0 || ncols <= 0) return;
+  static std::mutex mu;
+  static cublasHandle_t handles[64] = {};
+  int dev = 0;
+  H2_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  cublasHandle_t& h = handles[dev & 63];
+  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw Error(H2_ERR_CUDA, "cublasCreate failed");
+  cublasSetStream(h, st);
+  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);   // FP64 (DMMA tensor cores when profitable), no reduced precision
+  const double one = 1.0, zero = 0.0;
+  const cublasStatus_t r = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, ncols, (int)(row1 - row0), (int)n, &one, Om,
+                                       (int)ldo, A + row0 * lda, (int)lda, &zero, Y, (int)ldy);
+  if (r != CUBLAS_STATUS_SUCCESS) throw Error(H2_ERR_CUDA, "cublasDgemm failed: " + std::to_string((int)r));
 }
 
 }  // namespace h2

@@ -234,7 +234,7 @@ def _stats_dict(s):
 
 
 def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, comm=None,
-          h2_sketch=None, **opts):
+          h2_sketch=None, dense=None, **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
@@ -245,6 +245,8 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     CUDA tensor in tree order) with the library's H^2-matvec + low-rank sketch and entry
     extraction.  h2_sketch=H_base: the O(N) black-box sketch Y = A_H Omega of an existing H^2 on
     this tree (e.g. K at a tighter tolerance), entries from ``kernel``.
+    dense=A: an explicit (n, n) float64 CUDA operator in TREE order (row-major): sketch A Omega
+    (one DGEMM per draw) and entries A[i, j] (S§8(f) NEXT #4, a frontal-matrix stand-in).
     comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
     by subtrees (h2_build_dist); call ``H.allgather(comm)`` before matvec / block export.
     opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
@@ -262,6 +264,12 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         keep += [Hb, U]
         sk.kind = L.H2_S_H2_LOWRANK
         sk.base, sk.U, sk.ld_U, sk.rank = Hb._h, U.data_ptr(), U.stride(0), U.shape[1]
+    elif dense is not None:
+        assert dense.is_cuda and dense.dtype == torch.float64 and dense.shape == (tree.n, tree.n)
+        assert dense.stride(1) == 1
+        keep.append(dense)
+        sk.kind = L.H2_S_DENSE_MATRIX
+        sk.A, sk.ld_A = dense.data_ptr(), dense.stride(0)
     elif h2_sketch is not None:
         assert h2_sketch.tree is tree, "h2_sketch: the H^2 must be built on the same Tree"
         keep.append(h2_sketch)
@@ -289,7 +297,10 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         sk.fn = cb
     en = L.h2_entry()
     en.kern = kern
-    if update is not None:
+    if dense is not None:
+        en.kind = L.H2_E_DENSE_MATRIX
+        en.A, en.ld_A = dense.data_ptr(), dense.stride(0)
+    elif update is not None:
         en.kind = L.H2_E_H2_LOWRANK
         en.base, en.U, en.ld_U, en.rank = sk.base, sk.U, sk.ld_U, sk.rank
     elif entry is None:

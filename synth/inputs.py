@@ -58,6 +58,12 @@ WORKLOADS = {
     "cov3d_5k": dict(points=lambda: uniform_points(5000, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     "ie3d_4k": dict(points=lambda: grid_points((16, 16, 16), 1.0 / 16), kernel="helmholtz", param=3.0,
                     leaf=64, tol=1e-4),
+    # an explicit dense operator (frontal-matrix stand-in) -- the exp kernel
+    # matrix materialised on the GPU in tree order; sketch = DGEMM, entries = lookups
+    "dense_op_32k": dict(points=lambda: uniform_points(1 << 15, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6,
+                         dense=True),
+    "dense_op_64k": dict(points=lambda: uniform_points(1 << 16, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6,
+                         dense=True),
 }
 
 

@@ -50,6 +50,13 @@ if "update_rank" in w:      # configs[4]: base H^2 of A (untimed setup, like PAP
     U = torch.from_numpy(lowrank_factor(n, w["update_rank"])).cuda()
     update = (Hbase, U)
 h2sk = None
+dense = None
+if w.get("dense"):   # NEXT #4: materialise the operator in tree order (row blocks: no n x n temporaries)
+    Xt = torch.from_numpy(X[T.perm]).cuda()
+    dense = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for r0 in range(0, n, 4096):
+        dense[r0:r0 + 4096] = torch.exp(-torch.cdist(Xt[r0:r0 + 4096], Xt) / w["param"])
+    out["dense_operator_GB"] = dense.numel() * 8 / 1e9
 if a.bootstrap is not None:
     t0 = time.perf_counter()
     h2sk = g.build(T, kern, a.bootstrap, d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, d_max=1024)
@@ -62,7 +69,7 @@ for r in range(a.reps):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk,
-                tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk,
+                tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk, dense=dense,
                 d_max=w.get("d_max", 512))
     e1.record()
     e1.synchronize()
@@ -76,7 +83,9 @@ out.update({"build_s": times, "samples": st["samples"], "phase_ms": st["t_phase_
             "peak_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "launches": st["launches"]})
 Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, a.probes))).cuda()
 t0 = time.perf_counter()
-if update is not None:      # M X = A_H X + U (U^T X): the operator the update build compresses
+if dense is not None:
+    KX = dense @ Xp
+elif update is not None:      # M X = A_H X + U (U^T X): the operator the update build compresses
     KX = update[0].matvec(Xp) + update[1] @ (update[1].T @ Xp)
 else:
     KX = g.dense_sketch(T, Xp, kern)
