@@ -686,6 +686,7 @@ struct Builder {
     a.ldp = ldd;
     a.c0 = 0;
     a.c1 = nc;
+    a.max_k = L.max_k;
     launch_shrink_project(a, st);
     timer.end();
   }

@@ -350,34 +350,65 @@ void launch_id(const IdArgs& a, cudaStream_t st) {
 // shrink + project for columns [c0, c1):  Yp(roff+i) = Yl(poff+J[i]),
 // Op(roff+i) = Ol(poff+J[i]) + sum_cc T(i,cc) Ol(poff+Rhat[cc])   (= X^T Ol, identity rows exact)
 // ------------------------------------------------------------------------------------------
-// CTA = (cluster, 32-column block): the top levels have only 32-128 clusters, so the columns
-// are split over blockIdx.y to fill the GPU.
-constexpr int SP_CB = 32;
+// CTA = (cluster, 32 skeleton rows i, 32 columns): Op(i, :) = Ol(J_i, :) + sum_cc T(i, cc)
+// Ol(Rhat_cc, :) as a shared-memory tiled product over 32-deep cc slabs (the interpolation rows
+// X(Rhat_cc, i) and the sample rows Ol(Rhat_cc, :) staged once per slab and reused 32 times);
+// each thread 4 rows of one column, cc ascending from Ol(J_i) (the order of the scalar version).
+constexpr int SP_T = 32;
 __global__ void __launch_bounds__(256) shrink_project_kernel(ShrinkArgs a) {
+  __shared__ double sX[SP_T][SP_T + 1];   // [cc][i]
+  __shared__ double sO[SP_T][SP_T + 1];   // [cc][col]
+  __shared__ int sR[SP_T];
   const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c], k = a.k[c];
+  const int i0 = blockIdx.y * SP_T;
+  const int cb0 = a.c0 + blockIdx.z * SP_T;
+  const int nc = min(SP_T, a.c1 - cb0);
+  if (i0 >= k || nc <= 0) return;
   const int64_t off = a.poff[c];
   const int* perm = a.perm + off;
   const double* X = a.X + a.xoff[c];
-  const int cb0 = a.c0 + blockIdx.y * SP_CB;
-  const int nc = min(SP_CB, a.c1 - cb0);
-  if (nc <= 0) return;
-  for (int e = threadIdx.x; e < k * nc; e += blockDim.x) {
-    const int i = e / nc, col = cb0 + e % nc;
-    const int64_t src = off + perm[i];
-    a.Yp[(a.roff[c] + i) * a.ldp + col] = a.Yl[src * a.ld + col];
-    double s = a.Ol[src * a.ld + col];
-    for (int cc = 0; cc < m - k; ++cc) {
-      const int rr = perm[k + cc];
-      s = fma(X[(int64_t)rr * k + i], a.Ol[(off + rr) * a.ld + col], s);
+  const int tid = threadIdx.x, col = tid & 31, ib = (tid >> 5) * 4;
+  double acc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + ib + r;
+    acc[r] = 0.0;
+    if (i < k && col < nc) {
+      const int64_t src = off + perm[i];
+      a.Yp[(a.roff[c] + i) * a.ldp + cb0 + col] = a.Yl[src * a.ld + cb0 + col];   // batchedShrink
+      acc[r] = a.Ol[src * a.ld + cb0 + col];
     }
-    a.Op[(a.roff[c] + i) * a.ldp + col] = s;
+  }
+  for (int cc0 = 0; cc0 < m - k; cc0 += SP_T) {
+    const int nt = min(SP_T, m - k - cc0);
+    __syncthreads();
+    if (tid < SP_T) sR[tid] = tid < nt ? perm[k + cc0 + tid] : 0;
+    __syncthreads();
+    for (int e = tid; e < SP_T * SP_T; e += 256) {
+      const int t = e >> 5, x = e & 31;
+      const bool ok = t < nt;
+      sX[t][x] = (ok && i0 + x < k) ? X[(int64_t)sR[t] * k + i0 + x] : 0.0;
+      sO[t][x] = (ok && x < nc) ? a.Ol[(off + sR[t]) * a.ld + cb0 + x] : 0.0;
+    }
+    __syncthreads();
+    for (int t = 0; t < nt; ++t) {
+      const double o = sO[t][col];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fma(sX[t][ib + r], o, acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + ib + r;
+    if (i < k && col < nc) a.Op[(a.roff[c] + i) * a.ldp + cb0 + col] = acc[r];
   }
 }
 
 void launch_shrink_project(const ShrinkArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0 || a.c1 <= a.c0) return;
-  shrink_project_kernel<<<dim3(a.nclusters, div_up(a.c1 - a.c0, SP_CB)), 256, 0, st>>>(a);
+  const dim3 grid(a.nclusters, div_up(std::max(a.max_k, 1), SP_T), div_up(a.c1 - a.c0, SP_T));
+  shrink_project_kernel<<<grid, 256, 0, st>>>(a);
   H2_CHECK_LAUNCH();
 }
 

@@ -139,6 +139,7 @@ struct ShrinkArgs {
   double* Op;
   int64_t ldp;
   int c0, c1;
+  int32_t max_k;          // max k over the clusters (grid sizing)
 };
 void launch_shrink_project(const ShrinkArgs& a, cudaStream_t st);
 
