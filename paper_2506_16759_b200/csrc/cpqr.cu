@@ -236,8 +236,167 @@ static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   cpqr_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a);
 }
 
+// Small panels (m <= 64 rows, the leaf level): one WARP per panel, 4 panels per CTA, no block
+// barriers.  Lane l owns panel rows l and l + 32 (row-major in shared memory, odd row stride:
+// conflict-free column walks); the pivot is a warp Top2 butterfly, the reflector is built by
+// the whole warp, the trailing update of a row is a sequential dot / update / norm over its
+// columns (two accumulators).  Same decisions as the block kernel (max recomputed norm, ties ->
+// lowest index, LAPACK dlarfg), same certificates.
+constexpr int CW_WPB = 4;
+__host__ __device__ inline int cw_ld(int d) { return d | 1; }
+__host__ __device__ inline size_t cw_warp_doubles(int d) { return (size_t)64 * cw_ld(d) + d + 64 + 32; }
+
+__global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ci = blockIdx.x * CW_WPB + warp;
+  if (ci >= a.nclusters) return;
+  const int c = a.c_begin + ci;
+  const int m = a.m[c], d = a.d, LD = cw_ld(d);
+  double* A = smem + (size_t)warp * cw_warp_doubles(d);
+  double* v = A + (size_t)64 * LD;
+  double* nrm = v + d;
+  int* perm = reinterpret_cast<int*>(nrm + 64);
+  const int64_t off = a.poff[c];
+  for (int j = 0; j < m; ++j)
+    for (int r = lane; r < d; r += 32) A[j * LD + r] = a.Y[(off + j) * a.ldy + r];
+  __syncwarp();
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (j < m) {
+      double s0 = 0.0, s1 = 0.0;
+      int r = 0;
+      for (; r + 1 < d; r += 2) {
+        s0 = fma(A[j * LD + r], A[j * LD + r], s0);
+        s1 = fma(A[j * LD + r + 1], A[j * LD + r + 1], s1);
+      }
+      if (r < d) s0 = fma(A[j * LD + r], A[j * LD + r], s0);
+      nrm[j] = sqrt(s0 + s1);
+      perm[j] = j;
+    }
+  }
+  __syncwarp();
+  const int kfull = min(d, m);
+  const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
+  double min_gap = INFINITY, margin = INFINITY;
+  int k = 0;
+  for (int i = 0;; ++i) {
+    Top2 t{-1.0, 0x7fffffff, -1.0};
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      if (j >= i && j < m) t = top2_merge(t, Top2{nrm[j], j, -1.0});
+    }
+    t = warp_top2(t);
+    if (i >= m) break;
+    if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    if (i == kcap || !(t.v > a.eps)) {
+      k = i;
+      break;
+    }
+    if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    const int p = t.i;
+    double* Ai = A + i * LD;
+    if (p != i) {
+      double* Ap = A + p * LD;
+      for (int r = lane; r < d; r += 32) {
+        const double x = Ai[r];
+        Ai[r] = Ap[r];
+        Ap[r] = x;
+      }
+      if (lane == 0) {
+        const int q = perm[i];
+        perm[i] = perm[p];
+        perm[p] = q;
+        const double x = nrm[i];
+        nrm[i] = nrm[p];
+        nrm[p] = x;
+      }
+      __syncwarp();
+    }
+    // Householder reflector of A(i:d, i), LAPACK dlarfg convention
+    double x2 = 0.0;
+    for (int r = i + 1 + lane; r < d; r += 32) x2 = fma(Ai[r], Ai[r], x2);
+    x2 = warp_sum(x2);
+    const double alpha = Ai[i];
+    const double xnorm = sqrt(x2);
+    double tau, beta;
+    if (xnorm == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+    } else {
+      const double h = hypot(alpha, xnorm);
+      beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
+      tau = (beta - alpha) / beta;
+    }
+    const double den = alpha - beta;
+    __syncwarp();
+    for (int r = i + 1 + lane; r < d; r += 32) {
+      v[r] = tau != 0.0 ? Ai[r] / den : 0.0;
+      Ai[r] = 0.0;
+    }
+    if (lane == 0) {
+      v[i] = 1.0;
+      Ai[i] = beta;
+    }
+    __syncwarp();
+    // trailing update of this lane's rows j > i + next residual norms
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      if (j <= i || j >= m) continue;
+      double* Aj = A + j * LD;
+      double w0 = 0.0, w1 = 0.0;
+      int r = i;
+      for (; r + 1 < d; r += 2) {
+        w0 = fma(v[r], Aj[r], w0);
+        w1 = fma(v[r + 1], Aj[r + 1], w1);
+      }
+      if (r < d) w0 = fma(v[r], Aj[r], w0);
+      const double w = (w0 + w1) * tau;
+      double q0 = 0.0, q1 = 0.0;
+      Aj[i] = fma(-w, v[i], Aj[i]);
+      for (r = i + 1; r + 1 < d; r += 2) {
+        const double x0 = fma(-w, v[r], Aj[r]);
+        const double x1 = fma(-w, v[r + 1], Aj[r + 1]);
+        Aj[r] = x0;
+        Aj[r + 1] = x1;
+        q0 = fma(x0, x0, q0);
+        q1 = fma(x1, x1, q1);
+      }
+      if (r < d) {
+        const double x0 = fma(-w, v[r], Aj[r]);
+        Aj[r] = x0;
+        q0 = fma(x0, x0, q0);
+      }
+      nrm[j] = sqrt(q0 + q1);
+    }
+    __syncwarp();
+    k = i + 1;
+  }
+  __syncwarp();
+  for (int j = lane; j < m; j += 32) a.perm[off + j] = perm[j];
+  double* Wc = a.W + off * d;
+  for (int j = 0; j < m; ++j)
+    for (int r = lane; r < d; r += 32) Wc[(int64_t)j * d + r] = A[j * LD + r];
+  if (lane == 0) {
+    a.k[c] = k;
+    a.cert[2 * c] = min_gap;
+    a.cert[2 * c + 1] = margin;
+  }
+}
+
 void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
+  const size_t wsm = sizeof(double) * cw_warp_doubles(a.d) * CW_WPB;
+  if (a.max_m <= 64 && wsm <= 200 * 1024 && env_int("H2_CQ_WARP", 1) != 0) {
+    static bool attr = false;
+    if (!attr) {
+      H2_CUDA(cudaFuncSetAttribute(cpqr_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    cpqr_warp_kernel<<<div_up(a.nclusters, CW_WPB), 32 * CW_WPB, wsm, st>>>(a);
+    H2_CHECK_LAUNCH();
+    return;
+  }
   size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
   size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
   // rows per pass = threads / 8 (32 or 64); 512 threads once a panel has more than 32 rows
