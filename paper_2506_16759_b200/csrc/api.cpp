@@ -252,7 +252,7 @@ struct Builder {
   KernelParams ekp{}, skp{};
   int d = 0;
   Panel cur;                    // full-width panel of the depth being processed
-  DArr<double> sumsq_scratch, sumsq_acc;
+  DArr<double> sumsq_acc;
   DArr<int> nonfinite;
   DArr<double> W;               // CPQR workspace
   PhaseTimer timer;
@@ -864,7 +864,6 @@ struct Builder {
     }
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
     d = std::min(o.d_init, o.d_max);
-    sumsq_scratch.alloc(div_up(T.n, 1024), st);
     sumsq_acc.alloc(1, st);
     nonfinite.alloc(1, st);
     H2_CUDA(cudaMemsetAsync(sumsq_acc.p, 0, sizeof(double), st));

@@ -32,9 +32,6 @@ void launch_sketch_combine(const double* P, int S, int64_t rows, int ncols, doub
 void launch_sumsq_leaf(const double* Y, const int64_t* leaf_begin, int cb, int ce, int64_t ld, int c0, int c1,
                        double* part, cudaStream_t st);
 void launch_sumsq_total(const double* part, int nleaf, double* accum, int* nonfinite, cudaStream_t st);
-void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum,
-                  int* nonfinite, cudaStream_t st);
-
 // batchedGen over unique pairs u: out[out_off[u] + i*nc + j] = K(idx[off[us]+i], idx[off[ub]+j])
 // (L212 for D with idx = iota, off = cluster begin; L258 for B with idx = skeletons)
 struct GenArgs {

@@ -306,32 +306,8 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
 }
 
 // ------------------------------------------------------------------------------------------
-// sum of squares of Y(:, c0:c1): fixed 1024-row chunks, fixed-order combination -> bitwise
-// reproducible for a given n (R10: rho^2 N = ||Y||_F^2, accumulated over rounds).
+// sum of squares of Y(:, c0:c1) (R10: rho^2 N = ||Y||_F^2, accumulated over the draws)
 // ------------------------------------------------------------------------------------------
-__global__ void sumsq_partial_kernel(const double* __restrict__ Y, int64_t n, int64_t ld, int c0, int c1,
-                                     double* __restrict__ part) {
-  __shared__ double red[32];
-  int64_t r0 = (int64_t)blockIdx.x * 1024;
-  double s = 0.0;
-  const int w = c1 - c0;
-  for (int e = threadIdx.x; e < 1024 * w; e += blockDim.x) {
-    int64_t r = r0 + e / w;
-    if (r < n) {
-      double v = Y[r * ld + c0 + e % w];
-      s = fma(v, v, s);
-    }
-  }
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) part[blockIdx.x] = v;
-  }
-}
-
 __global__ void sumsq_final_kernel(const double* __restrict__ part, int np, double* __restrict__ out, int* flag) {
   __shared__ double red[32];
   double s = 0.0;
@@ -384,14 +360,6 @@ void launch_sumsq_total(const double* part, int nleaf, double* accum, int* nonfi
   H2_CHECK_LAUNCH();
 }
 
-void launch_sumsq(const double* Y, int64_t n, int64_t ld, int c0, int c1, double* scratch, double* accum, int* nonfinite,
-                  cudaStream_t st) {
-  int np = div_up(n, 1024);
-  sumsq_partial_kernel<<<np, 256, 0, st>>>(Y, n, ld, c0, c1, scratch);
-  H2_CHECK_LAUNCH();
-  sumsq_final_kernel<<<1, 1024, 0, st>>>(scratch, np, accum, nonfinite);
-  H2_CHECK_LAUNCH();
-}
 
 // Y (rows x ncols, row-major, ldy) = A(rows, :) (row-major, lda) Omega (n x ncols, row-major, ldo):
 // in column-major terms Y^T = Omega^T A(rows,:)^T, one DGEMM.

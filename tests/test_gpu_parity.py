@@ -221,3 +221,16 @@ def test_speculative_sketch_columns_bitwise(monkeypatch):
         assert all(np.array_equal(a, b) for a, b in zip(H0.skel(t), H1.skel(t)))
         assert np.array_equal(H0._export(g._lib.H2_X_BASIS, t), H1._export(g._lib.H2_X_BASIS, t))
         assert np.array_equal(H0._export(g._lib.H2_X_B, t), H1._export(g._lib.H2_X_B, t))
+
+
+def test_helmholtz_sketch_with_coincident_points():
+    """Coincident points (r_min = 0: no fixed-point scale for the Helmholtz tensor-core sketch)
+    take the FP64 DMMA path; K(x, x) = 0 (R20) on every coincident pair.  Matches the oracle."""
+    X = grid_points((8, 8, 8), 1 / 8)
+    X = np.concatenate([X, X[:37]])            # 37 duplicated points
+    T = g.Tree(X, 64)
+    Om = rng.omega_block(1, 0, 0, T.n, 0, 40)
+    op = kernels.KernelOperator("helmholtz", 3.0, X[T.perm])
+    ref = op.sampler(Om)
+    y = g.dense_sketch(T, torch.from_numpy(Om).cuda(), ("helmholtz", 3.0), omega_quarters=True).cpu().numpy()
+    assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
