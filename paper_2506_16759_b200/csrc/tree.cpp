@@ -244,21 +244,42 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
     diam[t].resize(box[t].size());
     for (size_t c = 0; c < box[t].size(); ++c) diam[t][c] = diameter(box[t][c]);
   }
+  // the pairs of a depth are split into contiguous ranges over threads; the per-thread lists are
+  // concatenated in range order, so the result is identical to the serial traversal
+  const int nthr = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   for (int t = 0; t <= Dl; ++t) {
+    const int64_t np = (int64_t)cur.size();
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthr, np / 4096));
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> far_t(nt), nxt_t(nt), near_t(nt);
+    auto work = [&](int q) {
+      for (int64_t e = np * q / nt; e < np * (q + 1) / nt; ++e) {
+        const auto& p = cur[e];
+        const int32_t s = p.first, u = p.second;
+        bool adm = false;
+        if (s != u) {
+          const double dist = distance(box[t][s], box[t][u], rule);
+          adm = (diam[t][s] + diam[t][u]) * 0.5 <= eta * dist;   // Eq.(1)
+        }
+        if (adm) far_t[q].push_back(p);
+        else if (t == Dl) near_t[q].push_back(p);
+        else
+          for (int a = 0; a < 2; ++a)
+            for (int bb = 0; bb < 2; ++bb) nxt_t[q].push_back({2 * s + a, 2 * u + bb});
+      }
+    };
+    if (nt == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int q = 0; q < nt; ++q) th.emplace_back(work, q);
+      for (auto& x : th) x.join();
+    }
     std::vector<std::pair<int32_t, int32_t>> far;
     nxt.clear();
-    for (auto& p : cur) {
-      int32_t s = p.first, u = p.second;
-      bool adm = false;
-      if (s != u) {
-        double dist = distance(box[t][s], box[t][u], rule);
-        adm = (diam[t][s] + diam[t][u]) * 0.5 <= eta * dist;   // Eq.(1)
-      }
-      if (adm) far.push_back(p);
-      else if (t == Dl) near.push_back(p);
-      else
-        for (int a = 0; a < 2; ++a)
-          for (int bb = 0; bb < 2; ++bb) nxt.push_back({2 * s + a, 2 * u + bb});
+    for (int q = 0; q < nt; ++q) {
+      far.insert(far.end(), far_t[q].begin(), far_t[q].end());
+      nxt.insert(nxt.end(), nxt_t[q].begin(), nxt_t[q].end());
+      near.insert(near.end(), near_t[q].begin(), near_t[q].end());
     }
     if (!far.empty() && T.top < 0) T.top = t;
     make_csr(T.far[t], far, 1 << t, true);
