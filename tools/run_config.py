@@ -24,6 +24,8 @@ p.add_argument("--s", type=float, default=0.1)
 p.add_argument("--s-update", type=float, default=None, help="tol_safety of the update build (configs[4]); default --s")
 p.add_argument("--d-blk", type=int, default=32)
 p.add_argument("--probes", type=int, default=16)
+p.add_argument("--p-os", type=int, default=None, help="oversampling margin of the convergence test (R12); "
+               "default: the workload's (configs[4]: 32), else 10")
 p.add_argument("--bootstrap", type=float, default=None,
                help="S8(f) NEXT #1: build an H^2 of K at this tighter tol (dense sketch, timed separately), "
                     "then the timed build at the workload tol with its O(N) H^2-matvec sketch")
@@ -68,7 +70,7 @@ for r in range(a.reps):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk,
+    H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, p_os=a.p_os if a.p_os is not None else w.get("p_os", 10),
                 tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk, dense=dense,
                 d_max=w.get("d_max", 512))
     e1.record()
