@@ -74,9 +74,26 @@ def owned_range(n_clusters: int, rank: int, world: int):
 def allgatherv_(buf: torch.Tensor, counts, displs, group=None):
     """In-place all-gather of byte segments of a 1-D uint8 tensor: segment r =
     buf[displs[r] : displs[r] + counts[r]] is valid on rank r on entry and on every rank on
-    return.  One broadcast per non-empty segment (NCCL: on-device; gloo: host staging)."""
+    return.  NCCL (device tensors): one all-gather of max-size segments through a staging
+    buffer; otherwise one broadcast per non-empty segment (gloo: host staging)."""
     nccl = dist.get_backend(group) == "nccl"
     me = dist.get_rank(group)
+    if nccl and buf.is_cuda:
+        # one NCCL all-gather of equal (max) segments, in place in a staging buffer, then the
+        # variable segments are copied out (P small device copies instead of P broadcasts)
+        P = len(counts)
+        mx = max(counts)
+        if mx == 0:
+            return
+        stage = torch.empty(P * mx, dtype=torch.uint8, device=buf.device)
+        c, d = counts[me], displs[me]
+        if c:
+            stage[me * mx:me * mx + c].copy_(buf[d:d + c])
+        dist.all_gather_into_tensor(stage, stage[me * mx:(me + 1) * mx], group=group)
+        for r in range(P):
+            if r != me and counts[r]:
+                buf[displs[r]:displs[r] + counts[r]].copy_(stage[r * mx:r * mx + counts[r]])
+        return
     for r, (c, d) in enumerate(zip(counts, displs)):
         if c == 0:
             continue
