@@ -86,10 +86,11 @@ def allgatherv_(buf: torch.Tensor, counts, displs, group=None):
         if mx == 0:
             return
         stage = torch.empty(P * mx, dtype=torch.uint8, device=buf.device)
+        mine = torch.zeros(mx, dtype=torch.uint8, device=buf.device)
         c, d = counts[me], displs[me]
         if c:
-            stage[me * mx:me * mx + c].copy_(buf[d:d + c])
-        dist.all_gather_into_tensor(stage, stage[me * mx:(me + 1) * mx], group=group)
+            mine[:c].copy_(buf[d:d + c])
+        dist.all_gather_into_tensor(stage, mine, group=group)
         for r in range(P):
             if r != me and counts[r]:
                 buf[displs[r]:displs[r] + counts[r]].copy_(stage[r * mx:r * mx + counts[r]])
