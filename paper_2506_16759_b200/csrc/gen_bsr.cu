@@ -124,9 +124,11 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool va
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
 }
 
-template <int CW>
-__global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
-  constexpr int NT = 4 * CW;           // threads
+// WM: 8-row DMMA blocks per warp (warp tile 8 WM x 32); warps: NWR along rows x CW/32 along columns
+template <int CW, int WM>
+__global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(BsrArgs a, double alpha) {
+  constexpr int NWR = 64 / (8 * WM);
+  constexpr int NT = 32 * NWR * (CW / 32);   // threads
   constexpr int LDB = CW + 4;
   constexpr int BSZ = BT_K * LDB;
   extern __shared__ __align__(16) double bsm[];   // NS x (A slab + B slab)
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
   const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
   if (e0 == e1) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp & 3, wc = warp >> 2;
+  const int wr = warp % NWR, wc = warp / NWR;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bsm);
   // loader state: next (partner, k0) to load
   int le = e0, lk = 0;
@@ -188,9 +190,9 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
       lk = 0;
     }
   };
-  double acc[2][4][2];
+  double acc[WM][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   int nitems = 0;
@@ -214,24 +216,24 @@ __global__ void __launch_bounds__(4 * CW) bsr_kernel(BsrArgs a, double alpha) {
     const int ksteps = (nk + 3) >> 2;
     for (int ks = 0; ks < ksteps; ++ks) {
       const int kk = ks * 4 + (lane & 3);
-      double af[2], bf[4];
+      double af[WM], bf[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int r = wr * 16 + i * 8 + (lane >> 2);
+      for (int i = 0; i < WM; ++i) {
+        const int r = wr * (8 * WM) + i * 8 + (lane >> 2);
         af[i] = direct ? sA[r * BT_LDD + kk] : sA[kk * BT_LDT + r];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = sB[kk * LDB + wc * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < WM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int r = r0 + wr * 16 + i * 8 + (lane >> 2);
+  for (int i = 0; i < WM; ++i) {
+    const int r = r0 + wr * (8 * WM) + i * 8 + (lane >> 2);
     if (r >= ms) continue;
     double* y = a.Y + (a.yoff[s] + r) * a.ldy + cb;
 #pragma unroll
@@ -249,16 +251,19 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   constexpr size_t sm32 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (32 + 4));
   constexpr size_t sm64 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (64 + 4));
   if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32));
-    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
+    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32));
+    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
+    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
     attr = true;
   }
+  static const int wm64 = env_int("H2_BSR_WM64", 4);   // 32 x 32 warp tiles for 64-column passes (-3 ms at C2)
   if (a.ncols > 32) {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 64));
-    bsr_kernel<64><<<grid, 256, sm64, st>>>(a, alpha);
+    if (wm64 == 4) bsr_kernel<64, 4><<<grid, 128, sm64, st>>>(a, alpha);
+    else bsr_kernel<64, 2><<<grid, 256, sm64, st>>>(a, alpha);
   } else {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 32));
-    bsr_kernel<32><<<grid, 128, sm32, st>>>(a, alpha);
+    bsr_kernel<32, 2><<<grid, 128, sm32, st>>>(a, alpha);
   }
   H2_CHECK_LAUNCH();
 }
