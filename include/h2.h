@@ -107,6 +107,7 @@ typedef struct {
   double* y;           /* dev */
   int64_t ld_y;
   void* stream;
+  int32_t transpose;   /* h2_build_nonsym only: 1 = write y = K^T omega (the column sketch), 0 = K omega */
 } h2_sketch_req;
 typedef int (*h2_sketch_fn)(void* ctx, const h2_sketch_req* req);
 
@@ -248,6 +249,21 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
 h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                         const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
                         h2_build_stats* stats);
+/* Non-symmetric construction ("the extension to the non-symmetric case is
+ * straightforward"; R29): K ~ D + U B V^T with row bases U / E
+ * from the sketch Y = K Omega and column bases V / F from Z = K^T Psi, built level by level in
+ * lockstep (the two sides meet in the far-field subtraction).  Psi is the h2_omega stream
+ * opts->stream_id + 1 (Omega: stream_id).  tol applies to the RMS row norm of Y and Z together;
+ * a level converges when every cluster of both sides passes the test.  Operators: sketch
+ * H2_S_DENSE_MATRIX (Z via A^T, cuBLAS), H2_S_CALLBACK (called with req->transpose = 0 and 1)
+ * or H2_S_DENSE_KERNEL (the built-in kernels are symmetric: Z = K Psi); entry H2_E_BUILTIN,
+ * H2_E_CALLBACK or H2_E_DENSE_MATRIX.  One GPU.  The result works with h2_matvec (upward pass
+ * with V, couplings, downward pass with U) and h2_export: H2_X_RANK/SKEL/BASIS/CERT give the row
+ * side, H2_X_*_C the column side; D and B are stored for every ORDERED pair (s, b) in (s, b)
+ * order, D_{s,b} m_s x m_b, B_{s,b} = K(I~_s, J~_b) k_s x kc_b.  Errors as h2_build. */
+h2_status h2_build_nonsym(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                          const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats);
+
 /* Collective: all-gather bases X, certificates, B and D so that every rank holds the full
  * matrix (segments by owner of the cluster / of the stored block's row cluster). */
 h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream);
@@ -284,7 +300,9 @@ h2_status h2_omega(uint64_t seed, uint32_t stream_id, int64_t row0, int64_t nrow
  *   B[t]      : float64, unique far pairs (s < b) of depth t in sorted order, k_s x k_b
  *   cert[t]   : float64 pairs (min pivot gap, stop margin) per cluster (CPQR certification)
  * ------------------------------------------------------------------------------------- */
-enum { H2_X_RANK = 0, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT };
+enum { H2_X_RANK = 0, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT,
+       /* column side of a non-symmetric matrix (h2_build_nonsym): ranks, J~, V / [F1; F2], cert */
+       H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C };
 h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_t* count);
 h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst);
 h2_status h2_matrix_get_stats(const h2_matrix* H, h2_build_stats* stats);

@@ -34,8 +34,13 @@ class H2NonSym:
     Xc: dict = field(default_factory=dict)       # depth -> list of column bases (V / [F1; F2])
     D: dict = field(default_factory=dict)        # (s, b) ordered near pairs
     B: dict = field(default_factory=dict)        # depth -> {(s, b): K(I~_s, J~_b)} ordered far pairs
+    ids_r: dict = field(default_factory=dict)    # depth -> list of RowID (certification data)
+    ids_c: dict = field(default_factory=dict)
+    panels_r: dict = field(default_factory=dict) # depth -> list of Y^loc_tau at commit
+    panels_c: dict = field(default_factory=dict) # depth -> list of Z^loc_tau at commit
     samples: int = 0
     rounds: dict = field(default_factory=dict)
+    eps: float = 0.0
 
 
 def build_nonsym(tree, part, sampler, sampler_t, entry, omega, psi, tol, opts: BuildOpts = None) -> H2NonSym:
@@ -141,7 +146,10 @@ def build_nonsym(tree, part, sampler, sampler_t, entry, omega, psi, tol, opts: B
             Pl = [np.hstack([Pl[c], nP[c]]) for c in range(1 << t)]
             d += opts.d_blk
         H.rounds[t] = rounds
+        H.eps = eps
         ids_r[t], ids_c[t] = ir, ic
+        H.ids_r[t], H.ids_c[t] = ir, ic
+        H.panels_r[t], H.panels_c[t] = Yl, Zl
         H.Xr[t] = [i.X for i in ir]
         H.Xc[t] = [i.X for i in ic]
         H.rank_r[t] = np.array([i.k for i in ir], np.int64)

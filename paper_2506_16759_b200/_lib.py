@@ -17,7 +17,7 @@ H2_K_EXP, H2_K_HELMHOLTZ = 0, 1
 H2_S_DENSE_KERNEL, H2_S_CALLBACK, H2_S_H2_LOWRANK, H2_S_DENSE_MATRIX = 0, 1, 2, 3
 H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK, H2_E_DENSE_MATRIX = 0, 1, 2, 3
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
-H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT = range(6)
+H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C = range(10)
 H2_SKETCH_OMEGA_QUARTERS = 1
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
 H2_NPHASE = len(PHASES)
@@ -36,7 +36,7 @@ class h2_kernel(C.Structure):
 class h2_sketch_req(C.Structure):
     _fields_ = [("n", C.c_int64), ("row_begin", C.c_int64), ("row_end", C.c_int64), ("col0", C.c_int32),
                 ("ncols", C.c_int32), ("omega", C.c_void_p), ("ld_omega", C.c_int64), ("y", C.c_void_p),
-                ("ld_y", C.c_int64), ("stream", C.c_void_p)]
+                ("ld_y", C.c_int64), ("stream", C.c_void_p), ("transpose", C.c_int32)]
 
 
 SKETCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(h2_sketch_req))
@@ -98,6 +98,8 @@ SIGNATURES = {
     "h2_build_opts_default": (None, [C.POINTER(h2_build_opts)]),
     "h2_build": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts), _P,
                            C.POINTER(_P), C.POINTER(h2_build_stats)]),
+    "h2_build_nonsym": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double,
+                                  C.POINTER(h2_build_opts), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
                                 C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_matrix_allgather": (C.c_int, [_P, C.POINTER(h2_comm), _P]),

@@ -105,6 +105,17 @@ struct h2_matrix {
   h2_build_stats stats{};
   Level& L(int t) { return lv[t - top]; }
   const Level& L(int t) const { return lv[t - top]; }
+  // non-symmetric build (h2_build_nonsym): lv holds the row side (ranks, skeletons I~, bases U/E,
+  // and the couplings B_{s,b} of every ORDERED far pair in CSR order), lvc the column side
+  // (J~, V/F); D holds every ordered near pair in CSR order at offsets D_off
+  bool nonsym = false;
+  std::vector<Level> lvc;
+  std::vector<int64_t> D_off;
+  DArr<int64_t> d_D_off;
+  Level& C(int t) { return lvc[t - top]; }
+  const Level& C(int t) const { return lvc[t - top]; }
+  Level& S(int sd, int t) { return sd ? C(t) : L(t); }
+  const Level& S(int sd, int t) const { return sd ? C(t) : L(t); }
 };
 
 namespace {
@@ -252,6 +263,8 @@ struct Builder {
   KernelParams ekp{}, skp{};
   int d = 0;
   Panel cur;                    // full-width panel of the depth being processed
+  Panel curc;                   // non-symmetric build: the column-side panel (Z, Omega^l)
+  DArr<double> Wc;              // its CPQR workspace
   DArr<double> sumsq_acc;
   DArr<int> nonfinite;
   DArr<double> W;               // CPQR workspace
@@ -489,7 +502,8 @@ struct Builder {
     H2_CUDA(cudaMemcpyAsync(&nf, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     H2_CUDA(cudaStreamSynchronize(st));
     if (nf) throw Error(H2_ERR_NONFINITE, "the sketch produced a non-finite sample");
-    if (o.tol_rule == H2_TOL_RMS) return o.tol_safety * tol * std::sqrt(acc / (double)T.n);
+    // non-symmetric: acc holds ||Y||^2 + ||Z||^2 (R29: RMS over both sketches)
+    if (o.tol_rule == H2_TOL_RMS) return o.tol_safety * tol * std::sqrt(acc / (double)(ns ? 2 * T.n : T.n));
     return tol * o.norm;
   }
 
@@ -512,7 +526,7 @@ struct Builder {
       co.alloc(g.nblocks, st);
       outp.alloc(g.nblocks, st);
       launch_gen_batch_desc(g, m.p, nc.p, ro.p, co.p, outp.p, ld.p, st);
-      h2_block_batch bb{g.nblocks, m.p, nc.p, ro.p, co.p, g.idx, g.idx, outp.p, ld.p, st};
+      h2_block_batch bb{g.nblocks, m.p, nc.p, ro.p, co.p, g.idx, g.idx2 ? g.idx2 : g.idx, outp.p, ld.p, st};
       int rc = E.fn(E.ctx, &bb);
       if (rc != 0) throw Error(H2_ERR_CALLBACK, "entry callback returned " + std::to_string(rc));
       H2_CUDA(cudaStreamSynchronize(st));
@@ -563,8 +577,8 @@ struct Builder {
   }
 
   // ---------------------------------------------------------------- level set-up
-  void setup_level(int t) {
-    Level& L = H.L(t);
+  void setup_level(int t, int sd = 0) {
+    Level& L = H.S(sd, t);
     L.t = t;
     L.nclus = 1 << t;
     L.m.resize(L.nclus);
@@ -575,7 +589,7 @@ struct Builder {
         L.poff[c] = T.begin[t][c];
       }
     } else {
-      const Level& C = H.L(t + 1);
+      const Level& C = H.S(sd, t + 1);
       for (int c = 0; c < L.nclus; ++c) {
         L.m[c] = C.k[2 * c] + C.k[2 * c + 1];
         L.poff[c] = C.roff[2 * c];
@@ -595,8 +609,10 @@ struct Builder {
   }
 
   // CPQR of every panel of depth t (current panel, d columns); returns host ranks
-  void cpqr(int t, double eps) {
-    Level& L = H.L(t);
+  void cpqr(int t, double eps, int sd = 0) {
+    Level& L = H.S(sd, t);
+    DArr<double>& W = sd ? Wc : this->W;
+    const Panel& cur = sd ? curc : this->cur;
     int64_t need = std::max<int64_t>(L.rows * d, 1);
     if (W.n < need) W.alloc(need, st);
     timer.begin(H2_PH_CPQR);
@@ -621,8 +637,9 @@ struct Builder {
     L.k = download(L.d_k, L.nclus, st);
   }
 
-  void commit(int t) {
-    Level& L = H.L(t);
+  void commit(int t, int sd = 0) {
+    Level& L = H.S(sd, t);
+    DArr<double>& W = sd ? Wc : this->W;
     L.roff.assign(L.nclus, 0);
     L.xoff.assign(L.nclus, 0);
     L.rtot = L.xtot = 0;
@@ -650,7 +667,7 @@ struct Builder {
     a.perm = L.d_perm.p;
     a.xoff = L.d_xoff.p;
     a.X = L.X.p;
-    a.ibar = (t == T.Dl) ? T.d_iota : H.L(t + 1).d_skel.p;
+    a.ibar = (t == T.Dl) ? T.d_iota : H.S(sd, t + 1).d_skel.p;
     a.roff = L.d_roff.p;
     a.skel = L.d_skel.p;
     a.max_k = L.max_k;
@@ -665,8 +682,9 @@ struct Builder {
 
   // batchedShrink + Omega upsweep of committed depth u, nc columns: source panel (depth u)
   // -> destination panel (depth u-1); pointers at the first column of each.
-  void shrink(int u, const double* Ys, const double* Os, int64_t lds, double* Yd, double* Od, int64_t ldd, int nc) {
-    Level& L = H.L(u);
+  void shrink(int u, const double* Ys, const double* Os, int64_t lds, double* Yd, double* Od, int64_t ldd, int nc,
+              int sd = 0) {
+    Level& L = H.S(sd, u);
     timer.begin(H2_PH_ID);
     ShrinkArgs a{};
     a.c_begin = cb(u);
@@ -835,6 +853,286 @@ struct Builder {
     }
   }
 
+  // ================================================================ non-symmetric construction
+  // h2_build_nonsym ("the extension to the non-symmetric case is straightforward";
+  // DESIGN.md R29; oracle/h2_nonsym.py).  Two panels per depth: cur = (Y^l: samples of K Omega,
+  // Psi^l: the column stream projected with the ROW bases) in the row layout, curc = (Z^l: samples
+  // of K^T Psi, Omega^l projected with the COLUMN bases) in the column layout.  Each side runs the
+  // per-level steps of the symmetric build on its own panel (CPQR/ID, shrink + projection); they
+  // meet in the BSR subtraction: Y -= B Omega^l (blocks B_{s,b} read directly) and
+  // Z -= B^T Psi^l (B_{b,s} read transposed).  D and B are stored for every ORDERED pair in CSR
+  // order (D_{s,b} = K(I_s, I_b), B_{s,b} = K(I~_s, J~_b)).
+  bool ns = false;
+  struct Ordered {
+    std::vector<int32_t> os;   // row cluster of CSR entry e
+    DArr<int32_t> d_os, d_tpos;   // d_tpos[e]: CSR position of the transposed pair
+  };
+  Ordered near_o;
+  std::vector<Ordered> far_o;
+  void ordered_of(const PairCSR& F, int nclus, Ordered& O) {
+    const int64_t nnz = F.nnz();
+    O.os.assign(nnz, 0);
+    std::vector<int32_t> tpos(nnz, 0);
+    for (int c = 0; c < nclus; ++c)
+      for (int e = F.ptr[c]; e < F.ptr[c + 1]; ++e) O.os[e] = c;
+    for (int64_t e = 0; e < nnz; ++e) {
+      const int b = F.idx[e], c = O.os[e];
+      auto it = std::lower_bound(F.idx.begin() + F.ptr[b], F.idx.begin() + F.ptr[b + 1], c);
+      if (it == F.idx.begin() + F.ptr[b + 1] || *it != c) throw Error(H2_ERR_INVALID_ARG, "pair set is not symmetric");
+      tpos[e] = (int32_t)(it - F.idx.begin());
+    }
+    O.d_os.upload(O.os, st);
+    O.d_tpos.upload(tpos, st);
+  }
+
+  // Omega -> Om (column panel), Psi -> Ps (row panel), Y = K Omega, Z = K^T Psi; ||Y||^2 + ||Z||^2
+  void ns_draw(double* Y, double* Ps, int64_t ldr, double* Z, double* Om, int64_t ldc, int c0, int nc) {
+    timer.begin(H2_PH_RAND);
+    launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Om, ldc, st);
+    launch_omega(o.seed, o.stream_id + 1, 0, T.n, c0, nc, Ps, ldr, st);
+    timer.end();
+    timer.begin(H2_PH_SKETCH);
+    sketch_columns += nc;
+    for (int tr = 0; tr < 2; ++tr) {
+      const double* in = tr ? Ps : Om;
+      const int64_t ldi = tr ? ldr : ldc;
+      double* out = tr ? Z : Y;
+      const int64_t ldo = tr ? ldc : ldr;
+      if (S.kind == H2_S_DENSE_KERNEL) {   // the built-in kernels are symmetric: K^T Psi = K Psi
+        launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, in, ldi, nc, out, ldo, true, st);
+        entries_sketch += T.n * T.n * (int64_t)div_up(nc, 64);
+      } else if (S.kind == H2_S_DENSE_MATRIX) {
+        dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, in, ldi, nc, out, ldo, st, tr == 1);
+      } else {
+        h2_sketch_req rq{};
+        rq.n = T.n;
+        rq.row_begin = 0;
+        rq.row_end = T.n;
+        rq.col0 = c0;
+        rq.ncols = nc;
+        rq.omega = in;
+        rq.ld_omega = ldi;
+        rq.y = out;
+        rq.ld_y = ldo;
+        rq.stream = st;
+        rq.transpose = tr;
+        int rc = S.fn(S.ctx, &rq);
+        if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+      }
+    }
+    timer.end();
+    timer.begin(H2_PH_MISC);
+    const int nleaf = 1 << T.Dl;
+    if (leaf_part.n < nleaf) leaf_part.alloc(nleaf, st);
+    launch_sumsq_leaf(Y, T.d_leaf_begin, 0, nleaf, ldr, 0, nc, leaf_part.p, st);
+    launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
+    launch_sumsq_leaf(Z, T.d_leaf_begin, 0, nleaf, ldc, 0, nc, leaf_part.p, st);
+    launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
+    timer.end();
+  }
+
+  // side sd (0: rows, 1: columns) of the BSR subtraction on a panel of depth t
+  void ns_bsr(int t, int sd, double* Yp, int64_t ldy, const double* Op, int64_t ldo, int nc) {
+    timer.begin(H2_PH_BSR);
+    BsrArgs a{};
+    a.c0 = 0;
+    a.ncols = nc;
+    a.c_begin = 0;
+    a.tmode = sd ? 2 : 1;
+    if (t == T.Dl) {
+      a.nclusters = 1 << T.Dl;
+      a.max_rows = H.L(T.Dl).max_m;
+      a.yoff = a.ooff = T.d_leaf_begin;
+      a.cnt = T.d_leaf_size;
+      a.ptr = T.d_near.ptr;
+      a.idx = T.d_near.idx;
+      a.uidx = sd ? near_o.d_tpos.p : nullptr;
+      a.blk_off = H.d_D_off.p;
+      a.blk = H.D.p;
+    } else {
+      const Level& Ls = H.S(sd, t + 1);
+      const Level& Lo = H.S(1 - sd, t + 1);
+      a.nclusters = 1 << (t + 1);
+      a.max_rows = Ls.max_k;
+      a.yoff = Ls.d_roff.p;
+      a.ooff = Lo.d_roff.p;
+      a.cnt = Ls.d_k.p;
+      a.kcnt = Lo.d_k.p;
+      a.ptr = T.d_far[t + 1].ptr;
+      a.idx = T.d_far[t + 1].idx;
+      a.uidx = sd ? far_o[t + 1].d_tpos.p : nullptr;
+      a.blk_off = H.L(t + 1).d_B_off.p;
+      a.blk = H.L(t + 1).B.p;
+    }
+    a.Y = Yp;
+    a.ldy = ldy;
+    a.Om = Op;
+    a.ldo = ldo;
+    launch_bsr(a, st);
+    timer.end();
+  }
+
+  void ns_gen_D() {
+    const PairCSR& F = T.near;
+    H.D_off.assign(F.nnz() + 1, 0);
+    for (int64_t e = 0; e < F.nnz(); ++e)
+      H.D_off[e + 1] = H.D_off[e] + (T.end[T.Dl][near_o.os[e]] - T.begin[T.Dl][near_o.os[e]]) *
+                                        (T.end[T.Dl][F.idx[e]] - T.begin[T.Dl][F.idx[e]]);
+    H.d_D_off.upload(H.D_off, st);
+    H.D.alloc(H.D_off.back(), st);
+    GenArgs g{};
+    g.nblocks = F.nnz();
+    g.us = near_o.d_os.p;
+    g.ub = T.d_near.idx;
+    g.cnt = T.d_leaf_size;
+    g.off = T.d_leaf_begin;
+    g.idx = T.d_iota;
+    g.out_off = H.d_D_off.p;
+    g.out = H.D.p;
+    gen(g);
+  }
+
+  void ns_gen_B(int t) {
+    Level& L = H.L(t);
+    const Level& C = H.C(t);
+    const PairCSR& F = T.far[t];
+    L.B_off.assign(F.nnz() + 1, 0);
+    for (int64_t e = 0; e < F.nnz(); ++e)
+      L.B_off[e + 1] = L.B_off[e] + (int64_t)L.k[far_o[t].os[e]] * C.k[F.idx[e]];
+    L.d_B_off.upload(L.B_off, st);
+    L.B.alloc(L.B_off.back(), st);
+    GenArgs g{};
+    g.nblocks = F.nnz();
+    g.us = far_o[t].d_os.p;
+    g.ub = T.d_far[t].idx;
+    g.cnt = L.d_k.p;
+    g.off = L.d_roff.p;
+    g.idx = L.d_skel.p;
+    g.cnt2 = C.d_k.p;
+    g.off2 = C.d_roff.p;
+    g.idx2 = C.d_skel.p;
+    g.out_off = L.d_B_off.p;
+    g.out = L.B.p;
+    gen(g);
+  }
+
+  void ns_bsr_both(int t, Panel& R, Panel& Cp, int c0, int nc) {
+    ns_bsr(t, 0, R.Y.p + c0, R.ld, Cp.O.p + c0, Cp.ld, nc);
+    ns_bsr(t, 1, Cp.Y.p + c0, Cp.ld, R.O.p + c0, R.ld, nc);
+  }
+
+  // updateSamples for both sides: b new columns of Omega and Psi swept up to depth t
+  void ns_update_samples(int t, int b) {
+    const int c0 = d;
+    grow(cur, d + b);
+    grow(curc, d + b);
+    if (t == T.Dl) {
+      ns_draw(cur.Y.p + c0, cur.O.p + c0, cur.ld, curc.Y.p + c0, curc.O.p + c0, curc.ld, c0, b);
+      ns_bsr_both(T.Dl, cur, curc, c0, b);
+      return;
+    }
+    Panel sr, sc;
+    sr.alloc(T.n, b, st);
+    sc.alloc(T.n, b, st);
+    ns_draw(sr.Y.p, sr.O.p, sr.ld, sc.Y.p, sc.O.p, sc.ld, c0, b);
+    ns_bsr_both(T.Dl, sr, sc, 0, b);
+    for (int u = T.Dl; u > t; --u) {
+      if (u - 1 == t) {
+        shrink(u, sr.Y.p, sr.O.p, sr.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, b, 0);
+        shrink(u, sc.Y.p, sc.O.p, sc.ld, curc.Y.p + c0, curc.O.p + c0, curc.ld, b, 1);
+        ns_bsr_both(t, cur, curc, c0, b);
+      } else {
+        Panel dr, dc;
+        dr.alloc(H.L(u).rtot, b, st);
+        dc.alloc(H.C(u).rtot, b, st);
+        shrink(u, sr.Y.p, sr.O.p, sr.ld, dr.Y.p, dr.O.p, dr.ld, b, 0);
+        shrink(u, sc.Y.p, sc.O.p, sc.ld, dc.Y.p, dc.O.p, dc.ld, b, 1);
+        ns_bsr_both(u - 1, dr, dc, 0, b);
+        sr = std::move(dr);
+        sc = std::move(dc);
+      }
+    }
+  }
+
+  void run_nonsym() {
+    ns = true;
+    user_st = st;
+    st = prio_stream(true);
+    timer.st = st;
+    stream_after(st, user_st);
+    const int Dl = T.Dl;
+    const int top = T.top < 0 ? Dl : T.top;
+    H.nonsym = true;
+    H.top = top;
+    H.Dl = Dl;
+    H.n = T.n;
+    H.lv.resize(Dl - top + 1);
+    H.lvc.resize(Dl - top + 1);
+    if (S.kind == H2_S_DENSE_KERNEL) skp = tree_kernel(&T, S.kern, st);
+    if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
+    d = std::min(o.d_init, o.d_max);
+    sumsq_acc.alloc(1, st);
+    nonfinite.alloc(1, st);
+    H2_CUDA(cudaMemsetAsync(sumsq_acc.p, 0, sizeof(double), st));
+    H2_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+    ordered_of(T.near, 1 << Dl, near_o);
+    far_o.resize(Dl + 1);
+    for (int t = top; t <= Dl; ++t) ordered_of(T.far[t], 1 << t, far_o[t]);
+
+    cur.alloc(T.n, ld_for(T.n, d), st);
+    curc.alloc(T.n, ld_for(T.n, d), st);
+    ns_draw(cur.Y.p, cur.O.p, cur.ld, curc.Y.p, curc.O.p, curc.ld, 0, d);   // line 1, both sketches
+    ns_gen_D();                                                            // line 212, ordered pairs
+    setup_level(Dl, 0);
+    setup_level(Dl, 1);
+    ns_bsr_both(Dl, cur, curc, 0, d);                                      // line 213
+    for (int t = Dl; t >= top; --t) {
+      if (t < Dl) {
+        setup_level(t, 0);
+        setup_level(t, 1);
+        ns_bsr_both(t, cur, curc, 0, d);                                   // lines 240-243
+      }
+      Level& L = H.L(t);
+      Level& C = H.C(t);
+      int rounds = 0;
+      double eps = 0;
+      while (true) {
+        eps = eps_now();
+        cpqr(t, eps, 0);
+        cpqr(t, eps, 1);
+        ++rounds;
+        if (!o.adaptive) break;
+        bool conv = true;
+        const int pos = (o.tol_rule == H2_TOL_RMS) ? o.p_os : 0;
+        for (int c = 0; c < L.nclus && conv; ++c)
+          conv = (L.m[c] <= d || L.k[c] <= d - 1 - pos) && (C.m[c] <= d || C.k[c] <= d - 1 - pos);
+        if (conv) break;
+        if (d + o.d_blk > o.d_max) {
+          H.stats.failed_depth = t;
+          throw Error(H2_ERR_NOT_CONVERGED, "adaptive sampling reached d_max=" + std::to_string(o.d_max) +
+                                                " at depth " + std::to_string(t));
+        }
+        ns_update_samples(t, o.d_blk);
+        d += o.d_blk;
+      }
+      H.stats.rounds[t] = rounds;
+      H.stats.eps = eps;
+      commit(t, 0);
+      commit(t, 1);
+      Panel nr, nc;
+      if (t > top) {
+        nr.alloc(L.rtot, ld_for(L.rtot, d), st);
+        nc.alloc(C.rtot, ld_for(C.rtot, d), st);
+        shrink(t, cur.Y.p, cur.O.p, cur.ld, nr.Y.p, nr.O.p, nr.ld, d, 0);
+        shrink(t, curc.Y.p, curc.O.p, curc.ld, nc.Y.p, nc.O.p, nc.ld, d, 1);
+      }
+      ns_gen_B(t);                                                         // line 258, ordered pairs
+      cur = std::move(nr);
+      curc = std::move(nc);
+    }
+    finish(top, Dl);
+  }
+
   ~Builder() {
     // an exception may leave work queued on the internal streams: drain them before the
     // members (allocated on them) are released
@@ -950,23 +1248,32 @@ struct Builder {
       gen_B(t);                                     // line 258
       cur = std::move(next);
     }
+    finish(top, Dl);
+  }
+
+  // wait for the build, hand the level arrays to the matrix, fill the statistics
+  void finish(int top, int Dl) {
     join_prefetch();   // an unused speculative pass is waited for (at most one pass)
     H2_CUDA(cudaStreamSynchronize(st));
     stream_after(user_st, st);
     cur.release();
+    curc.release();
     W.release();
-    for (auto& L : H.lv) {
-      for (auto* a : {&L.d_m, &L.d_k, &L.d_perm, &L.d_skel}) a->detach();
-      for (auto* a : {&L.d_poff, &L.d_roff, &L.d_xoff, &L.d_B_off}) a->detach();
-      for (auto* a : {&L.X, &L.cert, &L.B}) a->detach();
-    }
+    Wc.release();
+    for (auto* lvs : {&H.lv, &H.lvc})
+      for (auto& L : *lvs) {
+        for (auto* a : {&L.d_m, &L.d_k, &L.d_perm, &L.d_skel}) a->detach();
+        for (auto* a : {&L.d_poff, &L.d_roff, &L.d_xoff, &L.d_B_off}) a->detach();
+        for (auto* a : {&L.X, &L.cert, &L.B}) a->detach();
+      }
     H.D.detach();
+    H.d_D_off.detach();
     // stats
     h2_build_stats& s = H.stats;
     s.samples = d;
     s.top_depth = top;
     s.leaf_depth = Dl;
-    s.entries_D = T.D_off.back();
+    s.entries_D = ns ? H.D_off.back() : T.D_off.back();
     s.entries_sketch = entries_sketch;
     s.sketch_columns = sketch_columns;
     s.bytes_D = H.D.bytes();
@@ -986,6 +1293,10 @@ struct Builder {
       s.bytes_B += L.B.bytes();
       if (t == Dl) s.bytes_U += L.X.bytes();
       else s.bytes_E += L.X.bytes();
+      if (ns) {
+        if (t == Dl) s.bytes_U += H.C(t).X.bytes();
+        else s.bytes_E += H.C(t).X.bytes();
+      }
     }
     timer.collect(s.t_phase_ms);
     if (getenv("H2_TRACE")) {
@@ -1003,17 +1314,19 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
   const h2_matrix* H = &Hm;
     const h2_tree& T = *H->tree;
   const int Dl = H->Dl, top = H->top;
+  // non-symmetric: the upward pass uses the column side (V, F), the downward pass the row side
+  const int up = H->nonsym ? 1 : 0;
   std::vector<DArr<double>> xh(Dl + 1), yh(Dl + 1);
   for (int t = top; t <= Dl; ++t) {
     const Level& L = H->L(t);
-    xh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
+    xh[t].alloc(std::max<int64_t>(H->S(up, t).rtot, 1) * q, st);
     yh[t].alloc(std::max<int64_t>(L.rtot, 1) * q, st);
     H2_CUDA(cudaMemsetAsync(yh[t].p, 0, sizeof(double) * std::max<int64_t>(L.rtot, 1) * q, st));
   }
   if (beta != 1.0) launch_scale(y, T.n, ldy, q, beta, st);
   // upward pass
   for (int t = Dl; t >= top; --t) {
-    const Level& L = H->L(t);
+    const Level& L = H->S(up, t);
     UpArgs a{};
     a.nclusters = L.nclus;
     a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
@@ -1045,6 +1358,12 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
     s.us = T.d_far[t].us;
     s.blk_off = L.d_B_off.p;
     s.blk = L.B.p;
+    if (H->nonsym) {   // ordered B_{s,b} (k_s x kc_b), read directly
+      s.xoff = H->C(t).d_roff.p;
+      s.kcnt = H->C(t).d_k.p;
+      s.uidx = nullptr;
+      s.tmode = 1;
+    }
     s.x = xh[t].p;
     s.ldx = q;
     s.y = yh[t].p;
@@ -1087,6 +1406,11 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
     s.us = T.d_near.us;
     s.blk_off = T.d_D_off;
     s.blk = H->D.p;
+    if (H->nonsym) {
+      s.blk_off = H->d_D_off.p;
+      s.uidx = nullptr;
+      s.tmode = 1;
+    }
     s.x = x;
     s.ldx = ldx;
     s.y = y;
@@ -1233,9 +1557,9 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
   return h2_build_dist(tree, sketch, entry, tol, opts, nullptr, stream, out, stats);
 }
 
-h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
-                        const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
-                        h2_build_stats* stats) {
+static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                            const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                            h2_build_stats* stats, bool nonsym) {
   if (!out) return (g_err = "h2_build: out is NULL", H2_ERR_INVALID_ARG);
   *out = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1278,6 +1602,12 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
       if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
+    if (nonsym)
+      H2_REQUIRE(sketch->kind != H2_S_H2_LOWRANK && entry->kind != H2_E_H2_LOWRANK,
+                 "h2_build_nonsym: H2 + low-rank operators are symmetric-only");
+    for (const h2_matrix* b : {sketch->kind == H2_S_H2_LOWRANK ? sketch->base : nullptr,
+                               entry->kind == H2_E_H2_LOWRANK ? entry->base : nullptr})
+      H2_REQUIRE(!b || (!b->nonsym && !b->partial), "h2_build: the H2+low-rank base must be a complete symmetric H2");
     const bool dist = comm && comm->nranks > 1;
     if (comm)
       H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks && (!dist || comm->allgatherv),
@@ -1294,7 +1624,8 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
     H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
     {
       Builder B(*tree, *sketch, *entry, tol, o, st, *H, comm);
-      B.run();
+      if (nonsym) B.run_nonsym();
+      else B.run();
     }
     if (dist) {
       H->nranks = comm->nranks;
@@ -1318,6 +1649,17 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
     g_err = "h2_build: host out of memory";
     return H2_ERR_OOM;
   }
+}
+
+h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                        const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                        h2_build_stats* stats) {
+  return build_impl(tree, sketch, entry, tol, opts, comm, stream, out, stats, false);
+}
+
+h2_status h2_build_nonsym(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                          const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats) {
+  return build_impl(tree, sketch, entry, tol, opts, nullptr, stream, out, stats, true);
 }
 
 h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream) {
@@ -1404,6 +1746,17 @@ h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_
     return H2_OK;
   }
   if (depth < H->top || depth > H->Dl) return (g_err = "h2_export_size: depth outside [top, leaf]", H2_ERR_INVALID_ARG);
+  if (what >= H2_X_RANK_C && what <= H2_X_CERT_C) {
+    if (!H->nonsym) return (g_err = "h2_export_size: column side exists for h2_build_nonsym matrices only", H2_ERR_INVALID_ARG);
+    const Level& C = H->C(depth);
+    switch (what) {
+      case H2_X_RANK_C: *count = C.nclus; break;
+      case H2_X_SKEL_C: *count = C.rtot; break;
+      case H2_X_BASIS_C: *count = C.xtot; break;
+      default: *count = 2 * (int64_t)C.nclus; break;
+    }
+    return H2_OK;
+  }
   const Level& L = H->L(depth);
   switch (what) {
     case H2_X_RANK: *count = L.nclus; break;
@@ -1417,7 +1770,7 @@ h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_
 }
 
 h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst) {
-  if (H && H->partial && (what == H2_X_BASIS || what == H2_X_D || what == H2_X_B || what == H2_X_CERT))
+  if (H && H->partial && (what == H2_X_BASIS || what == H2_X_D || what == H2_X_B || what == H2_X_CERT || what >= H2_X_RANK_C))
     return (g_err = "h2_export: distributed matrix: call h2_matrix_allgather first", H2_ERR_INVALID_ARG);
   int64_t cnt = 0;
   h2_status s = h2_export_size(H, what, depth, &cnt);
@@ -1427,7 +1780,15 @@ h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst) 
   const void* src = nullptr;
   size_t el = 8;
   if (what == H2_X_D) src = H->D.p;
-  else {
+  else if (what >= H2_X_RANK_C) {
+    const Level& C = H->C(depth);
+    switch (what) {
+      case H2_X_RANK_C: src = C.d_k.p; el = 4; break;
+      case H2_X_SKEL_C: src = C.d_skel.p; el = 4; break;
+      case H2_X_BASIS_C: src = C.X.p; break;
+      default: src = C.cert.p; break;
+    }
+  } else {
     const Level& L = H->L(depth);
     switch (what) {
       case H2_X_RANK: src = L.d_k.p; el = 4; break;
@@ -1451,8 +1812,9 @@ h2_status h2_matrix_get_stats(const h2_matrix* H, h2_build_stats* stats) {
 int64_t h2_matrix_device_bytes(const h2_matrix* H) {
   if (!H) return 0;
   int64_t b = H->D.bytes();
-  for (auto& L : H->lv)
-    b += L.X.bytes() + L.B.bytes() + L.d_skel.bytes() + L.d_perm.bytes();
+  for (auto* lvs : {&H->lv, &H->lvc})
+    for (auto& L : *lvs) b += L.X.bytes() + L.B.bytes() + L.d_skel.bytes() + L.d_perm.bytes();
+  b += H->d_D_off.bytes();
   return b;
 }
 

@@ -21,9 +21,9 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
   for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
     const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
-    const int m = a.cnt[s], nc = a.cnt[b];
+    const int m = a.cnt[s], nc = a.cnt2 ? a.cnt2[b] : a.cnt[b];
     const int32_t* ri = a.idx + a.off[s];
-    const int32_t* ci = a.idx + a.off[b];
+    const int32_t* ci = a.cnt2 ? a.idx2 + a.off2[b] : a.idx + a.off[b];
     double* out = a.out + a.out_off[u];
     for (int j0 = 0; j0 < nc; j0 += 256) {
       const int nj = min(256, nc - j0);
@@ -52,9 +52,9 @@ __global__ void __launch_bounds__(256) gen_dense_kernel(const double* __restrict
   for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
     const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
-    const int m = a.cnt[s], nc = a.cnt[b];
+    const int m = a.cnt[s], nc = a.cnt2 ? a.cnt2[b] : a.cnt[b];
     const int32_t* ri = a.idx + a.off[s];
-    const int32_t* ci = a.idx + a.off[b];
+    const int32_t* ci = a.cnt2 ? a.idx2 + a.off2[b] : a.idx + a.off[b];
     double* out = a.out + a.out_off[u];
     for (int i = warp; i < m; i += 8) {
       const double* arow = A + (int64_t)ri[i] * lda;
@@ -86,10 +86,10 @@ __global__ void gen_desc_kernel(GenArgs a, int32_t* m, int32_t* nc, int64_t* rof
     const int64_t u = a.ulist ? a.ulist[q] : q;
     int s = a.us[u], b = a.ub[u];
     m[q] = a.cnt[s];
-    nc[q] = a.cnt[b];
-    ld[q] = a.cnt[b];
+    nc[q] = a.cnt2 ? a.cnt2[b] : a.cnt[b];
+    ld[q] = nc[q];
     roff[q] = a.off[s];
-    coff[q] = a.off[b];
+    coff[q] = a.cnt2 ? a.off2[b] : a.off[b];
     outp[q] = a.out + a.out_off[u];
   }
 }
@@ -149,9 +149,9 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
   auto load_next = [&](int buf) {
     if (le >= e1) return;
     const int b = a.idx[le];
-    const int u = a.uidx[le];
-    const int mb = a.cnt[b];
-    const bool direct = (a.us[u] == s);
+    const int u = a.uidx ? a.uidx[le] : le;
+    const int mb = a.kcnt ? a.kcnt[b] : a.cnt[b];
+    const bool direct = a.tmode == 0 ? (a.us[u] == s) : (a.tmode == 1);
     const double* blk = a.blk + a.blk_off[u];
     const double* om = a.Om + a.ooff[b] * a.ldo + cb;
     const int nk = min(BT_K, mb - lk);
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   int nitems = 0;
-  for (int e = e0; e < e1; ++e) nitems += (a.cnt[a.idx[e]] + BT_K - 1) / BT_K;
+  for (int e = e0; e < e1; ++e) nitems += ((a.kcnt ? a.kcnt : a.cnt)[a.idx[e]] + BT_K - 1) / BT_K;
 #pragma unroll
   for (int q = 0; q < BSR_NS - 1; ++q) {
     load_next(q);
@@ -282,6 +282,8 @@ void launch_spmm(const SpmmArgs& s, cudaStream_t st) {
   a.us = s.us;
   a.blk_off = s.blk_off;
   a.blk = s.blk;
+  a.kcnt = s.kcnt;
+  a.tmode = s.tmode;
   a.Y = s.y;
   a.ldy = s.ldy;
   a.Om = s.x;

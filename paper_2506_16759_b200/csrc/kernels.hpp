@@ -44,13 +44,18 @@ struct GenArgs {
   const int32_t* idx;     // tree-order point indices
   const int64_t* out_off; // per unique pair
   double* out;
+  // optional column side (non-symmetric B_{s,b} = K(I~_s, J~_b)): columns from cnt2/off2/idx2
+  const int32_t* cnt2;
+  const int64_t* off2;
+  const int32_t* idx2;
 };
 void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, const GenArgs& a,
                 cudaStream_t st);
 void launch_gen_dense(const double* A, int64_t lda, const GenArgs& a, cudaStream_t st);
-// Y(rows) = A(rows, :) Omega for a dense row-major operator (cuBLAS DGEMM, the plain library GEMM)
+// Y(rows) = A(rows, :) Omega for a dense row-major operator (cuBLAS DGEMM, the plain library GEMM);
+// trans: Y(rows) = A(:, rows)^T Omega (the column sketch of the non-symmetric build)
 void dense_matrix_sketch(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, const double* Om,
-                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st);
+                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st, bool trans = false);
 // fill the pointer / size arrays of an h2_block_batch for a user entry callback
 void launch_gen_batch_desc(const GenArgs& a, int32_t* m, int32_t* nc, int64_t* roff, int64_t* coff, double** outp,
                            int32_t* ld, cudaStream_t st);
@@ -66,10 +71,12 @@ struct BsrArgs {
   const int32_t* cnt;     // per cluster: rows
   const int32_t* ptr;
   const int32_t* idx;
-  const int32_t* uidx;
+  const int32_t* uidx;    // block of CSR entry e: uidx[e] (NULL: e)
   const int32_t* us;      // stored orientation of unique pair u: rows = cluster us[u]
   const int64_t* blk_off;
   const double* blk;
+  const int32_t* kcnt;    // per partner cluster: rows of Om (NULL: cnt; non-symmetric ranks)
+  int tmode;              // 0: direct iff us[u] == s; 1: every block direct; 2: every block transposed
   double* Y;
   int64_t ldy;
   const double* Om;
@@ -190,6 +197,8 @@ struct SpmmArgs {
   const int32_t* us;
   const int64_t* blk_off;
   const double* blk;
+  const int32_t* kcnt;    // see BsrArgs
+  int tmode;
   const double* x;
   int64_t ldx;
   double* y;

@@ -364,7 +364,7 @@ void launch_sumsq_total(const double* part, int nleaf, double* accum, int* nonfi
 // Y (rows x ncols, row-major, ldy) = A(rows, :) (row-major, lda) Omega (n x ncols, row-major, ldo):
 // in column-major terms Y^T = Omega^T A(rows,:)^T, one DGEMM.
 void dense_matrix_sketch(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, const double* Om,
-                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st) {
+                         int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st, bool trans) {
   if (row1 <= row0 || ncols <= 0) return;
   static std::mutex mu;
   static cublasHandle_t handles[64] = {};
@@ -376,8 +376,12 @@ void dense_matrix_sketch(const double* A, int64_t lda, int64_t n, int64_t row0, 
   cublasSetStream(h, st);
   cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);   // FP64 (DMMA tensor cores when profitable), no reduced precision
   const double one = 1.0, zero = 0.0;
-  const cublasStatus_t r = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, ncols, (int)(row1 - row0), (int)n, &one, Om,
-                                       (int)ldo, A + row0 * lda, (int)lda, &zero, Y, (int)ldy);
+  // column-major view: Y^T = Om^T A(rows,:)^T;  trans: Y^T = Om^T A(:,rows)
+  const cublasStatus_t r =
+      trans ? cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ncols, (int)(row1 - row0), (int)n, &one, Om, (int)ldo,
+                          A + row0, (int)lda, &zero, Y, (int)ldy)
+            : cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, ncols, (int)(row1 - row0), (int)n, &one, Om, (int)ldo,
+                          A + row0 * lda, (int)lda, &zero, Y, (int)ldy);
   if (r != CUBLAS_STATUS_SUCCESS) throw Error(H2_ERR_CUDA, "cublasDgemm failed: " + std::to_string((int)r));
 }
 

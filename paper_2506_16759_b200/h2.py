@@ -115,8 +115,9 @@ def _kernel(kind, param):
 class H2Matrix:
     """Result of Algorithm 1: U (leaves), E (transfer), B (couplings), D (dense), I~ (skeletons)."""
 
-    def __init__(self, handle, tree, stats, keep=()):
+    def __init__(self, handle, tree, stats, keep=(), nonsym=False):
         self._h = handle
+        self.nonsym = nonsym      # h2_build_nonsym: row side (rank/skel/basis) + column side (*_c)
         self.tree = tree          # the matrix references the tree: keep it alive
         self.stats = stats
         self._keep = keep
@@ -144,56 +145,60 @@ class H2Matrix:
     def samples(self):
         return self.stats["samples"]
 
-    def rank(self, t):
-        return self._export(L.H2_X_RANK, t, np.int32).astype(np.int64)
+    def rank(self, t, side=0):
+        """side 0: row ranks (the symmetric build's only side); 1: column ranks (non-symmetric)."""
+        return self._export(L.H2_X_RANK_C if side else L.H2_X_RANK, t, np.int32).astype(np.int64)
 
-    def skel(self, t):
-        r = self.rank(t)
-        s = self._export(L.H2_X_SKEL, t, np.int32).astype(np.int64)
+    def skel(self, t, side=0):
+        r = self.rank(t, side)
+        s = self._export(L.H2_X_SKEL_C if side else L.H2_X_SKEL, t, np.int32).astype(np.int64)
         return np.split(s, np.cumsum(r)[:-1])
 
-    def panel_rows(self, t):
+    def panel_rows(self, t, side=0):
         if t == self.tree.leaf_depth:
             return (self.tree.end[t] - self.tree.begin[t]).astype(np.int64)
-        rc = self.rank(t + 1)
+        rc = self.rank(t + 1, side)
         return rc[0::2] + rc[1::2]
 
-    def basis(self, t):
-        """X_tau per cluster of depth t (m x k): U_tau at the leaves, [E_nu1; E_nu2] above."""
-        r = self.rank(t)
-        m = self.panel_rows(t)
-        x = self._export(L.H2_X_BASIS, t)
+    def basis(self, t, side=0):
+        """X_tau per cluster of depth t (m x k): U_tau at the leaves, [E_nu1; E_nu2] above
+        (side 1: the column bases V / [F1; F2] of a non-symmetric matrix)."""
+        r = self.rank(t, side)
+        m = self.panel_rows(t, side)
+        x = self._export(L.H2_X_BASIS_C if side else L.H2_X_BASIS, t)
         out, o = [], 0
         for mi, ki in zip(m, r):
             out.append(x[o:o + mi * ki].reshape(mi, ki))
             o += mi * ki
         return out
 
-    def cert(self, t):
-        return self._export(L.H2_X_CERT, t).reshape(-1, 2)
+    def cert(self, t, side=0):
+        return self._export(L.H2_X_CERT_C if side else L.H2_X_CERT, t).reshape(-1, 2)
 
     def D_blocks(self):
-        """dict (s, b) -> m_s x m_b for unique near pairs s <= b."""
+        """dict (s, b) -> m_s x m_b for unique near pairs s <= b (every ordered pair if nonsym)."""
         Dl = self.tree.leaf_depth
         raw = self._export(L.H2_X_D)
         sz = self.tree.end[Dl] - self.tree.begin[Dl]
         out, o = {}, 0
         for s, b in self.tree.near:
-            if s <= b:
+            if s <= b or self.nonsym:
                 n = sz[s] * sz[b]
                 out[(int(s), int(b))] = raw[o:o + n].reshape(sz[s], sz[b])
                 o += n
         return out
 
     def B_blocks(self, t):
-        """dict (s, b) -> k_s x k_b for unique far pairs s < b of depth t."""
+        """dict (s, b) -> k_s x k_b for unique far pairs s < b of depth t (nonsym: every ordered
+        pair, k_s x kc_b)."""
         r = self.rank(t)
+        rc = self.rank(t, 1) if self.nonsym else r
         raw = self._export(L.H2_X_B, t)
         out, o = {}, 0
         for s, b in self.tree.far[t]:
-            if s < b:
-                n = r[s] * r[b]
-                out[(int(s), int(b))] = raw[o:o + n].reshape(r[s], r[b])
+            if s < b or self.nonsym:
+                n = r[s] * rc[b]
+                out[(int(s), int(b))] = raw[o:o + n].reshape(r[s], rc[b])
                 o += n
         return out
 
@@ -234,7 +239,7 @@ def _stats_dict(s):
 
 
 def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, comm=None,
-          h2_sketch=None, dense=None, **opts):
+          h2_sketch=None, dense=None, nonsym=False, **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
@@ -247,6 +252,9 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     this tree (e.g. K at a tighter tolerance), entries from ``kernel``.
     dense=A: an explicit (n, n) float64 CUDA operator in TREE order (row-major): sketch A Omega
     (one DGEMM per draw) and entries A[i, j] (S§8(f) NEXT #4, a frontal-matrix stand-in).
+    nonsym=True: the non-symmetric construction K ~ D + U B V^T (h2_build_nonsym; row bases from
+    K Omega, column bases from K^T Psi); a ``sketch`` callable then receives transpose=0/1 as a
+    keyword and must write K^T omega for transpose=1; ``dense`` A is used as given (A^T via DGEMM).
     comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
     by subtrees (h2_build_dist); call ``H.allgather(comm)`` before matvec / block export.
     opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
@@ -286,7 +294,10 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
                 n, nr, nc = r.n, r.row_end - r.row_begin, r.ncols
                 om = device_view(r.omega, (n, nc), (r.ld_omega, 1))
                 y = device_view(r.y, (nr, nc), (r.ld_y, 1))
-                sketch(om, y, r.col0, r.row_begin, r.row_end)
+                if nonsym:
+                    sketch(om, y, r.col0, r.row_begin, r.row_end, transpose=r.transpose)
+                else:
+                    sketch(om, y, r.col0, r.row_begin, r.row_end)
                 return 0
             except Exception as exc:  # reported as H2_ERR_CALLBACK
                 import traceback
@@ -323,6 +334,11 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     h = C.c_void_p()
     st = L.h2_build_stats()
     cm = None
+    if nonsym:
+        assert comm is None, "the non-symmetric build is single-GPU"
+        check(lib.h2_build_nonsym(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o), _stream(stream),
+                                  C.byref(h), C.byref(st)))
+        return H2Matrix(h, tree, _stats_dict(st), keep, nonsym=True)
     if comm is not None:
         cm = C.byref(comm.struct)
         keep.append(comm)
