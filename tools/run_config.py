@@ -29,6 +29,9 @@ p.add_argument("--p-os", type=int, default=None, help="oversampling margin of th
 p.add_argument("--bootstrap", type=float, default=None,
                help="S8(f) NEXT #1: build an H^2 of K at this tighter tol (dense sketch, timed separately), "
                     "then the timed build at the workload tol with its O(N) H^2-matvec sketch")
+p.add_argument("--nonsym", type=float, default=None,
+               help="S8(f) NEXT #3 (dense workloads): operator exp(-r/l)(1 + v (x_0 - y_0)) with this v, "
+                    "built with h2_build_nonsym")
 a = p.parse_args()
 w = dict(WORKLOADS[a.workload])
 X = w["points"]()
@@ -58,6 +61,10 @@ if w.get("dense"):   # NEXT #4: materialise the operator in tree order (row bloc
     dense = torch.empty((n, n), dtype=torch.float64, device="cuda")
     for r0 in range(0, n, 4096):
         dense[r0:r0 + 4096] = torch.exp(-torch.cdist(Xt[r0:r0 + 4096], Xt) / w["param"])
+        if a.nonsym is not None:
+            dense[r0:r0 + 4096] *= 1 + a.nonsym * (Xt[r0:r0 + 4096, :1] - Xt[:, 0][None, :])
+    if a.nonsym is not None:
+        out["nonsym_v"] = a.nonsym
     out["dense_operator_GB"] = dense.numel() * 8 / 1e9
 if a.bootstrap is not None:
     t0 = time.perf_counter()
@@ -72,7 +79,7 @@ for r in range(a.reps):
     e0.record()
     H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, p_os=a.p_os if a.p_os is not None else w.get("p_os", 10),
                 tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk, dense=dense,
-                d_max=w.get("d_max", 512))
+                d_max=w.get("d_max", 512), nonsym=a.nonsym is not None)
     e1.record()
     e1.synchronize()
     times.append(e0.elapsed_time(e1) / 1e3)
@@ -81,6 +88,8 @@ for r in range(a.reps):
 st = H.stats
 out.update({"build_s": times, "samples": st["samples"], "phase_ms": st["t_phase_ms"], "rounds": st["rounds"],
             "ranks": {t: [st["rank_min"][t], st["rank_max"][t], round(st["rank_mean"][t], 1)] for t in st["rank_min"]},
+            **({"col_rank_mean": {t: round(float(H.rank(t, 1).mean()), 1)
+                                  for t in range(H.top_depth, T.leaf_depth + 1)}} if H.nonsym else {}),
             "entries_D": st["entries_D"], "entries_B": st["entries_B"], "matrix_GB": H.device_bytes() / 1e9,
             "peak_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "launches": st["launches"]})
 Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, a.probes))).cuda()
