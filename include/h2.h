@@ -183,6 +183,13 @@ typedef struct {
   int32_t max_rank;    /* cap on every rank, <=0: none                                 [0]   */
   uint64_t seed;       /* Omega stream key (Philox4x32-10, R8)               [1]   */
   uint32_t stream_id;  /* Omega stream id (counter word 2)                             [0]   */
+  /* A-posteriori check (PAPER.md L447 sampler-based error check; DESIGN.md
+   * R30): after the build, e = ||H Om_h - K_blk(Om_h)||_F / ||K_blk(Om_h)||_F over verify_probes
+   * held-out columns Om_h of stream stream_id + 2; while e > tol and fewer than verify_retries
+   * rebuilds were made, tol_safety /= 3 and the build is redone.  One GPU only (ignored under a
+   * communicator). */
+  int32_t verify_probes;   /* q, 0 = off, <= 64                                           [0]   */
+  int32_t verify_retries;  /* rebuild cap                                                  [2]   */
 } h2_build_opts;
 void h2_build_opts_default(h2_build_opts* opts);
 
@@ -205,6 +212,9 @@ typedef struct {
   int64_t launches;           /* device kernel launches issued by h2_build                  */
   double t_phase_ms[H2_NPHASE];
   double t_total_ms;
+  double verify_error;        /* e of the returned matrix (opts.verify_probes > 0), else 0    */
+  int32_t verify_rebuilds;    /* rebuilds with s/3 made by the a-posteriori check            */
+  double tol_safety_used;     /* s of the returned matrix                                    */
 } h2_build_stats;
 
 /* ---------------------------------------------------------------------------------------
@@ -273,6 +283,13 @@ h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream);
  * ldx, ldy >= ncols.  1 <= ncols <= 64. */
 h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y, int64_t ldy,
                     int32_t ncols, double alpha, double beta, void* stream);
+
+/* A-posteriori error estimate: Om_h = ncols columns of the
+ * h2_omega stream (seed, stream_id), Y_h = K_blk(Om_h) with `sketch` (any kind; a callback is
+ * called once for all n rows with transpose = 0), *err = ||H Om_h - Y_h||_F / ||Y_h||_F.
+ * 1 <= ncols <= 64.  Errors: INVALID_ARG (partial matrix, bad sketch), CUDA, CALLBACK. */
+h2_status h2_verify(const h2_matrix* H, const h2_sketch* sketch, int32_t ncols, uint64_t seed,
+                    uint32_t stream_id, void* stream, double* err);
 
 /* Built-in dense operator product, rows [row_begin,row_end): y = K(rows,:) * omega (the dense
  * sketch of BASELINE configs[1], also the multi-GPU row shard).  omega: dev, all n rows.

@@ -66,7 +66,8 @@ class h2_entry(C.Structure):
 class h2_build_opts(C.Structure):
     _fields_ = [("d_init", C.c_int32), ("d_blk", C.c_int32), ("d_max", C.c_int32), ("adaptive", C.c_int32),
                 ("tol_rule", C.c_int32), ("tol_safety", C.c_double), ("p_os", C.c_int32), ("norm", C.c_double),
-                ("max_rank", C.c_int32), ("seed", C.c_uint64), ("stream_id", C.c_uint32)]
+                ("max_rank", C.c_int32), ("seed", C.c_uint64), ("stream_id", C.c_uint32),
+                ("verify_probes", C.c_int32), ("verify_retries", C.c_int32)]
 
 
 class h2_build_stats(C.Structure):
@@ -76,7 +77,8 @@ class h2_build_stats(C.Structure):
                 ("entries_D", C.c_int64), ("entries_B", C.c_int64), ("entries_sketch", C.c_int64),
                 ("sketch_columns", C.c_int64),
                 ("bytes_U", C.c_int64), ("bytes_E", C.c_int64), ("bytes_B", C.c_int64), ("bytes_D", C.c_int64),
-                ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double)]
+                ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double),
+                ("verify_error", C.c_double), ("verify_rebuilds", C.c_int32), ("tol_safety_used", C.c_double)]
 
 
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)
@@ -100,6 +102,7 @@ SIGNATURES = {
                            C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_build_nonsym": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double,
                                   C.POINTER(h2_build_opts), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
+    "h2_verify": (C.c_int, [_P, C.POINTER(h2_sketch), C.c_int32, C.c_uint64, C.c_uint32, _P, C.POINTER(C.c_double)]),
     "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
                                 C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_matrix_allgather": (C.c_int, [_P, C.POINTER(h2_comm), _P]),

@@ -1542,6 +1542,8 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->max_rank = 0;
   o->seed = 1;
   o->stream_id = 0;
+  o->verify_probes = 0;
+  o->verify_retries = 2;
 }
 
 h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end) {
@@ -1555,6 +1557,94 @@ h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_
 h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                    const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats) {
   return h2_build_dist(tree, sketch, entry, tol, opts, nullptr, stream, out, stats);
+}
+
+}  // extern "C"
+
+namespace {
+// O10 a-posteriori check: ||H Om_h - K_blk(Om_h)||_F / ||K_blk(Om_h)||_F (h2_verify)
+double verify_impl(const h2_matrix& H, const h2_sketch& S, int q, uint64_t seed, uint32_t sid, cudaStream_t st) {
+  const h2_tree& T = *H.tree;
+  const int nleaf = 1 << T.Dl;
+  DArr<double> Om, Yh, part, acc;
+  DArr<int> nf;
+  Om.alloc(T.n * q, st);
+  Yh.alloc(T.n * q, st);
+  part.alloc(nleaf, st);
+  acc.alloc(2, st);
+  nf.alloc(1, st);
+  H2_CUDA(cudaMemsetAsync(acc.p, 0, 2 * sizeof(double), st));
+  H2_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), st));
+  launch_omega(seed, sid, 0, T.n, 0, q, Om.p, q, st);
+  if (S.kind == H2_S_DENSE_KERNEL) {
+    launch_dense_sketch(tree_kernel(&T, S.kern, st), T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om.p, q, q, Yh.p, q, true, st);
+  } else if (S.kind == H2_S_DENSE_MATRIX) {
+    dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, Om.p, q, q, Yh.p, q, st);
+  } else if (S.kind == H2_S_H2_LOWRANK) {
+    matvec_impl(*S.base, Om.p, q, Yh.p, q, q, 1.0, 0.0, st);
+    if (S.rank > 0) {
+      DArr<double> scr;
+      scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * q, st);
+      launch_lowrank_sketch(S.U, S.ld_U, S.rank, Om.p, q, q, T.n, Yh.p, q, scr.p, st);
+    }
+  } else {
+    h2_sketch_req rq{};
+    rq.n = T.n;
+    rq.row_begin = 0;
+    rq.row_end = T.n;
+    rq.col0 = 0;
+    rq.ncols = q;
+    rq.omega = Om.p;
+    rq.ld_omega = q;
+    rq.y = Yh.p;
+    rq.ld_y = q;
+    rq.stream = st;
+    int rc = S.fn(S.ctx, &rq);
+    if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+  }
+  launch_sumsq_leaf(Yh.p, T.d_leaf_begin, 0, nleaf, q, 0, q, part.p, st);
+  launch_sumsq_total(part.p, nleaf, acc.p, nf.p, st);
+  matvec_impl(H, Om.p, q, Yh.p, q, q, 1.0, -1.0, st);   // Yh = H Om_h - Y_h
+  launch_sumsq_leaf(Yh.p, T.d_leaf_begin, 0, nleaf, q, 0, q, part.p, st);
+  launch_sumsq_total(part.p, nleaf, acc.p + 1, nf.p, st);
+  double a[2];
+  int bad = 0;
+  H2_CUDA(cudaMemcpyAsync(a, acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  H2_CUDA(cudaMemcpyAsync(&bad, nf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  H2_CUDA(cudaStreamSynchronize(st));
+  if (bad) throw Error(H2_ERR_NONFINITE, "h2_verify: non-finite sample");
+  return a[0] > 0 ? std::sqrt(a[1] / a[0]) : std::sqrt(a[1]);
+}
+
+void reset_matrix(h2_matrix& H) {
+  H.lv.clear();
+  H.lvc.clear();
+  H.D = DArr<double>();
+  H.d_D_off = DArr<int64_t>();
+  H.D_off.clear();
+  H.nonsym = false;
+  std::memset(&H.stats, 0, sizeof(H.stats));
+  H.stats.failed_depth = -1;
+}
+}  // namespace
+
+extern "C" {
+
+h2_status h2_verify(const h2_matrix* H, const h2_sketch* sketch, int32_t ncols, uint64_t seed, uint32_t stream_id,
+                    void* stream, double* err) {
+  try {
+    H2_REQUIRE(H && sketch && err, "h2_verify: NULL argument");
+    H2_REQUIRE(!H->partial, "h2_verify: distributed matrix: call h2_matrix_allgather first");
+    H2_REQUIRE(ncols >= 1 && ncols <= 64, "h2_verify: need 1 <= ncols <= 64");
+    H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
+                   (sketch->kind == H2_S_H2_LOWRANK && sketch->base && !sketch->base->partial) ||
+                   (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= H->n),
+               "h2_verify: bad sketch");
+    *err = verify_impl(*H, *sketch, ncols, seed, stream_id, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
 }
 
 static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
@@ -1622,10 +1712,23 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     ensure_uploaded(tree);
     // the tree is owned by the caller; share it without taking ownership
     H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
-    {
-      Builder B(*tree, *sketch, *entry, tol, o, st, *H, comm);
-      if (nonsym) B.run_nonsym();
-      else B.run();
+    H2_REQUIRE(o.verify_probes >= 0 && o.verify_probes <= 64 && o.verify_retries >= 0,
+               "h2_build: need 0 <= verify_probes <= 64, verify_retries >= 0");
+    for (int rebuilds = 0;; ++rebuilds) {
+      {
+        Builder B(*tree, *sketch, *entry, tol, o, st, *H, comm);
+        if (nonsym) B.run_nonsym();
+        else B.run();
+      }
+      H->stats.tol_safety_used = o.tol_safety;
+      H->stats.verify_rebuilds = rebuilds;
+      if (dist || o.verify_probes <= 0) break;
+      // O10 (R30): held-out columns of stream stream_id + 2; rebuild with s / 3 while e > tol
+      const double e = verify_impl(*H, *sketch, o.verify_probes, o.seed, o.stream_id + 2, st);
+      H->stats.verify_error = e;
+      if (!(e > tol) || rebuilds >= o.verify_retries) break;
+      reset_matrix(*H);
+      o.tol_safety /= 3;
     }
     if (dist) {
       H->nranks = comm->nranks;

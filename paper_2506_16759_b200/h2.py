@@ -202,6 +202,20 @@ class H2Matrix:
                 o += n
         return out
 
+    def verify(self, kernel=("exp", 0.2), q=8, seed=1, stream_id=2, dense=None, stream=None):
+        """A-posteriori estimate (h2_verify): ||H Om_h - K Om_h||_F / ||K Om_h||_F
+        over q held-out columns of the Omega stream (seed, stream_id); K the built-in kernel or
+        the dense tree-order operator ``dense``."""
+        sk = L.h2_sketch()
+        sk.kern = _kernel(*kernel)
+        if dense is not None:
+            sk.kind, sk.A, sk.ld_A = L.H2_S_DENSE_MATRIX, dense.data_ptr(), dense.stride(0)
+        else:
+            sk.kind = L.H2_S_DENSE_KERNEL
+        e = C.c_double()
+        check(lib.h2_verify(self._h, C.byref(sk), q, seed, stream_id, _stream(stream), C.byref(e)))
+        return e.value
+
     def allgather(self, comm, stream=None):
         """Complete a distributed build on every rank (h2_matrix_allgather; collective)."""
         check(lib.h2_matrix_allgather(self._h, C.byref(comm.struct), _stream(stream)))
@@ -228,7 +242,7 @@ class H2Matrix:
 def _stats_dict(s):
     d = {k: getattr(s, k) for k in ("samples", "failed_depth", "top_depth", "leaf_depth", "eps", "entries_D",
                                     "entries_B", "entries_sketch", "sketch_columns", "bytes_U", "bytes_E", "bytes_B", "bytes_D",
-                                    "launches", "t_total_ms")}
+                                    "launches", "t_total_ms", "verify_error", "verify_rebuilds", "tol_safety_used")}
     lo, hi = s.top_depth, s.leaf_depth
     d["rounds"] = {t: s.rounds[t] for t in range(lo, hi + 1)}
     d["rank_min"] = {t: s.rank_min[t] for t in range(lo, hi + 1)}

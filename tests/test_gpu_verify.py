@@ -1,0 +1,49 @@
+"""O10 a-posteriori check (h2_verify / opts.verify_probes, R30) against oracle/verify.py."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import geometry, kernels, h2 as oh2, rng, verify
+from synth import uniform_points
+import paper_2506_16759_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(X, s, retries):
+    tree = geometry.build_cluster_tree(X, 64)
+    part = geometry.build_partition(tree, 0.7)
+    op = kernels.KernelOperator("exp", 0.2, X[tree.perm])
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, tree.n, c0, nc)
+    Oh = rng.omega_block(1, 2, 0, tree.n, 0, 8)
+    return verify.build_verified(tree, part, op.sampler, op.entry, om, Oh, 1e-6, oh2.BuildOpts(tol_safety=s),
+                                 retries=retries)
+
+
+@pytest.mark.parametrize("s", [0.1, 30.0])
+def test_verify_matches_oracle(s):
+    X = uniform_points(2048, 3, 0)
+    T = g.Tree(X, 64)
+    Hg = g.build(T, ("exp", 0.2), 1e-6, tol_safety=s, verify_probes=8, verify_retries=6)
+    Ho, e, r, s_used = _oracle(X, s, 6)
+    st = Hg.stats
+    assert st["verify_rebuilds"] == r
+    assert st["tol_safety_used"] == s_used
+    assert st["verify_error"] <= 1e-6 and e <= 1e-6
+    assert abs(st["verify_error"] - e) <= 0.05 * e
+    # the standalone call is the same computation
+    assert Hg.verify(q=8) == st["verify_error"]
+
+
+def test_verify_dense_operator_and_no_retry_when_off():
+    X = uniform_points(3000, 3, 5)
+    T = g.Tree(X, 64)
+    Xt = torch.from_numpy(X[T.perm]).cuda()
+    A = torch.exp(-torch.cdist(Xt, Xt) / 0.2)
+    H = g.build(T, ("exp", 0.2), 1e-6, dense=A, tol_safety=30.0)
+    assert H.stats["verify_rebuilds"] == 0 and H.stats["verify_error"] == 0.0
+    e = H.verify(dense=A)
+    P = g.omega(T.n, 8, seed=1, stream_id=2)
+    ref = A @ P
+    direct = (torch.linalg.norm(H.matvec(P) - ref) / torch.linalg.norm(ref)).item()
+    assert abs(e - direct) <= 1e-6 * direct
