@@ -177,7 +177,7 @@ typedef struct {
   int32_t adaptive;    /* 1: §III-B convergence loop; 0: fixed sample size §III-A      [1]   */
   int32_t tol_rule;    /* H2_TOL_RMS: eps_l = s*tol*||Y||_F/sqrt(N)  (R10/R11)         [RMS] */
                        /* H2_TOL_LITERAL: eps_l = tol*norm (p_os = 0)          */
-  double tol_safety;   /* s                                                            [0.1] */
+  double tol_safety;   /* s (at the leaf depth; see eps_decay, R31)          [0.04] */
   int32_t p_os;        /* oversampling margin: converged iff m<=d or k<=d-1-p_os (R12) [10]  */
   double norm;         /* nu for H2_TOL_LITERAL                                        [0]   */
   int32_t max_rank;    /* cap on every rank, <=0: none                                 [0]   */
@@ -190,6 +190,10 @@ typedef struct {
    * communicator). */
   int32_t verify_probes;   /* q, 0 = off, <= 64                                           [0]   */
   int32_t verify_retries;  /* rebuild cap                                                  [2]   */
+  /* level schedule of the threshold (R31; a study of S§8(f) NEXT #2, the paper's
+   * "simple error compensation scheme" P:L496 being unspecified): eps_l at depth t is multiplied
+   * by eps_decay^(leaf_depth - t); 1 = the uniform eps_l of R11                    [1.25] */
+  double eps_decay;
 } h2_build_opts;
 void h2_build_opts_default(h2_build_opts* opts);
 
@@ -324,6 +328,11 @@ h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_
 h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst);
 h2_status h2_matrix_get_stats(const h2_matrix* H, h2_build_stats* stats);
 int64_t h2_matrix_device_bytes(const h2_matrix* H);
+/* Device memory held by libh2's block cache (freed workspaces kept for reuse across builds, the
+ * "single allocation per operation" of PAPER.md L384) on the current device, and its release
+ * (cudaFree of every cached block after a device synchronisation). */
+int64_t h2_cache_bytes(void);
+void h2_cache_trim(void);
 void h2_free(h2_matrix* H);
 
 const char* h2_last_error(void);

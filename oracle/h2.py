@@ -32,10 +32,11 @@ class BuildOpts:
     d_max: int = 512
     adaptive: bool = True
     tol_rule: str = "rms"        # "rms": eps = s * tol * ||Y||_F / sqrt(N);  "literal": eps = tol * nu
-    tol_safety: float = 0.1      # s
+    tol_safety: float = 0.04     # s (leaf depth; R31)
     p_os: int = 10               # oversampling margin in the convergence test (0 in literal mode)
     norm: float = 0.0            # nu for the literal rule
     max_rank: int = None
+    eps_decay: float = 1.25      # R31: eps at depth t scaled by eps_decay^(Dl - t)
 
 
 @dataclass
@@ -55,12 +56,14 @@ class H2Matrix:
     eps: float = 0.0
 
 
-def _eps(opts, tol, sumsq, n):
-    """R10/R11: eps_l (eps_abs = eps * approximate norm)."""
+def _eps(opts, tol, sumsq, n, levels_up=0):
+    """R10/R11: eps_l (eps_abs = eps * approximate norm); R31: times
+    eps_decay^levels_up (levels_up = Dl - t)."""
+    lvl = 1.0 if opts.eps_decay == 1.0 else opts.eps_decay ** levels_up
     if opts.tol_rule == "rms":
-        return opts.tol_safety * tol * np.sqrt(sumsq / n)
+        return lvl * (opts.tol_safety * tol * np.sqrt(sumsq / n))
     if opts.tol_rule == "literal":
-        return tol * opts.norm
+        return lvl * (tol * opts.norm)
     raise ValueError(opts.tol_rule)
 
 
@@ -146,7 +149,7 @@ def build(tree, part, sampler, entry, omega, tol, opts: BuildOpts = None) -> H2M
             Yl, Ol = inner_subtract(t, Yn, On)
         rounds = 0
         while True:
-            eps = _eps(opts, tol, sumsq, N)
+            eps = _eps(opts, tol, sumsq, N, Dl - t)
             ids = [row_id(Yl[c], eps, opts.max_rank) for c in range(1 << t)]
             rounds += 1
             if not opts.adaptive:

@@ -59,10 +59,11 @@ def build_nonsym(tree, part, sampler, sampler_t, entry, omega, psi, tol, opts: B
     for (s, b) in part.near:
         H.D[(int(s), int(b))] = entry(rng_of(Dl, s), rng_of(Dl, b))
 
-    def eps_now():
+    def eps_now(t):
+        lvl = 1.0 if opts.eps_decay == 1.0 else opts.eps_decay ** (Dl - t)   # R31
         if opts.tol_rule == "rms":
-            return opts.tol_safety * tol * np.sqrt(sumsq / (2 * N))
-        return tol * opts.norm
+            return lvl * (opts.tol_safety * tol * np.sqrt(sumsq / (2 * N)))
+        return lvl * (tol * opts.norm)
 
     def leaf_subtract(Yc, Zc, Oc, Pc):
         """line 213 for both sides: Y^loc = Y - sum D Omega_b, Z^loc = Z - sum D_{b,tau}^T Psi_b."""
@@ -125,7 +126,7 @@ def build_nonsym(tree, part, sampler, sampler_t, entry, omega, psi, tol, opts: B
             Yl, Zl, Ol, Pl = inner_subtract(t, Yn, Zn, On, Pn)
         rounds = 0
         while True:
-            eps = eps_now()
+            eps = eps_now(t)
             ir = [row_id(Yl[c], eps, opts.max_rank) for c in range(1 << t)]
             ic = [row_id(Zl[c], eps, opts.max_rank) for c in range(1 << t)]
             rounds += 1

@@ -67,7 +67,7 @@ class h2_build_opts(C.Structure):
     _fields_ = [("d_init", C.c_int32), ("d_blk", C.c_int32), ("d_max", C.c_int32), ("adaptive", C.c_int32),
                 ("tol_rule", C.c_int32), ("tol_safety", C.c_double), ("p_os", C.c_int32), ("norm", C.c_double),
                 ("max_rank", C.c_int32), ("seed", C.c_uint64), ("stream_id", C.c_uint32),
-                ("verify_probes", C.c_int32), ("verify_retries", C.c_int32)]
+                ("verify_probes", C.c_int32), ("verify_retries", C.c_int32), ("eps_decay", C.c_double)]
 
 
 class h2_build_stats(C.Structure):
@@ -102,6 +102,8 @@ SIGNATURES = {
                            C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_build_nonsym": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double,
                                   C.POINTER(h2_build_opts), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
+    "h2_cache_bytes": (C.c_int64, []),
+    "h2_cache_trim": (None, []),
     "h2_verify": (C.c_int, [_P, C.POINTER(h2_sketch), C.c_int32, C.c_uint64, C.c_uint32, _P, C.POINTER(C.c_double)]),
     "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
                                 C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),

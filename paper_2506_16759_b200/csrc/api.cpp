@@ -495,7 +495,9 @@ struct Builder {
     timer.end();
   }
 
-  double eps_now() {
+  double eps_now(int t) {
+    // level schedule (R31, S§8(f) NEXT #2 study): eps_t = eps * eps_decay^(Dl - t)
+    const double lvl = o.eps_decay == 1.0 ? 1.0 : std::pow(o.eps_decay, (double)(T.Dl - t));
     double acc = 0;
     int nf = 0;
     H2_CUDA(cudaMemcpyAsync(&acc, sumsq_acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -503,8 +505,8 @@ struct Builder {
     H2_CUDA(cudaStreamSynchronize(st));
     if (nf) throw Error(H2_ERR_NONFINITE, "the sketch produced a non-finite sample");
     // non-symmetric: acc holds ||Y||^2 + ||Z||^2 (R29: RMS over both sketches)
-    if (o.tol_rule == H2_TOL_RMS) return o.tol_safety * tol * std::sqrt(acc / (double)(ns ? 2 * T.n : T.n));
-    return tol * o.norm;
+    if (o.tol_rule == H2_TOL_RMS) return lvl * (o.tol_safety * tol * std::sqrt(acc / (double)(ns ? 2 * T.n : T.n)));
+    return lvl * (tol * o.norm);
   }
 
   // ---------------------------------------------------------------- batched entry generation
@@ -1097,7 +1099,7 @@ struct Builder {
       int rounds = 0;
       double eps = 0;
       while (true) {
-        eps = eps_now();
+        eps = eps_now(t);
         cpqr(t, eps, 0);
         cpqr(t, eps, 1);
         ++rounds;
@@ -1220,7 +1222,7 @@ struct Builder {
       int rounds = 0;
       double eps = 0;
       while (true) {
-        eps = eps_now();
+        eps = eps_now(t);
         cpqr(t, eps);
         ++rounds;
         if (!o.adaptive) break;
@@ -1536,7 +1538,7 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->d_max = 512;
   o->adaptive = 1;
   o->tol_rule = H2_TOL_RMS;
-  o->tol_safety = 0.1;
+  o->tol_safety = 0.04;
   o->p_os = 10;
   o->norm = 0.0;
   o->max_rank = 0;
@@ -1544,6 +1546,7 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->stream_id = 0;
   o->verify_probes = 0;
   o->verify_retries = 2;
+  o->eps_decay = 1.25;
 }
 
 h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end) {
@@ -1712,6 +1715,7 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     ensure_uploaded(tree);
     // the tree is owned by the caller; share it without taking ownership
     H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
+    H2_REQUIRE(o.eps_decay > 0 && std::isfinite(o.eps_decay), "h2_build: eps_decay must be > 0");
     H2_REQUIRE(o.verify_probes >= 0 && o.verify_probes <= 64 && o.verify_retries >= 0,
                "h2_build: need 0 <= verify_probes <= 64, verify_retries >= 0");
     for (int rebuilds = 0;; ++rebuilds) {
@@ -1922,5 +1926,8 @@ int64_t h2_matrix_device_bytes(const h2_matrix* H) {
 }
 
 void h2_free(h2_matrix* H) { delete H; }
+
+int64_t h2_cache_bytes(void) { return (int64_t)h2::cache_bytes_held(); }
+void h2_cache_trim(void) { h2::cache_trim(); }
 
 }  // extern "C"

@@ -176,3 +176,19 @@ def test_deterministic():
         assert np.array_equal(H1.rank[t], H2.rank[t])
         for a, b in zip(H1.X[t], H2.X[t]):
             assert np.array_equal(a, b)
+
+
+def test_eps_decay_schedule_leaf_identity_and_monotone_parent():
+    """R31 level schedule: the leaf threshold is unchanged (decay^0), so leaf ranks and skeletons
+    equal the uniform build's; one level up the panels are identical, and a smaller threshold
+    cannot truncate earlier, so ranks there are >= the uniform build's."""
+    X = uniform_points(2048, 3, 0)
+    tree, part, om = setup(X, 64)
+    op = kernels.KernelOperator("exp", 0.2, X[tree.perm])
+    kw = dict(adaptive=False, d_init=160)
+    H1 = h2.build(tree, part, op.sampler, op.entry, om, 1e-6, h2.BuildOpts(**kw))
+    Hg = h2.build(tree, part, op.sampler, op.entry, om, 1e-6, h2.BuildOpts(eps_decay=0.5, **kw))
+    Dl = tree.leaf_depth
+    assert np.array_equal(H1.rank[Dl], Hg.rank[Dl])
+    assert all(np.array_equal(a, b) for a, b in zip(H1.skel[Dl], Hg.skel[Dl]))
+    assert np.all(Hg.rank[Dl - 1] >= H1.rank[Dl - 1]) and Hg.rank[Dl - 1].sum() > H1.rank[Dl - 1].sum()

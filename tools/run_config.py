@@ -32,6 +32,7 @@ p.add_argument("--bootstrap", type=float, default=None,
 p.add_argument("--nonsym", type=float, default=None,
                help="S8(f) NEXT #3 (dense workloads): operator exp(-r/l)(1 + v (x_0 - y_0)) with this v, "
                     "built with h2_build_nonsym")
+p.add_argument("--eps-decay", type=float, default=1.0, help="R31 level schedule eps_t = eps * decay^(Dl-t)")
 a = p.parse_args()
 w = dict(WORKLOADS[a.workload])
 X = w["points"]()
@@ -40,7 +41,7 @@ kern = (w["kernel"], w["param"])
 t0 = time.perf_counter()
 T = g.Tree(X, w["leaf"], 0.7)
 t_tree = time.perf_counter() - t0
-out = {"workload": a.workload, "n": n, "leaf": w["leaf"], "tol": w["tol"], "tree_s": t_tree,
+out = {"workload": a.workload, "eps_decay": a.eps_decay, "n": n, "leaf": w["leaf"], "tol": w["tol"], "tree_s": t_tree,
        "leaf_depth": T.leaf_depth, "top_depth": T.top_depth, "near_nnz": T.near_nnz, "far_nnz": T.far_nnz_total,
        "csp": T.csp}
 times = []
@@ -48,7 +49,7 @@ update = None
 if "update_rank" in w:      # configs[4]: base H^2 of A (untimed setup, like PAPER.md L479), then M = A_H + U U^T
     from synth import lowrank_factor
     t0 = time.perf_counter()
-    Hbase = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s)
+    Hbase = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, tol_safety=a.s, eps_decay=a.eps_decay)
     torch.cuda.synchronize()
     out["base_build_s"] = time.perf_counter() - t0
     out["base_samples"] = Hbase.samples
@@ -79,7 +80,7 @@ for r in range(a.reps):
     e0.record()
     H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, p_os=a.p_os if a.p_os is not None else w.get("p_os", 10),
                 tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk, dense=dense,
-                d_max=w.get("d_max", 512), nonsym=a.nonsym is not None)
+                d_max=w.get("d_max", 512), nonsym=a.nonsym is not None, eps_decay=a.eps_decay)
     e1.record()
     e1.synchronize()
     times.append(e0.elapsed_time(e1) / 1e3)
@@ -92,6 +93,9 @@ out.update({"build_s": times, "samples": st["samples"], "phase_ms": st["t_phase_
                                   for t in range(H.top_depth, T.leaf_depth + 1)}} if H.nonsym else {}),
             "entries_D": st["entries_D"], "entries_B": st["entries_B"], "matrix_GB": H.device_bytes() / 1e9,
             "peak_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "launches": st["launches"]})
+from paper_2506_16759_b200._lib import lib as _lib  # noqa: E402
+out["cache_GB_before_trim"] = _lib.h2_cache_bytes() / 1e9
+_lib.h2_cache_trim()
 Xp = torch.from_numpy(np.random.default_rng(2).standard_normal((n, a.probes))).cuda()
 t0 = time.perf_counter()
 if dense is not None:
