@@ -377,8 +377,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
       const int jj0 = 16 * g + 8 * h;
       uint32_t lo[RPT][8], hi[RPT][8];
+#ifdef H2_EXP_HALF
+      constexpr int QE = 4;   // experiment: evaluate half the j of a chunk (the rest copied)
+#else
+      constexpr int QE = 8;
+#endif
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < QE; ++q) {
         const int jj = jj0 + q;
         const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
 #pragma unroll
@@ -389,6 +394,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
           hi[k][q] = m.y;
         }
       }
+#pragma unroll
+      for (int q = QE; q < 8; ++q)
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          lo[k][q] = lo[k][q - QE] ^ (uint32_t)q;
+          hi[k][q] = hi[k][q - QE];
+        }
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         uint32_t w[4][4];
@@ -467,6 +479,279 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
+
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant of the 128-column pass (cta_group::2): two CTAs of
+// a cluster own adjacent 64-row tiles and the same j range; the leader issues
+// tcgen05.mma.cta_group::2 with M = 128 (64 rows per SM) x N = 128 x K = 32, whose A operand is
+// each CTA's own K slices and whose B operand is split by columns (CTA r holds Omega columns
+// [64 r, 64 r + 64) of the chunk).  Each SM's 64 x 128 accumulator of a slice occupies all 128
+// TMEM lanes x 64 columns (lanes 64 h + m: row m, columns [64 h, 64 h + 64)), 7 slices in 448
+// columns, and an M = 128 dispatch runs the tensor core at its full rate (an M = 64 single-CTA
+// dispatch costs the same cycles for half the rows).  Producers, ring and drain as above; the
+// peer's producers arrive on the leader's full barrier (cluster scope) and the MMA completion is
+// multicast to the empty / drain barriers of both CTAs.
+// ------------------------------------------------------------------------------------------
+constexpr int PR_TM = 64, PR_NCOL = 128, PR_NH = 64, PR_JC = 128;
+struct PairPlan {
+  static constexpr int SLICE = PR_TM * PR_JC;              // 8 KB
+  static constexpr int ABUF = TC_NS * SLICE;               // 56 KB
+  static constexpr int NA = 2;
+  static constexpr int BBUF = PR_NH * PR_JC;               // this CTA's half of B: 8 KB
+  static constexpr int CBUF = PR_JC * 32 + PR_JC * 2;
+  static constexpr int DRAIN = TC_DRAIN_J / PR_JC;
+  static constexpr int A0 = 0;
+  static constexpr int B0 = NA * ABUF;
+  static constexpr int C0 = B0 + TC_NB * BBUF;
+  static constexpr int BAR = C0 + TC_NB * CBUF;
+  static constexpr int TOTAL = BAR + 8 * (2 * NA + TC_NB + 1) + 16;
+  static_assert(TOTAL + 16 * 256 * 8 <= 227 * 1024, "shared memory plan exceeds 227 KB");
+};
+
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITC_%=;\n}\n" ::"r"(addr),
+      "r"(parity));
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::);
+}
+
+template <int KIND, int NPW>
+__global__ void __launch_bounds__(32 * (NPW + 1), 1)
+    sketch_tc_pair_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
+                          const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout,
+                          int64_t ldy, int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag) {
+  using P = PairPlan;
+  constexpr int TM = PR_TM, JC = PR_JC;
+  constexpr int G = JC / 16;
+  constexpr int CBUF = P::CBUF;
+  constexpr int NA = P::NA;
+  constexpr int RPT = TM * G / (16 * NPW);
+  constexpr int BBUF = P::BBUF;
+  constexpr int LBO_A = TM * 16;
+  constexpr int LBO_B = PR_NH * 16;
+  constexpr uint32_t IDESC = idesc_i8<128, PR_NCOL>();   // M = 128 over the CTA pair
+  constexpr uint32_t IDESC6 = KIND == H2_K_EXP ? IDESC : (IDESC | (1u << 7));
+  static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(128) double tab[16 * 256];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t bar_full = sbase + P::BAR;
+  const uint32_t bar_empty = bar_full + 8 * NA;
+  const uint32_t bar_loaded = bar_empty + 8 * NA;
+  const uint32_t bar_drain = bar_loaded + 8 * TC_NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + P::BAR + 8 * (2 * NA + TC_NB + 1));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+  const bool leader = crank == 0;
+  const int64_t rtile = row0 + (int64_t)blockIdx.x * TM;
+  const int64_t nunits = nchunks / (128 / JC);
+  const int64_t ch_b = nunits * blockIdx.y / gridDim.y * (128 / JC);
+  const int64_t ch_e = nunits * (blockIdx.y + 1) / gridDim.y * (128 / JC);
+  const int nch = (int)(ch_e - ch_b);
+  const bool control = (warp == NPW);
+  const int8_t* Bh = Bq + (int64_t)crank * nchunks * BBUF;   // this CTA's column half
+
+  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + 52.0);
+  if (tid == 0) {
+    for (int b = 0; b < NA; ++b) {
+      mbar_init(bar_full + 8 * b, leader ? 2 * NPW : NPW);   // leader: both CTAs' producers
+      mbar_init(bar_empty + 8 * b, 1);
+    }
+    for (int q = 0; q < TC_NB; ++q) mbar_init(bar_loaded + 8 * q, 32);
+    mbar_init(bar_drain, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  cluster_sync_all();   // peer barriers initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = *tmem_slot;
+  double* Yo = Yout + blockIdx.y * split_stride;
+
+  if (control) {
+    auto prefetch = [&](int it) {
+      if (it >= nch) return;
+      const int64_t t = ch_b + it;
+      const int slot = it & (TC_NB - 1);
+#pragma unroll
+      for (int q = 0; q < BBUF / 16 / 32; ++q) {
+        const int e = lane + 32 * q;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::B0 + slot * BBUF + e * 16),
+                     "l"(Bh + t * BBUF + e * 16));
+      }
+#pragma unroll
+      for (int q = 0; q < JC / 16; ++q) {
+        const int e = lane + 32 * q;
+        const int jc = e >> 1;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::C0 + slot * CBUF + e * 16 +
+                                                                          (jc >> 3) * 16),
+                     "l"(reinterpret_cast<const char*>(C + t * JC) + e * 16));
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
+    };
+    prefetch(0);
+    prefetch(1);
+    for (int it = 0; it < nch; ++it) {
+      const int buf = it % NA;
+      const int slot = it & (TC_NB - 1);
+      // full(it): both CTAs' producers (leader) / this CTA's producers (peer) finished chunk it,
+      // hence MMA(it - 2) completed and ring slot (it + 2) % 4 is free in this CTA
+      mbar_wait_cluster(bar_full + 8 * buf, (it / NA) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      if (leader && lane == 0) {
+        const bool first = (it % P::DRAIN) == 0;
+        const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
+        const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
+        const uint32_t b0 = sbase + P::B0 + slot * BBUF;
+#pragma unroll
+        for (int sl = 0; sl < TC_NS; ++sl)
+#pragma unroll
+          for (int kk = 0; kk < JC / 32; ++kk) {
+            const uint64_t ad = umma_desc(a0 + sl * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
+            const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
+            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(sl * PR_NH)),
+                "l"(ad), "l"(bd), "r"(sl == TC_NS - 1 ? IDESC6 : IDESC), "r"(acc));
+          }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                bar_empty + 8 * buf),
+            "h"((uint16_t)3));
+        if (drain)
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                  bar_drain),
+              "h"((uint16_t)3));
+      }
+      __syncwarp();
+      prefetch(it + 2);
+    }
+  } else {
+    const int g = warp % G;
+    const int rs = warp / G;
+    const int h = lane & 1;
+    const int r0 = 16 * rs + (lane >> 1);
+    double4 ci[RPT];
+    int off[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = r0 + k * 16 * (NPW / G);
+      ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
+      off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
+    }
+    uint32_t full_remote = 0;
+    if (!leader)
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(full_remote) : "r"(bar_full), "r"(0));
+    const uint32_t lane8 = 8u * (lane & 15);
+    uint32_t ovf = 0;
+    int drains = 0;
+    for (int it = 0; it < nch; ++it) {
+      const int buf = it % NA;
+      const int slot = it & (TC_NB - 1);
+      mbar_wait(bar_loaded + 8 * slot, (it / TC_NB) & 1);
+      if (it >= NA) mbar_wait(bar_empty + 8 * buf, ((it - NA) / NA) & 1);
+      const uint8_t* cb = smem + P::C0 + slot * CBUF;
+      uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
+      const int jj0 = 16 * g + 8 * h;
+      uint32_t lo[RPT][8], hi[RPT][8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int jj = jj0 + q;
+        const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51(r2, hs, ovf);
+          lo[k][q] = m.x;
+          hi[k][q] = m.y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        uint32_t w[4][4];
+        transpose4(lo[k][0], lo[k][1], lo[k][2], lo[k][3], w[0]);
+        transpose4(lo[k][4], lo[k][5], lo[k][6], lo[k][7], w[1]);
+        transpose4(hi[k][0], hi[k][1], hi[k][2], hi[k][3], w[2]);
+        transpose4(hi[k][4], hi[k][5], hi[k][6], hi[k][7], w[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint2*>(Ab + q * P::SLICE + off[k]) = make_uint2(w[0][q], w[1][q]);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          *reinterpret_cast<uint2*>(Ab + (q + 4) * P::SLICE + off[k]) = make_uint2(w[2][q], w[3][q]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
+        if (!leader)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(full_remote + 8 * buf));
+      }
+
+      const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
+      if (drain && warp < 4) {
+        mbar_wait(bar_drain, drains & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        // lane 32 w + l holds row 32 (w & 1) + l, columns [64 (w >> 1), +64), all 7 slices at
+        // columns 64 s; summed as (s0..s3 chain) + (s4..s6 chain) like the other pass shapes
+        const int64_t i = rtile + 32 * (warp & 1) + lane;
+        const int ch = 64 * (warp >> 1);
+        double* y = Yo + (i - row0) * ldy + ch;
+#pragma unroll 1
+        for (int c0 = 0; c0 < PR_NH; c0 += 8) {   // 8 columns at a time (register budget)
+          double v[8], u[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = u[c] = 0.0;
+#pragma unroll
+          for (int sl = 0; sl < TC_NS; ++sl) {
+            uint32_t r[8];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sl * PR_NH + c0);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                           "=r"(r[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const double wgt = ldexp(1.0, 8 * sl + wshift);
+            if (sl >= 4) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+            }
+          }
+          if (i < row1) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int col = ch + c0 + c;
+              if (col < ncols) y[c0 + c] = drains == 0 ? v[c] + u[c] : y[c0 + c] + (v[c] + u[c]);
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      }
+      if (drain) ++drains;
+    }
+    if (KIND != H2_K_EXP && ovf) atomicOr(ovf_flag, 1u);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  cluster_sync_all();   // no CTA leaves while its peer may still arrive or MMA into it
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 }  // namespace
 
 // exp: a point set whose scaled diameter keeps n = rint(-256 r'/ln2) in the range of the exponent
@@ -475,6 +760,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 bool sketch_tc_supported(const KernelParams& kp) {
   if (kp.kind == H2_K_EXP) return kp.rmax > 0 && kp.rmax <= 650.0;
   return kp.kind == H2_K_HELMHOLTZ && kp.rmax > 0 && kp.rmax <= 650.0 && kp.rmin > 0;
+}
+
+// CTA-pair (cta_group::2) 128-column pass, opt-in (H2_TC_PAIR=1): bitwise identical, but 200 vs
+// 178 ms per 128 columns at N = 2^18 (the full-rate M = 128 dispatch does not pay: the pass is
+// not bound by the tensor-core rate, and the pair couples two CTAs' producers per chunk)
+bool sketch_tc_pair() {
+  return env_int("H2_TC_PAIR", 0) != 0;
 }
 
 int sketch_tc_pass_cols() {
@@ -496,6 +788,33 @@ void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t 
   }
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
                                                                                 ld, sstride, hs, wshift, ovf);
+}
+
+template <int KIND>
+void tc_launch_pair(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1,
+                    const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs,
+                    int wshift, uint32_t* ovf) {
+  constexpr int NPW = 16;
+  static bool attr = false;
+  constexpr int smem = PairPlan::TOTAL;
+  if (!attr) {
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_pair_kernel<KIND, NPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(32 * (NPW + 1));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  H2_CUDA(cudaLaunchKernelEx(&cfg, sketch_tc_pair_kernel<KIND, NPW>, C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+                             sstride, hs, wshift, ovf));
 }
 
 template <int KIND>
@@ -569,15 +888,29 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
       part_elems = rows * nc * S;
       part = static_cast<double*>(cache_alloc(sizeof(double) * part_elems, st));
     }
-    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
-        Om + c0, ldo, n, nc, NCOL, JC, nchunks, Bq);
-    H2_CHECK_LAUNCH();
+    const bool pair = NCOL == 128 && sketch_tc_pair();
     double* yo = S > 1 ? part : Yout + c0;
     const int64_t ld = S > 1 ? nc : ldy;
     const int64_t ss = S > 1 ? rows * nc : 0;
-    const dim3 grid(tiles, S);
-    if (helm) tc_dispatch<H2_K_HELMHOLTZ>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-    else tc_dispatch<H2_K_EXP>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+    if (pair) {
+      // B split by columns: halves [0, 64) and [64, nc) packed as two 64-column operands
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const int nch = std::max(0, std::min(64, nc - 64 * hlf));
+        omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * 64 + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+            Om + c0 + 64 * hlf, ldo, n, nch, 64, JC, nchunks, Bq + (int64_t)hlf * nchunks * JC * 64);
+        H2_CHECK_LAUNCH();
+      }
+      const dim3 grid((unsigned)(2 * div_up(tiles, 2)), S);   // CTA pairs along x
+      if (helm) tc_launch_pair<H2_K_HELMHOLTZ>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      else tc_launch_pair<H2_K_EXP>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+    } else {
+      omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+          Om + c0, ldo, n, nc, NCOL, JC, nchunks, Bq);
+      H2_CHECK_LAUNCH();
+      const dim3 grid(tiles, S);
+      if (helm) tc_dispatch<H2_K_HELMHOLTZ>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      else tc_dispatch<H2_K_EXP>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+    }
     H2_CHECK_LAUNCH();
     if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
   }

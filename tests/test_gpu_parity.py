@@ -202,6 +202,27 @@ def test_tc_pass_width_bitwise(monkeypatch):
     assert torch.equal(y0, y1)
 
 
+@pytest.mark.parametrize("n,nc,kind", [(20001, 128, "exp"), (9000, 100, "exp"), (4100, 70, "exp"),
+                                       (8000, 128, "helmholtz")])
+def test_tc_pair_kernel_bitwise(monkeypatch, n, nc, kind):
+    """The CTA-pair (cta_group::2, M = 128 over two SMs, B split by columns) 128-column pass
+    gives the same bits as the single-CTA pass: ragged row tiles (odd tile counts pad the last
+    pair), a partial second column half, and the j-split."""
+    X = uniform_points(n, 3, 1) if kind == "exp" else grid_points((20, 20, 20), 1.0 / 20)
+    kern = ("exp", 0.2) if kind == "exp" else ("helmholtz", 3.0)
+    T = g.Tree(X, 64)
+    Od = torch.from_numpy(rng.omega_block(1, 0, 0, T.n, 0, nc)).cuda()
+    monkeypatch.setenv("H2_TC_PAIR", "0")
+    y0 = g.dense_sketch(T, Od, kern, omega_quarters=True)
+    monkeypatch.setenv("H2_TC_PAIR", "1")
+    y1 = g.dense_sketch(T, Od, kern, omega_quarters=True)
+    assert torch.equal(y0, y1)
+    Kd = kernels.KernelOperator(*kern, X[T.perm]).dense() if n <= 9000 else None
+    if Kd is not None:
+        ref = Kd @ Od.cpu().numpy()
+        assert np.abs(y1.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
 def test_speculative_sketch_columns_bitwise(monkeypatch):
     """Speculative 128-column tensor-core passes change how many Omega columns are
     pushed through the sketch, never the samples consumed: the build is bit-identical to one
