@@ -130,7 +130,7 @@ def run_reference(args, w, rank):
     if rank != 0:
         return
     X = w["points"]()
-    samples_hint = 224   # GPU samples at configs[1] (profiles/r1_bench_*.json); scales the oracle sample
+    samples_hint = 160   # GPU samples at configs[1] (profiles/r1_bench_*.json); scales the oracle sample
     cores = len(os.sched_getaffinity(0))
     for _ in range(args.warmup):
         oracle_sample_seconds(w, X, samples_hint, budget_rows=8, leaves=2)
