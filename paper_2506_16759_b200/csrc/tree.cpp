@@ -247,6 +247,9 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
   // the pairs of a depth are split into contiguous ranges over threads; the per-thread lists are
   // concatenated in range order, so the result is identical to the serial traversal
   const int nthr = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  // the CSR of a depth's far pairs is built on its own thread while the traversal descends
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> far_lists(Dl + 1);
+  std::vector<std::thread> csr_threads;
   for (int t = 0; t <= Dl; ++t) {
     const int64_t np = (int64_t)cur.size();
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthr, np / 4096));
@@ -274,7 +277,7 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
       for (int q = 0; q < nt; ++q) th.emplace_back(work, q);
       for (auto& x : th) x.join();
     }
-    std::vector<std::pair<int32_t, int32_t>> far;
+    std::vector<std::pair<int32_t, int32_t>>& far = far_lists[t];
     nxt.clear();
     for (int q = 0; q < nt; ++q) {
       far.insert(far.end(), far_t[q].begin(), far_t[q].end());
@@ -282,11 +285,12 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
       near.insert(near.end(), near_t[q].begin(), near_t[q].end());
     }
     if (!far.empty() && T.top < 0) T.top = t;
-    make_csr(T.far[t], far, 1 << t, true);
+    csr_threads.emplace_back([&T, &far, t] { make_csr(T.far[t], far, 1 << t, true); });
     cur.swap(nxt);
   }
   lap("traversal");
   make_csr(T.near, near, 1 << Dl, false);
+  for (auto& x : csr_threads) x.join();
   for (int t = 0; t <= Dl; ++t)
     for (int64_t r = 0; r < (int64_t(1) << t); ++r) {
       int row = T.far[t].ptr[r + 1] - T.far[t].ptr[r];

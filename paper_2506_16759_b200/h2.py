@@ -65,20 +65,35 @@ class Tree:
         self.perm = np.empty(self.n, np.int64)
         b = np.empty(nnodes, np.int64)
         e = np.empty(nnodes, np.int64)
-        near = np.empty((self.near_nnz, 2), np.int32)
         check(lib.h2_tree_export(h, self.perm.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
-                                 e.ctypes.data_as(C.c_void_p), near.ctypes.data_as(C.c_void_p)))
+                                 e.ctypes.data_as(C.c_void_p), None))
         self.begin = [b[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
         self.end = [e[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
-        self.near = near.astype(np.int64)
-        self.far = []
-        for t in range(self.leaf_depth + 1):
-            cnt = C.c_int64()
-            check(lib.h2_tree_far_count(h, t, C.byref(cnt)))
-            f = np.empty((cnt.value, 2), np.int32)
-            if cnt.value:
-                check(lib.h2_tree_export_far(h, t, f.ctypes.data_as(C.c_void_p)))
-            self.far.append(f.astype(np.int64))
+        self._near = self._far = None
+
+    @property
+    def near(self):
+        """Ordered near pairs (s, b) of the leaf depth (exported on first use)."""
+        if self._near is None:
+            near = np.empty((self.near_nnz, 2), np.int32)
+            check(lib.h2_tree_export(self._h, None, None, None, near.ctypes.data_as(C.c_void_p)))
+            self._near = near.astype(np.int64)
+        return self._near
+
+    @property
+    def far(self):
+        """Per depth: ordered admissible pairs (s, b) (exported on first use)."""
+        if self._far is None:
+            far = []
+            for t in range(self.leaf_depth + 1):
+                cnt = C.c_int64()
+                check(lib.h2_tree_far_count(self._h, t, C.byref(cnt)))
+                f = np.empty((cnt.value, 2), np.int32)
+                if cnt.value:
+                    check(lib.h2_tree_export_far(self._h, t, f.ctypes.data_as(C.c_void_p)))
+                far.append(f.astype(np.int64))
+            self._far = far
+        return self._far
 
     @property
     def handle(self):
