@@ -377,13 +377,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
       const int jj0 = 16 * g + 8 * h;
       uint32_t lo[RPT][8], hi[RPT][8];
-#ifdef H2_EXP_HALF
-      constexpr int QE = 4;   // experiment: evaluate half the j of a chunk (the rest copied)
-#else
-      constexpr int QE = 8;
-#endif
 #pragma unroll
-      for (int q = 0; q < QE; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int jj = jj0 + q;
         const double4 p = *reinterpret_cast<const double4*>(cb + jj * 32 + (jj >> 3) * 16);
 #pragma unroll
@@ -394,13 +389,6 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
           hi[k][q] = m.y;
         }
       }
-#pragma unroll
-      for (int q = QE; q < 8; ++q)
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          lo[k][q] = lo[k][q - QE] ^ (uint32_t)q;
-          hi[k][q] = hi[k][q - QE];
-        }
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         uint32_t w[4][4];
