@@ -197,3 +197,16 @@ def test_nonsym_column_exports_refused_on_symmetric():
     H = g.build(T, ("exp", 0.2), 1e-6)
     with pytest.raises(g.H2Error):
         H.rank(T.leaf_depth, 1)
+
+
+def test_nonsym_degenerate_inputs():
+    """n below one leaf (no admissible pair: D only) and a two-leaf problem: the non-symmetric
+    build reproduces the operator exactly (every block is dense)."""
+    for n, leaf in ((40, 64), (100, 64)):
+        X = uniform_points(n, 3, 3)
+        T = g.Tree(X, leaf)
+        A = np.random.default_rng(n).standard_normal((n, n))
+        Hg = g.build(T, ("exp", 0.2), 1e-6, dense=torch.from_numpy(A).cuda(), nonsym=True)
+        P = np.random.default_rng(1).standard_normal((n, 3))
+        y = Hg.matvec(torch.from_numpy(P).cuda()).cpu().numpy()
+        assert np.allclose(y, A @ P, rtol=0, atol=1e-12 * np.abs(A @ P).max())
