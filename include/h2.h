@@ -132,6 +132,10 @@ typedef struct {
    * one FP64 GEMM per draw (cuBLAS, the plain library GEMM). */
   const double* A;
   int64_t ld_A;
+  /* H2_S_H2_LOWRANK with a second factor (h2_build_nonsym only): M = A_H + U V^T, V dev n x rank
+   * (leading dim ld_V); NULL = V is U (the symmetric update) */
+  const double* V;
+  int64_t ld_V;
 } h2_sketch;
 
 /* Batched entry evaluator ("batched entry generator ... evaluate all D or B at a
@@ -164,6 +168,8 @@ typedef struct {
   int32_t rank;
   const double* A;    /* H2_E_DENSE_MATRIX: entries A[i * ld_A + j] (tree-order, dev)           */
   int64_t ld_A;
+  const double* V;    /* H2_E_H2_LOWRANK: entries of A_H + U V^T (h2_build_nonsym); NULL = U    */
+  int64_t ld_V;
 } h2_entry;
 
 /* ---------------------------------------------------------------------------------------

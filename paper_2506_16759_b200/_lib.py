@@ -45,7 +45,7 @@ SKETCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(h2_sketch_req))
 class h2_sketch(C.Structure):
     _fields_ = [("kind", C.c_int32), ("kern", h2_kernel), ("fn", SKETCH_FN), ("ctx", C.c_void_p),
                 ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32),
-                ("A", C.c_void_p), ("ld_A", C.c_int64)]
+                ("A", C.c_void_p), ("ld_A", C.c_int64), ("V", C.c_void_p), ("ld_V", C.c_int64)]
 
 
 class h2_block_batch(C.Structure):
@@ -60,7 +60,7 @@ ENTRY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(h2_block_batch))
 class h2_entry(C.Structure):
     _fields_ = [("kind", C.c_int32), ("kern", h2_kernel), ("fn", ENTRY_FN), ("ctx", C.c_void_p),
                 ("base", C.c_void_p), ("U", C.c_void_p), ("ld_U", C.c_int64), ("rank", C.c_int32),
-                ("A", C.c_void_p), ("ld_A", C.c_int64)]
+                ("A", C.c_void_p), ("ld_A", C.c_int64), ("V", C.c_void_p), ("ld_V", C.c_int64)]
 
 
 class h2_build_opts(C.Structure):

@@ -743,13 +743,11 @@ struct Builder {
   DArr<const int32_t*> base_k;
   DArr<const int64_t*> base_xoff;
   DArr<const double*> base_X;
-  void update_B(int t) {
-    Level& L = H.L(t);
+  // R_s = A's expanded basis rows at the skeletons of level Ln (depth t), kn_s x kb_s per cluster
+  void expand_base_rows(int t, const Level& Ln, DArr<double>& R, std::vector<int64_t>& rowoff,
+                        DArr<int64_t>& d_rowoff) {
     const h2_matrix& A = *E.base;
     const Level& La = A.L(t);
-    const PairCSR& F = T.far[t];
-    if (F.nuniq() == 0) return;
-    timer.begin(H2_PH_GEN);
     if (!base_k.p) {   // per-depth device pointers of A's levels
       std::vector<const int32_t*> kk(T.Dl + 1, nullptr);
       std::vector<const int64_t*> xo(T.Dl + 1, nullptr);
@@ -763,27 +761,24 @@ struct Builder {
       base_xoff.upload(xo, st);
       base_X.upload(xx, st);
     }
-    // R_s = A's expanded basis rows at the new skeletons of depth t (kn_s x kb_s)
-    std::vector<int64_t> rowoff(L.nclus + 1, 0);
-    std::vector<int32_t> ptc(std::max<int64_t>(L.rtot, 1), 0);
+    rowoff.assign(Ln.nclus + 1, 0);
+    std::vector<int32_t> ptc(std::max<int64_t>(Ln.rtot, 1), 0);
     int kmax = 1;
-    for (int c = 0; c < L.nclus; ++c) {
-      rowoff[c + 1] = rowoff[c] + (int64_t)L.k[c] * La.k[c];
-      for (int i = 0; i < L.k[c]; ++i) ptc[L.roff[c] + i] = c;
+    for (int c = 0; c < Ln.nclus; ++c) {
+      rowoff[c + 1] = rowoff[c] + (int64_t)Ln.k[c] * La.k[c];
+      for (int i = 0; i < Ln.k[c]; ++i) ptc[Ln.roff[c] + i] = c;
     }
     for (int u = t; u <= T.Dl; ++u)
       for (int32_t kv : A.L(u).k) kmax = std::max(kmax, kv);
-    DArr<int64_t> d_rowoff;
     DArr<int32_t> d_ptc;
-    DArr<double> R;
     d_rowoff.upload(rowoff, st);
     d_ptc.upload(ptc, st);
     R.alloc(std::max<int64_t>(rowoff.back(), 1), st);
     ExpandArgs ea{};
-    ea.npoints = L.rtot;
+    ea.npoints = Ln.rtot;
     ea.pt_cluster = d_ptc.p;
-    ea.roff_new = L.d_roff.p;
-    ea.skel_new = L.d_skel.p;
+    ea.roff_new = Ln.d_roff.p;
+    ea.skel_new = Ln.d_skel.p;
     ea.nleaf = 1 << T.Dl;
     ea.leaf_begin = T.d_leaf_begin;
     ea.Dl = T.Dl;
@@ -795,6 +790,19 @@ struct Builder {
     ea.R = R.p;
     ea.rowoff = d_rowoff.p;
     launch_expand_rows(ea, st);
+  }
+
+  void update_B(int t) {
+    Level& L = H.L(t);
+    const h2_matrix& A = *E.base;
+    const Level& La = A.L(t);
+    const PairCSR& F = T.far[t];
+    if (F.nuniq() == 0) return;
+    timer.begin(H2_PH_GEN);
+    std::vector<int64_t> rowoff;
+    DArr<int64_t> d_rowoff;
+    DArr<double> R;
+    expand_base_rows(t, L, R, rowoff, d_rowoff);
     int64_t gmax = 1;
     for (int64_t u = 0; u < F.nuniq(); ++u)
       gmax = std::max<int64_t>(gmax, (int64_t)La.k[F.us[u]] * L.k[F.ub[u]]);
@@ -905,6 +913,17 @@ struct Builder {
         entries_sketch += T.n * T.n * (int64_t)div_up(nc, 64);
       } else if (S.kind == H2_S_DENSE_MATRIX) {
         dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, in, ldi, nc, out, ldo, st, tr == 1);
+      } else if (S.kind == H2_S_H2_LOWRANK) {
+        // M = A_H + U V^T (A_H symmetric): Y = A_H Omega + U (V^T Omega), Z = A_H Psi + V (U^T Psi)
+        matvec_impl(*S.base, in, ldi, out, ldo, nc, 1.0, 0.0, st);
+        if (S.rank > 0) {
+          const double* V = S.V ? S.V : S.U;
+          const int64_t ldv = S.V ? S.ld_V : S.ld_U;
+          DArr<double> scr;
+          scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
+          if (tr == 0) launch_lowrank_sketch(S.U, S.ld_U, S.rank, in, ldi, nc, T.n, out, ldo, scr.p, st, V, ldv);
+          else launch_lowrank_sketch(V, ldv, S.rank, in, ldi, nc, T.n, out, ldo, scr.p, st, S.U, S.ld_U);
+        }
       } else {
         h2_sketch_req rq{};
         rq.n = T.n;
@@ -991,6 +1010,29 @@ struct Builder {
     g.idx = T.d_iota;
     g.out_off = H.d_D_off.p;
     g.out = H.D.p;
+    if (E.kind == H2_E_H2_LOWRANK) {   // D_A (unique, transposed for s > b) + U(I_s) V(I_b)^T
+      timer.begin(H2_PH_GEN);
+      UpdateNsArgs a{};
+      a.nblocks = F.nnz();
+      a.os = near_o.d_os.p;
+      a.ob = T.d_near.idx;
+      a.uidx = T.d_near.uidx;
+      a.us = T.d_near.us;
+      a.Bbase = E.base->D.p;
+      a.Boff = T.d_D_off;
+      a.out = H.D.p;
+      a.out_off = H.d_D_off.p;
+      a.cnt = T.d_leaf_size;
+      a.begin = T.d_leaf_begin;
+      a.U = E.U;
+      a.ldu = E.ld_U;
+      a.V = E.V ? E.V : E.U;
+      a.ldv = E.V ? E.ld_V : E.ld_U;
+      a.r = E.rank;
+      launch_update_ns(a, false, (int)std::min<int64_t>(F.nnz(), 148 * 8), st);
+      timer.end();
+      return;
+    }
     gen(g);
   }
 
@@ -1015,6 +1057,53 @@ struct Builder {
     g.idx2 = C.d_skel.p;
     g.out_off = L.d_B_off.p;
     g.out = L.B.p;
+    if (E.kind == H2_E_H2_LOWRANK) {
+      if (F.nnz() == 0) return;
+      timer.begin(H2_PH_GEN);
+      const Level& La = E.base->L(t);
+      std::vector<int64_t> ro_r, ro_c;
+      DArr<int64_t> d_ro_r, d_ro_c;
+      DArr<double> Rr, Rc;
+      expand_base_rows(t, L, Rr, ro_r, d_ro_r);   // base rows at the row skeletons I~
+      expand_base_rows(t, C, Rc, ro_c, d_ro_c);   // and at the column skeletons J~
+      int64_t gmax = 1;
+      for (int64_t e = 0; e < F.nnz(); ++e)
+        gmax = std::max<int64_t>(gmax, (int64_t)La.k[far_o[t].os[e]] * C.k[F.idx[e]]);
+      const int grid = (int)std::min<int64_t>(F.nnz(), 148 * 4);
+      DArr<double> scratch;
+      scratch.alloc(gmax * grid, st);
+      UpdateNsArgs a{};
+      a.nblocks = F.nnz();
+      a.os = far_o[t].d_os.p;
+      a.ob = T.d_far[t].idx;
+      a.uidx = T.d_far[t].uidx;
+      a.us = T.d_far[t].us;
+      a.Bbase = La.B.p;
+      a.Boff = La.d_B_off.p;
+      a.out = L.B.p;
+      a.out_off = L.d_B_off.p;
+      a.cnt = L.d_k.p;
+      a.cnt2 = C.d_k.p;
+      a.kb = La.d_k.p;
+      a.U = E.U;
+      a.ldu = E.ld_U;
+      a.V = E.V ? E.V : E.U;
+      a.ldv = E.V ? E.ld_V : E.ld_U;
+      a.r = E.rank;
+      a.R = Rr.p;
+      a.R2 = Rc.p;
+      a.rowoff = d_ro_r.p;
+      a.rowoff2 = d_ro_c.p;
+      a.skel = L.d_skel.p;
+      a.skel2 = C.d_skel.p;
+      a.roff = L.d_roff.p;
+      a.roff2 = C.d_roff.p;
+      a.scratch = scratch.p;
+      a.gmax = gmax;
+      launch_update_ns(a, true, grid, st);
+      timer.end();
+      return;
+    }
     gen(g);
   }
 
@@ -1695,9 +1784,10 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
       if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
-    if (nonsym)
-      H2_REQUIRE(sketch->kind != H2_S_H2_LOWRANK && entry->kind != H2_E_H2_LOWRANK,
-                 "h2_build_nonsym: H2 + low-rank operators are symmetric-only");
+    // U V^T (V != U) is a non-symmetric operator
+    H2_REQUIRE(nonsym || ((sketch->kind != H2_S_H2_LOWRANK || !sketch->V || sketch->V == sketch->U) &&
+                          (entry->kind != H2_E_H2_LOWRANK || !entry->V || entry->V == entry->U)),
+               "h2_build: an H2 + U V^T operator with V != U needs h2_build_nonsym");
     for (const h2_matrix* b : {sketch->kind == H2_S_H2_LOWRANK ? sketch->base : nullptr,
                                entry->kind == H2_E_H2_LOWRANK ? entry->base : nullptr})
       H2_REQUIRE(!b || (!b->nonsym && !b->partial), "h2_build: the H2+low-rank base must be a complete symmetric H2");

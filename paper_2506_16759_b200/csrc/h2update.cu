@@ -103,11 +103,15 @@ __global__ void lowrank_apply_kernel(const double* __restrict__ U, int64_t ldu, 
 }
 
 void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om, int64_t ldo, int nc, int64_t n,
-                           double* Y, int64_t ldy, double* scratch, cudaStream_t st) {
+                           double* Y, int64_t ldy, double* scratch, cudaStream_t st, const double* V, int64_t ldv) {
   if (r <= 0 || nc <= 0 || n <= 0) return;
+  if (!V) {
+    V = U;
+    ldv = ldu;
+  }
   const int np = div_up(n, 1024);
   double* W = scratch + (int64_t)np * r * nc;
-  lowrank_w_partial_kernel<<<np, 256, 0, st>>>(U, ldu, r, Om, ldo, nc, n, scratch);
+  lowrank_w_partial_kernel<<<np, 256, 0, st>>>(V, ldv, r, Om, ldo, nc, n, scratch);   // W = V^T Om
   H2_CHECK_LAUNCH();
   lowrank_w_final_kernel<<<div_up(r * nc, 256), 256, 0, st>>>(scratch, np, r * nc, W);
   H2_CHECK_LAUNCH();
@@ -213,6 +217,57 @@ __global__ void __launch_bounds__(256) update_B_kernel(UpdateBArgs a) {
              knb, 1.0);
     __syncthreads();
   }
+}
+
+// non-symmetric update M = A_H + U V^T, ordered pairs (h2_build_nonsym):
+//   D_{s,b} = D_A(s,b) + U(I_s) V(I_b)^T, D_A(s,b) read from A's unique storage (transposed if s > b)
+__global__ void __launch_bounds__(256) update_D_ns_kernel(UpdateNsArgs a) {
+  for (int64_t e = blockIdx.x; e < a.nblocks; e += gridDim.x) {
+    const int s = a.os[e], b = a.ob[e];
+    const int ms = a.cnt[s], mb = a.cnt[b];
+    const int64_t u = a.uidx[e];
+    const bool tr = a.us[u] != s;
+    const double* src = a.Bbase + a.Boff[u];
+    double* out = a.out + a.out_off[e];
+    for (int q = threadIdx.x; q < ms * mb; q += blockDim.x) {
+      const int i = q / mb, j = q - (q / mb) * mb;
+      out[q] = tr ? src[(int64_t)j * ms + i] : src[q];
+    }
+    __syncthreads();
+    cta_gemm(ms, mb, a.r, a.U + a.begin[s] * a.ldu, a.ldu, false, nullptr, a.V + a.begin[b] * a.ldv, a.ldv, true,
+             nullptr, out, mb, 1.0);
+    __syncthreads();
+  }
+}
+
+//   B_{s,b} = Rr_s B_A(s,b) Rc_b^T + U(I~_s) V(J~_b)^T: Rr_s / Rc_b = A's expanded basis rows at the
+//   new row / column skeletons (launch_expand_rows), B_A(s,b) transposed from storage if s > b
+__global__ void __launch_bounds__(256) update_B_ns_kernel(UpdateNsArgs a) {
+  double* G = a.scratch + (int64_t)blockIdx.x * a.gmax;
+  for (int64_t e = blockIdx.x; e < a.nblocks; e += gridDim.x) {
+    const int s = a.os[e], b = a.ob[e];
+    const int kns = a.cnt[s], knb = a.cnt2[b], kbs = a.kb[s], kbb = a.kb[b];
+    const int64_t u = a.uidx[e];
+    const bool tr = a.us[u] != s;
+    double* out = a.out + a.out_off[e];
+    const double* Rs = a.R + a.rowoff[s];
+    const double* Rb = a.R2 + a.rowoff2[b];
+    // G = B_A(s,b) Rc_b^T (kbs x knb); stored block is kbs x kbb, or kbb x kbs when transposed
+    cta_gemm(kbs, knb, kbb, a.Bbase + a.Boff[u], tr ? kbs : kbb, tr, nullptr, Rb, kbb, true, nullptr, G, knb, 0.0);
+    __syncthreads();
+    cta_gemm(kns, knb, kbs, Rs, kbs, false, nullptr, G, knb, false, nullptr, out, knb, 0.0);
+    __syncthreads();
+    cta_gemm(kns, knb, a.r, a.U, a.ldu, false, a.skel + a.roff[s], a.V, a.ldv, true, a.skel2 + a.roff2[b], out, knb,
+             1.0);
+    __syncthreads();
+  }
+}
+
+void launch_update_ns(const UpdateNsArgs& a, bool coupling, int grid, cudaStream_t st) {
+  if (a.nblocks <= 0) return;
+  if (coupling) update_B_ns_kernel<<<grid, 256, 0, st>>>(a);
+  else update_D_ns_kernel<<<grid, 256, 0, st>>>(a);
+  H2_CHECK_LAUNCH();
 }
 
 void launch_update_B(const UpdateBArgs& a, int grid, cudaStream_t st) {

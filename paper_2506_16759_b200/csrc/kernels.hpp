@@ -210,8 +210,10 @@ void launch_spmm(const SpmmArgs& a, cudaStream_t st);
 
 // ---- H^2 + low-rank update operators (h2update.cu, BASELINE configs[4])
 // Y += U (U^T Omega): scratch >= (ceil(n/1024) + 1) * r * nc doubles
+// Y += U (V^T Omega) (V NULL: V = U)
 void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om, int64_t ldo, int nc, int64_t n,
-                           double* Y, int64_t ldy, double* scratch, cudaStream_t st);
+                           double* Y, int64_t ldy, double* scratch, cudaStream_t st, const double* V = nullptr,
+                           int64_t ldv = 0);
 struct UpdateDArgs {            // D_new = D_A + U(I_s) U(I_b)^T over unique near pairs
   int64_t nblocks;
   const int32_t *us, *ub, *cnt;
@@ -257,6 +259,31 @@ struct UpdateBArgs {            // B_new = R_s B_A R_b^T + U(I~_s) U(I~_b)^T ove
   int64_t gmax;                 // scratch doubles per CTA (>= max kb_s * kn_b)
 };
 void launch_update_B(const UpdateBArgs& a, int grid, cudaStream_t st);
+// non-symmetric update M = A_H + U V^T over ORDERED pairs e (h2_build_nonsym): D (coupling = false:
+// cnt = leaf sizes, begin = leaf begins) or B (coupling = true: row side cnt/roff/skel, column side
+// cnt2/roff2/skel2, R / R2 the base's expanded basis rows at the row / column skeletons)
+struct UpdateNsArgs {
+  int64_t nblocks;
+  const int32_t *os, *ob;       // row / column cluster of entry e
+  const int32_t* uidx;          // unique (base) pair of entry e
+  const int32_t* us;            // stored orientation of the base's unique pair: rows = us[u]
+  const double* Bbase;
+  const int64_t* Boff;
+  double* out;
+  const int64_t* out_off;       // per ordered entry
+  const int32_t *cnt, *cnt2, *kb;
+  const int64_t* begin;
+  const double *U, *V;
+  int64_t ldu, ldv;
+  int r;
+  const double *R, *R2;
+  const int64_t *rowoff, *rowoff2;
+  const int32_t *skel, *skel2;
+  const int64_t *roff, *roff2;
+  double* scratch;
+  int64_t gmax;
+};
+void launch_update_ns(const UpdateNsArgs& a, bool coupling, int grid, cudaStream_t st);
 void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStream_t st);
 
 }  // namespace h2

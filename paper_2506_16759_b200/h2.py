@@ -274,7 +274,8 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
     unless ``sketch`` is given).  sketch: optional callable sketch(omega, y, col0, row_begin,
     row_end) filling y (tree-order rows) for a black-box K_blk; entry: optional callable
-    entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  update=(H_base, U):
+    entry(row_idx, col_idx, blocks) (see include/h2.h h2_block_batch).  update=(H_base, U) or
+    (H_base, U, V) (M = A_H + U V^T, with nonsym=True):
     recompress M = H_base + U U^T (H_base built on this tree, U a (n, r) float64
     CUDA tensor in tree order) with the library's H^2-matvec + low-rank sketch and entry
     extraction.  h2_sketch=H_base: the O(N) black-box sketch Y = A_H Omega of an existing H^2 on
@@ -293,14 +294,21 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     keep = []
     sk = L.h2_sketch()
     sk.kern = kern
+    V = None
     if update is not None:
-        Hb, U = update
+        Hb, U = update[0], update[1]
+        V = update[2] if len(update) > 2 else None
         assert Hb.tree is tree, "update: the base H^2 must be built on the same Tree"
         U = U.contiguous()
         assert U.is_cuda and U.dtype == torch.float64 and U.shape[0] == tree.n
         keep += [Hb, U]
         sk.kind = L.H2_S_H2_LOWRANK
         sk.base, sk.U, sk.ld_U, sk.rank = Hb._h, U.data_ptr(), U.stride(0), U.shape[1]
+        if V is not None:   # M = A_H + U V^T (non-symmetric: nonsym=True)
+            V = V.contiguous()
+            assert V.is_cuda and V.dtype == torch.float64 and V.shape == U.shape
+            keep.append(V)
+            sk.V, sk.ld_V = V.data_ptr(), V.stride(0)
     elif dense is not None:
         assert dense.is_cuda and dense.dtype == torch.float64 and dense.shape == (tree.n, tree.n)
         assert dense.stride(1) == 1
@@ -343,6 +351,7 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     elif update is not None:
         en.kind = L.H2_E_H2_LOWRANK
         en.base, en.U, en.ld_U, en.rank = sk.base, sk.U, sk.ld_U, sk.rank
+        en.V, en.ld_V = sk.V, sk.ld_V
     elif entry is None:
         en.kind = L.H2_E_BUILTIN
     else:

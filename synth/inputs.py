@@ -54,6 +54,9 @@ WORKLOADS = {
     # BASELINE configs[4]: recompress H2(A) + U U^T, A = exp covariance H^2 (tol 1e-6), rank-64 update
     "h2update_1m": dict(points=lambda: uniform_points(1 << 20, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6,
                         update_rank=64, d_max=1024, p_os=32),
+    # configs[4] shape at N = 2^18 (the U V^T update of h2_build_nonsym stores every ordered block)
+    "h2update_256k": dict(points=lambda: uniform_points(1 << 18, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6,
+                          update_rank=64, d_max=1024, p_os=32),
     # small parity cases (ragged sizes, several tiles)
     "cov3d_5k": dict(points=lambda: uniform_points(5000, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     "ie3d_4k": dict(points=lambda: grid_points((16, 16, 16), 1.0 / 16), kernel="helmholtz", param=3.0,

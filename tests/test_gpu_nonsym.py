@@ -210,3 +210,42 @@ def test_nonsym_degenerate_inputs():
         P = np.random.default_rng(1).standard_normal((n, 3))
         y = Hg.matvec(torch.from_numpy(P).cuda()).cpu().numpy()
         assert np.allclose(y, A @ P, rtol=0, atol=1e-12 * np.abs(A @ P).max())
+
+
+def test_nonsym_h2_plus_uvt_update():
+    """BASELINE configs[4] with a genuinely non-symmetric update: M = A_H + U V^T (V != U),
+    recompressed by h2_build_nonsym from the H^2-matvec + low-rank sketch (Y = A_H Omega +
+    U V^T Omega, Z = A_H Psi + V U^T Psi) with entries extracted from A_H's blocks and bases.
+    Against the oracle's non-symmetric build of the dense M: ranks / skeletons of both sides
+    bit-exact or certified, D and B entries = M's entries, probe error <= 2 tol."""
+    X, T, tree, part = setup(2048, 3, 64, 21)
+    n = T.n
+    Hb = g.build(T, ("exp", 0.2), 1e-9)
+    rr = np.random.default_rng(7)
+    U = torch.from_numpy(rr.standard_normal((n, 6)) * 0.3).cuda()
+    V = torch.from_numpy(rr.standard_normal((n, 6)) * 0.3).cuda()
+    I = torch.eye(n, dtype=torch.float64, device="cuda")
+    KH = torch.cat([Hb.matvec(I[:, c:c + 64]) for c in range(0, n, 64)], dim=1)
+    M = (KH + U @ V.T).cpu().numpy()
+    tol = 1e-6
+    Hg = g.build(T, ("exp", 0.2), tol, update=(Hb, U, V), nonsym=True)
+    Ho = oracle_nonsym(tree, part, M, tol)
+    assert Hg.samples == Ho.samples
+    for side in (0, 1):
+        c, m = compare_side(Hg, Ho, side)
+        assert c <= max(2, m // 50)
+    Dl = tree.leaf_depth
+    D = Hg.D_blocks()
+    for (s, b) in list(D)[::7]:
+        ref = M[tree.begin[Dl][s]:tree.end[Dl][s], tree.begin[Dl][b]:tree.end[Dl][b]]
+        assert np.abs(D[(s, b)] - ref).max() <= 1e-12 * np.abs(M).max()
+    for t in range(Hg.top_depth, Dl + 1):
+        Bb = Hg.B_blocks(t)
+        sr, sc = Hg.skel(t, 0), Hg.skel(t, 1)
+        for (s, b) in list(Bb)[::5]:
+            assert np.abs(Bb[(s, b)] - M[np.ix_(sr[s], sc[b])]).max() <= 1e-10 * np.abs(M).max(), (t, s, b)
+    P = np.random.default_rng(8).standard_normal((n, 6))
+    y = Hg.matvec(torch.from_numpy(P).cuda()).cpu().numpy()
+    assert np.linalg.norm(y - M @ P) <= 2 * tol * np.linalg.norm(M @ P)
+    with pytest.raises(g.H2Error):   # U V^T is non-symmetric: the symmetric build refuses it
+        g.build(T, ("exp", 0.2), tol, update=(Hb, U, V))

@@ -20,7 +20,7 @@ from synth import WORKLOADS
 p = argparse.ArgumentParser()
 p.add_argument("workload")
 p.add_argument("--reps", type=int, default=1)
-p.add_argument("--s", type=float, default=0.1)
+p.add_argument("--s", type=float, default=None, help="tol_safety (default: the library's, R31)")
 p.add_argument("--s-update", type=float, default=None, help="tol_safety of the update build (configs[4]); default --s")
 p.add_argument("--d-blk", type=int, default=32)
 p.add_argument("--probes", type=int, default=16)
@@ -32,7 +32,8 @@ p.add_argument("--bootstrap", type=float, default=None,
 p.add_argument("--nonsym", type=float, default=None,
                help="S8(f) NEXT #3 (dense workloads): operator exp(-r/l)(1 + v (x_0 - y_0)) with this v, "
                     "built with h2_build_nonsym")
-p.add_argument("--eps-decay", type=float, default=1.0, help="R31 level schedule eps_t = eps * decay^(Dl-t)")
+p.add_argument("--uvt", action="store_true", help="configs[4] with M = A_H + U V^T (V != U, h2_build_nonsym)")
+p.add_argument("--eps-decay", type=float, default=None, help="R31 level schedule eps_t = eps * decay^(Dl-t) (default: the library's)")
 a = p.parse_args()
 w = dict(WORKLOADS[a.workload])
 X = w["points"]()
@@ -55,6 +56,9 @@ if "update_rank" in w:      # configs[4]: base H^2 of A (untimed setup, like PAP
     out["base_samples"] = Hbase.samples
     U = torch.from_numpy(lowrank_factor(n, w["update_rank"])).cuda()
     update = (Hbase, U)
+    if a.uvt:
+        update = (Hbase, U, torch.from_numpy(lowrank_factor(n, w["update_rank"], seed=4)).cuda())
+        out["update"] = "U V^T (nonsym)"
 h2sk = None
 dense = None
 if w.get("dense"):   # NEXT #4: materialise the operator in tree order (row blocks: no n x n temporaries)
@@ -80,7 +84,7 @@ for r in range(a.reps):
     e0.record()
     H = g.build(T, kern, w["tol"], d_init=a.d_blk, d_blk=a.d_blk, p_os=a.p_os if a.p_os is not None else w.get("p_os", 10),
                 tol_safety=a.s if (update is None or a.s_update is None) else a.s_update, update=update, h2_sketch=h2sk, dense=dense,
-                d_max=w.get("d_max", 512), nonsym=a.nonsym is not None, eps_decay=a.eps_decay)
+                d_max=w.get("d_max", 512), nonsym=a.nonsym is not None or a.uvt, eps_decay=a.eps_decay)
     e1.record()
     e1.synchronize()
     times.append(e0.elapsed_time(e1) / 1e3)
@@ -101,7 +105,7 @@ t0 = time.perf_counter()
 if dense is not None:
     KX = dense @ Xp
 elif update is not None:      # M X = A_H X + U (U^T X): the operator the update build compresses
-    KX = update[0].matvec(Xp) + update[1] @ (update[1].T @ Xp)
+    KX = update[0].matvec(Xp) + update[1] @ (update[-1].T @ Xp)
 else:
     KX = g.dense_sketch(T, Xp, kern)
 HX = H.matvec(Xp)
