@@ -276,7 +276,9 @@ def run_ours(args, w, rank, world, local_rank):
         "config": {"workload": args.workload, "n": n, "leaf": w["leaf"], "eta": 0.7, "tol": w["tol"],
                    "kernel": f"{w['kernel']}({w['param']})", "sketch": "dense-kernel (row shards)" if world > 1
                    else "dense-kernel", "d_init": 32, "d_blk": 32, "d_max": 512,
-                   "parallelism": f"subtree shards x{world} (sketch rows, clusters per level; NCCL all-gathers)"
+                   "parallelism": (f"subtree shards x{world} (sketch rows, clusters per level; "
+                                   f"{dist.get_backend().upper() if dist else ''} all-gathers"
+                                   f"{'' if dist and dist.get_backend() == 'nccl' else ', ranks share a GPU'})")
                    if world > 1 else "1 GPU",
                    "l2": "256 MiB flush before every timed step; working set (N x d_max x 16 B = 2 GiB) > L2"},
         "samples": st["samples"], "sketch_columns": st["sketch_columns"], "sketch_launches": sk_launches,
