@@ -219,18 +219,19 @@ def run_ours(args, w, rank, world, local_rank):
     KX = g.dense_sketch(T, Xp, kern)
     HX = H.matvec(Xp)
     verr = float(torch.linalg.norm(HX - KX) / torch.linalg.norm(KX))
-    # roofline of the dominant kernel (sketch_tc_kernel, one launch per 128-column pass): the
+    # roofline of the dominant kernel (sketch_tc_kernel, one launch per 160-column pass): the
     # contraction runs exactly on the int8 tensor cores, so the bound is the FP64 pipe evaluating
     # K: algorithmic work = N_rows * N entries x F_EVAL FP64 ops per launch
     sk_launches = st["entries_sketch"] // (n * n)
     ncol_launch = -(-st["sketch_columns"] // max(sk_launches, 1))
-    ncol_launch = min(128, -(-ncol_launch // 32) * 32)
+    slices = 7 if os.environ.get("H2_TC_SLICES") == "7" else 6   # libh2's fixed-point byte slices
+    ncol_launch = min(160 if slices == 6 else 128, -(-ncol_launch // 32) * 32)
     t_sk_ms = float(np.mean([s["t_phase_ms"]["sketch"] for s in stats]))
     per_launch_ms = t_sk_ms / max(sk_launches, 1)
     rows_local = n if world == 1 else (n // world)
     entries_launch = float(rows_local) * n
     achieved = entries_launch * F_EVAL / (per_launch_ms * 1e-3) / 1e12
-    int8_ops = entries_launch * ncol_launch * 7 * 2 / (per_launch_ms * 1e-3) / 1e12
+    int8_ops = entries_launch * ncol_launch * slices * 2 / (per_launch_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r1_sketch_tc_traffic.json")
     if os.path.exists(tpath) and args.workload == "cov3d_256k" and world == 1:
@@ -299,7 +300,7 @@ def run_ours(args, w, rank, world, local_rank):
                      "int8_tensor_tops": int8_ops, "int8_tensor_frac": int8_ops / INT8_DENSE_TOPS,
                      "per_launch_ms": per_launch_ms,
                      "note": f"achieved = N^2 entries x {F_EVAL} FP64 ops (SASS) per launch / CUDA-event time of the "
-                             "sketch phase per 128-column pass (speculative: columns beyond the converged d are computed, not used); peak = 148 SM x 64 FP64 lanes/clk x 1.965 GHz "
+                             "sketch phase per 160-column pass (speculative: columns beyond the converged d are computed, not used); peak = 148 SM x 64 FP64 lanes/clk x 1.965 GHz "
                              "(microbenchmarked DFMA 37.0 TF/s = 99.5 %); traffic = ncu dram bytes per launch"},
         "clocks": clk,
         "e2e": e2e,

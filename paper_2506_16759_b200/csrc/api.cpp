@@ -1249,7 +1249,7 @@ struct Builder {
     if (S.kind == H2_S_DENSE_KERNEL) {
       skp = tree_kernel(&T, S.kern, st);
       spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
-      spec_w = sketch_tc_pass_cols();
+      spec_w = sketch_tc_pass_cols(skp.kind);
     }
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
     d = std::min(o.d_init, o.d_max);

@@ -17,7 +17,8 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
                          int64_t ldy, bool omega_quarters, cudaStream_t st);
 // exp-kernel sketch on the int8 tensor cores (tcgen05 kind::i8, exact slices; sketch_tc.cu)
 bool sketch_tc_supported(const KernelParams& kp);
-int sketch_tc_pass_cols();   // Omega columns per tensor-core sketch pass (K evaluated once per pass)
+int sketch_tc_pass_cols(int kind);   // Omega columns per tensor-core sketch pass (K evaluated once per pass)
+int sketch_tc_slices(int kind);      // byte slices of the fixed-point K (6: 47-bit grid, 7: 52-bit)
 int env_int(const char* name, int def);
 bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,

@@ -25,7 +25,15 @@ namespace h2 {
 namespace {
 
 
-constexpr int TC_NS = 7;                       // byte slices of the 52-bit fixed-point K
+// Byte slices NS of the fixed-point K: 7 (52-bit grid, K 2^52 / v 2^51) or 6 (47-bit grid, K 2^47 /
+// v 2^46: its rounding, <= 2^-48 max|K| per entry, stays below the accumulated rounding of an FP64
+// GEMM of the same sums, and 6 slices leave TMEM room for 160-column passes).  The low-half /
+// high-half split of the slices (summation chains and TMEM lane halves) is NSPLIT.
+template <int NS> struct SliceFmt {
+  static constexpr int NSPLIT = NS == 7 ? 4 : 3;
+  static constexpr int KEXP = NS == 7 ? 52 : 47;   // exp: m = round(K 2^KEXP)
+  static constexpr int HEXP = NS == 7 ? 51 : 46;   // Helmholtz: m = round(v 2^HEXP), |v| < 1
+};
 constexpr int TC_NB = 4;                       // coordinate / B ring depth
 constexpr int TC_DRAIN_J = 65536;              // j per TMEM drain: 65536 * 255 * 32 < 2^31
 
@@ -33,10 +41,10 @@ constexpr int TC_DRAIN_J = 65536;              // j per TMEM drain: 65536 * 255 
 //   A: NA buffers of 7 byte slices (TM x JC each), B ring: NB x (NCOL x JC) int8,
 //   coordinate ring NB x CBUF, mbarriers (the 32 KB lane-replicated exp table is static shared
 //   memory: its address is an immediate of the table loads).
-template <int TM, int NCOL, int JC>
+template <int TM, int NCOL, int JC, int NS>
 struct TcPlan {
   static constexpr int SLICE = TM * JC;                    // bytes of one slice
-  static constexpr int ABUF = TC_NS * SLICE;               // 56 KB (TM x JC = 8192) / 28 KB (4096)
+  static constexpr int ABUF = NS * SLICE;                  // 56 / 48 KB (TM x JC = 8192), 28 / 24 KB (4096)
   static constexpr int NA = ABUF > 32768 ? (NCOL > 64 ? 2 : 3) : 4;   // A buffers
   static constexpr int BBUF = NCOL * JC;
   static constexpr int CBUF = JC * 32 + JC * 2;            // JC x (x, y, z, pad) doubles, +16 B per 8 j (bank skew)
@@ -68,10 +76,11 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
 //             16 q + l -> lane 32 q + l); a second one interleaves in lanes 16-31 at the same
 //             columns.  Slices 0-3 take the low half at columns s*NCOL, slices 4-6 the high
 //             half (lane offset 16) at columns (s-4)*NCOL: 7 x 128 columns in 4 x 128.
-template <int TM, int NCOL>
+template <int TM, int NCOL, int NS>
 __device__ __forceinline__ uint32_t tmem_slice(int s) {
+  constexpr int H = SliceFmt<NS>::NSPLIT;
   if constexpr (TM == 128) return (uint32_t)(s * NCOL);
-  else return (s < 4) ? (uint32_t)(s * NCOL) : ((16u << 16) | (uint32_t)((s - 4) * NCOL));
+  else return (s < H) ? (uint32_t)(s * NCOL) : ((16u << 16) | (uint32_t)((s - H) * NCOL));
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -145,6 +154,7 @@ __device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restric
 // polynomials on |x| <= pi/4 (to x^16 / x^17: truncation < 1e-16), quadrant by n & 3.
 // 1/r': the cubic-corrected rsqrt.  r' = 0 (the diagonal; r2 = the 2^-1000 floor) gives 0.
 // FP64 pipe: 6 (r'^2) + 5 (1/r') + 1 (r') + 4 (reduction) + 1 (x^2) + 8 (cos) + 9 (sin) + 2 + 1.
+template <int HEXP>
 __device__ __forceinline__ uint2 helm_fixed51(double r2, double hs, uint32_t& ovf) {
   double y0;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
@@ -181,9 +191,9 @@ __device__ __forceinline__ uint2 helm_fixed51(double r2, double hs, uint32_t& ov
                                      __double2loint(odd ? sn : c));
   double v = (hs * tr) * y;
   if (__double2hiint(r2) < 0x03B00000) v = 0.0;                    // r2 < 2^-900: x' = y'
-  const double w = fma(v, 2251799813685248.0, 6755399441055744.0);  // v 2^51 + 3 2^51
+  const double w = fma(v, (double)(1ull << HEXP), 6755399441055744.0);  // v 2^HEXP + 3 2^51
   const int mh = __double2hiint(w) - 0x43380000;
-  ovf |= (uint32_t)(mh + 0x80000) > 0x100000u;
+  ovf |= (uint32_t)(mh + (1 << (HEXP - 32))) > (2u << (HEXP - 32));
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
 }
 
@@ -231,12 +241,13 @@ __global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int6
 //     chunk.
 // TM = 128, NCOL <= 64 : 7 x NCOL TMEM columns.  TM = 64, NCOL = 128 : the M = 64 accumulators
 // pack two slices per TMEM column (tmem_slice), so one evaluation of K feeds 128 columns.
-template <int KIND, int TM, int NPW, int NCOL, int JC>
+template <int KIND, int TM, int NPW, int NCOL, int JC, int NS>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag) {
-  using P = TcPlan<TM, NCOL, JC>;
+  using P = TcPlan<TM, NCOL, JC, NS>;
+  constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
   constexpr int CBUF = P::CBUF;
   constexpr int NTH = 32 * (NPW + 1);
@@ -245,12 +256,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   constexpr int BBUF = P::BBUF;            // B chunk bytes
   constexpr int LBO_A = TM * 16;           // K-direction core-matrix stride of A
   constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
-  constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL == 32) ? 256 : 512;
+  constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL * NS <= 256) ? 256 : 512;
   constexpr uint32_t IDESC = idesc_i8<TM, NCOL>();
   // Helmholtz: the top slice holds the sign (two's complement of the signed fixed point): s8
   constexpr uint32_t IDESC6 = KIND == H2_K_EXP ? IDESC : (IDESC | (1u << 7));
   static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
-  static_assert((TM == 128 && NCOL <= 64) || (TM == 64 && NCOL == 128), "TMEM plan");
+  static_assert((TM == 128 && NCOL * NS <= 512) || (TM == 64 && NCOL * (NS - NSPLIT > NSPLIT ? NS - NSPLIT : NSPLIT) <= 512),
+                "TMEM plan");
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(128) double tab[16 * 256];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const int nch = (int)(ch_e - ch_b);
   const bool control = (warp == NPW);
 
-  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + 52.0);
+  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, NPW);
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
         const uint32_t b0 = sbase + P::B0 + slot * BBUF;
 #pragma unroll
-        for (int s = 0; s < TC_NS; ++s)
+        for (int s = 0; s < NS; ++s)
 #pragma unroll
           for (int kk = 0; kk < JC / 32; ++kk) {
             const uint64_t ad = umma_desc(a0 + s * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
@@ -334,8 +346,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + tmem_slice<TM, NCOL>(s)),
-                "l"(ad), "l"(bd), "r"(s == TC_NS - 1 ? IDESC6 : IDESC), "r"(acc));
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + tmem_slice<TM, NCOL, NS>(s)),
+                "l"(ad), "l"(bd), "r"(s == NS - 1 ? IDESC6 : IDESC), "r"(acc));
           }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             bar_empty + 8 * buf));
@@ -384,7 +396,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
-          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51(r2, hs, ovf);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51<SliceFmt<NS>::HEXP>(r2, hs, ovf);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         for (int s = 0; s < 4; ++s)
           *reinterpret_cast<uint2*>(Ab + s * P::SLICE + off[k]) = make_uint2(w[0][s], w[1][s]);
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
+        for (int s = 0; s < NS - 4; ++s)
           *reinterpret_cast<uint2*>(Ab + (s + 4) * P::SLICE + off[k]) = make_uint2(w[2][s], w[3][s]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
@@ -425,10 +437,10 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
           for (int c = 0; c < 16; ++c) v[c] = u[c] = 0.0;
 #pragma unroll
-          for (int s = 0; s < TC_NS; ++s) {
-            if (TM == 64 && s >= 4) break;
+          for (int s = 0; s < NS; ++s) {
+            if (TM == 64 && s >= NSPLIT) break;
             uint32_t r[16];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + tmem_slice<TM, NCOL>(s) + (uint32_t)c0;
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + tmem_slice<TM, NCOL, NS>(s) + (uint32_t)c0;
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                 "[%16];\n"
@@ -437,10 +449,10 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
                   "=r"(r[15])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-            // slice weight 2^(8 sl) * 2^-52 * (1/4); at TM = 64 the high lanes hold slice s + 4
-            const int sl = (TM == 128 || lane < 16) ? s : s + 4;
-            const double wgt = sl < TC_NS ? ldexp(1.0, 8 * sl + wshift) : 0.0;
-            if (TM == 128 && s >= 4) {
+            // slice weight 2^(8 sl) * 2^-KEXP * (1/4); at TM = 64 the high lanes hold slice s + NSPLIT
+            const int sl = (TM == 128 || lane < 16) ? s : s + NSPLIT;
+            const double wgt = sl < NS ? ldexp(1.0, 8 * sl + wshift) : 0.0;
+            if (TM == 128 && s >= NSPLIT) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
             } else {
@@ -481,9 +493,10 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 // multicast to the empty / drain barriers of both CTAs.
 // ------------------------------------------------------------------------------------------
 constexpr int PR_TM = 64, PR_NCOL = 128, PR_NH = 64, PR_JC = 128;
+template <int NS>
 struct PairPlan {
   static constexpr int SLICE = PR_TM * PR_JC;              // 8 KB
-  static constexpr int ABUF = TC_NS * SLICE;               // 56 KB
+  static constexpr int ABUF = NS * SLICE;                  // 56 / 48 KB
   static constexpr int NA = 2;
   static constexpr int BBUF = PR_NH * PR_JC;               // this CTA's half of B: 8 KB
   static constexpr int CBUF = PR_JC * 32 + PR_JC * 2;
@@ -507,12 +520,13 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::);
 }
 
-template <int KIND, int NPW>
+template <int KIND, int NPW, int NS>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_pair_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                           const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout,
                           int64_t ldy, int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag) {
-  using P = PairPlan;
+  using P = PairPlan<NS>;
+  constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int TM = PR_TM, JC = PR_JC;
   constexpr int G = JC / 16;
   constexpr int CBUF = P::CBUF;
@@ -544,7 +558,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const bool control = (warp == NPW);
   const int8_t* Bh = Bq + (int64_t)crank * nchunks * BBUF;   // this CTA's column half
 
-  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + 52.0);
+  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, leader ? 2 * NPW : NPW);   // leader: both CTAs' producers
@@ -602,7 +616,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
         const uint32_t b0 = sbase + P::B0 + slot * BBUF;
 #pragma unroll
-        for (int sl = 0; sl < TC_NS; ++sl)
+        for (int sl = 0; sl < NS; ++sl)
 #pragma unroll
           for (int kk = 0; kk < JC / 32; ++kk) {
             const uint64_t ad = umma_desc(a0 + sl * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
@@ -611,7 +625,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                 " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(sl * PR_NH)),
-                "l"(ad), "l"(bd), "r"(sl == TC_NS - 1 ? IDESC6 : IDESC), "r"(acc));
+                "l"(ad), "l"(bd), "r"(sl == NS - 1 ? IDESC6 : IDESC), "r"(acc));
           }
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
@@ -661,7 +675,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
-          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51(r2, hs, ovf);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51<SliceFmt<NS>::HEXP>(r2, hs, ovf);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
@@ -677,7 +691,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         for (int q = 0; q < 4; ++q)
           *reinterpret_cast<uint2*>(Ab + q * P::SLICE + off[k]) = make_uint2(w[0][q], w[1][q]);
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
+        for (int q = 0; q < NS - 4; ++q)
           *reinterpret_cast<uint2*>(Ab + (q + 4) * P::SLICE + off[k]) = make_uint2(w[2][q], w[3][q]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
@@ -703,7 +717,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c] = u[c] = 0.0;
 #pragma unroll
-          for (int sl = 0; sl < TC_NS; ++sl) {
+          for (int sl = 0; sl < NS; ++sl) {
             uint32_t r[8];
             const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(sl * PR_NH + c0);
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -712,7 +726,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
                          : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
             const double wgt = ldexp(1.0, 8 * sl + wshift);
-            if (sl >= 4) {
+            if (sl >= NSPLIT) {
 #pragma unroll
               for (int c = 0; c < 8; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
             } else {
@@ -757,36 +771,46 @@ bool sketch_tc_pair() {
   return env_int("H2_TC_PAIR", 0) != 0;
 }
 
-int sketch_tc_pass_cols() {
+// byte slices of the fixed-point K (SliceFmt): exp 6 (H2_TC_SLICES=7: 7); Helmholtz 7 (its scale
+// 2^E >= 4 max|K| leaves 2^-45 max|K| per entry at 6 slices, above the FP64-GEMM-level bound)
+int sketch_tc_slices(int kind) {
+  if (kind != H2_K_EXP) return 7;
+  return env_int("H2_TC_SLICES", 6) == 7 ? 7 : 6;
+}
+
+// widest pass: 160 columns with 6 slices (3 x 160 TMEM columns per lane half), 128 with 7;
+// H2_TC_WIDE=0: 64
+int sketch_tc_pass_cols(int kind) {
   const char* e = getenv("H2_TC_WIDE");
-  return (e && atoi(e) == 0) ? 64 : 128;
+  if (e && atoi(e) == 0) return 64;
+  return sketch_tc_slices(kind) == 6 ? 160 : 128;
 }
 
 namespace {
-template <int KIND, int TM, int NCOL, int JC>
+template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
   constexpr int NPW = 16;   // producer warps (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128)
   static bool attr = false;
-  constexpr int smem = TcPlan<TM, NCOL, JC>::TOTAL;
+  constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
   if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC>,
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  sketch_tc_kernel<KIND, TM, NPW, NCOL, JC><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
-                                                                                ld, sstride, hs, wshift, ovf);
+  sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
+                                                                                    yo, ld, sstride, hs, wshift, ovf);
 }
 
-template <int KIND>
+template <int KIND, int NS>
 void tc_launch_pair(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1,
                     const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs,
                     int wshift, uint32_t* ovf) {
   constexpr int NPW = 16;
   static bool attr = false;
-  constexpr int smem = PairPlan::TOTAL;
+  constexpr int smem = PairPlan<NS>::TOTAL;
   if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_pair_kernel<KIND, NPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    H2_CUDA(cudaFuncSetAttribute(sketch_tc_pair_kernel<KIND, NPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -801,17 +825,23 @@ void tc_launch_pair(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  H2_CUDA(cudaLaunchKernelEx(&cfg, sketch_tc_pair_kernel<KIND, NPW>, C, n, row0, row1, Bq, nchunks, nc, yo, ld,
+  H2_CUDA(cudaLaunchKernelEx(&cfg, sketch_tc_pair_kernel<KIND, NPW, NS>, C, n, row0, row1, Bq, nchunks, nc, yo, ld,
                              sstride, hs, wshift, ovf));
 }
 
-template <int KIND>
+template <int KIND, int NS>
 void tc_dispatch(int NCOL, dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1,
                  const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t ss, double hs, int wshift,
                  uint32_t* ovf) {
-  if (NCOL == 128) tc_launch<KIND, 64, 128, 128>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-  else if (NCOL == 64) tc_launch<KIND, 128, 64, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-  else tc_launch<KIND, 128, 32, 64>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  if constexpr (NS == 6) {
+    if (NCOL == 160) {
+      tc_launch<KIND, 64, 160, 128, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      return;
+    }
+  }
+  if (NCOL == 128) tc_launch<KIND, 64, 128, 128, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  else if (NCOL == 64) tc_launch<KIND, 128, 64, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  else tc_launch<KIND, 128, 32, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
 }
 
 // j-split S fills the last wave (1 CTA / SM)
@@ -842,7 +872,7 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int wmax = sketch_tc_pass_cols();
+  const int wmax = sketch_tc_pass_cols(kp.kind);
   const int64_t npad = ((n + 127) / 128) * 128;   // 128-j units: every chunk shape tiles it
   const int64_t rows = row1 - row0;
   const bool helm = kp.kind == H2_K_HELMHOLTZ;
@@ -850,9 +880,11 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   // 2^(8s) 2^E 2^-51 / 4; exp: K in (0, 1], weight 2^(8s) 2^-52 / 4
   const int E = helm ? (int)std::ceil(std::log2(1.0 / kp.rmin)) + 2 : 0;
   const double hs = helm ? std::ldexp(kp.param, -E) : 0.0;
-  const int wshift = helm ? E - 53 : -54;
+  const int NS = sketch_tc_slices(kp.kind);
+  // slice weight 2^(8 s) x 2^-KEXP / 4 (exp) or 2^E 2^-HEXP / 4 (Helmholtz)
+  const int wshift = helm ? E - (NS == 7 ? 51 : 46) - 2 : -(NS == 7 ? 52 : 47) - 2;
   double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
-  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 128, st));
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 160, st));
   uint32_t* ovf = static_cast<uint32_t*>(cache_alloc(sizeof(uint32_t), st));
   H2_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
   double* part = nullptr;
@@ -862,9 +894,9 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   H2_CHECK_LAUNCH();
   for (int c0 = 0; c0 < ncols; c0 += wmax) {
     const int nc = std::min(wmax, ncols - c0);
-    const int NCOL = nc > 64 ? 128 : nc > 32 ? 64 : 32;
-    const int TM = NCOL == 128 ? 64 : 128;
-    const int JC = NCOL == 128 ? 128 : 64;
+    const int NCOL = nc > 128 ? 160 : nc > 64 ? 128 : nc > 32 ? 64 : 32;
+    const int TM = NCOL >= 128 ? 64 : 128;
+    const int JC = NCOL >= 128 ? 128 : 64;
     const int64_t nchunks = npad / JC;
     const int tiles = div_up(rows, TM);
     // the split is chosen from n only -- for the row shard of the largest rank count of one box
@@ -889,15 +921,25 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
         H2_CHECK_LAUNCH();
       }
       const dim3 grid((unsigned)(2 * div_up(tiles, 2)), S);   // CTA pairs along x
-      if (helm) tc_launch_pair<H2_K_HELMHOLTZ>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-      else tc_launch_pair<H2_K_EXP>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      if (NS == 7) {
+        if (helm) tc_launch_pair<H2_K_HELMHOLTZ, 7>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+        else tc_launch_pair<H2_K_EXP, 7>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      } else {
+        if (helm) tc_launch_pair<H2_K_HELMHOLTZ, 6>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+        else tc_launch_pair<H2_K_EXP, 6>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      }
     } else {
       omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
           Om + c0, ldo, n, nc, NCOL, JC, nchunks, Bq);
       H2_CHECK_LAUNCH();
       const dim3 grid(tiles, S);
-      if (helm) tc_dispatch<H2_K_HELMHOLTZ>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-      else tc_dispatch<H2_K_EXP>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      if (NS == 7) {
+        if (helm) tc_dispatch<H2_K_HELMHOLTZ, 7>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+        else tc_dispatch<H2_K_EXP, 7>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      } else {
+        if (helm) tc_dispatch<H2_K_HELMHOLTZ, 6>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+        else tc_dispatch<H2_K_EXP, 6>(NCOL, grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+      }
     }
     H2_CHECK_LAUNCH();
     if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);

@@ -29,11 +29,13 @@ def test_omega_matches_oracle_generator():
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("quarters", [False, True])
-@pytest.mark.parametrize("ncols", [45, 128, 150])
+@pytest.mark.parametrize("ncols", [45, 128, 150, 170])
 def test_dense_sketch_matches_oracle(case, quarters, ncols):
-    """DMMA path (arbitrary Omega) and, for the exp kernel with the h2 Omega stream, the exact
-    int8 tensor-core path (sketch_tc.cu): 45 columns = one 128-row / 64-column pass, 128 = one
-    64-row / 128-column pass, 150 = a 128-column pass + a ragged 22-column pass."""
+    """DMMA path (arbitrary Omega) and, with the h2 Omega stream, the int8 tensor-core path
+    (sketch_tc.cu): exp (6 slices, 47-bit grid): 45 columns = one 128-row / 64-column pass, 128 =
+    one 64-row / 128-column pass, 150 = one 160-column pass, 170 = 160 + a ragged 10-column pass;
+    Helmholtz (7 slices): 128-column passes.  Bound 1e-13 max|Y| (the fixed-point grid
+    rounding, <= 2^-48 max|K| per entry, stays at the FP64 GEMM's own rounding level)."""
     mk, kind, p, leaf, tol = CASES[case]
     X = mk()
     T = g.Tree(X, leaf)
@@ -189,12 +191,15 @@ def test_deterministic_bitwise():
     assert np.array_equal(H1._export(g._lib.H2_X_D), H2._export(g._lib.H2_X_D))
 
 
-def test_tc_pass_width_bitwise(monkeypatch):
-    """The 128-column (M = 64) and 64-column (M = 128) tensor-core passes accumulate the same
-    exact integers and sum the byte slices in the same order: bit-identical sketches."""
+@pytest.mark.parametrize("nc,slices", [(128, "6"), (150, "6"), (160, "6"), (150, "7")])
+def test_tc_pass_width_bitwise(monkeypatch, nc, slices):
+    """The 160/128-column (M = 64) and 64-column (M = 128) tensor-core passes accumulate the same
+    exact integers and sum the byte slices in the same order: bit-identical sketches, for both
+    fixed-point formats (6 slices: 47-bit grid, 7: 52-bit)."""
+    monkeypatch.setenv("H2_TC_SLICES", slices)
     X = uniform_points(20000, 3, 0)
     T = g.Tree(X, 64)
-    Od = torch.from_numpy(rng.omega_block(1, 0, 0, T.n, 0, 128)).cuda()
+    Od = torch.from_numpy(rng.omega_block(1, 0, 0, T.n, 0, nc)).cuda()
     monkeypatch.setenv("H2_TC_WIDE", "0")
     y0 = g.dense_sketch(T, Od, ("exp", 0.2), omega_quarters=True)
     monkeypatch.setenv("H2_TC_WIDE", "1")
