@@ -59,7 +59,21 @@ void make_csr(PairCSR& C, std::vector<std::pair<int32_t, int32_t>>& pairs, int32
     std::vector<int32_t> fill(C.ptr.begin(), C.ptr.end() - 1);
     for (auto& p : pairs) C.idx[fill[p.first]++] = p.second;
   }
-  for (int32_t r = 0; r < nrows; ++r) std::sort(C.idx.begin() + C.ptr[r], C.idx.begin() + C.ptr[r + 1]);
+  // per-row work split over threads for large row counts (rows are independent; deterministic)
+  auto par_rows = [nrows](auto&& fn) {
+    const int nt = nrows >= 4096 ? (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1;
+    if (nt <= 1) {
+      fn(0, nrows);
+      return;
+    }
+    std::vector<std::thread> th;
+    for (int q = 0; q < nt; ++q)
+      th.emplace_back([&fn, q, nt, nrows] { fn((int32_t)((int64_t)nrows * q / nt), (int32_t)((int64_t)nrows * (q + 1) / nt)); });
+    for (auto& x : th) x.join();
+  };
+  par_rows([&](int32_t r0, int32_t r1) {
+    for (int32_t r = r0; r < r1; ++r) std::sort(C.idx.begin() + C.ptr[r], C.idx.begin() + C.ptr[r + 1]);
+  });
   // unique pairs (s, b), s <= b (s < b if strict), sorted by (s, b): row s's partners b >= s
   std::vector<int64_t> uoff(nrows + 1, 0);
   std::vector<int32_t> first(nrows);   // position in row s of its first partner b >= s (b > s)
@@ -78,15 +92,17 @@ void make_csr(PairCSR& C, std::vector<std::pair<int32_t, int32_t>>& pairs, int32
       C.us[uoff[r] + q] = r;
       C.ub[uoff[r] + q] = C.idx[e];
     }
-  for (int32_t r = 0; r < nrows; ++r)
-    for (int32_t e = C.ptr[r]; e < C.ptr[r + 1]; ++e) {
-      const int32_t b = C.idx[e];
-      const int32_t a = std::min(r, b), c = std::max(r, b);
-      // position of c among row a's partners >= a (rows are sorted; the symmetric set holds (a, c))
-      const int32_t* b0 = C.idx.data() + C.ptr[a] + first[a];
-      const int32_t* b1 = C.idx.data() + C.ptr[a + 1];
-      C.uidx[e] = (int32_t)(uoff[a] + (std::lower_bound(b0, b1, c) - b0));
-    }
+  par_rows([&](int32_t r0, int32_t r1) {
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t e = C.ptr[r]; e < C.ptr[r + 1]; ++e) {
+        const int32_t b = C.idx[e];
+        const int32_t a = std::min(r, b), c = std::max(r, b);
+        // position of c among row a's partners >= a (rows are sorted; the symmetric set holds (a, c))
+        const int32_t* b0 = C.idx.data() + C.ptr[a] + first[a];
+        const int32_t* b1 = C.idx.data() + C.ptr[a + 1];
+        C.uidx[e] = (int32_t)(uoff[a] + (std::lower_bound(b0, b1, c) - b0));
+      }
+  });
 }
 
 }  // namespace
