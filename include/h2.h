@@ -304,8 +304,10 @@ h2_status h2_verify(const h2_matrix* H, const h2_sketch* sketch, int32_t ncols, 
 /* Built-in dense operator product, rows [row_begin,row_end): y = K(rows,:) * omega (the dense
  * sketch of BASELINE configs[1], also the multi-GPU row shard).  omega: dev, all n rows.
  * flags: H2_SKETCH_OMEGA_QUARTERS asserts every omega entry is q/4 with integer |q| <= 32 (true
- * for the h2_omega stream); it enables the exact int8 tensor-core contraction for H2_K_EXP.
- * Without it (arbitrary omega) the FP64 DMMA path runs. */
+ * for the h2_omega stream); it enables the int8 tensor-core path: K evaluated in FP64, rounded
+ * once to a fixed-point grid (exp: 2^-47, 6 byte slices, 160-column passes; Helmholtz: 2^(E-51),
+ * 7 slices; R32) and contracted exactly in integers.  Without it (arbitrary omega) the
+ * FP64 DMMA path runs.  Environment: H2_TC_SLICES=7 selects the 52-bit grid for exp too. */
 enum { H2_SKETCH_OMEGA_QUARTERS = 1 };
 h2_status h2_dense_sketch(const h2_tree* tree, h2_kernel kern, int64_t row_begin, int64_t row_end,
                           const double* omega, int64_t ld_omega, int32_t ncols, double* y,
