@@ -12,7 +12,7 @@
 namespace h2 {
 
 // ------------------------------------------------------------------------------------------
-// CTA GEMM (256 threads, 64x64 output tiles, 16-deep k slabs, 4x4 DFMA register tile / thread)
+// CTA GEMM (256 threads, 64x64 output tiles, 16-deep k slabs; FP64 DMMA m8n8k4, warp tile 16 x 32)
 //   C(i,j) = beta C(i,j) + sum_k A(i,k) B(k,j)
 //   A(i,k) = tA ? A[k*lda + i] : A[arow(i)*lda + k]     (arow = identity when null)
 //   B(k,j) = tB ? B[bcol(j)*ldb + k] : B[k*ldb + j]      (bcol = identity when null)
@@ -23,10 +23,11 @@ __device__ void cta_gemm(int M, int N, int K, const double* __restrict__ A, int6
   __shared__ double sA[16][64 + 1];
   __shared__ double sB[16][64 + 1];
   const int tid = threadIdx.x;
-  const int ty = tid >> 4, tx = tid & 15;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;   // 8 warps: 4 x 16 rows, 2 x 32 columns
   for (int i0 = 0; i0 < M; i0 += 64)
     for (int j0 = 0; j0 < N; j0 += 64) {
-      double acc[4][4] = {};
+      double acc[2][4][2] = {};
       for (int k0 = 0; k0 < K; k0 += 16) {
         __syncthreads();
         for (int e = tid; e < 16 * 64; e += 256) {
@@ -41,30 +42,33 @@ __device__ void cta_gemm(int M, int N, int K, const double* __restrict__ A, int6
           sB[kk][r] = b;
         }
         __syncthreads();
+        // FP64 tensor cores (DMMA m8n8k4): warp (wr, wc) owns rows 16 wr.. x columns 32 wc..
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          double a[4], b[4];
+        for (int ks = 0; ks < 4; ++ks) {
+          const int kk = ks * 4 + (lane & 3);
+          double af[2], bf[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            a[q] = sA[kk][ty * 4 + q];
-            b[q] = sB[kk][tx * 4 + q];
-          }
+          for (int q = 0; q < 2; ++q) af[q] = sA[kk][wr * 16 + q * 8 + (lane >> 2)];
 #pragma unroll
-          for (int p = 0; p < 4; ++p)
+          for (int q = 0; q < 4; ++q) bf[q] = sB[kk][wc * 32 + q * 8 + (lane >> 2)];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[p][q][0], acc[p][q][1], af[p], bf[q]);
         }
       }
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = i0 + ty * 4 + p, j = j0 + tx * 4 + q;
-          if (i < M && j < N) {
-            double* c = C + (int64_t)i * ldc + j;
-            *c = beta == 0.0 ? acc[p][q] : fma(beta, *c, acc[p][q]);
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = i0 + wr * 16 + p * 8 + (lane >> 2), j = j0 + wc * 32 + q * 8 + 2 * (lane & 3) + h;
+            if (i < M && j < N) {
+              double* c = C + (int64_t)i * ldc + j;
+              *c = beta == 0.0 ? acc[p][q][h] : fma(beta, *c, acc[p][q][h]);
+            }
           }
-        }
     }
 }
 
