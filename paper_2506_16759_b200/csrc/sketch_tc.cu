@@ -29,6 +29,9 @@ namespace {
 // v 2^46: its rounding, <= 2^-48 max|K| per entry, stays below the accumulated rounding of an FP64
 // GEMM of the same sums, and 6 slices leave TMEM room for 160-column passes).  The low-half /
 // high-half split of the slices (summation chains and TMEM lane halves) is NSPLIT.
+#ifndef H2_TC_PACK
+#define H2_TC_PACK 1
+#endif
 template <int NS> struct SliceFmt {
   static constexpr int NSPLIT = NS == 7 ? 4 : 3;
   static constexpr int KEXP = NS == 7 ? 52 : 47;   // exp: m = round(K 2^KEXP)
@@ -254,10 +257,14 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   constexpr int NA = P::NA;
   constexpr int RPT = TM * G / (16 * NPW); // rows per producer thread (TM rows x JC j / (32 NPW lanes x 8 j))
   constexpr int BBUF = P::BBUF;            // B chunk bytes
-  constexpr int LBO_A = TM * 16;           // K-direction core-matrix stride of A
+  // PACK (exp, 6 slices, 64 rows): slices s and s + 3 stacked as the two 64-row halves of one
+  // M = 128 A operand (rows 0-63 slice s, 64-127 slice s + 3): 3 full-rate M = 128 MMAs per k step
+  // instead of 6 half-rate M = 64 ones; accumulator of pair p = all 128 lanes x NCOL columns at p NCOL
+  constexpr bool PACK = KIND == H2_K_EXP && NS == 6 && TM == 64 && H2_TC_PACK;
+  constexpr int LBO_A = PACK ? 2 * TM * 16 : TM * 16;   // K-direction core-matrix stride of A
   constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
   constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL * NS <= 256) ? 256 : 512;
-  constexpr uint32_t IDESC = idesc_i8<TM, NCOL>();
+  constexpr uint32_t IDESC = PACK ? idesc_i8<128, NCOL>() : idesc_i8<TM, NCOL>();
   // Helmholtz: the top slice holds the sign (two's complement of the signed fixed point): s8
   constexpr uint32_t IDESC6 = KIND == H2_K_EXP ? IDESC : (IDESC | (1u << 7));
   static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
@@ -338,16 +345,17 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
         const uint32_t b0 = sbase + P::B0 + slot * BBUF;
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
+        for (int s = 0; s < (PACK ? NS / 2 : NS); ++s)
 #pragma unroll
           for (int kk = 0; kk < JC / 32; ++kk) {
-            const uint64_t ad = umma_desc(a0 + s * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
+            const uint64_t ad = umma_desc(a0 + s * (PACK ? 2 : 1) * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
             const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            const uint32_t dcol = PACK ? (uint32_t)(s * NCOL) : tmem_slice<TM, NCOL, NS>(s);
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + tmem_slice<TM, NCOL, NS>(s)),
-                "l"(ad), "l"(bd), "r"(s == NS - 1 ? IDESC6 : IDESC), "r"(acc));
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + dcol),
+                "l"(ad), "l"(bd), "r"(!PACK && s == NS - 1 ? IDESC6 : IDESC), "r"(acc));
           }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             bar_empty + 8 * buf));
@@ -408,19 +416,65 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         transpose4(lo[k][4], lo[k][5], lo[k][6], lo[k][7], w[1]);
         transpose4(hi[k][0], hi[k][1], hi[k][2], hi[k][3], w[2]);
         transpose4(hi[k][4], hi[k][5], hi[k][6], hi[k][7], w[3]);
+        // slice s at s SLICE, or (PACK) pair s % 3, half s / 3 (64 rows x 16 B per k group)
+        auto sa = [&](int sl) { return PACK ? (sl % 3) * 2 * P::SLICE + (sl / 3) * TM * 16 : sl * P::SLICE; };
 #pragma unroll
         for (int s = 0; s < 4; ++s)
-          *reinterpret_cast<uint2*>(Ab + s * P::SLICE + off[k]) = make_uint2(w[0][s], w[1][s]);
+          *reinterpret_cast<uint2*>(Ab + sa(s) + off[k]) = make_uint2(w[0][s], w[1][s]);
 #pragma unroll
         for (int s = 0; s < NS - 4; ++s)
-          *reinterpret_cast<uint2*>(Ab + (s + 4) * P::SLICE + off[k]) = make_uint2(w[2][s], w[3][s]);
+          *reinterpret_cast<uint2*>(Ab + sa(s + 4) + off[k]) = make_uint2(w[2][s], w[3][s]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
 
       const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
-      if (drain && warp < 4) {
+      if (PACK && drain && warp < 4) {
+        mbar_wait(bar_drain, drains & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        // lane 32 w + l: row 32 (w & 1) + l; warps 0-1 hold slices 0-2 (pairs' low halves), warps
+        // 2-3 slices 3-5.  Chains (s0..s2) and (s3..s5) as in the other shapes; the high warps hand
+        // theirs to the low warps through the coordinate slot of this chunk (consumed, and not
+        // refilled before chunk it + 4), 8 columns at a time.
+        const int64_t i = rtile + 32 * (warp & 1) + lane;
+        const bool high = warp >= 2;
+        double* xb = reinterpret_cast<double*>(smem + P::C0 + slot * CBUF) + (32 * (warp & 1) + lane) * 8;
+        double* y = Yo + (i - row0) * ldy;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NCOL; c0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = 0.0;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            uint32_t r[8];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(p * NCOL + c0);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                           "=r"(r[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const double wgt = ldexp(1.0, 8 * (p + (high ? 3 : 0)) + wshift);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+          }
+          if (high) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) xb[c] = v[c];
+          }
+          asm volatile("bar.sync 1, 128;\n" ::);
+          if (!high && i < row1) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const double t = v[c] + xb[c];
+              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? t : y[c0 + c] + t;
+            }
+          }
+          asm volatile("bar.sync 1, 128;\n" ::);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      } else if (drain && warp < 4) {
         mbar_wait(bar_drain, drains & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         // TM = 128: lane l of warp w holds row 32 w + l, all 7 slices.
