@@ -6,13 +6,16 @@
 //   * Omega entries are exact quarters q/4, q in [-32, 32] (the centred binomial, R8):
 //     one signed int8 operand.
 //   * every kernel entry K in (0, 1] (exp kernel) is generated in FP64 registers and converted
-//     to the 52-bit fixed-point integer m = round(K 2^52) (the mantissa of 1 + K: one DADD,
-//     rounding error <= 2^-53, as for an FP64 value <= 1); its 7 low bytes are 7 unsigned int8
-//     slices A_s (K-major UMMA core-matrix layout in shared memory).
-//   * tcgen05.mma.kind::i8 accumulates D_s = A_s B exactly in int32 TMEM (7 x 32 columns);
-//     every 65536 j the accumulators are drained: Y += sum_s 2^(8s-54) D_s in FP64.
-// The result is the exact product of the 2^-52-rounded K with Omega, rounded only at the
-// drains: as accurate as an FP64 GEMM, and the FP64 pipe only evaluates K.
+//     to the fixed-point integer m = round(K 2^47) (6 bytes; 2^52 / 7 bytes with H2_TC_SLICES=7;
+//     Helmholtz: a signed 53-bit format, 7 bytes, R32) by one FMA; its bytes are the
+//     int8 slices A_s (K-major UMMA core-matrix layout in shared memory).
+//   * tcgen05.mma.kind::i8 accumulates D_s = A_s B exactly in int32 TMEM; every 65536 j the
+//     accumulators are drained: Y += sum_s 2^(8s - 47 - 2) D_s in FP64.
+//   * 160-column passes (exp): 64 rows per CTA, slices s and s + 3 stacked as one M = 128 A
+//     operand, so each K evaluation feeds 160 columns at the tensor core's full M = 128 rate.
+// The result is the exact product of the grid-rounded K with Omega, rounded only at the drains
+// (the grid rounding is at the level of an FP64 GEMM's own accumulated rounding), and the FP64
+// pipe only evaluates K.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -237,13 +240,15 @@ __global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int6
 //   NPW producer warps: wait loaded[slot] (coordinates + B of the chunk landed) and empty[buf]
 //     (the MMA that last read A[buf] finished), evaluate TM/(4 NPW) rows x 8 j each, write the 7
 //     byte slices to A[buf], fence.proxy.async, arrive on full[buf];
-//   1 control warp: waits full[buf], issues the 14 tcgen05.mma (M TM, N NCOL, K 32) of the
-//     chunk, commits empty[buf] (and drain on drain chunks), then refills the coordinate / B ring
-//     with cp.async tracked by mbarriers (cp.async.mbarrier.arrive.noinc) two chunks ahead;
+//   1 control warp: waits full[buf], issues the tcgen05.mma of the chunk (NS x JC/32, or NS/2 x
+//     JC/32 packed M = 128 ones), commits empty[buf] (and drain on drain chunks), then refills the
+//     coordinate / B ring with cp.async tracked by mbarriers (cp.async.mbarrier.arrive.noinc) two
+//     chunks ahead;
 //   producer warps 0-3 (TMEM sub-partitions 0-3) drain the int32 accumulators after every drain
 //     chunk.
-// TM = 128, NCOL <= 64 : 7 x NCOL TMEM columns.  TM = 64, NCOL = 128 : the M = 64 accumulators
-// pack two slices per TMEM column (tmem_slice), so one evaluation of K feeds 128 columns.
+// TM = 128, NCOL <= 64 : NS x NCOL TMEM columns.  TM = 64 : either the M = 64 accumulators of
+// two slices share TMEM columns in the two lane halves (tmem_slice), or (PACK) slices s and s + 3
+// form one M = 128 accumulator in all 128 lanes; one evaluation of K feeds 128 / 160 columns.
 template <int KIND, int TM, int NPW, int NCOL, int JC, int NS>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
