@@ -36,7 +36,7 @@ namespace {
 #define H2_TC_PACK 1
 #endif
 template <int NS> struct SliceFmt {
-  static constexpr int NSPLIT = NS == 7 ? 4 : 3;
+  static constexpr int NSPLIT = 3;                 // chains (s0..s2) + (s3..s{NS-1})
   static constexpr int KEXP = NS == 7 ? 52 : 47;   // exp: m = round(K 2^KEXP)
   static constexpr int HEXP = NS == 7 ? 51 : 46;   // Helmholtz: m = round(v 2^HEXP), |v| < 1
 };
@@ -482,11 +482,11 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       } else if (drain && warp < 4) {
         mbar_wait(bar_drain, drains & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        // TM = 128: lane l of warp w holds row 32 w + l, all 7 slices.
-        // TM = 64 : lanes l < 16 hold row 16 w + l (slices 0-3), lanes 16 + l the same row
-        //           (slices 4-6); the halves are summed with one shuffle.
-        // Both shapes sum the slices as (s0..s3 chain) + (s4..s6 chain), so the sketch is bitwise
-        // independent of the pass width.
+        // TM = 128: lane l of warp w holds row 32 w + l, all slices.
+        // TM = 64 : lanes l < 16 hold row 16 w + l (slices 0-2), lanes 16 + l the same row
+        //           (slices 3..NS-1); the halves are summed with one shuffle.
+        // Every shape sums the slices as (s0..s2 chain) + (s3..s{NS-1} chain), so the sketch is
+        // bitwise independent of the pass width.
         const int64_t i = TM == 128 ? rtile + warp * 32 + lane : rtile + warp * 16 + (lane & 15);
         const bool writer = TM == 128 || lane < 16;
         double* y = Yo + (i - row0) * ldy;
@@ -497,9 +497,11 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
           for (int c = 0; c < 16; ++c) v[c] = u[c] = 0.0;
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
-            if (TM == 64 && s >= NSPLIT) break;
+            if (TM == 64 && s >= (NS - NSPLIT > NSPLIT ? NS - NSPLIT : NSPLIT)) break;
             uint32_t r[16];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + tmem_slice<TM, NCOL, NS>(s) + (uint32_t)c0;
+            // TM = 64: column s NCOL holds slice s (low lanes, s < NSPLIT) and slice s + NSPLIT (high)
+            const uint32_t col = TM == 64 ? (uint32_t)(s * NCOL) : tmem_slice<TM, NCOL, NS>(s);
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + col + (uint32_t)c0;
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                 "[%16];\n"
@@ -510,7 +512,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
             // slice weight 2^(8 sl) * 2^-KEXP * (1/4); at TM = 64 the high lanes hold slice s + NSPLIT
             const int sl = (TM == 128 || lane < 16) ? s : s + NSPLIT;
-            const double wgt = sl < NS ? ldexp(1.0, 8 * sl + wshift) : 0.0;
+            const bool valid = (TM == 128 || lane >= 16) ? sl < NS : s < NSPLIT;
+            const double wgt = valid ? ldexp(1.0, 8 * sl + wshift) : 0.0;
             if (TM == 128 && s >= NSPLIT) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) u[c] = fma((double)(int)r[c], wgt, u[c]);
