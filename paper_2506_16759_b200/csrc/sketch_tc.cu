@@ -266,10 +266,15 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   // M = 128 A operand (rows 0-63 slice s, 64-127 slice s + 3): 3 full-rate M = 128 MMAs per k step
   // instead of 6 half-rate M = 64 ones; accumulator of pair p = all 128 lanes x NCOL columns at p NCOL
   constexpr bool PACK = KIND == H2_K_EXP && NS == 6 && TM == 64 && H2_TC_PACK;
-  constexpr int LBO_A = PACK ? 2 * TM * 16 : TM * 16;   // K-direction core-matrix stride of A
+  // PACK7 (7 slices, 64 rows: Helmholtz, or exp with H2_TC_SLICES=7): the unsigned slices 0-5 as
+  // three packed M = 128 pairs (s, s + 3) and the top slice 6 (s8 for Helmholtz) as one M = 64
+  // MMA into the low lane half of TMEM columns [3 NCOL, 4 NCOL)
+  constexpr bool PACK7 = KIND != H2_K_EXP && NS == 7 && TM == 64 && H2_TC_PACK;   // exp-7: 196 vs 178 ms unpacked
+  constexpr int LBO_A = (PACK || PACK7) ? 2 * TM * 16 : TM * 16;   // K-direction core-matrix stride of A
   constexpr int LBO_B = NCOL * 16;         // K-direction core-matrix stride of B
   constexpr uint32_t TMEM_COLS = (TM == 128 && NCOL * NS <= 256) ? 256 : 512;
-  constexpr uint32_t IDESC = PACK ? idesc_i8<128, NCOL>() : idesc_i8<TM, NCOL>();
+  constexpr uint32_t IDESC = (PACK || PACK7) ? idesc_i8<128, NCOL>() : idesc_i8<TM, NCOL>();
+  constexpr uint32_t IDESC64 = idesc_i8<64, NCOL>() | (KIND == H2_K_EXP ? 0u : (1u << 7));   // PACK7 top slice
   // Helmholtz: the top slice holds the sign (two's complement of the signed fixed point): s8
   constexpr uint32_t IDESC6 = KIND == H2_K_EXP ? IDESC : (IDESC | (1u << 7));
   static_assert(RPT >= 1 && NPW % G == 0 && TM * JC == RPT * 32 * NPW * 8, "producer tiling");
@@ -349,18 +354,30 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       if (lane == 0) {
         const uint32_t a0 = sbase + P::A0 + buf * P::ABUF;
         const uint32_t b0 = sbase + P::B0 + slot * BBUF;
-#pragma unroll
-        for (int s = 0; s < (PACK ? NS / 2 : NS); ++s)
+        if (PACK7) {
 #pragma unroll
           for (int kk = 0; kk < JC / 32; ++kk) {
-            const uint64_t ad = umma_desc(a0 + s * (PACK ? 2 : 1) * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
+            const uint64_t ad = umma_desc(a0 + 6 * P::SLICE + kk * 2 * (TM * 16), TM * 16, 128);
             const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-            const uint32_t dcol = PACK ? (uint32_t)(s * NCOL) : tmem_slice<TM, NCOL, NS>(s);
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(3 * NCOL)),
+                "l"(ad), "l"(bd), "r"(IDESC64), "r"(acc));
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < (PACK || PACK7 ? 3 : NS); ++s)
+#pragma unroll
+          for (int kk = 0; kk < JC / 32; ++kk) {
+            const uint64_t ad = umma_desc(a0 + s * (PACK || PACK7 ? 2 : 1) * P::SLICE + kk * 2 * LBO_A, LBO_A, 128);
+            const uint64_t bd = umma_desc(b0 + kk * 2 * LBO_B, LBO_B, 128);
+            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            const uint32_t dcol = (PACK || PACK7) ? (uint32_t)(s * NCOL) : tmem_slice<TM, NCOL, NS>(s);
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                 " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + dcol),
-                "l"(ad), "l"(bd), "r"(!PACK && s == NS - 1 ? IDESC6 : IDESC), "r"(acc));
+                "l"(ad), "l"(bd), "r"(!PACK && !PACK7 && s == NS - 1 ? IDESC6 : IDESC), "r"(acc));
           }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             bar_empty + 8 * buf));
@@ -390,6 +407,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
       off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
+    // PACK7: the M = 64 layout of the top slice (64 rows x 16 B per k group)
+    const int off6d = g * (TM * 16) - g * LBO_A;
     const uint32_t lane8 = 8u * (lane & 15);
     uint32_t ovf = 0;
     int drains = 0;
@@ -422,7 +441,10 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         transpose4(hi[k][0], hi[k][1], hi[k][2], hi[k][3], w[2]);
         transpose4(hi[k][4], hi[k][5], hi[k][6], hi[k][7], w[3]);
         // slice s at s SLICE, or (PACK) pair s % 3, half s / 3 (64 rows x 16 B per k group)
-        auto sa = [&](int sl) { return PACK ? (sl % 3) * 2 * P::SLICE + (sl / 3) * TM * 16 : sl * P::SLICE; };
+        auto sa = [&](int sl) {
+          if (PACK7 && sl == 6) return 6 * P::SLICE + off6d;
+          return (PACK || PACK7) ? (sl % 3) * 2 * P::SLICE + (sl / 3) * TM * 16 : sl * P::SLICE;
+        };
 #pragma unroll
         for (int s = 0; s < 4; ++s)
           *reinterpret_cast<uint2*>(Ab + sa(s) + off[k]) = make_uint2(w[0][s], w[1][s]);
@@ -473,6 +495,61 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const double t = v[c] + xb[c];
+              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? t : y[c0 + c] + t;
+            }
+          }
+          asm volatile("bar.sync 1, 128;\n" ::);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      } else if (PACK7 && drain && warp < 4) {
+        mbar_wait(bar_drain, drains & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        // pairs: lane 32 w + l holds row 32 (w & 1) + l, slices 0-2 (w < 2) or 3-5 (w >= 2); the
+        // top slice (M = 64 layout) holds row 16 w + l in lanes l < 16.  Chains (s0..s2) and
+        // (s3..s6): the top slice goes to the high warps and their chain to the low warps through
+        // the consumed coordinate slot of this chunk, 4 columns at a time.
+        const int row = 32 * (warp & 1) + lane;
+        const int64_t i = rtile + row;
+        const bool high = warp >= 2;
+        int32_t* xs6 = reinterpret_cast<int32_t*>(smem + P::C0 + slot * CBUF);   // 64 x 4 int32
+        double* xu = reinterpret_cast<double*>(smem + P::C0 + slot * CBUF + 64 * 4 * 4);   // 64 x 4
+        double* y = Yo + (i - row0) * ldy;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NCOL; c0 += 4) {
+          uint32_t r6[4];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                       : "=r"(r6[0]), "=r"(r6[1]), "=r"(r6[2]), "=r"(r6[3])
+                       : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(3 * NCOL + c0)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+          if (lane < 16) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) xs6[(16 * warp + lane) * 4 + c] = (int32_t)r6[c];
+          }
+          double v[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[c] = 0.0;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            uint32_t r[4];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                         : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(p * NCOL + c0)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+            const double wgt = ldexp(1.0, 8 * (p + (high ? 3 : 0)) + wshift);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = fma((double)(int)r[c], wgt, v[c]);
+          }
+          asm volatile("bar.sync 1, 128;\n" ::);
+          if (high) {
+            const double w6 = ldexp(1.0, 8 * 6 + wshift);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) xu[row * 4 + c] = fma((double)xs6[row * 4 + c], w6, v[c]);
+          }
+          asm volatile("bar.sync 1, 128;\n" ::);
+          if (!high && i < row1) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double t = v[c] + xu[row * 4 + c];
               if (c0 + c < ncols) y[c0 + c] = drains == 0 ? t : y[c0 + c] + t;
             }
           }
