@@ -277,6 +277,8 @@ def run_ours(args, w, rank, world, local_rank):
         "config": {"workload": args.workload, "n": n, "leaf": w["leaf"], "eta": 0.7, "tol": w["tol"],
                    "kernel": f"{w['kernel']}({w['param']})", "sketch": "dense-kernel (row shards)" if world > 1
                    else "dense-kernel", "d_init": 32, "d_blk": 32, "d_max": 512,
+                   "eps_rule": "s*tol*rho*gamma^(Dl-t), s=0.04, gamma=1.25 (DESIGN.md R31)",
+                   "sketch_format": "int8 tcgen05, 6-byte fixed-point K (2^-47 grid), 160-column pass (R32)",
                    "parallelism": (f"subtree shards x{world} (sketch rows, clusters per level; "
                                    f"{dist.get_backend().upper() if dist else ''} all-gathers"
                                    f"{'' if dist and dist.get_backend() == 'nccl' else ', ranks share a GPU'})")
