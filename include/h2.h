@@ -225,7 +225,16 @@ typedef struct {
   double verify_error;        /* e of the returned matrix (opts.verify_probes > 0), else 0    */
   int32_t verify_rebuilds;    /* rebuilds with s/3 made by the a-posteriori check            */
   double tol_safety_used;     /* s of the returned matrix                                    */
+  int32_t cpqr_variants;      /* bitmask of the CPQR kernels that ran (H2_CQ_V_*)             */
+  double t_depth_ms[64];      /* device time of each processed depth t (its BSR subtraction,
+                                 convergence tests, updateSamples replays, ID, shrink, B)   */
+  double norm_est;            /* nu used by H2_TOL_LITERAL (opts.norm, or the power-iteration
+                                 estimate when opts.norm <= 0), else 0                       */
 } h2_build_stats;
+/* CPQR kernel variants (h2_build_stats.cpqr_variants; H2_CQ_VARIANT=warp|smem|global forces one
+ * where it applies): one warp per panel (m <= 64), one CTA per panel with the panel in shared
+ * memory, one CTA per panel with the panel in global memory (L1/L2 resident). */
+enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4 };
 
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU (§IV-B: "the batch count becomes roughly the number

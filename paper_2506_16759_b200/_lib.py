@@ -19,6 +19,7 @@ H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK, H2_E_DENSE_MATRIX = 0, 1, 2, 3
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C = range(10)
 H2_SKETCH_OMEGA_QUARTERS = 1
+H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL = 1, 2, 4
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
 H2_NPHASE = len(PHASES)
 
@@ -78,7 +79,8 @@ class h2_build_stats(C.Structure):
                 ("sketch_columns", C.c_int64),
                 ("bytes_U", C.c_int64), ("bytes_E", C.c_int64), ("bytes_B", C.c_int64), ("bytes_D", C.c_int64),
                 ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double),
-                ("verify_error", C.c_double), ("verify_rebuilds", C.c_int32), ("tol_safety_used", C.c_double)]
+                ("verify_error", C.c_double), ("verify_rebuilds", C.c_int32), ("tol_safety_used", C.c_double),
+                ("cpqr_variants", C.c_int32), ("t_depth_ms", C.c_double * 64), ("norm_est", C.c_double)]
 
 
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)

@@ -152,11 +152,27 @@ struct PhaseTimer {
       out[x.first] += ms;
     }
   }
+  // per-depth device time (h2_build_stats.t_depth_ms): [mark(t), mark(next)) on the build stream
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  void mark(int t) {
+    cudaEvent_t e;
+    H2_CUDA(cudaEventCreate(&e));
+    H2_CUDA(cudaEventRecord(e, st));
+    marks.push_back({t, e});
+  }
+  void collect_depths(double* out) {
+    for (size_t i = 0; i + 1 < marks.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, marks[i].second, marks[i + 1].second);
+      if (marks[i].first >= 0 && marks[i].first < 64) out[marks[i].first] += ms;
+    }
+  }
   ~PhaseTimer() {
     for (auto& x : ev) {
       cudaEventDestroy(x.second.first);
       cudaEventDestroy(x.second.second);
     }
+    for (auto& m : marks) cudaEventDestroy(m.second);
   }
 };
 
@@ -633,7 +649,7 @@ struct Builder {
     a.k = L.d_k.p;
     a.perm = L.d_perm.p;
     a.cert = L.cert.p;
-    launch_cpqr(a, st);
+    H.stats.cpqr_variants |= launch_cpqr(a, st);
     timer.end();
     if (comm) comm_allgather_clusters(comm, L.d_k.p, 4, t, [](int c) { return (int64_t)c; }, st);
     L.k = download(L.d_k, L.nclus, st);
@@ -1173,12 +1189,14 @@ struct Builder {
     cur.alloc(T.n, ld_for(T.n, d), st);
     curc.alloc(T.n, ld_for(T.n, d), st);
     ns_draw(cur.Y.p, cur.O.p, cur.ld, curc.Y.p, curc.O.p, curc.ld, 0, d);   // line 1, both sketches
+    timer.mark(Dl);
     ns_gen_D();                                                            // line 212, ordered pairs
     setup_level(Dl, 0);
     setup_level(Dl, 1);
     ns_bsr_both(Dl, cur, curc, 0, d);                                      // line 213
     for (int t = Dl; t >= top; --t) {
       if (t < Dl) {
+        timer.mark(t);
         setup_level(t, 0);
         setup_level(t, 1);
         ns_bsr_both(t, cur, curc, 0, d);                                   // lines 240-243
@@ -1221,6 +1239,7 @@ struct Builder {
       cur = std::move(nr);
       curc = std::move(nc);
     }
+    timer.mark(-1);
     finish(top, Dl);
   }
 
@@ -1262,6 +1281,7 @@ struct Builder {
     cur.alloc(T.n, ld_for(T.n, d), st);
     draw(cur.Y.p, cur.O.p, cur.ld, 0, d);
     // line 212: D_{tau,b} = K(I_tau, I_b), one unique block per unordered pair
+    timer.mark(Dl);
     H.D.alloc(T.D_off.back(), st);
     {
       GenArgs g{};
@@ -1304,6 +1324,7 @@ struct Builder {
     bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
     for (int t = Dl; t >= top; --t) {
       if (t < Dl) {
+        timer.mark(t);
         setup_level(t);
         bsr(t, cur.Y.p, cur.O.p, cur.ld, d);   // lines 240-243
       }
@@ -1339,6 +1360,7 @@ struct Builder {
       gen_B(t);                                     // line 258
       cur = std::move(next);
     }
+    timer.mark(-1);
     finish(top, Dl);
   }
 
@@ -1390,6 +1412,7 @@ struct Builder {
       }
     }
     timer.collect(s.t_phase_ms);
+    timer.collect_depths(s.t_depth_ms);
     if (getenv("H2_TRACE")) {
       fprintf(stderr, "[h2 trace] host ms per phase:");
       for (int p = 0; p < H2_NPHASE; ++p) fprintf(stderr, " %.1f", timer.host_ms[p]);

@@ -384,32 +384,41 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
   }
 }
 
-void launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
-  if (a.nclusters <= 0) return;
+static int forced_variant() {
+  const char* v = getenv("H2_CQ_VARIANT");
+  if (!v) return 0;
+  const std::string s(v);
+  return s == "warp" ? H2_CQ_V_WARP : s == "smem" ? H2_CQ_V_SMEM : s == "global" ? H2_CQ_V_GLOBAL : 0;
+}
+
+int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
+  if (a.nclusters <= 0) return 0;
+  const int force = forced_variant();
   const size_t wsm = sizeof(double) * cw_warp_doubles(a.d) * CW_WPB;
-  if (a.max_m <= 64 && wsm <= 200 * 1024 && env_int("H2_CQ_WARP", 1) != 0) {
-    static bool attr = false;
-    if (!attr) {
-      H2_CUDA(cudaFuncSetAttribute(cpqr_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+  if (a.max_m <= 64 && wsm <= 200 * 1024 && env_int("H2_CQ_WARP", 1) != 0 && (force == 0 || force == H2_CQ_V_WARP)) {
+    // per launch: the attribute is per device (a process may drive several GPUs)
+    H2_CUDA(cudaFuncSetAttribute(cpqr_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     cpqr_warp_kernel<<<div_up(a.nclusters, CW_WPB), 32 * CW_WPB, wsm, st>>>(a);
     H2_CHECK_LAUNCH();
-    return;
+    return H2_CQ_V_WARP;
   }
   size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
   size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
   // rows per pass = threads / 8 (32 or 64); 512 threads once a panel has more than 32 rows
   const bool big = a.max_m > 32;
-  if (sm + panel <= 200 * 1024) {
+  int used;
+  if (sm + panel <= 200 * 1024 && force != H2_CQ_V_GLOBAL) {
     sm += panel;
     if (big) cpqr_launch<true, 512>(a, sm, st);
     else cpqr_launch<true, 256>(a, sm, st);
+    used = H2_CQ_V_SMEM;
   } else {
     if (big) cpqr_launch<false, 512>(a, sm, st);
     else cpqr_launch<false, 256>(a, sm, st);
+    used = H2_CQ_V_GLOBAL;
   }
   H2_CHECK_LAUNCH();
+  return used;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -489,11 +498,8 @@ void launch_id(const IdArgs& a, cudaStream_t st) {
   if (a.nclusters <= 0) return;
   const int ny = std::max(1, div_up(a.max_red, ID_CB));
   const size_t smem = sizeof(double) * (size_t)std::max(a.max_k, 1) * (ID_CB + 1);
-  static bool attr = false;   // static sD + dynamic may exceed 48 KB for any k > 150
-  if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  // static sD + dynamic may exceed 48 KB for any k > 150; per launch (the attribute is per device)
+  H2_CUDA(cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   if (smem <= 200 * 1024) {
     id_kernel<<<dim3(a.nclusters, ny), 256, smem, st>>>(a, nullptr);
     H2_CHECK_LAUNCH();

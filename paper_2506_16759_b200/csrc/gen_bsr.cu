@@ -247,15 +247,12 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
 
 static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
-  static bool attr = false;
   constexpr size_t sm32 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (32 + 4));
   constexpr size_t sm64 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (64 + 4));
-  if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32));
-    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
-    H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
-    attr = true;
-  }
+  // per launch: the attribute is per device (a process may drive several GPUs)
+  H2_CUDA(cudaFuncSetAttribute(bsr_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32));
+  H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
+  H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
   static const int wm64 = env_int("H2_BSR_WM64", 4);   // 32 x 32 warp tiles for 64-column passes (-3 ms at C2)
   if (a.ncols > 32) {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 64));

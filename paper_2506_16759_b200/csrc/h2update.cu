@@ -92,11 +92,17 @@ __global__ void lowrank_w_final_kernel(const double* __restrict__ part, int npar
   }
 }
 // Y(i, c) += sum_a U(i, a) W(a, c)
+template <bool SMEM>
 __global__ void lowrank_apply_kernel(const double* __restrict__ U, int64_t ldu, int r, const double* __restrict__ W,
                                      int nc, int64_t n, double* __restrict__ Y, int64_t ldy) {
-  extern __shared__ double sW[];
-  for (int e = threadIdx.x; e < r * nc; e += blockDim.x) sW[e] = W[e];
-  __syncthreads();
+  extern __shared__ double smW[];
+  // W = V^T Om (r x nc) staged in shared memory when it fits the default 48 KB, else read
+  // through L1 (any rank / column count the build accepts)
+  const double* sW = SMEM ? smW : W;
+  if (SMEM) {
+    for (int e = threadIdx.x; e < r * nc; e += blockDim.x) smW[e] = W[e];
+    __syncthreads();
+  }
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * nc; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / nc;
     const int c = (int)(t - i * nc);
@@ -120,7 +126,9 @@ void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om
   lowrank_w_final_kernel<<<div_up(r * nc, 256), 256, 0, st>>>(scratch, np, r * nc, W);
   H2_CHECK_LAUNCH();
   const int grid = (int)std::min<int64_t>((n * nc + 255) / 256, 148 * 16);
-  lowrank_apply_kernel<<<grid, 256, sizeof(double) * r * nc, st>>>(U, ldu, r, W, nc, n, Y, ldy);
+  const size_t wbytes = sizeof(double) * (size_t)r * nc;
+  if (wbytes <= 48 * 1024) lowrank_apply_kernel<true><<<grid, 256, wbytes, st>>>(U, ldu, r, W, nc, n, Y, ldy);
+  else lowrank_apply_kernel<false><<<grid, 256, 0, st>>>(U, ldu, r, W, nc, n, Y, ldy);
   H2_CHECK_LAUNCH();
 }
 

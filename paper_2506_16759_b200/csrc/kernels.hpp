@@ -104,7 +104,10 @@ struct CpqrArgs {
   int32_t* perm;          // at poff[c]
   double* cert;           // 2 per cluster (min gap, stop margin)
 };
-void launch_cpqr(const CpqrArgs& a, cudaStream_t st);
+// returns the variant that ran: H2_CQ_V_WARP (warp per panel, m <= 64), H2_CQ_V_SMEM (CTA per
+// panel, panel in shared memory) or H2_CQ_V_GLOBAL (CTA per panel, panel in global W).
+// H2_CQ_VARIANT=warp|smem|global forces a variant where it applies (tests of each path).
+int launch_cpqr(const CpqrArgs& a, cudaStream_t st);
 
 // ID epilogue: X_c (m x k, U or [E1;E2]) from T = R11^{-1} R12 (R15); skeletons I~ (L224, L253)
 struct IdArgs {

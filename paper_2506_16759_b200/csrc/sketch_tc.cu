@@ -930,13 +930,10 @@ template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
   constexpr int NPW = 16;   // producer warps (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128)
-  static bool attr = false;
   constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
-  if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  // per launch: the attribute is per device (a process may drive several GPUs)
+  H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
                                                                                     yo, ld, sstride, hs, wshift, ovf);
 }
@@ -946,12 +943,8 @@ void tc_launch_pair(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int
                     const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs,
                     int wshift, uint32_t* ovf) {
   constexpr int NPW = 16;
-  static bool attr = false;
   constexpr int smem = PairPlan<NS>::TOTAL;
-  if (!attr) {
-    H2_CUDA(cudaFuncSetAttribute(sketch_tc_pair_kernel<KIND, NPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  H2_CUDA(cudaFuncSetAttribute(sketch_tc_pair_kernel<KIND, NPW, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(32 * (NPW + 1));

@@ -257,13 +257,15 @@ class H2Matrix:
 def _stats_dict(s):
     d = {k: getattr(s, k) for k in ("samples", "failed_depth", "top_depth", "leaf_depth", "eps", "entries_D",
                                     "entries_B", "entries_sketch", "sketch_columns", "bytes_U", "bytes_E", "bytes_B", "bytes_D",
-                                    "launches", "t_total_ms", "verify_error", "verify_rebuilds", "tol_safety_used")}
+                                    "launches", "t_total_ms", "verify_error", "verify_rebuilds", "tol_safety_used",
+                                    "cpqr_variants", "norm_est")}
     lo, hi = s.top_depth, s.leaf_depth
     d["rounds"] = {t: s.rounds[t] for t in range(lo, hi + 1)}
     d["rank_min"] = {t: s.rank_min[t] for t in range(lo, hi + 1)}
     d["rank_max"] = {t: s.rank_max[t] for t in range(lo, hi + 1)}
     d["rank_mean"] = {t: s.rank_mean[t] for t in range(lo, hi + 1)}
     d["t_phase_ms"] = {L.PHASES[i]: s.t_phase_ms[i] for i in range(L.H2_NPHASE)}
+    d["t_depth_ms"] = {t: s.t_depth_ms[t] for t in range(lo, hi + 1)}
     return d
 
 
@@ -329,12 +331,15 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
             try:
                 r = req.contents
                 n, nr, nc = r.n, r.row_end - r.row_begin, r.ncols
-                om = device_view(r.omega, (n, nc), (r.ld_omega, 1))
-                y = device_view(r.y, (nr, nc), (r.ld_y, 1))
-                if nonsym:
-                    sketch(om, y, r.col0, r.row_begin, r.row_end, transpose=r.transpose)
-                else:
-                    sketch(om, y, r.col0, r.row_begin, r.row_end)
+                # the callback's torch work is enqueued on libh2's stream (req.stream): ordered
+                # after the Omega generation and before the library's next kernels (h2.h)
+                with torch.cuda.stream(torch.cuda.ExternalStream(r.stream or 0)):
+                    om = device_view(r.omega, (n, nc), (r.ld_omega, 1))
+                    y = device_view(r.y, (nr, nc), (r.ld_y, 1))
+                    if nonsym:
+                        sketch(om, y, r.col0, r.row_begin, r.row_end, transpose=r.transpose)
+                    else:
+                        sketch(om, y, r.col0, r.row_begin, r.row_end)
                 return 0
             except Exception as exc:  # reported as H2_ERR_CALLBACK
                 import traceback
@@ -360,7 +365,8 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
         def _en(ctx, batch):
             try:
                 b = batch.contents
-                entry(b)
+                with torch.cuda.stream(torch.cuda.ExternalStream(b.stream or 0)):
+                    entry(b)
                 return 0
             except Exception:
                 import traceback

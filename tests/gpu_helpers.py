@@ -22,10 +22,11 @@ def oracle_build(X, kind, param, leaf, tol, eta=0.7, seed=1, **opts):
     return H, op
 
 
-def compare_builds(Hg, Ho):
+def compare_builds(Hg, Ho, diverged_out=None):
     """Level by level from the leaves: ranks and skeletons bit-exact where comparable; a
     mismatch must be certified by the oracle (near-tie).  Descendants of a diverged cluster
-    (its ancestors in the tree) are excluded.  Returns (#certified mismatches, #compared)."""
+    (its ancestors in the tree) are excluded.  Returns (#certified mismatches, #compared);
+    diverged_out (dict) receives depth -> bool mask of the clusters excluded or diverged."""
     Dl = Ho.tree.leaf_depth
     assert Hg.top_depth == Ho.top
     diverged = {Dl + 1: np.zeros(1 << (Dl + 1), bool)}
@@ -63,7 +64,40 @@ def compare_builds(Hg, Ho):
                 bound = np.sqrt(max(P.shape[0] - len(J), 0)) * Ho.eps
                 assert res <= 1.01 * bound + 1e-12 * np.linalg.norm(P), (t, c, res, res_o, bound)
         diverged[t] = div
+    if diverged_out is not None:
+        diverged_out.update({t: diverged[t] for t in range(Ho.top, Dl + 1)})
     return certified, compared
+
+
+def compare_blocks(Hg, Ho, diverged, tol_b=4e-15, tol_d=3.2e-15):
+    """D blocks entrywise (they do not depend on the skeletons: every near pair is compared) and B
+    blocks of every far pair whose two clusters have bit-identical skeletons (diverged clusters
+    are compared by error instead, see compare_matvec).  Returns the number of B blocks compared."""
+    for (s, b), blk in Hg.D_blocks().items():
+        ref = Ho.D[(s, b)]
+        assert np.abs(blk - ref).max() <= tol_d * max(1.0, np.abs(ref).max()), (s, b)
+    nb = 0
+    for t in range(Ho.top, Ho.tree.leaf_depth + 1):
+        div = diverged[t]
+        for (s, b), blk in Hg.B_blocks(t).items():
+            if div[s] or div[b]:
+                continue
+            ref = Ho.B[t][(s, b)]
+            assert np.abs(blk - ref).max() <= tol_b * max(1.0, np.abs(ref).max()), (t, s, b)
+            nb += 1
+    return nb
+
+
+def compare_matvec(Hg, Ho, certified, err_bound, seed=3, exact_bound=1e-10):
+    """H^2 matvecs of both representations: <= 1e-10 relative when every skeleton matched
+    (BASELINE north_star); with certified near-tie divergences the two are different valid
+    approximations and agree to the sum of their error bounds (each within err_bound of K)."""
+    x = np.random.default_rng(seed).standard_normal((Ho.tree.n, 5))
+    yg = Hg.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = oh2.matvec(Ho, x)
+    rel = np.linalg.norm(yg - yo) / np.linalg.norm(yo)
+    assert rel <= (exact_bound if certified == 0 else 2 * err_bound), rel
+    return rel
 
 
 def probe_error(Hg, K, q=8, seed=2):

@@ -45,16 +45,34 @@ def test_fullsize_omega_sampled_rows_bitwise():
     assert np.array_equal(got, want)
 
 
-def test_fullsize_sketch_rows(full):
-    """One 128-column tensor-core pass over all N rows (the bench's pass shape) vs the oracle's
-    K(rows, :) Omega for 48 sampled rows: <= 1e-13 max|Y| (fixed-point rounding of K at 2^-53)."""
+@pytest.mark.parametrize("ncols", [160, 128])
+def test_fullsize_sketch_rows(full, ncols):
+    """The bench's sketch launch: ONE 160-column packed tensor-core pass over all N = 2^18 rows
+    (M = 128 slice pairs, 64-row tiles, the j-split chosen for this N, all TMEM drains of
+    65536-j chunks), exactly what h2_build issues for the speculative pass (the build above
+    reports one sketch launch of 160 columns), vs the oracle's K(rows, :) Omega for 48 sampled
+    rows: <= 1e-13 max|Y| (fixed-point rounding of K at 2^-47, R32).  128 columns:
+    the 7-slice / Helmholtz pass shape."""
     X, T, H, op = full
-    Om = g.omega(N, 128)
+    assert H.stats["sketch_columns"] == 160 and H.stats["entries_sketch"] == N * N   # bench launch shape
+    Om = g.omega(N, ncols)
     Y = g.dense_sketch(T, Om, KERN, omega_quarters=True)
-    rows = np.sort(np.random.default_rng(6).choice(N, 48, replace=False))
+    rows = np.sort(np.random.default_rng(6 + ncols).choice(N, 48, replace=False))
+    rows[0], rows[-1] = 0, N - 1            # first and last row tiles (ragged j-split edges)
     ref = op.sketch_rows(Om.cpu().numpy(), rows)
     got = Y[torch.from_numpy(rows).cuda()].cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_fullsize_cpqr_variants(full):
+    """Which CPQR kernels the bench's launch configuration runs (h2_build_stats.cpqr_variants);
+    each of them is forced on every level of an oracle-parity build in
+    test_gpu_parity.py::test_build_parity_each_cpqr_variant."""
+    X, T, H, op = full
+    cv = H.stats["cpqr_variants"]
+    # the bench's launch configuration runs all three CPQR paths at N = 2^18: the warp kernel on
+    # the 64-row leaf panels and the CTA kernels (shared / global panel) on the inner levels
+    assert cv & g._lib.H2_CQ_V_WARP and cv & (g._lib.H2_CQ_V_SMEM | g._lib.H2_CQ_V_GLOBAL), cv
 
 
 def test_fullsize_convergence_and_identity_rows(full):

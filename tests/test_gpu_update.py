@@ -125,3 +125,51 @@ def test_dense_operator_workload():
         rs = np.arange(T.begin[T.leaf_depth][s], T.end[T.leaf_depth][s])
         rb = np.arange(T.begin[T.leaf_depth][b], T.end[T.leaf_depth][b])
         assert np.array_equal(D[(s, b)], Ah[np.ix_(rs, rb)])
+
+
+def test_update_build_parity_vs_oracle_M():
+    """configs[4] path against the oracle's M (advisor/verdict item): M = A* + U U^T with A* a
+    seeded synthetic symmetric H^2 of known ranks on the tree (tests/synthetic_h2.py, an input,
+    not an output of either path) and U a rank-8 update.  GPU: the base H^2(A*) is built from the
+    explicit operator (dense=A*, exact recovery at 1e-12), then M is recompressed through the
+    library's H^2-matvec + low-rank sketch and entry extraction (update=(H_A, U)).  Oracle:
+    Algorithm 1 on M itself (sampler M Omega, entries M(I, J)).  Both use the same Omega stream:
+    ranks and skeletons bit-exact (or certified near-ties), samples equal, D = A*(I_s, I_b) +
+    U U^T and B = M(I~_s, I~_b) entrywise against the oracle's blocks, matvecs agree."""
+    from synthetic_h2 import synthetic_h2
+    from gpu_helpers import compare_builds, compare_blocks, compare_matvec
+    n, r = 2048, 8
+    X = uniform_points(n, 3, 12)
+    tree = geometry.build_cluster_tree(X, 64)
+    part = geometry.build_partition(tree, 0.7)
+    A, _, _ = synthetic_h2(tree, part, lambda t, m: min(m, 5 + (t % 3) * 2), 4)
+    A /= np.abs(A).max()
+    Ul = np.random.default_rng(6).standard_normal((n, r)) / np.sqrt(r)
+    M = A + Ul @ Ul.T
+    nu = float(np.linalg.norm(M, 2))
+    # tolerance well above the base's representation error (1e-12) and well below every
+    # retained singular value: no truncation decision near eps on either side
+    tol = 1e-8
+    opts = dict(tol_rule="literal", norm=nu, adaptive=True, d_init=16, d_blk=16, d_max=256)
+    T = g.Tree(X, 64)
+    assert np.array_equal(T.perm, tree.perm)
+    Ad = torch.from_numpy(A).cuda()
+    Hb = g.build(T, ("exp", 0.2), 1e-12, dense=Ad, tol_rule="literal", norm=float(np.linalg.norm(A, 2)),
+                 adaptive=False, d_init=96)
+    Hu = g.build(T, ("exp", 0.2), tol, update=(Hb, torch.from_numpy(Ul).cuda()), **opts)
+    om = lambda c0, nc: rng.omega_block(1, 0, 0, n, c0, nc)
+    Ho = oh2.build(tree, part, lambda O: M @ O, lambda I, J: M[np.ix_(I, J)], om, tol,
+                   oh2.BuildOpts(**{k: v for k, v in opts.items()}))
+    div = {}
+    certified, compared = compare_builds(Hu, Ho, div)
+    assert certified <= max(1, compared // 100)
+    if certified == 0:
+        assert Hu.samples == Ho.samples
+    # D: the base's D blocks are A*'s entries (lookups) plus U U^T on the device (DMMA)
+    nb = compare_blocks(Hu, Ho, div, tol_b=1e-10, tol_d=1e-14)
+    assert nb > 0
+    x = np.random.default_rng(3).standard_normal((n, 5))
+    yu = Hu.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.linalg.norm(yu - M @ x) <= 4 * tol * nu * np.linalg.norm(x) * 10
+    # the two operators differ by the base's representation error (<= 1e-12 relative)
+    compare_matvec(Hu, Ho, certified, 1e-6, exact_bound=1e-8)
