@@ -79,6 +79,31 @@ h2_status h2_tree_get_info(const h2_tree* tree, h2_tree_info* info);
 h2_status h2_tree_export(const h2_tree* tree, int64_t* perm, int64_t* begin, int64_t* end,
                          int32_t* near_pairs);
 h2_status h2_tree_far_count(const h2_tree* tree, int32_t depth, int64_t* nnz);
+
+/* A partition built elsewhere (e.g. by the CPU oracle), so that libh2 and another implementation
+ * consume the SAME tree (Algorithm 1 takes "a hierarchical partitioning" as input).
+ * All arrays are host memory owned by the caller (copied).  Layouts as h2_tree_export:
+ *   coords    n x dim row-major, ORIGINAL order;  perm[n]: tree index -> original index
+ *   begin/end cluster index ranges (tree order) in heap order, node (t, c) at 2^t - 1 + c,
+ *             2^(leaf_depth+1) - 1 entries: a complete binary tree, children split their parent
+ *             contiguously, all leaves at leaf_depth
+ *   near      near_nnz ordered pairs (s, b) of leaves, symmetric set, including every (s, s)
+ *   far[t]    far_nnz[t] ordered admissible pairs of depth t (s != b, symmetric), t = 0..leaf_depth
+ * Checked (INVALID_ARG): permutation, nesting, ranges, duplicates, symmetry, and that the block
+ * areas sum to n^2.  The admissibility rule is the caller's (eta / dist_rule are not used). */
+typedef struct {
+  int64_t n;
+  int32_t dim, leaf_depth;
+  const double* coords;
+  const int64_t* perm;
+  const int64_t* begin;
+  const int64_t* end;
+  int64_t near_nnz;
+  const int32_t* near_pairs;
+  const int64_t* far_nnz;
+  const int32_t* const* far_pairs;
+} h2_tree_desc;
+h2_status h2_tree_import(const h2_tree_desc* desc, h2_tree** out);
 h2_status h2_tree_export_far(const h2_tree* tree, int32_t depth, int32_t* far_pairs);
 void h2_tree_free(h2_tree* tree);
 
@@ -86,8 +111,12 @@ void h2_tree_free(h2_tree* tree);
  * Operators.  Built-in kernels (§V-A) enable the fused device paths:
  *   H2_K_EXP       K(x,y) = exp(-|x-y|/param)                (Eq. cov, l = 0.2 in L431)
  *   H2_K_HELMHOLTZ K(x,y) = cos(param |x-y|)/|x-y|, 0 at x=y (Eq. ie, k = 3 in L439)
+ *   H2_K_RATIONAL  K(x,y) = 1 / (1 + |x-y|^2 / param^2)   (not in the paper: a smooth test kernel
+ *                  whose entries are correctly rounded operations only, r^2 = (dx*dx + dy*dy) + dz*dz,
+ *                  so CPU and GPU evaluate it bitwise alike -- the exact-order parity mode,
+ *                  SURVEY §8(c) contract 2; sketched by the exact-order kernel, any Omega)
  * ------------------------------------------------------------------------------------- */
-enum { H2_K_EXP = 0, H2_K_HELMHOLTZ = 1 };
+enum { H2_K_EXP = 0, H2_K_HELMHOLTZ = 1, H2_K_RATIONAL = 2 };
 typedef struct {
   int32_t kind;
   double param;
@@ -200,6 +229,24 @@ typedef struct {
    * "simple error compensation scheme" P:L496 being unspecified): eps_l at depth t is multiplied
    * by eps_decay^(leaf_depth - t); 1 = the uniform eps_l of R11                    [1.25] */
   double eps_decay;
+  /* Exact-order mode (SURVEY §8(c) parity contract 2): every step runs the
+   * exact-order kernels (sequential fma chains in the order the CPU reference states, correctly
+   * rounded division / sqrt, no tensor cores, no tree reductions): with H2_K_RATIONAL and the
+   * h2_omega stream the result is bitwise the C oracle's.  Slow by design (N <= ~10^4).
+   * Symmetric builds with the built-in dense-kernel sketch and built-in entries only.     [0]   */
+  int32_t exact_order;
+  /* Optional external Omega (SURVEY §8(b) omega_external): dev, n x (>= d_max) row-major with
+   * leading dim ld_omega_ext, tree-order rows; sample column c of the build is column c of this
+   * array instead of the h2_omega stream (e.g. Gaussian test matrices).  The caller owns it and
+   * keeps it alive during h2_build.  The int8 tensor-core sketch needs the stream (quarters), so
+   * the dense-kernel sketch runs on the FP64 DMMA path.                                [NULL] */
+  const double* omega_ext;
+  int64_t ld_omega_ext;
+  /* H2_TOL_LITERAL with norm <= 0: nu = ||K||_2 estimated by norm_iters power iterations through
+   * the sketch operator ("an approximate norm ... provided via sketching"; the
+   * start vector is column 0 of the h2_omega stream (seed, stream_id + 3)); the estimate is
+   * reported in h2_build_stats.norm_est.                                                  [10]  */
+  int32_t norm_iters;
 } h2_build_opts;
 void h2_build_opts_default(h2_build_opts* opts);
 
@@ -234,7 +281,7 @@ typedef struct {
 /* CPQR kernel variants (h2_build_stats.cpqr_variants; H2_CQ_VARIANT=warp|smem|global forces one
  * where it applies): one warp per panel (m <= 64), one CTA per panel with the panel in shared
  * memory, one CTA per panel with the panel in global memory (L1/L2 resident). */
-enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4 };
+enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4, H2_CQ_V_EXACT = 8 /* exact-order mode */ };
 
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU (§IV-B: "the batch count becomes roughly the number

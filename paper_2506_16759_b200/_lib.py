@@ -13,13 +13,13 @@ LIB_PATH = os.path.join(_HERE, "libh2.so")
 H2_OK, H2_ERR_INVALID_ARG, H2_ERR_OOM, H2_ERR_CUDA = 0, -1, -2, -3
 H2_ERR_CALLBACK, H2_ERR_NOT_CONVERGED, H2_ERR_NONFINITE = -5, -6, -7
 H2_DIST_CENTER, H2_DIST_BOX = 0, 1
-H2_K_EXP, H2_K_HELMHOLTZ = 0, 1
+H2_K_EXP, H2_K_HELMHOLTZ, H2_K_RATIONAL = 0, 1, 2
 H2_S_DENSE_KERNEL, H2_S_CALLBACK, H2_S_H2_LOWRANK, H2_S_DENSE_MATRIX = 0, 1, 2, 3
 H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK, H2_E_DENSE_MATRIX = 0, 1, 2, 3
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C = range(10)
 H2_SKETCH_OMEGA_QUARTERS = 1
-H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL = 1, 2, 4
+H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL, H2_CQ_V_EXACT = 1, 2, 4, 8
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
 H2_NPHASE = len(PHASES)
 
@@ -28,6 +28,12 @@ class h2_tree_info(C.Structure):
     _fields_ = [("n", C.c_int64), ("dim", C.c_int32), ("leaf_size", C.c_int32), ("leaf_depth", C.c_int32),
                 ("top_depth", C.c_int32), ("near_nnz", C.c_int64), ("far_nnz_total", C.c_int64),
                 ("csp", C.c_int32)]
+
+
+class h2_tree_desc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("dim", C.c_int32), ("leaf_depth", C.c_int32), ("coords", C.c_void_p),
+                ("perm", C.c_void_p), ("begin", C.c_void_p), ("end", C.c_void_p), ("near_nnz", C.c_int64),
+                ("near_pairs", C.c_void_p), ("far_nnz", C.c_void_p), ("far_pairs", C.c_void_p)]
 
 
 class h2_kernel(C.Structure):
@@ -68,7 +74,9 @@ class h2_build_opts(C.Structure):
     _fields_ = [("d_init", C.c_int32), ("d_blk", C.c_int32), ("d_max", C.c_int32), ("adaptive", C.c_int32),
                 ("tol_rule", C.c_int32), ("tol_safety", C.c_double), ("p_os", C.c_int32), ("norm", C.c_double),
                 ("max_rank", C.c_int32), ("seed", C.c_uint64), ("stream_id", C.c_uint32),
-                ("verify_probes", C.c_int32), ("verify_retries", C.c_int32), ("eps_decay", C.c_double)]
+                ("verify_probes", C.c_int32), ("verify_retries", C.c_int32), ("eps_decay", C.c_double),
+                ("exact_order", C.c_int32), ("omega_ext", C.c_void_p), ("ld_omega_ext", C.c_int64),
+                ("norm_iters", C.c_int32)]
 
 
 class h2_build_stats(C.Structure):
@@ -94,6 +102,7 @@ class h2_comm(C.Structure):
 _P = C.c_void_p
 SIGNATURES = {
     "h2_tree_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)]),
+    "h2_tree_import": (C.c_int, [C.POINTER(h2_tree_desc), C.POINTER(_P)]),
     "h2_tree_get_info": (C.c_int, [_P, C.POINTER(h2_tree_info)]),
     "h2_tree_export": (C.c_int, [_P, _P, _P, _P, _P]),
     "h2_tree_far_count": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64)]),

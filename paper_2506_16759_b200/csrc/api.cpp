@@ -205,6 +205,8 @@ struct Panel {
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                  double beta, cudaStream_t st);
 KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st);
+void apply_sketch_op(const h2_tree& T, const h2_sketch& S, const double* Om, int64_t ldo, int nc, double* Y,
+                     int64_t ldy, bool quarters, bool exact, cudaStream_t st);
 
 // Cluster ownership under a communicator (S§8(e)): cluster c of depth t (2^t clusters) belongs
 // to rank floor(c P / 2^t).  Ranges are contiguous and subtree-aligned (the children of an owned
@@ -290,6 +292,25 @@ struct Builder {
   int P = 1, R = 0;
   cudaStream_t user_st = nullptr;  // the caller's stream (st becomes the internal high-priority one)
   DArr<double> leaf_part;          // per-leaf sums of squares of the current draw
+  bool ex = false;                 // exact-order mode (opts.exact_order, exact.cu)
+
+  // Omega columns [c0, c0+nc) (all n rows) -> Od: the h2_omega stream, or the caller's array
+  void fill_omega(double* Od, int64_t ld, int c0, int nc, cudaStream_t s) {
+    if (o.omega_ext) {
+      if (nc > 0)
+        H2_CUDA(cudaMemcpy2DAsync(Od, ld * 8, o.omega_ext + c0, o.ld_omega_ext * 8, (size_t)nc * 8, T.n,
+                                  cudaMemcpyDeviceToDevice, s));
+    } else {
+      launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, s);
+    }
+  }
+  // the int8 tensor-core sketch needs the exactly representable stream (quarters)
+  bool quarters() const { return o.omega_ext == nullptr; }
+  void sketch_rows(const double* Od, int64_t ld, int nc, double* Yd, cudaStream_t s) {
+    if (ex) launch_exact_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, s);
+    else launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld,
+                             quarters(), s);
+  }
 
   Builder(const h2_tree& t, const h2_sketch& s, const h2_entry& e, double tl, const h2_build_opts& op,
           cudaStream_t stream, h2_matrix& h, const h2_comm* cm)
@@ -408,7 +429,7 @@ struct Builder {
     H2_CUDA(cudaEventCreate(&t0));
     H2_CUDA(cudaEventCreate(&t1));
     H2_CUDA(cudaEventRecord(t0, ss));
-    launch_omega(o.seed, o.stream_id, 0, T.n, c0, spec_w, pre.O.p, pre.ld, ss);
+    fill_omega(pre.O.p, pre.ld, c0, spec_w, ss);
     launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), pre.O.p, pre.ld, spec_w,
                         pre.Y.p + row_b() * pre.ld, pre.ld, true, ss);
     H2_CUDA(cudaEventRecord(t1, ss));
@@ -428,11 +449,11 @@ struct Builder {
   }
 
   void sketch_cols(double* Yd, double* Od, int64_t ld, int c0, int nc) {
-    launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
+    fill_omega(Od, ld, c0, nc, st);
     timer.end();
     timer.begin(H2_PH_SKETCH);
     // this rank's leaf rows only (Omega is regenerated for all rows on every rank)
-    launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, true, st);
+    sketch_rows(Od, ld, nc, Yd, st);
     entries_sketch += T.n * T.n * (int64_t)div_up(nc, spec_on ? spec_w : 64);
     sketch_columns += nc;
   }
@@ -471,7 +492,7 @@ struct Builder {
     } else if (S.kind == H2_S_DENSE_KERNEL) {
       sketch_cols(Yd, Od, ld, c0, nc);
     } else {
-      launch_omega(o.seed, o.stream_id, 0, T.n, c0, nc, Od, ld, st);
+      fill_omega(Od, ld, c0, nc, st);
       timer.end();
       timer.begin(H2_PH_SKETCH);
       sketch_columns += nc;
@@ -505,10 +526,54 @@ struct Builder {
     // summed in leaf order: bitwise the same for any number of GPUs
     const int nleaf = 1 << T.Dl;
     if (leaf_part.n < nleaf) leaf_part.alloc(nleaf, st);
-    launch_sumsq_leaf(Yd, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, nc, leaf_part.p, st);
+    if (ex) launch_exact_sumsq_leaf(Yd, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, nc, leaf_part.p, st);
+    else launch_sumsq_leaf(Yd, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, nc, leaf_part.p, st);
     if (comm) comm_allgather_clusters(comm, leaf_part.p, 8, T.Dl, [](int c) { return (int64_t)c; }, st);
-    launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
+    if (ex) launch_exact_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
+    else launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
     timer.end();
+  }
+
+  // nu ~ ||K||_2 by power iteration through the sketch operator ("an approximate
+  // norm ... provided via sketching"; literal rule with opts.norm <= 0): x = e/|e| with e column 0
+  // of the h2_omega stream (seed, stream_id + 3); y = K_blk x; nu = |y|; x = y (norm_iters times).
+  // Replicated on every rank (all rows), so every rank holds the same nu.
+  double estimate_norm() {
+    timer.begin(H2_PH_SKETCH);
+    const int nleaf = 1 << T.Dl;
+    DArr<double> x, y, part, acc;
+    DArr<int> nf;
+    x.alloc(T.n, st);
+    y.alloc(T.n, st);
+    part.alloc(nleaf, st);
+    acc.alloc(1, st);
+    nf.alloc(1, st);
+    launch_omega(o.seed, o.stream_id + 3, 0, T.n, 0, 1, x.p, 1, st);
+    auto norm2 = [&](const double* v) {
+      H2_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), st));
+      H2_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), st));
+      launch_sumsq_leaf(v, T.d_leaf_begin, 0, nleaf, 1, 0, 1, part.p, st);
+      launch_sumsq_total(part.p, nleaf, acc.p, nf.p, st);
+      double a = 0;
+      int bad = 0;
+      H2_CUDA(cudaMemcpyAsync(&a, acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      H2_CUDA(cudaMemcpyAsync(&bad, nf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      H2_CUDA(cudaStreamSynchronize(st));
+      if (bad) throw Error(H2_ERR_NONFINITE, "norm estimate: non-finite sketch sample");
+      return std::sqrt(a);
+    };
+    double nu = 0;
+    const int iters = std::max(1, o.norm_iters);
+    for (int it = 0; it < iters; ++it) {
+      const double nx = norm2(x.p);
+      if (!(nx > 0)) break;
+      launch_scale(x.p, T.n, 1, 1, 1.0 / nx, st);
+      apply_sketch_op(T, S, x.p, 1, 1, y.p, 1, false, ex, st);
+      nu = norm2(y.p);
+      std::swap(x, y);
+    }
+    timer.end();
+    return nu;
   }
 
   double eps_now(int t) {
@@ -590,7 +655,8 @@ struct Builder {
     a.Y = Yp;
     a.Om = Op;
     a.ldy = a.ldo = ld;
-    launch_bsr(a, st);
+    if (ex) launch_exact_bsr(a, st);
+    else launch_bsr(a, st);
     timer.end();
   }
 
@@ -649,7 +715,12 @@ struct Builder {
     a.k = L.d_k.p;
     a.perm = L.d_perm.p;
     a.cert = L.cert.p;
-    H.stats.cpqr_variants |= launch_cpqr(a, st);
+    if (ex) {
+      launch_exact_cpqr(a, st);
+      H.stats.cpqr_variants |= H2_CQ_V_EXACT;
+    } else {
+      H.stats.cpqr_variants |= launch_cpqr(a, st);
+    }
     timer.end();
     if (comm) comm_allgather_clusters(comm, L.d_k.p, 4, t, [](int c) { return (int64_t)c; }, st);
     L.k = download(L.d_k, L.nclus, st);
@@ -691,7 +762,8 @@ struct Builder {
     a.max_k = L.max_k;
     a.max_red = 0;
     for (int c = 0; c < L.nclus; ++c) a.max_red = std::max(a.max_red, L.m[c] - L.k[c]);
-    launch_id(a, st);
+    if (ex) launch_exact_id(a, st);
+    else launch_id(a, st);
     if (comm)   // skeletons I~ of every cluster (B generation of cross-rank pairs, parent Ibar)
       comm_allgather_clusters(comm, L.d_skel.p, 4, t,
                               [&](int c) { return c < L.nclus ? L.roff[c] : L.rtot; }, st);
@@ -1265,11 +1337,15 @@ struct Builder {
     H.Dl = Dl;
     H.n = T.n;
     H.lv.resize(Dl - top + 1);
+    ex = o.exact_order != 0;
     if (S.kind == H2_S_DENSE_KERNEL) {
       skp = tree_kernel(&T, S.kern, st);
-      spec_on = sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 && env_int("H2_SPEC", 1) != 0;
+      spec_on = !ex && quarters() && sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 &&
+                env_int("H2_SPEC", 1) != 0;
       spec_w = sketch_tc_pass_cols(skp.kind);
     }
+    if (o.tol_rule == H2_TOL_LITERAL && !(o.norm > 0)) o.norm = estimate_norm();
+    if (o.tol_rule == H2_TOL_LITERAL) H.stats.norm_est = o.norm;
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
     d = std::min(o.d_init, o.d_max);
     sumsq_acc.alloc(1, st);
@@ -1590,6 +1666,24 @@ h2_status h2_tree_build(const double* coords_host, int64_t n, int32_t dim, int32
   }
 }
 
+h2_status h2_tree_import(const h2_tree_desc* desc, h2_tree** out) {
+  if (!out) return (g_err = "h2_tree_import: out is NULL", H2_ERR_INVALID_ARG);
+  *out = nullptr;
+  try {
+    H2_REQUIRE(desc != nullptr, "h2_tree_import: desc is NULL");
+    auto* T = new h2_tree();
+    std::unique_ptr<h2_tree> guard(T);
+    tree_import_host(*T, *desc);
+    *out = guard.release();
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    g_err = "h2_tree_import: host out of memory";
+    return H2_ERR_OOM;
+  }
+}
+
 h2_status h2_tree_get_info(const h2_tree* T, h2_tree_info* info) {
   if (!T || !info) return (g_err = "h2_tree_get_info: NULL argument", H2_ERR_INVALID_ARG);
   info->n = T->n;
@@ -1659,6 +1753,10 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->verify_probes = 0;
   o->verify_retries = 2;
   o->eps_decay = 1.25;
+  o->exact_order = 0;
+  o->omega_ext = nullptr;
+  o->ld_omega_ext = 0;
+  o->norm_iters = 10;
 }
 
 h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end) {
@@ -1691,32 +1789,7 @@ double verify_impl(const h2_matrix& H, const h2_sketch& S, int q, uint64_t seed,
   H2_CUDA(cudaMemsetAsync(acc.p, 0, 2 * sizeof(double), st));
   H2_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), st));
   launch_omega(seed, sid, 0, T.n, 0, q, Om.p, q, st);
-  if (S.kind == H2_S_DENSE_KERNEL) {
-    launch_dense_sketch(tree_kernel(&T, S.kern, st), T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om.p, q, q, Yh.p, q, true, st);
-  } else if (S.kind == H2_S_DENSE_MATRIX) {
-    dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, Om.p, q, q, Yh.p, q, st);
-  } else if (S.kind == H2_S_H2_LOWRANK) {
-    matvec_impl(*S.base, Om.p, q, Yh.p, q, q, 1.0, 0.0, st);
-    if (S.rank > 0) {
-      DArr<double> scr;
-      scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * q, st);
-      launch_lowrank_sketch(S.U, S.ld_U, S.rank, Om.p, q, q, T.n, Yh.p, q, scr.p, st);
-    }
-  } else {
-    h2_sketch_req rq{};
-    rq.n = T.n;
-    rq.row_begin = 0;
-    rq.row_end = T.n;
-    rq.col0 = 0;
-    rq.ncols = q;
-    rq.omega = Om.p;
-    rq.ld_omega = q;
-    rq.y = Yh.p;
-    rq.ld_y = q;
-    rq.stream = st;
-    int rc = S.fn(S.ctx, &rq);
-    if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
-  }
+  apply_sketch_op(T, S, Om.p, q, q, Yh.p, q, true, false, st);
   launch_sumsq_leaf(Yh.p, T.d_leaf_begin, 0, nleaf, q, 0, q, part.p, st);
   launch_sumsq_total(part.p, nleaf, acc.p, nf.p, st);
   matvec_impl(H, Om.p, q, Yh.p, q, q, 1.0, -1.0, st);   // Yh = H Om_h - Y_h
@@ -1729,6 +1802,43 @@ double verify_impl(const h2_matrix& H, const h2_sketch& S, int q, uint64_t seed,
   H2_CUDA(cudaStreamSynchronize(st));
   if (bad) throw Error(H2_ERR_NONFINITE, "h2_verify: non-finite sample");
   return a[0] > 0 ? std::sqrt(a[1] / a[0]) : std::sqrt(a[1]);
+}
+
+}  // namespace
+
+namespace {
+// Y = K_blk(Om) for all n rows with any sketch operator (a-posteriori check, norm estimate);
+// quarters: Om is the h2_omega stream (tensor-core sketch allowed); exact: exact-order sketch
+void apply_sketch_op(const h2_tree& T, const h2_sketch& S, const double* Om, int64_t ldo, int q, double* Y,
+                     int64_t ldy, bool quarters, bool exact, cudaStream_t st) {
+  if (S.kind == H2_S_DENSE_KERNEL) {
+    const KernelParams kp = tree_kernel(&T, S.kern, st);
+    if (exact) launch_exact_sketch(kp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om, ldo, q, Y, ldy, st);
+    else launch_dense_sketch(kp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, Om, ldo, q, Y, ldy, quarters, st);
+  } else if (S.kind == H2_S_DENSE_MATRIX) {
+    dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, Om, ldo, q, Y, ldy, st);
+  } else if (S.kind == H2_S_H2_LOWRANK) {
+    matvec_impl(*S.base, Om, ldo, Y, ldy, q, 1.0, 0.0, st);
+    if (S.rank > 0) {
+      DArr<double> scr;
+      scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * q, st);
+      launch_lowrank_sketch(S.U, S.ld_U, S.rank, Om, ldo, q, T.n, Y, ldy, scr.p, st);
+    }
+  } else {
+    h2_sketch_req rq{};
+    rq.n = T.n;
+    rq.row_begin = 0;
+    rq.row_end = T.n;
+    rq.col0 = 0;
+    rq.ncols = q;
+    rq.omega = Om;
+    rq.ld_omega = ldo;
+    rq.y = Y;
+    rq.ld_y = ldy;
+    rq.stream = st;
+    int rc = S.fn(S.ctx, &rq);
+    if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+  }
 }
 
 void reset_matrix(h2_matrix& H) {
@@ -1782,7 +1892,12 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     H2_REQUIRE(tol >= 0 && std::isfinite(tol), "h2_build: tol must be finite and >= 0");
     H2_REQUIRE(o.d_init >= 1 && o.d_blk >= 1 && o.d_max >= o.d_init, "h2_build: need 1 <= d_init <= d_max, d_blk >= 1");
     H2_REQUIRE(o.tol_rule == H2_TOL_RMS || o.tol_rule == H2_TOL_LITERAL, "h2_build: bad tol_rule");
-    H2_REQUIRE(o.tol_rule != H2_TOL_LITERAL || o.norm > 0, "h2_build: literal tolerance needs opts.norm > 0");
+    H2_REQUIRE(o.tol_rule != H2_TOL_LITERAL || o.norm > 0 || (!nonsym && o.norm_iters >= 0),
+               "h2_build: literal tolerance needs opts.norm > 0 (or the power-iteration estimate, symmetric builds)");
+    H2_REQUIRE(!o.exact_order || (!nonsym && sketch->kind == H2_S_DENSE_KERNEL && entry->kind == H2_E_BUILTIN),
+               "h2_build: exact_order needs a symmetric build with the built-in dense-kernel sketch and entries");
+    H2_REQUIRE(!o.omega_ext || (!nonsym && o.ld_omega_ext >= o.d_max),
+               "h2_build: omega_ext needs ld_omega_ext >= d_max (symmetric builds)");
     H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
                    sketch->kind == H2_S_H2_LOWRANK ||
                    (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= tree->n),
@@ -1806,7 +1921,9 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     }
     for (const h2_kernel* k : {sketch->kind == H2_S_DENSE_KERNEL ? &sketch->kern : nullptr,
                                entry->kind == H2_E_BUILTIN ? &entry->kern : nullptr})
-      if (k) H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ) && k->param > 0, "h2_build: bad kernel");
+      if (k)
+        H2_REQUIRE((k->kind == H2_K_EXP || k->kind == H2_K_HELMHOLTZ || k->kind == H2_K_RATIONAL) && k->param > 0,
+                   "h2_build: bad kernel");
     // U V^T (V != U) is a non-symmetric operator
     H2_REQUIRE(nonsym || ((sketch->kind != H2_S_H2_LOWRANK || !sketch->V || sketch->V == sketch->U) &&
                           (entry->kind != H2_E_H2_LOWRANK || !entry->V || entry->V == entry->U)),
@@ -1938,7 +2055,8 @@ h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, i
     H2_REQUIRE(T && omega && y, "h2_dense_sketch: NULL argument");
     H2_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= T->n, "h2_dense_sketch: bad row range");
     H2_REQUIRE(ncols >= 0 && ld_omega >= ncols && ld_y >= ncols, "h2_dense_sketch: bad ncols / leading dims");
-    H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ) && kern.param > 0, "h2_dense_sketch: bad kernel");
+    H2_REQUIRE((kern.kind == H2_K_EXP || kern.kind == H2_K_HELMHOLTZ || kern.kind == H2_K_RATIONAL) && kern.param > 0,
+               "h2_dense_sketch: bad kernel");
     ensure_uploaded(T);
     launch_dense_sketch(tree_kernel(T, kern, (cudaStream_t)stream), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
                         ld_y, (flags & H2_SKETCH_OMEGA_QUARTERS) != 0, (cudaStream_t)stream);

@@ -48,6 +48,7 @@ struct KernelParams {
   double inv;     // 1/l for exp
   double rmax;    // upper bound of the scaled distance over the point set (|x-y|/l, k|x-y|); 0 = unknown
   double rmin;    // minimum distance of distinct points (unscaled; Helmholtz fixed-point scale); 0 = unknown
+  double l2;      // param^2 (rational test kernel)
 };
 
 inline KernelParams make_kernel(const h2_kernel& k, double diam = -1.0, double rmin = 0.0) {
@@ -57,7 +58,19 @@ inline KernelParams make_kernel(const h2_kernel& k, double diam = -1.0, double r
   p.inv = 1.0 / k.param;
   p.rmax = diam >= 0 ? diam * (k.kind == H2_K_EXP ? p.inv : k.param) : 0.0;
   p.rmin = rmin;
+  p.l2 = k.param * k.param;
   return p;
+}
+
+// Rational test kernel K = 1 / (1 + r^2 / l^2), r^2 = (dx*dx + dy*dy) + dz*dz, every operation
+// correctly rounded and never contracted (explicit _rn intrinsics): bitwise the value the C
+// oracle computes (DESIGN.md §3 exact-order specification; H2_K_RATIONAL).
+__device__ __forceinline__ double r2_exact(double xi, double yi, double zi, double xj, double yj, double zj) {
+  const double dx = __dadd_rn(xi, -xj), dy = __dadd_rn(yi, -yj), dz = __dadd_rn(zi, -zj);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+__device__ __forceinline__ double k_rational(double r2, double l2) {
+  return __ddiv_rn(1.0, __dadd_rn(1.0, __ddiv_rn(r2, l2)));
 }
 
 // exp(x) for x <= 0 in ~10 FP64 pipe operations (libdevice exp costs ~2.5x more, measured):

@@ -39,8 +39,12 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
         const int p = ri[i];
         const double xi = X[p], yi = Yc[p], zi = Zc[p];
         double* orow = out + (int64_t)i * nc + j0;
-        for (int j = lane; j < nj; j += 32)
-          orow[j] = kernel_of_r2<KIND>(dist2(xi, yi, zi, cx[j], cy[j], cz[j]), param, inv, tab);
+        if (KIND == H2_K_RATIONAL) {   // exact-order entries (inv carries l^2)
+          for (int j = lane; j < nj; j += 32) orow[j] = k_rational(r2_exact(xi, yi, zi, cx[j], cy[j], cz[j]), inv);
+        } else {
+          for (int j = lane; j < nj; j += 32)
+            orow[j] = kernel_of_r2<KIND>(dist2(xi, yi, zi, cx[j], cy[j], cz[j]), param, inv, tab);
+        }
       }
     }
   }
@@ -75,6 +79,8 @@ void launch_gen(const KernelParams& kp, const double* X, const double* Yc, const
   int grid = (int)std::min<int64_t>(a.nblocks, 148 * 32);
   if (kp.kind == H2_K_EXP)
     gen_kernel<H2_K_EXP><<<grid, 256, 0, st>>>(X, Yc, Zc, a, kp.param, kp.inv);
+  else if (kp.kind == H2_K_RATIONAL)
+    gen_kernel<H2_K_RATIONAL><<<grid, 256, 0, st>>>(X, Yc, Zc, a, kp.param, kp.l2);
   else
     gen_kernel<H2_K_HELMHOLTZ><<<grid, 256, 0, st>>>(X, Yc, Zc, a, kp.param, kp.inv);
   H2_CHECK_LAUNCH();

@@ -110,6 +110,7 @@ struct CpqrArgs {
 int launch_cpqr(const CpqrArgs& a, cudaStream_t st);
 
 // ID epilogue: X_c (m x k, U or [E1;E2]) from T = R11^{-1} R12 (R15); skeletons I~ (L224, L253)
+struct IdArgs;
 struct IdArgs {
   int32_t nclusters;      // clusters c_begin .. c_begin + nclusters - 1
   int32_t c_begin;
@@ -289,5 +290,16 @@ struct UpdateNsArgs {
 };
 void launch_update_ns(const UpdateNsArgs& a, bool coupling, int grid, cudaStream_t st);
 void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStream_t st);
+
+// ---- exact-order mode (exact.cu, --fmad=false): the C oracle's operation order
+void launch_exact_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                         int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Y, int64_t ldy,
+                         cudaStream_t st);
+void launch_exact_sumsq_leaf(const double* Y, const int64_t* leaf_begin, int cb, int ce, int64_t ld, int c0, int c1,
+                             double* part, cudaStream_t st);
+void launch_exact_sumsq_total(const double* part, int nleaf, double* acc, int* nonfinite, cudaStream_t st);
+void launch_exact_bsr(const BsrArgs& a, cudaStream_t st);
+void launch_exact_cpqr(const CpqrArgs& a, cudaStream_t st);
+void launch_exact_id(const IdArgs& a, cudaStream_t st);
 
 }  // namespace h2

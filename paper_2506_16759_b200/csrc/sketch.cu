@@ -244,6 +244,10 @@ void launch_dense_sketch(const KernelParams& kp, const double* X, const double* 
                          int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                          int64_t ldy, bool omega_quarters, cudaStream_t st) {
   if (row1 <= row0 || ncols <= 0) return;
+  if (kp.kind == H2_K_RATIONAL) {   // the exact-order test kernel has only the exact-order sketch
+    launch_exact_sketch(kp, X, Yc, Zc, n, row0, row1, Om, ldo, ncols, Yout, ldy, st);
+    return;
+  }
   // exp kernel with Omega in quarters (the h2 stream): exact int8 tensor-core contraction
   // (sketch_tc.cu); any other Omega, or H2_SK_TC=0, takes the DMMA path
   if (omega_quarters && sketch_tc_supported(kp) && env_int("H2_SK_TC", 1) != 0) {

@@ -323,6 +323,112 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
   lap("near csr");
 }
 
+// h2_tree_import: a partition built elsewhere (e.g. the CPU oracle), so that both paths consume
+// the SAME tree ("a hierarchical partitioning" is an input of
+// Algorithm 1).  Checked: perm is a permutation; the cluster ranges form a complete binary tree
+// (children split their parent contiguously); pair indices in range, no duplicates, symmetric
+// sets, no (s, s) far pair; the blocks' areas sum to n^2 (a necessary covering condition).
+void tree_import_host(h2_tree& T, const h2_tree_desc& D) {
+  const int64_t n = D.n;
+  const int dim = D.dim, Dl = D.leaf_depth;
+  H2_REQUIRE(n >= 1 && n < (int64_t(1) << 31), "h2_tree_import: need 1 <= n < 2^31");
+  H2_REQUIRE(dim >= 1 && dim <= 3, "h2_tree_import: dim must be 1, 2 or 3");
+  H2_REQUIRE(Dl >= 0 && Dl < 31 && (int64_t(1) << Dl) <= n, "h2_tree_import: need 0 <= leaf_depth, 2^leaf_depth <= n");
+  H2_REQUIRE(D.coords && D.perm && D.begin && D.end && D.near_pairs && D.far_nnz, "h2_tree_import: NULL array");
+  for (int64_t i = 0; i < n * dim; ++i) H2_REQUIRE(std::isfinite(D.coords[i]), "h2_tree_import: non-finite coordinate");
+  T.n = n;
+  T.dim = dim;
+  T.Dl = Dl;
+  T.eta = 0.0;
+  T.rule = -1;   // imported: admissibility rule unknown
+  {
+    std::vector<char> seen(n, 0);
+    T.perm.assign(D.perm, D.perm + n);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t p = T.perm[i];
+      H2_REQUIRE(p >= 0 && p < n && !seen[p], "h2_tree_import: perm is not a permutation of 0..n-1");
+      seen[p] = 1;
+    }
+  }
+  T.begin.assign(Dl + 1, {});
+  T.end.assign(Dl + 1, {});
+  for (int t = 0; t <= Dl; ++t) {
+    const int64_t nn = int64_t(1) << t;
+    T.begin[t].assign(D.begin + (nn - 1), D.begin + (2 * nn - 1));
+    T.end[t].assign(D.end + (nn - 1), D.end + (2 * nn - 1));
+  }
+  H2_REQUIRE(T.begin[0][0] == 0 && T.end[0][0] == n, "h2_tree_import: the root must hold [0, n)");
+  for (int t = 0; t < Dl; ++t)
+    for (int64_t c = 0; c < (int64_t(1) << t); ++c) {
+      const int64_t b = T.begin[t][c], e = T.end[t][c];
+      const int64_t m1 = T.end[t + 1][2 * c];
+      H2_REQUIRE(T.begin[t + 1][2 * c] == b && T.begin[t + 1][2 * c + 1] == m1 && T.end[t + 1][2 * c + 1] == e &&
+                     b <= m1 && m1 <= e,
+                 "h2_tree_import: children must split their parent's index range contiguously");
+    }
+  T.leaf_size = 0;
+  for (int64_t c = 0; c < (int64_t(1) << Dl); ++c)
+    T.leaf_size = std::max<int32_t>(T.leaf_size, (int32_t)(T.end[Dl][c] - T.begin[Dl][c]));
+  T.xt.resize(n);
+  T.yt.resize(n);
+  T.zt.resize(n);
+  double lo[3] = {1e308, 1e308, 1e308}, hi[3] = {-1e308, -1e308, -1e308};
+  for (int64_t i = 0; i < n; ++i) {
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < dim; ++a) v[a] = D.coords[T.perm[i] * dim + a];
+    T.xt[i] = v[0];
+    T.yt[i] = v[1];
+    T.zt[i] = v[2];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], v[a]);
+      hi[a] = std::max(hi[a], v[a]);
+    }
+  }
+  T.diam = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                     (hi[2] - lo[2]) * (hi[2] - lo[2]));
+  auto size_of = [&](int t, int64_t c) { return T.end[t][c] - T.begin[t][c]; };
+  long double area = 0;
+  auto load = [&](const int32_t* pr, int64_t nnz, int t, bool strict, PairCSR& C) {
+    const int64_t nn = int64_t(1) << t;
+    std::vector<std::pair<int32_t, int32_t>> pairs(nnz);
+    for (int64_t e = 0; e < nnz; ++e) {
+      const int32_t s = pr[2 * e], b = pr[2 * e + 1];
+      H2_REQUIRE(s >= 0 && s < nn && b >= 0 && b < nn, "h2_tree_import: pair index out of range");
+      H2_REQUIRE(!strict || s != b, "h2_tree_import: an admissible pair (s, s)");
+      pairs[e] = {s, b};
+      area += (long double)size_of(t, s) * (long double)size_of(t, b);
+    }
+    make_csr(C, pairs, (int32_t)nn, strict);
+    for (int64_t r = 0; r < nn; ++r)
+      for (int32_t e = C.ptr[r]; e < C.ptr[r + 1]; ++e) {
+        H2_REQUIRE(e == C.ptr[r] || C.idx[e] > C.idx[e - 1], "h2_tree_import: duplicate pair");
+        const int32_t b = C.idx[e];
+        auto it = std::lower_bound(C.idx.begin() + C.ptr[b], C.idx.begin() + C.ptr[b + 1], (int32_t)r);
+        H2_REQUIRE(it != C.idx.begin() + C.ptr[b + 1] && *it == (int32_t)r, "h2_tree_import: pair set not symmetric");
+      }
+  };
+  load(D.near_pairs, D.near_nnz, Dl, false, T.near);
+  T.far.assign(Dl + 1, PairCSR{});
+  T.top = -1;
+  for (int t = 0; t <= Dl; ++t) {
+    const int64_t nnz = D.far_nnz[t];
+    H2_REQUIRE(nnz >= 0 && (nnz == 0 || (D.far_pairs && D.far_pairs[t])), "h2_tree_import: far pairs missing");
+    load(nnz ? D.far_pairs[t] : nullptr, nnz, t, true, T.far[t]);
+    if (nnz > 0 && T.top < 0) T.top = t;
+  }
+  H2_REQUIRE(area == (long double)n * (long double)n, "h2_tree_import: the blocks do not tile the n x n matrix");
+  T.csp = 0;
+  for (int t = 0; t <= Dl; ++t)
+    for (int64_t r = 0; r < (int64_t(1) << t); ++r) {
+      int row = T.far[t].ptr[r + 1] - T.far[t].ptr[r];
+      if (t == Dl) row += T.near.ptr[r + 1] - T.near.ptr[r];
+      T.csp = std::max(T.csp, row);
+    }
+  T.D_off.assign(T.near.nuniq() + 1, 0);
+  for (int64_t q = 0; q < T.near.nuniq(); ++q)
+    T.D_off[q + 1] = T.D_off[q] + size_of(Dl, T.near.us[q]) * size_of(Dl, T.near.ub[q]);
+}
+
 namespace {
 template <class V>
 typename V::value_type* upload(const V& v) {

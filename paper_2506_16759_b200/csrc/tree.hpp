@@ -47,4 +47,5 @@ struct h2_tree {
 };
 
 void tree_build_host(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+void tree_import_host(h2_tree& T, const h2_tree_desc& desc);
 void tree_upload(h2_tree& T);

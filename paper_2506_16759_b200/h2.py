@@ -13,7 +13,7 @@ import torch
 from . import _lib as L
 from ._lib import check, lib
 
-KERNELS = {"exp": L.H2_K_EXP, "helmholtz": L.H2_K_HELMHOLTZ}
+KERNELS = {"exp": L.H2_K_EXP, "helmholtz": L.H2_K_HELMHOLTZ, "rational": L.H2_K_RATIONAL}
 
 
 def _ptr(t):
@@ -46,14 +46,16 @@ class Tree:
     points: n x dim float64 in original order (host).  The tree keeps tree-ordered
     coordinates on the current CUDA device for the built-in kernels."""
 
-    def __init__(self, points, leaf_size=64, eta=0.7, dist_rule="center"):
+    def __init__(self, points, leaf_size=64, eta=0.7, dist_rule="center", _handle=None):
         P = np.ascontiguousarray(points, dtype=np.float64)
         if P.ndim == 1:
             P = P[:, None]
         self.points = P
-        h = C.c_void_p()
-        check(lib.h2_tree_build(P.ctypes.data_as(C.c_void_p), P.shape[0], P.shape[1], leaf_size, float(eta),
-                                L.H2_DIST_CENTER if dist_rule == "center" else L.H2_DIST_BOX, C.byref(h)))
+        h = _handle
+        if h is None:
+            h = C.c_void_p()
+            check(lib.h2_tree_build(P.ctypes.data_as(C.c_void_p), P.shape[0], P.shape[1], leaf_size, float(eta),
+                                    L.H2_DIST_CENTER if dist_rule == "center" else L.H2_DIST_BOX, C.byref(h)))
         self._h = h
         info = L.h2_tree_info()
         check(lib.h2_tree_get_info(h, C.byref(info)))
@@ -70,6 +72,28 @@ class Tree:
         self.begin = [b[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
         self.end = [e[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
         self._near = self._far = None
+
+    @classmethod
+    def from_partition(cls, points, perm, begin, end, near, far):
+        """A partition built elsewhere (h2_tree_import): perm (tree -> original index), begin/end
+        per depth (lists of int arrays, depth 0 = root), near (ordered leaf pairs, k x 2), far
+        (per depth, ordered admissible pairs, k_t x 2)."""
+        P = np.ascontiguousarray(points, dtype=np.float64)
+        if P.ndim == 1:
+            P = P[:, None]
+        Dl = len(begin) - 1
+        perm = np.ascontiguousarray(perm, np.int64)
+        b = np.ascontiguousarray(np.concatenate([np.asarray(x, np.int64) for x in begin]))
+        e = np.ascontiguousarray(np.concatenate([np.asarray(x, np.int64) for x in end]))
+        nr = np.ascontiguousarray(np.asarray(near, np.int32).reshape(-1, 2))
+        fr = [np.ascontiguousarray(np.asarray(f, np.int32).reshape(-1, 2)) for f in far]
+        fnnz = np.array([len(f) for f in fr], np.int64)
+        fptr = (C.c_void_p * (Dl + 1))(*[f.ctypes.data if len(f) else None for f in fr])
+        d = L.h2_tree_desc(P.shape[0], P.shape[1], Dl, P.ctypes.data, perm.ctypes.data, b.ctypes.data,
+                           e.ctypes.data, len(nr), nr.ctypes.data, fnnz.ctypes.data, C.cast(fptr, C.c_void_p))
+        h = C.c_void_p()
+        check(lib.h2_tree_import(C.byref(d), C.byref(h)))
+        return cls(P, _handle=h)
 
     @property
     def near(self):
@@ -270,7 +294,7 @@ def _stats_dict(s):
 
 
 def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, stream=None, update=None, comm=None,
-          h2_sketch=None, dense=None, nonsym=False, **opts):
+          h2_sketch=None, dense=None, nonsym=False, omega=None, **opts):
     """Algorithm 1 on the current device.
 
     kernel: (kind, param) built-in kernel used for the entry evaluator (and the dense sketch
@@ -289,11 +313,17 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     keyword and must write K^T omega for transpose=1; ``dense`` A is used as given (A^T via DGEMM).
     comm: optional ``dist.Comm`` (one process per GPU): the construction is sharded
     by subtrees (h2_build_dist); call ``H.allgather(comm)`` before matvec / block export.
+    omega: optional (n, >= d_max) float64 CUDA tensor, tree-order rows: an external Omega
+    (h2_build_opts.omega_ext) instead of the h2_omega stream.
     opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
-    tol_safety, p_os, norm, max_rank, seed, stream_id)."""
+    tol_safety, p_os, norm, max_rank, seed, stream_id, exact_order, norm_iters, eps_decay)."""
     o = build_opts(**opts)
     kern = _kernel(*kernel)
     keep = []
+    if omega is not None:
+        assert omega.is_cuda and omega.dtype == torch.float64 and omega.shape[0] == tree.n and omega.stride(1) == 1
+        keep.append(omega)
+        o.omega_ext, o.ld_omega_ext = omega.data_ptr(), omega.stride(0)
     sk = L.h2_sketch()
     sk.kern = kern
     V = None

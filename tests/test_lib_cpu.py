@@ -76,3 +76,32 @@ def test_tree_errors_are_reported():
     bad[3, 1] = np.nan
     with pytest.raises(H2Error, match="non-finite"):
         Tree(bad, 4)
+
+
+def test_tree_import_roundtrip_and_validation():
+    """h2_tree_import: the oracle's partition imported into libh2 exports back
+    unchanged; malformed partitions are refused with INVALID_ARG (host logic, no device)."""
+    import paper_2506_16759_b200 as g
+    X = uniform_points(3000, 3, 4)
+    tree = geometry.build_cluster_tree(X, 64)
+    part = geometry.build_partition(tree, 0.7)
+    T = g.Tree.from_partition(X, tree.perm, tree.begin, tree.end, part.near, part.far)
+    assert np.array_equal(T.perm, tree.perm)
+    assert np.array_equal(T.near, part.near)
+    assert all(np.array_equal(a, b) for a, b in zip(T.far, part.far))
+    assert all(np.array_equal(T.begin[t], tree.begin[t]) for t in range(tree.leaf_depth + 1))
+    assert T.top_depth == part.top_depth()
+    bad_perm = tree.perm.copy()
+    bad_perm[0] = bad_perm[1]
+    far_asym = [f.copy() for f in part.far]
+    t0 = part.top_depth()
+    far_asym[t0] = far_asym[t0][far_asym[t0][:, 0] != far_asym[t0][0, 0]]   # drop one row's pairs
+    ends = [e.copy() for e in tree.end]
+    ends[1][0] += 1
+    for args in [(bad_perm, tree.begin, tree.end, part.near, part.far),
+                 (tree.perm, tree.begin, tree.end, part.near, far_asym),
+                 (tree.perm, tree.begin, ends, part.near, part.far),
+                 (tree.perm, tree.begin, tree.end, part.near[:-1], part.far)]:
+        with pytest.raises(g.H2Error) as e:
+            g.Tree.from_partition(X, *args)
+        assert e.value.status == -1
