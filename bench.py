@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cov3d_256k")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-c3", action="store_true", help="skip the N = 2^21 (configs[2]) extra timing")
     return p.parse_args()
 
 
@@ -90,64 +92,136 @@ def workload_cfg(name):
 
 
 # ------------------------------------------------------------------------------------------
-# reference arm: the CPU oracle on a bounded sample, extrapolated to the full workload
+# reference arm / cpu_baseline: the C oracle (oracle/c/h2oracle.c, OpenMP on the host cores)
 # ------------------------------------------------------------------------------------------
-def oracle_sample_seconds(w, X, samples_hint, budget_rows=96, leaves=16):
-    """Oracle time for the workload, extrapolated from a bounded sample:
-    (a) sketch: K(rows, :) Omega for `budget_rows` rows and one 32-column block, scaled by
-        N / budget_rows x (samples / 32);
-    (b) construction proper: the oracle's leaf-level work (D generation, BSR subtraction, CPQR
-        row ID) for `leaves` leaves at d = samples, scaled by #leaves x 2 (inner levels hold about
-        as many panel rows as the leaf level)."""
-    from oracle import geometry, kernels, rng, cpqr
-    n = X.shape[0]
+SKETCH_SAMPLE_ROWS = 128   # rows of the oracle's own dense sketch timed per step (scaled by N / rows)
+TABLE_COLS = 256           # sketch columns supplied as a table to the oracle's construction proper
+
+
+class OracleSetup:
+    """Untimed set-up of the oracle timing (SURVEY §8(d) "Oracle timing"): the oracle's own
+    KD-tree and partition (oracle/geometry.py), and the sketch Y = K Omega of the first
+    TABLE_COLS columns of the Omega stream as a TABLE (data shared, code not: computed by plain
+    torch FP64 -- cdist without the matmul shortcut, exp, DGEMM -- on the GPU when present; no
+    libh2 code), so that the oracle's construction proper runs on the real sketch of the workload
+    with its own adaptive loop and sample count."""
+
+    def __init__(self, w, X, table=True):
+        from oracle import geometry, c_h2
+        self.c_h2 = c_h2
+        t0 = time.perf_counter()
+        self.tree = geometry.build_cluster_tree(X, w["leaf"])
+        self.part = geometry.build_partition(self.tree, 0.7)
+        self.ta = c_h2.TreeArrays(self.tree, self.part, X)
+        self.w = w
+        self.n = X.shape[0]
+        self.Om = c_h2.omega(1, 0, 0, self.n, 0, TABLE_COLS)
+        self.Y = self._table() if table else None
+        self.setup_s = time.perf_counter() - t0
+
+    def _table(self):
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        P = torch.from_numpy(self.ta.pts).to(dev)
+        Om = torch.from_numpy(self.Om).to(dev)
+        Y = torch.empty((self.n, TABLE_COLS), dtype=torch.float64, device=dev)
+        blk = 4096 if dev == "cuda" else 256
+        kind, p = self.w["kernel"], self.w["param"]
+        for r0 in range(0, self.n, blk):
+            r = torch.cdist(P[r0:r0 + blk], P, compute_mode="donot_use_mm_for_euclid_dist")
+            if kind == "exp":
+                K = torch.exp(-r / p)
+            else:
+                K = torch.where(r > 0, torch.cos(p * r) / torch.where(r > 0, r, 1.0), 0.0)
+            Y[r0:r0 + blk] = K @ Om
+            del r, K
+        out = Y.cpu().numpy()
+        del Y, Om, P
+        if dev == "cuda":
+            torch.cuda.empty_cache()
+        return out
+
+    def step(self, threads=0):
+        """One reference step: (a) the oracle's construction proper (Algorithm 1 after the sketch:
+        D/B generation, BSR, CPQR convergence tests, updateSamples replays, ID, shrink, projection,
+        every level) on the table, measured in full; (b) the oracle's own dense sketch for the
+        draws its adaptive loop made (d_init, then d_blk per extra round), timed on
+        SKETCH_SAMPLE_ROWS rows and scaled by N / rows (every row costs the same N kernel
+        evaluations and N x nc multiply-adds).  Returns seconds (construction + extrapolated
+        sketch) and the details."""
+        c_h2, w = self.c_h2, self.w
+        opts = dict(d_init=32, d_blk=32, d_max=512, threads=threads)
+        R = c_h2.build(self.ta, w["kernel"], w["param"], w["tol"], y_table=self.Y, **opts)
+        t_cons = R.seconds["total"] - R.seconds["sketch"]          # table copies are not sketch work
+        draws = [(0, 32)] + [(c0, 32) for c0 in range(32, R.samples, 32)]
+        r0 = self.n // 2 - SKETCH_SAMPLE_ROWS // 2
+        t_sk = 0.0
+        for c0, nc in draws:
+            Om = np.ascontiguousarray(self.Om[:, c0:c0 + nc])
+            t1 = time.perf_counter()
+            c_h2.dense_sketch(self.ta, w["kernel"], w["param"], Om, rows=(r0, r0 + SKETCH_SAMPLE_ROWS))
+            t_sk += time.perf_counter() - t1
+        factor = self.n / SKETCH_SAMPLE_ROWS
+        return t_cons + t_sk * factor, {"construction_s": t_cons, "sketch_sample_s": t_sk, "sketch_factor": factor,
+                                        "sketch_extrapolated_s": t_sk * factor, "samples": R.samples,
+                                        "draws": len(draws), "phase_s": {k: round(v, 4) for k, v in R.seconds.items()}}
+
+
+def oracle_c1_seconds():
+    """BASELINE configs[0] (C1): the full C oracle (own sketch) end to end, all threads and one
+    thread; median of 3."""
+    from oracle import geometry, c_h2
+    from synth import WORKLOADS
+    w = WORKLOADS["cov2d_1k"]
+    X = w["points"]()
     tree = geometry.build_cluster_tree(X, w["leaf"])
-    Dl = tree.leaf_depth
-    op = kernels.KernelOperator(w["kernel"], w["param"], X[tree.perm])
-    om32 = rng.omega_block(1, 0, 0, n, 0, 32)
-    rows = np.arange(0, n, max(1, n // budget_rows))[:budget_rows]
-    t0 = time.perf_counter()
-    op.sketch_rows(om32, rows)
-    t_sk = (time.perf_counter() - t0) * (n / len(rows)) * (samples_hint / 32)
-    # leaf-level sample (partition of the whole tree is needed for N_tau; build it untimed)
-    part = geometry.build_partition(tree, 0.7)
-    d = samples_hint
-    Om = rng.omega_block(1, 0, 0, n, 0, d)
-    rng_of = lambda c: np.arange(tree.begin[Dl][c], tree.end[Dl][c])
-    lv = np.linspace(0, (1 << Dl) - 1, leaves).astype(int)
-    Ys = {c: np.random.default_rng(c).standard_normal((len(rng_of(c)), d)) for c in lv}  # stand-in samples
-    t0 = time.perf_counter()
-    for c in lv:
-        Yl = Ys[c].copy()
-        for b in part.near_of(c):
-            Yl -= op.entry(rng_of(c), rng_of(int(b))) @ Om[rng_of(int(b))]
-        cpqr.row_id(Yl, 1e-7 * np.linalg.norm(Yl) / np.sqrt(Yl.shape[0]))
-    t_cp = (time.perf_counter() - t0) * ((1 << Dl) / len(lv)) * 2.0
-    return t_sk + t_cp, {"sketch_s": t_sk, "construction_s": t_cp, "rows": len(rows), "leaves": len(lv)}
+    ta = c_h2.TreeArrays(tree, geometry.build_partition(tree, 0.7), X)
+    out = {}
+    for th, name in ((0, "all_threads_s"), (1, "one_thread_s")):
+        c_h2.build(ta, "exp", 0.2, 1e-6, threads=th)
+        out[name] = float(statistics.median(c_h2.build(ta, "exp", 0.2, 1e-6, threads=th).seconds["total"]
+                                            for _ in range(3)))
+    out["samples"] = c_h2.build(ta, "exp", 0.2, 1e-6).samples
+    return out
+
+
+def cpu_baseline_record(value, info, setup, steps_timed, cores):
+    return {"value": value, "unit": "s", "cores": cores, "kind": "extrapolated",
+            "sample": (f"per step: the C oracle's construction proper on the FULL workload (all levels, its own "
+                       f"adaptive loop: {info['samples']} samples) on the sketch supplied as a table, measured "
+                       f"({info['construction_s']:.2f} s), + its own dense sketch for its {info['draws']} draws timed "
+                       f"on {SKETCH_SAMPLE_ROWS} rows ({info['sketch_sample_s']:.2f} s) x N/rows = "
+                       f"{info['sketch_factor']:.0f} (extrapolated {info['sketch_extrapolated_s']:.1f} s)"),
+            "timed_s_per_step": info["construction_s"] + info["sketch_sample_s"],
+            "construction_s": info["construction_s"], "sketch_extrapolated_s": info["sketch_extrapolated_s"],
+            "extrapolation_factor_sketch": info["sketch_factor"], "oracle_samples": info["samples"],
+            "oracle_phase_s": info["phase_s"], "setup_untimed_s": round(setup.setup_s, 1),
+            "steps_timed": steps_timed}
 
 
 def run_reference(args, w, rank):
     if rank != 0:
         return
+    from oracle import c_h2
     X = w["points"]()
-    samples_hint = 160   # GPU samples at configs[1] (profiles/r1_bench_*.json); scales the oracle sample
-    cores = len(os.sched_getaffinity(0))
-    for _ in range(args.warmup):
-        oracle_sample_seconds(w, X, samples_hint, budget_rows=8, leaves=2)
+    cores = c_h2.max_threads()
+    setup = OracleSetup(w, X)
+    for _ in range(min(args.warmup, 1)):   # warm-up: one untimed step (page-in, thread pool)
+        setup.step()
     vals, info = [], None
     for _ in range(args.steps):
-        v, info = oracle_sample_seconds(w, X, samples_hint)
+        v, info = setup.step()
         vals.append(v)
     value = float(statistics.median(vals))
-    sample = (f"per step: oracle dense sketch of {info['rows']} rows x 32 samples scaled to N rows x "
-              f"{samples_hint} samples + oracle leaf work (D gen, BSR, CPQR ID) of {info['leaves']} leaves "
-              f"scaled to all leaves x2 for inner levels")
+    cpu = cpu_baseline_record(value, info, setup, args.steps, cores)
+    cpu["c1_full_oracle"] = oracle_c1_seconds()
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": args.workload, "n": int(X.shape[0]), "leaf": w["leaf"], "tol": w["tol"],
-                      "kernel": w["kernel"], "sketch": "dense-kernel"},
-           "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+           "config": {"workload": args.workload, "n": int(X.shape[0]), "leaf": w["leaf"], "eta": 0.7, "tol": w["tol"],
+                      "kernel": f"{w['kernel']}({w['param']})", "sketch": "dense-kernel", "d_init": 32, "d_blk": 32,
+                      "d_max": 512},
+           "cpu_baseline": cpu,
            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -265,11 +339,11 @@ def run_ours(args, w, rank, world, local_rank):
     if rank != 0:
         return
     cpu = None
-    if world == 1:
-        v, info = oracle_sample_seconds(w, X, st["samples"])
-        cpu = {"value": v, "unit": "s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": f"oracle dense sketch of {info['rows']} rows x 32 samples scaled to N x {st['samples']} "
-                         f"samples + oracle leaf work of {info['leaves']} leaves scaled to all leaves x2"}
+    if world == 1 and not args.no_cpu:
+        from oracle import c_h2
+        setup = OracleSetup(w, X)
+        v, info = setup.step()
+        cpu = cpu_baseline_record(v, info, setup, 1, c_h2.max_threads())
     out = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
@@ -308,7 +382,66 @@ def run_ours(args, w, rank, world, local_rank):
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    if world == 1 and not args.no_c3 and args.workload == "cov3d_256k":
+        del H
+        out["north_star_c3"] = time_c3(g, torch, stream, flush)
     print(json.dumps(out), flush=True)
+
+
+def time_c3(g, torch, stream, flush, steps=2):
+    """BASELINE configs[2] / north-star size (N = 2^21, 3D exp covariance, tol 1e-6) on ONE GPU,
+    driver-timed inside the bench run (extra key; `value` stays configs[1]): build time (CUDA
+    events, 1 warm-up + `steps` timed builds, L2 flushed), samples, per-phase times, the sketch
+    roofline, and the error against the ORACLE's K X on 48 sampled rows of 16 probes (the oracle
+    evaluates those rows one by one; oracle/kernels.py)."""
+    from synth import WORKLOADS
+    from oracle import kernels
+    w = WORKLOADS["cov3d_2m"]
+    g._lib.lib.h2_cache_trim()
+    torch.cuda.empty_cache()
+    X = w["points"]()
+    n = X.shape[0]
+    t0 = time.perf_counter()
+    T = g.Tree(X, w["leaf"], 0.7)
+    tree_s = time.perf_counter() - t0
+    kern = (w["kernel"], w["param"])
+    opts = dict(adaptive=True, d_init=32, d_blk=32, d_max=512)
+    H = g.build(T, kern, w["tol"], **opts)
+    del H
+    times, stats = [], []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        H = g.build(T, kern, w["tol"], **opts)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stats.append(H.stats)
+        if len(times) < steps:
+            del H
+    st = stats[-1]
+    P = np.random.default_rng(2).standard_normal((n, 16))
+    HX = H.matvec(torch.from_numpy(P).cuda()).cpu().numpy()
+    rows = np.sort(np.random.default_rng(9).choice(n, 48, replace=False))
+    KX = kernels.KernelOperator(w["kernel"], w["param"], X[T.perm]).sketch_rows(P, rows)
+    err = float(np.linalg.norm(HX[rows] - KX) / np.linalg.norm(KX))
+    sk_launches = max(st["entries_sketch"] // (n * n), 1)
+    per_launch = float(np.mean([s["t_phase_ms"]["sketch"] for s in stats])) / sk_launches
+    achieved = float(n) * n * F_EVAL / (per_launch * 1e-3) / 1e12
+    ms = float(np.mean(times))
+    res = {"workload": "cov3d_2m", "n": n, "build_s": ms / 1e3, "step_ms": [round(t, 1) for t in times],
+           "samples": st["samples"], "verified_error_oracle_rows": err,
+           "phase_ms": {k: round(v, 1) for k, v in st["t_phase_ms"].items()},
+           "construction_proper_ms": round(ms - st["t_phase_ms"]["sketch"], 1),
+           "entries_evaluated_per_s": (st["entries_D"] + st["entries_B"]) / (ms / 1e3),
+           "sketch_roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PIPE_TOPS,
+                               "unit": "TOP/s (FP64 pipe ops)", "frac": achieved / FP64_PIPE_TOPS,
+                               "per_launch_ms": per_launch, "launches": int(sk_launches)},
+           "device_bytes": H.device_bytes(), "host_tree_s": round(tree_s, 2), "gpus": 1}
+    del H, T
+    g._lib.lib.h2_cache_trim()
+    return res
 
 
 def main():

@@ -86,10 +86,17 @@ typedef struct {
   int64_t ld_ext;
   const double* dense;                      /* H2O_K_TABLE operator, n x ld_dense (host)        */
   int64_t ld_dense;
+  /* sketch supplied as a table (SURVEY §8(d) "the oracle's construction proper, timed with the
+   * sketch supplied as a table"): Y(:, c) = y_table column c for c < table_cols; a draw beyond
+   * the table fails (status -2).  The Omega columns are still the oracle's own stream. */
+  const double* y_table;
+  int64_t ld_table;
+  int32_t table_cols;
 } h2o_opts;
 
 typedef struct {
-  int32_t status;                           /* 0 ok, -6 not converged, -1 bad argument          */
+  int32_t status;                           /* 0 ok, -6 not converged, -1 bad argument,
+                                               -2 sketch table exhausted                        */
   int32_t samples, top, leaf_depth, failed_depth;
   int32_t rounds[H2O_MAXD];
   double eps;
@@ -358,6 +365,7 @@ typedef struct {
   double* D;
   double* B[H2O_MAXD];
   double acc;             /* ||Y||_F^2 over all draws */
+  int table_short;        /* a draw went beyond the sketch table */
   h2o_result* res;
 } bld_t;
 
@@ -431,7 +439,17 @@ static void draw(bld_t* b, double* Y, double* O, int64_t ld, int c0, int nc) {
     h2o_omega(b->o->seed, b->o->stream_id, 0, n, c0, nc, O, ld);
   }
   double t0 = wtime();
-  sketch_rows(&b->K, n, 0, n, O, ld, nc, Y, ld);
+  if (b->o->y_table) {
+    if (c0 + nc > b->o->table_cols) {
+      b->table_short = 1;
+      nc = b->o->table_cols > c0 ? b->o->table_cols - c0 : 0;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+      for (int j = 0; j < nc; ++j) Y[i * ld + j] = b->o->y_table[i * b->o->ld_table + c0 + j];
+  } else {
+    sketch_rows(&b->K, n, 0, n, O, ld, nc, Y, ld);
+  }
   b->res->t_sketch += wtime() - t0;
   const int nleaf = 1 << b->Dl;
   double* part = (double*)xcalloc(nleaf, sizeof(double));
@@ -762,6 +780,11 @@ h2o_result* h2o_build(const h2o_tree* T, int32_t kind, double param, double tol,
       }
       update_samples(b, t, &cur, o->d_blk);
       d = b->d = d + o->d_blk;
+      if (b->table_short) {
+        res->status = -2;
+        res->failed_depth = t;
+        goto out;
+      }
     }
     res->rounds[t] = rounds;
     commit(b, t);                                      /* lines 221-224 / 250-253 */

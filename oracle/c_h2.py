@@ -43,7 +43,8 @@ class _Opts(C.Structure):
                 ("tol_rule", C.c_int32), ("tol_safety", C.c_double), ("norm", C.c_double),
                 ("eps_decay", C.c_double), ("p_os", C.c_int32), ("max_rank", C.c_int32), ("seed", C.c_uint64),
                 ("stream_id", C.c_uint32), ("threads", C.c_int32), ("omega_ext", C.c_void_p),
-                ("ld_ext", C.c_int64), ("dense", C.c_void_p), ("ld_dense", C.c_int64)]
+                ("ld_ext", C.c_int64), ("dense", C.c_void_p), ("ld_dense", C.c_int64), ("y_table", C.c_void_p),
+                ("ld_table", C.c_int64), ("table_cols", C.c_int32)]
 
 
 class _Result(C.Structure):
@@ -184,7 +185,7 @@ class Result:
 
 def build(ta: TreeArrays, kind, param, tol, d_init=32, d_blk=32, d_max=512, adaptive=True, tol_rule="rms",
           tol_safety=0.04, norm=0.0, eps_decay=1.25, p_os=10, max_rank=0, seed=1, stream_id=0, threads=0,
-          omega_ext=None, dense=None):
+          omega_ext=None, dense=None, y_table=None):
     """Algorithm 1 in the C oracle.  Defaults = libh2's h2_build_opts_default (R9-R12,
     R31).  omega_ext: optional (n, >= d_max) float64 Omega (tree-order rows) instead of the
     Philox stream; kind "table" with dense = (n, n) tree-order operator.  Raises NotConverged at
@@ -199,6 +200,10 @@ def build(ta: TreeArrays, kind, param, tol, d_init=32, d_blk=32, d_max=512, adap
     if omega_ext is not None:
         keep = np.ascontiguousarray(omega_ext, dtype=np.float64)
         o.omega_ext, o.ld_ext = keep.ctypes.data, keep.shape[1]
+    keep3 = None
+    if y_table is not None:   # the sketch supplied as a table (n, c): Y columns 0..c-1
+        keep3 = np.ascontiguousarray(y_table, dtype=np.float64)
+        o.y_table, o.ld_table, o.table_cols = keep3.ctypes.data, keep3.shape[1], keep3.shape[1]
     keep2 = None
     if dense is not None:
         keep2 = np.ascontiguousarray(dense, dtype=np.float64)
@@ -209,6 +214,8 @@ def build(ta: TreeArrays, kind, param, tol, d_init=32, d_blk=32, d_max=512, adap
     try:
         if r.status == -6:
             raise NotConverged(f"C oracle: d_max reached at depth {r.failed_depth}")
+        if r.status == -2:
+            raise ValueError(f"C oracle: the sketch table ran out of columns at depth {r.failed_depth}")
         if r.status != 0:
             raise ValueError(f"C oracle: status {r.status}")
         return Result(r, ta)
