@@ -102,8 +102,8 @@ class OracleSetup:
     """Untimed set-up of the oracle timing (SURVEY §8(d) "Oracle timing"): the oracle's own
     KD-tree and partition (oracle/geometry.py), and the sketch Y = K Omega of the first
     TABLE_COLS columns of the Omega stream as a TABLE (data shared, code not: computed by plain
-    torch FP64 -- cdist without the matmul shortcut, exp, DGEMM -- on the GPU when present; no
-    libh2 code), so that the oracle's construction proper runs on the real sketch of the workload
+    torch FP64 -- elementwise distances, exp, DGEMM -- on the GPU when present; no libh2 code),
+    so that the oracle's construction proper runs on the real sketch of the workload
     with its own adaptive loop and sample count."""
 
     def __init__(self, w, X, table=True):
@@ -128,7 +128,12 @@ class OracleSetup:
         blk = 4096 if dev == "cuda" else 256
         kind, p = self.w["kernel"], self.w["param"]
         for r0 in range(0, self.n, blk):
-            r = torch.cdist(P[r0:r0 + blk], P, compute_mode="donot_use_mm_for_euclid_dist")
+            Q = P[r0:r0 + blk]
+            # r^2 = (dx*dx + dy*dy) + dz*dz elementwise (no |x|^2 + |y|^2 - 2xy cancellation)
+            r2 = (Q[:, None, 0] - P[None, :, 0]) ** 2
+            r2 += (Q[:, None, 1] - P[None, :, 1]) ** 2
+            r2 += (Q[:, None, 2] - P[None, :, 2]) ** 2
+            r = torch.sqrt_(r2)
             if kind == "exp":
                 K = torch.exp(-r / p)
             else:
@@ -246,8 +251,10 @@ def run_ours(args, w, rank, world, local_rank):
         # level, sketch rows of its leaves, its blocks; per-level NCCL all-gathers of ranks,
         # skeleton indices and Omega rows
         import torch.distributed as dist
-        from paper_2506_16759_b200.dist import Comm
-        comm = Comm()
+        from paper_2506_16759_b200.dist import Comm, NcclComm
+        # NCCL: libh2's in-library communicator (h2_comm_init, stream-ordered broadcast groups);
+        # gloo (ranks sharing one GPU): the torch.distributed callback communicator
+        comm = NcclComm() if dist.get_backend() == "nccl" else Comm()
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > L2 (126 MB)
     stream = torch.cuda.current_stream()
@@ -354,7 +361,7 @@ def run_ours(args, w, rank, world, local_rank):
                    "eps_rule": "s*tol*rho*gamma^(Dl-t), s=0.04, gamma=1.25 (DESIGN.md R31)",
                    "sketch_format": "int8 tcgen05, 6-byte fixed-point K (2^-47 grid), 160-column pass (R32)",
                    "parallelism": (f"subtree shards x{world} (sketch rows, clusters per level; "
-                                   f"{dist.get_backend().upper() if dist else ''} all-gathers"
+                                   f"{'in-library NCCL' if dist and dist.get_backend() == 'nccl' else 'gloo'} all-gathers"
                                    f"{'' if dist and dist.get_backend() == 'nccl' else ', ranks share a GPU'})")
                    if world > 1 else "1 GPU",
                    "l2": "256 MiB flush before every timed step; working set (N x d_max x 16 B = 2 GiB) > L2"},

@@ -37,6 +37,7 @@ typedef enum {
   H2_ERR_INVALID_ARG = -1,
   H2_ERR_OOM = -2,
   H2_ERR_CUDA = -3,
+  H2_ERR_NCCL = -4,          /* NCCL unavailable or an NCCL call failed (h2_comm_*)         */
   H2_ERR_CALLBACK = -5,      /* a user sketch/entry callback returned non-zero             */
   H2_ERR_NOT_CONVERGED = -6, /* adaptive sampling hit d_max; stats.failed_depth says where */
   H2_ERR_NONFINITE = -7      /* the sketch produced a non-finite sample                    */
@@ -302,9 +303,28 @@ typedef int (*h2_allgatherv_fn)(void* ctx, void* buf, const int64_t* counts, con
                                 void* stream);
 typedef struct {
   int32_t rank, nranks;
-  h2_allgatherv_fn allgatherv;
+  h2_allgatherv_fn allgatherv;   /* caller's communicator (e.g. torch.distributed), or NULL      */
   void* ctx;
+  void* nccl;                    /* library-owned NCCL communicator (h2_comm_init), used when
+                                    allgatherv is NULL: grouped ncclBroadcast per segment,
+                                    stream-ordered, no host synchronisation                    */
 } h2_comm;
+
+/* In-library NCCL communicator (one process per GPU; the NCCL library is loaded at run time,
+ * libnccl.so.2 -- the one torch already loaded, if any).  Rank 0 calls h2_comm_get_unique_id
+ * and sends the 128 bytes to every rank out of band (torch.distributed in the Python binding);
+ * every rank then calls h2_comm_init collectively on its current device.  The returned h2_comm
+ * is owned by the library (h2_comm_free).  Errors: H2_ERR_NCCL (library missing / NCCL error),
+ * INVALID_ARG. */
+h2_status h2_comm_get_unique_id(void* id128);
+h2_status h2_comm_init(const void* id128, int32_t rank, int32_t nranks, h2_comm** out);
+void h2_comm_free(h2_comm* comm);
+/* The collective libh2 runs per level (exposed for tests and users): in-place all-gather of byte
+ * segments [displs[r], displs[r] + counts[r]) of the device buffer buf, segment r valid on rank r
+ * on entry, on every rank on return; counts/displs host arrays of nranks entries; stream-ordered.
+ * Uses comm->allgatherv when set, else the NCCL communicator. */
+h2_status h2_comm_allgatherv(const h2_comm* comm, void* buf, const int64_t* counts, const int64_t* displs,
+                             void* stream);
 
 /* Owned cluster range [*begin, *end) of `rank` among `nranks` at a depth with n_clusters
  * clusters (host logic, no device).  Errors: INVALID_ARG. */

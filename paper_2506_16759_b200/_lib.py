@@ -10,7 +10,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libh2.so")
 
-H2_OK, H2_ERR_INVALID_ARG, H2_ERR_OOM, H2_ERR_CUDA = 0, -1, -2, -3
+H2_OK, H2_ERR_INVALID_ARG, H2_ERR_OOM, H2_ERR_CUDA, H2_ERR_NCCL = 0, -1, -2, -3, -4
 H2_ERR_CALLBACK, H2_ERR_NOT_CONVERGED, H2_ERR_NONFINITE = -5, -6, -7
 H2_DIST_CENTER, H2_DIST_BOX = 0, 1
 H2_K_EXP, H2_K_HELMHOLTZ, H2_K_RATIONAL = 0, 1, 2
@@ -95,7 +95,8 @@ ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64
 
 
 class h2_comm(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("allgatherv", ALLGATHERV_FN), ("ctx", C.c_void_p)]
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("allgatherv", ALLGATHERV_FN), ("ctx", C.c_void_p),
+                ("nccl", C.c_void_p)]
 
 
 # every symbol include/h2.h declares, with its ctypes signature
@@ -119,6 +120,10 @@ SIGNATURES = {
     "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
                                 C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),
     "h2_matrix_allgather": (C.c_int, [_P, C.POINTER(h2_comm), _P]),
+    "h2_comm_get_unique_id": (C.c_int, [_P]),
+    "h2_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.POINTER(h2_comm))]),
+    "h2_comm_free": (None, [C.POINTER(h2_comm)]),
+    "h2_comm_allgatherv": (C.c_int, [C.POINTER(h2_comm), _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P]),
     "h2_dist_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "h2_matvec": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P]),
     "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64,

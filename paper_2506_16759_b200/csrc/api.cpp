@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "alloc.hpp"
+#include "comm.hpp"
 #include "kernels.hpp"
 #include "tree.hpp"
 
@@ -223,6 +224,10 @@ void comm_allgather(const h2_comm* comm, void* base, const std::vector<int64_t>&
   int64_t tot = 0;
   for (int64_t c : counts) tot += c;
   if (tot == 0) return;
+  if (!comm->allgatherv) {   // in-library NCCL: stream-ordered, no host synchronisation
+    nccl_allgatherv(comm->nccl, comm->nranks, base, counts.data(), displs.data(), st);
+    return;
+  }
   // the segments are produced by kernels on `st`; a host-staged communicator reads them on the
   // host side, so complete them first (a few times per level)
   H2_CUDA(cudaStreamSynchronize(st));
@@ -1933,7 +1938,8 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
       H2_REQUIRE(!b || (!b->nonsym && !b->partial), "h2_build: the H2+low-rank base must be a complete symmetric H2");
     const bool dist = comm && comm->nranks > 1;
     if (comm)
-      H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks && (!dist || comm->allgatherv),
+      H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks &&
+                     (!dist || comm->allgatherv || comm->nccl),
                  "h2_build_dist: bad communicator");
     H2_REQUIRE(!dist || (sketch->kind != H2_S_H2_LOWRANK && entry->kind != H2_E_H2_LOWRANK),
                "h2_build_dist: H2 + low-rank operators are single-GPU only");
@@ -2003,7 +2009,7 @@ h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream) {
   try {
     H2_REQUIRE(H, "h2_matrix_allgather: NULL matrix");
     if (!H->partial) return H2_OK;
-    H2_REQUIRE(comm && comm->nranks == H->nranks && comm->rank == H->rank && comm->allgatherv,
+    H2_REQUIRE(comm && comm->nranks == H->nranks && comm->rank == H->rank && (comm->allgatherv || comm->nccl),
                "h2_matrix_allgather: communicator does not match the build");
     cudaStream_t st = (cudaStream_t)stream;
     const h2_tree& T = *H->tree;
@@ -2157,6 +2163,62 @@ int64_t h2_matrix_device_bytes(const h2_matrix* H) {
 }
 
 void h2_free(h2_matrix* H) { delete H; }
+
+h2_status h2_comm_get_unique_id(void* id128) {
+  try {
+    H2_REQUIRE(id128, "h2_comm_get_unique_id: NULL id");
+    h2::nccl_unique_id(id128);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_comm_init(const void* id128, int32_t rank, int32_t nranks, h2_comm** out) {
+  if (!out) return (g_err = "h2_comm_init: out is NULL", H2_ERR_INVALID_ARG);
+  *out = nullptr;
+  try {
+    H2_REQUIRE(id128 && nranks >= 1 && rank >= 0 && rank < nranks, "h2_comm_init: bad argument");
+    auto* c = new h2_comm{};
+    c->rank = rank;
+    c->nranks = nranks;
+    c->allgatherv = nullptr;
+    c->ctx = nullptr;
+    try {
+      c->nccl = h2::nccl_comm_init(id128, rank, nranks);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+void h2_comm_free(h2_comm* c) {
+  if (!c) return;
+  try {
+    h2::nccl_comm_free(c->nccl);
+  } catch (const Error&) {
+  }
+  delete c;
+}
+
+h2_status h2_comm_allgatherv(const h2_comm* comm, void* buf, const int64_t* counts, const int64_t* displs,
+                             void* stream) {
+  try {
+    H2_REQUIRE(comm && counts && displs && (comm->allgatherv || comm->nccl) && comm->nranks >= 1,
+               "h2_comm_allgatherv: bad argument");
+    std::vector<int64_t> c(counts, counts + comm->nranks), d(displs, displs + comm->nranks);
+    for (int r = 0; r < comm->nranks; ++r) H2_REQUIRE(c[r] >= 0 && d[r] >= 0, "h2_comm_allgatherv: negative segment");
+    comm_allgather(comm, buf, c, d, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
 
 int64_t h2_cache_bytes(void) { return (int64_t)h2::cache_bytes_held(); }
 void h2_cache_trim(void) { h2::cache_trim(); }

@@ -141,3 +141,45 @@ class Comm:
                 return 1
         self._cb = L.ALLGATHERV_FN(_agv)
         self.struct = L.h2_comm(self.rank, self.world, self._cb, None)
+
+
+class NcclComm:
+    """libh2's in-library NCCL communicator (h2_comm_init; one process per GPU): the 128-byte NCCL
+    unique id of rank 0 is broadcast with torch.distributed, every rank initialises NCCL on its
+    current device, and the per-level all-gathers of the sharded construction run inside libh2
+    as stream-ordered NCCL broadcast groups (no Python callback, no host synchronisation)."""
+
+    def __init__(self, group=None):
+        from . import _lib as L
+        self._L = L
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        idb = C.create_string_buffer(128)
+        if self.rank == 0:
+            L.check(L.lib.h2_comm_get_unique_id(idb))
+        obj = [bytes(idb.raw) if self.rank == 0 else None]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        idb = C.create_string_buffer(obj[0], 128)
+        p = C.POINTER(L.h2_comm)()
+        L.check(L.lib.h2_comm_init(idb, self.rank, self.world, C.byref(p)))
+        self._p = p
+        self.struct = p.contents
+
+    def allgatherv(self, buf, counts, displs, stream=None):
+        """In-place all-gather of byte segments of a CUDA tensor (h2_comm_allgatherv)."""
+        import torch
+        P = self.world
+        cnt = (C.c_int64 * P)(*counts)
+        dsp = (C.c_int64 * P)(*displs)
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        self._L.check(self._L.lib.h2_comm_allgatherv(self._p, C.c_void_p(buf.data_ptr()), cnt, dsp, C.c_void_p(s)))
+
+    def close(self):
+        if getattr(self, "_p", None):
+            self._L.lib.h2_comm_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        self.close()
