@@ -391,13 +391,15 @@ struct Builder {
     return std::min<int64_t>(std::max<int64_t>(l, dneed), full);
   }
 
-  void grow(Panel& P, int dneed) {
+  // widen panel P to >= dneed columns, keeping its first `keep` columns (default: d)
+  void grow(Panel& P, int dneed, int keep = -1) {
     if (dneed <= P.ld) return;
+    if (keep < 0) keep = d;
     Panel Q;
     Q.alloc(P.rows, ld_for(P.rows, dneed), st);
-    if (P.rows > 0 && d > 0) {
-      H2_CUDA(cudaMemcpy2DAsync(Q.Y.p, Q.ld * 8, P.Y.p, P.ld * 8, (size_t)d * 8, P.rows, cudaMemcpyDeviceToDevice, st));
-      H2_CUDA(cudaMemcpy2DAsync(Q.O.p, Q.ld * 8, P.O.p, P.ld * 8, (size_t)d * 8, P.rows, cudaMemcpyDeviceToDevice, st));
+    if (P.rows > 0 && keep > 0) {
+      H2_CUDA(cudaMemcpy2DAsync(Q.Y.p, Q.ld * 8, P.Y.p, P.ld * 8, (size_t)keep * 8, P.rows, cudaMemcpyDeviceToDevice, st));
+      H2_CUDA(cudaMemcpy2DAsync(Q.O.p, Q.ld * 8, P.O.p, P.ld * 8, (size_t)keep * 8, P.rows, cudaMemcpyDeviceToDevice, st));
     }
     P = std::move(Q);
   }
@@ -956,6 +958,178 @@ struct Builder {
     }
   }
 
+  // ================================================================ eager sweep of sketch passes
+  //   One tensor-core sketch pass computes up to spec_w stream columns at the cost
+  // of one evaluation of K (R27).  Instead of banking the extra columns and replaying every d_blk
+  // block later through all committed depths (leaf BSR, shrink + projection and inner BSR, once
+  // per block and depth: updateSamples L216-217/L246-247), every column of a pass is swept up
+  // with the panel: each BSR / shrink launch of a depth covers the panel's full width dw, and a
+  // convergence round that needs the next d_blk samples finds them already in its panel.  The
+  // samples CONSUMED are unchanged (the first d columns; the tolerance scale adds each d_blk
+  // block's sum of squares when the block is consumed, from per-leaf partials taken right after
+  // the sketch), and the arithmetic is column-separable, so the H^2 is bitwise the block-by-block
+  // (lazy) result -- H2_EAGER=0 selects the lazy driver (tests compare the two).
+  int dw = 0;                                           // columns present in the current panel
+  std::vector<std::pair<int, DArr<double>>> blk_part;   // consumption block start -> per-leaf partials
+
+  // consumption blocks: [0, d_init), then d_blk columns each
+  int block_end(int b0) const { return b0 == 0 ? std::min(o.d_init, o.d_max) : std::min(b0 + o.d_blk, o.d_max); }
+  // width of the pass starting at stream column c0 (a block boundary): whole blocks, as many as
+  // one tensor-core pass evaluates K for (spec_w), at least one block
+  int pass_width(int c0) const {
+    int e = block_end(c0);
+    if (S.kind == H2_S_DENSE_KERNEL && spec_on)
+      while (e < o.d_max && block_end(e) - c0 <= spec_w) e = block_end(e);
+    return e - c0;
+  }
+  // Omega + K_blk(Omega) for stream columns [c0, c0+nc) into (Yd, Od) (pointers at column c0) and
+  // the per-leaf sums of squares of every consumption block of the pass (R10)
+  void draw_pass(double* Yd, double* Od, int64_t ld, int c0, int nc) {
+    timer.begin(H2_PH_RAND);
+    if (S.kind == H2_S_DENSE_KERNEL) {
+      sketch_cols(Yd, Od, ld, c0, nc);
+    } else {
+      fill_omega(Od, ld, c0, nc, st);
+      timer.end();
+      timer.begin(H2_PH_SKETCH);
+      sketch_columns += nc;
+      if (S.kind == H2_S_DENSE_MATRIX) {
+        dense_matrix_sketch(S.A, S.ld_A, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, st);
+      } else if (S.kind == H2_S_H2_LOWRANK) {
+        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
+        DArr<double> scr;
+        scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
+        launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
+      } else {
+        h2_sketch_req rq{};
+        rq.n = T.n;
+        rq.row_begin = row_b();
+        rq.row_end = row_e();
+        rq.col0 = c0;
+        rq.ncols = nc;
+        rq.omega = Od;
+        rq.ld_omega = ld;
+        rq.y = Yd + row_b() * ld;
+        rq.ld_y = ld;
+        rq.stream = st;
+        int rc = S.fn(S.ctx, &rq);
+        if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+      }
+    }
+    timer.end();
+    timer.begin(H2_PH_MISC);
+    const int nleaf = 1 << T.Dl;
+    for (int b0 = c0; b0 < c0 + nc; b0 = block_end(b0)) {
+      const int b1 = block_end(b0);
+      DArr<double> part;
+      part.alloc(nleaf, st);
+      if (ex) launch_exact_sumsq_leaf(Yd + (b0 - c0), T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, b1 - b0, part.p, st);
+      else launch_sumsq_leaf(Yd + (b0 - c0), T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ld, 0, b1 - b0, part.p, st);
+      if (comm) comm_allgather_clusters(comm, part.p, 8, T.Dl, [](int c) { return (int64_t)c; }, st);
+      blk_part.emplace_back(b0, std::move(part));
+    }
+    timer.end();
+  }
+  // the block starting at column b0 is consumed: ||Y||_F^2 += its sum of squares
+  void consume(int b0) {
+    for (auto it = blk_part.begin(); it != blk_part.end(); ++it)
+      if (it->first == b0) {
+        timer.begin(H2_PH_MISC);
+        if (ex) launch_exact_sumsq_total(it->second.p, 1 << T.Dl, sumsq_acc.p, nonfinite.p, st);
+        else launch_sumsq_total(it->second.p, 1 << T.Dl, sumsq_acc.p, nonfinite.p, st);
+        timer.end();
+        blk_part.erase(it);
+        return;
+      }
+    throw Error(H2_ERR_INVALID_ARG, "internal: sample block " + std::to_string(b0) + " was never drawn");
+  }
+  // the next pass (columns [dw, dw + W)) swept up through the committed depths Dl..t+1 and
+  // appended to the panel of depth t
+  void extend(int t) {
+    const int c0 = dw, W = pass_width(dw);
+    grow(cur, dw + W, dw);
+    if (t == T.Dl) {
+      draw_pass(cur.Y.p + c0, cur.O.p + c0, cur.ld, c0, W);
+      bsr(T.Dl, cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
+    } else {
+      Panel src;
+      src.alloc(T.n, W, st);
+      draw_pass(src.Y.p, src.O.p, W, c0, W);
+      bsr(T.Dl, src.Y.p, src.O.p, W, W);
+      for (int u = T.Dl; u > t; --u) {
+        if (u - 1 == t) {
+          shrink(u, src.Y.p, src.O.p, src.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
+          allgather_skel_rows(u, cur.O.p + c0, cur.ld, W);
+          bsr(t, cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
+        } else {
+          Panel dst;
+          dst.alloc(H.L(u).rtot, W, st);
+          shrink(u, src.Y.p, src.O.p, src.ld, dst.Y.p, dst.O.p, dst.ld, W);
+          allgather_skel_rows(u, dst.O.p, dst.ld, W);
+          bsr(u - 1, dst.Y.p, dst.O.p, dst.ld, W);
+          src = std::move(dst);
+        }
+      }
+    }
+    dw += W;
+  }
+
+  void run_eager() {
+    const int Dl = T.Dl;
+    const int top = T.top < 0 ? Dl : T.top;
+    d = std::min(o.d_init, o.d_max);
+    dw = pass_width(0);
+    // line 1: Y = K_blk(Omega) for the first pass into the leaf panel (Y^loc in place)
+    cur.alloc(T.n, ld_for(T.n, dw), st);
+    draw_pass(cur.Y.p, cur.O.p, cur.ld, 0, dw);
+    consume(0);
+    timer.mark(Dl);
+    gen_D();                                        // line 212
+    setup_level(Dl);
+    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, dw);          // line 213, every column of the pass
+    for (int t = Dl; t >= top; --t) {
+      if (t < Dl) {
+        timer.mark(t);
+        setup_level(t);
+        bsr(t, cur.Y.p, cur.O.p, cur.ld, dw);       // lines 240-243
+      }
+      Level& L = H.L(t);
+      int rounds = 0;
+      double eps = 0;
+      while (true) {
+        eps = eps_now(t);
+        cpqr(t, eps);                               // first d columns
+        ++rounds;
+        if (!o.adaptive) break;
+        bool conv = true;
+        const int pos = (o.tol_rule == H2_TOL_RMS) ? o.p_os : 0;
+        for (int c = 0; c < L.nclus && conv; ++c) conv = (L.m[c] <= d) || (L.k[c] <= d - 1 - pos);
+        if (conv) break;
+        if (d + o.d_blk > o.d_max) {
+          H.stats.failed_depth = t;
+          throw Error(H2_ERR_NOT_CONVERGED, "adaptive sampling reached d_max=" + std::to_string(o.d_max) +
+                                                " at depth " + std::to_string(t));
+        }
+        if (d + o.d_blk > dw) extend(t);            // updateSamples: a new pass, swept up to depth t
+        consume(d);
+        d += o.d_blk;
+      }
+      H.stats.rounds[t] = rounds;
+      H.stats.eps = eps;
+      commit(t);                                    // lines 221-224 / 250-253
+      Panel next;
+      if (t > top) {                                // lines 222-223 / 251-252, every column
+        next.alloc(L.rtot, ld_for(L.rtot, dw), st);
+        shrink(t, cur.Y.p, cur.O.p, cur.ld, next.Y.p, next.O.p, next.ld, dw);
+        allgather_skel_rows(t, next.O.p, next.ld, dw);
+      }
+      gen_B(t);                                     // line 258
+      cur = std::move(next);
+    }
+    timer.mark(-1);
+    finish(top, Dl);
+  }
+
   // ================================================================ non-symmetric construction
   // h2_build_nonsym ("the extension to the non-symmetric case is straightforward";
   // DESIGN.md R29; oracle/h2_nonsym.py).  Two panels per depth: cur = (Y^l: samples of K Omega,
@@ -1352,17 +1526,28 @@ struct Builder {
     if (o.tol_rule == H2_TOL_LITERAL && !(o.norm > 0)) o.norm = estimate_norm();
     if (o.tol_rule == H2_TOL_LITERAL) H.stats.norm_est = o.norm;
     if (E.kind == H2_E_BUILTIN) ekp = make_kernel(E.kern);
-    d = std::min(o.d_init, o.d_max);
     sumsq_acc.alloc(1, st);
     nonfinite.alloc(1, st);
     H2_CUDA(cudaMemsetAsync(sumsq_acc.p, 0, sizeof(double), st));
     H2_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+    if (env_int("H2_EAGER", 1) != 0) {   // DESIGN.md §5b; H2_EAGER=0: block-by-block replays
+      run_eager();
+      return;
+    }
+    d = std::min(o.d_init, o.d_max);
 
     // line 1: Y = K_blk(Omega) into the leaf panel (leaf Y^loc is computed in place)
     cur.alloc(T.n, ld_for(T.n, d), st);
     draw(cur.Y.p, cur.O.p, cur.ld, 0, d);
     // line 212: D_{tau,b} = K(I_tau, I_b), one unique block per unordered pair
     timer.mark(Dl);
+    gen_D();
+    setup_level(Dl);
+    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
+    run_levels(top, Dl);
+  }
+
+  void gen_D() {
     H.D.alloc(T.D_off.back(), st);
     {
       GenArgs g{};
@@ -1401,8 +1586,9 @@ struct Builder {
         gen(g);
       }
     }
-    setup_level(Dl);
-    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
+  }
+
+  void run_levels(int top, int Dl) {
     for (int t = Dl; t >= top; --t) {
       if (t < Dl) {
         timer.mark(t);

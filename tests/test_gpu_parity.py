@@ -287,3 +287,29 @@ def test_helmholtz_sketch_with_coincident_points():
     ref = op.sampler(Om)
     y = g.dense_sketch(T, torch.from_numpy(Om).cuda(), ("helmholtz", 3.0), omega_quarters=True).cpu().numpy()
     assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("case,opts", [("cov3d_5000", dict(d_init=16, d_blk=16)),
+                                       ("cov3d_5000", dict(d_init=32, d_blk=24)),
+                                       ("cov3d_5000", dict()),
+                                       ("ie_grid16", dict(d_init=16, d_blk=8)),
+                                       ("cov2d_1k", dict(d_init=8, d_blk=8, d_max=400))])
+def test_eager_sweep_bitwise(monkeypatch, case, opts):
+    """Eager sweep: every column of a sketch pass goes up with the panel (one
+    BSR / shrink launch per depth over the whole pass) instead of block-by-block updateSamples
+    replays -- bitwise the lazy build (ranks, skeletons, bases, B, D, certificates, samples)."""
+    mk, kind, p, leaf, tol = CASES[case]
+    X = mk()
+    T = g.Tree(X, leaf)
+    monkeypatch.setenv("H2_EAGER", "0")
+    H0 = g.build(T, (kind, p), tol, **opts)
+    monkeypatch.setenv("H2_EAGER", "1")
+    H1 = g.build(T, (kind, p), tol, **opts)
+    assert H0.samples == H1.samples
+    assert H0.stats["rounds"] == H1.stats["rounds"]
+    for t in range(H0.top_depth, T.leaf_depth + 1):
+        assert np.array_equal(H0.rank(t), H1.rank(t))
+        assert np.array_equal(H0._export(g._lib.H2_X_SKEL, t, np.int32), H1._export(g._lib.H2_X_SKEL, t, np.int32))
+        for w in (g._lib.H2_X_BASIS, g._lib.H2_X_B, g._lib.H2_X_CERT):
+            assert np.array_equal(H0._export(w, t), H1._export(w, t)), (t, w)
+    assert np.array_equal(H0._export(g._lib.H2_X_D), H1._export(g._lib.H2_X_D))
