@@ -722,6 +722,7 @@ struct Builder {
     a.k = L.d_k.p;
     a.perm = L.d_perm.p;
     a.cert = L.cert.p;
+    a.rows = L.rows;
     if (ex) {
       launch_exact_cpqr(a, st);
       H.stats.cpqr_variants |= H2_CQ_V_EXACT;

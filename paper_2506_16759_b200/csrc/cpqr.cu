@@ -229,6 +229,176 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   }
 }
 
+__host__ __device__ inline size_t cq1_head_doubles(int max_m) { return ((size_t)max_m * 5 + 15) / 16 * 2; }
+
+// One barrier per pivot step (round 2).  Panel rows are never swapped: a pivot row is retired in
+// place (its R column is final: entries < i were fixed by earlier reflectors, entry i becomes
+// beta one step later, when nobody reads it any more), and the factored panel is written to W in
+// pivot order at the end (position q <- row perm[q]; redundant rows in ascending row order).
+// Every warp rebuilds the reflector of the pivot row redundantly (same data, same order: the same
+// bits in every warp), so no second barrier publishes it: per step one __syncthreads separates
+// the trailing update (rows j: w = tau (A(j,i) + <A(p,i+1:), A(j,i+1:)> / den), A(j,i) -= w,
+// A(j,r) -= (w / den) A(p,r), next norm from the updated entries, local Top2) from the merge of
+// the per-warp pivot candidates.  Decisions as R12-R14 (max recomputed norm, ties -> lowest row,
+// dlarfg signs), the certificates as before.  SMEM: panel in shared memory; else in `scratch`
+// (global, L1/L2 resident), gathered into W at the end.
+template <bool SMEM, int NT>
+__global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restrict__ scratch) {
+  constexpr int NW = NT / 32;
+  constexpr int RPP = NT / CQ_TPR;
+  extern __shared__ double smem[];
+  const int c = a.c_begin + blockIdx.x;
+  const int m = a.m[c];
+  const int d = a.d;
+  const int LD = SMEM ? cq_ld(d) : d;
+  int* perm = reinterpret_cast<int*>(smem);                          // max_m
+  unsigned char* retired = reinterpret_cast<unsigned char*>(perm + a.max_m);
+  double* spanel = smem + cq1_head_doubles(a.max_m);                 // after perm + retired
+  __shared__ Top2 red[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
+  const int64_t off = a.poff[c];
+  double* A = SMEM ? spanel : scratch + off * d;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += NT) {
+    const int64_t j = e / d;
+    A[j * LD + (e - j * d)] = a.Y[(off + j) * a.ldy + (e - j * d)];
+  }
+  for (int j = threadIdx.x; j < m; j += NT) retired[j] = 0;
+  __syncthreads();
+  auto row_sum = [&](double x) {
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    return x;
+  };
+  auto warp_best = [&](Top2 t) {
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      Top2 u;
+      u.v = __shfl_xor_sync(0xffffffffu, t.v, o);
+      u.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+      u.s = __shfl_xor_sync(0xffffffffu, t.s, o);
+      t = top2_merge(t, u);
+    }
+    return t;
+  };
+  {
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    for (int j0 = 0; j0 < m; j0 += RPP) {
+      const int j = j0 + rloc;
+      double q = 0.0;
+      if (j < m)
+        for (int r = sub; r < d; r += CQ_TPR) q = fma(A[(int64_t)j * LD + r], A[(int64_t)j * LD + r], q);
+      q = row_sum(q);
+      if (j < m) loc = top2_merge(loc, Top2{sqrt(q), j, -1.0});
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red[warp] = loc;
+  }
+  const int kfull = min(d, m);
+  const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
+  double min_gap = INFINITY, margin = INFINITY;
+  int k = 0, p_prev = -1;
+  double beta_prev = 0.0;
+  for (int i = 0;; ++i) {
+    __syncthreads();
+    if (threadIdx.x == 0 && p_prev >= 0) {   // the previous pivot's R diagonal; nobody reads it now
+      A[(int64_t)p_prev * LD + (i - 1)] = beta_prev;
+      retired[p_prev] = 1;
+      perm[i - 1] = p_prev;
+    }
+    Top2 t = lane < NW ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
+    t = warp_top2(t);
+    if (i >= m) break;
+    if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    if (i == kcap || !(t.v > a.eps)) {
+      k = i;
+      break;
+    }
+    if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    const int p = t.i;
+    const double* Ap = A + (int64_t)p * LD;
+    // Householder reflector of the pivot column (LAPACK dlarfg), rebuilt by every warp
+    double x2 = 0.0;
+    for (int r = i + 1 + lane; r < d; r += 32) x2 = fma(Ap[r], Ap[r], x2);
+    x2 = warp_sum(x2);
+    const double alpha = Ap[i];
+    const double xnorm = sqrt(x2);
+    double tau, beta;
+    if (xnorm == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+    } else {
+      const double h = hypot(alpha, xnorm);
+      beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
+      tau = (beta - alpha) / beta;
+    }
+    const double den = alpha - beta;
+    // trailing update of the unretired rows (the pivot row p excluded) + next norms + local pivot
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    const int r0 = (i + 1) + ((sub - (i + 1)) & (CQ_TPR - 1));   // first r > i with r = sub mod 8
+    for (int j0 = 0; j0 < m; j0 += RPP) {
+      const int j = j0 + rloc;
+      const bool act = j < m && j != p && j != p_prev && !retired[j];
+      double* Aj = A + (int64_t)(act ? j : p) * LD;
+      double s = 0.0, aji = 0.0;
+      if (act) {
+        aji = Aj[i];
+        if (tau != 0.0)
+          for (int r = r0; r < d; r += CQ_TPR) s = fma(Ap[r], Aj[r], s);
+      }
+      s = row_sum(s);
+      __syncwarp();   // every lane of the row read A(j, i) before it is updated
+      double q = 0.0;
+      if (act) {
+        if (tau != 0.0) {
+          const double w = tau * (aji + s / den);
+          const double wd = w / den;
+          if (sub == 0) Aj[i] = aji - w;
+          for (int r = r0; r < d; r += CQ_TPR) {
+            const double x = fma(-wd, Ap[r], Aj[r]);
+            Aj[r] = x;
+            q = fma(x, x, q);
+          }
+        } else {
+          for (int r = r0; r < d; r += CQ_TPR) q = fma(Aj[r], Aj[r], q);
+        }
+      }
+      q = row_sum(q);
+      if (act) loc = top2_merge(loc, Top2{sqrt(q), j, -1.0});
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red[warp] = loc;
+    p_prev = p;
+    beta_prev = beta;
+    k = i + 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int q = k;   // redundant rows after the pivots, ascending row index
+    for (int j = 0; j < m; ++j)
+      if (!retired[j]) perm[q++] = j;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += NT) a.perm[off + j] = perm[j];
+  double* Wc = a.W + off * d;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += NT) {
+    const int64_t q = e / d;
+    Wc[e] = A[(int64_t)perm[q] * LD + (e - q * d)];
+  }
+  if (threadIdx.x == 0) {
+    a.k[c] = k;
+    a.cert[2 * c] = min_gap;
+    a.cert[2 * c + 1] = margin;
+  }
+}
+
+template <bool SMEM, int NT>
+static void cpqr1_launch(const CpqrArgs& a, size_t sm, double* scratch, cudaStream_t st) {
+  H2_CUDA(cudaFuncSetAttribute(cpqr1_kernel<SMEM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr1_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a, scratch);
+}
+
 template <bool SMEM, int NT>
 static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024)
@@ -401,6 +571,28 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     cpqr_warp_kernel<<<div_up(a.nclusters, CW_WPB), 32 * CW_WPB, wsm, st>>>(a);
     H2_CHECK_LAUNCH();
     return H2_CQ_V_WARP;
+  }
+  if (env_int("H2_CQ_OLD", 0) == 0) {
+    // one-barrier kernel: perm + retired flags + (SMEM) the padded panel
+    size_t sm = sizeof(double) * cq1_head_doubles(a.max_m);
+    const size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
+    // threads: 8 per panel row pass; 1024 when few panels leave SMs idle (upper levels)
+    const int NTsel = a.max_m > 64 && a.nclusters < 148 ? 1024 : (a.max_m > 32 ? 512 : 256);
+    if (sm + panel <= 200 * 1024 && force != H2_CQ_V_GLOBAL) {
+      sm += panel;
+      if (NTsel == 1024) cpqr1_launch<true, 1024>(a, sm, nullptr, st);
+      else if (NTsel == 512) cpqr1_launch<true, 512>(a, sm, nullptr, st);
+      else cpqr1_launch<true, 256>(a, sm, nullptr, st);
+      H2_CHECK_LAUNCH();
+      return H2_CQ_V_SMEM;
+    }
+    double* scr = static_cast<double*>(cache_alloc(sizeof(double) * std::max<int64_t>(a.rows * a.d, 1), st));
+    if (NTsel == 1024) cpqr1_launch<false, 1024>(a, sm, scr, st);
+    else if (NTsel == 512) cpqr1_launch<false, 512>(a, sm, scr, st);
+    else cpqr1_launch<false, 256>(a, sm, scr, st);
+    H2_CHECK_LAUNCH();
+    cache_free(scr, st);
+    return H2_CQ_V_GLOBAL;
   }
   size_t sm = sizeof(double) * (a.d + a.max_m + (a.max_m + 1) / 2);
   size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);

@@ -260,6 +260,23 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
   H2_CUDA(cudaFuncSetAttribute(bsr_kernel<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64));
   static const int wm64 = env_int("H2_BSR_WM64", 4);   // 32 x 32 warp tiles for 64-column passes (-3 ms at C2)
+  // wide passes (the eager sweep): one CTA covers up to 160 columns with 2 x CW/32
+  // warps of 32 x 32 tiles, so each block slab is read once per row tile and no column tile runs
+  // half empty (160 = 64 + 64 + 32 wasted 17 % of the DMMA work)
+  if (a.ncols > 64 && env_int("H2_BSR_WIDE", 1) != 0) {
+    const int cwn = std::min(5, div_up(a.ncols, 32));
+    auto go = [&](auto kern, int cw) {
+      const size_t sm = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (cw + 4));
+      H2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, cw));
+      kern<<<grid, 64 * (cw / 32), sm, st>>>(a, alpha);
+    };
+    if (cwn == 5) go(bsr_kernel<160, 4>, 160);
+    else if (cwn == 4) go(bsr_kernel<128, 4>, 128);
+    else go(bsr_kernel<96, 4>, 96);
+    H2_CHECK_LAUNCH();
+    return;
+  }
   if (a.ncols > 32) {
     dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, 64));
     if (wm64 == 4) bsr_kernel<64, 4><<<grid, 128, sm64, st>>>(a, alpha);

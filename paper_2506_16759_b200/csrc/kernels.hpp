@@ -103,6 +103,7 @@ struct CpqrArgs {
   int32_t* k;
   int32_t* perm;          // at poff[c]
   double* cert;           // 2 per cluster (min gap, stop margin)
+  int64_t rows;           // total panel rows (poff range) of the depth
 };
 // returns the variant that ran: H2_CQ_V_WARP (warp per panel, m <= 64), H2_CQ_V_SMEM (CTA per
 // panel, panel in shared memory) or H2_CQ_V_GLOBAL (CTA per panel, panel in global W).

@@ -51,24 +51,26 @@ KEYS = [
 def rep(path, title):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, units, v = rows[0], rows[1], rows[2]
-    d = dict(zip(h, v))
+    h, units = rows[0], rows[1]
     u = dict(zip(h, units))
-    print(f"# {title}\n\nKernel: `{d.get('Kernel Name', '?')[:120]}`\n")
-    print("| metric | value |\n|---|---|")
-    for k, lab in KEYS:
-        if k in d:
-            print(f"| {lab} (`{k}`) | {d[k]} {u.get(k, '')} |")
-    st = []
-    for k in h:
-        if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio"):
-            try:
-                st.append((float(d[k]), k.replace("smsp__average_warps_issue_stalled_", "").replace(
-                    "_per_issue_active.ratio", "")))
-            except ValueError:
-                pass
-    print("\nTop stall reasons (warps per issue-active cycle): " +
-          ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:6]))
+    print(f"# {title}\n")
+    for v in rows[2:]:
+        d = dict(zip(h, v))
+        print(f"\nKernel: `{d.get('Kernel Name', '?')[:120]}`\n")
+        print("| metric | value |\n|---|---|")
+        for k, lab in KEYS:
+            if k in d:
+                print(f"| {lab} (`{k}`) | {d[k]} {u.get(k, '')} |")
+        st = []
+        for k in h:
+            if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio"):
+                try:
+                    st.append((float(d[k]), k.replace("smsp__average_warps_issue_stalled_", "").replace(
+                        "_per_issue_active.ratio", "")))
+                except ValueError:
+                    pass
+        print("\nTop stall reasons (warps per issue-active cycle): " +
+              ", ".join(f"{n} {x:.2f}" for x, n in sorted(st, reverse=True)[:6]))
 
 
 if __name__ == "__main__":
