@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
   int* perm = reinterpret_cast<int*>(smem);                          // max_m
   unsigned char* retired = reinterpret_cast<unsigned char*>(perm + a.max_m);
   double* spanel = smem + cq1_head_doubles(a.max_m);                 // after perm + retired
-  __shared__ Top2 red[NW];
+  // per-warp pivot candidates, double buffered by step parity: a fast warp publishing step i's
+  // candidates never overwrites the ones a slow warp is still merging from step i - 1
+  __shared__ Top2 red2[2][NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
   const int64_t off = a.poff[c];
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
       if (j < m) loc = top2_merge(loc, Top2{sqrt(q), j, -1.0});
     }
     loc = warp_best(loc);
-    if (lane == 0) red[warp] = loc;
+    if (lane == 0) red2[0][warp] = loc;
   }
   const int kfull = min(d, m);
   const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
       retired[p_prev] = 1;
       perm[i - 1] = p_prev;
     }
-    Top2 t = lane < NW ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
+    Top2 t = lane < NW ? red2[i & 1][lane] : Top2{-1.0, 0x7fffffff, -1.0};
     t = warp_top2(t);
     if (i >= m) break;
     if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
       beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
       tau = (beta - alpha) / beta;
     }
-    const double den = alpha - beta;
+    const double rden = 1.0 / (alpha - beta);
     // trailing update of the unretired rows (the pivot row p excluded) + next norms + local pivot
     Top2 loc{-1.0, 0x7fffffff, -1.0};
     const int r0 = (i + 1) + ((sub - (i + 1)) & (CQ_TPR - 1));   // first r > i with r = sub mod 8
@@ -352,8 +354,8 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
       double q = 0.0;
       if (act) {
         if (tau != 0.0) {
-          const double w = tau * (aji + s / den);
-          const double wd = w / den;
+          const double w = tau * fma(s, rden, aji);
+          const double wd = w * rden;
           if (sub == 0) Aj[i] = aji - w;
           for (int r = r0; r < d; r += CQ_TPR) {
             const double x = fma(-wd, Ap[r], Aj[r]);
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
       if (act) loc = top2_merge(loc, Top2{sqrt(q), j, -1.0});
     }
     loc = warp_best(loc);
-    if (lane == 0) red[warp] = loc;
+    if (lane == 0) red2[(i + 1) & 1][warp] = loc;
     p_prev = p;
     beta_prev = beta;
     k = i + 1;

@@ -131,18 +131,20 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool va
 }
 
 // WM: 8-row DMMA blocks per warp (warp tile 8 WM x 32); warps: NWR along rows x CW/32 along columns
-template <int CW, int WM>
+// NS: cp.async ring stages; COLFAST: grid x = column tile (the column tiles of one row tile run
+// together and share the block slabs through L2), y = cluster, z = row tile
+template <int CW, int WM, int NS = BSR_NS, bool COLFAST = false>
 __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(BsrArgs a, double alpha) {
   constexpr int NWR = 64 / (8 * WM);
   constexpr int NT = 32 * NWR * (CW / 32);   // threads
   constexpr int LDB = CW + 4;
   constexpr int BSZ = BT_K * LDB;
   extern __shared__ __align__(16) double bsm[];   // NS x (A slab + B slab)
-  __shared__ int st_nk[BSR_NS], st_dir[BSR_NS];
-  const int s = a.c_begin + blockIdx.x;
+  __shared__ int st_nk[NS], st_dir[NS];
+  const int s = a.c_begin + (COLFAST ? blockIdx.y : blockIdx.x);
   const int ms = a.cnt[s];
-  const int r0 = blockIdx.y * BT_R;
-  const int cb = a.c0 + blockIdx.z * CW;
+  const int r0 = (COLFAST ? blockIdx.z : blockIdx.y) * BT_R;
+  const int cb = a.c0 + (COLFAST ? blockIdx.x : blockIdx.z) * CW;
   const int nc = min(CW, a.c0 + a.ncols - cb);
   if (r0 >= ms || nc <= 0) return;
   const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
@@ -204,17 +206,17 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
   int nitems = 0;
   for (int e = e0; e < e1; ++e) nitems += ((a.kcnt ? a.kcnt : a.cnt)[a.idx[e]] + BT_K - 1) / BT_K;
 #pragma unroll
-  for (int q = 0; q < BSR_NS - 1; ++q) {
+  for (int q = 0; q < NS - 1; ++q) {
     load_next(q);
     asm volatile("cp.async.commit_group;\n" ::);
   }
   for (int it = 0; it < nitems; ++it) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(BSR_NS - 2));
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NS - 2));
     __syncthreads();
     // the buffer of slab it-1 was consumed before this barrier: refill it with slab it+NS-1
-    load_next((it + BSR_NS - 1) % BSR_NS);
+    load_next((it + NS - 1) % NS);
     asm volatile("cp.async.commit_group;\n" ::);
-    const int buf = it % BSR_NS;
+    const int buf = it % NS;
     const double* sA = bsm + buf * (BT_ASZ + BSZ);
     const double* sB = sA + BT_ASZ;
     const int nk = st_nk[buf];
@@ -263,17 +265,31 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   // wide passes (the eager sweep): one CTA covers up to 160 columns with 2 x CW/32
   // warps of 32 x 32 tiles, so each block slab is read once per row tile and no column tile runs
   // half empty (160 = 64 + 64 + 32 wasted 17 % of the DMMA work)
-  if (a.ncols > 64 && env_int("H2_BSR_WIDE", 1) != 0) {
-    const int cwn = std::min(5, div_up(a.ncols, 32));
-    auto go = [&](auto kern, int cw) {
-      const size_t sm = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (cw + 4));
+  static const int var = env_int("H2_BSR_VAR", 0);
+  if (a.ncols > 64 && var != 0) {
+    auto go = [&](auto kern, int cw, int wm, int ns, bool colfast) {
+      const size_t sm = sizeof(double) * ns * (BT_ASZ + BT_K * (cw + 4));
       H2_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      dim3 grid(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, cw));
-      kern<<<grid, 64 * (cw / 32), sm, st>>>(a, alpha);
+      const int nt = 32 * (64 / (8 * wm)) * (cw / 32);
+      if (colfast) kern<<<dim3(div_up(a.ncols, cw), a.nclusters, div_up(a.max_rows, BT_R)), nt, sm, st>>>(a, alpha);
+      else kern<<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, cw)), nt, sm, st>>>(a, alpha);
     };
-    if (cwn == 5) go(bsr_kernel<160, 4>, 160);
-    else if (cwn == 4) go(bsr_kernel<128, 4>, 128);
-    else go(bsr_kernel<96, 4>, 96);
+    const int cwn = std::min(5, div_up(a.ncols, 32));
+    if (var == 1) {
+      if (cwn == 5) go(bsr_kernel<160, 4>, 160, 4, BSR_NS, false);
+      else if (cwn == 4) go(bsr_kernel<128, 4>, 128, 4, BSR_NS, false);
+      else go(bsr_kernel<96, 4>, 96, 4, BSR_NS, false);
+    } else if (var == 2) {
+      if (cwn == 5) go(bsr_kernel<160, 4, 3>, 160, 4, 3, false);
+      else if (cwn == 4) go(bsr_kernel<128, 4, 3>, 128, 4, 3, false);
+      else go(bsr_kernel<96, 4, 3>, 96, 4, 3, false);
+    } else if (var == 3) {
+      go(bsr_kernel<32, 2, BSR_NS, true>, 32, 2, BSR_NS, true);
+    } else if (var == 4) {
+      go(bsr_kernel<64, 4, BSR_NS, true>, 64, 4, BSR_NS, true);
+    } else {
+      go(bsr_kernel<64, 4, 3>, 64, 4, 3, false);
+    }
     H2_CHECK_LAUNCH();
     return;
   }
