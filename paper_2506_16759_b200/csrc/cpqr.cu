@@ -56,7 +56,11 @@ __device__ __forceinline__ Top2 warp_top2(Top2 t) {
 constexpr int CQ_TPR = 8;
 __host__ __device__ inline int cq_ld(int d) { return ((d + 7) / 8) * 8 + (((d + 7) / 8) % 2 == 0 ? 8 : 0); }
 
-template <bool SMEM, int CQ_THREADS>
+// E > 0 (round 2): a thread's E entries r = sub + 8 q of the reflector v and of the row being
+// updated are held in registers for the step (the row is read once and written once instead of
+// read twice and written once, v is read once per step instead of twice per row); the same
+// operations in the same order as E = 0, so the factorisation is bitwise unchanged.
+template <bool SMEM, int CQ_THREADS, int E = 0>
 __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   constexpr int CQ_WARPS = CQ_THREADS / 32;
   constexpr int RPP = CQ_THREADS / CQ_TPR;      // rows per pass
@@ -186,6 +190,45 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     // ---- trailing update of rows j > i (columns of A) + next residual norms + local pivot
     Top2 loc{-1.0, 0x7fffffff, -1.0};
     const int r0 = i + ((sub - i) & (CQ_TPR - 1));   // first r >= i with r = sub mod 8
+    if constexpr (E > 0) {
+      double vq[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int r = sub + CQ_TPR * q;
+        vq[q] = (r >= r0 && r < d) ? v[r] : 0.0;
+      }
+      for (int j0 = i + 1; j0 < m; j0 += RPP) {
+        const int j = j0 + rloc;
+        const bool act = j < m;
+        double* Aj = A + (int64_t)(act ? j : i) * LD;
+        double x[E];
+        double w = 0.0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+          const int r = sub + CQ_TPR * q;
+          const bool in = act && r >= r0 && r < d;
+          x[q] = in ? Aj[r] : 0.0;
+          if (in) w = fma(vq[q], x[q], w);
+        }
+        w = row_sum(w) * tau;
+        double qn = 0.0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+          const int r = sub + CQ_TPR * q;
+          if (act && r >= r0 && r < d) {
+            const double xx = fma(-w, vq[q], x[q]);
+            Aj[r] = xx;
+            if (r > i) qn = fma(xx, xx, qn);
+          }
+        }
+        qn = row_sum(qn);
+        if (act) {
+          const double nj = sqrt(qn);
+          if (sub == 0) nrm[j] = nj;
+          loc = top2_merge(loc, Top2{nj, j, -1.0});
+        }
+      }
+    } else
     for (int j0 = i + 1; j0 < m; j0 += RPP) {
       const int j = j0 + rloc;
       const bool act = j < m;
@@ -401,11 +444,23 @@ static void cpqr1_launch(const CpqrArgs& a, size_t sm, double* scratch, cudaStre
   cpqr1_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a, scratch);
 }
 
+template <bool SMEM, int NT, int E = 0>
+static void cpqr_launch_e(const CpqrArgs& a, size_t sm, cudaStream_t st) {
+  if (sm > 48 * 1024)
+    H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<SMEM, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr_kernel<SMEM, NT, E><<<a.nclusters, NT, sm, st>>>(a);
+}
+
+// register-cached variant when every thread's entries fit E (d <= 8 E), H2_CQ_REG=0 disables
 template <bool SMEM, int NT>
 static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
-  if (sm > 48 * 1024)
-    H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<SMEM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  cpqr_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a);
+  static const bool reg = env_int("H2_CQ_REG", 1) != 0;
+  const int need = (a.d + CQ_TPR - 1) / CQ_TPR;
+  if (reg && need <= 8) cpqr_launch_e<SMEM, NT, 8>(a, sm, st);
+  else if (reg && need <= 16) cpqr_launch_e<SMEM, NT, 16>(a, sm, st);
+  else if (reg && need <= 20) cpqr_launch_e<SMEM, NT, 20>(a, sm, st);
+  else if (reg && need <= 24) cpqr_launch_e<SMEM, NT, 24>(a, sm, st);
+  else cpqr_launch_e<SMEM, NT, 0>(a, sm, st);
 }
 
 // Small panels (m <= 64 rows, the leaf level): one WARP per panel, 4 panels per CTA, no block
@@ -574,7 +629,7 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     H2_CHECK_LAUNCH();
     return H2_CQ_V_WARP;
   }
-  if (env_int("H2_CQ_OLD", 0) == 0) {
+  if (env_int("H2_CQ_ONEBAR", 0) != 0) {   // measured slower at C2 (33.6 vs 30.4 ms): opt-in
     // one-barrier kernel: perm + retired flags + (SMEM) the padded panel
     size_t sm = sizeof(double) * cq1_head_doubles(a.max_m);
     const size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);

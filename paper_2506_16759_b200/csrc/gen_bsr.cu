@@ -265,7 +265,11 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   // wide passes (the eager sweep): one CTA covers up to 160 columns with 2 x CW/32
   // warps of 32 x 32 tiles, so each block slab is read once per row tile and no column tile runs
   // half empty (160 = 64 + 64 + 32 wasted 17 % of the DMMA work)
-  static const int var = env_int("H2_BSR_VAR", 0);
+  // wide passes (> 64 columns, the eager sweep): 32-column CTA tiles in a column-fast grid (the
+  // tiles of one row tile run together and share its block slabs through L2) measured 68.0 vs
+  // 72.2 ms at C2; the other variants (160-column CTAs, 3-stage rings, 64-column column-fast)
+  // were slower (tools/ab_phases.py)
+  static const int var = env_int("H2_BSR_VAR", 3);
   if (a.ncols > 64 && var != 0) {
     auto go = [&](auto kern, int cw, int wm, int ns, bool colfast) {
       const size_t sm = sizeof(double) * ns * (BT_ASZ + BT_K * (cw + 4));

@@ -313,3 +313,32 @@ def test_eager_sweep_bitwise(monkeypatch, case, opts):
         for w in (g._lib.H2_X_BASIS, g._lib.H2_X_B, g._lib.H2_X_CERT):
             assert np.array_equal(H0._export(w, t), H1._export(w, t)), (t, w)
     assert np.array_equal(H0._export(g._lib.H2_X_D), H1._export(g._lib.H2_X_D))
+
+
+@pytest.mark.parametrize("env,a,b", [("H2_CQ_REG", "0", "1"), ("H2_BSR_VAR", "0", "3"), ("H2_BSR_VAR", "0", "1")])
+def test_kernel_variants_bitwise(monkeypatch, env, a, b):
+    """Performance variants that keep every element's operation order: the register-cached CPQR
+    update (H2_CQ_REG) and the BSR tilings of wide passes (H2_BSR_VAR: 64-column tiles, 32-column
+    tiles in a column-fast grid, 160-column CTAs) give bitwise the same H^2 (variants are chosen
+    once per process: each side runs in its own subprocess)."""
+    import subprocess, sys, os
+    code = r'''
+import sys, os, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+import paper_2506_16759_b200 as g
+from synth import uniform_points
+T = g.Tree(uniform_points(6000, 3, 2), 64)
+H = g.build(T, ("exp", 0.2), 1e-6, d_init=32, d_blk=32)
+out = [H._export(g._lib.H2_X_BASIS, t) for t in range(H.top_depth, T.leaf_depth + 1)]
+out += [H._export(g._lib.H2_X_B, t) for t in range(H.top_depth, T.leaf_depth + 1)]
+np.save(sys.argv[1], np.concatenate(out + [H._export(g._lib.H2_X_D), np.array([H.samples], float)]))
+'''
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for val in (a, b):
+        f = tempfile.mktemp(suffix=".npy")
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=dict(os.environ, ROOT=root, **{env: val}))
+        res.append(np.load(f))
+        os.remove(f)
+    assert res[0].shape == res[1].shape and np.array_equal(res[0], res[1])
