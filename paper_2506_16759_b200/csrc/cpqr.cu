@@ -451,10 +451,12 @@ static void cpqr_launch_e(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   cpqr_kernel<SMEM, NT, E><<<a.nclusters, NT, sm, st>>>(a);
 }
 
-// register-cached variant when every thread's entries fit E (d <= 8 E), H2_CQ_REG=0 disables
+// register-cached variant when every thread's entries fit E (d <= 8 E): opt-in (H2_CQ_REG=1);
+// measured slower at C2 (33.5 vs 30.4 ms: 128 registers x 512 threads leave one CTA per SM on
+// the global-panel levels, which ran two)
 template <bool SMEM, int NT>
 static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
-  static const bool reg = env_int("H2_CQ_REG", 1) != 0;
+  static const bool reg = env_int("H2_CQ_REG", 0) != 0;
   const int need = (a.d + CQ_TPR - 1) / CQ_TPR;
   if (reg && need <= 8) cpqr_launch_e<SMEM, NT, 8>(a, sm, st);
   else if (reg && need <= 16) cpqr_launch_e<SMEM, NT, 16>(a, sm, st);

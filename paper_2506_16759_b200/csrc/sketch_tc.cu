@@ -32,6 +32,9 @@ namespace {
 // v 2^46: its rounding, <= 2^-48 max|K| per entry, stays below the accumulated rounding of an FP64
 // GEMM of the same sums, and 6 slices leave TMEM room for 160-column passes).  The low-half /
 // high-half split of the slices (summation chains and TMEM lane halves) is NSPLIT.
+#ifndef H2_TC_NPW
+#define H2_TC_NPW 16
+#endif
 #ifndef H2_TC_PACK
 #define H2_TC_PACK 1
 #endif
@@ -253,7 +256,7 @@ template <int KIND, int TM, int NPW, int NCOL, int JC, int NS>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
-                     int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag) {
+                     int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag, int pfd) {
   using P = TcPlan<TM, NCOL, JC, NS>;
   constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
@@ -342,8 +345,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
     };
-    prefetch(0);
-    prefetch(1);
+    for (int q = 0; q < pfd; ++q) prefetch(q);
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
@@ -390,8 +392,16 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       // full(it-2) and its B by MMA(it-2) -> wait for that MMA.  With NA <= 2 the producers of
       // chunk it already waited for MMA(it-NA) before arriving on full(it), and waiting here
       // could alias: MMA(it) commits to the same barrier and may complete its phase too.
-      if (NA > 2 && it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % NA), ((it - 2) / NA) & 1);
-      prefetch(it + 2);
+      if (pfd == 3) {
+        // prefetch distance 3 (TC_NB = 4 slots): the slot of chunk it+3 was last used by chunk
+        // it-1, whose coordinates were consumed before full(it-1) and its B by MMA(it-1): wait for
+        // MMA(it-1) (its empty barrier is not the one MMA(it) just committed to)
+        if (it >= 1) mbar_wait(bar_empty + 8 * ((it - 1) % NA), ((it - 1) / NA) & 1);
+        prefetch(it + 3);
+      } else {
+        if (NA > 2 && it >= 2) mbar_wait(bar_empty + 8 * ((it - 2) % NA), ((it - 2) / NA) & 1);
+        prefetch(it + 2);
+      }
     }
   } else {
     // producer: rows rs*16 + pair + k*16*(NPW/G) (k < RPT), 8 consecutive j (half h of 16-j group g)
@@ -929,13 +939,25 @@ namespace {
 template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
-  constexpr int NPW = 16;   // producer warps (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128)
+  // producer warps: 16 (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128); the
+  // 160-column pass also has a 32-warp build (H2_TC_NPW=32, one row per producer thread)
   constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
+  static const int pfd = env_int("H2_TC_PF", 2) == 3 ? 3 : 2;   // cp.async ring prefetch distance
+  if constexpr (NCOL == 160) {
+    if (env_int("H2_TC_NPW", 16) == 32) {
+      H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, 32, NCOL, JC, NS>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      sketch_tc_kernel<KIND, TM, 32, NCOL, JC, NS><<<grid, 32 * 33, smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
+                                                                                 ld, sstride, hs, wshift, ovf, pfd);
+      return;
+    }
+  }
+  constexpr int NPW = 16;
   // per launch: the attribute is per device (a process may drive several GPUs)
   H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
-                                                                                    yo, ld, sstride, hs, wshift, ovf);
+                                                                                    yo, ld, sstride, hs, wshift, ovf, pfd);
 }
 
 template <int KIND, int NS>
