@@ -95,6 +95,16 @@ __device__ __forceinline__ uint32_t tmem_slice(int s) {
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count));
 }
+// with a suspend-time hint (ns): the waiting warp is parked by the hardware until the phase
+// completes (or the hint expires) instead of re-issuing try_wait, which keeps issue slots free
+// for the evaluating warps (the kernel is issue-bound: ~1 non-FP64 instruction per FP64 one)
+__device__ __forceinline__ void mbar_wait_hint(uint32_t addr, uint32_t parity, uint32_t hint) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITH_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAITH_%=;\n}\n" ::"r"(addr),
+      "r"(parity), "r"(hint));
+}
 __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
@@ -256,7 +266,8 @@ template <int KIND, int TM, int NPW, int NCOL, int JC, int NS>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
-                     int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag, int pfd) {
+                     int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag, int pfd,
+                     uint32_t hint) {
   using P = TcPlan<TM, NCOL, JC, NS>;
   constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
@@ -349,7 +360,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
-      mbar_wait(bar_full + 8 * buf, (it / NA) & 1);
+      if (hint) mbar_wait_hint(bar_full + 8 * buf, (it / NA) & 1, hint);
+      else mbar_wait(bar_full + 8 * buf, (it / NA) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       const bool first = (it % P::DRAIN) == 0;
       const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
@@ -425,8 +437,13 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
-      mbar_wait(bar_loaded + 8 * slot, (it / TC_NB) & 1);
-      if (it >= NA) mbar_wait(bar_empty + 8 * buf, ((it - NA) / NA) & 1);
+      if (hint) {
+        mbar_wait_hint(bar_loaded + 8 * slot, (it / TC_NB) & 1, hint);
+        if (it >= NA) mbar_wait_hint(bar_empty + 8 * buf, ((it - NA) / NA) & 1, hint);
+      } else {
+        mbar_wait(bar_loaded + 8 * slot, (it / TC_NB) & 1);
+        if (it >= NA) mbar_wait(bar_empty + 8 * buf, ((it - NA) / NA) & 1);
+      }
       const uint8_t* cb = smem + P::C0 + slot * CBUF;
       uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
       const int jj0 = 16 * g + 8 * h;
@@ -939,25 +956,17 @@ namespace {
 template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
-  // producer warps: 16 (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128); the
-  // 160-column pass also has a 32-warp build (H2_TC_NPW=32, one row per producer thread)
+  // producer warps: 16 (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128; 32
+  // would exceed 1024 threads per CTA with the control warp)
   constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
   static const int pfd = env_int("H2_TC_PF", 2) == 3 ? 3 : 2;   // cp.async ring prefetch distance
-  if constexpr (NCOL == 160) {
-    if (env_int("H2_TC_NPW", 16) == 32) {
-      H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, 32, NCOL, JC, NS>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      sketch_tc_kernel<KIND, TM, 32, NCOL, JC, NS><<<grid, 32 * 33, smem, st>>>(C, n, row0, row1, Bq, nchunks, nc, yo,
-                                                                                 ld, sstride, hs, wshift, ovf, pfd);
-      return;
-    }
-  }
+  static const uint32_t hint = (uint32_t)env_int("H2_TC_HINT", 0); // mbarrier wait suspend hint (ns), 0 = none
   constexpr int NPW = 16;
   // per launch: the attribute is per device (a process may drive several GPUs)
   H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
-                                                                                    yo, ld, sstride, hs, wshift, ovf, pfd);
+                                                                                    yo, ld, sstride, hs, wshift, ovf, pfd, hint);
 }
 
 template <int KIND, int NS>
