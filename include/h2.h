@@ -159,7 +159,9 @@ typedef struct {
   int32_t rank;
   /* H2_S_DENSE_MATRIX (an explicit operator such as a frontal matrix,
    * PAPER.md L443/L487): Y = A Omega with A dev n x n row-major in TREE order (leading dim ld_A),
-   * one FP64 GEMM per draw (cuBLAS, the plain library GEMM). */
+   * on the int8 tensor cores in passes of 128 columns (h2_dense_op_sketch; the Omega stream), or
+   * one cuBLAS DGEMM per draw with an external Omega, the non-symmetric build's K^T Psi, or
+   * H2_DENSE_TC=0. */
   const double* A;
   int64_t ld_A;
   /* H2_S_H2_LOWRANK with a second factor (h2_build_nonsym only): M = A_H + U V^T, V dev n x rank
@@ -388,6 +390,17 @@ enum { H2_SKETCH_OMEGA_QUARTERS = 1 };
 h2_status h2_dense_sketch(const h2_tree* tree, h2_kernel kern, int64_t row_begin, int64_t row_end,
                           const double* omega, int64_t ld_omega, int32_t ncols, double* y,
                           int64_t ld_y, int32_t flags, void* stream);
+
+/* Explicit dense operator product (the H2_S_DENSE_MATRIX sketch), rows
+ * [row_begin, row_end): y = A(rows, :) omega, A dev row-major n x n (leading dim lda >= n, tree
+ * order), omega dev all n rows.  flags & H2_SKETCH_OMEGA_QUARTERS (omega = the h2_omega stream):
+ * int8 tensor cores -- A rounded once to a signed 53-bit fixed point of scale 2^E >= max|A|
+ * (<= 2^-52 max|A| per entry, the normwise error level of an FP64 GEMM), 7 byte slices, exact
+ * int32 contraction, A read once per 128 columns; otherwise one cuBLAS DGEMM.  Errors:
+ * INVALID_ARG, CUDA. */
+h2_status h2_dense_op_sketch(const double* A, int64_t lda, int64_t n, int64_t row_begin, int64_t row_end,
+                             const double* omega, int64_t ld_omega, int32_t ncols, double* y, int64_t ld_y,
+                             int32_t flags, void* stream);
 
 /* Omega stream (Philox4x32-10 -> centred binomial (popcount(64 bits) - 32)/4, R8):
  * rows [row0,row0+nrows) x sample columns [col0,col0+ncols) into out (dev, row-major, ld). */

@@ -128,6 +128,8 @@ SIGNATURES = {
     "h2_matvec": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P]),
     "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64,
                                   C.c_int32, _P]),
+    "h2_dense_op_sketch": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P,
+                                     C.c_int64, C.c_int32, _P]),
     "h2_omega": (C.c_int, [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, C.c_int64, _P]),
     "h2_export_size": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "h2_export": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),

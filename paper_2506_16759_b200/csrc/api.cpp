@@ -311,6 +311,18 @@ struct Builder {
   }
   // the int8 tensor-core sketch needs the exactly representable stream (quarters)
   bool quarters() const { return o.omega_ext == nullptr; }
+  // explicit dense operator (H2_S_DENSE_MATRIX): the int8 tensor-core product of the h2 stream
+  // (one HBM read of A per pass of up to 128 columns) or cuBLAS DGEMM
+  bool dense_tc = false;
+  double dense_amax = -1.0;
+  void dense_op_sketch(const double* Od, int64_t ld, int nc, double* Yd, cudaStream_t s) {
+    if (dense_tc) {
+      if (dense_amax < 0) dense_amax = dense_absmax(S.A, S.ld_A, T.n, s);
+      launch_dense_op_tc(S.A, S.ld_A, T.n, row_b(), row_e(), dense_amax, Od, ld, nc, Yd + row_b() * ld, ld, s);
+    } else {
+      dense_matrix_sketch(S.A, S.ld_A, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, s);
+    }
+  }
   void sketch_rows(const double* Od, int64_t ld, int nc, double* Yd, cudaStream_t s) {
     if (ex) launch_exact_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, s);
     else launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld,
@@ -504,7 +516,7 @@ struct Builder {
       timer.begin(H2_PH_SKETCH);
       sketch_columns += nc;
       if (S.kind == H2_S_DENSE_MATRIX) {
-        dense_matrix_sketch(S.A, S.ld_A, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, st);
+        dense_op_sketch(Od, ld, nc, Yd, st);
       } else if (S.kind == H2_S_H2_LOWRANK) {
         // K_blk = A_H Omega + U (U^T Omega)
         matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
@@ -979,7 +991,7 @@ struct Builder {
   // one tensor-core pass evaluates K for (spec_w), at least one block
   int pass_width(int c0) const {
     int e = block_end(c0);
-    if (S.kind == H2_S_DENSE_KERNEL && spec_on)
+    if ((S.kind == H2_S_DENSE_KERNEL || S.kind == H2_S_DENSE_MATRIX) && spec_on)
       while (e < o.d_max && block_end(e) - c0 <= spec_w) e = block_end(e);
     return e - c0;
   }
@@ -995,7 +1007,7 @@ struct Builder {
       timer.begin(H2_PH_SKETCH);
       sketch_columns += nc;
       if (S.kind == H2_S_DENSE_MATRIX) {
-        dense_matrix_sketch(S.A, S.ld_A, T.n, row_b(), row_e(), Od, ld, nc, Yd + row_b() * ld, ld, st);
+        dense_op_sketch(Od, ld, nc, Yd, st);
       } else if (S.kind == H2_S_H2_LOWRANK) {
         matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
         DArr<double> scr;
@@ -1523,6 +1535,11 @@ struct Builder {
       spec_on = !ex && quarters() && sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 &&
                 env_int("H2_SPEC", 1) != 0;
       spec_w = sketch_tc_pass_cols(skp.kind);
+    }
+    if (S.kind == H2_S_DENSE_MATRIX) {   // tensor-core operator product: passes of 128 columns
+      dense_tc = !ex && quarters() && env_int("H2_DENSE_TC", 1) != 0;
+      spec_on = dense_tc && env_int("H2_SPEC", 1) != 0;
+      spec_w = 128;
     }
     if (o.tol_rule == H2_TOL_LITERAL && !(o.norm > 0)) o.norm = estimate_norm();
     if (o.tol_rule == H2_TOL_LITERAL) H.stats.norm_est = o.norm;
@@ -2253,6 +2270,24 @@ h2_status h2_dense_sketch(const h2_tree* T, h2_kernel kern, int64_t row_begin, i
     ensure_uploaded(T);
     launch_dense_sketch(tree_kernel(T, kern, (cudaStream_t)stream), T->d_x, T->d_y, T->d_z, T->n, row_begin, row_end, omega, ld_omega, ncols, y,
                         ld_y, (flags & H2_SKETCH_OMEGA_QUARTERS) != 0, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_dense_op_sketch(const double* A, int64_t lda, int64_t n, int64_t row_begin, int64_t row_end,
+                             const double* omega, int64_t ld_omega, int32_t ncols, double* y, int64_t ld_y, int32_t flags,
+                             void* stream) {
+  try {
+    H2_REQUIRE(A && omega && y && n >= 1 && lda >= n, "h2_dense_op_sketch: bad argument");
+    H2_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= n, "h2_dense_op_sketch: bad row range");
+    H2_REQUIRE(ncols >= 0 && ld_omega >= ncols && ld_y >= ncols, "h2_dense_op_sketch: bad ncols / leading dims");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (flags & H2_SKETCH_OMEGA_QUARTERS)
+      launch_dense_op_tc(A, lda, n, row_begin, row_end, dense_absmax(A, lda, n, st), omega, ld_omega, ncols, y, ld_y, st);
+    else
+      dense_matrix_sketch(A, lda, n, row_begin, row_end, omega, ld_omega, ncols, y, ld_y, st);
     return H2_OK;
   } catch (const Error& e) {
     return fail(e);

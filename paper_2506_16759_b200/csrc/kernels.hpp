@@ -23,6 +23,11 @@ int env_int(const char* name, int def);
 bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st);
+// explicit dense operator on the int8 tensor cores (Omega = the h2 stream):
+// Y(rows) = A(rows, :) Omega, A row-major n x n (lda), 7-slice fixed point of scale 2^E >= amax
+double dense_absmax(const double* A, int64_t lda, int64_t n, cudaStream_t st);
+void launch_dense_op_tc(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, double amax,
+                        const double* Om, int64_t ldo, int ncols, double* Y, int64_t ldy, cudaStream_t st);
 // minimum squared distance of distinct points over the near-field leaf pairs (Helmholtz scale)
 double min_near_dist2(const double* X, const double* Y, const double* Z, const int64_t* leaf_begin, int nleaf,
                       const int32_t* near_ptr, const int32_t* near_idx, cudaStream_t st);

@@ -216,6 +216,20 @@ __device__ __forceinline__ uint2 helm_fixed51(double r2, double hs, uint32_t& ov
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
 }
 
+// Explicit dense operator (H2_S_DENSE_MATRIX): the producers read A(i, j)
+// from HBM instead of evaluating a kernel; with a power-of-two scale 2^E >= max|A| (hs = 2^-E,
+// exact), v = A hs in [-1, 1] takes the signed 53-bit format of the Helmholtz path:
+// w = v 2^51 + 3 2^51 (one FMA: the fixed-point rounding, <= 2^-52 max|A| per entry),
+// m = bits(w) - bits(2^52) - 2^51, 7 byte slices, the top one signed.  FP64 pipe: 2 per entry.
+constexpr int KDENSE = 3;
+template <int HEXP>
+__device__ __forceinline__ uint2 dense_fixed(double x, double hs, uint32_t& ovf) {
+  const double w = fma(x * hs, (double)(1ull << HEXP), 6755399441055744.0);
+  const int mh = __double2hiint(w) - 0x43380000;
+  ovf |= (uint32_t)(mh + (1 << (HEXP - 32))) > (2u << (HEXP - 32));
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
+}
+
 // 4x4 byte transpose: out[s] = bytes s of (a, b, c, d)
 __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* o) {
   uint32_t p = __byte_perm(a, b, 0x5140), q = __byte_perm(c, d, 0x5140);
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag, int pfd,
-                     uint32_t hint) {
+                     uint32_t hint, const double* __restrict__ Aop, int64_t lda) {
   using P = TcPlan<TM, NCOL, JC, NS>;
   constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
@@ -346,13 +360,15 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::B0 + slot * BBUF + e * 16),
                      "l"(Bq + t * BBUF + e * 16));
       }
+      if (KIND != KDENSE) {
 #pragma unroll
-      for (int q = 0; q < JC / 16; ++q) {
-        const int e = lane + 32 * q;
-        const int jc = e >> 1;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::C0 + slot * CBUF + e * 16 +
-                                                                          (jc >> 3) * 16),
-                     "l"(reinterpret_cast<const char*>(C + t * JC) + e * 16));
+        for (int q = 0; q < JC / 16; ++q) {
+          const int e = lane + 32 * q;
+          const int jc = e >> 1;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + P::C0 + slot * CBUF + e * 16 +
+                                                                            (jc >> 3) * 16),
+                       "l"(reinterpret_cast<const char*>(C + t * JC) + e * 16));
+        }
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_loaded + 8 * slot));
     };
@@ -422,11 +438,14 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     const int h = lane & 1;
     const int r0 = 16 * rs + (lane >> 1);
     double4 ci[RPT];
+    const double* arow[RPT];   // KDENSE: the operator rows
     int off[RPT];
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const int r = r0 + k * 16 * (NPW / G);
-      ci[k] = C[(rtile + r < row1) ? (rtile + r) : (row1 - 1)];
+      const int64_t ri = (rtile + r < row1) ? (rtile + r) : (row1 - 1);
+      if (KIND == KDENSE) arow[k] = Aop + ri * lda;
+      else ci[k] = C[ri];
       off[k] = g * LBO_A + (r >> 3) * 128 + (r & 7) * 16 + 8 * h;
     }
     // PACK7: the M = 64 layout of the top slice (64 rows x 16 B per k group)
@@ -448,6 +467,23 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       uint8_t* Ab = smem + P::A0 + buf * P::ABUF;
       const int jj0 = 16 * g + 8 * h;
       uint32_t lo[RPT][8], hi[RPT][8];
+      if constexpr (KIND == KDENSE) {
+        // 8 consecutive j of each row from HBM (read-only path); columns beyond n are 0
+        const int64_t j0 = (ch_b + it) * JC + jj0;
+        double x[RPT][8];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x[k][q] = (j0 + q < n) ? __ldg(arow[k] + j0 + q) : 0.0;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint2 m = dense_fixed<SliceFmt<NS>::HEXP>(x[k][q], hs, ovf);
+            lo[k][q] = m.x;
+            hi[k][q] = m.y;
+          }
+      } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int jj = jj0 + q;
@@ -459,6 +495,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
+      }
       }
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
@@ -955,7 +992,8 @@ int sketch_tc_pass_cols(int kind) {
 namespace {
 template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
-               int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf) {
+               int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf,
+               const double* Aop = nullptr, int64_t lda = 0) {
   // producer warps: 16 (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128; 32
   // would exceed 1024 threads per CTA with the control warp)
   constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
@@ -966,7 +1004,8 @@ void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t 
   H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
-                                                                                    yo, ld, sstride, hs, wshift, ovf, pfd, hint);
+                                                                                    yo, ld, sstride, hs, wshift, ovf, pfd, hint,
+                                                                                    Aop, lda);
 }
 
 template <int KIND, int NS>
@@ -995,16 +1034,19 @@ void tc_launch_pair(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int
 template <int KIND, int NS>
 void tc_dispatch(int NCOL, dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1,
                  const int8_t* Bq, int64_t nchunks, int nc, double* yo, int64_t ld, int64_t ss, double hs, int wshift,
-                 uint32_t* ovf) {
+                 uint32_t* ovf, const double* Aop = nullptr, int64_t lda = 0) {
   if constexpr (NS == 6) {
     if (NCOL == 160) {
       tc_launch<KIND, 64, 160, 128, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
       return;
     }
   }
-  if (NCOL == 128) tc_launch<KIND, 64, 128, 128, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-  else if (NCOL == 64) tc_launch<KIND, 128, 64, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
-  else tc_launch<KIND, 128, 32, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf);
+  if (NCOL == 128)
+    tc_launch<KIND, 64, 128, 128, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf, Aop, lda);
+  else if (NCOL == 64)
+    tc_launch<KIND, 128, 64, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf, Aop, lda);
+  else
+    tc_launch<KIND, 128, 32, 64, NS>(grid, st, C, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift, ovf, Aop, lda);
 }
 
 // j-split S fills the last wave (1 CTA / SM)
@@ -1117,6 +1159,84 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   cache_free(ovf, st);
   if (part) cache_free(part, st);
   return h_ovf == 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// Explicit dense operator on the int8 tensor cores (H2_S_DENSE_MATRIX):
+// Y(rows) = A(rows, :) Omega for the h2 Omega stream.  A (row-major, lda, tree order) is read
+// once per pass of up to 128 columns and converted to the 7-slice signed fixed point of scale
+// 2^E >= max|A| (dense_fixed); the contraction is exact in int32 TMEM accumulators, so the only
+// rounding is the grid (<= 2^-52 max|A| per entry) and the FP64 drains -- the normwise error
+// level of an FP64 GEMM.  HBM-bound (8 bytes per entry per pass) instead of DGEMM-bound.
+// ------------------------------------------------------------------------------------------
+__global__ void absmax_kernel(const double* __restrict__ A, int64_t lda, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n;
+    m = fmax(m, fabs(A[i * lda + (e - i * n)]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));   // m >= 0: bit order
+}
+
+double dense_absmax(const double* A, int64_t lda, int64_t n, cudaStream_t st) {
+  unsigned long long* d = static_cast<unsigned long long*>(cache_alloc(8, st));
+  H2_CUDA(cudaMemsetAsync(d, 0, 8, st));
+  absmax_kernel<<<148 * 8, 256, 0, st>>>(A, lda, n, d);
+  H2_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  H2_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
+  H2_CUDA(cudaStreamSynchronize(st));
+  cache_free(d, st);
+  double v;
+  std::memcpy(&v, &h, 8);
+  return v;
+}
+
+void launch_dense_op_tc(const double* A, int64_t lda, int64_t n, int64_t row0, int64_t row1, double amax,
+                        const double* Om, int64_t ldo, int ncols, double* Yout, int64_t ldy, cudaStream_t st) {
+  if (row1 <= row0 || ncols <= 0) return;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t npad = ((n + 127) / 128) * 128;
+  const int64_t rows = row1 - row0;
+  // scale 2^E >= max|A|: v = A 2^-E in [-1, 1]; slice weight 2^(8 s) 2^E 2^-51 / 4
+  const int E = amax > 0 ? (int)std::ceil(std::log2(amax)) : 0;
+  const double hs = std::ldexp(1.0, -E);
+  const int wshift = E - 51 - 2;
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 128, st));
+  uint32_t* ovf = static_cast<uint32_t*>(cache_alloc(sizeof(uint32_t), st));
+  H2_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
+  double* part = nullptr;
+  int64_t part_elems = 0;
+  for (int c0 = 0; c0 < ncols; c0 += 128) {
+    const int nc = std::min(128, ncols - c0);
+    const int NCOL = nc > 64 ? 128 : nc > 32 ? 64 : 32;
+    const int TM = NCOL >= 128 ? 64 : 128;
+    const int JC = NCOL >= 128 ? 128 : 64;
+    const int64_t nchunks = npad / JC;
+    const int tiles = div_up(rows, TM);
+    const int S = pick_split(div_up(n, 64 * 8), npad / 128, sms);
+    if (S > 1 && part_elems < rows * nc * S) {
+      if (part) cache_free(part, st);
+      part_elems = rows * nc * S;
+      part = static_cast<double*>(cache_alloc(sizeof(double) * part_elems, st));
+    }
+    double* yo = S > 1 ? part : Yout + c0;
+    const int64_t ld = S > 1 ? nc : ldy;
+    const int64_t ss = S > 1 ? rows * nc : 0;
+    omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * JC * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+        Om + c0, ldo, n, nc, NCOL, JC, nchunks, Bq);
+    H2_CHECK_LAUNCH();
+    tc_dispatch<KDENSE, 7>(NCOL, dim3(tiles, S), st, nullptr, n, row0, row1, Bq, nchunks, nc, yo, ld, ss, hs, wshift,
+                           ovf, A, lda);
+    H2_CHECK_LAUNCH();
+    if (S > 1) launch_sketch_combine(part, S, rows, nc, Yout + c0, ldy, st);
+  }
+  cache_free(Bq, st);
+  cache_free(ovf, st);
+  if (part) cache_free(part, st);
 }
 
 // minimum squared distance between distinct points over the near-field leaf pairs (the closest

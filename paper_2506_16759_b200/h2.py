@@ -437,6 +437,22 @@ def dense_sketch(tree: Tree, omega, kernel=("exp", 0.2), row_begin=0, row_end=No
     return out
 
 
+def dense_op_sketch(A, omega, row_begin=0, row_end=None, out=None, stream=None, omega_quarters=False):
+    """Y(rows, :) = A(rows, :) Omega for an explicit (n, n) float64 CUDA operator A (row-major):
+    omega_quarters=True (Omega = the h2 stream) runs the int8 tensor-core product, else DGEMM."""
+    n = A.shape[0]
+    row_end = n if row_end is None else row_end
+    assert A.is_cuda and A.dtype == torch.float64 and A.shape == (n, n) and A.stride(1) == 1
+    assert omega.is_cuda and omega.dtype == torch.float64 and omega.shape[0] == n and omega.stride(1) == 1
+    nc = omega.shape[1]
+    if out is None:
+        out = torch.empty((row_end - row_begin, nc), dtype=torch.float64, device=omega.device)
+    check(lib.h2_dense_op_sketch(_ptr(A), A.stride(0), n, row_begin, row_end, _ptr(omega), omega.stride(0), nc,
+                                 _ptr(out), out.stride(0), L.H2_SKETCH_OMEGA_QUARTERS if omega_quarters else 0,
+                                 _stream(stream)))
+    return out
+
+
 def omega(nrows, ncols, seed=1, stream_id=0, row0=0, col0=0, device="cuda", stream=None):
     """Rows [row0,row0+nrows) x columns [col0,col0+ncols) of the Omega stream (Philox4x32-10)."""
     out = torch.empty((nrows, ncols), dtype=torch.float64, device=device)

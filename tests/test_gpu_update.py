@@ -173,3 +173,41 @@ def test_update_build_parity_vs_oracle_M():
     assert np.linalg.norm(yu - M @ x) <= 4 * tol * nu * np.linalg.norm(x) * 10
     # the two operators differ by the base's representation error (<= 1e-12 relative)
     compare_matvec(Hu, Ho, certified, 1e-6, exact_bound=1e-8)
+
+
+@pytest.mark.parametrize("n,nc", [(5000, 128), (4100, 45), (3000, 150), (2048, 32)])
+def test_dense_operator_tensor_core_sketch(n, nc):
+    """S§8(f) NEXT #4 on the tensor cores (h2_dense_op_sketch): Y = A Omega for an explicit
+    operator with mixed signs and a wide dynamic range (exp kernel + Gaussian noise + a large
+    entry) vs the oracle's FP64 product (numpy): every entry within 1e-13 max|Y| (the 2^-52
+    max|A| grid, the normwise level of an FP64 GEMM), ragged n and pass widths, row shards."""
+    X = uniform_points(n, 3, 1)
+    A = kernels.kernel_block("exp", 0.2, X, X) + 1e-3 * np.random.default_rng(4).standard_normal((n, n))
+    A[7, 11] = 37.0
+    Om = rng.omega_block(1, 0, 0, n, 0, nc)
+    ref = A @ Om
+    Ad, Od = torch.from_numpy(A).cuda(), torch.from_numpy(Om).cuda()
+    Y = g.dense_op_sketch(Ad, Od, omega_quarters=True).cpu().numpy()
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(ref).max()
+    r0, r1 = 333, n - 17
+    Y2 = g.dense_op_sketch(Ad, Od, r0, r1, omega_quarters=True).cpu().numpy()
+    assert np.array_equal(Y2, Y[r0:r1])       # row shards: bitwise the rows of the full product
+
+
+def test_dense_operator_workload_tensor_core_vs_dgemm(monkeypatch):
+    """The dense-operator build with the tensor-core sketch (default) and with cuBLAS DGEMM
+    (H2_DENSE_TC=0) both meet 2 tol against the operator, with the same sample count."""
+    X = uniform_points(5000, 3, 7)
+    T = g.Tree(X, 64)
+    Xt = torch.from_numpy(X[T.perm]).cuda()
+    A = torch.exp(-torch.cdist(Xt, Xt, compute_mode="donot_use_mm_for_euclid_dist") / 0.2).contiguous()
+    P = torch.from_numpy(np.random.default_rng(2).standard_normal((T.n, 8))).cuda()
+    AP = A @ P
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("H2_DENSE_TC", flag)
+        H = g.build(T, ("exp", 0.2), 1e-6, dense=A)
+        res[flag] = H.samples
+        err = (torch.linalg.norm(H.matvec(P) - AP) / torch.linalg.norm(AP)).item()
+        assert err <= 2e-6, (flag, err)
+    assert res["1"] == res["0"]
