@@ -453,6 +453,19 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     const uint32_t lane8 = 8u * (lane & 15);
     uint32_t ovf = 0;
     int drains = 0;
+    // KDENSE: the next chunk's operator entries are loaded into registers while this chunk is
+    // converted (one chunk of HBM reads in flight per thread: latency hidden, bandwidth-bound)
+    double xa[KIND == KDENSE ? RPT : 1][8];
+    auto load_a = [&](int itx, double (&dst)[KIND == KDENSE ? RPT : 1][8]) {
+      if constexpr (KIND == KDENSE) {
+        const int64_t j0 = (ch_b + itx) * JC + 16 * g + 8 * h;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[k][q] = (itx < nch && j0 + q < n) ? __ldg(arow[k] + j0 + q) : 0.0;
+      }
+    };
+    load_a(0, xa);
     for (int it = 0; it < nch; ++it) {
       const int buf = it % NA;
       const int slot = it & (TC_NB - 1);
@@ -468,21 +481,21 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       const int jj0 = 16 * g + 8 * h;
       uint32_t lo[RPT][8], hi[RPT][8];
       if constexpr (KIND == KDENSE) {
-        // 8 consecutive j of each row from HBM (read-only path); columns beyond n are 0
-        const int64_t j0 = (ch_b + it) * JC + jj0;
-        double x[RPT][8];
-#pragma unroll
-        for (int k = 0; k < RPT; ++k)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) x[k][q] = (j0 + q < n) ? __ldg(arow[k] + j0 + q) : 0.0;
+        // 8 consecutive j of each row (loaded one chunk ahead); columns beyond n are 0
+        double xn[RPT][8];
+        load_a(it + 1, xn);
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const uint2 m = dense_fixed<SliceFmt<NS>::HEXP>(x[k][q], hs, ovf);
+            const uint2 m = dense_fixed<SliceFmt<NS>::HEXP>(xa[k][q], hs, ovf);
             lo[k][q] = m.x;
             hi[k][q] = m.y;
           }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xa[k][q] = xn[k][q];
       } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -1171,9 +1184,15 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
 // ------------------------------------------------------------------------------------------
 __global__ void absmax_kernel(const double* __restrict__ A, int64_t lda, int64_t n, unsigned long long* out) {
   double m = 0.0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n;
-    m = fmax(m, fabs(A[i * lda + (e - i * n)]));
+  // one row per CTA iteration, 4 independent loads in flight per thread
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* a = A + i * lda;
+    for (int64_t j = threadIdx.x; j < n; j += 4 * blockDim.x) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = j + u * blockDim.x < n ? fabs(__ldg(a + j + u * blockDim.x)) : 0.0;
+      m = fmax(m, fmax(fmax(v[0], v[1]), fmax(v[2], v[3])));
+    }
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));   // m >= 0: bit order
