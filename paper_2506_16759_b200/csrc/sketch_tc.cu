@@ -459,10 +459,21 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     auto load_a = [&](int itx, double (&dst)[KIND == KDENSE ? RPT : 1][8]) {
       if constexpr (KIND == KDENSE) {
         const int64_t j0 = (ch_b + itx) * JC + 16 * g + 8 * h;
+        if (itx < nch && j0 + 8 <= n && (lda & 1) == 0) {   // 16-byte loads (even lda, even j0)
 #pragma unroll
-        for (int k = 0; k < RPT; ++k)
+          for (int k = 0; k < RPT; ++k)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) dst[k][q] = (itx < nch && j0 + q < n) ? __ldg(arow[k] + j0 + q) : 0.0;
+            for (int u = 0; u < 4; ++u) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(arow[k] + j0) + u);
+              dst[k][2 * u] = v.x;
+              dst[k][2 * u + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[k][q] = (itx < nch && j0 + q < n) ? __ldg(arow[k] + j0 + q) : 0.0;
+        }
       }
     };
     load_a(0, xa);
