@@ -31,6 +31,49 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 64 FP64 FMA/clk/SM (DFMA = 
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12          # FP64 pipe instructions (lane-ops) per second
 F_EVAL = 19   # FP64 pipe ops per kernel entry in sketch_tc_kernel (SASS: 6 r^2, 5 r, 7 exp, 1 fixed-point DFMA)
 INT8_DENSE_TOPS = 4500.0                            # nominal dense int8 tensor ops/s (B200, guide)
+# measured int8 tcgen05 rate at the sketch's shape (M = 128, N = 160, K = 32, smem operands):
+# profiles/r2_mma_overlap.txt (tools/microbench/mma_fp64_overlap.cu)
+INT8_MEASURED_TOPS = 4307.5
+FP64_DFMA_TFLOPS = 37.0   # measured DFMA (profiles/r2_fp64_mix.txt: 64 lane-ops/clk/SM; r1: 37.0 TF/s)
+
+
+def hbm_peak():
+    """HBM copy bandwidth (GB/s): the driver-written MEASURED_PEAKS.json, else the profiling guide's
+    fallback (6.65 TB/s)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def whole_build_roofline(stats, ms, n, rows_local, sk_launches, ncol_launch, slices, f_eval=F_EVAL):
+    """T* = sum over phases of max(F / P_fp64, B / P_hbm) over the ALGORITHMIC work
+    libh2 counts (h2_build_stats.work_flops / work_bytes), plus the dense sketch at its serialised
+    bound (FP64 evaluation + int8 contraction: the two do not overlap on an SM,
+    profiles/r2_sketch_serialization.md); frac = T* / measured build time."""
+    hbm, hbm_src = hbm_peak()
+    p64 = FP64_DFMA_TFLOPS * 1e12
+    phases = {}
+    for ph in ("rand", "gen", "bsr", "cpqr", "id"):
+        F, B = stats["work_flops"][ph], stats["work_bytes"][ph]
+        t = max(F / p64, B / (hbm * 1e9)) * 1e3
+        phases[ph] = {"flops": F, "bytes": B, "t_star_ms": round(t, 3),
+                      "bound": "fp64" if F / p64 >= B / (hbm * 1e9) else "hbm",
+                      "measured_ms": round(stats["t_phase_ms"][ph], 3)}
+    ent = float(rows_local) * n * sk_launches
+    t_fp64 = ent * f_eval / (FP64_PIPE_TOPS * 1e12) * 1e3
+    t_i8 = ent * ncol_launch * slices * 2 / (INT8_MEASURED_TOPS * 1e12) * 1e3
+    phases["sketch"] = {"fp64_ops": ent * f_eval, "int8_ops": ent * ncol_launch * slices * 2,
+                        "t_fp64_ms": round(t_fp64, 2), "t_int8_ms": round(t_i8, 2), "t_star_ms": round(t_fp64 + t_i8, 2),
+                        "bound": "fp64 + int8 (serialised)", "measured_ms": round(stats["t_phase_ms"]["sketch"], 3)}
+    tstar = sum(v["t_star_ms"] for v in phases.values())
+    return {"t_star_ms": round(tstar, 2), "measured_ms": round(ms, 2), "frac": tstar / ms,
+            "peaks": {"fp64_tflops": FP64_DFMA_TFLOPS, "hbm_gbs": hbm, "hbm_source": hbm_src,
+                      "int8_tops": INT8_MEASURED_TOPS, "fp64_pipe_tops": FP64_PIPE_TOPS},
+            "phases": phases,
+            "note": "construction phases: libh2's algorithmic work counters (BSR 2 nc sum rows x cols, CPQR "
+                    "sum 4(d-i)(m-i), ID k^2(m-k) + shrink 2k(m-k)nc, gen 8 B per stored entry); sketch: N^2 x "
+                    f"{f_eval} FP64 ops + the exact int8 contraction at the measured tcgen05 rate, serialised"}
 
 
 def parse():
@@ -382,9 +425,19 @@ def run_ours(args, w, rank, world, local_rank):
                      "entries_per_s": entries_launch / (per_launch_ms * 1e-3),
                      "int8_tensor_tops": int8_ops, "int8_tensor_frac": int8_ops / INT8_DENSE_TOPS,
                      "per_launch_ms": per_launch_ms,
+                     # the int8 UMMA stream and the FP64 pipe serialise on an SM (profiles/
+                     # r2_sketch_serialization.md): the kernel's bound is the SUM of both times
+                     "serialised_bound": {
+                         "t_fp64_ms": entries_launch * F_EVAL / (FP64_PIPE_TOPS * 1e12) * 1e3,
+                         "t_int8_ms": entries_launch * ncol_launch * slices * 2 / (INT8_MEASURED_TOPS * 1e12) * 1e3,
+                         "frac": (entries_launch * F_EVAL / (FP64_PIPE_TOPS * 1e12)
+                                  + entries_launch * ncol_launch * slices * 2 / (INT8_MEASURED_TOPS * 1e12))
+                                 / (per_launch_ms * 1e-3),
+                         "int8_peak_tops": INT8_MEASURED_TOPS},
                      "note": f"achieved = N^2 entries x {F_EVAL} FP64 ops (SASS) per launch / CUDA-event time of the "
                              "sketch phase per 160-column pass (speculative: columns beyond the converged d are computed, not used); peak = 148 SM x 64 FP64 lanes/clk x 1.965 GHz "
                              "(microbenchmarked DFMA 37.0 TF/s = 99.5 %); traffic = ncu dram bytes per launch"},
+        "whole_build_roofline": whole_build_roofline(st, ms, n, rows_local, sk_launches, ncol_launch, slices),
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -472,6 +525,9 @@ def time_workload(g, torch, stream, flush, name, steps=2):
                                   "unit": "TOP/s (FP64 pipe ops)", "frac": achieved / FP64_PIPE_TOPS,
                                   "per_launch_ms": per_launch, "launches": int(sk_launches),
                                   "fp64_ops_per_entry": f_eval}
+        exp = w["kernel"] == "exp"
+        res["whole_build_roofline"] = whole_build_roofline(st, ms, n, n, int(sk_launches), 160 if exp else 128,
+                                                           6 if exp else 7, f_eval)
     del H, T
     if upd is not None:
         del upd, opts

@@ -280,6 +280,17 @@ typedef struct {
                                  convergence tests, updateSamples replays, ID, shrink, B)   */
   double norm_est;            /* nu used by H2_TOL_LITERAL (opts.norm, or the power-iteration
                                  estimate when opts.norm <= 0), else 0                       */
+  /* ALGORITHMIC work of the symmetric construction per phase (what the method computes / moves,
+   * not what the kernels execute; DESIGN.md §6 "whole-build roofline"), this rank's clusters:
+   *   bsr   2 nc sum_{ordered pairs} rows_s cols_b flops; 8 B per block entry read + Y/Omega rows
+   *   cpqr  sum_c sum_{i<k_c} 4 (d - i)(m_c - i) flops (Householder, no pivot-norm work); panel in/out
+   *   id    sum_c k_c^2 (m_c - k_c) flops (T = R11^-1 R12); panel read + X written
+   *   shrink (counted under H2_PH_ID) sum_c 2 k_c (m_c - k_c) nc flops; panel rows in/out
+   *   gen   8 B written per unique D / B entry (flops 0: the entry chain is counted by the caller)
+   *   rand  8 B written per Omega entry
+   * The dense sketch's own work (N^2 entries per pass + the contraction) is not included. */
+  double work_flops[H2_NPHASE];
+  double work_bytes[H2_NPHASE];
 } h2_build_stats;
 /* CPQR kernel variants (h2_build_stats.cpqr_variants; H2_CQ_VARIANT=warp|smem|global forces one
  * where it applies): one warp per panel (m <= 64), one CTA per panel with the panel in shared

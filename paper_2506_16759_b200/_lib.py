@@ -88,7 +88,8 @@ class h2_build_stats(C.Structure):
                 ("bytes_U", C.c_int64), ("bytes_E", C.c_int64), ("bytes_B", C.c_int64), ("bytes_D", C.c_int64),
                 ("launches", C.c_int64), ("t_phase_ms", C.c_double * H2_NPHASE), ("t_total_ms", C.c_double),
                 ("verify_error", C.c_double), ("verify_rebuilds", C.c_int32), ("tol_safety_used", C.c_double),
-                ("cpqr_variants", C.c_int32), ("t_depth_ms", C.c_double * 64), ("norm_est", C.c_double)]
+                ("cpqr_variants", C.c_int32), ("t_depth_ms", C.c_double * 64), ("norm_est", C.c_double),
+                ("work_flops", C.c_double * H2_NPHASE), ("work_bytes", C.c_double * H2_NPHASE)]
 
 
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)

@@ -13,6 +13,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -636,6 +637,29 @@ struct Builder {
     timer.end();
   }
 
+  // ---------------------------------------------------------------- algorithmic work (stats)
+  // h2_build_stats.work_flops / work_bytes (DESIGN.md §6 "whole-build roofline"): what the
+  // method computes and moves per phase, counted on the host from the partition and the ranks
+  double wf[H2_NPHASE] = {}, wb[H2_NPHASE] = {};
+  std::map<int, std::pair<double, double>> bsr_work;   // depth t -> (sum rows_s cols_b, rows)
+  std::pair<double, double> bsr_entries(int t) {
+    auto it = bsr_work.find(t);
+    if (it != bsr_work.end()) return it->second;
+    const bool leaf = t == T.Dl;
+    const PairCSR& P = leaf ? T.near : T.far[t + 1];
+    const int tc = leaf ? T.Dl : t + 1;
+    auto rows = [&](int c) -> double {
+      return leaf ? (double)(T.end[T.Dl][c] - T.begin[T.Dl][c]) : (double)H.L(t + 1).k[c];
+    };
+    double e = 0, r = 0;
+    for (int c = cb(tc); c < ce(tc); ++c) {
+      const double rc = rows(c);
+      r += rc;
+      for (int q = P.ptr[c]; q < P.ptr[c + 1]; ++q) e += rc * rows(P.idx[q]);
+    }
+    return bsr_work[t] = {e, r};
+  }
+
   // ---------------------------------------------------------------- BSR subtraction on a panel of depth t
   // leaf (t == Dl): Y(I_tau) -= sum_{b in N_tau} D Om(I_b)   (L213)
   // inner: Y^l_t(rows of child nu) -= sum_{b in F_nu} B_{nu,b} Om^l_t(rows of b)   (L240-243)
@@ -674,6 +698,11 @@ struct Builder {
     a.Y = Yp;
     a.Om = Op;
     a.ldy = a.ldo = ld;
+    {
+      const auto er = bsr_entries(t);   // block entries (each orientation) read once, Y in/out, Omega once
+      wf[H2_PH_BSR] += 2.0 * nc * er.first;
+      wb[H2_PH_BSR] += 8.0 * er.first + 8.0 * nc * 3.0 * er.second;
+    }
     if (ex) launch_exact_bsr(a, st);
     else launch_bsr(a, st);
     timer.end();
@@ -744,6 +773,11 @@ struct Builder {
     timer.end();
     if (comm) comm_allgather_clusters(comm, L.d_k.p, 4, t, [](int c) { return (int64_t)c; }, st);
     L.k = download(L.d_k, L.nclus, st);
+    for (int c = cb(t); c < ce(t); ++c) {   // sum_{i<k} 4 (d-i)(m-i); panel read + written
+      const double kk = L.k[c], mm = L.m[c], dd = d;
+      wf[H2_PH_CPQR] += 4.0 * (kk * dd * mm - (dd + mm) * kk * (kk - 1) / 2 + (kk - 1) * kk * (2 * kk - 1) / 6);
+      wb[H2_PH_CPQR] += 16.0 * dd * mm;
+    }
   }
 
   void commit(int t, int sd = 0) {
@@ -784,6 +818,11 @@ struct Builder {
     for (int c = 0; c < L.nclus; ++c) a.max_red = std::max(a.max_red, L.m[c] - L.k[c]);
     if (ex) launch_exact_id(a, st);
     else launch_id(a, st);
+    for (int c = cb(t); c < ce(t); ++c) {   // T = R11^-1 R12: k^2 (m-k); R read, X written
+      const double kk = L.k[c], mm = L.m[c];
+      wf[H2_PH_ID] += kk * kk * (mm - kk);
+      wb[H2_PH_ID] += 8.0 * (mm * kk + kk * mm);
+    }
     if (comm)   // skeletons I~ of every cluster (B generation of cross-rank pairs, parent Ibar)
       comm_allgather_clusters(comm, L.d_skel.p, 4, t,
                               [&](int c) { return c < L.nclus ? L.roff[c] : L.rtot; }, st);
@@ -816,6 +855,11 @@ struct Builder {
     a.c1 = nc;
     a.max_k = L.max_k;
     launch_shrink_project(a, st);
+    for (int c = cb(u); c < ce(u); ++c) {   // 2 k (m-k) nc; Y^l, Omega^l rows in, skeleton rows out
+      const double kk = L.k[c], mm = L.m[c];
+      wf[H2_PH_ID] += 2.0 * kk * (mm - kk) * nc;
+      wb[H2_PH_ID] += 8.0 * nc * (2.0 * mm + 2.0 * kk);
+    }
     timer.end();
   }
 
@@ -1698,6 +1742,12 @@ struct Builder {
     }
     timer.collect(s.t_phase_ms);
     timer.collect_depths(s.t_depth_ms);
+    wb[H2_PH_GEN] = 8.0 * (double)(s.entries_D + s.entries_B);
+    wb[H2_PH_RAND] = 8.0 * (double)sketch_columns * (double)(row_e() - row_b());
+    for (int p = 0; p < H2_NPHASE; ++p) {
+      s.work_flops[p] = wf[p];
+      s.work_bytes[p] = wb[p];
+    }
     if (getenv("H2_TRACE")) {
       fprintf(stderr, "[h2 trace] host ms per phase:");
       for (int p = 0; p < H2_NPHASE; ++p) fprintf(stderr, " %.1f", timer.host_ms[p]);

@@ -290,6 +290,8 @@ def _stats_dict(s):
     d["rank_mean"] = {t: s.rank_mean[t] for t in range(lo, hi + 1)}
     d["t_phase_ms"] = {L.PHASES[i]: s.t_phase_ms[i] for i in range(L.H2_NPHASE)}
     d["t_depth_ms"] = {t: s.t_depth_ms[t] for t in range(lo, hi + 1)}
+    d["work_flops"] = {L.PHASES[i]: s.work_flops[i] for i in range(L.H2_NPHASE)}
+    d["work_bytes"] = {L.PHASES[i]: s.work_bytes[i] for i in range(L.H2_NPHASE)}
     return d
 
 
