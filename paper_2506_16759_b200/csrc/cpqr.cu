@@ -631,7 +631,10 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     H2_CHECK_LAUNCH();
     return H2_CQ_V_WARP;
   }
-  if (env_int("H2_CQ_ONEBAR", 0) != 0) {   // measured slower at C2 (33.6 vs 30.4 ms): opt-in
+  static const int onebar = env_int("H2_CQ_ONEBAR", 0);
+  // 1: every block-panel level (measured slower at C2: 33.6 vs 30.4 ms); 2: only levels with fewer
+  // panels than SMs (the latency-bound upper levels, 1024 threads per panel)
+  if (onebar == 1 || (onebar == 2 && a.nclusters < 148)) {
     // one-barrier kernel: perm + retired flags + (SMEM) the padded panel
     size_t sm = sizeof(double) * cq1_head_doubles(a.max_m);
     const size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);

@@ -253,8 +253,222 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// bsr2_kernel (round 2): the same product, the same DMMA sequence per accumulator (partners in
+// CSR order, k ascending, 4-deep DMMA k groups, zero-filled ragged k) -> bitwise the results of
+// bsr_kernel, with the instruction overhead per DMMA cut from ~16.6 to a few
+// (profiles/r2_bsr2.md: bsr_kernel was issue-bound at 61 % issue-slot use, 0.6 DMMA per 16
+// pipe cycles):
+//   * the A slab is stored in ONE layout ([r][kk], row stride 36 doubles) for both orientations:
+//     a transposed block is transposed by the loader's scatter (cp.async destinations), so the
+//     k loop has no orientation select;
+//   * the 8 k steps of a slab are unrolled with compile-time shared-memory offsets (LDS with
+//     immediate offsets: no address arithmetic per fragment);
+//   * every thread's loader positions are fixed per slab (one row pointer per element row,
+//     advanced by a constant), no div/mod per element.
+// CTA = (64-row tile, CW columns), 4 row warps x CW/32 column warps, warp tile 16 x 32 (2 x 4
+// DMMA m8n8k4 tiles).  NS-stage cp.async ring of (A slab 64 x 32, B slab 32 x CW).
+// ------------------------------------------------------------------------------------------
+constexpr int B2_LDA = 36;   // A slab row stride (doubles): conflict-free fragment reads
+constexpr int B2_MAXP = 256; // partners per row cluster staged in shared memory
+template <int CW, int NS, bool COLFAST>
+__global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
+  constexpr int NT = 4 * CW;                 // 128 threads per 32 columns
+  constexpr int NW = NT / 32;
+  constexpr int LDB = CW + 4;
+  constexpr int ASZ = BT_R * B2_LDA;         // 2304 doubles
+  constexpr int BSZ = BT_K * LDB;
+  constexpr int STG = ASZ + BSZ;
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ int st_nk[NS];
+  const int s = a.c_begin + (COLFAST ? blockIdx.y : blockIdx.x);
+  const int ms = a.cnt[s];
+  const int r0 = (COLFAST ? blockIdx.z : blockIdx.y) * BT_R;
+  const int cb = a.c0 + (COLFAST ? blockIdx.x : blockIdx.z) * CW;
+  const int nc = min(CW, a.c0 + a.ncols - cb);
+  if (r0 >= ms || nc <= 0) return;
+  const int e0 = a.ptr[s], e1 = a.ptr[s + 1];
+  if (e0 == e1) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bsm);
+  const int rows_here = min(BT_R, ms - r0);
+  // loader geometry (fixed per thread): B element (kk = warp / (CW/32) + 4 q, c = lane + 32 (warp % (CW/32)))
+  const int bc = lane + 32 * (warp % (CW / 32));
+  const int bk0 = warp / (CW / 32);
+  // partner metadata of this row cluster staged once in shared memory (one round trip per CTA
+  // instead of a dependent global-load chain idx -> uidx -> blk_off / cnt per slab, which was the
+  // top stall after the loop rewrite: long scoreboard on the slab addresses)
+  __shared__ int64_t p_blk[B2_MAXP], p_om[B2_MAXP];
+  __shared__ int p_mb[B2_MAXP];
+  __shared__ int s_items;
+  const int np = e1 - e0;
+  const bool staged = np <= B2_MAXP;
+  if (tid == 0) s_items = 0;
+  __syncthreads();
+  if (staged) {
+    int my = 0;
+    for (int q = tid; q < np; q += NT) {
+      const int e = e0 + q;
+      const int b = a.idx[e];
+      const int u = a.uidx ? a.uidx[e] : e;
+      const int mb = a.kcnt ? a.kcnt[b] : a.cnt[b];
+      const bool direct = a.tmode == 0 ? (a.us[u] == s) : (a.tmode == 1);
+      p_blk[q] = a.blk_off[u];
+      p_om[q] = a.ooff[b];
+      p_mb[q] = direct ? mb : -mb;
+      my += (mb + BT_K - 1) / BT_K;
+    }
+    if (my) atomicAdd(&s_items, my);
+  } else if (tid == 0) {
+    int n = 0;
+    for (int e = e0; e < e1; ++e) n += ((a.kcnt ? a.kcnt : a.cnt)[a.idx[e]] + BT_K - 1) / BT_K;
+    s_items = n;
+  }
+  __syncthreads();
+  const int nitems = s_items;
+  int le = e0, lk = 0;
+  auto load_next = [&](int buf) {
+    if (le >= e1) return;
+    int mb;
+    bool direct;
+    int64_t boff, orow;
+    if (staged) {
+      const int q = le - e0;
+      const int sm = p_mb[q];
+      mb = sm < 0 ? -sm : sm;
+      direct = sm > 0 || (sm == 0 && a.tmode != 2);
+      boff = p_blk[q];
+      orow = p_om[q];
+    } else {
+      const int b = a.idx[le];
+      const int u = a.uidx ? a.uidx[le] : le;
+      mb = a.kcnt ? a.kcnt[b] : a.cnt[b];
+      direct = a.tmode == 0 ? (a.us[u] == s) : (a.tmode == 1);
+      boff = a.blk_off[u];
+      orow = a.ooff[b];
+    }
+    const double* blk = a.blk + boff;
+    const int nk = min(BT_K, mb - lk);
+    const uint32_t sa = sbase + (uint32_t)(buf * STG) * 8u;
+    const uint32_t sb = sa + (uint32_t)ASZ * 8u;
+    if (direct) {
+      // lane = kk (a 256-byte row segment per warp), rows r = warp + NW q
+      const bool kok = lane < nk;
+      const double* src = blk + (int64_t)(r0 + warp) * mb + lk + lane;
+      const int64_t step = (int64_t)NW * mb;
+#pragma unroll
+      for (int q = 0; q < BT_R / NW; ++q) {
+        const int r = warp + NW * q;
+        const bool ok = kok && r < rows_here;
+        cp_async8(sa + (uint32_t)(r * B2_LDA + lane) * 8u, ok ? src : blk, ok);
+        src += step;
+      }
+    } else {
+      // stored block is b x s: entry (kk, r) at blk[(lk + kk) * ms + r0 + r]; a warp covers 8 r x
+      // 4 kk (64-byte global runs), scattered transposed into [r][kk]
+      const int rl = lane & 7, kl = lane >> 3;
+#pragma unroll
+      for (int q = 0; q < BT_R / NW; ++q) {
+        const int t = warp + NW * q;                      // 64 tiles of 8 r x 4 kk
+        const int r = 8 * (t & 7) + rl, kk = 4 * (t >> 3) + kl;
+        const bool ok = kk < nk && r < rows_here;
+        cp_async8(sa + (uint32_t)(r * B2_LDA + kk) * 8u, ok ? blk + (int64_t)(lk + kk) * ms + r0 + r : blk, ok);
+      }
+    }
+    {
+      const double* om = a.Om + orow * a.ldo + cb + bc;
+      const bool cok = bc < nc;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int kk = bk0 + 4 * q;
+        const bool ok = cok && kk < nk;
+        cp_async8(sb + (uint32_t)(kk * LDB + bc) * 8u, ok ? om + (int64_t)(lk + kk) * a.ldo : a.Om, ok);
+      }
+    }
+    if (tid == 0) st_nk[buf] = nk;
+    lk += BT_K;
+    if (lk >= mb) {
+      ++le;
+      lk = 0;
+    }
+  };
+  const int wr = warp & 3, wc = warp >> 2;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q) {
+    load_next(q);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  // fragment base offsets (doubles) inside a stage
+  const int offa = (wr * 16 + (lane >> 2)) * B2_LDA + (lane & 3);
+  const int offb = ASZ + (lane & 3) * LDB + wc * 32 + (lane >> 2);
+  for (int it = 0; it < nitems; ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NS - 2));
+    __syncthreads();
+    load_next((it + NS - 1) % NS);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const double* st = bsm + (it % NS) * STG;
+    const double* pa = st + offa;
+    const double* pb = st + offb;
+    const int ksteps = (st_nk[it % NS] + 3) >> 2;
+#pragma unroll
+    for (int ks = 0; ks < BT_K / 4; ++ks) {
+      if (ks < ksteps) {
+        const double a0 = pa[ks * 4], a1 = pa[8 * B2_LDA + ks * 4];
+        double bf[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = pb[ks * 4 * LDB + j * 8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0, bf[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1, bf[j]);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + wr * 16 + i * 8 + (lane >> 2);
+    if (r >= ms) continue;
+    double* y = a.Y + (a.yoff[s] + r) * a.ldy + cb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = wc * 32 + j * 8 + 2 * (lane & 3);
+      if (c < nc) y[c] = fma(alpha, acc[i][j][0], y[c]);
+      if (c + 1 < nc) y[c + 1] = fma(alpha, acc[i][j][1], y[c + 1]);
+    }
+  }
+}
+
+template <int CW, int NS, bool COLFAST>
+static void bsr2_go(const BsrArgs& a, double alpha, cudaStream_t st) {
+  const size_t sm = sizeof(double) * NS * (BT_R * B2_LDA + BT_K * (CW + 4));
+  H2_CUDA(cudaFuncSetAttribute(bsr2_kernel<CW, NS, COLFAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  if (COLFAST)
+    bsr2_kernel<CW, NS, COLFAST><<<dim3(div_up(a.ncols, CW), a.nclusters, div_up(a.max_rows, BT_R)), 4 * CW, sm, st>>>(
+        a, alpha);
+  else
+    bsr2_kernel<CW, NS, COLFAST><<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, CW)), 4 * CW, sm, st>>>(
+        a, alpha);
+  H2_CHECK_LAUNCH();
+}
+
 static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
+  // H2_BSR2: 0 = the round-1 kernel family below; 1 = bsr2 32-column tiles (column-fast grid for
+  // wide passes); 2 = bsr2 64-column tiles; 3 = bsr2 32-column tiles, 3-stage ring
+  static const int v2 = env_int("H2_BSR2", 1);
+  if (v2 != 0) {
+    const bool wide = a.ncols > 32;
+    if (v2 == 2 && a.ncols > 32) bsr2_go<64, 2, true>(a, alpha, st);
+    else if (v2 == 3) wide ? bsr2_go<32, 3, true>(a, alpha, st) : bsr2_go<32, 3, false>(a, alpha, st);
+    else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);
+    return;
+  }
   constexpr size_t sm32 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (32 + 4));
   constexpr size_t sm64 = sizeof(double) * BSR_NS * (BT_ASZ + BT_K * (64 + 4));
   // per launch: the attribute is per device (a process may drive several GPUs)

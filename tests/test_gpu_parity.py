@@ -315,11 +315,14 @@ def test_eager_sweep_bitwise(monkeypatch, case, opts):
     assert np.array_equal(H0._export(g._lib.H2_X_D), H1._export(g._lib.H2_X_D))
 
 
-@pytest.mark.parametrize("env,a,b", [("H2_CQ_REG", "0", "1"), ("H2_BSR_VAR", "0", "3"), ("H2_BSR_VAR", "0", "1")])
+@pytest.mark.parametrize("env,a,b", [("H2_CQ_REG", "0", "1"), ("H2_BSR_VAR", "0", "3"), ("H2_BSR_VAR", "0", "1"),
+                                     ("H2_BSR2", "0", "1"), ("H2_BSR2", "1", "2"), ("H2_BSR2", "1", "3")])
 def test_kernel_variants_bitwise(monkeypatch, env, a, b):
     """Performance variants that keep every element's operation order: the register-cached CPQR
     update (H2_CQ_REG) and the BSR tilings of wide passes (H2_BSR_VAR: 64-column tiles, 32-column
-    tiles in a column-fast grid, 160-column CTAs) give bitwise the same H^2 (variants are chosen
+    tiles in a column-fast grid, 160-column CTAs; H2_BSR2: the round-2 kernel with one shared-memory
+    layout for both block orientations vs the round-1 family, and its 64-column / 3-stage forms)
+    give bitwise the same H^2 (variants are chosen
     once per process: each side runs in its own subprocess)."""
     import subprocess, sys, os
     code = r'''
