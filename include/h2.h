@@ -353,8 +353,11 @@ h2_status h2_build(const h2_tree* tree, const h2_sketch* sketch, const h2_entry*
  * holds this rank's bases, the blocks touching its clusters, and every rank / skeleton index;
  * h2_matrix_allgather completes it on every rank (needed before h2_matvec / h2_export of the
  * bases and blocks, which fail with INVALID_ARG on a partial matrix).  nranks must be a power
- * of two <= 2^top_depth (subtree-aligned ownership); H2 + low-rank operators are single-GPU
- * only (INVALID_ARG). */
+ * of two <= 2^top_depth (subtree-aligned ownership).  H2 + low-rank operators (H2_S_H2_LOWRANK /
+ * H2_E_H2_LOWRANK, SURVEY §8(e) "Config 5's H2 sketch is a distributed h2_matvec") need the base
+ * complete on every rank (INVALID_ARG if partial): its matvec is row-sharded (upward pass over
+ * all clusters, couplings / downward pass / dense leaves over the owned clusters: no
+ * communication, bitwise the one-GPU rows) and its entries are extracted for the owned pairs. */
 h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                         const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
                         h2_build_stats* stats);

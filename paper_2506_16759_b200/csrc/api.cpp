@@ -205,7 +205,7 @@ struct Panel {
 };
 
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
-                 double beta, cudaStream_t st);
+                 double beta, cudaStream_t st, int rank = 0, int nranks = 1);
 KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st);
 void apply_sketch_op(const h2_tree& T, const h2_sketch& S, const double* Om, int64_t ldo, int nc, double* Y,
                      int64_t ldy, bool quarters, bool exact, cudaStream_t st);
@@ -519,8 +519,9 @@ struct Builder {
       if (S.kind == H2_S_DENSE_MATRIX) {
         dense_op_sketch(Od, ld, nc, Yd, st);
       } else if (S.kind == H2_S_H2_LOWRANK) {
-        // K_blk = A_H Omega + U (U^T Omega)
-        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
+        // K_blk = A_H Omega + U (U^T Omega); under a communicator the rank's
+        // own leaf rows only (row-sharded matvec of the complete, replicated base)
+        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st, R, P);
         DArr<double> scr;
         scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
         launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
@@ -958,11 +959,19 @@ struct Builder {
     int64_t gmax = 1;
     for (int64_t u = 0; u < F.nuniq(); ++u)
       gmax = std::max<int64_t>(gmax, (int64_t)La.k[F.us[u]] * L.k[F.ub[u]]);
-    const int grid = (int)std::min<int64_t>(F.nuniq(), 148 * 4);
+    DArr<int32_t> ul;
+    int64_t nb = F.nuniq();
+    if (comm) {   // the rank's owned pairs (as gen_B)
+      const std::vector<int32_t> l = owned_pairs(F, t);
+      ul.upload(l, st);
+      nb = (int64_t)l.size();
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 4));
     DArr<double> scratch;
     scratch.alloc(gmax * grid, st);
     UpdateBArgs ba{};
-    ba.nblocks = F.nuniq();
+    ba.nblocks = nb;
+    ba.ulist = ul.p;
     ba.us = T.d_far[t].us;
     ba.ub = T.d_far[t].ub;
     ba.kn = L.d_k.p;
@@ -1053,7 +1062,7 @@ struct Builder {
       if (S.kind == H2_S_DENSE_MATRIX) {
         dense_op_sketch(Od, ld, nc, Yd, st);
       } else if (S.kind == H2_S_H2_LOWRANK) {
-        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st);
+        matvec_impl(*S.base, Od, ld, Yd, ld, nc, 1.0, 0.0, st, R, P);
         DArr<double> scr;
         scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
         launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
@@ -1632,6 +1641,7 @@ struct Builder {
         timer.begin(H2_PH_GEN);
         UpdateDArgs a{};
         a.nblocks = g.nblocks;
+        a.ulist = g.ulist;
         a.us = g.us;
         a.ub = g.ub;
         a.cnt = T.d_leaf_size;
@@ -1758,11 +1768,19 @@ struct Builder {
 
 // y = alpha K_H x + beta y (CS4: upward pass, couplings, downward pass, dense leaves); stream-ordered,
 // workspaces released stream-ordered on return
+// Row-sharded form (rank, nranks > 1; S§8(e) "Config 5's H^2 sketch is a distributed h2_matvec"):
+// the matrix is complete on every rank and x is replicated (the Omega stream is regenerated on
+// every rank); the upward pass runs over all clusters (O(N q), the cheap part), the couplings,
+// the downward pass and the dense leaves only over the rank's owned clusters (subtree-aligned
+// ranges own_begin), so y is computed for the rank's leaf rows only -- no communication, and
+// each owned row's arithmetic is the one-GPU arithmetic (bitwise).
 void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
-                 double beta, cudaStream_t st) {
+                 double beta, cudaStream_t st, int rank, int nranks) {
   const h2_matrix* H = &Hm;
     const h2_tree& T = *H->tree;
   const int Dl = H->Dl, top = H->top;
+  auto ob = [&](int t) { return nranks > 1 ? own_begin(t, rank, nranks) : 0; };
+  auto oe = [&](int t) { return nranks > 1 ? own_begin(t, rank + 1, nranks) : (1 << t); };
   // non-symmetric: the upward pass uses the column side (V, F), the downward pass the row side
   const int up = H->nonsym ? 1 : 0;
   std::vector<DArr<double>> xh(Dl + 1), yh(Dl + 1);
@@ -1797,7 +1815,8 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
     const Level& L = H->L(t);
     if (T.far[t].nnz() == 0) continue;
     SpmmArgs s{};
-    s.nclusters = L.nclus;
+    s.c_begin = ob(t);
+    s.nclusters = oe(t) - ob(t);
     s.max_rows = L.max_k;
     s.yoff = s.xoff = L.d_roff.p;
     s.cnt = L.d_k.p;
@@ -1825,7 +1844,8 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
   for (int t = top; t <= Dl; ++t) {
     const Level& L = H->L(t);
     DownArgs a{};
-    a.nclusters = L.nclus;
+    a.c_begin = ob(t);
+    a.nclusters = oe(t) - ob(t);
     a.ioff = (t == Dl) ? T.d_leaf_begin : L.d_poff.p;
     a.m = L.d_m.p;
     a.k = L.d_k.p;
@@ -1845,7 +1865,8 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
   // dense leaves  y += alpha sum_{b in N} D x
   {
     SpmmArgs s{};
-    s.nclusters = 1 << Dl;
+    s.c_begin = ob(Dl);
+    s.nclusters = oe(Dl) - ob(Dl);
     s.max_rows = H->L(Dl).max_m;
     s.yoff = s.xoff = T.d_leaf_begin;
     s.cnt = T.d_leaf_size;
@@ -2195,8 +2216,8 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
       H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks &&
                      (!dist || comm->allgatherv || comm->nccl),
                  "h2_build_dist: bad communicator");
-    H2_REQUIRE(!dist || (sketch->kind != H2_S_H2_LOWRANK && entry->kind != H2_E_H2_LOWRANK),
-               "h2_build_dist: H2 + low-rank operators are single-GPU only");
+    // H2 + low-rank operators under a communicator: the base must be complete on every rank
+    // (checked above: not partial); its matvec is row-sharded, its entries extracted per owned pair
     // subtree-aligned ownership at every processed depth: a power-of-two rank count with at
     // least one cluster per rank at the coarsest processed depth
     H2_REQUIRE(!dist || ((comm->nranks & (comm->nranks - 1)) == 0 && tree->top >= 0 &&

@@ -438,6 +438,222 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
   }
 }
 
+// cpqr2 (round 2, the default block-panel kernel): one barrier per pivot step and NO serial
+// reflector warp.  profiles/r2_cpqr2.md: in cpqr_kernel 15 warps waited at a barrier (36 % of
+// all stall samples) while warp 0 swapped the pivot row, reduced its norm and divided d entries
+// by alpha - beta.  Here
+//   * x2 = sum_{r > i} A(p, r)^2 of the next pivot is a by-product of the previous trailing update
+//     (each row keeps S2_j = sum_{r >= i+2} x_r^2 beside its norm^2 = x_{i+1}^2 + S2_j), so every
+//     warp derives the reflector scalars (alpha, beta, tau, 1/(alpha - beta)) redundantly in O(1)
+//     from shared memory -- same data, same order, the same bits in every warp;
+//   * rows are never swapped: the pivot row is retired in place (its R column is final except
+//     R(i, i) = beta, written one step later when nobody reads the row), the active rows are a
+//     list (double-buffered in shared memory; warp 0 writes the next step's list, the pivot
+//     swap-removed, while every warp reads the current one), so the update loop visits only the
+//     m - i - 1 active rows;
+//   * v is never materialised: the update reads the pivot row and scales by 1/(alpha - beta)
+//     (LAPACK dlarfg scales x by 1/(alpha - beta) too).
+// Decisions as R12-R14 (max recomputed norm, ties -> lowest row index, dlarfg signs); the norms
+// are recomputed from the updated entries every step (no downdating); certificates as before.
+// The factored panel is written to W in pivot order, redundant rows in ascending row index.
+__host__ __device__ inline size_t cq2_head_doubles(int max_m) {
+  // x2s (max_m doubles) + lists (2 max_m int) + retired flags (max_m bytes), 16-byte aligned
+  return (size_t)max_m + ((size_t)max_m * 9 + 15) / 16 * 2;
+}
+
+template <bool SMEM, int NT>
+__global__ void __launch_bounds__(NT) cpqr2_kernel(CpqrArgs a, double* __restrict__ scratch) {
+  constexpr int NW = NT / 32;
+  constexpr int RPP = NT / CQ_TPR;
+  extern __shared__ double smem[];
+  const int c = a.c_begin + blockIdx.x;
+  const int m = a.m[c];
+  const int d = a.d;
+  const int LD = SMEM ? cq_ld(d) : d;
+  double* x2s = smem;                                                 // max_m
+  int* lst = reinterpret_cast<int*>(smem + a.max_m);                  // 2 x max_m
+  unsigned char* retired = reinterpret_cast<unsigned char*>(lst + 2 * a.max_m);   // max_m
+  double* spanel = smem + cq2_head_doubles(a.max_m);
+  __shared__ Top2 red2[2][NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
+  const int64_t off = a.poff[c];
+  int* gperm = a.perm + off;
+  double* A = SMEM ? spanel : scratch + off * d;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += NT) {
+    const int64_t j = e / d;
+    A[j * LD + (e - j * d)] = a.Y[(off + j) * a.ldy + (e - j * d)];
+  }
+  for (int j = threadIdx.x; j < m; j += NT) {
+    lst[j] = j;
+    retired[j] = 0;
+  }
+  __syncthreads();
+  auto row_sum = [&](double x) {
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    return x;
+  };
+  auto warp_best = [&](Top2 t) {
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      Top2 u;
+      u.v = __shfl_xor_sync(0xffffffffu, t.v, o);
+      u.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+      u.s = __shfl_xor_sync(0xffffffffu, t.s, o);
+      t = top2_merge(t, u);
+    }
+    return t;
+  };
+  {
+    // initial norms over r >= 0 and S2 over r >= 1
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    for (int j0 = 0; j0 < m; j0 += RPP) {
+      const int j = j0 + rloc;
+      double s2 = 0.0, x0 = 0.0;
+      if (j < m) {
+        for (int r = sub; r < d; r += CQ_TPR) {
+          const double x = A[(int64_t)j * LD + r];
+          if (r == 0) x0 = x;
+          else s2 = fma(x, x, s2);
+        }
+      }
+      s2 = row_sum(s2);
+      x0 = row_sum(x0);
+      if (j < m) {
+        if (sub == 0) x2s[j] = s2;
+        loc = top2_merge(loc, Top2{sqrt(fma(x0, x0, s2)), j, -1.0});
+      }
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red2[0][warp] = loc;
+  }
+  const int kfull = min(d, m);
+  const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
+  double min_gap = INFINITY, margin = INFINITY;
+  int k = 0, p_prev = -1;
+  double beta_prev = 0.0;
+  for (int i = 0;; ++i) {
+    __syncthreads();
+    if (p_prev >= 0) {   // finalize the previous pivot row: R(i-1, i-1) = beta, zeros below
+      double* Aq = A + (int64_t)p_prev * LD;
+      for (int r = i + threadIdx.x; r < d; r += NT) Aq[r] = 0.0;
+      if (threadIdx.x == 0) {
+        Aq[i - 1] = beta_prev;
+        retired[p_prev] = 1;
+        gperm[i - 1] = p_prev;
+      }
+    }
+    Top2 t = lane < NW ? red2[i & 1][lane] : Top2{-1.0, 0x7fffffff, -1.0};
+    t = warp_top2(t);
+    if (i >= m) break;
+    if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    if (i == kcap || !(t.v > a.eps)) {
+      k = i;
+      break;
+    }
+    if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    const int p = t.i;
+    const double* Ap = A + (int64_t)p * LD;
+    // Householder reflector of the pivot column (LAPACK dlarfg) from shared scalars
+    const double alpha = Ap[i];
+    const double x2 = x2s[p];
+    const double xnorm = sqrt(x2);
+    double tau, beta;
+    if (xnorm == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+    } else {
+      const double h = hypot(alpha, xnorm);
+      beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
+      tau = (beta - alpha) / beta;
+    }
+    const double rden = 1.0 / (alpha - beta);
+    const int cnt = m - i;                       // active rows (incl. p) in lst[i & 1]
+    const int* L = lst + (i & 1) * a.max_m;
+    if (warp == 0) {                             // next step's list: p swap-removed
+      int* Ln = lst + ((i + 1) & 1) * a.max_m;
+      const int last = L[cnt - 1];
+      for (int q = lane; q < cnt - 1; q += 32) {
+        const int v = L[q];
+        Ln[q] = v == p ? last : v;
+      }
+    }
+    // trailing update of the active rows (p excluded) + next norms, S2 and local pivot
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    const int r0 = (i + 1) + ((sub - (i + 1)) & (CQ_TPR - 1));   // first r > i with r = sub mod 8
+    for (int q0 = 0; q0 < cnt; q0 += RPP) {
+      const int q = q0 + rloc;
+      const int j = q < cnt ? L[q] : p;
+      const bool act = j != p;
+      double* Aj = A + (int64_t)j * LD;
+      double s = 0.0, aji = 0.0;
+      if (act) {
+        aji = Aj[i];
+        if (tau != 0.0)
+          for (int r = r0; r < d; r += CQ_TPR) s = fma(Ap[r], Aj[r], s);
+      }
+      s = row_sum(s);
+      __syncwarp();   // every lane of the row read A(j, i) before it is updated
+      double s2 = 0.0, x1 = 0.0;
+      if (act) {
+        if (tau != 0.0) {
+          const double w = tau * fma(s, rden, aji);
+          const double wd = w * rden;
+          if (sub == 0) Aj[i] = aji - w;
+          for (int r = r0; r < d; r += CQ_TPR) {
+            const double x = fma(-wd, Ap[r], Aj[r]);
+            Aj[r] = x;
+            if (r == i + 1) x1 = x;
+            else s2 = fma(x, x, s2);
+          }
+        } else {
+          for (int r = r0; r < d; r += CQ_TPR) {
+            const double x = Aj[r];
+            if (r == i + 1) x1 = x;
+            else s2 = fma(x, x, s2);
+          }
+        }
+      }
+      s2 = row_sum(s2);
+      x1 = row_sum(x1);   // one owner, exact zeros elsewhere
+      if (act) {
+        if (sub == 0) x2s[j] = s2;
+        loc = top2_merge(loc, Top2{sqrt(fma(x1, x1, s2)), j, -1.0});
+      }
+    }
+    loc = warp_best(loc);
+    if (lane == 0) red2[(i + 1) & 1][warp] = loc;
+    p_prev = p;
+    beta_prev = beta;
+    k = i + 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int q = k;   // redundant rows after the pivots, ascending row index
+    for (int j = 0; j < m; ++j)
+      if (!retired[j]) gperm[q++] = j;
+  }
+  __syncthreads();
+  double* Wc = a.W + off * d;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += NT) {
+    const int64_t q = e / d;
+    Wc[e] = A[(int64_t)gperm[q] * LD + (e - q * d)];
+  }
+  if (threadIdx.x == 0) {
+    a.k[c] = k;
+    a.cert[2 * c] = min_gap;
+    a.cert[2 * c + 1] = margin;
+  }
+}
+
+template <bool SMEM, int NT>
+static void cpqr2_launch(const CpqrArgs& a, size_t sm, double* scratch, cudaStream_t st) {
+  H2_CUDA(cudaFuncSetAttribute(cpqr2_kernel<SMEM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr2_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a, scratch);
+}
+
 template <bool SMEM, int NT>
 static void cpqr1_launch(const CpqrArgs& a, size_t sm, double* scratch, cudaStream_t st) {
   H2_CUDA(cudaFuncSetAttribute(cpqr1_kernel<SMEM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -630,6 +846,28 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     cpqr_warp_kernel<<<div_up(a.nclusters, CW_WPB), 32 * CW_WPB, wsm, st>>>(a);
     H2_CHECK_LAUNCH();
     return H2_CQ_V_WARP;
+  }
+  static const int cq2 = env_int("H2_CQ2", 1);
+  if (cq2 != 0 && env_int("H2_CQ_ONEBAR", 0) == 0) {
+    // cpqr2 (default): x2 by-product, in-place retirement, active-row list, one barrier per step
+    size_t sm = sizeof(double) * cq2_head_doubles(a.max_m);
+    const size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
+    const int NTsel = a.max_m > 64 && a.nclusters < 148 ? 1024 : (a.max_m > 32 ? 512 : 256);
+    if (sm + panel <= 200 * 1024 && force != H2_CQ_V_GLOBAL) {
+      sm += panel;
+      if (NTsel == 1024) cpqr2_launch<true, 1024>(a, sm, nullptr, st);
+      else if (NTsel == 512) cpqr2_launch<true, 512>(a, sm, nullptr, st);
+      else cpqr2_launch<true, 256>(a, sm, nullptr, st);
+      H2_CHECK_LAUNCH();
+      return H2_CQ_V_SMEM;
+    }
+    double* scr = static_cast<double*>(cache_alloc(sizeof(double) * std::max<int64_t>(a.rows * a.d, 1), st));
+    if (NTsel == 1024) cpqr2_launch<false, 1024>(a, sm, scr, st);
+    else if (NTsel == 512) cpqr2_launch<false, 512>(a, sm, scr, st);
+    else cpqr2_launch<false, 256>(a, sm, scr, st);
+    H2_CHECK_LAUNCH();
+    cache_free(scr, st);
+    return H2_CQ_V_GLOBAL;
   }
   static const int onebar = env_int("H2_CQ_ONEBAR", 0);
   // 1: every block-panel level (measured slower at C2: 33.6 vs 30.4 ms); 2: only levels with fewer

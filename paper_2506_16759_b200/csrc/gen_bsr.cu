@@ -527,6 +527,7 @@ void launch_bsr(const BsrArgs& a, cudaStream_t st) { bsr_launch(a, -1.0, st); }
 void launch_spmm(const SpmmArgs& s, cudaStream_t st) {
   BsrArgs a{};
   a.nclusters = s.nclusters;
+  a.c_begin = s.c_begin;
   a.yoff = s.yoff;
   a.ooff = s.xoff;
   a.cnt = s.cnt;

@@ -134,7 +134,8 @@ void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om
 
 // ---- entries: D blocks of M over unique near pairs u (stored orientation us <= ub)
 __global__ void __launch_bounds__(256) update_D_kernel(UpdateDArgs a) {
-  for (int64_t u = blockIdx.x; u < a.nblocks; u += gridDim.x) {
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
     const int ms = a.cnt[s], mb = a.cnt[b];
     const double* src = a.Dbase + a.off[u];
@@ -212,7 +213,8 @@ void launch_expand_rows(const ExpandArgs& a, cudaStream_t st) {
 // ---- B blocks of M over unique far pairs of depth t: B = R_s (B_A R_b^T) + U(I~_s) U(I~_b)^T
 __global__ void __launch_bounds__(256) update_B_kernel(UpdateBArgs a) {
   double* G = a.scratch + (int64_t)blockIdx.x * a.gmax;
-  for (int64_t u = blockIdx.x; u < a.nblocks; u += gridDim.x) {
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t u = a.ulist ? a.ulist[q] : q;
     const int s = a.us[u], b = a.ub[u];
     const int kns = a.kn[s], knb = a.kn[b], kbs = a.kb[s], kbb = a.kb[b];
     double* out = a.out + a.out_off[u];

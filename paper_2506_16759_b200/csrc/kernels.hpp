@@ -193,6 +193,7 @@ struct DownArgs {
   double alpha;
   int accumulate;          // 1: yout += ..., 0: yout = ...
   int32_t max_out;        // max m over the clusters (grid sizing)
+  int32_t c_begin;        // clusters c_begin .. c_begin + nclusters - 1 (a rank's owned range)
 };
 void launch_downward(const DownArgs& a, cudaStream_t st);
 // y(rows of s) += alpha * sum_b Blk(s,b) x(rows of b)   (coupling B / dense D products)
@@ -216,6 +217,7 @@ struct SpmmArgs {
   int64_t ldy;
   int q;
   double alpha;
+  int32_t c_begin;        // row clusters c_begin .. c_begin + nclusters - 1
 };
 void launch_spmm(const SpmmArgs& a, cudaStream_t st);
 
@@ -227,6 +229,7 @@ void launch_lowrank_sketch(const double* U, int64_t ldu, int r, const double* Om
                            int64_t ldv = 0);
 struct UpdateDArgs {            // D_new = D_A + U(I_s) U(I_b)^T over unique near pairs
   int64_t nblocks;
+  const int32_t* ulist;         // unique pairs to produce (a rank's owned pairs); NULL: 0..nblocks-1
   const int32_t *us, *ub, *cnt;
   const int64_t *begin, *off;
   const double* Dbase;
@@ -254,6 +257,7 @@ struct ExpandArgs {             // rows of A's expanded basis at the new skeleto
 void launch_expand_rows(const ExpandArgs& a, cudaStream_t st);
 struct UpdateBArgs {            // B_new = R_s B_A R_b^T + U(I~_s) U(I~_b)^T over unique far pairs
   int64_t nblocks;
+  const int32_t* ulist;         // unique pairs to produce (a rank's owned pairs); NULL: 0..nblocks-1
   const int32_t *us, *ub, *kn, *kb;
   double* out;
   const int64_t* out_off;

@@ -48,7 +48,7 @@ void launch_upward(const UpArgs& a, cudaStream_t st) {
 
 // yout(ioff+j, q) (+)= alpha * sum_i X(j, i) yh(roff+i, q)
 __global__ void __launch_bounds__(256) downward_kernel(DownArgs a) {
-  const int c = blockIdx.x;
+  const int c = a.c_begin + blockIdx.x;
   const int m = a.m[c], k = a.k[c];
   const int j0 = blockIdx.y * MV_ROWS + (threadIdx.x >> 5) * 4;
   if (blockIdx.y * MV_ROWS >= m) return;

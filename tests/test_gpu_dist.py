@@ -48,6 +48,7 @@ def _worker(rank, world, port, case, q):
         from synth import uniform_points
         n, adaptive = case[:2]
         exact = len(case) > 2 and case[2]
+        mode = case[3] if len(case) > 3 else None
         X = uniform_points(n, 3, 0)
         T = g.Tree(X, 64)
         comm = Comm()
@@ -56,6 +57,16 @@ def _worker(rank, world, port, case, q):
         if exact:   # exact-order kernels under sharding (rational test kernel)
             opts["exact_order"] = 1
             kern = ("rational", 0.3)
+        if mode is not None:
+            # H^2 + low-rank operators under sharding (S§8(e) "Config 5's H^2 sketch is a distributed
+            # h2_matvec"): the base is complete on every rank (built here per rank), its matvec
+            # row-sharded, its entries extracted per owned pair
+            from synth import lowrank_factor
+            Hb = g.build(T, kern, 1e-8)
+            if mode == "update":     # BASELINE configs[4] shape: M = A_H + U U^T
+                opts["update"] = (Hb, torch.from_numpy(lowrank_factor(n, 16)).cuda())
+            else:                    # NEXT #1: O(N) H^2-matvec sketch of the base, kernel entries
+                opts["h2_sketch"] = Hb
         Hd = g.build(T, kern, 1e-6, comm=comm, **opts)
         partial_refused = False
         try:
@@ -76,10 +87,12 @@ def _worker(rank, world, port, case, q):
 
 
 @pytest.mark.parametrize("world,case", [(2, (5000, True)), (4, (5000, True)), (2, (8192, False)),
-                                        (4, (8192, False)), (8, (32768, True)), (2, (3000, True, True))])
+                                        (4, (8192, False)), (8, (32768, True)), (2, (3000, True, True)),
+                                        (2, (6000, True, False, "update")), (4, (6000, True, False, "h2sketch"))])
 def test_distributed_build_bitwise(world, case):
-    """world 8 (the 8 x B200 target's shard count, top depth >= 3 at N = 2^15) and the exact-order
-    kernels under sharding included."""
+    """world 8 (the 8 x B200 target's shard count, top depth >= 3 at N = 2^15), the exact-order
+    kernels under sharding, and the H^2 + low-rank operators (row-sharded H^2 matvec sketch,
+    per-owned-pair entry extraction) included."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
