@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(NT) cpqr1_kernel(CpqrArgs a, double* __restric
   }
 }
 
-// cpqr2 (round 2, the default block-panel kernel): one barrier per pivot step and NO serial
+// cpqr2 (round 2, opt-in H2_CQ2=1): one barrier per pivot step and NO serial
 // reflector warp.  profiles/r2_cpqr2.md: in cpqr_kernel 15 warps waited at a barrier (36 % of
 // all stall samples) while warp 0 swapped the pivot row, reduced its norm and divided d entries
 // by alpha - beta.  Here
@@ -847,9 +847,12 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     H2_CHECK_LAUNCH();
     return H2_CQ_V_WARP;
   }
-  static const int cq2 = env_int("H2_CQ2", 1);
+  // cpqr2 (opt-in H2_CQ2=1): x2 by-product, in-place retirement, active-row list, one barrier per
+  // step -- measured slower at C2 (33.2 vs 30.3 ms summed kernel time, ncu launch lists
+  // profiles/r2_cpqr2.md): the shorter critical path does not pay for the extra shuffles and the
+  // list indirection; the big (global-panel) levels are L2-latency bound either way
+  const int cq2 = env_int("H2_CQ2", 0);   // per launch (tests switch it)
   if (cq2 != 0 && env_int("H2_CQ_ONEBAR", 0) == 0) {
-    // cpqr2 (default): x2 by-product, in-place retirement, active-row list, one barrier per step
     size_t sm = sizeof(double) * cq2_head_doubles(a.max_m);
     const size_t panel = sizeof(double) * (size_t)a.max_m * cq_ld(a.d);
     const int NTsel = a.max_m > 64 && a.nclusters < 148 ? 1024 : (a.max_m > 32 ? 512 : 256);

@@ -82,17 +82,20 @@ def test_build_parity(case, adaptive):
     compare_matvec(Hg, Ho, certified, bound)
 
 
-@pytest.mark.parametrize("variant", ["warp", "smem", "global"])
+@pytest.mark.parametrize("variant", ["warp", "smem", "global", "smem2", "global2"])
 @pytest.mark.parametrize("case", ["cov3d_5000", "ie_grid16"])
 def test_build_parity_each_cpqr_variant(monkeypatch, case, variant):
     """Every CPQR kernel variant (warp per panel / CTA with the panel in shared memory / CTA with
-    the panel in global W, the one large inner panels take at N = 2^18) forced on every level of
-    an adaptive build: same skeleton / rank / sample parity with the oracle, and the stats name
-    the variant that ran."""
+    the panel in global W, the one large inner panels take at N = 2^18; "2": the opt-in cpqr2
+    kernel, H2_CQ2=1) forced on every level of an adaptive build: same skeleton / rank / sample
+    parity with the oracle, and the stats name the variant that ran."""
     mk, kind, p, leaf, tol = CASES[case]
     X = mk()
     Ho, op = oracle_build(X, kind, p, leaf, tol)
     T = g.Tree(X, leaf)
+    if variant.endswith("2"):
+        monkeypatch.setenv("H2_CQ2", "1")
+        variant = variant[:-1]
     monkeypatch.setenv("H2_CQ_VARIANT", variant)
     Hg = g.build(T, (kind, p), tol)
     bit = {"warp": g._lib.H2_CQ_V_WARP, "smem": g._lib.H2_CQ_V_SMEM, "global": g._lib.H2_CQ_V_GLOBAL}[variant]
