@@ -672,7 +672,10 @@ static void cpqr_launch_e(const CpqrArgs& a, size_t sm, cudaStream_t st) {
 // the global-panel levels, which ran two)
 template <bool SMEM, int NT>
 static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
-  static const bool reg = env_int("H2_CQ_REG", 0) != 0;
+  // H2_CQ_REG: 0 off, 1 every block panel, 2 shared-memory panels only (one CTA per SM there
+  // anyway, so the 128 registers cost no occupancy)
+  const int regm = env_int("H2_CQ_REG", 0);
+  const bool reg = regm == 1 || (regm == 2 && SMEM);
   const int need = (a.d + CQ_TPR - 1) / CQ_TPR;
   if (reg && need <= 8) cpqr_launch_e<SMEM, NT, 8>(a, sm, st);
   else if (reg && need <= 16) cpqr_launch_e<SMEM, NT, 16>(a, sm, st);

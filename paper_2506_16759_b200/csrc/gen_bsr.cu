@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
 // bsr2_kernel (round 2): the same product, the same DMMA sequence per accumulator (partners in
 // CSR order, k ascending, 4-deep DMMA k groups, zero-filled ragged k) -> bitwise the results of
 // bsr_kernel, with the instruction overhead per DMMA cut from ~16.6 to a few
-// (profiles/r2_bsr2.md: bsr_kernel was issue-bound at 61 % issue-slot use, 0.6 DMMA per 16
+// (profiles/r2_bsr2_ncu.md: bsr_kernel was issue-bound at 61 % issue-slot use, 0.6 DMMA per 16
 // pipe cycles):
 //   * the A slab is stored in ONE layout ([r][kk], row stride 36 doubles) for both orientations:
 //     a transposed block is transposed by the loader's scatter (cp.async destinations), so the
@@ -415,18 +415,25 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
     const double* pa = st + offa;
     const double* pb = st + offb;
     const int ksteps = (st_nk[it % NS] + 3) >> 2;
+    auto kstep = [&](int ks) {
+      const double a0 = pa[ks * 4], a1 = pa[8 * B2_LDA + ks * 4];
+      double bf[4];
 #pragma unroll
-    for (int ks = 0; ks < BT_K / 4; ++ks) {
-      if (ks < ksteps) {
-        const double a0 = pa[ks * 4], a1 = pa[8 * B2_LDA + ks * 4];
-        double bf[4];
+      for (int j = 0; j < 4; ++j) bf[j] = pb[ks * 4 * LDB + j * 8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = pb[ks * 4 * LDB + j * 8];
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0, bf[j]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0, bf[j]);
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1, bf[j]);
+    };
+    if (ksteps == BT_K / 4) {
+      // full slab: no per-step guard, so the fragment loads of later k steps can be scheduled
+      // ahead of the current step's DMMAs
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1, bf[j]);
-      }
+      for (int ks = 0; ks < BT_K / 4; ++ks) kstep(ks);
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < BT_K / 4; ++ks)
+        if (ks < ksteps) kstep(ks);
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
