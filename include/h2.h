@@ -73,6 +73,17 @@ typedef struct {
 } h2_tree_info;
 h2_status h2_tree_get_info(const h2_tree* tree, h2_tree_info* info);
 
+/* h2_tree_build with the block partition built on a host thread: returns once the KD ordering
+ * (R4) and the tree-order coordinates exist.  Every call that reads the partition
+ * (h2_tree_get_info, h2_tree_export of near pairs, h2_tree_far_count / export_far, h2_build*)
+ * waits for it; h2_build with the built-in exp dense-kernel sketch (symmetric, one GPU, RMS
+ * tolerance rule) launches its first sketch pass BEFORE waiting, so the host's dual traversal
+ * and CSR construction overlap the O(N^2) pass on the GPU (the end-to-end path of bench.py).
+ * Arguments, ownership and errors as h2_tree_build; an error of the partition itself is reported
+ * by the first call that waits for it. */
+h2_status h2_tree_build_async(const double* coords_host, int64_t n, int32_t dim, int32_t leaf_size, double eta,
+                              int32_t dist_rule, h2_tree** out);
+
 /* Host copies of the partition.  perm[n] (tree index -> original index), begin/end of every
  * cluster in heap order (node (depth t, index c) at position 2^t - 1 + c; total 2^(Dl+1)-1
  * entries each), near pairs (near_nnz x 2, sorted), far pairs of one depth (sorted).

@@ -104,6 +104,7 @@ class h2_comm(C.Structure):
 _P = C.c_void_p
 SIGNATURES = {
     "h2_tree_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)]),
+    "h2_tree_build_async": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.POINTER(_P)]),
     "h2_tree_import": (C.c_int, [C.POINTER(h2_tree_desc), C.POINTER(_P)]),
     "h2_tree_get_info": (C.c_int, [_P, C.POINTER(h2_tree_info)]),
     "h2_tree_export": (C.c_int, [_P, _P, _P, _P, _P]),

@@ -206,6 +206,7 @@ struct Panel {
 
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                  double beta, cudaStream_t st, int rank = 0, int nranks = 1);
+void ensure_partition_uploaded(const h2_tree* tree);
 KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st);
 void apply_sketch_op(const h2_tree& T, const h2_sketch& S, const double* Om, int64_t ldo, int nc, double* Y,
                      int64_t ldy, bool quarters, bool exact, cudaStream_t st);
@@ -1142,13 +1143,14 @@ struct Builder {
 
   void run_eager() {
     const int Dl = T.Dl;
-    const int top = T.top < 0 ? Dl : T.top;
     d = std::min(o.d_init, o.d_max);
     dw = pass_width(0);
     // line 1: Y = K_blk(Omega) for the first pass into the leaf panel (Y^loc in place)
     cur.alloc(T.n, ld_for(T.n, dw), st);
     draw_pass(cur.Y.p, cur.O.p, cur.ld, 0, dw);
     consume(0);
+    tree_ready();                                   // the partition (overlapped with the pass)
+    const int top = H.top;
     timer.mark(Dl);
     gen_D();                                        // line 212
     setup_level(Dl);
@@ -1570,6 +1572,21 @@ struct Builder {
     }
   }
 
+  // the block partition is needed from here on (an asynchronous tree: wait for its host thread
+  // and upload the CSR descriptors), and the level structure of H follows from its top depth
+  bool tree_ready_done = false;
+  void tree_ready() {
+    if (tree_ready_done) return;
+    tree_ready_done = true;
+    ensure_partition_uploaded(&T);
+    const int Dl = T.Dl;
+    const int top = T.top < 0 ? Dl : T.top;
+    H.top = top;
+    H.Dl = Dl;
+    H.n = T.n;
+    H.lv.resize(Dl - top + 1);
+  }
+
   void run() {
     // internal high-priority stream, ordered after the caller's stream
     user_st = st;
@@ -1577,12 +1594,13 @@ struct Builder {
     timer.st = st;
     stream_after(st, user_st);
     const int Dl = T.Dl;
-    const int top = T.top < 0 ? Dl : T.top;
-    H.top = top;
-    H.Dl = Dl;
-    H.n = T.n;
-    H.lv.resize(Dl - top + 1);
     ex = o.exact_order != 0;
+    // the first tensor-core sketch pass needs only the ordering: with an asynchronous tree it is
+    // launched before the partition is waited for (run_eager), so the host's dual traversal and
+    // CSR construction overlap the O(N^2) pass on the GPU
+    const bool lazy = env_int("H2_EAGER", 1) != 0 && S.kind == H2_S_DENSE_KERNEL && S.kern.kind == H2_K_EXP &&
+                      !comm && o.tol_rule == H2_TOL_RMS && !o.exact_order;
+    if (!lazy) tree_ready();
     if (S.kind == H2_S_DENSE_KERNEL) {
       skp = tree_kernel(&T, S.kern, st);
       spec_on = !ex && quarters() && sketch_tc_supported(skp) && env_int("H2_SK_TC", 1) != 0 &&
@@ -1615,7 +1633,7 @@ struct Builder {
     gen_D();
     setup_level(Dl);
     bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
-    run_levels(top, Dl);
+    run_levels(H.top, Dl);
   }
 
   void gen_D() {
@@ -1892,12 +1910,23 @@ void matvec_impl(const h2_matrix& Hm, const double* x, int64_t ldx, double* y, i
 }
 
 // the tree is built on the host; its device mirror is created on first use (current device)
-void ensure_uploaded(const h2_tree* tree) {
+// device mirrors of the tree: the ordering part (coordinates, leaf ranges) and, after waiting
+// for an asynchronous partition (h2_tree_build_async), the CSR batch descriptors
+void ensure_order_uploaded(const h2_tree* tree) {
   h2_tree* T = const_cast<h2_tree*>(tree);
   int dev = 0;
   H2_CUDA(cudaGetDevice(&dev));
-  if (T->device < 0) tree_upload(*T);
+  if (T->device < 0) tree_upload_order(*T);
   H2_REQUIRE(dev == T->device, "libh2: the tree was uploaded to another device");
+}
+void ensure_partition_uploaded(const h2_tree* tree) {
+  h2_tree* T = const_cast<h2_tree*>(tree);
+  T->wait_partition();
+  if (!T->part_uploaded) tree_upload_partition(*T);
+}
+void ensure_uploaded(const h2_tree* tree) {
+  ensure_order_uploaded(tree);
+  ensure_partition_uploaded(tree);
 }
 
 // built-in kernel parameters on a tree: diameter (exp / Helmholtz range guards) and, for the
@@ -1946,6 +1975,34 @@ h2_status h2_tree_build(const double* coords_host, int64_t n, int32_t dim, int32
   }
 }
 
+h2_status h2_tree_build_async(const double* coords_host, int64_t n, int32_t dim, int32_t leaf_size, double eta,
+                              int32_t dist_rule, h2_tree** out) {
+  if (!out) return (g_err = "h2_tree_build_async: out is NULL", H2_ERR_INVALID_ARG);
+  *out = nullptr;
+  try {
+    H2_REQUIRE(coords_host != nullptr, "h2_tree_build_async: coords is NULL");
+    auto* T = new h2_tree();
+    std::unique_ptr<h2_tree> guard(T);
+    tree_build_order(*T, coords_host, n, dim, leaf_size, eta, dist_rule);
+    T->part_thread = std::thread([T] {
+      try {
+        tree_build_partition(*T);
+      } catch (const Error& e) {
+        T->part_error = e.what();
+      } catch (const std::exception& e) {
+        T->part_error = std::string("h2_tree_build_async: ") + e.what();
+      }
+    });
+    *out = guard.release();
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    g_err = "h2_tree_build_async: host out of memory";
+    return H2_ERR_OOM;
+  }
+}
+
 h2_status h2_tree_import(const h2_tree_desc* desc, h2_tree** out) {
   if (!out) return (g_err = "h2_tree_import: out is NULL", H2_ERR_INVALID_ARG);
   *out = nullptr;
@@ -1966,6 +2023,11 @@ h2_status h2_tree_import(const h2_tree_desc* desc, h2_tree** out) {
 
 h2_status h2_tree_get_info(const h2_tree* T, h2_tree_info* info) {
   if (!T || !info) return (g_err = "h2_tree_get_info: NULL argument", H2_ERR_INVALID_ARG);
+  try {
+    const_cast<h2_tree*>(T)->wait_partition();
+  } catch (const Error& e) {
+    return fail(e);
+  }
   info->n = T->n;
   info->dim = T->dim;
   info->leaf_size = T->leaf_size;
@@ -1988,6 +2050,11 @@ h2_status h2_tree_export(const h2_tree* T, int64_t* perm, int64_t* begin, int64_
       if (end) end[pos] = T->end[t][c];
     }
   if (near_pairs) {
+    try {
+      const_cast<h2_tree*>(T)->wait_partition();
+    } catch (const Error& e) {
+      return fail(e);
+    }
     for (int64_t s = 0; s < (int64_t)T->near.ptr.size() - 1; ++s)
       for (int e = T->near.ptr[s]; e < T->near.ptr[s + 1]; ++e) {
         near_pairs[2 * e] = (int32_t)s;
@@ -1999,6 +2066,11 @@ h2_status h2_tree_export(const h2_tree* T, int64_t* perm, int64_t* begin, int64_
 
 h2_status h2_tree_far_count(const h2_tree* T, int32_t depth, int64_t* nnz) {
   if (!T || !nnz || depth < 0 || depth > T->Dl) return (g_err = "h2_tree_far_count: bad argument", H2_ERR_INVALID_ARG);
+  try {
+    const_cast<h2_tree*>(T)->wait_partition();
+  } catch (const Error& e) {
+    return fail(e);
+  }
   *nnz = T->far[depth].nnz();
   return H2_OK;
 }
@@ -2006,6 +2078,11 @@ h2_status h2_tree_far_count(const h2_tree* T, int32_t depth, int64_t* nnz) {
 h2_status h2_tree_export_far(const h2_tree* T, int32_t depth, int32_t* far_pairs) {
   if (!T || !far_pairs || depth < 0 || depth > T->Dl)
     return (g_err = "h2_tree_export_far: bad argument", H2_ERR_INVALID_ARG);
+  try {
+    const_cast<h2_tree*>(T)->wait_partition();
+  } catch (const Error& e) {
+    return fail(e);
+  }
   const PairCSR& F = T->far[depth];
   for (int64_t s = 0; s < (int64_t)F.ptr.size() - 1; ++s)
     for (int e = F.ptr[s]; e < F.ptr[s + 1]; ++e) {
@@ -2220,10 +2297,11 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
     // (checked above: not partial); its matvec is row-sharded, its entries extracted per owned pair
     // subtree-aligned ownership at every processed depth: a power-of-two rank count with at
     // least one cluster per rank at the coarsest processed depth
+    if (dist || nonsym) ensure_uploaded(tree);   // the partition up front
+    else ensure_order_uploaded(tree);            // Builder::run waits for it (tree_ready)
     H2_REQUIRE(!dist || ((comm->nranks & (comm->nranks - 1)) == 0 && tree->top >= 0 &&
                          (int64_t(1) << tree->top) >= comm->nranks),
                "h2_build_dist: nranks must be a power of two <= 2^top_depth");
-    ensure_uploaded(tree);
     // the tree is owned by the caller; share it without taking ownership
     H->tree = std::shared_ptr<h2_tree>(const_cast<h2_tree*>(tree), [](h2_tree*) {});
     H2_REQUIRE(o.eps_decay > 0 && std::isfinite(o.eps_decay), "h2_build: eps_decay must be > 0");

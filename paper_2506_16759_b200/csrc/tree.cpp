@@ -108,6 +108,12 @@ void make_csr(PairCSR& C, std::vector<std::pair<int32_t, int32_t>>& pairs, int32
 }  // namespace
 
 void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, double eta, int rule) {
+  tree_build_order(T, X, n, dim, leaf, eta, rule);
+  tree_build_partition(T);
+}
+
+// The KD ordering (R4) and the tree-order coordinates: everything the dense sketch needs.
+void tree_build_order(h2_tree& T, const double* X, int64_t n, int dim, int leaf, double eta, int rule) {
   H2_REQUIRE(n >= 1 && n < (int64_t(1) << 31), "h2_tree_build: need 1 <= n < 2^31");
   H2_REQUIRE(dim >= 1 && dim <= 3, "h2_tree_build: dim must be 1, 2 or 3");
   H2_REQUIRE(leaf >= 2, "h2_tree_build: leaf_size >= 2");
@@ -220,6 +226,22 @@ void tree_build_host(h2_tree& T, const double* X, int64_t n, int dim, int leaf, 
   }
 
   lap("coords");
+}
+
+// The block partition of an ordered tree (bounding boxes, dual traversal, CSR batch descriptors,
+// unique D offsets).  Synchronous in h2_tree_build; on a host thread in h2_tree_build_async.
+void tree_build_partition(h2_tree& T) {
+  const int Dl = T.Dl;
+  const double eta = T.eta;
+  const int rule = T.rule;
+  const bool trace = getenv("H2_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[h2 tree] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   // ---- bounding boxes per depth (tree order, zero padded)
   std::vector<std::vector<BBox>> box(Dl + 1);
   for (int t = Dl; t >= 0; --t) {
@@ -458,6 +480,11 @@ void free_csr(DeviceCSR& d) {
 }  // namespace
 
 void tree_upload(h2_tree& T) {
+  tree_upload_order(T);
+  tree_upload_partition(T);
+}
+
+void tree_upload_order(h2_tree& T) {
   int dev = 0;
   H2_CUDA(cudaGetDevice(&dev));
   T.d_x = upload(T.xt);
@@ -472,14 +499,25 @@ void tree_upload(h2_tree& T) {
   std::vector<int32_t> ls(T.begin[T.Dl].size());
   for (size_t c = 0; c < ls.size(); ++c) ls[c] = (int32_t)(T.end[T.Dl][c] - T.begin[T.Dl][c]);
   T.d_leaf_size = upload(ls);
+  T.device = dev;
+}
+
+void tree_upload_partition(h2_tree& T) {
   T.d_D_off = upload(T.D_off);
   T.d_near = upload_csr(T.near);
   T.d_far.resize(T.Dl + 1);
   for (int t = 0; t <= T.Dl; ++t) T.d_far[t] = upload_csr(T.far[t]);
-  T.device = dev;
+  T.part_uploaded = true;
+}
+
+void h2_tree::wait_partition() {
+  std::lock_guard<std::mutex> g(part_mu);
+  if (part_thread.joinable()) part_thread.join();
+  if (!part_error.empty()) throw h2::Error(H2_ERR_INVALID_ARG, part_error);
 }
 
 h2_tree::~h2_tree() {
+  if (part_thread.joinable()) part_thread.join();
   if (device < 0) return;
   int prev = 0;
   cudaGetDevice(&prev);

@@ -2,6 +2,9 @@
 // per-level CSR batch descriptors (§IV-A "stored contiguously level by level").
 #pragma once
 #include <cstdint>
+#include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/h2.h"
@@ -33,6 +36,16 @@ struct h2_tree {
   std::vector<PairCSR> far;                        // per depth
   std::vector<int64_t> D_off;                      // unique near pair offsets (m_s*m_b prefix)
 
+  // asynchronous partition (h2_tree_build_async): the KD ordering and tree-order coordinates are
+  // ready at return, the block partition (boxes, dual traversal, CSR, D offsets) is built on a
+  // host thread; every reader of the partition calls wait_partition() first (it rethrows a
+  // partition error).  The first dense-sketch pass of h2_build runs before that wait.
+  std::thread part_thread;
+  std::mutex part_mu;
+  std::string part_error;
+  bool part_uploaded = false;
+  void wait_partition();
+
   // device mirrors (current device at build time)
   int device = -1;
   double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr;
@@ -47,5 +60,9 @@ struct h2_tree {
 };
 
 void tree_build_host(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+void tree_build_order(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+void tree_build_partition(h2_tree& T);
+void tree_upload_order(h2_tree& T);
+void tree_upload_partition(h2_tree& T);
 void tree_import_host(h2_tree& T, const h2_tree_desc& desc);
 void tree_upload(h2_tree& T);

@@ -46,32 +46,49 @@ class Tree:
     points: n x dim float64 in original order (host).  The tree keeps tree-ordered
     coordinates on the current CUDA device for the built-in kernels."""
 
-    def __init__(self, points, leaf_size=64, eta=0.7, dist_rule="center", _handle=None):
+    def __init__(self, points, leaf_size=64, eta=0.7, dist_rule="center", _handle=None, asynchronous=False):
+        """asynchronous=True: h2_tree_build_async -- the block partition is built on a host thread
+        and waited for by the first call that needs it; h2_build's first sketch pass overlaps it.
+        The partition-dependent attributes below are then fetched on first access."""
         P = np.ascontiguousarray(points, dtype=np.float64)
         if P.ndim == 1:
             P = P[:, None]
         self.points = P
+        self.n = P.shape[0]
         h = _handle
         if h is None:
             h = C.c_void_p()
-            check(lib.h2_tree_build(P.ctypes.data_as(C.c_void_p), P.shape[0], P.shape[1], leaf_size, float(eta),
-                                    L.H2_DIST_CENTER if dist_rule == "center" else L.H2_DIST_BOX, C.byref(h)))
+            fn = lib.h2_tree_build_async if asynchronous else lib.h2_tree_build
+            check(fn(P.ctypes.data_as(C.c_void_p), P.shape[0], P.shape[1], leaf_size, float(eta),
+                     L.H2_DIST_CENTER if dist_rule == "center" else L.H2_DIST_BOX, C.byref(h)))
         self._h = h
+        self._info = None
+        self._near = self._far = None
+        if not asynchronous:
+            self._load_info()
+
+    def _load_info(self):
         info = L.h2_tree_info()
-        check(lib.h2_tree_get_info(h, C.byref(info)))
-        self.n, self.dim, self.leaf_size = info.n, info.dim, info.leaf_size
-        self.leaf_depth = info.leaf_depth
-        self.top_depth = info.top_depth
-        self.near_nnz, self.far_nnz_total, self.csp = info.near_nnz, info.far_nnz_total, info.csp
-        nnodes = (1 << (self.leaf_depth + 1)) - 1
-        self.perm = np.empty(self.n, np.int64)
+        check(lib.h2_tree_get_info(self._h, C.byref(info)))
+        nnodes = (1 << (info.leaf_depth + 1)) - 1
+        perm = np.empty(self.n, np.int64)
         b = np.empty(nnodes, np.int64)
         e = np.empty(nnodes, np.int64)
-        check(lib.h2_tree_export(h, self.perm.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+        check(lib.h2_tree_export(self._h, perm.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
                                  e.ctypes.data_as(C.c_void_p), None))
-        self.begin = [b[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
-        self.end = [e[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(self.leaf_depth + 1)]
-        self._near = self._far = None
+        self._info = dict(dim=info.dim, leaf_size=info.leaf_size, leaf_depth=info.leaf_depth,
+                          top_depth=info.top_depth, near_nnz=info.near_nnz, far_nnz_total=info.far_nnz_total,
+                          csp=info.csp, perm=perm,
+                          begin=[b[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(info.leaf_depth + 1)],
+                          end=[e[(1 << t) - 1:(1 << (t + 1)) - 1] for t in range(info.leaf_depth + 1)])
+
+    def __getattr__(self, name):   # partition-dependent attributes, loaded on first access
+        if name in ("dim", "leaf_size", "leaf_depth", "top_depth", "near_nnz", "far_nnz_total", "csp", "perm",
+                    "begin", "end"):
+            if self.__dict__.get("_info") is None:
+                self._load_info()
+            return self.__dict__["_info"][name]
+        raise AttributeError(name)
 
     @classmethod
     def from_partition(cls, points, perm, begin, end, near, far):

@@ -209,6 +209,21 @@ def test_degenerate_inputs():
     assert np.abs(y - K[:, :7]).max() <= 1e-13
 
 
+def test_async_tree_build_bitwise():
+    """h2_tree_build_async: h2_build launches the first sketch pass before waiting for the
+    partition thread; the H^2 is bitwise the one built on a synchronous tree."""
+    X = uniform_points(6000, 3, 5)
+    Hs = g.build(g.Tree(X, 64), ("exp", 0.2), 1e-6)
+    Ta = g.Tree(X, 64, asynchronous=True)
+    Ha = g.build(Ta, ("exp", 0.2), 1e-6)
+    assert Hs.samples == Ha.samples
+    for t in range(Hs.top_depth, Ta.leaf_depth + 1):
+        assert np.array_equal(Hs.rank(t), Ha.rank(t))
+        for w in (g._lib.H2_X_BASIS, g._lib.H2_X_B):
+            assert np.array_equal(Hs._export(w, t), Ha._export(w, t))
+    assert np.array_equal(Hs._export(g._lib.H2_X_D), Ha._export(g._lib.H2_X_D))
+
+
 def test_deterministic_bitwise():
     X = uniform_points(5000, 3, 0)
     T = g.Tree(X, 64)

@@ -105,3 +105,22 @@ def test_tree_import_roundtrip_and_validation():
         with pytest.raises(g.H2Error) as e:
             g.Tree.from_partition(X, *args)
         assert e.value.status == -1
+
+
+@pytest.mark.parametrize("case", ["u3d_5000_64", "u2d_1024_32", "grid_8x8x8_16"])
+def test_async_tree_matches_sync(case):
+    """h2_tree_build_async (the block partition on a host thread, waited for by its first reader)
+    yields exactly the synchronous partition; freeing an async tree with its thread still running
+    is safe (the destructor joins)."""
+    import paper_2506_16759_b200 as g
+    X, leaf = {"u3d_5000_64": (uniform_points(5000, 3, 0), 64), "u2d_1024_32": (uniform_points(1024, 2, 0), 32),
+               "grid_8x8x8_16": (grid_points((8, 8, 8), 1 / 8), 16)}[case]
+    Ts, Ta = g.Tree(X, leaf), g.Tree(X, leaf, asynchronous=True)
+    for a in ("leaf_depth", "top_depth", "csp", "near_nnz", "far_nnz_total"):
+        assert getattr(Ts, a) == getattr(Ta, a), a
+    assert np.array_equal(Ts.perm, Ta.perm)
+    assert np.array_equal(Ts.near, Ta.near)
+    assert all(np.array_equal(a, b) for a, b in zip(Ts.far, Ta.far))
+    for _ in range(3):
+        T = g.Tree(X, leaf, asynchronous=True)
+        del T
