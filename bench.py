@@ -373,9 +373,8 @@ def run_ours(args, w, rank, world, local_rank):
             # asynchronous partition: the host's dual traversal overlaps the first sketch pass
             T2 = g.Tree(Xpin.numpy(), w["leaf"], 0.7, asynchronous=True)
             H2 = g.build(T2, kern, w["tol"], comm=comm, **opts)
-            d2h = 0
-            for t in range(H2.top_depth, T2.leaf_depth + 1):
-                d2h += H2.rank(t).nbytes // 2 + sum(s.nbytes // 2 for s in H2.skel(t))
+            rk, sk = H2.ranks_and_skeletons()   # the result read: ranks + skeletons, every depth
+            d2h = rk.nbytes + sk.nbytes
             torch.cuda.synchronize()
             if it:
                 e_times.append(time.perf_counter() - t0)

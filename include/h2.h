@@ -442,7 +442,10 @@ h2_status h2_omega(uint64_t seed, uint32_t stream_id, int64_t row0, int64_t nrow
  *   D         : float64, unique near pairs (s <= b) in sorted order, each m_s x m_b row-major
  *   B[t]      : float64, unique far pairs (s < b) of depth t in sorted order, k_s x k_b
  *   cert[t]   : float64 pairs (min pivot gap, stop margin) per cluster (CPQR certification)
+ * depth = H2_ALL_DEPTHS (-1) with H2_X_RANK / H2_X_SKEL (or the _C forms): every processed depth
+ * top_depth..leaf_depth concatenated in that order, in ONE call (the end-to-end result read).
  * ------------------------------------------------------------------------------------- */
+#define H2_ALL_DEPTHS (-1)
 enum { H2_X_RANK = 0, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT,
        /* column side of a non-symmetric matrix (h2_build_nonsym): ranks, J~, V / [F1; F2], cert */
        H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C };

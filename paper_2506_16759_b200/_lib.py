@@ -21,6 +21,7 @@ H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_S
 H2_SKETCH_OMEGA_QUARTERS = 1
 H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL, H2_CQ_V_EXACT = 1, 2, 4, 8
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
+H2_ALL_DEPTHS = -1   # h2_export: every processed depth concatenated (ranks / skeletons)
 H2_NPHASE = len(PHASES)
 
 

@@ -2460,6 +2460,19 @@ h2_status h2_export_size(const h2_matrix* H, int32_t what, int32_t depth, int64_
     *count = H->D.n;
     return H2_OK;
   }
+  if (depth == H2_ALL_DEPTHS) {
+    if (!(what == H2_X_RANK || what == H2_X_SKEL || ((what == H2_X_RANK_C || what == H2_X_SKEL_C) && H->nonsym)))
+      return (g_err = "h2_export_size: all depths for ranks / skeletons only", H2_ERR_INVALID_ARG);
+    int64_t c = 0;
+    for (int t = H->top; t <= H->Dl; ++t) {
+      int64_t ct = 0;
+      h2_status s = h2_export_size(H, what, t, &ct);
+      if (s != H2_OK) return s;
+      c += ct;
+    }
+    *count = c;
+    return H2_OK;
+  }
   if (depth < H->top || depth > H->Dl) return (g_err = "h2_export_size: depth outside [top, leaf]", H2_ERR_INVALID_ARG);
   if (what >= H2_X_RANK_C && what <= H2_X_CERT_C) {
     if (!H->nonsym) return (g_err = "h2_export_size: column side exists for h2_build_nonsym matrices only", H2_ERR_INVALID_ARG);
@@ -2492,6 +2505,23 @@ h2_status h2_export(const h2_matrix* H, int32_t what, int32_t depth, void* dst) 
   if (s != H2_OK) return s;
   if (!dst) return (g_err = "h2_export: NULL dst", H2_ERR_INVALID_ARG);
   if (cnt == 0) return H2_OK;
+  if (depth == H2_ALL_DEPTHS) {   // ranks / skeletons of every depth: async copies, one sync
+    char* out = static_cast<char*>(dst);
+    for (int t = H->top; t <= H->Dl; ++t) {
+      const Level& L = (what >= H2_X_RANK_C) ? H->C(t) : H->L(t);
+      const bool rk = what == H2_X_RANK || what == H2_X_RANK_C;
+      const int64_t n = rk ? L.nclus : L.rtot;
+      if (n > 0) {
+        cudaError_t e = cudaMemcpyAsync(out, rk ? (const void*)L.d_k.p : (const void*)L.d_skel.p, 4 * n,
+                                        cudaMemcpyDefault, 0);
+        if (e != cudaSuccess) return (g_err = std::string("h2_export: ") + cudaGetErrorString(e), H2_ERR_CUDA);
+      }
+      out += 4 * n;
+    }
+    cudaError_t e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) return (g_err = std::string("h2_export: ") + cudaGetErrorString(e), H2_ERR_CUDA);
+    return H2_OK;
+  }
   const void* src = nullptr;
   size_t el = 8;
   if (what == H2_X_D) src = H->D.p;

@@ -205,6 +205,13 @@ class H2Matrix:
         """side 0: row ranks (the symmetric build's only side); 1: column ranks (non-symmetric)."""
         return self._export(L.H2_X_RANK_C if side else L.H2_X_RANK, t, np.int32).astype(np.int64)
 
+    def ranks_and_skeletons(self, side=0):
+        """Ranks and skeleton indices of every processed depth (top..leaf, concatenated) in two
+        calls (h2_export with H2_ALL_DEPTHS): the end-to-end result read."""
+        rk = self._export(L.H2_X_RANK_C if side else L.H2_X_RANK, L.H2_ALL_DEPTHS, np.int32)
+        sk = self._export(L.H2_X_SKEL_C if side else L.H2_X_SKEL, L.H2_ALL_DEPTHS, np.int32)
+        return rk, sk
+
     def skel(self, t, side=0):
         r = self.rank(t, side)
         s = self._export(L.H2_X_SKEL_C if side else L.H2_X_SKEL, t, np.int32).astype(np.int64)

@@ -222,6 +222,10 @@ def test_async_tree_build_bitwise():
         for w in (g._lib.H2_X_BASIS, g._lib.H2_X_B):
             assert np.array_equal(Hs._export(w, t), Ha._export(w, t))
     assert np.array_equal(Hs._export(g._lib.H2_X_D), Ha._export(g._lib.H2_X_D))
+    # the one-call result read (h2_export with H2_ALL_DEPTHS) = the per-depth exports concatenated
+    rk, sk = Ha.ranks_and_skeletons()
+    assert np.array_equal(rk, np.concatenate([Ha.rank(t) for t in range(Ha.top_depth, Ta.leaf_depth + 1)]))
+    assert np.array_equal(sk, np.concatenate([np.concatenate(Ha.skel(t)) for t in range(Ha.top_depth, Ta.leaf_depth + 1)]))
 
 
 def test_deterministic_bitwise():
