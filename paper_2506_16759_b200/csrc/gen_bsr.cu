@@ -271,13 +271,14 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
 // ------------------------------------------------------------------------------------------
 constexpr int B2_LDA = 36;   // A slab row stride (doubles): conflict-free fragment reads
 constexpr int B2_MAXP = 256; // partners per row cluster staged in shared memory
-template <int CW, int NS, bool COLFAST>
+template <int CW, int NS, bool COLFAST, int KD = 32>
 __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
   constexpr int NT = 4 * CW;                 // 128 threads per 32 columns
   constexpr int NW = NT / 32;
+  constexpr int LDA = KD + 4;                // A slab row stride: = 4 mod 16 doubles, conflict-free fragments
   constexpr int LDB = CW + 4;
-  constexpr int ASZ = BT_R * B2_LDA;         // 2304 doubles
-  constexpr int BSZ = BT_K * LDB;
+  constexpr int ASZ = BT_R * LDA;            // 2304 doubles at KD = 32
+  constexpr int BSZ = KD * LDB;
   constexpr int STG = ASZ + BSZ;
   extern __shared__ __align__(16) double bsm[];
   __shared__ int st_nk[NS];
@@ -316,12 +317,12 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       p_blk[q] = a.blk_off[u];
       p_om[q] = a.ooff[b];
       p_mb[q] = direct ? mb : -mb;
-      my += (mb + BT_K - 1) / BT_K;
+      my += (mb + KD - 1) / KD;
     }
     if (my) atomicAdd(&s_items, my);
   } else if (tid == 0) {
     int n = 0;
-    for (int e = e0; e < e1; ++e) n += ((a.kcnt ? a.kcnt : a.cnt)[a.idx[e]] + BT_K - 1) / BT_K;
+    for (int e = e0; e < e1; ++e) n += ((a.kcnt ? a.kcnt : a.cnt)[a.idx[e]] + KD - 1) / KD;
     s_items = n;
   }
   __syncthreads();
@@ -348,19 +349,22 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       orow = a.ooff[b];
     }
     const double* blk = a.blk + boff;
-    const int nk = min(BT_K, mb - lk);
+    const int nk = min(KD, mb - lk);
     const uint32_t sa = sbase + (uint32_t)(buf * STG) * 8u;
     const uint32_t sb = sa + (uint32_t)ASZ * 8u;
     if (direct) {
-      // lane = kk (a 256-byte row segment per warp), rows r = warp + NW q
-      const bool kok = lane < nk;
-      const double* src = blk + (int64_t)(r0 + warp) * mb + lk + lane;
-      const int64_t step = (int64_t)NW * mb;
+      // KD consecutive lanes cover one row segment (KD x 8 bytes contiguous), 32 / KD rows per
+      // warp instruction, rows r = rl + (32 / KD)(warp + NW q)
+      constexpr int RPW = 32 / KD;
+      const int kk = lane % KD, rl = lane / KD;
+      const bool kok = kk < nk;
+      const double* src = blk + (int64_t)(r0 + rl + RPW * warp) * mb + lk + kk;
+      const int64_t step = (int64_t)RPW * NW * mb;
 #pragma unroll
-      for (int q = 0; q < BT_R / NW; ++q) {
-        const int r = warp + NW * q;
+      for (int q = 0; q < BT_R / (RPW * NW); ++q) {
+        const int r = rl + RPW * (warp + NW * q);
         const bool ok = kok && r < rows_here;
-        cp_async8(sa + (uint32_t)(r * B2_LDA + lane) * 8u, ok ? src : blk, ok);
+        cp_async8(sa + (uint32_t)(r * LDA + kk) * 8u, ok ? src : blk, ok);
         src += step;
       }
     } else {
@@ -368,25 +372,25 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       // 4 kk (64-byte global runs), scattered transposed into [r][kk]
       const int rl = lane & 7, kl = lane >> 3;
 #pragma unroll
-      for (int q = 0; q < BT_R / NW; ++q) {
-        const int t = warp + NW * q;                      // 64 tiles of 8 r x 4 kk
+      for (int q = 0; q < 2 * KD / NW; ++q) {
+        const int t = warp + NW * q;                      // 2 KD tiles of 8 r x 4 kk
         const int r = 8 * (t & 7) + rl, kk = 4 * (t >> 3) + kl;
         const bool ok = kk < nk && r < rows_here;
-        cp_async8(sa + (uint32_t)(r * B2_LDA + kk) * 8u, ok ? blk + (int64_t)(lk + kk) * ms + r0 + r : blk, ok);
+        cp_async8(sa + (uint32_t)(r * LDA + kk) * 8u, ok ? blk + (int64_t)(lk + kk) * ms + r0 + r : blk, ok);
       }
     }
     {
       const double* om = a.Om + orow * a.ldo + cb + bc;
       const bool cok = bc < nc;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < KD / 4; ++q) {
         const int kk = bk0 + 4 * q;
         const bool ok = cok && kk < nk;
         cp_async8(sb + (uint32_t)(kk * LDB + bc) * 8u, ok ? om + (int64_t)(lk + kk) * a.ldo : a.Om, ok);
       }
     }
     if (tid == 0) st_nk[buf] = nk;
-    lk += BT_K;
+    lk += KD;
     if (lk >= mb) {
       ++le;
       lk = 0;
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
     asm volatile("cp.async.commit_group;\n" ::);
   }
   // fragment base offsets (doubles) inside a stage
-  const int offa = (wr * 16 + (lane >> 2)) * B2_LDA + (lane & 3);
+  const int offa = (wr * 16 + (lane >> 2)) * LDA + (lane & 3);
   const int offb = ASZ + (lane & 3) * LDB + wc * 32 + (lane >> 2);
   for (int it = 0; it < nitems; ++it) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(NS - 2));
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
     const double* pb = st + offb;
     const int ksteps = (st_nk[it % NS] + 3) >> 2;
     auto kstep = [&](int ks) {
-      const double a0 = pa[ks * 4], a1 = pa[8 * B2_LDA + ks * 4];
+      const double a0 = pa[ks * 4], a1 = pa[8 * LDA + ks * 4];
       double bf[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = pb[ks * 4 * LDB + j * 8];
@@ -425,14 +429,14 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1, bf[j]);
     };
-    if (ksteps == BT_K / 4) {
+    if (ksteps == KD / 4) {
       // full slab: no per-step guard, so the fragment loads of later k steps can be scheduled
       // ahead of the current step's DMMAs
 #pragma unroll
-      for (int ks = 0; ks < BT_K / 4; ++ks) kstep(ks);
+      for (int ks = 0; ks < KD / 4; ++ks) kstep(ks);
     } else {
 #pragma unroll
-      for (int ks = 0; ks < BT_K / 4; ++ks)
+      for (int ks = 0; ks < KD / 4; ++ks)
         if (ks < ksteps) kstep(ks);
     }
   }
@@ -451,28 +455,31 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
   }
 }
 
-template <int CW, int NS, bool COLFAST>
+template <int CW, int NS, bool COLFAST, int KD = 32>
 static void bsr2_go(const BsrArgs& a, double alpha, cudaStream_t st) {
-  const size_t sm = sizeof(double) * NS * (BT_R * B2_LDA + BT_K * (CW + 4));
-  H2_CUDA(cudaFuncSetAttribute(bsr2_kernel<CW, NS, COLFAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const size_t sm = sizeof(double) * NS * (BT_R * (KD + 4) + KD * (CW + 4));
+  H2_CUDA(cudaFuncSetAttribute(bsr2_kernel<CW, NS, COLFAST, KD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   if (COLFAST)
-    bsr2_kernel<CW, NS, COLFAST><<<dim3(div_up(a.ncols, CW), a.nclusters, div_up(a.max_rows, BT_R)), 4 * CW, sm, st>>>(
-        a, alpha);
+    bsr2_kernel<CW, NS, COLFAST, KD><<<dim3(div_up(a.ncols, CW), a.nclusters, div_up(a.max_rows, BT_R)), 4 * CW, sm,
+                                       st>>>(a, alpha);
   else
-    bsr2_kernel<CW, NS, COLFAST><<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, CW)), 4 * CW, sm, st>>>(
-        a, alpha);
+    bsr2_kernel<CW, NS, COLFAST, KD><<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, CW)), 4 * CW, sm,
+                                       st>>>(a, alpha);
   H2_CHECK_LAUNCH();
 }
 
 static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
   // H2_BSR2: 0 = the round-1 kernel family below; 1 = bsr2 32-column tiles (column-fast grid for
-  // wide passes); 2 = bsr2 64-column tiles; 3 = bsr2 32-column tiles, 3-stage ring
+  // wide passes); 2 = bsr2 64-column tiles; 3 = bsr2 32-column tiles, 3-stage ring; 4 / 5 = 16-deep
+  // slabs (half the shared memory per stage: 7 / 5 CTAs per SM), 2 / 3 stages
   static const int v2 = env_int("H2_BSR2", 1);
   if (v2 != 0) {
     const bool wide = a.ncols > 32;
     if (v2 == 2 && a.ncols > 32) bsr2_go<64, 2, true>(a, alpha, st);
     else if (v2 == 3) wide ? bsr2_go<32, 3, true>(a, alpha, st) : bsr2_go<32, 3, false>(a, alpha, st);
+    else if (v2 == 4) wide ? bsr2_go<32, 2, true, 16>(a, alpha, st) : bsr2_go<32, 2, false, 16>(a, alpha, st);
+    else if (v2 == 5) wide ? bsr2_go<32, 3, true, 16>(a, alpha, st) : bsr2_go<32, 3, false, 16>(a, alpha, st);
     else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);
     return;
   }
