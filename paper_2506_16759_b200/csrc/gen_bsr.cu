@@ -361,8 +361,9 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       const double* src = blk + (int64_t)(r0 + rl + RPW * warp) * mb + lk + kk;
       const int64_t step = (int64_t)RPW * NW * mb;
 #pragma unroll
-      for (int q = 0; q < BT_R / (RPW * NW); ++q) {
+      for (int q = 0; q < (BT_R + RPW * NW - 1) / (RPW * NW); ++q) {   // NW need not divide 64
         const int r = rl + RPW * (warp + NW * q);
+        if (r >= BT_R) break;
         const bool ok = kok && r < rows_here;
         cp_async8(sa + (uint32_t)(r * LDA + kk) * 8u, ok ? src : blk, ok);
         src += step;
@@ -372,8 +373,9 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       // 4 kk (64-byte global runs), scattered transposed into [r][kk]
       const int rl = lane & 7, kl = lane >> 3;
 #pragma unroll
-      for (int q = 0; q < 2 * KD / NW; ++q) {
+      for (int q = 0; q < (2 * KD + NW - 1) / NW; ++q) {
         const int t = warp + NW * q;                      // 2 KD tiles of 8 r x 4 kk
+        if (t >= 2 * KD) break;
         const int r = 8 * (t & 7) + rl, kk = 4 * (t >> 3) + kl;
         const bool ok = kk < nk && r < rows_here;
         cp_async8(sa + (uint32_t)(r * LDA + kk) * 8u, ok ? blk + (int64_t)(lk + kk) * ms + r0 + r : blk, ok);
@@ -480,6 +482,8 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
     else if (v2 == 3) wide ? bsr2_go<32, 3, true>(a, alpha, st) : bsr2_go<32, 3, false>(a, alpha, st);
     else if (v2 == 4) wide ? bsr2_go<32, 2, true, 16>(a, alpha, st) : bsr2_go<32, 2, false, 16>(a, alpha, st);
     else if (v2 == 5) wide ? bsr2_go<32, 3, true, 16>(a, alpha, st) : bsr2_go<32, 3, false, 16>(a, alpha, st);
+    else if (v2 == 6 && a.ncols > 128) bsr2_go<160, 2, true>(a, alpha, st);   // one CTA per 160 columns
+    else if (v2 == 7 && a.ncols > 64) bsr2_go<96, 2, true>(a, alpha, st);
     else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);
     return;
   }
