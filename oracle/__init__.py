@@ -9,7 +9,8 @@ oracle never imports the product: the two share no code.  The only shared module
 ``synth`` (seeded point clouds / probes; none of the method's arithmetic).
 
 Modules (each function cites the passage it follows):
-  rng       Philox4x32-10 counter-based generator + Box-Muller Gaussians for Omega
+  rng       Philox4x32-10 counter-based generator -> the centred binomial Omega of DESIGN.md R8
+            ("a random matrix"; Gaussian Omega: a caller's array, R34)
   geometry  KD-tree cluster tree, Eq.(1) admissibility, dual-tree traversal
   kernels   exponential covariance / Helmholtz IE entry evaluation
   cpqr      column-pivoted QR and row interpolative decomposition (Eq.3)

@@ -102,7 +102,16 @@ def build(tree, part, sampler, entry, omega, tol, opts: BuildOpts = None) -> H2M
     d = opts.d_init
     Om = omega(0, d)
     Y = sampler(Om)
-    sumsq = float(np.sum(Y * Y))
+
+    def block_sumsq(Yb):
+        """||Y_block||_F^2 as DESIGN.md R28 reads it: per-leaf partial sums, added in leaf order."""
+        tot = 0.0
+        for c in range(1 << Dl):
+            rows = Yb[tree.begin[Dl][c]:tree.end[Dl][c]]
+            tot += float(np.sum(rows * rows))
+        return tot
+
+    sumsq = block_sumsq(Y)
     # line 212: D_{tau,b} = K(I_tau, I_b), b in N_tau
     for (s, b) in part.near:
         H.D[(int(s), int(b))] = entry(rng_of(Dl, s), rng_of(Dl, b))
@@ -161,7 +170,7 @@ def build(tree, part, sampler, entry, omega, tol, opts: BuildOpts = None) -> H2M
             # lines 216-217 / 246-247: new random block and samples, swept up to this level
             Obar = omega(d, opts.d_blk)
             Ybar = sampler(Obar)
-            sumsq += float(np.sum(Ybar * Ybar))
+            sumsq += block_sumsq(Ybar)
             nY, nO = sweep_new(t, Ybar, Obar)
             Yl = [np.hstack([Yl[c], nY[c]]) for c in range(1 << t)]
             Ol = [np.hstack([Ol[c], nO[c]]) for c in range(1 << t)]
