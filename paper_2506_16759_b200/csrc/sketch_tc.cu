@@ -134,7 +134,44 @@ __device__ __forceinline__ double dist2_floor(double xi, double yi, double zi, d
 //   m = bits(w) - bits(2^52): the FP64 bit pattern is monotonic, so for w in [2^52, 2^53] this
 //       is exactly w - 2^52, including K -> 1 (w = 2^53, m = 2^52, slice 6 = 0x10).
 // FP64 pipe: 6 (r'^2, caller) + 5 (r') + 7 (g, p) + 1 (w) = 19.
-__device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restrict__ tab, uint32_t lane8) {
+// H2_TC_EXP1024 (default): a 1024-entry table 2^(KEXP + j/1024) in 4 lane-interleaved copies
+// (entry j of copy c at byte 32 j + 8 c, copy = lane & 3) and a degree-3 polynomial on
+// |g| <= ln2/2048 constrained to p(0) = 1 (minimax for the relative error: 2.2e-16, i.e. 0.03
+// units of the 2^-47 grid), one FP64 operation less than the degree-4 / 256-entry form:
+// FP64 pipe 6 (r'^2) + 5 (r') + 6 (g, p) + 1 (w) = 18.
+#ifndef H2_TC_EXP1024
+#define H2_TC_EXP1024 1
+#endif
+constexpr int TC_TAB_SHIFT = H2_TC_EXP1024 ? 2 : 4;        // log2(copies): 4 copies x 1024 or 16 x 256
+constexpr double TC_TAB_STEP = H2_TC_EXP1024 ? 1.0 / 1024.0 : 1.0 / 256.0;
+__device__ __forceinline__ uint32_t tc_lane8(int lane) { return 8u * (uint32_t)(lane & ((1 << TC_TAB_SHIFT) - 1)); }
+
+__device__ __forceinline__ uint2 expk_fixed52_t1024(double r2, const double* __restrict__ tab, uint32_t lane8) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double r0 = r2 * y0;
+  const double e = fma(-r0, y0, 1.0);
+  const double pc = fma(e, 0.375, 0.5);
+  const double r = fma(r0 * e, pc, r0);
+  const double SH = 6755399441055744.0;
+  const double t = fma(r, -1477.3197218702985, SH);       // -1024/ln2
+  const double kf = t - SH;
+  const int n = __double2loint(t);
+  const double g = fma(kf, -0.0006769015435155716, -r);   // |g| <= ln2/2048
+  double q = fma(g, 0.16666666522088344, 0.5000000039549349);
+  q = fma(q, g, 1.0000000000000002);
+  const double p = fma(q, g, 1.0);
+  uint32_t idx;   // ((n & 1023) << 5) | lane8 in one LOP3
+  asm("lop3.b32 %0, %1, 0x7FE0, %2, 0xEA;" : "=r"(idx) : "r"((uint32_t)n << 5), "r"(lane8));
+  const double tv = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tab) + idx);
+  int th;   // hi(T_j) + (n >> 10) 2^20
+  asm("{\n .reg .s32 e;\n shr.s32 e, %1, 10;\n mad.lo.s32 %0, e, 1048576, %2;\n}\n"
+      : "=r"(th) : "r"(n), "r"(__double2hiint(tv)));
+  const double w = fma(__hiloint2double(th, __double2loint(tv)), p, 4503599627370496.0);
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)(__double2hiint(w) - 0x43300000));
+}
+
+__device__ __forceinline__ uint2 expk_fixed52_t256(double r2, const double* __restrict__ tab, uint32_t lane8) {
   double y0;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
   const double r0 = r2 * y0;
@@ -158,6 +195,11 @@ __device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restric
       : "=r"(th) : "r"(n), "r"(__double2hiint(tv)));
   const double w = fma(__hiloint2double(th, __double2loint(tv)), p, 4503599627370496.0);
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)(__double2hiint(w) - 0x43300000));
+}
+
+__device__ __forceinline__ uint2 expk_fixed52(double r2, const double* __restrict__ tab, uint32_t lane8) {
+  if constexpr (H2_TC_EXP1024) return expk_fixed52_t1024(r2, tab, lane8);
+  else return expk_fixed52_t256(r2, tab, lane8);
 }
 
 // Helmholtz (PAPER.md Eq. ie, R20): K = cos(k r)/r, 0 at r = 0, in scaled coordinates
@@ -326,7 +368,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const int nch = (int)(ch_e - ch_b);
   const bool control = (warp == NPW);
 
-  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + (double)SliceFmt<NS>::KEXP);
+  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, NPW);
@@ -450,7 +492,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     }
     // PACK7: the M = 64 layout of the top slice (64 rows x 16 B per k group)
     const int off6d = g * (TM * 16) - g * LBO_A;
-    const uint32_t lane8 = 8u * (lane & 15);
+    const uint32_t lane8 = tc_lane8(lane);
     uint32_t ovf = 0;
     int drains = 0;
     // KDENSE: the next chunk's operator entries are loaded into registers while this chunk is
@@ -785,7 +827,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const bool control = (warp == NPW);
   const int8_t* Bh = Bq + (int64_t)crank * nchunks * BBUF;   // this CTA's column half
 
-  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> 4) * (1.0 / 256.0) + (double)SliceFmt<NS>::KEXP);
+  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, leader ? 2 * NPW : NPW);   // leader: both CTAs' producers
@@ -883,7 +925,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     uint32_t full_remote = 0;
     if (!leader)
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(full_remote) : "r"(bar_full), "r"(0));
-    const uint32_t lane8 = 8u * (lane & 15);
+    const uint32_t lane8 = tc_lane8(lane);
     uint32_t ovf = 0;
     int drains = 0;
     for (int it = 0; it < nch; ++it) {
