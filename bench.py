@@ -31,6 +31,7 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 64 FP64 FMA/clk/SM (DFMA = 
 FP64_PIPE_TOPS = 148 * 64 * 1.965e9 / 1e12          # FP64 pipe instructions (lane-ops) per second
 F_EVAL = 18   # FP64 pipe ops per kernel entry in sketch_tc_kernel (SASS: 6 r^2, 5 r, 6 exp (1024-entry table,
               # degree-3 polynomial), 1 fixed-point DFMA); 19 with the round-1 256-entry / degree-4 form
+F_EVAL_HELM = 27   # Helmholtz entry (SASS): 6 r^2, 5 1/r', 1 r', 4 reduction, 1 g^2, 2 c, 3 s, 2 C c - S s, 2 v, 1 w
 INT8_DENSE_TOPS = 4500.0                            # nominal dense int8 tensor ops/s (B200, guide)
 # measured int8 tcgen05 rate at the sketch's shape (M = 128, N = 160, K = 32, smem operands):
 # profiles/r2_mma_overlap.txt (tools/microbench/mma_fp64_overlap.cu)
@@ -550,7 +551,7 @@ def time_workload(g, torch, stream, flush, name, steps=2):
     if st["entries_sketch"] > 0 and upd is None:
         sk_launches = max(st["entries_sketch"] // (n * n), 1)
         per_launch = float(np.mean([s["t_phase_ms"]["sketch"] for s in stats])) / sk_launches
-        f_eval = F_EVAL if w["kernel"] == "exp" else 37
+        f_eval = F_EVAL if w["kernel"] == "exp" else F_EVAL_HELM
         achieved = float(n) * n * f_eval / (per_launch * 1e-3) / 1e12
         res["sketch_roofline"] = {"bound": "alu", "achieved": achieved, "peak": FP64_PIPE_TOPS,
                                   "unit": "TOP/s (FP64 pipe ops)", "frac": achieved / FP64_PIPE_TOPS,

@@ -258,6 +258,62 @@ __device__ __forceinline__ uint2 helm_fixed51(double r2, double hs, uint32_t& ov
   return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
 }
 
+// H2_TC_HTAB (default): cos(r') from a table of (cos, sin)(2 pi j / 1024), j < 1024, in 2
+// lane-interleaved copies (16-byte entries; the exp table's 32 KB of static shared memory), and
+// short polynomials on the remainder |g| <= pi/1024:  cos(a + g) = C_j c(g) - S_j s(g) with
+// c = 1 - g^2/2 + g^4/24 (truncation g^6/720 < 1.2e-18) and s = g - g^3/6 + g^5/120 (< 5e-22);
+// reduction g = r' - n (2 pi / 1024) by a 2-term Cody-Waite split (hi has 36 significant bits:
+// n hi is exact for n < 2^17, i.e. r' <= 650, the host-checked range).  FP64 pipe: 6 (r'^2)
+// + 5 (1/r') + 1 (r') + 4 (reduction) + 1 (g^2) + 2 (c) + 3 (s) + 2 (C c - S s) + 2 (v) + 1 (w)
+// = 27 instead of 37 (Taylor to x^16 / x^17 on |x| <= pi/4 with the quadrant logic).
+#ifndef H2_TC_HTAB
+#define H2_TC_HTAB 1
+#endif
+constexpr int TC_HTAB_N = 1024;
+__device__ __forceinline__ void fill_cs_table(double* tab, int tid, int nth) {
+  // entry j, copy c at doubles 4 j + 2 c: (cos, sin)(2 pi j / 1024); sincospi of the exact 2j/1024
+  for (int e = tid; e < 2 * TC_HTAB_N; e += nth) {
+    double sv, cv;
+    sincospi((double)(e >> 1) * (2.0 / TC_HTAB_N), &sv, &cv);
+    tab[2 * e] = cv;
+    tab[2 * e + 1] = sv;
+  }
+}
+template <int HEXP>
+__device__ __forceinline__ uint2 helm_fixed51_tab(double r2, double hs, uint32_t& ovf, const double* __restrict__ tab,
+                                                  uint32_t lane16) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double y = fma(fma(e, 0.375, 0.5), y0 * e, y0);            // 1/r'
+  const double r = r2 * y;
+  const double SH = 6755399441055744.0;
+  const double t = fma(r, 162.97466172610083, SH);                 // 1024 / (2 pi)
+  const double nf = t - SH;
+  const int n = __double2loint(t);
+  double g = fma(nf, -0.006135923151532552, r);                    // 2 pi / 1024, 36-bit head
+  g = fma(nf, -1.001306309216609e-14, g);                          // tail
+  const double z = g * g;
+  const double c = fma(fma(z, 4.1666666666666666667e-02, -0.5), z, 1.0);
+  const double sn = fma(fma(z, 8.3333333333333333333e-03, -0.16666666666666666667) * z, g, g);
+  uint32_t idx;   // byte offset 32 (n & 1023) + 16 (lane & 1)
+  asm("lop3.b32 %0, %1, 0x7FE0, %2, 0xEA;" : "=r"(idx) : "r"((uint32_t)n << 5), "r"(lane16));
+  const double2 cs = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + idx);
+  const double tr = fma(cs.x, c, -(cs.y * sn));                    // cos(r')
+  double v = (hs * tr) * y;
+  if (__double2hiint(r2) < 0x03B00000) v = 0.0;                    // r2 < 2^-900: x' = y'
+  const double w = fma(v, (double)(1ull << HEXP), 6755399441055744.0);  // v 2^HEXP + 3 2^51
+  const int mh = __double2hiint(w) - 0x43380000;
+  ovf |= (uint32_t)(mh + (1 << (HEXP - 32))) > (2u << (HEXP - 32));
+  return make_uint2((uint32_t)__double2loint(w), (uint32_t)mh);
+}
+template <int HEXP>
+__device__ __forceinline__ uint2 helm_eval(double r2, double hs, uint32_t& ovf, const double* __restrict__ tab,
+                                           int lane) {
+  if constexpr (H2_TC_HTAB) return helm_fixed51_tab<HEXP>(r2, hs, ovf, tab, 16u * (uint32_t)(lane & 1));
+  else return helm_fixed51<HEXP>(r2, hs, ovf);
+}
+
 // Explicit dense operator (H2_S_DENSE_MATRIX): the producers read A(i, j)
 // from HBM instead of evaluating a kernel; with a power-of-two scale 2^E >= max|A| (hs = 2^-E,
 // exact), v = A hs in [-1, 1] takes the signed 53-bit format of the Helmholtz path:
@@ -368,7 +424,9 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const int nch = (int)(ch_e - ch_b);
   const bool control = (warp == NPW);
 
-  for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
+  if (KIND == H2_K_HELMHOLTZ && H2_TC_HTAB) fill_cs_table(tab, tid, NTH);
+  else
+    for (int e = tid; e < 16 * 256; e += NTH) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, NPW);
@@ -557,7 +615,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
-          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51<SliceFmt<NS>::HEXP>(r2, hs, ovf);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8)
+                                           : helm_eval<SliceFmt<NS>::HEXP>(r2, hs, ovf, tab, lane);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }
@@ -827,7 +886,9 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   const bool control = (warp == NPW);
   const int8_t* Bh = Bq + (int64_t)crank * nchunks * BBUF;   // this CTA's column half
 
-  for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
+  if (KIND == H2_K_HELMHOLTZ && H2_TC_HTAB) fill_cs_table(tab, tid, 32 * (NPW + 1));
+  else
+    for (int e = tid; e < 16 * 256; e += 32 * (NPW + 1)) tab[e] = exp2((double)(e >> TC_TAB_SHIFT) * TC_TAB_STEP + (double)SliceFmt<NS>::KEXP);
   if (tid == 0) {
     for (int b = 0; b < NA; ++b) {
       mbar_init(bar_full + 8 * b, leader ? 2 * NPW : NPW);   // leader: both CTAs' producers
@@ -944,7 +1005,8 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const double r2 = dist2_floor(ci[k].x, ci[k].y, ci[k].z, p.x, p.y, p.z);
-          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8) : helm_fixed51<SliceFmt<NS>::HEXP>(r2, hs, ovf);
+          const uint2 m = KIND == H2_K_EXP ? expk_fixed52(r2, tab, lane8)
+                                           : helm_eval<SliceFmt<NS>::HEXP>(r2, hs, ovf, tab, lane);
           lo[k][q] = m.x;
           hi[k][q] = m.y;
         }

@@ -10,16 +10,23 @@ CHILD = r'''
 import os, sys
 sys.path.insert(0, os.environ["ROOT"])
 import torch, paper_2506_16759_b200 as g
-from synth import uniform_points
+from synth import uniform_points, grid_points
 n, nc = int(sys.argv[1]), int(sys.argv[2])
-T = g.Tree(uniform_points(n, 3, 0), 64)
+kind = os.environ.get("AB_KIND", "exp")
+if kind == "exp":
+    X, kern = uniform_points(n, 3, 0), ("exp", 0.2)
+else:   # IE grid (BASELINE configs[3] shape): 2:2:1 box
+    m = int(round((n / 4) ** (1 / 3)))
+    X, kern = grid_points((2 * m, 2 * m, m), 1.0 / (2 * m)), ("helmholtz", 3.0)
+    n = X.shape[0]
+T = g.Tree(X, 64)
 Om = g.omega(n, nc)
-y = g.dense_sketch(T, Om, ("exp", 0.2), omega_quarters=True)
+y = g.dense_sketch(T, Om, kern, omega_quarters=True)
 torch.cuda.synchronize()
 ms = []
 for _ in range(3):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record(); y2 = g.dense_sketch(T, Om, ("exp", 0.2), omega_quarters=True); e1.record(); e1.synchronize()
+    e0.record(); y2 = g.dense_sketch(T, Om, kern, omega_quarters=True); e1.record(); e1.synchronize()
     ms.append(e0.elapsed_time(e1))
 print(f"{min(ms):8.2f} ms  (runs {', '.join(f'{m:.2f}' for m in ms)})  bitwise-equal {bool(torch.equal(y, y2))}  |y| {float(y.norm()):.12e}")
 '''
