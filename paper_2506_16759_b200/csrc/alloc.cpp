@@ -1,6 +1,7 @@
 // Device block cache (see alloc.hpp).
 #include "alloc.hpp"
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -9,6 +10,7 @@
 #include "common.cuh"
 
 namespace h2 {
+std::atomic<int64_t> g_cache_mallocs{0}, g_cache_malloc_bytes{0}, g_cache_frees{0};   // H2_TRACE
 namespace {
 
 struct Block {
@@ -52,6 +54,7 @@ void release_all(DeviceCache& c) {
     cudaEventSynchronize(kv.second.ready);
     cudaEventDestroy(kv.second.ready);
     cudaFree(kv.second.p);
+    ++g_cache_frees;
     c.held -= kv.second.bytes;
   }
   c.free_.clear();
@@ -63,9 +66,13 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
   DeviceCache& c = cache_of_current();
   const size_t want = round_size(bytes);
   std::lock_guard<std::mutex> g(c.mu);
-  // best fit among blocks of size in [want, 1.25 want]
+  // best fit among blocks of size in [want, 1.25 want]; large blocks (>= 64 MiB: the H^2's per-level
+  // B / D / basis arrays, sizes that repeat exactly from one build to the next) only within 1/32,
+  // so a request never takes the block an equally large later request of the same build needs
+  // (configs[4] near device capacity re-allocated ~85 GB per build with the 1.25 window)
+  const size_t slack = want >= (size_t(64) << 20) ? want / 32 : want / 4;
   auto it = c.free_.lower_bound(want);
-  if (it != c.free_.end() && it->first <= want + want / 4) {
+  if (it != c.free_.end() && it->first <= want + slack) {
     Block b = it->second;
     c.free_.erase(it);
     if (b.stream != st) H2_CUDA(cudaStreamWaitEvent(st, b.ready, 0));
@@ -75,9 +82,23 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, want);
-  if (e == cudaErrorMemoryAllocation) {
+  // out of device memory: release cached free blocks largest first, only as many bytes as the
+  // request needs (+ 1/8 slack), and retry; everything only as the last resort.  Releasing the
+  // whole cache on every miss made near-capacity workloads (configs[4]: base + new H^2 ~ 176 GB)
+  // re-allocate their entire working set every build (~1.1 s of cudaMalloc / cudaFree per build).
+  while (e == cudaErrorMemoryAllocation && !c.free_.empty()) {
     cudaGetLastError();
-    release_all(c);
+    size_t freed = 0;
+    while (!c.free_.empty() && freed < want + want / 8) {
+      auto last = std::prev(c.free_.end());
+      cudaEventSynchronize(last->second.ready);
+      cudaEventDestroy(last->second.ready);
+      cudaFree(last->second.p);
+      ++g_cache_frees;
+      c.held -= last->second.bytes;
+      freed += last->second.bytes;
+      c.free_.erase(last);
+    }
     e = cudaMalloc(&p, want);
   }
   if (e != cudaSuccess) {
@@ -87,6 +108,8 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
   }
   c.live[p] = want;
   c.held += want;
+  ++g_cache_mallocs;
+  g_cache_malloc_bytes += (int64_t)want;
   return p;
 }
 

@@ -5,9 +5,13 @@
 // reservation fragmented (measured, H2_TRACE=1).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstddef>
+#include <cstdint>
 
 namespace h2 {
+// cudaMalloc / cudaFree calls made by the cache (H2_TRACE=1 diagnostics, reset per build report)
+extern std::atomic<int64_t> g_cache_mallocs, g_cache_malloc_bytes, g_cache_frees;
 void* cache_alloc(size_t bytes, cudaStream_t st);   // throws h2::Error(H2_ERR_OOM) on failure
 void cache_free(void* p, cudaStream_t st);
 void cache_trim();                                  // release every cached block of this device

@@ -30,7 +30,8 @@ void count_launch() { ++g_launches; }
 namespace {
 
 thread_local std::string g_err;
-thread_local double g_alloc_ms = 0;   // host time inside cudaMallocAsync (H2_TRACE=1 diagnostics)
+thread_local double g_alloc_ms = 0;
+   // host time inside cudaMallocAsync (H2_TRACE=1 diagnostics)
 
 // Stream-ordered device array on the libh2 block cache (alloc.hpp): the per-level "single
 // allocation per operation" of PAPER.md L384 is a cache hit after the first build.
@@ -1779,7 +1780,9 @@ struct Builder {
     if (getenv("H2_TRACE")) {
       fprintf(stderr, "[h2 trace] host ms per phase:");
       for (int p = 0; p < H2_NPHASE; ++p) fprintf(stderr, " %.1f", timer.host_ms[p]);
-      fprintf(stderr, " | alloc %.1f ms\n", g_alloc_ms);
+      fprintf(stderr, " | alloc %.1f ms, cudaMalloc %lld (%.2f GB), cudaFree %lld\n", g_alloc_ms,
+              (long long)h2::g_cache_mallocs.exchange(0), h2::g_cache_malloc_bytes.exchange(0) / 1e9,
+              (long long)h2::g_cache_frees.exchange(0));
     }
   }
 };
