@@ -66,11 +66,8 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
   DeviceCache& c = cache_of_current();
   const size_t want = round_size(bytes);
   std::lock_guard<std::mutex> g(c.mu);
-  // best fit among blocks of size in [want, 1.25 want]; large blocks (>= 64 MiB: the H^2's per-level
-  // B / D / basis arrays, sizes that repeat exactly from one build to the next) only within 1/32,
-  // so a request never takes the block an equally large later request of the same build needs
-  // (configs[4] near device capacity re-allocated ~85 GB per build with the 1.25 window)
-  const size_t slack = want >= (size_t(64) << 20) ? want / 32 : want / 4;
+  // best fit among blocks of size in [want, 1.25 want]
+  const size_t slack = want / 4;
   auto it = c.free_.lower_bound(want);
   if (it != c.free_.end() && it->first <= want + slack) {
     Block b = it->second;
@@ -82,22 +79,34 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, want);
-  // out of device memory: release cached free blocks largest first, only as many bytes as the
-  // request needs (+ 1/8 slack), and retry; everything only as the last resort.  Releasing the
-  // whole cache on every miss made near-capacity workloads (configs[4]: base + new H^2 ~ 176 GB)
-  // re-allocate their entire working set every build (~1.1 s of cudaMalloc / cudaFree per build).
+  // out of device memory: release as little of the cache as the request needs -- first the
+  // smallest free block that covers the deficit (want - the device's free memory), else the
+  // largest ones until it is covered -- and retry; releasing the whole cache on every miss made
+  // near-capacity workloads (configs[4]: base + new H^2 ~ 176 GB of 180) re-allocate their entire
+  // working set every build.
   while (e == cudaErrorMemoryAllocation && !c.free_.empty()) {
     cudaGetLastError();
-    size_t freed = 0;
-    while (!c.free_.empty() && freed < want + want / 8) {
-      auto last = std::prev(c.free_.end());
-      cudaEventSynchronize(last->second.ready);
-      cudaEventDestroy(last->second.ready);
-      cudaFree(last->second.p);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t deficit = want > fr ? want - fr + (size_t(64) << 20) : (size_t(64) << 20);
+    auto drop = [&](std::multimap<size_t, Block>::iterator it) {
+      cudaEventSynchronize(it->second.ready);
+      cudaEventDestroy(it->second.ready);
+      cudaFree(it->second.p);
       ++g_cache_frees;
-      c.held -= last->second.bytes;
-      freed += last->second.bytes;
-      c.free_.erase(last);
+      c.held -= it->second.bytes;
+      c.free_.erase(it);
+    };
+    auto cover = c.free_.lower_bound(deficit);
+    if (cover != c.free_.end()) {
+      drop(cover);
+    } else {
+      size_t freed = 0;
+      while (!c.free_.empty() && freed < deficit) {
+        auto last = std::prev(c.free_.end());
+        freed += last->second.bytes;
+        drop(last);
+      }
     }
     e = cudaMalloc(&p, want);
   }

@@ -20,28 +20,48 @@ namespace h2 {
 __device__ void cta_gemm(int M, int N, int K, const double* __restrict__ A, int64_t lda, bool tA,
                          const int32_t* __restrict__ arow, const double* __restrict__ B, int64_t ldb, bool tB,
                          const int32_t* __restrict__ bcol, double* __restrict__ C, int64_t ldc, double beta) {
+  // Round 2: (a) the slab loads are coalesced for every operand orientation -- a row-major operand
+  // (A not transposed, B transposed: one row of the slab is 16 consecutive k) is read by
+  // half-warps along k, a column-major one along i / j -- instead of 8 bytes per 32-byte sector
+  // for the strided ones; (b) the next slab is loaded into registers while the current one is
+  // multiplied (one slab in flight per thread).  The DMMA sequence per accumulator (k ascending
+  // in groups of 4, zero-filled edges) is unchanged: bitwise the previous results.
   __shared__ double sA[16][64 + 1];
   __shared__ double sB[16][64 + 1];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 3, wc = warp >> 2;   // 8 warps: 4 x 16 rows, 2 x 32 columns
+  // element q of this thread: A slab entry (ar[q], ak[q]) and B slab entry (bk[q], bc[q])
+  int ar[4], ak[4], bk[4], bc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + 256 * q;
+    if (tA) { ak[q] = e >> 6; ar[q] = e & 63; } else { ar[q] = e >> 4; ak[q] = e & 15; }
+    if (tB) { bc[q] = e >> 4; bk[q] = e & 15; } else { bk[q] = e >> 6; bc[q] = e & 63; }
+  }
   for (int i0 = 0; i0 < M; i0 += 64)
     for (int j0 = 0; j0 < N; j0 += 64) {
       double acc[2][4][2] = {};
+      double ra[4], rb[4];
+      auto load = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + ar[q], k = k0 + ak[q];
+          ra[q] = (i < M && k < K) ? (tA ? A[(int64_t)k * lda + i] : A[(int64_t)(arow ? arow[i] : i) * lda + k]) : 0.0;
+          const int j = j0 + bc[q], kb = k0 + bk[q];
+          rb[q] = (j < N && kb < K) ? (tB ? B[(int64_t)(bcol ? bcol[j] : j) * ldb + kb] : B[(int64_t)kb * ldb + j]) : 0.0;
+        }
+      };
+      load(0);
       for (int k0 = 0; k0 < K; k0 += 16) {
-        __syncthreads();
-        for (int e = tid; e < 16 * 64; e += 256) {
-          const int kk = e >> 6, r = e & 63;
-          const int i = i0 + r, k = k0 + kk;
-          double a = 0.0;
-          if (i < M && k < K) a = tA ? A[(int64_t)k * lda + i] : A[(int64_t)(arow ? arow[i] : i) * lda + k];
-          sA[kk][r] = a;
-          const int j = j0 + r;
-          double b = 0.0;
-          if (j < N && k < K) b = tB ? B[(int64_t)(bcol ? bcol[j] : j) * ldb + k] : B[(int64_t)k * ldb + j];
-          sB[kk][r] = b;
+        __syncthreads();   // the previous slab's fragments have been read
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          sA[ak[q]][ar[q]] = ra[q];
+          sB[bk[q]][bc[q]] = rb[q];
         }
         __syncthreads();
+        if (k0 + 16 < K) load(k0 + 16);   // in flight during the DMMAs below
         // FP64 tensor cores (DMMA m8n8k4): warp (wr, wc) owns rows 16 wr.. x columns 32 wc..
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
@@ -69,6 +89,7 @@ __device__ void cta_gemm(int M, int N, int K, const double* __restrict__ A, int6
               *c = beta == 0.0 ? acc[p][q][h] : fma(beta, *c, acc[p][q][h]);
             }
           }
+      __syncthreads();   // the next tile overwrites sA / sB
     }
 }
 
