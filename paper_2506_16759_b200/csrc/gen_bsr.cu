@@ -271,9 +271,12 @@ __global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr_kernel(B
 // ------------------------------------------------------------------------------------------
 constexpr int B2_LDA = 36;   // A slab row stride (doubles): conflict-free fragment reads
 constexpr int B2_MAXP = 256; // partners per row cluster staged in shared memory
-template <int CW, int NS, bool COLFAST, int KD = 32>
-__global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
-  constexpr int NT = 4 * CW;                 // 128 threads per 32 columns
+// WM: 8-row DMMA blocks per warp (2: warp tile 16 x 32, 4: 32 x 32 -- half the A-fragment loads per
+// DMMA); warps NWR = 64 / (8 WM) along rows x CW / 32 along columns
+template <int CW, int NS, bool COLFAST, int KD = 32, int WM = 2>
+__global__ void __launch_bounds__(32 * (64 / (8 * WM)) * (CW / 32)) bsr2_kernel(BsrArgs a, double alpha) {
+  constexpr int NWR = 64 / (8 * WM);
+  constexpr int NT = 32 * NWR * (CW / 32);
   constexpr int NW = NT / 32;
   constexpr int LDA = KD + 4;                // A slab row stride: = 4 mod 16 doubles, conflict-free fragments
   constexpr int LDB = CW + 4;
@@ -293,9 +296,6 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bsm);
   const int rows_here = min(BT_R, ms - r0);
-  // loader geometry (fixed per thread): B element (kk = warp / (CW/32) + 4 q, c = lane + 32 (warp % (CW/32)))
-  const int bc = lane + 32 * (warp % (CW / 32));
-  const int bk0 = warp / (CW / 32);
   // partner metadata of this row cluster staged once in shared memory (one round trip per CTA
   // instead of a dependent global-load chain idx -> uidx -> blk_off / cnt per slab, which was the
   // top stall after the loop rewrite: long scoreboard on the slab addresses)
@@ -382,13 +382,14 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       }
     }
     {
-      const double* om = a.Om + orow * a.ldo + cb + bc;
-      const bool cok = bc < nc;
+      // B slab element e = tid + NT q: (kk = e / CW, c = e % CW), consecutive lanes along c
+      const double* om = a.Om + orow * a.ldo + cb;
 #pragma unroll
-      for (int q = 0; q < KD / 4; ++q) {
-        const int kk = bk0 + 4 * q;
-        const bool ok = cok && kk < nk;
-        cp_async8(sb + (uint32_t)(kk * LDB + bc) * 8u, ok ? om + (int64_t)(lk + kk) * a.ldo : a.Om, ok);
+      for (int q = 0; q < KD * CW / NT; ++q) {
+        const int e = tid + NT * q;
+        const int kk = e / CW, c = e % CW;
+        const bool ok = c < nc && kk < nk;
+        cp_async8(sb + (uint32_t)(kk * LDB + c) * 8u, ok ? om + (int64_t)(lk + kk) * a.ldo + c : a.Om, ok);
       }
     }
     if (tid == 0) st_nk[buf] = nk;
@@ -398,10 +399,10 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
       lk = 0;
     }
   };
-  const int wr = warp & 3, wc = warp >> 2;
-  double acc[2][4][2];
+  const int wr = warp % NWR, wc = warp / NWR;
+  double acc[WM][4][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
     asm volatile("cp.async.commit_group;\n" ::);
   }
   // fragment base offsets (doubles) inside a stage
-  const int offa = (wr * 16 + (lane >> 2)) * LDA + (lane & 3);
+  const int offa = (wr * 8 * WM + (lane >> 2)) * LDA + (lane & 3);
   const int offb = ASZ + (lane & 3) * LDB + wc * 32 + (lane >> 2);
   for (int it = 0; it < nitems; ++it) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(NS - 2));
@@ -422,14 +423,15 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
     const double* pb = st + offb;
     const int ksteps = (st_nk[it % NS] + 3) >> 2;
     auto kstep = [&](int ks) {
-      const double a0 = pa[ks * 4], a1 = pa[8 * LDA + ks * 4];
-      double bf[4];
+      double af[WM], bf[4];
+#pragma unroll
+      for (int i = 0; i < WM; ++i) af[i] = pa[i * 8 * LDA + ks * 4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = pb[ks * 4 * LDB + j * 8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[0][j][0], acc[0][j][1], a0, bf[j]);
+      for (int i = 0; i < WM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[1][j][0], acc[1][j][1], a1, bf[j]);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     };
     if (ksteps == KD / 4) {
       // full slab: no per-step guard, so the fragment loads of later k steps can be scheduled
@@ -444,8 +446,8 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int r = r0 + wr * 16 + i * 8 + (lane >> 2);
+  for (int i = 0; i < WM; ++i) {
+    const int r = r0 + wr * 8 * WM + i * 8 + (lane >> 2);
     if (r >= ms) continue;
     double* y = a.Y + (a.yoff[s] + r) * a.ldy + cb;
 #pragma unroll
@@ -457,16 +459,18 @@ __global__ void __launch_bounds__(4 * CW) bsr2_kernel(BsrArgs a, double alpha) {
   }
 }
 
-template <int CW, int NS, bool COLFAST, int KD = 32>
+template <int CW, int NS, bool COLFAST, int KD = 32, int WM = 2>
 static void bsr2_go(const BsrArgs& a, double alpha, cudaStream_t st) {
   const size_t sm = sizeof(double) * NS * (BT_R * (KD + 4) + KD * (CW + 4));
-  H2_CUDA(cudaFuncSetAttribute(bsr2_kernel<CW, NS, COLFAST, KD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  constexpr int NT = 32 * (64 / (8 * WM)) * (CW / 32);
+  H2_CUDA(cudaFuncSetAttribute(bsr2_kernel<CW, NS, COLFAST, KD, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm));
   if (COLFAST)
-    bsr2_kernel<CW, NS, COLFAST, KD><<<dim3(div_up(a.ncols, CW), a.nclusters, div_up(a.max_rows, BT_R)), 4 * CW, sm,
-                                       st>>>(a, alpha);
+    bsr2_kernel<CW, NS, COLFAST, KD, WM><<<dim3(div_up(a.ncols, CW), a.nclusters, div_up(a.max_rows, BT_R)), NT, sm,
+                                           st>>>(a, alpha);
   else
-    bsr2_kernel<CW, NS, COLFAST, KD><<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, CW)), 4 * CW, sm,
-                                       st>>>(a, alpha);
+    bsr2_kernel<CW, NS, COLFAST, KD, WM><<<dim3(a.nclusters, div_up(a.max_rows, BT_R), div_up(a.ncols, CW)), NT, sm,
+                                           st>>>(a, alpha);
   H2_CHECK_LAUNCH();
 }
 
@@ -474,8 +478,12 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
   if (a.nclusters <= 0 || a.ncols <= 0 || a.max_rows <= 0) return;
   // H2_BSR2: 0 = the round-1 kernel family below; 1 = bsr2 32-column tiles (column-fast grid for
   // wide passes); 2 = bsr2 64-column tiles; 3 = bsr2 32-column tiles, 3-stage ring; 4 / 5 = 16-deep
-  // slabs (half the shared memory per stage: 7 / 5 CTAs per SM), 2 / 3 stages
-  static const int v2 = env_int("H2_BSR2", 1);
+  // slabs (half the shared memory per stage: 7 / 5 CTAs per SM), 2 / 3 stages; 6 / 7 = 160- / 96-column
+  // CTAs; 8 / 9 / 10 = 64-column CTAs of four 32 x 32 warp tiles (half the A-fragment loads per DMMA)
+  // over the 64-multiple of the columns + 32-column tiles for the rest, 32-deep / 16-deep slabs,
+  // 16-deep with 3 stages
+  // default 9: 54.9 vs 57.9 ms (variant 1) for the C2 BSR phase (profiles/r2_bsr2_ncu.md)
+  static const int v2 = env_int("H2_BSR2", 9);
   if (v2 != 0) {
     const bool wide = a.ncols > 32;
     if (v2 == 2 && a.ncols > 32) bsr2_go<64, 2, true>(a, alpha, st);
@@ -484,6 +492,22 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
     else if (v2 == 5) wide ? bsr2_go<32, 3, true, 16>(a, alpha, st) : bsr2_go<32, 3, false, 16>(a, alpha, st);
     else if (v2 == 6 && a.ncols > 128) bsr2_go<160, 2, true>(a, alpha, st);   // one CTA per 160 columns
     else if (v2 == 7 && a.ncols > 64) bsr2_go<96, 2, true>(a, alpha, st);
+    else if ((v2 == 8 || v2 == 9 || v2 == 10) && a.ncols > 32) {
+      // 64-column CTA tiles with 32 x 32 warp tiles over the first 64-multiple of the columns, the
+      // remaining (< 64) columns in 32-column tiles: no half-empty column tile at 160 columns
+      const int main = a.ncols / 64 * 64;
+      BsrArgs m = a;
+      m.ncols = main;
+      if (v2 == 8) bsr2_go<64, 2, true, 32, 4>(m, alpha, st);
+      else if (v2 == 9) bsr2_go<64, 2, true, 16, 4>(m, alpha, st);
+      else bsr2_go<64, 3, true, 16, 4>(m, alpha, st);
+      if (a.ncols > main) {
+        BsrArgs t = a;
+        t.c0 = a.c0 + main;
+        t.ncols = a.ncols - main;
+        bsr2_go<32, 2, true>(t, alpha, st);
+      }
+    }
     else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);
     return;
   }
