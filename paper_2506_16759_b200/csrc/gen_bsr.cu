@@ -498,7 +498,8 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
       const int main = a.ncols / 64 * 64;
       BsrArgs m = a;
       m.ncols = main;
-      if (v2 == 8) bsr2_go<64, 2, true, 32, 4>(m, alpha, st);
+      if (main == 0) {
+      } else if (v2 == 8) bsr2_go<64, 2, true, 32, 4>(m, alpha, st);
       else if (v2 == 9) bsr2_go<64, 2, true, 16, 4>(m, alpha, st);
       else bsr2_go<64, 3, true, 16, 4>(m, alpha, st);
       if (a.ncols > main) {
