@@ -60,7 +60,11 @@ __host__ __device__ inline int cq_ld(int d) { return ((d + 7) / 8) * 8 + (((d + 
 // updated are held in registers for the step (the row is read once and written once instead of
 // read twice and written once, v is read once per step instead of twice per row); the same
 // operations in the same order as E = 0, so the factorisation is bitwise unchanged.
-template <bool SMEM, int CQ_THREADS, int E = 0>
+// HYB (global-panel variant only, round 2): once the ACTIVE part of the panel (rows i.., columns
+// i..) fits the dynamic shared memory, it is moved there (rows of later pivots swap their retired
+// columns < i0 in W) and the factorisation continues in shared memory; copied back at the end.
+// Same operations in the same order: bitwise the all-global factorisation.
+template <bool SMEM, int CQ_THREADS, int E = 0, bool HYB = false>
 __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   constexpr int CQ_WARPS = CQ_THREADS / 32;
   constexpr int RPP = CQ_THREADS / CQ_TPR;      // rows per pass
@@ -79,6 +83,15 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
   const int64_t off = a.poff[c];
   double* A = SMEM ? spanel : a.W + off * d;
+  // element (j, r) of the work panel at rowp(j)[r], r >= ro: before a HYB switch the panel itself
+  // (ro = 0), after it the shared-memory copy of rows / columns >= ro
+  double* Ab = A;
+  int64_t LDa = LD;
+  int ro = 0;
+  auto rowp = [&](int j) { return Ab + (int64_t)(j - ro) * LDa - ro; };
+  uint32_t dyn_bytes = 0;
+  if constexpr (HYB) asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
+  const int64_t hyb_cap = HYB ? (int64_t)(dyn_bytes / 8) - (int64_t)(spanel - smem) : 0;   // doubles
   // copy panel rows (Y^loc rows) into the work panel
   for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
     const int64_t j = e / d;
@@ -126,6 +139,20 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   double min_gap = INFINITY, margin = INFINITY;
   int k = 0;
   for (int i = 0;; ++i) {
+    if constexpr (HYB) {
+      // all threads passed the previous step's final barrier: move the active part if it fits
+      if (ro == 0 && i > 0 && i < m && i < d && (int64_t)(m - i) * cq_ld(d - i) <= hyb_cap) {
+        const int LDs = cq_ld(d - i), w = d - i;
+        for (int64_t e = threadIdx.x; e < (int64_t)(m - i) * w; e += CQ_THREADS) {
+          const int64_t j = e / w;
+          spanel[j * LDs + (e - j * w)] = A[(i + j) * (int64_t)LD + i + (e - j * w)];
+        }
+        __syncthreads();
+        Ab = spanel;
+        LDa = LDs;
+        ro = i;
+      }
+    }
     // every warp merges the per-warp candidates with one butterfly (same result in all threads)
     Top2 t = lane < CQ_WARPS ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
     t = warp_top2(t);
@@ -138,15 +165,24 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     }
     if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
     const int p = t.i;
-    double* Ai = A + (int64_t)i * LD;
+    double* Ai = rowp(i);
     if (warp == 0) {
       // ---- swap rows i and p of the panel (columns of A)
       if (p != i) {
-        double* Ap = A + (int64_t)p * LD;
-        for (int r = lane; r < d; r += 32) {
+        double* Ap = rowp(p);
+        for (int r = ro + lane; r < d; r += 32) {
           const double x = Ai[r];
           Ai[r] = Ap[r];
           Ap[r] = x;
+        }
+        if (HYB && ro > 0) {   // their retired columns < ro stay in the panel in W
+          double* Gi = A + (int64_t)i * LD;
+          double* Gp = A + (int64_t)p * LD;
+          for (int r = lane; r < ro; r += 32) {
+            const double x = Gi[r];
+            Gi[r] = Gp[r];
+            Gp[r] = x;
+          }
         }
         if (lane == 0) {
           const int q = perm[i];
@@ -232,7 +268,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     for (int j0 = i + 1; j0 < m; j0 += RPP) {
       const int j = j0 + rloc;
       const bool act = j < m;
-      double* Aj = A + (int64_t)(act ? j : i) * LD;
+      double* Aj = rowp(act ? j : i);
       double w = 0.0;
       if (act)
         for (int r = r0; r < d; r += CQ_TPR) w = fma(v[r], Aj[r], w);
@@ -257,6 +293,13 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     k = i + 1;
   }
   __syncthreads();
+  if (HYB && ro > 0) {   // the shared-memory part back into the panel in W
+    const int w = d - ro;
+    for (int64_t e = threadIdx.x; e < (int64_t)(m - ro) * w; e += CQ_THREADS) {
+      const int64_t j = e / w;
+      A[(ro + j) * (int64_t)LD + ro + (e - j * w)] = spanel[j * LDa + (e - j * w)];
+    }
+  }
   for (int j = threadIdx.x; j < m; j += CQ_THREADS) a.perm[off + j] = perm[j];
   if (SMEM) {
     double* Wc = a.W + off * d;
@@ -660,11 +703,11 @@ static void cpqr1_launch(const CpqrArgs& a, size_t sm, double* scratch, cudaStre
   cpqr1_kernel<SMEM, NT><<<a.nclusters, NT, sm, st>>>(a, scratch);
 }
 
-template <bool SMEM, int NT, int E = 0>
+template <bool SMEM, int NT, int E = 0, bool HYB = false>
 static void cpqr_launch_e(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   if (sm > 48 * 1024)
-    H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<SMEM, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  cpqr_kernel<SMEM, NT, E><<<a.nclusters, NT, sm, st>>>(a);
+    H2_CUDA(cudaFuncSetAttribute(cpqr_kernel<SMEM, NT, E, HYB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cpqr_kernel<SMEM, NT, E, HYB><<<a.nclusters, NT, sm, st>>>(a);
 }
 
 // register-cached variant when every thread's entries fit E (d <= 8 E): opt-in (H2_CQ_REG=1);
@@ -911,7 +954,14 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
     else cpqr_launch<true, 256>(a, sm, st);
     used = H2_CQ_V_SMEM;
   } else {
-    if (big) cpqr_launch<false, 512>(a, sm, st);
+    // H2_CQ_HYB = shared memory (KB) per CTA for the global-panel variant's switch to shared
+    // memory once the active part fits (0: off)
+    const int hyb = env_int("H2_CQ_HYB", 0);
+    if (hyb > 0) {
+      const size_t smh = std::max(sm, (size_t)std::min(hyb, 200) * 1024);
+      if (big) cpqr_launch_e<false, 512, 0, true>(a, smh, st);
+      else cpqr_launch_e<false, 256, 0, true>(a, smh, st);
+    } else if (big) cpqr_launch<false, 512>(a, sm, st);
     else cpqr_launch<false, 256>(a, sm, st);
     used = H2_CQ_V_GLOBAL;
   }

@@ -370,3 +370,33 @@ np.save(sys.argv[1], np.concatenate(out + [H._export(g._lib.H2_X_D), np.array([H
         res.append(np.load(f))
         os.remove(f)
     assert res[0].shape == res[1].shape and np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("hyb", ["110", "200"])
+def test_cpqr_hybrid_panel_bitwise(hyb):
+    """H2_CQ_HYB: the global-panel CPQR moves the active part of the panel into shared memory once
+    it fits and continues there -- the same operations in the same order, so with the global
+    variant forced on every block-panel level the H^2 is bitwise the all-global one."""
+    import subprocess, sys, os, tempfile
+    code = r'''
+import sys, os, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+import paper_2506_16759_b200 as g
+from synth import uniform_points
+T = g.Tree(uniform_points(6000, 3, 2), 64)
+H = g.build(T, ("exp", 0.2), 1e-6, d_init=32, d_blk=32)
+assert H.stats["cpqr_variants"] & g._lib.H2_CQ_V_GLOBAL
+out = [H._export(g._lib.H2_X_BASIS, t) for t in range(H.top_depth, T.leaf_depth + 1)]
+out += [H._export(g._lib.H2_X_CERT, t) for t in range(H.top_depth, T.leaf_depth + 1)]
+out += [H._export(g._lib.H2_X_B, t) for t in range(H.top_depth, T.leaf_depth + 1)]
+np.save(sys.argv[1], np.concatenate(out + [np.array([H.samples], float)]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for val in ("0", hyb):
+        f = tempfile.mktemp(suffix=".npy")
+        env = dict(os.environ, ROOT=root, H2_CQ_VARIANT="global", H2_CQ_HYB=val)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=env)
+        res.append(np.load(f))
+        os.remove(f)
+    assert res[0].shape == res[1].shape and np.array_equal(res[0], res[1])
