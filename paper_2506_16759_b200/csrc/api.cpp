@@ -16,6 +16,8 @@
 #include <map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "alloc.hpp"
 #include "comm.hpp"
@@ -133,7 +135,12 @@ struct PhaseTimer {
   double host_ms[H2_NPHASE] = {};   // host wall time spent issuing each phase (H2_TRACE=1)
   std::chrono::steady_clock::time_point h0;
   explicit PhaseTimer(cudaStream_t s) : st(s) {}
+  // NVTX ranges (SURVEY §5 tracing): one per phase ("h2 sketch", "h2 bsr", ...) nested in one
+  // per processed depth ("h2 depth t"), for nsys / ncu --nvtx
+  bool depth_open = false;
   void begin(int ph) {
+    static const char* names[H2_NPHASE] = {"h2 rand", "h2 sketch", "h2 gen", "h2 bsr", "h2 cpqr", "h2 id", "h2 misc"};
+    nvtxRangePushA(names[ph]);
     h0 = std::chrono::steady_clock::now();
     cudaEvent_t e;
     H2_CUDA(cudaEventCreate(&e));
@@ -147,6 +154,7 @@ struct PhaseTimer {
     H2_CUDA(cudaEventRecord(e, st));
     ev.push_back({cur, {cur_ev, e}});
     host_ms[cur] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    nvtxRangePop();
   }
   void collect(double* out) {
     for (auto& x : ev) {
@@ -158,6 +166,13 @@ struct PhaseTimer {
   // per-depth device time (h2_build_stats.t_depth_ms): [mark(t), mark(next)) on the build stream
   std::vector<std::pair<int, cudaEvent_t>> marks;
   void mark(int t) {
+    if (depth_open) nvtxRangePop();
+    depth_open = t >= 0;
+    if (depth_open) {
+      char nm[32];
+      snprintf(nm, sizeof nm, "h2 depth %d", t);
+      nvtxRangePushA(nm);
+    }
     cudaEvent_t e;
     H2_CUDA(cudaEventCreate(&e));
     H2_CUDA(cudaEventRecord(e, st));
