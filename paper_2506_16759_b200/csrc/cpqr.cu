@@ -138,6 +138,14 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
   double min_gap = INFINITY, margin = INFINITY;
   int k = 0;
+  // -DH2_CQ_PROF: cycles per pivot step by phase (clock64), printed for two CTAs
+#ifdef H2_CQ_PROF
+  long long pr[6] = {0, 0, 0, 0, 0, 0}, tp0 = 0, tp1 = 0;
+#define CQP(n) do { tp1 = clock64(); pr[n] += tp1 - tp0; tp0 = tp1; } while (0)
+  tp0 = clock64();
+#else
+#define CQP(n) do { } while (0)
+#endif
   for (int i = 0;; ++i) {
     if constexpr (HYB) {
       // all threads passed the previous step's final barrier: move the active part if it fits
@@ -156,6 +164,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     // every warp merges the per-warp candidates with one butterfly (same result in all threads)
     Top2 t = lane < CQ_WARPS ? red[lane] : Top2{-1.0, 0x7fffffff, -1.0};
     t = warp_top2(t);
+    CQP(0);   // pivot merge
     if (i >= m) break;
     // truncation margin of every decision taken (R13); no decision exists at i = min(d, m)
     if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
@@ -221,7 +230,9 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
         s_tau = tau;
       }
     }
+    CQP(1);   // warp 0: swap + reflector (other warps: arrive)
     __syncthreads();
+    CQP(2);   // barrier 1
     const double tau = s_tau;
     // ---- trailing update of rows j > i (columns of A) + next residual norms + local pivot
     Top2 loc{-1.0, 0x7fffffff, -1.0};
@@ -289,9 +300,18 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     }
     loc = warp_best(loc);
     if (lane == 0) red[warp] = loc;
+    CQP(3);   // trailing update + local pivot
     __syncthreads();
+    CQP(4);   // barrier 2
     k = i + 1;
   }
+#ifdef H2_CQ_PROF
+  if ((threadIdx.x == 0 || threadIdx.x == 32 * (CQ_WARPS - 1)) && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2))
+    printf("[cq prof] blk %d thr %d m %d d %d k %d | merge %lld refl %lld bar1 %lld upd %lld bar2 %lld (cycles/step %lld)\n",
+           blockIdx.x, threadIdx.x, m, d, k, pr[0] / max(k, 1), pr[1] / max(k, 1), pr[2] / max(k, 1), pr[3] / max(k, 1),
+           pr[4] / max(k, 1), (pr[0] + pr[1] + pr[2] + pr[3] + pr[4]) / max(k, 1));
+#endif
+#undef CQP
   __syncthreads();
   if (HYB && ro > 0) {   // the shared-memory part back into the panel in W
     const int w = d - ro;
