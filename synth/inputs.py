@@ -47,6 +47,8 @@ WORKLOADS = {
     # BASELINE.json configs[1]: 3D covariance, N=2^18 uniform, leaf 64, tol 1e-6, dense-kernel sketch
     "cov3d_256k": dict(points=lambda: uniform_points(1 << 18, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     # BASELINE.json configs[2]: 3D exp covariance, N=2^21
+    # S§8(f) NEXT #1 at N = 2^20 (the O(N) H^2-matvec sketch of a bootstrap H^2; tools/run_config.py --bootstrap)
+    "cov3d_1m": dict(points=lambda: uniform_points(1 << 20, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     "cov3d_2m": dict(points=lambda: uniform_points(1 << 21, 3, 0), kernel="exp", param=0.2, leaf=64, tol=1e-6),
     # BASELINE.json configs[3]: volume IE cos(3r)/r on a 128x128x64 grid (N=2^20), tol 1e-4
     "ie3d_1m": dict(points=lambda: grid_points((128, 128, 64), 1.0 / 128), kernel="helmholtz", param=3.0,
