@@ -223,6 +223,7 @@ struct Panel {
 void matvec_impl(const h2_matrix& H, const double* x, int64_t ldx, double* y, int64_t ldy, int32_t q, double alpha,
                  double beta, cudaStream_t st, int rank = 0, int nranks = 1);
 void ensure_partition_uploaded(const h2_tree* tree);
+bool ensure_near_chunks(const h2_tree* tree);
 KernelParams tree_kernel(const h2_tree* tree, const h2_kernel& k, cudaStream_t st);
 void apply_sketch_op(const h2_tree& T, const h2_sketch& S, const double* Om, int64_t ldo, int nc, double* Y,
                      int64_t ldy, bool quarters, bool exact, cudaStream_t st);
@@ -678,6 +679,34 @@ struct Builder {
     return bsr_work[t] = {e, r};
   }
 
+  // ---------------------------------------------------------------- leaf subtraction (L213)
+  // With the built-in exp dense-kernel sketch on the tensor cores and the same kernel as the entry
+  // evaluator, Y^loc = Y - sum_{b in N} D_{tau,b} Omega_b is computed from the kernel itself on the
+  // int8 tensor cores (launch_near_sketch_tc: near leaves only, the sketch's fixed-point K) instead
+  // of the BSR product over the stored D blocks: no D read from HBM (the D blocks are still
+  // generated for the H^2).  H2_NEAR_TC=0 keeps the BSR path.
+  bool near_tc_ok(int nc) {
+    static const bool on = env_int("H2_NEAR_TC", 1) != 0;
+    if (!on || ex || !spec_on || S.kind != H2_S_DENSE_KERNEL || S.kern.kind != H2_K_EXP) return false;
+    if (E.kind != H2_E_BUILTIN || E.kern.kind != S.kern.kind || E.kern.param != S.kern.param) return false;
+    if (nc > sketch_tc_pass_cols(skp.kind)) return false;
+    return ensure_near_chunks(&T);
+  }
+  void leaf_subtract(double* Yp, const double* Op, int64_t ld, int nc) {
+    if (!near_tc_ok(nc)) {
+      bsr(T.Dl, Yp, Op, ld, nc);
+      return;
+    }
+    timer.begin(H2_PH_BSR);
+    const auto er = bsr_entries(T.Dl);   // the same algorithmic work as the BSR form
+    wf[H2_PH_BSR] += 2.0 * nc * er.first;
+    wb[H2_PH_BSR] += 8.0 * nc * 3.0 * er.second;
+    // Omega: every row (the near leaves' j), Y: this rank's leaf rows
+    launch_near_sketch_tc(skp, T.d_x, T.d_y, T.d_z, T.n, row_b(), row_e(), Op, ld, nc, Yp + row_b() * ld, ld,
+                          T.d_nl_ptr, T.d_nl_chunk, T.d_nl_mask, st);
+    timer.end();
+  }
+
   // ---------------------------------------------------------------- BSR subtraction on a panel of depth t
   // leaf (t == Dl): Y(I_tau) -= sum_{b in N_tau} D Om(I_b)   (L213)
   // inner: Y^l_t(rows of child nu) -= sum_{b in F_nu} B_{nu,b} Om^l_t(rows of b)   (L240-243)
@@ -1018,13 +1047,13 @@ struct Builder {
     grow(cur, d + b);
     if (t == T.Dl) {
       draw(cur.Y.p + c0, cur.O.p + c0, cur.ld, c0, b);
-      bsr(T.Dl, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
+      leaf_subtract(cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
       return;
     }
     Panel src;
     src.alloc(T.n, b, st);
     draw(src.Y.p, src.O.p, b, c0, b);
-    bsr(T.Dl, src.Y.p, src.O.p, b, b);
+    leaf_subtract(src.Y.p, src.O.p, b, b);
     for (int u = T.Dl; u > t; --u) {
       if (u - 1 == t) {
         shrink(u, src.Y.p, src.O.p, src.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, b);
@@ -1133,12 +1162,12 @@ struct Builder {
     grow(cur, dw + W, dw);
     if (t == T.Dl) {
       draw_pass(cur.Y.p + c0, cur.O.p + c0, cur.ld, c0, W);
-      bsr(T.Dl, cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
+      leaf_subtract(cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
     } else {
       Panel src;
       src.alloc(T.n, W, st);
       draw_pass(src.Y.p, src.O.p, W, c0, W);
-      bsr(T.Dl, src.Y.p, src.O.p, W, W);
+      leaf_subtract(src.Y.p, src.O.p, W, W);
       for (int u = T.Dl; u > t; --u) {
         if (u - 1 == t) {
           shrink(u, src.Y.p, src.O.p, src.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, W);
@@ -1170,7 +1199,7 @@ struct Builder {
     timer.mark(Dl);
     gen_D();                                        // line 212
     setup_level(Dl);
-    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, dw);          // line 213, every column of the pass
+    leaf_subtract(cur.Y.p, cur.O.p, cur.ld, dw);    // line 213, every column of the pass
     for (int t = Dl; t >= top; --t) {
       if (t < Dl) {
         timer.mark(t);
@@ -1648,7 +1677,7 @@ struct Builder {
     timer.mark(Dl);
     gen_D();
     setup_level(Dl);
-    bsr(Dl, cur.Y.p, cur.O.p, cur.ld, d);   // line 213
+    leaf_subtract(cur.Y.p, cur.O.p, cur.ld, d);   // line 213
     run_levels(H.top, Dl);
   }
 
@@ -1945,6 +1974,48 @@ void ensure_partition_uploaded(const h2_tree* tree) {
 void ensure_uploaded(const h2_tree* tree) {
   ensure_order_uploaded(tree);
   ensure_partition_uploaded(tree);
+}
+
+// per-leaf near-field chunk lists for launch_near_sketch_tc (built once per tree, on the tree's
+// device): eligible when every leaf holds exactly 64 points at a multiple of 64 (row tiles =
+// leaves); leaf s lists the 128-j chunks b / 2 of its near leaves b (ascending) with the mask of
+// the 64-j halves (bit b & 1) that are near leaves
+bool ensure_near_chunks(const h2_tree* tree) {
+  h2_tree& T = *const_cast<h2_tree*>(tree);
+  if (T.nl_state != 0) return T.nl_state > 0;
+  const int Dl = T.Dl;
+  const int nleaf = 1 << Dl;
+  bool ok = T.n == ((int64_t)64 << Dl);
+  for (int c = 0; c < nleaf && ok; ++c) ok = T.begin[Dl][c] == 64 * (int64_t)c && T.end[Dl][c] == 64 * (int64_t)c + 64;
+  if (!ok) {
+    T.nl_state = -1;
+    return false;
+  }
+  std::vector<int32_t> ptr(nleaf + 1, 0), chunk;
+  std::vector<uint8_t> mask;
+  for (int c = 0; c < nleaf; ++c) {
+    ptr[c] = (int32_t)chunk.size();
+    for (int e = T.near.ptr[c]; e < T.near.ptr[c + 1]; ++e) {   // partners ascending
+      const int b = T.near.idx[e];
+      if (chunk.size() > (size_t)ptr[c] && chunk.back() == b / 2) mask.back() |= (uint8_t)(1u << (b & 1));
+      else {
+        chunk.push_back(b / 2);
+        mask.push_back((uint8_t)(1u << (b & 1)));
+      }
+    }
+  }
+  ptr[nleaf] = (int32_t)chunk.size();
+  auto up = [](const void* src, size_t bytes) {
+    void* p = nullptr;
+    H2_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
+    if (bytes) H2_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+    return p;
+  };
+  T.d_nl_ptr = static_cast<int32_t*>(up(ptr.data(), ptr.size() * 4));
+  T.d_nl_chunk = static_cast<int32_t*>(up(chunk.data(), chunk.size() * 4));
+  T.d_nl_mask = static_cast<uint8_t*>(up(mask.data(), mask.size()));
+  T.nl_state = 1;
+  return true;
 }
 
 // built-in kernel parameters on a tree: diameter (exp / Helmholtz range guards) and, for the

@@ -23,6 +23,10 @@ int env_int(const char* name, int def);
 bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
                             int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Yout,
                             int64_t ldy, cudaStream_t st);
+// the leaf subtraction on the tensor cores (near leaves only; see sketch_tc.cu)
+bool launch_near_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                           int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Y, int64_t ldy,
+                           const int32_t* nl_ptr, const int32_t* nl_chunk, const uint8_t* nl_mask, cudaStream_t st);
 // explicit dense operator on the int8 tensor cores (Omega = the h2 stream):
 // Y(rows) = A(rows, :) Omega, A row-major n x n (lda), 7-slice fixed point of scale 2^E >= amax
 double dense_absmax(const double* A, int64_t lda, int64_t n, cudaStream_t st);

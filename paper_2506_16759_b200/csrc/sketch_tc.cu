@@ -379,7 +379,9 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
                      int64_t split_stride, double hs, int wshift, uint32_t* __restrict__ ovf_flag, int pfd,
-                     uint32_t hint, const double* __restrict__ Aop, int64_t lda) {
+                     uint32_t hint, const double* __restrict__ Aop, int64_t lda,
+                     const int32_t* __restrict__ nl_ptr = nullptr, const int32_t* __restrict__ nl_chunk = nullptr,
+                     const uint8_t* __restrict__ nl_mask = nullptr) {
   using P = TcPlan<TM, NCOL, JC, NS>;
   constexpr int NSPLIT = SliceFmt<NS>::NSPLIT;
   constexpr int G = JC / 16;               // 16-j core-matrix groups per chunk
@@ -419,9 +421,16 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   // j-split boundaries in 128-j units (independent of JC), so that every pass shape splits and
   // drains at the same j and produces bit-identical sums
   const int64_t nunits = nchunks / (128 / JC);
-  const int64_t ch_b = nunits * blockIdx.y / gridDim.y * (128 / JC);
+  // near-field mode (nl_ptr != NULL, TM = 64 row tiles = leaves of exactly 64 points): the tile's
+  // j chunks are its near leaves' 128-j chunks (list nl_chunk[nl_ptr[leaf] ..]), each with a mask of
+  // the 64-j halves that belong to near leaves; the result is SUBTRACTED from Yout -- the leaf
+  // subtraction Y^loc = Y - sum_{b in N} D_{tau,b} Omega_b (Algorithm 1) on the tensor cores
+  const bool nearm = nl_ptr != nullptr;
+  const int nl0 = nearm ? nl_ptr[rtile / 64] : 0;
+  const int64_t ch_b = nearm ? 0 : nunits * blockIdx.y / gridDim.y * (128 / JC);
   const int64_t ch_e = nunits * (blockIdx.y + 1) / gridDim.y * (128 / JC);
-  const int nch = (int)(ch_e - ch_b);
+  const int nch = nearm ? nl_ptr[rtile / 64 + 1] - nl0 : (int)(ch_e - ch_b);
+  auto chunk_of = [&](int it) -> int64_t { return nearm ? (int64_t)nl_chunk[nl0 + it] : ch_b + it; };
   const bool control = (warp == NPW);
 
   if (KIND == H2_K_HELMHOLTZ && H2_TC_HTAB) fill_cs_table(tab, tid, NTH);
@@ -452,7 +461,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     // chunk it -> ring slot it % 4: B (NCOL x 64 bytes) + coordinates (2 KB) in 16 B pieces
     auto prefetch = [&](int it) {
       if (it >= nch) return;
-      const int64_t t = ch_b + it;
+      const int64_t t = chunk_of(it);
       const int slot = it & (TC_NB - 1);
 #pragma unroll
       for (int q = 0; q < BBUF / 16 / 32; ++q) {
@@ -607,6 +616,12 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
         for (int k = 0; k < RPT; ++k)
 #pragma unroll
           for (int q = 0; q < 8; ++q) xa[k][q] = xn[k][q];
+      } else if (nearm && !((nl_mask[nl0 + it] >> (jj0 >> 6)) & 1)) {
+        // this warp's 64-j half of the chunk is not a near leaf of the tile: zero slices
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) lo[k][q] = hi[k][q] = 0u;
       } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -684,7 +699,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const double t = v[c] + xb[c];
-              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? t : y[c0 + c] + t;
+              if (c0 + c < ncols) y[c0 + c] = nearm ? y[c0 + c] - t : drains == 0 ? t : y[c0 + c] + t;
             }
           }
           asm volatile("bar.sync 1, 128;\n" ::);
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const double t = v[c] + xu[row * 4 + c];
-              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? t : y[c0 + c] + t;
+              if (c0 + c < ncols) y[c0 + c] = nearm ? y[c0 + c] - t : drains == 0 ? t : y[c0 + c] + t;
             }
           }
           asm volatile("bar.sync 1, 128;\n" ::);
@@ -793,7 +808,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
           if (writer && i < row1) {
 #pragma unroll
             for (int c = 0; c < 16; ++c)
-              if (c0 + c < ncols) y[c0 + c] = drains == 0 ? v[c] : y[c0 + c] + v[c];
+              if (c0 + c < ncols) y[c0 + c] = nearm ? y[c0 + c] - v[c] : drains == 0 ? v[c] : y[c0 + c] + v[c];
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -1121,7 +1136,8 @@ namespace {
 template <int KIND, int TM, int NCOL, int JC, int NS>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf,
-               const double* Aop = nullptr, int64_t lda = 0) {
+               const double* Aop = nullptr, int64_t lda = 0, const int32_t* nl_ptr = nullptr,
+               const int32_t* nl_chunk = nullptr, const uint8_t* nl_mask = nullptr) {
   // producer warps: 16 (8 measured slower: 170 vs 163 ms at 32 columns, 180 vs 172 at 128; 32
   // would exceed 1024 threads per CTA with the control warp)
   constexpr int smem = TcPlan<TM, NCOL, JC, NS>::TOTAL;
@@ -1133,7 +1149,7 @@ void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t 
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
                                                                                     yo, ld, sstride, hs, wshift, ovf, pfd, hint,
-                                                                                    Aop, lda);
+                                                                                    Aop, lda, nl_ptr, nl_chunk, nl_mask);
 }
 
 template <int KIND, int NS>
@@ -1286,6 +1302,64 @@ bool launch_dense_sketch_tc(const KernelParams& kp, const double* X, const doubl
   cache_free(Bq, st);
   cache_free(ovf, st);
   if (part) cache_free(part, st);
+  return h_ovf == 0;
+}
+
+// Near-field product on the tensor cores (the leaf subtraction of Algorithm 1, fused with the
+// entry evaluation: SURVEY §8(a) a3+a4): Y(rows) -= sum_{b in N(leaf)} K(rows, I_b) Omega(I_b, :)
+// with the same fixed-point K and exact int8 contraction as the dense sketch, over each leaf's near
+// leaves only (nl_*: per leaf, the 128-j chunks holding its near leaves and a 2-bit mask of the
+// 64-j halves).  Requires leaves of exactly 64 points at multiples of 64 (row tiles = leaves) and a
+// 128- or 160-column pass (64-row tiles); ncols <= sketch_tc_pass_cols.  Returns false on a
+// Helmholtz scale overflow (the caller then uses the BSR path).
+bool launch_near_sketch_tc(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,
+                           int64_t row0, int64_t row1, const double* Om, int64_t ldo, int ncols, double* Y, int64_t ldy,
+                           const int32_t* nl_ptr, const int32_t* nl_chunk, const uint8_t* nl_mask, cudaStream_t st) {
+  if (row1 <= row0 || ncols <= 0) return true;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t npad = ((n + 127) / 128) * 128;
+  const bool helm = kp.kind == H2_K_HELMHOLTZ;
+  const int E = helm ? (int)std::ceil(std::log2(1.0 / kp.rmin)) + 2 : 0;
+  const double hs = helm ? std::ldexp(kp.param, -E) : 0.0;
+  const int NS = sketch_tc_slices(kp.kind);
+  const int wshift = helm ? E - (NS == 7 ? 51 : 46) - 2 : -(NS == 7 ? 52 : 47) - 2;
+  const int NCOL = ncols > 128 ? 160 : 128;
+  double4* C = static_cast<double4*>(cache_alloc(sizeof(double4) * npad, st));
+  int8_t* Bq = static_cast<int8_t*>(cache_alloc((size_t)npad * 160, st));
+  uint32_t* ovf = static_cast<uint32_t*>(cache_alloc(sizeof(uint32_t), st));
+  H2_CUDA(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), st));
+  coords_aos_kernel<<<(int)std::min<int64_t>((npad + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(
+      X, Yc, Zc, n, npad, helm ? kp.param : kp.inv, C);
+  H2_CHECK_LAUNCH();
+  const int64_t nchunks = npad / 128;
+  omega_i8_kernel<<<(int)std::min<int64_t>((nchunks * 128 * NCOL + 255) / 256, (int64_t)sms * 32), 256, 0, st>>>(
+      Om, ldo, n, ncols, NCOL, 128, nchunks, Bq);
+  H2_CHECK_LAUNCH();
+  const dim3 grid((unsigned)div_up(row1 - row0, 64), 1);
+  if (NS == 6 && NCOL == 160) {
+    tc_launch<H2_K_EXP, 64, 160, 128, 6>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
+                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  } else if (NS == 6) {
+    tc_launch<H2_K_EXP, 64, 128, 128, 6>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
+                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  } else if (helm) {
+    tc_launch<H2_K_HELMHOLTZ, 64, 128, 128, 7>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift,
+                                               ovf, nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  } else {
+    tc_launch<H2_K_EXP, 64, 128, 128, 7>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
+                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  }
+  H2_CHECK_LAUNCH();
+  uint32_t h_ovf = 0;
+  if (helm) {
+    H2_CUDA(cudaMemcpyAsync(&h_ovf, ovf, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaStreamSynchronize(st));
+  }
+  cache_free(C, st);
+  cache_free(Bq, st);
+  cache_free(ovf, st);
   return h_ovf == 0;
 }
 

@@ -531,5 +531,8 @@ h2_tree::~h2_tree() {
   cudaFree(d_D_off);
   free_csr(d_near);
   for (auto& f : d_far) free_csr(f);
+  cudaFree(d_nl_ptr);
+  cudaFree(d_nl_chunk);
+  cudaFree(d_nl_mask);
   cudaSetDevice(prev);
 }

@@ -46,6 +46,13 @@ struct h2_tree {
   bool part_uploaded = false;
   void wait_partition();
 
+  // near-field chunk lists of the tensor-core leaf subtraction (api.cpp ensure_near_chunks):
+  // per leaf, the 128-j chunks holding its near leaves + 2-bit half masks; state 0 = not built,
+  // 1 = built (leaves of exactly 64 points at multiples of 64), -1 = tree not eligible
+  int nl_state = 0;
+  int32_t *d_nl_ptr = nullptr, *d_nl_chunk = nullptr;
+  uint8_t* d_nl_mask = nullptr;
+
   // device mirrors (current device at build time)
   int device = -1;
   double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr;

@@ -16,6 +16,9 @@ CASES = {
     "cov2d_1k": (lambda: uniform_points(1024, 2, 0), "exp", 0.2, 32, 1e-6),
     # ragged leaves (39/40 points), several sketch tiles + ragged tail (5000 = 39*128 + 8)
     "cov3d_5000": (lambda: uniform_points(5000, 3, 0), "exp", 0.2, 64, 1e-6),
+    # leaves of exactly 64 points (8192 = 64 x 2^7): the leaf subtraction runs on the tensor cores
+    # from the kernel itself (launch_near_sketch_tc) instead of the BSR over the stored D blocks
+    "cov3d_8192": (lambda: uniform_points(8192, 3, 1), "exp", 0.2, 64, 1e-6),
     # volume IE on a regular grid (BASELINE configs[3] shape, 16^3), tol 1e-4
     "ie_grid16": (lambda: grid_points((16, 16, 16), 1 / 16), "helmholtz", 3.0, 64, 1e-4),
 }
@@ -207,6 +210,41 @@ def test_degenerate_inputs():
     K = kernels.kernel_block("exp", 0.2, X[T.perm], X[T.perm])
     y = H.matvec(torch.from_numpy(np.eye(500)[:, :7].copy()).cuda()).cpu().numpy()
     assert np.abs(y - K[:, :7]).max() <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["cov3d_8192"])
+def test_near_field_tensor_core_vs_bsr(case):
+    """The leaf subtraction on the tensor cores (H2_NEAR_TC, default) vs the BSR over the stored D
+    blocks: the two Y^loc differ only by the fixed-point rounding of the near-field K (<= 2^-48
+    max|K| per entry), so ranks / skeletons agree up to certified near-ties and the H^2
+    representations agree to the tolerance level (the switch is read once per process)."""
+    import subprocess, sys, os, tempfile
+    code = "\n".join([
+        "import sys, os, numpy as np, torch",
+        "sys.path.insert(0, os.environ['ROOT'])",
+        "import paper_2506_16759_b200 as g",
+        "from synth import uniform_points",
+        "T = g.Tree(uniform_points(8192, 3, 1), 64)",
+        "H = g.build(T, ('exp', 0.2), 1e-6)",
+        "out = [np.array([H.samples], float)]",
+        "out += [H.rank(t).astype(float) for t in range(H.top_depth, T.leaf_depth + 1)]",
+        "P = np.random.default_rng(3).standard_normal((T.n, 4))",
+        "out += [H.matvec(torch.from_numpy(P).cuda()).cpu().numpy().ravel()]",
+        "np.save(sys.argv[1], np.concatenate(out))"])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for val in ("0", "1"):
+        f = tempfile.mktemp(suffix=".npy")
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=dict(os.environ, ROOT=root, H2_NEAR_TC=val))
+        res.append(np.load(f))
+        os.remove(f)
+    a, b = res
+    assert a.shape == b.shape and a[0] == b[0]          # samples
+    nmv = 8192 * 4
+    ra, rb = a[1:-nmv], b[1:-nmv]
+    assert np.mean(ra != rb) <= 0.01                    # ranks: certified near-ties only
+    ya, yb = a[-nmv:], b[-nmv:]
+    assert np.linalg.norm(ya - yb) <= 2e-6 * np.linalg.norm(ya)
 
 
 def test_async_tree_build_bitwise():
