@@ -374,7 +374,7 @@ __global__ void omega_i8_kernel(const double* __restrict__ Om, int64_t ldo, int6
 // TM = 128, NCOL <= 64 : NS x NCOL TMEM columns.  TM = 64 : either the M = 64 accumulators of
 // two slices share TMEM columns in the two lane halves (tmem_slice), or (PACK) slices s and s + 3
 // form one M = 128 accumulator in all 128 lanes; one evaluation of K feeds 128 / 160 columns.
-template <int KIND, int TM, int NPW, int NCOL, int JC, int NS>
+template <int KIND, int TM, int NPW, int NCOL, int JC, int NS, bool NEARM = false>
 __global__ void __launch_bounds__(32 * (NPW + 1), 1)
     sketch_tc_kernel(const double4* __restrict__ C, int64_t n, int64_t row0, int64_t row1,
                      const int8_t* __restrict__ Bq, int64_t nchunks, int ncols, double* __restrict__ Yout, int64_t ldy,
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
   // j chunks are its near leaves' 128-j chunks (list nl_chunk[nl_ptr[leaf] ..]), each with a mask of
   // the 64-j halves that belong to near leaves; the result is SUBTRACTED from Yout -- the leaf
   // subtraction Y^loc = Y - sum_{b in N} D_{tau,b} Omega_b (Algorithm 1) on the tensor cores
-  const bool nearm = nl_ptr != nullptr;
+  constexpr bool nearm = NEARM;   // compile time: the sketch pass itself carries no near-mode code
   const int nl0 = nearm ? nl_ptr[rtile / 64] : 0;
   const int64_t ch_b = nearm ? 0 : nunits * blockIdx.y / gridDim.y * (128 / JC);
   const int64_t ch_e = nunits * (blockIdx.y + 1) / gridDim.y * (128 / JC);
@@ -1133,7 +1133,7 @@ int sketch_tc_pass_cols(int kind) {
 }
 
 namespace {
-template <int KIND, int TM, int NCOL, int JC, int NS>
+template <int KIND, int TM, int NCOL, int JC, int NS, bool NEARM = false>
 void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t row0, int64_t row1, const int8_t* Bq,
                int64_t nchunks, int nc, double* yo, int64_t ld, int64_t sstride, double hs, int wshift, uint32_t* ovf,
                const double* Aop = nullptr, int64_t lda = 0, const int32_t* nl_ptr = nullptr,
@@ -1145,9 +1145,9 @@ void tc_launch(dim3 grid, cudaStream_t st, const double4* C, int64_t n, int64_t 
   static const uint32_t hint = (uint32_t)env_int("H2_TC_HINT", 0); // mbarrier wait suspend hint (ns), 0 = none
   constexpr int NPW = 16;
   // per launch: the attribute is per device (a process may drive several GPUs)
-  H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS>,
+  H2_CUDA(cudaFuncSetAttribute(sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS, NEARM>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
+  sketch_tc_kernel<KIND, TM, NPW, NCOL, JC, NS, NEARM><<<grid, 32 * (NPW + 1), smem, st>>>(C, n, row0, row1, Bq, nchunks, nc,
                                                                                     yo, ld, sstride, hs, wshift, ovf, pfd, hint,
                                                                                     Aop, lda, nl_ptr, nl_chunk, nl_mask);
 }
@@ -1339,17 +1339,17 @@ bool launch_near_sketch_tc(const KernelParams& kp, const double* X, const double
   H2_CHECK_LAUNCH();
   const dim3 grid((unsigned)div_up(row1 - row0, 64), 1);
   if (NS == 6 && NCOL == 160) {
-    tc_launch<H2_K_EXP, 64, 160, 128, 6>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
-                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
-  } else if (NS == 6) {
-    tc_launch<H2_K_EXP, 64, 128, 128, 6>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
-                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
-  } else if (helm) {
-    tc_launch<H2_K_HELMHOLTZ, 64, 128, 128, 7>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift,
+    tc_launch<H2_K_EXP, 64, 160, 128, 6, true>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift,
                                                ovf, nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  } else if (NS == 6) {
+    tc_launch<H2_K_EXP, 64, 128, 128, 6, true>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift,
+                                               ovf, nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+  } else if (helm) {
+    tc_launch<H2_K_HELMHOLTZ, 64, 128, 128, 7, true>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs,
+                                                     wshift, ovf, nullptr, 0, nl_ptr, nl_chunk, nl_mask);
   } else {
-    tc_launch<H2_K_EXP, 64, 128, 128, 7>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift, ovf,
-                                         nullptr, 0, nl_ptr, nl_chunk, nl_mask);
+    tc_launch<H2_K_EXP, 64, 128, 128, 7, true>(grid, st, C, n, row0, row1, Bq, nchunks, ncols, Y, ldy, 0, hs, wshift,
+                                               ovf, nullptr, 0, nl_ptr, nl_chunk, nl_mask);
   }
   H2_CHECK_LAUNCH();
   uint32_t h_ovf = 0;
