@@ -492,7 +492,8 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
     else if (v2 == 5) wide ? bsr2_go<32, 3, true, 16>(a, alpha, st) : bsr2_go<32, 3, false, 16>(a, alpha, st);
     else if (v2 == 6 && a.ncols > 128) bsr2_go<160, 2, true>(a, alpha, st);   // one CTA per 160 columns
     else if (v2 == 7 && a.ncols > 64) bsr2_go<96, 2, true>(a, alpha, st);
-    else if ((v2 == 8 || v2 == 9 || v2 == 10) && a.ncols > 32) {
+    else if (v2 == 11 && a.ncols > 32) bsr2_go<64, 2, true, 16, 4>(a, alpha, st);   // no tail split
+    else if ((v2 == 8 || v2 == 9 || v2 == 10 || v2 == 12) && a.ncols > 32) {
       // 64-column CTA tiles with 32 x 32 warp tiles over the first 64-multiple of the columns, the
       // remaining (< 64) columns in 32-column tiles: no half-empty column tile at 160 columns
       const int main = a.ncols / 64 * 64;
@@ -506,7 +507,8 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
         BsrArgs t = a;
         t.c0 = a.c0 + main;
         t.ncols = a.ncols - main;
-        bsr2_go<32, 2, true>(t, alpha, st);
+        if (v2 == 12) bsr2_go<32, 2, true, 16, 4>(t, alpha, st);   // tail in 32 x 32 warp tiles too
+        else bsr2_go<32, 2, true>(t, alpha, st);
       }
     }
     else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);

@@ -379,7 +379,8 @@ def test_eager_sweep_bitwise(monkeypatch, case, opts):
                                      ("H2_BSR2", "0", "1"), ("H2_BSR2", "0", "9"), ("H2_BSR2", "1", "2"), ("H2_BSR2", "1", "3"),
                                      ("H2_BSR2", "1", "4"), ("H2_BSR2", "1", "5"),
                                      ("H2_BSR2", "1", "6"), ("H2_BSR2", "1", "7"),
-                                     ("H2_BSR2", "1", "8"), ("H2_BSR2", "1", "9")])
+                                     ("H2_BSR2", "1", "8"), ("H2_BSR2", "1", "9"),
+                                     ("H2_BSR2", "1", "11"), ("H2_BSR2", "1", "12")])
 def test_kernel_variants_bitwise(monkeypatch, env, a, b):
     """Performance variants that keep every element's operation order: the register-cached CPQR
     update (H2_CQ_REG) and the BSR tilings of wide passes (H2_BSR_VAR: 64-column tiles, 32-column
