@@ -220,8 +220,11 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
       }
       const double den = alpha - beta;
       __syncwarp();
+      // v = x / (alpha - beta): one reciprocal and d multiplications (LAPACK dlarfg scales x by
+      // 1 / (alpha - beta) the same way) instead of d FP64 divisions on warp 0's serial path
+      const double rden = 1.0 / den;
       for (int r = i + 1 + lane; r < d; r += 32) {
-        v[r] = tau != 0.0 ? Ai[r] / den : 0.0;
+        v[r] = tau != 0.0 ? Ai[r] * rden : 0.0;
         Ai[r] = 0.0;
       }
       if (lane == 0) {
@@ -841,8 +844,9 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
     }
     const double den = alpha - beta;
     __syncwarp();
+    const double rden = 1.0 / den;   // dlarfg: x scaled by 1 / (alpha - beta)
     for (int r = i + 1 + lane; r < d; r += 32) {
-      v[r] = tau != 0.0 ? Ai[r] / den : 0.0;
+      v[r] = tau != 0.0 ? Ai[r] * rden : 0.0;
       Ai[r] = 0.0;
     }
     if (lane == 0) {
