@@ -7,14 +7,16 @@ namespace h2 {
 
 // ------------------------------------------------------------------------------------------
 // batchedGen: one CTA per unique block (grid-stride).  Warp w takes rows i = w, w+8, ...; its
-// lanes the columns (coalesced row-major writes); the column coordinates of a 256-column chunk
-// are staged in shared memory, the row point is a warp-uniform load.
+// lanes the columns (coalesced row-major writes).  The coordinates of a 256-row x 256-column
+// chunk are staged in shared memory up front (row and column gathers issued together, one
+// latency per chunk instead of two dependent global loads per row).
 // ------------------------------------------------------------------------------------------
 template <int KIND>
 __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, const double* __restrict__ Yc,
                                                   const double* __restrict__ Zc, GenArgs a, double param,
                                                   double inv) {
   __shared__ double cx[256], cy[256], cz[256];
+  __shared__ double rx[256], ry[256], rz[256];
   __shared__ double tab[64];
   fill_exp_table(tab);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -25,25 +27,33 @@ __global__ void __launch_bounds__(256) gen_kernel(const double* __restrict__ X, 
     const int32_t* ri = a.idx + a.off[s];
     const int32_t* ci = a.cnt2 ? a.idx2 + a.off2[b] : a.idx + a.off[b];
     double* out = a.out + a.out_off[u];
-    for (int j0 = 0; j0 < nc; j0 += 256) {
-      const int nj = min(256, nc - j0);
-      __syncthreads();
-      if (threadIdx.x < nj) {
-        const int p = ci[j0 + threadIdx.x];
-        cx[threadIdx.x] = X[p];
-        cy[threadIdx.x] = Yc[p];
-        cz[threadIdx.x] = Zc[p];
-      }
-      __syncthreads();
-      for (int i = warp; i < m; i += 8) {
-        const int p = ri[i];
-        const double xi = X[p], yi = Yc[p], zi = Zc[p];
-        double* orow = out + (int64_t)i * nc + j0;
-        if (KIND == H2_K_RATIONAL) {   // exact-order entries (inv carries l^2)
-          for (int j = lane; j < nj; j += 32) orow[j] = k_rational(r2_exact(xi, yi, zi, cx[j], cy[j], cz[j]), inv);
-        } else {
-          for (int j = lane; j < nj; j += 32)
-            orow[j] = kernel_of_r2<KIND>(dist2(xi, yi, zi, cx[j], cy[j], cz[j]), param, inv, tab);
+    for (int i0 = 0; i0 < m; i0 += 256) {
+      const int mi = min(256, m - i0);
+      for (int j0 = 0; j0 < nc; j0 += 256) {
+        const int nj = min(256, nc - j0);
+        __syncthreads();
+        if (threadIdx.x < nj) {
+          const int p = ci[j0 + threadIdx.x];
+          cx[threadIdx.x] = X[p];
+          cy[threadIdx.x] = Yc[p];
+          cz[threadIdx.x] = Zc[p];
+        }
+        if (j0 == 0 && threadIdx.x < mi) {
+          const int p = ri[i0 + threadIdx.x];
+          rx[threadIdx.x] = X[p];
+          ry[threadIdx.x] = Yc[p];
+          rz[threadIdx.x] = Zc[p];
+        }
+        __syncthreads();
+        for (int i = warp; i < mi; i += 8) {
+          const double xi = rx[i], yi = ry[i], zi = rz[i];
+          double* orow = out + (int64_t)(i0 + i) * nc + j0;
+          if (KIND == H2_K_RATIONAL) {   // exact-order entries (inv carries l^2)
+            for (int j = lane; j < nj; j += 32) orow[j] = k_rational(r2_exact(xi, yi, zi, cx[j], cy[j], cz[j]), inv);
+          } else {
+            for (int j = lane; j < nj; j += 32)
+              orow[j] = kernel_of_r2<KIND>(dist2(xi, yi, zi, cx[j], cy[j], cz[j]), param, inv, tab);
+          }
         }
       }
     }
