@@ -78,15 +78,35 @@ __device__ __forceinline__ double k_rational(double r2, double l2) {
 // (fdlibm ln2 split; |n| < 2^17 keeps kf*hi exact), |g| <= ln2/128, e^g by the degree-5 Taylor
 // polynomial (truncation 3.5e-17 relative), 2^(j/64) from a 64-entry table `tab`, 2^(n>>6) by
 // exponent arithmetic.  Max error ~1.5 ulp.  x < -700 -> 0 (true value < 1e-304).
-__device__ __forceinline__ double exp_neg(double x, const double* __restrict__ tab) {
+// The non-short constants are passed as register values (ExpNegC) that a kernel loads ONCE from
+// shared memory (exp_neg_consts_fill / _load): as literals, the compiler rematerialises each
+// 64-bit constant with two integer MOVs (or an LDC) per evaluation, and the batchedGen loop was
+// issue-bound on them.
+struct ExpNegC {
+  double c[6];
+};
+__device__ __forceinline__ void exp_neg_consts_fill(double* sk) {
+  const double v[6] = {92.332482616893656,        // 64/ln2
+                       -0.01083042469326756,      // ln2_hi/64 (fdlibm 0x3fe62e42fee00000)
+                       -2.9815858269852933e-12,   // ln2_lo/64 (fdlibm 0x3dea39ef35793c76)
+                       1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+  if (threadIdx.x < 6) sk[threadIdx.x] = v[threadIdx.x];
+}
+__device__ __forceinline__ ExpNegC exp_neg_consts_load(const double* sk) {
+  ExpNegC k;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) k.c[i] = sk[i];
+  return k;
+}
+__device__ __forceinline__ double exp_neg(double x, const double* __restrict__ tab, const ExpNegC& k) {
   const double SH = 6755399441055744.0;                 // 1.5 * 2^52
-  double t = fma(x, 92.332482616893656, SH);            // 64/ln2
+  double t = fma(x, k.c[0], SH);
   double kf = t - SH;
   int n = __double2loint(t);
-  double g = fma(kf, -0.01083042469326756, x);          // ln2_hi/64 (fdlibm 0x3fe62e42fee00000)
-  g = fma(kf, -2.9815858269852933e-12, g);              // ln2_lo/64 (fdlibm 0x3dea39ef35793c76)
-  double p = fma(g, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(p, g, 1.0 / 6.0);
+  double g = fma(kf, k.c[1], x);
+  g = fma(kf, k.c[2], g);
+  double p = fma(g, k.c[3], k.c[4]);
+  p = fma(p, g, k.c[5]);
   p = fma(p, g, 0.5);
   p = fma(p, g, 1.0);
   p = fma(p, g, 1.0);
@@ -152,10 +172,11 @@ __device__ __forceinline__ void fill_exp_table(double* tab) {
 }
 
 template <int KIND>
-__device__ __forceinline__ double kernel_of_r2(double r2, double param, double inv, const double* tab) {
+__device__ __forceinline__ double kernel_of_r2(double r2, double param, double inv, const double* tab,
+                                               const ExpNegC& ek) {
   if (KIND == H2_K_EXP) {
     // exp(-|x-y|/l)  (PAPER.md Eq. cov)
-    return exp_neg(-sqrt(r2) * inv, tab);
+    return exp_neg(-sqrt(r2) * inv, tab, ek);
   } else {
     double r = sqrt(r2);
     return r2 > 0.0 ? cos(param * r) / r : 0.0;
