@@ -733,15 +733,19 @@ static void cpqr_launch_e(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   cpqr_kernel<SMEM, NT, E, HYB><<<a.nclusters, NT, sm, st>>>(a);
 }
 
-// register-cached variant when every thread's entries fit E (d <= 8 E): opt-in (H2_CQ_REG=1);
-// measured slower at C2 (33.5 vs 30.4 ms: 128 registers x 512 threads leave one CTA per SM on
-// the global-panel levels, which ran two)
+// register-cached variant when every thread's entries fit E (d <= 8 E): on every level
+// (H2_CQ_REG=1) measured slower at C2 (33.5 vs 30.4 ms: 128 registers x 512 threads leave one
+// CTA per SM on the global-panel levels, which ran two); on the levels with at most one panel
+// per SM only (default) slightly faster
 template <bool SMEM, int NT>
 static void cpqr_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
   // H2_CQ_REG: 0 off, 1 every block panel, 2 shared-memory panels only (one CTA per SM there
   // anyway, so the 128 registers cost no occupancy)
-  const int regm = env_int("H2_CQ_REG", 0);
-  const bool reg = regm == 1 || (regm == 2 && SMEM);
+  // 3: global-panel levels with at most one panel per SM (the L2-latency-bound upper levels:
+  // all E row loads of a pass in flight at once); 4: 2 + 3
+  const int regm = env_int("H2_CQ_REG", 3);   // default 3: 29.4 vs 30.0 ms at C2 (bitwise)
+  const bool few = !SMEM && a.nclusters <= 148;
+  const bool reg = regm == 1 || (regm == 2 && SMEM) || (regm == 3 && few) || (regm == 4 && (SMEM || few));
   const int need = (a.d + CQ_TPR - 1) / CQ_TPR;
   if (reg && need <= 8) cpqr_launch_e<SMEM, NT, 8>(a, sm, st);
   else if (reg && need <= 16) cpqr_launch_e<SMEM, NT, 16>(a, sm, st);

@@ -375,7 +375,7 @@ def test_eager_sweep_bitwise(monkeypatch, case, opts):
     assert np.array_equal(H0._export(g._lib.H2_X_D), H1._export(g._lib.H2_X_D))
 
 
-@pytest.mark.parametrize("env,a,b", [("H2_CQ_REG", "0", "1"), ("H2_BSR_VAR", "0", "3"), ("H2_BSR_VAR", "0", "1"),
+@pytest.mark.parametrize("env,a,b", [("H2_CQ_REG", "0", "1"), ("H2_CQ_REG", "0", "3"), ("H2_BSR_VAR", "0", "3"), ("H2_BSR_VAR", "0", "1"),
                                      ("H2_BSR2", "0", "1"), ("H2_BSR2", "0", "9"), ("H2_BSR2", "1", "2"), ("H2_BSR2", "1", "3"),
                                      ("H2_BSR2", "1", "4"), ("H2_BSR2", "1", "5"),
                                      ("H2_BSR2", "1", "6"), ("H2_BSR2", "1", "7"),
