@@ -261,7 +261,21 @@ typedef struct {
    * start vector is column 0 of the h2_omega stream (seed, stream_id + 3)); the estimate is
    * reported in h2_build_stats.norm_est.                                                  [10]  */
   int32_t norm_iters;
+  /* Work split of an H2_S_CALLBACK sketch under a communicator (BASELINE north
+   * star "splitting the sketch's sample columns ... over GPUs"):
+   *   H2_SPLIT_ROWS: every rank's callback computes its own leaf rows for all ncols columns
+   *                  (row_begin/row_end = the rank's rows): no communication;
+   *   H2_SPLIT_COLS: an opaque operator that can only produce whole columns (e.g. a black-box
+   *                  matvec): rank g's callback computes ALL n rows of the column slice
+   *                  [col0 + c_g, col0 + c_{g+1}), c_g = floor(g ncols / P), into a scratch panel,
+   *                  and one all-to-all (comm->alltoallv, or grouped ncclSend/ncclRecv of the
+   *                  in-library communicator) turns the column shards into row shards: rank g
+   *                  sends rows [row_b(h), row_e(h)) of its slice to rank h and receives its own
+   *                  rows of every other slice (n ncols 8 (P-1)/P bytes per draw in total).
+   * Ignored on one GPU and for the built-in operators (which shard rows with no exchange). [ROWS] */
+  int32_t sketch_split;
 } h2_build_opts;
+enum { H2_SPLIT_ROWS = 0, H2_SPLIT_COLS = 1 };
 void h2_build_opts_default(h2_build_opts* opts);
 
 enum {
@@ -325,6 +339,13 @@ enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4, H2_CQ_V_EXACT = 8
  * ------------------------------------------------------------------------------------- */
 typedef int (*h2_allgatherv_fn)(void* ctx, void* buf, const int64_t* counts, const int64_t* displs,
                                 void* stream);
+/* alltoallv(ctx, send, scounts, sdispls, recv, rcounts, rdispls, stream): send and recv are
+ * distinct device buffers; byte segment [sdispls[r], sdispls[r] + scounts[r]) of send goes to
+ * rank r, which receives it at [rdispls[me], rdispls[me] + rcounts[me]) of its recv (so
+ * rcounts[r] on rank me == scounts[me] on rank r).  Host arrays of nranks entries; stream-ordered
+ * on `stream`.  Used by sketch_split = H2_SPLIT_COLS only; may be NULL otherwise. */
+typedef int (*h2_alltoallv_fn)(void* ctx, const void* send, const int64_t* scounts, const int64_t* sdispls,
+                               void* recv, const int64_t* rcounts, const int64_t* rdispls, void* stream);
 typedef struct {
   int32_t rank, nranks;
   h2_allgatherv_fn allgatherv;   /* caller's communicator (e.g. torch.distributed), or NULL      */
@@ -332,6 +353,8 @@ typedef struct {
   void* nccl;                    /* library-owned NCCL communicator (h2_comm_init), used when
                                     allgatherv is NULL: grouped ncclBroadcast per segment,
                                     stream-ordered, no host synchronisation                    */
+  h2_alltoallv_fn alltoallv;     /* caller's all-to-all (same ctx), or NULL: the NCCL
+                                    communicator's grouped ncclSend / ncclRecv                  */
 } h2_comm;
 
 /* In-library NCCL communicator (one process per GPU; the NCCL library is loaded at run time,
@@ -349,6 +372,12 @@ void h2_comm_free(h2_comm* comm);
  * Uses comm->allgatherv when set, else the NCCL communicator. */
 h2_status h2_comm_allgatherv(const h2_comm* comm, void* buf, const int64_t* counts, const int64_t* displs,
                              void* stream);
+/* The exchange of the column-split sketch (sketch_split = H2_SPLIT_COLS; exposed for tests and
+ * users): all-to-all of byte segments as h2_alltoallv_fn above.  Uses comm->alltoallv when set,
+ * else the NCCL communicator (one group of ncclSend / ncclRecv; the own segment is a device
+ * copy).  Errors: INVALID_ARG (no all-to-all available, negative segments), NCCL, CALLBACK. */
+h2_status h2_comm_alltoallv(const h2_comm* comm, const void* send, const int64_t* scounts, const int64_t* sdispls,
+                            void* recv, const int64_t* rcounts, const int64_t* rdispls, void* stream);
 
 /* Owned cluster range [*begin, *end) of `rank` among `nranks` at a depth with n_clusters
  * clusters (host logic, no device).  Errors: INVALID_ARG. */

@@ -17,6 +17,7 @@ H2_K_EXP, H2_K_HELMHOLTZ, H2_K_RATIONAL = 0, 1, 2
 H2_S_DENSE_KERNEL, H2_S_CALLBACK, H2_S_H2_LOWRANK, H2_S_DENSE_MATRIX = 0, 1, 2, 3
 H2_E_BUILTIN, H2_E_CALLBACK, H2_E_H2_LOWRANK, H2_E_DENSE_MATRIX = 0, 1, 2, 3
 H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
+H2_SPLIT_ROWS, H2_SPLIT_COLS = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C = range(10)
 H2_SKETCH_OMEGA_QUARTERS = 1
 H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL, H2_CQ_V_EXACT = 1, 2, 4, 8
@@ -77,7 +78,7 @@ class h2_build_opts(C.Structure):
                 ("max_rank", C.c_int32), ("seed", C.c_uint64), ("stream_id", C.c_uint32),
                 ("verify_probes", C.c_int32), ("verify_retries", C.c_int32), ("eps_decay", C.c_double),
                 ("exact_order", C.c_int32), ("omega_ext", C.c_void_p), ("ld_omega_ext", C.c_int64),
-                ("norm_iters", C.c_int32)]
+                ("norm_iters", C.c_int32), ("sketch_split", C.c_int32)]
 
 
 class h2_build_stats(C.Structure):
@@ -94,11 +95,13 @@ class h2_build_stats(C.Structure):
 
 
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p)
 
 
 class h2_comm(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("allgatherv", ALLGATHERV_FN), ("ctx", C.c_void_p),
-                ("nccl", C.c_void_p)]
+                ("nccl", C.c_void_p), ("alltoallv", ALLTOALLV_FN)]
 
 
 # every symbol include/h2.h declares, with its ctypes signature
@@ -127,6 +130,8 @@ SIGNATURES = {
     "h2_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.POINTER(h2_comm))]),
     "h2_comm_free": (None, [C.POINTER(h2_comm)]),
     "h2_comm_allgatherv": (C.c_int, [C.POINTER(h2_comm), _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P]),
+    "h2_comm_alltoallv": (C.c_int, [C.POINTER(h2_comm), _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P,
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P]),
     "h2_dist_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "h2_matvec": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P]),
     "h2_dense_sketch": (C.c_int, [_P, h2_kernel, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64,

@@ -254,6 +254,21 @@ void comm_allgather(const h2_comm* comm, void* base, const std::vector<int64_t>&
   if (rc != 0) throw Error(H2_ERR_CALLBACK, "communicator allgatherv returned " + std::to_string(rc));
 }
 
+// all-to-all of byte segments (the column-split sketch exchange, S§8(e)): the caller's
+// alltoallv (host-staged: the send segments are completed first) or the in-library NCCL group
+void comm_alltoall(const h2_comm* comm, const void* send, const std::vector<int64_t>& sc,
+                   const std::vector<int64_t>& sd, void* recv, const std::vector<int64_t>& rc,
+                   const std::vector<int64_t>& rd, cudaStream_t st) {
+  if (comm->alltoallv) {
+    H2_CUDA(cudaStreamSynchronize(st));
+    const int r = comm->alltoallv(comm->ctx, send, sc.data(), sd.data(), recv, rc.data(), rd.data(), st);
+    if (r != 0) throw Error(H2_ERR_CALLBACK, "communicator alltoallv returned " + std::to_string(r));
+    return;
+  }
+  H2_REQUIRE(comm->nccl, "column-split sketch: the communicator has no all-to-all (alltoallv or NCCL)");
+  nccl_alltoallv(comm->nccl, comm->rank, comm->nranks, send, sc.data(), sd.data(), recv, rc.data(), rd.data(), st);
+}
+
 // all-gather of a per-cluster array of depth t: element offsets off(c), c in [0, 2^t]
 template <class F>
 void comm_allgather_clusters(const h2_comm* comm, void* base, size_t es, int t, F off, cudaStream_t st) {
@@ -496,6 +511,69 @@ struct Builder {
     sketch_columns += nc;
   }
 
+  // H2_S_CALLBACK sketch of stream columns [c0, c0+nc) (Od/Yd at the draw's first column):
+  // this rank's leaf rows of Y.  Row split (default): one call for the rank's rows.  Column split
+  // (opts.sketch_split = H2_SPLIT_COLS under a communicator, S§8(e)): the callback produces ALL n
+  // rows of this rank's column slice [c_R, c_{R+1}), c_r = floor(r nc / P), into a packed n x w
+  // panel whose rows of rank h are one contiguous segment; one all-to-all moves segment h to rank
+  // h, which receives its rows of every slice (packed per source rank) and scatters them into Yd.
+  int64_t a2a_bytes = 0;
+  void callback_sketch(const double* Od, int64_t ld, int c0, int nc, double* Yd) {
+    h2_sketch_req rq{};
+    rq.n = T.n;
+    rq.omega = Od;
+    rq.ld_omega = ld;
+    rq.stream = st;
+    if (!comm || o.sketch_split != H2_SPLIT_COLS) {
+      rq.row_begin = row_b();
+      rq.row_end = row_e();
+      rq.col0 = c0;
+      rq.ncols = nc;
+      rq.y = Yd + row_b() * ld;
+      rq.ld_y = ld;
+      const int rc = S.fn(S.ctx, &rq);
+      if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+      return;
+    }
+    std::vector<int> cs(P + 1);
+    std::vector<int64_t> rb(P + 1);
+    for (int r = 0; r <= P; ++r) {
+      cs[r] = (int)((int64_t)r * nc / P);
+      rb[r] = leaf_row(own_begin(T.Dl, r, P));
+    }
+    const int w = cs[R + 1] - cs[R];
+    const int64_t mine = rb[R + 1] - rb[R];
+    DArr<double> sb, rbuf;
+    sb.alloc(std::max<int64_t>(T.n * w, 1), st);
+    rbuf.alloc(std::max<int64_t>(mine * nc, 1), st);
+    if (w > 0) {
+      rq.row_begin = 0;
+      rq.row_end = T.n;
+      rq.col0 = c0 + cs[R];
+      rq.ncols = w;
+      rq.omega = Od + cs[R];
+      rq.y = sb.p;
+      rq.ld_y = w;
+      const int rc = S.fn(S.ctx, &rq);
+      if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+    }
+    std::vector<int64_t> sc(P), sd(P), rc(P), rd(P);
+    for (int h = 0; h < P; ++h) {
+      sd[h] = rb[h] * w * 8;
+      sc[h] = (rb[h + 1] - rb[h]) * w * 8;
+      rd[h] = mine * cs[h] * 8;
+      rc[h] = mine * (cs[h + 1] - cs[h]) * 8;
+      if (h != R) a2a_bytes += sc[h];
+    }
+    comm_alltoall(comm, sb.p, sc, sd, rbuf.p, rc, rd, st);
+    for (int h = 0; h < P; ++h) {
+      const int wh = cs[h + 1] - cs[h];
+      if (wh > 0 && mine > 0)
+        H2_CUDA(cudaMemcpy2DAsync(Yd + rb[R] * ld + cs[h], ld * 8, rbuf.p + mine * cs[h], (size_t)wh * 8,
+                                  (size_t)wh * 8, mine, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+
   // ---------------------------------------------------------------- sketch of stream columns
   // Omega(:, c0:c0+nc) -> Od, Y = K_blk(Omega) -> Yd (pointers at the first destination column)
   void draw(double* Yd, double* Od, int64_t ld, int c0, int nc) {
@@ -544,19 +622,7 @@ struct Builder {
         scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
         launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
       } else {
-        h2_sketch_req rq{};
-        rq.n = T.n;
-        rq.row_begin = row_b();
-        rq.row_end = row_e();
-        rq.col0 = c0;
-        rq.ncols = nc;
-        rq.omega = Od;
-        rq.ld_omega = ld;
-        rq.y = Yd + row_b() * ld;
-        rq.ld_y = ld;
-        rq.stream = st;
-        int rc = S.fn(S.ctx, &rq);
-        if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+        callback_sketch(Od, ld, c0, nc, Yd);
       }
     }
     timer.end();
@@ -1113,19 +1179,7 @@ struct Builder {
         scr.alloc((int64_t)(div_up(T.n, 1024) + 1) * S.rank * nc, st);
         launch_lowrank_sketch(S.U, S.ld_U, S.rank, Od, ld, nc, T.n, Yd, ld, scr.p, st);
       } else {
-        h2_sketch_req rq{};
-        rq.n = T.n;
-        rq.row_begin = row_b();
-        rq.row_end = row_e();
-        rq.col0 = c0;
-        rq.ncols = nc;
-        rq.omega = Od;
-        rq.ld_omega = ld;
-        rq.y = Yd + row_b() * ld;
-        rq.ld_y = ld;
-        rq.stream = st;
-        int rc = S.fn(S.ctx, &rq);
-        if (rc != 0) throw Error(H2_ERR_CALLBACK, "sketch callback returned " + std::to_string(rc));
+        callback_sketch(Od, ld, c0, nc, Yd);
       }
     }
     timer.end();
@@ -2203,6 +2257,7 @@ void h2_build_opts_default(h2_build_opts* o) {
   o->omega_ext = nullptr;
   o->ld_omega_ext = 0;
   o->norm_iters = 10;
+  o->sketch_split = H2_SPLIT_ROWS;
 }
 
 h2_status h2_dist_range(int64_t n_clusters, int32_t rank, int32_t nranks, int64_t* begin, int64_t* end) {
@@ -2382,6 +2437,10 @@ static h2_status build_impl(const h2_tree* tree, const h2_sketch* sketch, const 
       H2_REQUIRE(comm->nranks >= 1 && comm->rank >= 0 && comm->rank < comm->nranks &&
                      (!dist || comm->allgatherv || comm->nccl),
                  "h2_build_dist: bad communicator");
+    H2_REQUIRE(o.sketch_split == H2_SPLIT_ROWS || o.sketch_split == H2_SPLIT_COLS, "h2_build: bad sketch_split");
+    H2_REQUIRE(!dist || o.sketch_split != H2_SPLIT_COLS || sketch->kind != H2_S_CALLBACK || comm->alltoallv ||
+                   comm->nccl,
+               "h2_build_dist: sketch_split = H2_SPLIT_COLS needs an all-to-all (comm->alltoallv or NCCL)");
     // H2 + low-rank operators under a communicator: the base must be complete on every rank
     // (checked above: not partial); its matvec is row-sharded, its entries extracted per owned pair
     // subtree-aligned ownership at every processed depth: a power-of-two rank count with at
@@ -2673,6 +2732,7 @@ h2_status h2_comm_init(const void* id128, int32_t rank, int32_t nranks, h2_comm*
     c->rank = rank;
     c->nranks = nranks;
     c->allgatherv = nullptr;
+    c->alltoallv = nullptr;
     c->ctx = nullptr;
     try {
       c->nccl = h2::nccl_comm_init(id128, rank, nranks);
@@ -2704,6 +2764,25 @@ h2_status h2_comm_allgatherv(const h2_comm* comm, void* buf, const int64_t* coun
     std::vector<int64_t> c(counts, counts + comm->nranks), d(displs, displs + comm->nranks);
     for (int r = 0; r < comm->nranks; ++r) H2_REQUIRE(c[r] >= 0 && d[r] >= 0, "h2_comm_allgatherv: negative segment");
     comm_allgather(comm, buf, c, d, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_comm_alltoallv(const h2_comm* comm, const void* send, const int64_t* scounts, const int64_t* sdispls,
+                            void* recv, const int64_t* rcounts, const int64_t* rdispls, void* stream) {
+  try {
+    H2_REQUIRE(comm && scounts && sdispls && rcounts && rdispls && comm->nranks >= 1 &&
+                   comm->rank >= 0 && comm->rank < comm->nranks,
+               "h2_comm_alltoallv: bad argument");
+    const int P = comm->nranks;
+    std::vector<int64_t> sc(scounts, scounts + P), sd(sdispls, sdispls + P), rc(rcounts, rcounts + P),
+        rd(rdispls, rdispls + P);
+    for (int r = 0; r < P; ++r)
+      H2_REQUIRE(sc[r] >= 0 && sd[r] >= 0 && rc[r] >= 0 && rd[r] >= 0, "h2_comm_alltoallv: negative segment");
+    H2_REQUIRE(sc[comm->rank] == rc[comm->rank], "h2_comm_alltoallv: own send and receive segments differ");
+    comm_alltoall(comm, send, sc, sd, recv, rc, rd, (cudaStream_t)stream);
     return H2_OK;
   } catch (const Error& e) {
     return fail(e);

@@ -23,6 +23,8 @@ struct Nccl {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
@@ -46,10 +48,12 @@ Nccl& nccl() {
     N.commInitRank = reinterpret_cast<decltype(N.commInitRank)>(sym("ncclCommInitRank"));
     N.commDestroy = reinterpret_cast<decltype(N.commDestroy)>(sym("ncclCommDestroy"));
     N.broadcast = reinterpret_cast<decltype(N.broadcast)>(sym("ncclBroadcast"));
+    N.send = reinterpret_cast<decltype(N.send)>(sym("ncclSend"));
+    N.recv = reinterpret_cast<decltype(N.recv)>(sym("ncclRecv"));
     N.groupStart = reinterpret_cast<decltype(N.groupStart)>(sym("ncclGroupStart"));
     N.groupEnd = reinterpret_cast<decltype(N.groupEnd)>(sym("ncclGroupEnd"));
     N.errorString = reinterpret_cast<decltype(N.errorString)>(sym("ncclGetErrorString"));
-    if (!N.getUniqueId || !N.commInitRank || !N.commDestroy || !N.broadcast || !N.groupStart || !N.groupEnd)
+    if (!N.getUniqueId || !N.commInitRank || !N.commDestroy || !N.broadcast || !N.send || !N.recv || !N.groupStart || !N.groupEnd)
       N.why = "libnccl.so.2 lacks a required symbol";
   });
   if (!N.why.empty()) throw Error(H2_ERR_NCCL, N.why);
@@ -92,6 +96,26 @@ void nccl_allgatherv(void* c, int nranks, void* buf, const int64_t* counts, cons
     if (counts[r] > 0)
       check(N.broadcast(b + displs[r], b + displs[r], (size_t)counts[r], ncclInt8, r, static_cast<ncclComm_t>(c), st),
             "ncclBroadcast");
+  check(N.groupEnd(), "ncclGroupEnd");
+}
+
+// all-to-all of byte segments (the column-split sketch exchange, S§8(e)): one NCCL group of
+// point-to-point sends / receives to and from every other rank; the own segment is a device copy
+void nccl_alltoallv(void* c, int rank, int nranks, const void* send, const int64_t* scounts, const int64_t* sdispls,
+                    void* recv, const int64_t* rcounts, const int64_t* rdispls, cudaStream_t st) {
+  Nccl& N = nccl();
+  const char* sb = static_cast<const char*>(send);
+  char* rb = static_cast<char*>(recv);
+  if (scounts[rank] > 0)
+    H2_CUDA(cudaMemcpyAsync(rb + rdispls[rank], sb + sdispls[rank], (size_t)scounts[rank], cudaMemcpyDeviceToDevice, st));
+  check(N.groupStart(), "ncclGroupStart");
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) continue;
+    if (scounts[r] > 0)
+      check(N.send(sb + sdispls[r], (size_t)scounts[r], ncclInt8, r, static_cast<ncclComm_t>(c), st), "ncclSend");
+    if (rcounts[r] > 0)
+      check(N.recv(rb + rdispls[r], (size_t)rcounts[r], ncclInt8, r, static_cast<ncclComm_t>(c), st), "ncclRecv");
+  }
   check(N.groupEnd(), "ncclGroupEnd");
 }
 

@@ -8,8 +8,9 @@ Arithmetic stays in libh2; this module only partitions rows and moves bytes.
 
 ``Comm`` is the communicator of the sharded construction (h2_build_dist, include/h2.h; S§8(e)):
 libh2 calls its in-place ``allgatherv`` on device buffers once per level (ranks, skeleton
-indices I~, the next level's Omega rows) and torch.distributed moves the bytes: NCCL over
-NVLink on GPU tensors, or gloo through host staging (multi-process tests on one GPU / CPU).
+indices I~, the next level's Omega rows), and its ``alltoallv`` once per draw of a column-split
+callback sketch (sketch_split="cols"), and torch.distributed moves the bytes: NCCL over NVLink
+on GPU tensors, or gloo through host staging (multi-process tests on one GPU / CPU).
 """
 import ctypes as C
 import os
@@ -109,6 +110,31 @@ def allgatherv_(buf: torch.Tensor, counts, displs, group=None):
                 seg.copy_(host)
 
 
+def alltoallv_(send: torch.Tensor, scounts, sdispls, recv: torch.Tensor, rcounts, rdispls, group=None):
+    """All-to-all of byte segments of 1-D uint8 tensors (the column-split sketch exchange,
+    include/h2.h h2_alltoallv_fn): send[sdispls[r] : sdispls[r] + scounts[r]] goes to rank r and
+    arrives at recv[rdispls[me] : rdispls[me] + rcounts[me]] there.  The segments are packed in rank
+    order into a staging tensor and moved by one ``all_to_all_single`` with split sizes (NCCL on
+    device tensors; gloo on host copies), then copied out."""
+    me = dist.get_rank(group)
+    P = len(scounts)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = send.device
+    stage_dev = dev if (nccl or not send.is_cuda) else torch.device("cpu")
+    packed = [send[d:d + c] for c, d in zip(scounts, sdispls)]
+    sbuf = torch.cat(packed).to(stage_dev) if sum(scounts) else torch.empty(0, dtype=torch.uint8, device=stage_dev)
+    rbuf = torch.empty(sum(rcounts), dtype=torch.uint8, device=stage_dev)
+    dist.all_to_all_single(rbuf, sbuf, output_split_sizes=list(rcounts), input_split_sizes=list(scounts),
+                           group=group)
+    o = 0
+    for r in range(P):
+        c = rcounts[r]
+        if c:
+            recv[rdispls[r]:rdispls[r] + c].copy_(rbuf[o:o + c])
+        o += c
+    return me
+
+
 class Comm:
     """h2_comm over a torch.distributed process group (one process per GPU)."""
 
@@ -139,8 +165,29 @@ class Comm:
                 import traceback
                 traceback.print_exc()
                 return 1
+        def _a2a(ctx, send, scounts, sdispls, recv, rcounts, rdispls, stream):
+            try:
+                P = self.world
+                sc = [int(scounts[i]) for i in range(P)]
+                sd = [int(sdispls[i]) for i in range(P)]
+                rc = [int(rcounts[i]) for i in range(P)]
+                rd = [int(rdispls[i]) for i in range(P)]
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+                    sv = device_view(send, (max(d + c for c, d in zip(sc, sd)),), (1,), dtype=torch.uint8)
+                    rv = device_view(recv, (max(d + c for c, d in zip(rc, rd)),), (1,), dtype=torch.uint8)
+                    alltoallv_(sv, sc, sd, rv, rc, rd, self.group)
+                self.a2a_calls += 1
+                self.a2a_bytes += sum(sc) - sc[self.rank]
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+        self.a2a_calls = 0
+        self.a2a_bytes = 0
         self._cb = L.ALLGATHERV_FN(_agv)
-        self.struct = L.h2_comm(self.rank, self.world, self._cb, None)
+        self._cb2 = L.ALLTOALLV_FN(_a2a)
+        self.struct = L.h2_comm(self.rank, self.world, self._cb, None, None, self._cb2)
 
 
 class NcclComm:
@@ -175,6 +222,17 @@ class NcclComm:
         dsp = (C.c_int64 * P)(*displs)
         s = (stream or torch.cuda.current_stream()).cuda_stream
         self._L.check(self._L.lib.h2_comm_allgatherv(self._p, C.c_void_p(buf.data_ptr()), cnt, dsp, C.c_void_p(s)))
+
+    def alltoallv(self, send, scounts, sdispls, recv, rcounts, rdispls, stream=None):
+        """All-to-all of byte segments between CUDA tensors (h2_comm_alltoallv: grouped
+        ncclSend / ncclRecv inside libh2)."""
+        import torch
+        P = self.world
+        arr = lambda v: (C.c_int64 * P)(*v)
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        self._L.check(self._L.lib.h2_comm_alltoallv(self._p, C.c_void_p(send.data_ptr()), arr(scounts), arr(sdispls),
+                                                    C.c_void_p(recv.data_ptr()), arr(rcounts), arr(rdispls),
+                                                    C.c_void_p(s)))
 
     def close(self):
         if getattr(self, "_p", None):

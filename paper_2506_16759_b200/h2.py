@@ -156,6 +156,8 @@ def build_opts(**kw):
             continue
         if k == "tol_rule":
             v = {"rms": L.H2_TOL_RMS, "literal": L.H2_TOL_LITERAL}[v] if isinstance(v, str) else v
+        if k == "sketch_split":
+            v = {"rows": L.H2_SPLIT_ROWS, "cols": L.H2_SPLIT_COLS}[v] if isinstance(v, str) else v
         if k == "adaptive":
             v = int(bool(v))
         if not hasattr(o, k) and k not in names:
@@ -342,7 +344,9 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     omega: optional (n, >= d_max) float64 CUDA tensor, tree-order rows: an external Omega
     (h2_build_opts.omega_ext) instead of the h2_omega stream.
     opts: h2_build_opts fields (d_init, d_blk, d_max, adaptive, tol_rule,
-    tol_safety, p_os, norm, max_rank, seed, stream_id, exact_order, norm_iters, eps_decay)."""
+    tol_safety, p_os, norm, max_rank, seed, stream_id, exact_order, norm_iters, eps_decay,
+    sketch_split: "rows" | "cols" -- with comm and a ``sketch`` callable, "cols" calls it on this
+    rank's slice of the sample columns for ALL rows and all-to-alls the slices into row shards)."""
     o = build_opts(**opts)
     kern = _kernel(*kernel)
     keep = []

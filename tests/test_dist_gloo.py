@@ -141,3 +141,77 @@ def test_owned_ranges_partition_and_subtrees(world):
                     cb, ce = mod.owned_range(2 * n, r, world)
                     assert cb <= 2 * c and 2 * c + 1 < ce
         assert prev == n
+
+
+def _a2a_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mod = _load_dist()
+        # (1) the primitive: uneven, empty and gapped segments; bytes outside them untouched
+        sc = [(3 * rank + 2 * r) % 5 for r in range(world)]          # rank -> r
+        sd, o = [], 1
+        for c in sc:
+            sd.append(o)
+            o += c + 2                                                  # gaps of 2
+        send = torch.full((o + 3,), 200, dtype=torch.uint8)
+        for r in range(world):
+            send[sd[r]:sd[r] + sc[r]] = 10 * rank + r
+        rc = [(3 * r + 2 * rank) % 5 for r in range(world)]            # what rank r sends me
+        rd, o = [], 4
+        for c in rc:
+            rd.append(o)
+            o += c + 1
+        recv = torch.full((o + 2,), 255, dtype=torch.uint8)
+        mod.alltoallv_(send, sc, sd, recv, rc, rd)
+        # (2) the column-split sketch exchange of libh2 (Builder::callback_sketch): rank g computes
+        # all n rows of its column slice, segment h = rows of rank h; receives its rows of every slice
+        n, nc = 37, 11
+        K = torch.from_numpy(np.random.default_rng(0).standard_normal((n, n)))
+        om = torch.from_numpy(np.random.default_rng(1).standard_normal((n, nc)))
+        cs = [r * nc // world for r in range(world + 1)]
+        rb = mod.row_bounds(n, world)
+        w, mine = cs[rank + 1] - cs[rank], rb[rank + 1] - rb[rank]
+        part = (K @ om[:, cs[rank]:cs[rank + 1]]).contiguous()          # n x w
+        sbytes = part.view(torch.uint8).reshape(-1)
+        ssc = [(rb[h + 1] - rb[h]) * w * 8 for h in range(world)]
+        ssd = [rb[h] * w * 8 for h in range(world)]
+        rrc = [mine * (cs[h + 1] - cs[h]) * 8 for h in range(world)]
+        rrd = [mine * cs[h] * 8 for h in range(world)]
+        rbuf = torch.zeros(max(mine * nc, 1), dtype=torch.float64)
+        mod.alltoallv_(sbytes, ssc, ssd, rbuf.view(torch.uint8), rrc, rrd)
+        y = torch.empty(mine, nc, dtype=torch.float64)
+        for h in range(world):
+            wh = cs[h + 1] - cs[h]
+            y[:, cs[h]:cs[h + 1]] = rbuf[mine * cs[h]:mine * cs[h] + mine * wh].reshape(mine, wh)
+        ok = bool(torch.allclose(y, (K @ om)[rb[rank]:rb[rank + 1]], rtol=0, atol=1e-12))
+        out_q.put((rank, recv.tolist(), rc, rd, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_alltoallv_gloo_and_column_split(world):
+    """The all-to-all libh2 calls for a column-split callback sketch (h2_comm.alltoallv, S§8(e)
+    "splitting the sketch's sample columns"): byte segments with gaps / empty ones arrive at the
+    receiver's displacements and nothing else is written; and the column-shard -> row-shard
+    exchange of Builder::callback_sketch reassembles Y(own rows, all columns) = (K Omega)(rows)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r[1:] for r in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for me in range(world):
+        recv, rc, rd, ok = res[me]
+        assert ok
+        want = [255] * len(recv)
+        for r in range(world):
+            for i in range(rc[r]):
+                want[rd[r] + i] = 10 * r + me
+        assert recv == want

@@ -57,7 +57,15 @@ def _worker(rank, world, port, case, q):
         if exact:   # exact-order kernels under sharding (rational test kernel)
             opts["exact_order"] = 1
             kern = ("rational", 0.3)
-        if mode is not None:
+        if mode == "cols":
+            # S§8(e) column split of an opaque callback sketch: each rank's callback computes ALL rows
+            # of its slice of the sample columns, one all-to-all turns the slices into row shards
+            def sk(om, y, col0, r0, r1):
+                assert (r0, r1) == (0, T.n)
+                g.dense_sketch(T, om, kern, r0, r1, out=y, omega_quarters=True)
+            opts["sketch"] = sk
+            opts["sketch_split"] = "cols"
+        elif mode is not None:
             # H^2 + low-rank operators under sharding (S§8(e) "Config 5's H^2 sketch is a distributed
             # h2_matvec"): the base is complete on every rank (built here per rank), its matvec
             # row-sharded, its entries extracted per owned pair
@@ -77,6 +85,8 @@ def _worker(rank, world, port, case, q):
         H1 = g.build(T, kern, 1e-6, **opts)
         a, b = _snapshot(Hd, g), _snapshot(H1, g)
         same = {str(k): bool(np.array_equal(a[k], b[k])) for k in b}
+        if mode == "cols":
+            same["a2a_used"] = comm.a2a_calls > 0 and comm.a2a_bytes > 0
         q.put((rank, same, partial_refused, comm.calls, comm.bytes))
     except Exception as exc:
         import traceback
@@ -88,7 +98,8 @@ def _worker(rank, world, port, case, q):
 
 @pytest.mark.parametrize("world,case", [(2, (5000, True)), (4, (5000, True)), (2, (8192, False)),
                                         (4, (8192, False)), (8, (32768, True)), (2, (3000, True, True)),
-                                        (2, (6000, True, False, "update")), (4, (6000, True, False, "h2sketch"))])
+                                        (2, (6000, True, False, "update")), (4, (6000, True, False, "h2sketch")),
+                                        (2, (5000, True, False, "cols")), (4, (8192, False, False, "cols"))])
 def test_distributed_build_bitwise(world, case):
     """world 8 (the 8 x B200 target's shard count, top depth >= 3 at N = 2^15), the exact-order
     kernels under sharding, and the H^2 + low-rank operators (row-sharded H^2 matvec sketch,
@@ -129,6 +140,12 @@ def _nccl_worker(port, q):
         comm.allgatherv(buf, [64], [0])
         torch.cuda.synchronize()
         ok_ag = bool(torch.equal(buf, ref))
+        src = torch.arange(50, dtype=torch.uint8, device="cuda")
+        dst = torch.full((60,), 7, dtype=torch.uint8, device="cuda")
+        comm.alltoallv(src, [20], [5], dst, [20], [30])     # world 1: the own segment (device copy)
+        torch.cuda.synchronize()
+        ok_ag = ok_ag and bool(torch.equal(dst[30:50], src[5:25])) and bool((dst[:30] == 7).all()) \
+            and bool((dst[50:] == 7).all())
         X = uniform_points(3000, 3, 1)
         T = g.Tree(X, 64)
         H = g.build(T, ("exp", 0.2), 1e-6, comm=comm)
