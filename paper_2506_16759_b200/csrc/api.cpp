@@ -301,6 +301,18 @@ cudaStream_t prio_stream(bool high) {
   return x;
 }
 
+// per-device side stream of the overlapped per-level all-gathers (default priority)
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t s[64] = {};
+  int dev = 0;
+  H2_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  cudaStream_t& x = s[dev & 63];
+  if (!x) H2_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  return x;
+}
+
 void stream_after(cudaStream_t later, cudaStream_t earlier) {
   cudaEvent_t e;
   H2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -392,33 +404,35 @@ struct Builder {
   }
 
   // all-gather rows [roff_r, roff_{r+1}) (per rank) of a row-major panel, columns [0, ncols)
-  void allgather_rows(double* p, int64_t ld, int ncols, const std::vector<int64_t>& rowb, int64_t nrows) {
+  void allgather_rows(double* p, int64_t ld, int ncols, const std::vector<int64_t>& rowb, int64_t nrows,
+                      cudaStream_t s = nullptr) {
     if (!comm || ncols <= 0) return;
+    if (!s) s = st;
     std::vector<int64_t> cnt(P), dsp(P);
     if (ld == ncols) {
       for (int r = 0; r < P; ++r) {
         dsp[r] = rowb[r] * ld * 8;
         cnt[r] = (rowb[r + 1] - rowb[r]) * ld * 8;
       }
-      comm_allgather(comm, p, cnt, dsp, st);
+      comm_allgather(comm, p, cnt, dsp, s);
       return;
     }
     DArr<double> pk;   // packed rows x ncols
-    pk.alloc(std::max<int64_t>(nrows, 1) * ncols, st);
+    pk.alloc(std::max<int64_t>(nrows, 1) * ncols, s);
     const int64_t r0 = rowb[R], r1 = rowb[R + 1];
     if (r1 > r0)
       H2_CUDA(cudaMemcpy2DAsync(pk.p + r0 * ncols, ncols * 8, p + r0 * ld, ld * 8, (size_t)ncols * 8, r1 - r0,
-                                cudaMemcpyDeviceToDevice, st));
+                                cudaMemcpyDeviceToDevice, s));
     for (int r = 0; r < P; ++r) {
       dsp[r] = rowb[r] * ncols * 8;
       cnt[r] = (rowb[r + 1] - rowb[r]) * ncols * 8;
     }
-    comm_allgather(comm, pk.p, cnt, dsp, st);
+    comm_allgather(comm, pk.p, cnt, dsp, s);
     if (nrows > 0)
-      H2_CUDA(cudaMemcpy2DAsync(p, ld * 8, pk.p, ncols * 8, (size_t)ncols * 8, nrows, cudaMemcpyDeviceToDevice, st));
+      H2_CUDA(cudaMemcpy2DAsync(p, ld * 8, pk.p, ncols * 8, (size_t)ncols * 8, nrows, cudaMemcpyDeviceToDevice, s));
   }
   // rows of the panel built by shrink(u): skeleton rows of depth u in roff order
-  void allgather_skel_rows(int u, double* p, int64_t ld, int ncols) {
+  void allgather_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s = nullptr) {
     if (!comm) return;
     const Level& L = H.L(u);
     std::vector<int64_t> rowb(P + 1);
@@ -426,7 +440,29 @@ struct Builder {
       const int c = own_begin(u, r, P);
       rowb[r] = c < L.nclus ? L.roff[c] : L.rtot;
     }
-    allgather_rows(p, ld, ncols, rowb, L.rtot);
+    allgather_rows(p, ld, ncols, rowb, L.rtot, s);
+  }
+  // Algorithm 1 line 258 (gen_B) with the all-gather of the parent panel's Omega^{l+1} rows
+  // (S§8(e); the BSR partners' samples of the next depth) overlapped: the gather runs on a side
+  // stream once the shrink is done while B is generated on the build stream (B needs only the
+  // skeletons, gathered in commit); the build stream waits for the gather before the next depth
+  // reads the panel.  gen_B is enqueued first, so a host-staged communicator (which blocks the
+  // host inside the gather) also overlaps with the device generating B.  H2_AG_OVERLAP=0: serial.
+  void gen_B_with_gather(int t, Panel* next, int ncols) {
+    if (!comm || !next) {
+      gen_B(t);
+      return;
+    }
+    if (env_int("H2_AG_OVERLAP", 1) == 0) {
+      allgather_skel_rows(t, next->O.p, next->ld, ncols);
+      gen_B(t);
+      return;
+    }
+    cudaStream_t cs = side_stream();
+    stream_after(cs, st);
+    gen_B(t);
+    allgather_skel_rows(t, next->O.p, next->ld, ncols, cs);
+    stream_after(st, cs);
   }
 
   // panel leading dimension: d_max when the panel is small, else the needed width + 2 blocks
@@ -1288,9 +1324,8 @@ struct Builder {
       if (t > top) {                                // lines 222-223 / 251-252, every column
         next.alloc(L.rtot, ld_for(L.rtot, dw), st);
         shrink(t, cur.Y.p, cur.O.p, cur.ld, next.Y.p, next.O.p, next.ld, dw);
-        allgather_skel_rows(t, next.O.p, next.ld, dw);
       }
-      gen_B(t);                                     // line 258
+      gen_B_with_gather(t, t > top ? &next : nullptr, dw);   // line 258 || Omega^{l+1} all-gather
       cur = std::move(next);
     }
     timer.mark(-1);
@@ -1811,9 +1846,8 @@ struct Builder {
       if (t > top) {                                // lines 222-223 / 251-252 into the parent panel
         next.alloc(L.rtot, ld_for(L.rtot, d), st);
         shrink(t, cur.Y.p, cur.O.p, cur.ld, next.Y.p, next.O.p, next.ld, d);
-        allgather_skel_rows(t, next.O.p, next.ld, d);   // Omega^{l+1} of every cluster (S§8(e))
       }
-      gen_B(t);                                     // line 258
+      gen_B_with_gather(t, t > top ? &next : nullptr, d);    // line 258 || Omega^{l+1} all-gather
       cur = std::move(next);
     }
     timer.mark(-1);
