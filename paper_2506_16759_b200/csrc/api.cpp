@@ -337,6 +337,7 @@ struct Builder {
   DArr<double> sumsq_acc;
   DArr<int> nonfinite;
   DArr<double> W;               // CPQR workspace
+  DArr<int32_t> fail_flag;      // CPQR early exit of a failing convergence test (CpqrArgs)
   PhaseTimer timer;
   int64_t entries_sketch = 0;
   const h2_comm* comm = nullptr;   // NULL: one GPU
@@ -913,6 +914,16 @@ struct Builder {
     a.perm = L.d_perm.p;
     a.cert = L.cert.p;
     a.rows = L.rows;
+    // adaptive early exit of a failing convergence test (CpqrArgs::fail_cap; H2_CQ_EARLY=0: off):
+    // the level decision is unchanged, the discarded round stops at the first definitive failure
+    const int pos = (o.tol_rule == H2_TOL_RMS) ? o.p_os : 0;
+    if (o.adaptive && !ex && d - pos - 1 >= 0 && env_int("H2_CQ_EARLY", 1) != 0) {
+      if (fail_flag.n == 0) fail_flag.alloc(1, st);
+      H2_CUDA(cudaMemsetAsync(fail_flag.p, 0, sizeof(int32_t), st));
+      a.fail_cap = d - pos - 1;
+      a.fail_k = d - pos;
+      a.fail_flag = fail_flag.p;
+    }
     if (ex) {
       launch_exact_cpqr(a, st);
       H.stats.cpqr_variants |= H2_CQ_V_EXACT;

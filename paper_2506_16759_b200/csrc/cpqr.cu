@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   double* spanel = nrm + a.max_m + (a.max_m + 1) / 2;   // m*LD (SMEM variant)
   __shared__ Top2 red[CQ_WARPS];
   __shared__ double s_tau;
+  __shared__ int s_abort;   // the level-failure flag as polled by thread 0 in the previous step
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = threadIdx.x & (CQ_TPR - 1), rloc = threadIdx.x / CQ_TPR;
   const int64_t off = a.poff[c];
@@ -92,12 +93,21 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   uint32_t dyn_bytes = 0;
   if constexpr (HYB) asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
   const int64_t hyb_cap = HYB ? (int64_t)(dyn_bytes / 8) - (int64_t)(spanel - smem) : 0;   // doubles
+  if (a.fail_flag) {   // the level already failed (CpqrArgs::fail_cap): skip the discarded panel
+    if (threadIdx.x == 0) s_abort = *reinterpret_cast<volatile int*>(a.fail_flag);
+    __syncthreads();
+    if (s_abort) {
+      if (threadIdx.x == 0) a.k[c] = 0;
+      return;
+    }
+  }
   // copy panel rows (Y^loc rows) into the work panel
   for (int64_t e = threadIdx.x; e < (int64_t)m * d; e += CQ_THREADS) {
     const int64_t j = e / d;
     A[j * LD + (e - j * d)] = a.Y[(off + j) * a.ldy + (e - j * d)];
   }
   for (int j = threadIdx.x; j < m; j += CQ_THREADS) perm[j] = j;
+  if (threadIdx.x == 0) s_abort = 0;
   __syncthreads();
   auto row_sum = [&](double x) {   // sum over the 8 threads of a row (fixed order)
     x += __shfl_xor_sync(0xffffffffu, x, 1);
@@ -138,6 +148,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
   const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
   double min_gap = INFINITY, margin = INFINITY;
   int k = 0;
+  bool aborted = false;
   // -DH2_CQ_PROF: cycles per pivot step by phase (clock64), printed for two CTAs
 #ifdef H2_CQ_PROF
   long long pr[6] = {0, 0, 0, 0, 0, 0}, tp0 = 0, tp1 = 0;
@@ -171,6 +182,19 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     if (i == kcap || !(t.v > a.eps)) {
       k = i;
       break;
+    }
+    if (a.fail_flag) {   // adaptive early exit (CpqrArgs::fail_cap): uniform decisions
+      if (i == a.fail_cap && m > d) {
+        if (threadIdx.x == 0) atomicExch(a.fail_flag, 1);
+        k = a.fail_k;
+        aborted = true;
+        break;
+      }
+      if (s_abort) {
+        k = i;
+        aborted = true;
+        break;
+      }
     }
     if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
     const int p = t.i;
@@ -237,6 +261,9 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     __syncthreads();
     CQP(2);   // barrier 1
     const double tau = s_tau;
+    // poll the level-failure flag (read by thread 0 now, acted on after the next merge)
+    int fl = 0;
+    if (a.fail_flag && threadIdx.x == 0) fl = *reinterpret_cast<volatile int*>(a.fail_flag);
     // ---- trailing update of rows j > i (columns of A) + next residual norms + local pivot
     Top2 loc{-1.0, 0x7fffffff, -1.0};
     const int r0 = i + ((sub - i) & (CQ_TPR - 1));   // first r >= i with r = sub mod 8
@@ -303,6 +330,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     }
     loc = warp_best(loc);
     if (lane == 0) red[warp] = loc;
+    if (a.fail_flag && threadIdx.x == 0) s_abort = fl;
     CQP(3);   // trailing update + local pivot
     __syncthreads();
     CQP(4);   // barrier 2
@@ -316,6 +344,10 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
 #endif
 #undef CQP
   __syncthreads();
+  if (aborted) {   // this round is discarded by the host (the level failed): only k is read
+    if (threadIdx.x == 0) a.k[c] = k;
+    return;
+  }
   if (HYB && ro > 0) {   // the shared-memory part back into the panel in W
     const int w = d - ro;
     for (int64_t e = threadIdx.x; e < (int64_t)(m - ro) * w; e += CQ_THREADS) {
@@ -776,6 +808,10 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
   double* nrm = v + d;
   int* perm = reinterpret_cast<int*>(nrm + 64);
   const int64_t off = a.poff[c];
+  if (a.fail_flag && __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile int*>(a.fail_flag) : 0, 0)) {
+    if (lane == 0) a.k[c] = 0;   // the level already failed: skip the discarded panel
+    return;
+  }
   for (int j = 0; j < m; ++j)
     for (int r = lane; r < d; r += 32) A[j * LD + r] = a.Y[(off + j) * a.ldy + r];
   __syncwarp();
@@ -798,6 +834,8 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
   const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
   double min_gap = INFINITY, margin = INFINITY;
   int k = 0;
+  bool aborted = false;
+  int fl = 0;   // level-failure flag polled by lane 0 in the previous step
   for (int i = 0;; ++i) {
     Top2 t{-1.0, 0x7fffffff, -1.0};
     for (int q = 0; q < 2; ++q) {
@@ -810,6 +848,20 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
     if (i == kcap || !(t.v > a.eps)) {
       k = i;
       break;
+    }
+    if (a.fail_flag) {   // adaptive early exit (CpqrArgs::fail_cap)
+      if (i == a.fail_cap && m > d) {
+        if (lane == 0) atomicExch(a.fail_flag, 1);
+        k = a.fail_k;
+        aborted = true;
+        break;
+      }
+      if (__shfl_sync(0xffffffffu, fl, 0)) {
+        k = i;
+        aborted = true;
+        break;
+      }
+      if (lane == 0) fl = *reinterpret_cast<volatile int*>(a.fail_flag);
     }
     if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
     const int p = t.i;
@@ -892,6 +944,10 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
     k = i + 1;
   }
   __syncwarp();
+  if (aborted) {   // this round is discarded by the host (the level failed): only k is read
+    if (lane == 0) a.k[c] = k;
+    return;
+  }
   for (int j = lane; j < m; j += 32) a.perm[off + j] = perm[j];
   double* Wc = a.W + off * d;
   for (int j = 0; j < m; ++j)

@@ -113,6 +113,15 @@ struct CpqrArgs {
   int32_t* perm;          // at poff[c]
   double* cert;           // 2 per cluster (min gap, stop margin)
   int64_t rows;           // total panel rows (poff range) of the depth
+  // Adaptive convergence test early exit (exact: the same level decision, no arithmetic change).
+  // A level is converged iff every cluster has m <= d or k <= d - 1 - p_os (R12); a cluster with
+  // m > d whose residual norm still exceeds eps at step fail_cap = d - p_os - 1 will take >= d - p_os
+  // pivots, so the level fails and this round's factorisations are all discarded.  That cluster
+  // writes k = fail_k (= d - p_os) and raises *fail_flag; every panel polls the flag once per step
+  // (one step late) and stops (k = steps done).  fail_flag NULL: off (fixed-rank builds).
+  int32_t fail_cap = -1;
+  int32_t fail_k = 0;
+  int32_t* fail_flag = nullptr;
 };
 // returns the variant that ran: H2_CQ_V_WARP (warp per panel, m <= 64), H2_CQ_V_SMEM (CTA per
 // panel, panel in shared memory) or H2_CQ_V_GLOBAL (CTA per panel, panel in global W).
