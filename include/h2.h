@@ -317,10 +317,11 @@ typedef struct {
   double work_flops[H2_NPHASE];
   double work_bytes[H2_NPHASE];
 } h2_build_stats;
-/* CPQR kernel variants (h2_build_stats.cpqr_variants; H2_CQ_VARIANT=warp|smem|global forces one
+/* CPQR kernel variants (h2_build_stats.cpqr_variants; H2_CQ_VARIANT=warp|smem|global|cluster forces one
  * where it applies): one warp per panel (m <= 64), one CTA per panel with the panel in shared
  * memory, one CTA per panel with the panel in global memory (L1/L2 resident). */
-enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4, H2_CQ_V_EXACT = 8 /* exact-order mode */ };
+enum { H2_CQ_V_WARP = 1, H2_CQ_V_SMEM = 2, H2_CQ_V_GLOBAL = 4, H2_CQ_V_EXACT = 8 /* exact-order mode */,
+       H2_CQ_V_CLUSTER = 16 /* a cluster of 2 or 4 CTAs per panel, rows in distributed shared memory */ };
 
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU (§IV-B: "the batch count becomes roughly the number

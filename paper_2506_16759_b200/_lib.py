@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libh2.so")
+LIB_PATH = os.environ.get("H2_LIB_PATH") or os.path.join(_HERE, "libh2.so")   # H2_LIB_PATH: a profiling build
 
 H2_OK, H2_ERR_INVALID_ARG, H2_ERR_OOM, H2_ERR_CUDA, H2_ERR_NCCL = 0, -1, -2, -3, -4
 H2_ERR_CALLBACK, H2_ERR_NOT_CONVERGED, H2_ERR_NONFINITE = -5, -6, -7
@@ -20,7 +20,7 @@ H2_TOL_RMS, H2_TOL_LITERAL = 0, 1
 H2_SPLIT_ROWS, H2_SPLIT_COLS = 0, 1
 H2_X_RANK, H2_X_SKEL, H2_X_BASIS, H2_X_D, H2_X_B, H2_X_CERT, H2_X_RANK_C, H2_X_SKEL_C, H2_X_BASIS_C, H2_X_CERT_C = range(10)
 H2_SKETCH_OMEGA_QUARTERS = 1
-H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL, H2_CQ_V_EXACT = 1, 2, 4, 8
+H2_CQ_V_WARP, H2_CQ_V_SMEM, H2_CQ_V_GLOBAL, H2_CQ_V_EXACT, H2_CQ_V_CLUSTER = 1, 2, 4, 8, 16
 PHASES = ["rand", "sketch", "gen", "bsr", "cpqr", "id", "misc"]
 H2_ALL_DEPTHS = -1   # h2_export: every processed depth concatenated (ranks / skeletons)
 H2_NPHASE = len(PHASES)

@@ -2,6 +2,8 @@
 // which is also the convergence test of §III-B (L361, "QR decomposition ... smallest absolute
 // value of the diagonal"; reading R12), the ID epilogue (T = R11^{-1} R12, Eq.(3)) and the
 // shrink / Omega upsweep (batchedShrink L222/L251, batchedGemm L223/L252).
+#include <cooperative_groups.h>
+
 #include "alloc.hpp"
 #include "common.cuh"
 #include "kernels.hpp"
@@ -178,7 +180,9 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
     CQP(0);   // pivot merge
     if (i >= m) break;
     // truncation margin of every decision taken (R13); no decision exists at i = min(d, m)
-    if (a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    // certificates (R13): one thread of the LAST warp (off warp 0's reflector path)
+    const bool certthr = threadIdx.x == CQ_THREADS - 32;
+    if (certthr && a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
     if (i == kcap || !(t.v > a.eps)) {
       k = i;
       break;
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
         break;
       }
     }
-    if (t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    if (certthr && t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
     const int p = t.i;
     double* Ai = rowp(i);
     if (warp == 0) {
@@ -363,8 +367,8 @@ __global__ void __launch_bounds__(CQ_THREADS) cpqr_kernel(CpqrArgs a) {
       Wc[e] = A[j * LD + (e - j * d)];
     }
   }
-  if (threadIdx.x == 0) {
-    a.k[c] = k;
+  if (threadIdx.x == 0) a.k[c] = k;
+  if (threadIdx.x == CQ_THREADS - 32) {
     a.cert[2 * c] = min_gap;
     a.cert[2 * c + 1] = margin;
   }
@@ -959,11 +963,307 @@ __global__ void __launch_bounds__(32 * CW_WPB) cpqr_warp_kernel(CpqrArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// CTA-cluster CPQR (round 2) for panels too large for one CTA's shared memory (m * d at the
+// upper depths: 180-240 rows x 160 samples = 230-320 KB), which the one-CTA kernel otherwise
+// streams from global memory every pivot step (L2-latency bound: 18-33 k cycles per step).
+// One cluster of CL CTAs per panel: panel row j lives in CTA j % CL (local row j / CL) in shared
+// memory, so each CTA updates 1/CL of the rows.  Rows never move: a pivot row is retired in
+// place and the positions are tracked (pos[row], rowat[position], replicated in every CTA), so
+// each row's arithmetic is exactly the one-CTA kernel's (same 8-thread row split, same fixed-order
+// reductions, same dlarfg reflector) and the pivot candidates carry (position << 16 | row): ties
+// go to the lowest POSITION as in the row-swapping kernels.  The result is bitwise theirs.
+// Per step: (A) cluster barrier -> every warp merges the NW x CL candidates (one per lane) ->
+// the owner CTA's warp 0 builds the reflector from its local pivot row and writes v, tau into
+// every CTA (distributed shared memory); thread 0 of every CTA swaps the two positions;
+// (B) cluster barrier -> trailing update of the local active rows (position > i), next norms,
+// per-warp candidates written into every CTA.  Early exit (CpqrArgs::fail_cap) as the one-CTA
+// kernel, with the polled flag broadcast by CTA 0 so that every CTA of the cluster decides alike.
+// ------------------------------------------------------------------------------------------
+namespace cgx = cooperative_groups;
+__host__ __device__ inline size_t cqc_head_bytes(int d, int max_m) {
+  return (((size_t)d * 8 + 32 * 8 * 2 + 32 * 4 + (size_t)max_m * 8 + 8) + 127) / 128 * 128;
+}
+template <int CL, int NT>
+__global__ void __launch_bounds__(NT) cpqr_cluster_kernel(CpqrArgs a) {
+  constexpr int NW = NT / 32;
+  static_assert(NW * CL <= 32, "one pivot candidate per lane of the merge");
+  constexpr int RPP = NT / CQ_TPR;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int c = a.c_begin + blockIdx.x / CL;
+  const int m = a.m[c], d = a.d, LD = cq_ld(d);
+  const int mloc = (m - crank + CL - 1) / CL;
+  extern __shared__ __align__(128) unsigned char cq_smem[];
+  double* v = reinterpret_cast<double*>(cq_smem);          // d
+  double* cv = v + d;                                      // 32 candidate values
+  double* cs = cv + 32;                                    // 32 second-best values
+  int* ci = reinterpret_cast<int*>(cs + 32);               // 32 packed indices
+  int* pos = ci + 32;                                      // max_m
+  int* rowat = pos + a.max_m;                              // max_m
+  double* P = reinterpret_cast<double*>(cq_smem + cqc_head_bytes(d, a.max_m));   // mloc x LD
+  __shared__ double s_tau;
+  __shared__ int s_abort;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = tid & (CQ_TPR - 1), rloc = tid / CQ_TPR;
+  const int64_t off = a.poff[c];
+  double* vr[CL];
+  double* cvr[CL];
+  double* csr[CL];
+  int* cir[CL];
+  double* taur[CL];
+  int* abr[CL];
+#pragma unroll
+  for (int q = 0; q < CL; ++q) {
+    vr[q] = cl.map_shared_rank(v, q);
+    cvr[q] = cl.map_shared_rank(cv, q);
+    csr[q] = cl.map_shared_rank(cs, q);
+    cir[q] = cl.map_shared_rank(ci, q);
+    taur[q] = cl.map_shared_rank(&s_tau, q);
+    abr[q] = cl.map_shared_rank(&s_abort, q);
+  }
+  if (tid == 0) s_abort = 0;
+  cl.sync();   // every CTA of the cluster runs before any distributed shared memory access
+  if (a.fail_flag) {   // the level already failed: skip the discarded panel (cluster-uniform)
+    if (crank == 0 && tid == 0) {
+      const int f = *reinterpret_cast<volatile int*>(a.fail_flag);
+#pragma unroll
+      for (int q = 0; q < CL; ++q) *abr[q] = f;
+    }
+    cl.sync();
+    if (s_abort) {
+      if (crank == 0 && tid == 0) a.k[c] = 0;
+      return;
+    }
+  }
+  for (int64_t e = tid; e < (int64_t)mloc * d; e += NT) {
+    const int64_t jl = e / d;
+    P[jl * LD + (e - jl * d)] = a.Y[(off + crank + CL * jl) * a.ldy + (e - jl * d)];
+  }
+  for (int j = tid; j < m; j += NT) {
+    pos[j] = j;
+    rowat[j] = j;
+  }
+  __syncthreads();
+  auto row_sum = [&](double x) {
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    return x;
+  };
+  auto warp_best = [&](Top2 t) {
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      Top2 u;
+      u.v = __shfl_xor_sync(0xffffffffu, t.v, o);
+      u.i = __shfl_xor_sync(0xffffffffu, t.i, o);
+      u.s = __shfl_xor_sync(0xffffffffu, t.s, o);
+      t = top2_merge(t, u);
+    }
+    return t;
+  };
+  auto publish = [&](Top2 t) {   // this warp's candidate into slot crank * NW + warp of every CTA
+    if (lane == 0) {
+      const int slot = crank * NW + warp;
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        cvr[q][slot] = t.v;
+        csr[q][slot] = t.s;
+        cir[q][slot] = t.i;
+      }
+    }
+  };
+  {
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    for (int jl0 = 0; jl0 < mloc; jl0 += RPP) {
+      const int jl = jl0 + rloc;
+      double q = 0.0;
+      if (jl < mloc)
+        for (int r = sub; r < d; r += CQ_TPR) q = fma(P[(int64_t)jl * LD + r], P[(int64_t)jl * LD + r], q);
+      q = row_sum(q);
+      if (jl < mloc) {
+        const int j = crank + CL * jl;
+        loc = top2_merge(loc, Top2{sqrt(q), (j << 16) | j, -1.0});
+      }
+    }
+    publish(warp_best(loc));
+  }
+  const int kfull = min(d, m);
+  const int kcap = a.kmax > 0 ? min(kfull, a.kmax) : kfull;
+  double min_gap = INFINITY, margin = INFINITY;
+  int k = 0;
+  bool aborted = false;
+#ifdef H2_CQ_PROF
+  long long pr[6] = {0, 0, 0, 0, 0, 0}, tp0 = clock64(), tp1 = 0;
+#define CQC(n) do { tp1 = clock64(); pr[n] += tp1 - tp0; tp0 = tp1; } while (0)
+#else
+#define CQC(n) do { } while (0)
+#endif
+  for (int i = 0;; ++i) {
+    CQC(4);   // publish
+    cl.sync();   // (A) the candidates of step i (and the polled flag) are visible
+    CQC(0);   // barrier A
+    Top2 t = lane < NW * CL ? Top2{cv[lane], ci[lane], cs[lane]} : Top2{-1.0, 0x7fffffff, -1.0};
+    t = warp_top2(t);
+    CQC(1);   // merge
+    if (i >= m) break;
+    const bool certthr = crank == 0 && tid == NT - 32;   // certificates (R13) off warp 0's path
+    if (certthr && a.eps > 0 && i < kfull) margin = fmin(margin, fabs(t.v - a.eps) / a.eps);
+    if (i == kcap || !(t.v > a.eps)) {
+      k = i;
+      break;
+    }
+    if (a.fail_flag) {
+      if (i == a.fail_cap && m > d) {
+        if (crank == 0 && tid == 0) atomicExch(a.fail_flag, 1);
+        k = a.fail_k;
+        aborted = true;
+        break;
+      }
+      if (s_abort) {
+        k = i;
+        aborted = true;
+        break;
+      }
+    }
+    if (certthr && t.s >= 0) min_gap = fmin(min_gap, (t.v - t.s) / t.v);
+    const int ppos = t.i >> 16, prow = t.i & 0xffff;
+    if (crank == prow % CL && warp == 0) {
+      // ---- Householder reflector of the pivot row's entries r >= i (dlarfg, as cpqr_kernel)
+      double* Ai = P + (int64_t)(prow / CL) * LD;
+      double x2 = 0.0;
+      for (int r = i + 1 + lane; r < d; r += 32) x2 = fma(Ai[r], Ai[r], x2);
+      x2 = warp_sum(x2);
+      const double alpha = Ai[i];
+      const double xnorm = sqrt(x2);
+      double tau, beta;
+      if (xnorm == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+      } else {
+        const double h = hypot(alpha, xnorm);
+        beta = alpha != 0.0 ? -copysign(h, alpha) : -h;
+        tau = (beta - alpha) / beta;
+      }
+      const double den = alpha - beta;
+      __syncwarp();
+      const double rden = 1.0 / den;
+      for (int r = i + 1 + lane; r < d; r += 32) {
+        const double x = tau != 0.0 ? Ai[r] * rden : 0.0;
+#pragma unroll
+        for (int q = 0; q < CL; ++q) vr[q][r] = x;
+        Ai[r] = 0.0;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < CL; ++q) {
+          vr[q][i] = 1.0;
+          *taur[q] = tau;
+        }
+        Ai[i] = beta;
+      }
+    }
+    if (tid == 0) {   // positions i and ppos exchange their rows (identical in every CTA)
+      const int r0w = rowat[i];
+      rowat[i] = prow;
+      rowat[ppos] = r0w;
+      pos[r0w] = ppos;
+      pos[prow] = i;
+    }
+    CQC(2);   // reflector (owner warp 0) + swap
+    cl.sync();   // (B) v, tau and the positions are visible
+    CQC(5);   // barrier B
+    // poll the level-failure flag (global load hidden behind the update; broadcast before (A))
+    int fl = 0;
+    if (a.fail_flag && crank == 0 && tid == NT - 32) fl = *reinterpret_cast<volatile int*>(a.fail_flag);
+    const double tau = s_tau;
+    Top2 loc{-1.0, 0x7fffffff, -1.0};
+    const int r0 = i + ((sub - i) & (CQ_TPR - 1));
+    for (int jl0 = 0; jl0 < mloc; jl0 += RPP) {
+      const int jl = jl0 + rloc;
+      const int j = crank + CL * jl;
+      const bool act = jl < mloc && pos[j] > i;
+      double* Aj = P + (int64_t)(act ? jl : 0) * LD;
+      double w = 0.0;
+      if (act)
+        for (int r = r0; r < d; r += CQ_TPR) w = fma(v[r], Aj[r], w);
+      w = row_sum(w) * tau;
+      double q = 0.0;
+      if (act)
+        for (int r = r0; r < d; r += CQ_TPR) {
+          const double x = fma(-w, v[r], Aj[r]);
+          Aj[r] = x;
+          if (r > i) q = fma(x, x, q);
+        }
+      q = row_sum(q);
+      if (act) loc = top2_merge(loc, Top2{sqrt(q), (pos[j] << 16) | j, -1.0});
+    }
+    CQC(3);   // update
+    publish(warp_best(loc));
+    if (a.fail_flag && crank == 0 && tid == NT - 32) {
+#pragma unroll
+      for (int q = 0; q < CL; ++q) *abr[q] = fl;
+    }
+    k = i + 1;
+  }
+#ifdef H2_CQ_PROF
+  if ((tid == 0 || tid == NT - 32) && blockIdx.x < CL && !aborted)
+    printf("[cqc prof] cta %d thr %d m %d d %d k %d | barA %lld merge %lld refl %lld upd %lld publ %lld barB %lld (cycles/step)\n",
+           crank, tid, m, d, k, pr[0] / max(k, 1), pr[1] / max(k, 1), pr[2] / max(k, 1), pr[3] / max(k, 1),
+           pr[4] / max(k, 1), pr[5] / max(k, 1));
+#endif
+#undef CQC
+  // no distributed shared memory access after the last (A): every CTA may leave
+  if (aborted) {
+    if (crank == 0 && tid == 0) a.k[c] = k;
+    return;
+  }
+  for (int64_t e = tid; e < (int64_t)mloc * d; e += NT) {
+    const int64_t jl = e / d;
+    const int j = crank + CL * (int)jl;
+    a.W[(off + pos[j]) * d + (e - jl * d)] = P[jl * LD + (e - jl * d)];
+  }
+  if (crank == 0) {
+    for (int q = tid; q < m; q += NT) a.perm[off + q] = rowat[q];
+    if (tid == 0) a.k[c] = k;
+    if (tid == NT - 32) {
+      a.cert[2 * c] = min_gap;
+      a.cert[2 * c + 1] = margin;
+    }
+  }
+}
+
+template <int CL, int NT>
+static void cpqr_cluster_launch(const CpqrArgs& a, size_t sm, cudaStream_t st) {
+  auto kfn = cpqr_cluster_kernel<CL, NT>;
+  H2_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)a.nclusters * CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  H2_CUDA(cudaLaunchKernelEx(&cfg, kfn, a));
+}
+
+// shared memory per CTA of the cluster kernel with CL CTAs per panel
+static size_t cqc_smem(const CpqrArgs& a, int CL) {
+  const int mloc = (a.max_m + CL - 1) / CL;
+  return cqc_head_bytes(a.d, a.max_m) + sizeof(double) * (size_t)mloc * cq_ld(a.d);
+}
+
 static int forced_variant() {
   const char* v = getenv("H2_CQ_VARIANT");
   if (!v) return 0;
   const std::string s(v);
-  return s == "warp" ? H2_CQ_V_WARP : s == "smem" ? H2_CQ_V_SMEM : s == "global" ? H2_CQ_V_GLOBAL : 0;
+  return s == "warp" ? H2_CQ_V_WARP : s == "smem" ? H2_CQ_V_SMEM : s == "global" ? H2_CQ_V_GLOBAL
+       : s == "cluster" ? H2_CQ_V_CLUSTER : 0;
 }
 
 int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
@@ -1032,6 +1332,27 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   // rows per pass = threads / 8 (32 or 64); 512 threads once a panel has more than 32 rows
   const bool big = a.max_m > 32;
   int used;
+  // CTA-cluster kernel (H2_CQ_CLUSTER, default 1: the panels that do not fit one CTA's shared
+  // memory on levels with at most 74 panels; 2: every such level; 0 off): 2 CTAs x 512 threads,
+  // or 4 x 256 when half a panel does not fit either
+  const int clus = env_int("H2_CQ_CLUSTER", 1);
+  const bool fits1 = sm + panel <= 200 * 1024;
+  // measured at C2 (ncu, profiles/r2_cpqr_cluster.md): faster on levels with few panels (32 / 64:
+  // 1.17 -> 0.76, 1.31 -> 0.93 ms), slower once 2 CTAs per panel exceed the SMs (128-1024 panels)
+  const bool few_panels = 2 * a.nclusters <= 148;
+  if ((force == H2_CQ_V_CLUSTER || (force == 0 && clus != 0 && !fits1 && (few_panels || clus == 2))) &&
+      a.max_m >= 2) {
+    if (cqc_smem(a, 2) <= 210 * 1024) {
+      cpqr_cluster_launch<2, 512>(a, cqc_smem(a, 2), st);
+      H2_CHECK_LAUNCH();
+      return H2_CQ_V_CLUSTER;
+    }
+    if (cqc_smem(a, 4) <= 210 * 1024) {
+      cpqr_cluster_launch<4, 256>(a, cqc_smem(a, 4), st);
+      H2_CHECK_LAUNCH();
+      return H2_CQ_V_CLUSTER;
+    }
+  }
   if (sm + panel <= 200 * 1024 && force != H2_CQ_V_GLOBAL) {
     sm += panel;
     if (big) cpqr_launch<true, 512>(a, sm, st);

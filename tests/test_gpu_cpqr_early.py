@@ -45,3 +45,28 @@ def test_early_exit_bitwise(case, monkeypatch):
     assert max(a["rounds"].values()) > 1, "case must contain a failing convergence test"
     bad = [k for k in a if not (a[k] == b[k] if k in ("samples", "rounds") else np.array_equal(a[k], b[k]))]
     assert not bad, bad
+
+
+@pytest.mark.parametrize("case", [(8192, 3, {"H2_CQ_VARIANT": "cluster"}, {"H2_CQ_VARIANT": "global"}),
+                                  (65536, 3, {}, {"H2_CQ_CLUSTER": "0"}),
+                                  (16384, 2, {"H2_CQ_VARIANT": "cluster"}, {"H2_CQ_VARIANT": "smem"})])
+def test_cluster_cpqr_bitwise(case, monkeypatch):
+    """The CTA-cluster CPQR (rows in distributed shared memory, retired in place, positions
+    tracked) performs each row's arithmetic and each pivot decision exactly as the row-swapping
+    one-CTA kernels: builds with it forced on every level, or chosen for the panels that do not
+    fit one CTA (default, N = 2^16), are bitwise the builds without it."""
+    n, dim, env_a, env_b = case
+    X = uniform_points(n, dim, 7)
+    T = g.Tree(X, 64)
+    out = []
+    for env in (env_a, env_b):
+        for k in ("H2_CQ_VARIANT", "H2_CQ_CLUSTER"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        H = g.build(T, ("exp", 0.2), 1e-6)
+        out.append((_snap(H), H.stats["cpqr_variants"]))
+    (a, va), (b, vb) = out
+    assert va & g._lib.H2_CQ_V_CLUSTER and not vb & g._lib.H2_CQ_V_CLUSTER, (va, vb)
+    bad = [k for k in a if not (a[k] == b[k] if k in ("samples", "rounds") else np.array_equal(a[k], b[k]))]
+    assert not bad, bad

@@ -85,11 +85,12 @@ def test_build_parity(case, adaptive):
     compare_matvec(Hg, Ho, certified, bound)
 
 
-@pytest.mark.parametrize("variant", ["warp", "smem", "global", "smem2", "global2"])
+@pytest.mark.parametrize("variant", ["warp", "smem", "global", "cluster", "smem2", "global2"])
 @pytest.mark.parametrize("case", ["cov3d_5000", "ie_grid16"])
 def test_build_parity_each_cpqr_variant(monkeypatch, case, variant):
     """Every CPQR kernel variant (warp per panel / CTA with the panel in shared memory / CTA with
-    the panel in global W, the one large inner panels take at N = 2^18; "2": the opt-in cpqr2
+    the panel in global W / a cluster of CTAs with the rows in distributed shared memory, the one
+    large inner panels take at N = 2^18; "2": the opt-in cpqr2
     kernel, H2_CQ2=1) forced on every level of an adaptive build: same skeleton / rank / sample
     parity with the oracle, and the stats name the variant that ran."""
     mk, kind, p, leaf, tol = CASES[case]
@@ -101,12 +102,13 @@ def test_build_parity_each_cpqr_variant(monkeypatch, case, variant):
         variant = variant[:-1]
     monkeypatch.setenv("H2_CQ_VARIANT", variant)
     Hg = g.build(T, (kind, p), tol)
-    bit = {"warp": g._lib.H2_CQ_V_WARP, "smem": g._lib.H2_CQ_V_SMEM, "global": g._lib.H2_CQ_V_GLOBAL}[variant]
+    bit = {"warp": g._lib.H2_CQ_V_WARP, "smem": g._lib.H2_CQ_V_SMEM, "global": g._lib.H2_CQ_V_GLOBAL,
+           "cluster": g._lib.H2_CQ_V_CLUSTER}[variant]
     used = Hg.stats["cpqr_variants"]
     assert used & bit, used
     if variant != "warp":
         assert not used & g._lib.H2_CQ_V_WARP        # forced on the leaf panels too
-    if variant == "global":
+    if variant in ("global", "cluster"):
         assert used == bit
     div = {}
     certified, compared = compare_builds(Hg, Ho, div)
