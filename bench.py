@@ -514,10 +514,11 @@ def time_workload(g, torch, stream, flush, name, steps=2):
         extra["base_build_s_untimed"] = round(time.perf_counter() - t0, 2)
         upd = (Hb, torch.from_numpy(lowrank_factor(n, w["update_rank"])).cuda())
         opts["update"] = upd
-    # warm-up builds: one, or three for configs[4] (near the 180 GB capacity the block cache
-    # reaches its steady state -- ~7 cudaMalloc per build -- only after a few builds; the first
-    # ones spend 0.3-0.6 s re-mapping blocks, H2_TRACE=1, tools/c5_trace.py)
-    for _ in range(3 if upd is not None else 1):
+    # warm-up builds: one, or four for configs[4] (near the 180 GB capacity the block cache
+    # reaches its steady state -- ~7 cudaMalloc per build -- only after four builds; the first
+    # ones spend 0.3-0.6 s re-mapping blocks, H2_TRACE=1, tools/c5_trace.py; serving oversized
+    # free blocks instead ran out of memory)
+    for _ in range(4 if upd is not None else 1):
         H = g.build(T, kern, w["tol"], **opts)
         del H
     times, stats = [], []
