@@ -432,9 +432,18 @@ struct Builder {
     if (nrows > 0)
       H2_CUDA(cudaMemcpy2DAsync(p, ld * 8, pk.p, ncols * 8, (size_t)ncols * 8, nrows, cudaMemcpyDeviceToDevice, s));
   }
-  // rows of the panel built by shrink(u): skeleton rows of depth u in roff order
+  // rows of the panel built by shrink(u): skeleton rows of depth u in roff order.  Their only
+  // remote reader is the BSR of depth u - 1 (far pairs of depth u, Algorithm 1), so by
+  // default (H2_HALO=1, a communicator with an all-to-all) only the HALO moves: rank R sends the
+  // rows of its cluster b to rank q iff b has a far partner owned by q (S§8(e): ~0.4x the
+  // all-gather bytes at P = 8).  H2_HALO=0: every rank's rows to every rank (all-gather).
+  int64_t halo_rows_sent = 0;
   void allgather_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s = nullptr) {
     if (!comm) return;
+    if (ncols > 0 && (comm->alltoallv || comm->nccl) && env_int("H2_HALO", 1) != 0) {
+      halo_skel_rows(u, p, ld, ncols, s ? s : st);
+      return;
+    }
     const Level& L = H.L(u);
     std::vector<int64_t> rowb(P + 1);
     for (int r = 0; r <= P; ++r) {
@@ -443,6 +452,50 @@ struct Builder {
     }
     allgather_rows(p, ld, ncols, rowb, L.rtot, s);
   }
+  void halo_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s) {
+    const Level& L = H.L(u);
+    const PairCSR& F = T.far[u];
+    const int n = L.nclus;
+    auto owner = [&](int c) { return (int)((int64_t)c * P / n); };
+    std::vector<std::vector<int32_t>> sendb(P), recvb(P);
+    std::vector<char> mark(P);
+    for (int b = cb(u); b < ce(u); ++b) {   // own clusters with a partner owned by q (ascending b)
+      std::fill(mark.begin(), mark.end(), 0);
+      for (int32_t e = F.ptr[b]; e < F.ptr[b + 1]; ++e) mark[owner(F.idx[e])] = 1;
+      for (int q = 0; q < P; ++q)
+        if (q != R && mark[q]) sendb[q].push_back(b);
+    }
+    for (int s0 = cb(u); s0 < ce(u); ++s0)   // remote partners of own clusters, per owner
+      for (int32_t e = F.ptr[s0]; e < F.ptr[s0 + 1]; ++e) {
+        const int b = F.idx[e], q = owner(b);
+        if (q != R) recvb[q].push_back(b);
+      }
+    std::vector<int32_t> srows, rrows;
+    std::vector<int64_t> sc(P, 0), sd(P, 0), rc(P, 0), rd(P, 0);
+    for (int q = 0; q < P; ++q) {
+      std::sort(recvb[q].begin(), recvb[q].end());
+      recvb[q].erase(std::unique(recvb[q].begin(), recvb[q].end()), recvb[q].end());
+      sd[q] = (int64_t)srows.size() * ncols * 8;
+      for (int b : sendb[q])
+        for (int i = 0; i < L.k[b]; ++i) srows.push_back((int32_t)(L.roff[b] + i));
+      sc[q] = (int64_t)srows.size() * ncols * 8 - sd[q];
+      rd[q] = (int64_t)rrows.size() * ncols * 8;
+      for (int b : recvb[q])
+        for (int i = 0; i < L.k[b]; ++i) rrows.push_back((int32_t)(L.roff[b] + i));
+      rc[q] = (int64_t)rrows.size() * ncols * 8 - rd[q];
+    }
+    halo_rows_sent += (int64_t)srows.size();
+    DArr<int32_t> sr, rr;
+    DArr<double> sbuf, rbuf;
+    sr.upload(srows, s);
+    rr.upload(rrows, s);
+    sbuf.alloc(std::max<int64_t>((int64_t)srows.size() * ncols, 1), s);
+    rbuf.alloc(std::max<int64_t>((int64_t)rrows.size() * ncols, 1), s);
+    launch_rows_move(p, ld, sr.p, (int64_t)srows.size(), ncols, sbuf.p, 0, s);
+    comm_alltoall(comm, sbuf.p, sc, sd, rbuf.p, rc, rd, s);
+    launch_rows_move(p, ld, rr.p, (int64_t)rrows.size(), ncols, rbuf.p, 1, s);
+  }
+
   // Algorithm 1 line 258 (gen_B) with the all-gather of the parent panel's Omega^{l+1} rows
   // (S§8(e); the BSR partners' samples of the next depth) overlapped: the gather runs on a side
   // stream once the shrink is done while B is generated on the build stream (B needs only the

@@ -313,6 +313,9 @@ struct UpdateNsArgs {
 };
 void launch_update_ns(const UpdateNsArgs& a, bool coupling, int grid, cudaStream_t st);
 void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStream_t st);
+// packed row e <-> panel row rows[e] (ncols columns): dir 0 gathers into buf, dir 1 scatters from it
+void launch_rows_move(double* P, int64_t ld, const int32_t* rows, int64_t nrows, int ncols, double* buf, int dir,
+                      cudaStream_t st);
 
 // ---- exact-order mode (exact.cu, --fmad=false): the C oracle's operation order
 void launch_exact_sketch(const KernelParams& kp, const double* X, const double* Yc, const double* Zc, int64_t n,

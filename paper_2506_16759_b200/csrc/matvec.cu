@@ -95,4 +95,29 @@ void launch_scale(double* y, int64_t n, int64_t ld, int q, double beta, cudaStre
   H2_CHECK_LAUNCH();
 }
 
+
+// Row gather / scatter of a row-major panel (the halo exchange of the sharded construction,
+// S§8(e)): packed row e <-> panel row rows[e], ncols columns.  dir 0: out[e] = P[rows[e]]
+// (pack for sending), dir 1: P[rows[e]] = in[e] (unpack after receiving).
+__global__ void __launch_bounds__(256) rows_move_kernel(double* __restrict__ P, int64_t ld, const int32_t* __restrict__ rows,
+                                                        int64_t nrows, int ncols, double* __restrict__ buf, int dir) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ncols;
+    const int c = (int)(e - r * ncols);
+    double* p = P + (int64_t)rows[r] * ld + c;
+    if (dir == 0) buf[e] = *p;
+    else *p = buf[e];
+  }
+}
+
+void launch_rows_move(double* P, int64_t ld, const int32_t* rows, int64_t nrows, int ncols, double* buf, int dir,
+                      cudaStream_t st) {
+  if (nrows <= 0 || ncols <= 0) return;
+  const int64_t total = nrows * ncols;
+  rows_move_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(P, ld, rows, nrows, ncols, buf,
+                                                                                        dir);
+  H2_CHECK_LAUNCH();
+}
+
 }  // namespace h2

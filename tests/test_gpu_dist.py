@@ -174,3 +174,68 @@ def test_in_library_nccl_communicator_single_rank():
     p.join(timeout=120)
     assert err is None, err
     assert ok_ag and same
+
+
+def _halo_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2506_16759_b200 as g
+        from paper_2506_16759_b200.dist import Comm
+        from synth import uniform_points
+        X = uniform_points(n, 3, 3)
+        T = g.Tree(X, 64)
+        comm = Comm()
+        res = {}
+        for halo in ("0", "1"):
+            os.environ["H2_HALO"] = halo
+            b0, a0 = comm.bytes, comm.a2a_bytes
+            Hd = g.build(T, ("exp", 0.2), 1e-6, comm=comm)
+            moved = (comm.bytes - b0) + (comm.a2a_bytes - a0)
+            Hd.allgather(comm)
+            res[halo] = (_snapshot(Hd, g), moved, comm.a2a_bytes - a0)
+        os.environ.pop("H2_HALO")
+        H1 = g.build(T, ("exp", 0.2), 1e-6)
+        ref = _snapshot(H1, g)
+        same = {f"{h}:{k}": bool(np.array_equal(res[h][0][k], ref[k])) for h in res for k in ref}
+        q.put((rank, same, res["0"][1], res["1"][1], res["1"][2]))
+    except Exception as exc:
+        import traceback
+        traceback.print_exc()
+        q.put((rank, {"error": repr(exc)}, 0, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(4, 16384), (8, 32768)])
+def test_halo_exchange_bitwise_and_fewer_bytes(world, n):
+    """Halo-only exchange of the Omega^{l+1} rows (H2_HALO=1, default; S§8(e)): each rank sends a
+    cluster's rows only to the ranks owning one of its far partners (one all-to-all per panel
+    instead of an all-gather).  Both modes are bitwise the one-GPU build, and the halo moves fewer
+    bytes in total (all collectives of the build counted on each rank)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    tot_ag = tot_halo = 0
+    for rank, same, ag, halo, a2a in res:
+        assert "error" not in same, same
+        bad = [k for k, v in same.items() if not v]
+        assert not bad, (rank, bad)
+        assert a2a > 0
+        tot_ag += ag
+        tot_halo += halo
+    assert tot_halo < tot_ag, (tot_halo, tot_ag)
+    print(f"world {world}: bytes sent per build, all-gather mode {tot_ag}, halo mode {tot_halo} "
+          f"({tot_halo / tot_ag:.2f}x)")
