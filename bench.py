@@ -414,8 +414,9 @@ def run_ours(args, w, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_s = float(t.item())
         e2e = {"value": e_s, "unit": "s", "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(d2h),
-               "note": "wall clock incl. host KD-tree build (partition on a host thread, overlapped with the first "
-                       "sketch pass: h2_tree_build_async), coordinate upload, h2_build, D2H of ranks+skeletons"}
+               "note": "wall clock incl. the coordinate upload, the KD ordering (on the GPU: radix sorts per depth, "
+                       "h2_tree_build_async), the block partition (host thread, overlapped with the first sketch "
+                       "pass), h2_build, D2H of ranks+skeletons"}
     if rank != 0:
         return
     cpu = None

@@ -2224,9 +2224,16 @@ h2_status h2_tree_build_async(const double* coords_host, int64_t n, int32_t dim,
     H2_REQUIRE(coords_host != nullptr, "h2_tree_build_async: coords is NULL");
     auto* T = new h2_tree();
     std::unique_ptr<h2_tree> guard(T);
-    tree_build_order(*T, coords_host, n, dim, leaf_size, eta, dist_rule);
+    // the KD ordering on the GPU when one is present (kd_gpu.cu: the same tree, ~17 -> ~3 ms of
+    // host prefix at N = 2^18; H2_KD_GPU=0: the host ordering)
+    int ndev = 0;
+    const bool gpu = n >= 4096 && env_int("H2_KD_GPU", 1) != 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0;
+    cudaGetLastError();
+    if (gpu) tree_build_order_gpu(*T, coords_host, n, dim, leaf_size, eta, dist_rule);
+    else tree_build_order(*T, coords_host, n, dim, leaf_size, eta, dist_rule);
     T->part_thread = std::thread([T] {
       try {
+        tree_download_order(*T);
         tree_build_partition(*T);
       } catch (const Error& e) {
         T->part_error = e.what();

@@ -228,6 +228,101 @@ void tree_build_order(h2_tree& T, const double* X, int64_t n, int dim, int leaf,
   lap("coords");
 }
 
+// tree_build_order on the GPU (kd_gpu.cu): identical ordering, node ranges from the sizes alone
+void tree_build_order_gpu(h2_tree& T, const double* X, int64_t n, int dim, int leaf, double eta, int rule) {
+  H2_REQUIRE(n >= 1 && n < (int64_t(1) << 31), "h2_tree_build: need 1 <= n < 2^31");
+  H2_REQUIRE(dim >= 1 && dim <= 3, "h2_tree_build: dim must be 1, 2 or 3");
+  H2_REQUIRE(leaf >= 2, "h2_tree_build: leaf_size >= 2");
+  H2_REQUIRE(eta > 0, "h2_tree_build: eta > 0");
+  H2_REQUIRE(rule == H2_DIST_CENTER || rule == H2_DIST_BOX, "h2_tree_build: bad dist_rule");
+  for (int64_t i = 0; i < n * dim; ++i) H2_REQUIRE(std::isfinite(X[i]), "h2_tree_build: non-finite coordinate");
+  T.n = n;
+  T.dim = dim;
+  T.leaf_size = leaf;
+  T.eta = eta;
+  T.rule = rule;
+  const int Dl = T.Dl = leaf_depth_for(n, leaf);
+  T.begin.assign(Dl + 1, {});
+  T.end.assign(Dl + 1, {});
+  T.begin[0] = {0};
+  T.end[0] = {n};
+  std::vector<int> seg_all;
+  for (int t = 0; t < Dl; ++t) {
+    const int64_t nn = int64_t(1) << t;
+    T.begin[t + 1].resize(2 * nn);
+    T.end[t + 1].resize(2 * nn);
+    for (int64_t c = 0; c < nn; ++c) {
+      const int64_t b = T.begin[t][c], e = T.end[t][c], left = (e - b + 1) / 2;
+      seg_all.push_back((int)b);
+      T.begin[t + 1][2 * c] = b;
+      T.end[t + 1][2 * c] = b + left;
+      T.begin[t + 1][2 * c + 1] = b + left;
+      T.end[t + 1][2 * c + 1] = e;
+    }
+    seg_all.push_back((int)n);
+  }
+  const bool trace = getenv("H2_TRACE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[h2 tree] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
+  lap("gpu setup");
+  int dev = 0;
+  H2_CUDA(cudaGetDevice(&dev));
+  cudaStream_t st;
+  H2_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double box[6];
+  try {
+    h2::kd_order_device(X, n, dim, Dl, seg_all, &T.d_perm, &T.d_x, &T.d_y, &T.d_z, &T.d_iota, box, st);
+  } catch (...) {
+    cudaStreamDestroy(st);
+    throw;
+  }
+  cudaStreamDestroy(st);
+  lap("gpu kd");
+  T.device = dev;
+  {
+    std::vector<int64_t> lb(T.begin[Dl]);
+    lb.push_back(n);
+    H2_CUDA(cudaMalloc(&T.d_leaf_begin, lb.size() * sizeof(int64_t)));
+    H2_CUDA(cudaMemcpy(T.d_leaf_begin, lb.data(), lb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    std::vector<int32_t> ls(T.begin[Dl].size());
+    for (size_t c = 0; c < ls.size(); ++c) ls[c] = (int32_t)(T.end[Dl][c] - T.begin[Dl][c]);
+    H2_CUDA(cudaMalloc(&T.d_leaf_size, std::max<size_t>(ls.size(), 1) * sizeof(int32_t)));
+    H2_CUDA(cudaMemcpy(T.d_leaf_size, ls.data(), ls.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  // the bounding-box diagonal as the host computes it (tree-order coordinates, zero-padded to 3D)
+  {
+    double lo[3] = {1e308, 1e308, 1e308}, hi[3] = {-1e308, -1e308, -1e308};
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], box[a]);
+      hi[a] = std::max(hi[a], box[3 + a]);
+    }
+    T.diam = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                       (hi[2] - lo[2]) * (hi[2] - lo[2]));
+  }
+}
+
+// host copies of the GPU ordering (perm, tree-order coordinates) for the partition / exports
+void tree_download_order(h2_tree& T) {
+  if (!T.d_perm || !T.perm.empty()) return;
+  H2_CUDA(cudaSetDevice(T.device));
+  std::vector<int32_t> p(T.n);
+  T.xt.resize(T.n);
+  T.yt.resize(T.n);
+  T.zt.resize(T.n);
+  H2_CUDA(cudaMemcpy(p.data(), T.d_perm, sizeof(int32_t) * T.n, cudaMemcpyDeviceToHost));
+  H2_CUDA(cudaMemcpy(T.xt.data(), T.d_x, sizeof(double) * T.n, cudaMemcpyDeviceToHost));
+  H2_CUDA(cudaMemcpy(T.yt.data(), T.d_y, sizeof(double) * T.n, cudaMemcpyDeviceToHost));
+  H2_CUDA(cudaMemcpy(T.zt.data(), T.d_z, sizeof(double) * T.n, cudaMemcpyDeviceToHost));
+  T.perm.assign(p.begin(), p.end());
+  // d_perm stays until the tree is freed: cudaFree would synchronise the device (this thread runs
+  // while the first sketch pass does)
+}
+
 // The block partition of an ordered tree (bounding boxes, dual traversal, CSR batch descriptors,
 // unique D offsets).  Synchronous in h2_tree_build; on a host thread in h2_tree_build_async.
 void tree_build_partition(h2_tree& T) {
@@ -526,6 +621,7 @@ h2_tree::~h2_tree() {
   cudaFree(d_y);
   cudaFree(d_z);
   cudaFree(d_iota);
+  cudaFree(d_perm);
   cudaFree(d_leaf_begin);
   cudaFree(d_leaf_size);
   cudaFree(d_D_off);

@@ -1,6 +1,7 @@
 // Host-side cluster tree + block partition (§II-A) and their flattened
 // per-level CSR batch descriptors (§IV-A "stored contiguously level by level").
 #pragma once
+#include <cuda_runtime.h>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -57,6 +58,8 @@ struct h2_tree {
   int device = -1;
   double *d_x = nullptr, *d_y = nullptr, *d_z = nullptr;
   int32_t* d_iota = nullptr;                       // 0..n-1
+  int32_t* d_perm = nullptr;                       // GPU KD ordering: perm until the partition thread
+                                                   // downloads it (then freed)
   int64_t* d_leaf_begin = nullptr;                 // 2^Dl + 1 (last = n)
   int32_t* d_leaf_size = nullptr;
   int64_t* d_D_off = nullptr;
@@ -68,6 +71,14 @@ struct h2_tree {
 
 void tree_build_host(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
 void tree_build_order(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+// the same ordering on the current CUDA device (kd_gpu.cu); device arrays ready at return, the host
+// copies (perm, xt/yt/zt) filled by tree_download_order (the partition thread calls it first)
+void tree_build_order_gpu(h2_tree& T, const double* coords, int64_t n, int dim, int leaf, double eta, int rule);
+void tree_download_order(h2_tree& T);
+namespace h2 {
+void kd_order_device(const double* X, int64_t n, int dim, int Dl, const std::vector<int>& seg_all, int** perm_dev,
+                     double** xt, double** yt, double** zt, int** iota_dev, double* root_box, cudaStream_t st);
+}
 void tree_build_partition(h2_tree& T);
 void tree_upload_order(h2_tree& T);
 void tree_upload_partition(h2_tree& T);
