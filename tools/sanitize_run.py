@@ -15,7 +15,7 @@ from synth import uniform_points, grid_points
 
 X = uniform_points(5000, 3, 0)
 T = g.Tree(X, 64)
-for variant in ("warp", "smem", "global"):
+for variant in ("warp", "smem", "global", "cluster"):
     os.environ["H2_CQ_VARIANT"] = variant
     H = g.build(T, ("exp", 0.2), 1e-6, d_init=16, d_blk=16)
     print(variant, "samples", H.samples, "cpqr_variants", H.stats["cpqr_variants"], flush=True)
@@ -28,5 +28,7 @@ Y2 = g.dense_sketch(T, Om[:, :45].contiguous(), ("exp", 0.2), omega_quarters=Tru
 Tg = g.Tree(grid_points((12, 12, 12), 1 / 12), 64)
 Hh = g.build(Tg, ("helmholtz", 3.0), 1e-4)                        # 7-slice Helmholtz pass
 He = g.build(g.Tree(uniform_points(1500, 3, 1), 64), ("rational", 0.3), 1e-6, exact_order=1)
+Ta = g.Tree(uniform_points(9000, 3, 2), 64, asynchronous=True)     # GPU KD ordering
+Ha = g.build(Ta, ("exp", 0.2), 1e-6)
 torch.cuda.synchronize()
-print("ok", float(y.norm()), float(Y.norm()), float(Y2.norm()), Hh.samples, He.samples, flush=True)
+print("ok", float(y.norm()), float(Y.norm()), float(Y2.norm()), Hh.samples, He.samples, Ha.samples, flush=True)
