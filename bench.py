@@ -435,7 +435,8 @@ def run_ours(args, w, rank, world, local_rank):
                    "eps_rule": "s*tol*rho*gamma^(Dl-t), s=0.04, gamma=1.25 (DESIGN.md R31)",
                    "sketch_format": "int8 tcgen05, 6-byte fixed-point K (2^-47 grid), 160-column pass (R32)",
                    "parallelism": (f"subtree shards x{world} (sketch rows, clusters per level; "
-                                   f"{'in-library NCCL' if dist and dist.get_backend() == 'nccl' else 'gloo'} all-gathers"
+                                   f"{'in-library NCCL' if dist and dist.get_backend() == 'nccl' else 'gloo'} "
+                                   f"all-gathers of ranks / skeletons + halo all-to-all of Omega rows"
                                    f"{'' if dist and dist.get_backend() == 'nccl' else ', ranks share a GPU'})")
                    if world > 1 else "1 GPU",
                    "l2": "256 MiB flush before every timed step; working set (N x d_max x 16 B = 2 GiB) > L2"},
