@@ -1340,8 +1340,17 @@ int launch_cpqr(const CpqrArgs& a, cudaStream_t st) {
   // measured at C2 (ncu, profiles/r2_cpqr_cluster.md): faster on levels with few panels (32 / 64:
   // 1.17 -> 0.76, 1.31 -> 0.93 ms), slower once 2 CTAs per panel exceed the SMs (128-1024 panels)
   const bool few_panels = 2 * a.nclusters <= 148;
-  if ((force == H2_CQ_V_CLUSTER || (force == 0 && clus != 0 && !fits1 && (few_panels || clus == 2))) &&
+  if ((force == H2_CQ_V_CLUSTER || (force == 0 && clus != 0 && !fits1 && (few_panels || clus >= 2))) &&
       a.max_m >= 2) {
+    // H2_CQ_CLUSTER=4 (A/B): 4 CTAs x 256 threads per panel on every level it is used (smaller
+    // CTAs: several clusters per SM on the many-panel levels)
+    // default: 4 x 256 when the level's clusters fit twice over the SMs (<= 74 panels: depths 5-6
+    // of C2, 0.73 -> 0.57 / 0.90 -> 0.79 ms), else 2 x 512
+    if ((clus == 4 || (clus == 1 && force == 0 && 4 * a.nclusters <= 2 * 148)) && cqc_smem(a, 4) <= 210 * 1024) {
+      cpqr_cluster_launch<4, 256>(a, cqc_smem(a, 4), st);
+      H2_CHECK_LAUNCH();
+      return H2_CQ_V_CLUSTER;
+    }
     if (cqc_smem(a, 2) <= 210 * 1024) {
       cpqr_cluster_launch<2, 512>(a, cqc_smem(a, 2), st);
       H2_CHECK_LAUNCH();
