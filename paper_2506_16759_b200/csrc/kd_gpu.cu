@@ -85,12 +85,92 @@ __global__ void __launch_bounds__(256) kd_level_kernel(const double* __restrict_
   }
 }
 
-// node id of every position (the nodes of a depth are contiguous position ranges): segid of the
-// point at position p, written at its ORIGINAL index
+// node id of every position (the nodes of a depth are contiguous position ranges, found by binary
+// search over the offsets): segid of the point at position p, written at its ORIGINAL index
 __global__ void kd_segid_kernel(const int* __restrict__ seg, int nseg, const int* __restrict__ idx, int n,
                                 int* __restrict__ segid_orig) {
-  for (int c = blockIdx.x; c < nseg; c += gridDim.x)
-    for (int p = seg[c] + threadIdx.x; p < seg[c + 1]; p += blockDim.x) segid_orig[idx[p]] = c;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg;   // seg[lo] <= p < seg[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (seg[mid] <= p) lo = mid;
+      else hi = mid;
+    }
+    segid_orig[idx[p]] = lo;
+  }
+}
+
+// two-stage node boxes for depths with few, large nodes: CTA (s, c) reduces slice s of node c to a
+// partial box (exact min / max, order-free) ...
+__global__ void __launch_bounds__(256) kd_box_partial_kernel(const double* __restrict__ X, int dim,
+                                                             const int* __restrict__ seg, const int* __restrict__ idx,
+                                                             int S, double* __restrict__ part) {
+  __shared__ double slo[3][8], shi[3][8];
+  const int c = blockIdx.y, sl = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = seg[c], e0 = seg[c + 1];
+  const int64_t len = e0 - b0;
+  const int b = b0 + (int)(len * sl / S), e = b0 + (int)(len * (sl + 1) / S);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int p = b + threadIdx.x; p < e; p += blockDim.x) {
+    const double* x = X + (int64_t)idx[p] * dim;
+    for (int a = 0; a < dim; ++a) {
+      lo[a] = fmin(lo[a], x[a]);
+      hi[a] = fmax(hi[a], x[a]);
+    }
+  }
+  for (int a = 0; a < dim; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if (lane == 0) {
+      slo[a][warp] = lo[a];
+      shi[a][warp] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int a = threadIdx.x;
+    double L = INFINITY, H = -INFINITY;
+    if (a < dim)
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        L = fmin(L, slo[a][w]);
+        H = fmax(H, shi[a][w]);
+      }
+    double* o = part + ((int64_t)c * S + sl) * 6;
+    o[a] = L;
+    o[3 + a] = H;
+  }
+}
+
+// ... and one thread per node merges its S partials and picks the axis (as the host)
+__global__ void kd_axis_kernel(const double* __restrict__ part, int nseg, int S, int dim, int* __restrict__ axis_out,
+                               double* __restrict__ box) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nseg; c += gridDim.x * blockDim.x) {
+    double L[3] = {INFINITY, INFINITY, INFINITY}, Hh[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int sl = 0; sl < S; ++sl) {
+      const double* o = part + ((int64_t)c * S + sl) * 6;
+      for (int a = 0; a < dim; ++a) {
+        L[a] = fmin(L[a], o[a]);
+        Hh[a] = fmax(Hh[a], o[3 + a]);
+      }
+    }
+    int axis = 0;
+    double best = Hh[0] - L[0];
+    for (int a = 1; a < dim; ++a)
+      if (Hh[a] - L[a] > best) {
+        best = Hh[a] - L[a];
+        axis = a;
+      }
+    if (axis_out) axis_out[c] = axis;
+    if (box)
+      for (int a = 0; a < 3; ++a) {
+        box[a] = a < dim ? L[a] : 0.0;
+        box[3 + a] = a < dim ? Hh[a] : 0.0;
+      }
+  }
 }
 
 // keys in ORIGINAL order: the coordinate of point o on its node's axis; values o
@@ -161,22 +241,34 @@ void kd_order_device(const double* X, int64_t n64, int dim, int Dl, const std::v
     tmp_bytes = std::max<size_t>(need, 16);
     tmp = cache_alloc(tmp_bytes, st);
   };
+  // node boxes -> axes: one CTA per node when there are many nodes, else S CTAs per node and a
+  // merge (the top depths hold few nodes of up to n points)
+  const int SMAX = 296;
+  double* part = static_cast<double*>(cache_alloc(sizeof(double) * 6 * SMAX, st));
+  auto boxes = [&](const int* sg, int nseg, int* ax, double* box) {
+    if (nseg >= 148) {
+      kd_level_kernel<<<std::min(nseg, 148 * 8), 256, 0, st>>>(dX, dim, sg, nseg, idx, ax, box);
+    } else {
+      const int S = SMAX / nseg;
+      kd_box_partial_kernel<<<dim3(S, nseg), 256, 0, st>>>(dX, dim, sg, idx, S, part);
+      H2_CHECK_LAUNCH();
+      kd_axis_kernel<<<1, 256, 0, st>>>(part, nseg, S, dim, ax, box);
+    }
+    H2_CHECK_LAUNCH();
+  };
   {   // the root box (the diameter; also the only "level" when Dl = 0)
     std::vector<int> root{0, n};
     int* rseg = static_cast<int*>(cache_alloc(sizeof(int) * 2, st));
     H2_CUDA(cudaMemcpyAsync(rseg, root.data(), sizeof(int) * 2, cudaMemcpyHostToDevice, st));
-    kd_level_kernel<<<1, 256, 0, st>>>(dX, dim, rseg, 1, idx, nullptr, dbox);
-    H2_CHECK_LAUNCH();
+    boxes(rseg, 1, nullptr, dbox);
     cache_free(rseg, st);
   }
   size_t off = 0;
   for (int t = 0; t < Dl; ++t) {
     const int nseg = 1 << t;
     const int* sg = seg + off;
-    const int gseg = std::min(nseg, 148 * 8);
-    kd_level_kernel<<<gseg, 256, 0, st>>>(dX, dim, sg, nseg, idx, axis, nullptr);   // (1) axes
-    H2_CHECK_LAUNCH();
-    kd_segid_kernel<<<gseg, 256, 0, st>>>(sg, nseg, idx, n, segid);
+    boxes(sg, nseg, axis, nullptr);   // (1) axes
+    kd_segid_kernel<<<grid1, 256, 0, st>>>(sg, nseg, idx, n, segid);
     H2_CHECK_LAUNCH();
     kd_keys_kernel<<<grid1, 256, 0, st>>>(dX, dim, segid, axis, n, key[0], val[0]);
     H2_CHECK_LAUNCH();
@@ -214,6 +306,7 @@ void kd_order_device(const double* X, int64_t n64, int dim, int Dl, const std::v
   cache_free(segid, st);
   cache_free(axis, st);
   cache_free(dbox, st);
+  cache_free(part, st);
   cache_free(seg, st);
   cache_free(dX, st);
 }
