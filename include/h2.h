@@ -410,12 +410,23 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
  * a level converges when every cluster of both sides passes the test.  Operators: sketch
  * H2_S_DENSE_MATRIX (Z via A^T, cuBLAS), H2_S_CALLBACK (called with req->transpose = 0 and 1)
  * or H2_S_DENSE_KERNEL (the built-in kernels are symmetric: Z = K Psi); entry H2_E_BUILTIN,
- * H2_E_CALLBACK or H2_E_DENSE_MATRIX.  One GPU.  The result works with h2_matvec (upward pass
+ * H2_E_CALLBACK or H2_E_DENSE_MATRIX.  One GPU (h2_build_nonsym_dist: sharded).  The result works with h2_matvec (upward pass
  * with V, couplings, downward pass with U) and h2_export: H2_X_RANK/SKEL/BASIS/CERT give the row
  * side, H2_X_*_C the column side; D and B are stored for every ORDERED pair (s, b) in (s, b)
  * order, D_{s,b} m_s x m_b, B_{s,b} = K(I~_s, J~_b) k_s x kc_b.  Errors as h2_build. */
 h2_status h2_build_nonsym(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
                           const h2_build_opts* opts, void* stream, h2_matrix** out, h2_build_stats* stats);
+/* The non-symmetric construction over a communicator (SURVEY §8(e) applied to NEXT #3): cluster
+ * ownership, sharded sketch rows (Y and Z rows of the owned leaves; Omega and Psi regenerated on
+ * every rank), owned-cluster BSR / CPQR-ID / shrink on both sides, the ordered D / B blocks with an
+ * owned endpoint, per-level all-gathers of ranks and skeletons of both sides and the halo (or
+ * all-gather) exchange of both sides' projected samples.  A callback sketch is called for the
+ * rank's rows (row split only).  The result is partial until h2_matrix_allgather (bases,
+ * certificates, ordered B and D by the owner of the row cluster); bitwise the one-GPU
+ * h2_build_nonsym.  Arguments and errors as h2_build_nonsym and h2_build_dist. */
+h2_status h2_build_nonsym_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                               const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                               h2_build_stats* stats);
 
 /* Collective: all-gather bases X, certificates, B and D so that every rank holds the full
  * matrix (segments by owner of the cluster / of the stored block's row cluster). */

@@ -404,6 +404,17 @@ struct Builder {
     return l;
   }
 
+  // ordered pairs e (row os[e], column F.idx[e]) with an owned endpoint: the blocks a rank's row
+  // and column BSRs read in the non-symmetric construction
+  std::vector<int32_t> owned_ordered(const PairCSR& F, const std::vector<int32_t>& os, int t) const {
+    std::vector<int32_t> l;
+    for (int64_t e = 0; e < F.nnz(); ++e) {
+      const int a = os[e], b = F.idx[e];
+      if ((a >= cb(t) && a < ce(t)) || (b >= cb(t) && b < ce(t))) l.push_back((int32_t)e);
+    }
+    return l;
+  }
+
   // all-gather rows [roff_r, roff_{r+1}) (per rank) of a row-major panel, columns [0, ncols)
   void allgather_rows(double* p, int64_t ld, int ncols, const std::vector<int64_t>& rowb, int64_t nrows,
                       cudaStream_t s = nullptr) {
@@ -438,13 +449,13 @@ struct Builder {
   // rows of its cluster b to rank q iff b has a far partner owned by q (S§8(e): ~0.4x the
   // all-gather bytes at P = 8).  H2_HALO=0: every rank's rows to every rank (all-gather).
   int64_t halo_rows_sent = 0;
-  void allgather_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s = nullptr) {
+  void allgather_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s = nullptr, int sd = 0) {
     if (!comm) return;
     if (ncols > 0 && (comm->alltoallv || comm->nccl) && env_int("H2_HALO", 1) != 0) {
-      halo_skel_rows(u, p, ld, ncols, s ? s : st);
+      halo_skel_rows(u, p, ld, ncols, s ? s : st, sd);
       return;
     }
-    const Level& L = H.L(u);
+    const Level& L = H.S(sd, u);
     std::vector<int64_t> rowb(P + 1);
     for (int r = 0; r <= P; ++r) {
       const int c = own_begin(u, r, P);
@@ -452,8 +463,8 @@ struct Builder {
     }
     allgather_rows(p, ld, ncols, rowb, L.rtot, s);
   }
-  void halo_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s) {
-    const Level& L = H.L(u);
+  void halo_skel_rows(int u, double* p, int64_t ld, int ncols, cudaStream_t s, int side = 0) {
+    const Level& L = H.S(side, u);
     const PairCSR& F = T.far[u];
     const int n = L.nclus;
     auto owner = [&](int c) { return (int)((int64_t)c * P / n); };
@@ -1436,19 +1447,22 @@ struct Builder {
     timer.end();
     timer.begin(H2_PH_SKETCH);
     sketch_columns += nc;
+    // under a communicator: this rank's leaf rows of Y and Z (Omega / Psi regenerated for all rows)
+    const int64_t r0 = row_b(), r1 = row_e();
     for (int tr = 0; tr < 2; ++tr) {
       const double* in = tr ? Ps : Om;
       const int64_t ldi = tr ? ldr : ldc;
       double* out = tr ? Z : Y;
       const int64_t ldo = tr ? ldc : ldr;
       if (S.kind == H2_S_DENSE_KERNEL) {   // the built-in kernels are symmetric: K^T Psi = K Psi
-        launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, 0, T.n, in, ldi, nc, out, ldo, true, st);
-        entries_sketch += T.n * T.n * (int64_t)div_up(nc, 64);
+        launch_dense_sketch(skp, T.d_x, T.d_y, T.d_z, T.n, r0, r1, in, ldi, nc, out + r0 * ldo, ldo, true, st);
+        entries_sketch += (r1 - r0) * T.n * (int64_t)div_up(nc, 64);
       } else if (S.kind == H2_S_DENSE_MATRIX) {
-        dense_matrix_sketch(S.A, S.ld_A, T.n, 0, T.n, in, ldi, nc, out, ldo, st, tr == 1);
+        dense_matrix_sketch(S.A, S.ld_A, T.n, r0, r1, in, ldi, nc, out + r0 * ldo, ldo, st, tr == 1);
       } else if (S.kind == H2_S_H2_LOWRANK) {
-        // M = A_H + U V^T (A_H symmetric): Y = A_H Omega + U (V^T Omega), Z = A_H Psi + V (U^T Psi)
-        matvec_impl(*S.base, in, ldi, out, ldo, nc, 1.0, 0.0, st);
+        // M = A_H + U V^T (A_H symmetric): Y = A_H Omega + U (V^T Omega), Z = A_H Psi + V (U^T Psi);
+        // row-sharded matvec of the complete base under a communicator
+        matvec_impl(*S.base, in, ldi, out, ldo, nc, 1.0, 0.0, st, R, P);
         if (S.rank > 0) {
           const double* V = S.V ? S.V : S.U;
           const int64_t ldv = S.V ? S.ld_V : S.ld_U;
@@ -1460,13 +1474,13 @@ struct Builder {
       } else {
         h2_sketch_req rq{};
         rq.n = T.n;
-        rq.row_begin = 0;
-        rq.row_end = T.n;
+        rq.row_begin = r0;
+        rq.row_end = r1;
         rq.col0 = c0;
         rq.ncols = nc;
         rq.omega = in;
         rq.ld_omega = ldi;
-        rq.y = out;
+        rq.y = out + r0 * ldo;
         rq.ld_y = ldo;
         rq.stream = st;
         rq.transpose = tr;
@@ -1478,9 +1492,12 @@ struct Builder {
     timer.begin(H2_PH_MISC);
     const int nleaf = 1 << T.Dl;
     if (leaf_part.n < nleaf) leaf_part.alloc(nleaf, st);
-    launch_sumsq_leaf(Y, T.d_leaf_begin, 0, nleaf, ldr, 0, nc, leaf_part.p, st);
+    // per-leaf partials of the owned leaves, all-gathered, summed in leaf order (R10)
+    launch_sumsq_leaf(Y, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ldr, 0, nc, leaf_part.p, st);
+    if (comm) comm_allgather_clusters(comm, leaf_part.p, 8, T.Dl, [](int c) { return (int64_t)c; }, st);
     launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
-    launch_sumsq_leaf(Z, T.d_leaf_begin, 0, nleaf, ldc, 0, nc, leaf_part.p, st);
+    launch_sumsq_leaf(Z, T.d_leaf_begin, cb(T.Dl), ce(T.Dl), ldc, 0, nc, leaf_part.p, st);
+    if (comm) comm_allgather_clusters(comm, leaf_part.p, 8, T.Dl, [](int c) { return (int64_t)c; }, st);
     launch_sumsq_total(leaf_part.p, nleaf, sumsq_acc.p, nonfinite.p, st);
     timer.end();
   }
@@ -1491,10 +1508,10 @@ struct Builder {
     BsrArgs a{};
     a.c0 = 0;
     a.ncols = nc;
-    a.c_begin = 0;
     a.tmode = sd ? 2 : 1;
+    a.c_begin = cb(t == T.Dl ? T.Dl : t + 1);   // owned row clusters (all on one GPU)
+    a.nclusters = ce(t == T.Dl ? T.Dl : t + 1) - a.c_begin;
     if (t == T.Dl) {
-      a.nclusters = 1 << T.Dl;
       a.max_rows = H.L(T.Dl).max_m;
       a.yoff = a.ooff = T.d_leaf_begin;
       a.cnt = T.d_leaf_size;
@@ -1506,7 +1523,6 @@ struct Builder {
     } else {
       const Level& Ls = H.S(sd, t + 1);
       const Level& Lo = H.S(1 - sd, t + 1);
-      a.nclusters = 1 << (t + 1);
       a.max_rows = Ls.max_k;
       a.yoff = Ls.d_roff.p;
       a.ooff = Lo.d_roff.p;
@@ -1536,6 +1552,12 @@ struct Builder {
     H.D.alloc(H.D_off.back(), st);
     GenArgs g{};
     g.nblocks = F.nnz();
+    DArr<int32_t> ul;
+    if (comm) {
+      ul.upload(owned_ordered(F, near_o.os, T.Dl), st);
+      g.ulist = ul.p;
+      g.nblocks = ul.n;
+    }
     g.us = near_o.d_os.p;
     g.ub = T.d_near.idx;
     g.cnt = T.d_leaf_size;
@@ -1546,7 +1568,8 @@ struct Builder {
     if (E.kind == H2_E_H2_LOWRANK) {   // D_A (unique, transposed for s > b) + U(I_s) V(I_b)^T
       timer.begin(H2_PH_GEN);
       UpdateNsArgs a{};
-      a.nblocks = F.nnz();
+      a.nblocks = g.nblocks;
+      a.ulist = g.ulist;
       a.os = near_o.d_os.p;
       a.ob = T.d_near.idx;
       a.uidx = T.d_near.uidx;
@@ -1562,7 +1585,7 @@ struct Builder {
       a.V = E.V ? E.V : E.U;
       a.ldv = E.V ? E.ld_V : E.ld_U;
       a.r = E.rank;
-      launch_update_ns(a, false, (int)std::min<int64_t>(F.nnz(), 148 * 8), st);
+      launch_update_ns(a, false, (int)std::min<int64_t>(std::max<int64_t>(a.nblocks, 1), 148 * 8), st);
       timer.end();
       return;
     }
@@ -1580,6 +1603,12 @@ struct Builder {
     L.B.alloc(L.B_off.back(), st);
     GenArgs g{};
     g.nblocks = F.nnz();
+    DArr<int32_t> ul;
+    if (comm) {
+      ul.upload(owned_ordered(F, far_o[t].os, t), st);
+      g.ulist = ul.p;
+      g.nblocks = ul.n;
+    }
     g.us = far_o[t].d_os.p;
     g.ub = T.d_far[t].idx;
     g.cnt = L.d_k.p;
@@ -1602,11 +1631,12 @@ struct Builder {
       int64_t gmax = 1;
       for (int64_t e = 0; e < F.nnz(); ++e)
         gmax = std::max<int64_t>(gmax, (int64_t)La.k[far_o[t].os[e]] * C.k[F.idx[e]]);
-      const int grid = (int)std::min<int64_t>(F.nnz(), 148 * 4);
+      const int grid = (int)std::min<int64_t>(std::max<int64_t>(g.nblocks, 1), 148 * 4);
       DArr<double> scratch;
       scratch.alloc(gmax * grid, st);
       UpdateNsArgs a{};
-      a.nblocks = F.nnz();
+      a.nblocks = g.nblocks;
+      a.ulist = g.ulist;
       a.os = far_o[t].d_os.p;
       a.ob = T.d_far[t].idx;
       a.uidx = T.d_far[t].uidx;
@@ -1664,6 +1694,8 @@ struct Builder {
       if (u - 1 == t) {
         shrink(u, sr.Y.p, sr.O.p, sr.ld, cur.Y.p + c0, cur.O.p + c0, cur.ld, b, 0);
         shrink(u, sc.Y.p, sc.O.p, sc.ld, curc.Y.p + c0, curc.O.p + c0, curc.ld, b, 1);
+        allgather_skel_rows(u, cur.O.p + c0, cur.ld, b, nullptr, 0);
+        allgather_skel_rows(u, curc.O.p + c0, curc.ld, b, nullptr, 1);
         ns_bsr_both(t, cur, curc, c0, b);
       } else {
         Panel dr, dc;
@@ -1671,6 +1703,8 @@ struct Builder {
         dc.alloc(H.C(u).rtot, b, st);
         shrink(u, sr.Y.p, sr.O.p, sr.ld, dr.Y.p, dr.O.p, dr.ld, b, 0);
         shrink(u, sc.Y.p, sc.O.p, sc.ld, dc.Y.p, dc.O.p, dc.ld, b, 1);
+        allgather_skel_rows(u, dr.O.p, dr.ld, b, nullptr, 0);
+        allgather_skel_rows(u, dc.O.p, dc.ld, b, nullptr, 1);
         ns_bsr_both(u - 1, dr, dc, 0, b);
         sr = std::move(dr);
         sc = std::move(dc);
@@ -1751,6 +1785,9 @@ struct Builder {
         nc.alloc(C.rtot, ld_for(C.rtot, d), st);
         shrink(t, cur.Y.p, cur.O.p, cur.ld, nr.Y.p, nr.O.p, nr.ld, d, 0);
         shrink(t, curc.Y.p, curc.O.p, curc.ld, nc.Y.p, nc.O.p, nc.ld, d, 1);
+        // the other side's BSR partners' projected samples (S§8(e); halo or all-gather)
+        allgather_skel_rows(t, nr.O.p, nr.ld, d, nullptr, 0);
+        allgather_skel_rows(t, nc.O.p, nc.ld, d, nullptr, 1);
       }
       ns_gen_B(t);                                                         // line 258, ordered pairs
       cur = std::move(nr);
@@ -2611,6 +2648,12 @@ h2_status h2_build_nonsym(const h2_tree* tree, const h2_sketch* sketch, const h2
   return build_impl(tree, sketch, entry, tol, opts, nullptr, stream, out, stats, true);
 }
 
+h2_status h2_build_nonsym_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_entry* entry, double tol,
+                               const h2_build_opts* opts, const h2_comm* comm, void* stream, h2_matrix** out,
+                               h2_build_stats* stats) {
+  return build_impl(tree, sketch, entry, tol, opts, comm, stream, out, stats, true);
+}
+
 h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream) {
   try {
     H2_REQUIRE(H, "h2_matrix_allgather: NULL matrix");
@@ -2633,6 +2676,31 @@ h2_status h2_matrix_allgather(h2_matrix* H, const h2_comm* comm, void* stream) {
       }
       comm_allgather(comm, base, cnt, dsp, st);
     };
+    if (H->nonsym) {
+      // ordered pairs e in CSR order (sorted by the row cluster s): rank r's rows are the entries
+      // [ptr[own_begin(r)], ptr[own_begin(r+1)])
+      auto ordered_ranges = [&](const PairCSR& F, int t, const std::vector<int64_t>& off, double* base) {
+        std::vector<int64_t> cnt(P), dsp(P);
+        for (int r = 0; r < P; ++r) {
+          const int64_t e0 = F.ptr[own_begin(t, r, P)], e1 = F.ptr[own_begin(t, r + 1, P)];
+          dsp[r] = off[e0] * 8;
+          cnt[r] = (off[e1] - off[e0]) * 8;
+        }
+        comm_allgather(comm, base, cnt, dsp, st);
+      };
+      for (int t = H->top; t <= H->Dl; ++t) {
+        for (int sd = 0; sd < 2; ++sd) {
+          Level& L = H->S(sd, t);
+          comm_allgather_clusters(comm, L.X.p, 8, t, [&](int c) { return c < L.nclus ? L.xoff[c] : L.xtot; }, st);
+          comm_allgather_clusters(comm, L.cert.p, 16, t, [](int c) { return (int64_t)c; }, st);
+        }
+        if (T.far[t].nnz() > 0) ordered_ranges(T.far[t], t, H->L(t).B_off, H->L(t).B.p);
+      }
+      ordered_ranges(T.near, T.Dl, H->D_off, H->D.p);
+      H2_CUDA(cudaStreamSynchronize(st));
+      H->partial = false;
+      return H2_OK;
+    }
     for (int t = H->top; t <= H->Dl; ++t) {
       Level& L = H->L(t);
       comm_allgather_clusters(comm, L.X.p, 8, t, [&](int c) { return c < L.nclus ? L.xoff[c] : L.xtot; }, st);

@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(256) update_B_kernel(UpdateBArgs a) {
 // non-symmetric update M = A_H + U V^T, ordered pairs (h2_build_nonsym):
 //   D_{s,b} = D_A(s,b) + U(I_s) V(I_b)^T, D_A(s,b) read from A's unique storage (transposed if s > b)
 __global__ void __launch_bounds__(256) update_D_ns_kernel(UpdateNsArgs a) {
-  for (int64_t e = blockIdx.x; e < a.nblocks; e += gridDim.x) {
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t e = a.ulist ? a.ulist[q] : q;
     const int s = a.os[e], b = a.ob[e];
     const int ms = a.cnt[s], mb = a.cnt[b];
     const int64_t u = a.uidx[e];
@@ -279,7 +280,8 @@ __global__ void __launch_bounds__(256) update_D_ns_kernel(UpdateNsArgs a) {
 //   new row / column skeletons (launch_expand_rows), B_A(s,b) transposed from storage if s > b
 __global__ void __launch_bounds__(256) update_B_ns_kernel(UpdateNsArgs a) {
   double* G = a.scratch + (int64_t)blockIdx.x * a.gmax;
-  for (int64_t e = blockIdx.x; e < a.nblocks; e += gridDim.x) {
+  for (int64_t q = blockIdx.x; q < a.nblocks; q += gridDim.x) {
+    const int64_t e = a.ulist ? a.ulist[q] : q;
     const int s = a.os[e], b = a.ob[e];
     const int kns = a.cnt[s], knb = a.cnt2[b], kbs = a.kb[s], kbb = a.kb[b];
     const int64_t u = a.uidx[e];

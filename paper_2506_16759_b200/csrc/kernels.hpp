@@ -292,6 +292,7 @@ void launch_update_B(const UpdateBArgs& a, int grid, cudaStream_t st);
 // cnt2/roff2/skel2, R / R2 the base's expanded basis rows at the row / column skeletons)
 struct UpdateNsArgs {
   int64_t nblocks;
+  const int32_t* ulist = nullptr;   // ordered entries to produce (NULL: 0..nblocks-1; sharded builds)
   const int32_t *os, *ob;       // row / column cluster of entry e
   const int32_t* uidx;          // unique (base) pair of entry e
   const int32_t* us;            // stored orientation of the base's unique pair: rows = us[u]

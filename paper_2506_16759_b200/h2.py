@@ -439,9 +439,13 @@ def build(tree: Tree, kernel=("exp", 0.2), tol=1e-6, sketch=None, entry=None, st
     st = L.h2_build_stats()
     cm = None
     if nonsym:
-        assert comm is None, "the non-symmetric build is single-GPU"
-        check(lib.h2_build_nonsym(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o), _stream(stream),
-                                  C.byref(h), C.byref(st)))
+        if comm is not None:   # sharded non-symmetric construction (h2_build_nonsym_dist)
+            keep.append(comm)
+            check(lib.h2_build_nonsym_dist(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o),
+                                           C.byref(comm.struct), _stream(stream), C.byref(h), C.byref(st)))
+        else:
+            check(lib.h2_build_nonsym(tree.handle, C.byref(sk), C.byref(en), float(tol), C.byref(o),
+                                      _stream(stream), C.byref(h), C.byref(st)))
         return H2Matrix(h, tree, _stats_dict(st), keep, nonsym=True)
     if comm is not None:
         cm = C.byref(comm.struct)

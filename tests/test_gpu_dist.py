@@ -239,3 +239,94 @@ def test_halo_exchange_bitwise_and_fewer_bytes(world, n):
     assert tot_halo < tot_ag, (tot_halo, tot_ag)
     print(f"world {world}: bytes sent per build, all-gather mode {tot_ag}, halo mode {tot_halo} "
           f"({tot_halo / tot_ag:.2f}x)")
+
+
+def _ns_snapshot(H, g):
+    L = g._lib
+    out = {"samples": H.samples}
+    for t in range(H.top_depth, H.tree.leaf_depth + 1):
+        for what in (L.H2_X_RANK, L.H2_X_SKEL, L.H2_X_RANK_C, L.H2_X_SKEL_C):
+            out[(what, t)] = H._export(what, t, dtype=np.int32).copy()
+        for what in (L.H2_X_BASIS, L.H2_X_BASIS_C, L.H2_X_B, L.H2_X_CERT, L.H2_X_CERT_C):
+            out[(what, t)] = H._export(what, t).copy()
+    out["D"] = H._export(L.H2_X_D).copy()
+    return out
+
+
+def _ns_worker(rank, world, port, n, mode, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2506_16759_b200 as g
+        from paper_2506_16759_b200.dist import Comm
+        from synth import uniform_points, lowrank_factor
+        X = uniform_points(n, 3, 4)
+        T = g.Tree(X, 64)
+        comm = Comm()
+        kern = ("exp", 0.2)
+        opts = {}
+        if mode == "callback":
+            calls = []
+
+            def sk(om, y, col0, r0, r1, transpose=0):   # K is symmetric: K^T Psi = K Psi
+                calls.append((r0, r1))
+                g.dense_sketch(T, om, kern, r0, r1, out=y, omega_quarters=True)
+            opts["sketch"] = sk
+        elif mode == "uvt":
+            Hb = g.build(T, kern, 1e-8)
+            U = torch.from_numpy(lowrank_factor(n, 8, 5)).cuda()
+            V = torch.from_numpy(lowrank_factor(n, 8, 6)).cuda()
+            opts["update"] = (Hb, U, V)
+        Hd = g.build(T, kern, 1e-6, nonsym=True, comm=comm, **opts)
+        refused = False
+        try:
+            Hd.matvec(torch.zeros(T.n, 1, dtype=torch.float64, device="cuda"))
+        except g.H2Error:
+            refused = True
+        Hd.allgather(comm)
+        H1 = g.build(T, kern, 1e-6, nonsym=True, **opts)
+        a, b = _ns_snapshot(Hd, g), _ns_snapshot(H1, g)
+        same = {str(k): bool(np.array_equal(a[k], b[k])) for k in b}
+        x = torch.randn(T.n, 3, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+        same["matvec"] = bool(torch.equal(Hd.matvec(x), H1.matvec(x)))
+        if mode == "callback":
+            lo, hi = [c for c in calls if c != (0, T.n)][0] if world > 1 else (0, T.n)
+            same["rows_only"] = hi - lo < T.n
+        q.put((rank, same, refused, comm.calls))
+    except Exception as exc:
+        import traceback
+        traceback.print_exc()
+        q.put((rank, {"error": repr(exc)}, False, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,mode", [(2, 6000, "kernel"), (4, 16384, "kernel"), (2, 6000, "callback"),
+                                          (2, 6000, "uvt")])
+def test_nonsym_distributed_bitwise(world, n, mode):
+    """h2_build_nonsym_dist (S§8(e) for the non-symmetric construction, NEXT #3): row and column
+    sketches sharded by rows, owned-cluster BSR / CPQR-ID / shrink on both sides, ordered blocks
+    with an owned endpoint, halo exchange of both sides' samples; after h2_matrix_allgather bitwise
+    the one-GPU non-symmetric build (both sides' ranks, skeletons, bases, certificates, ordered B
+    and D, and the matvec), for the built-in kernel, a row-range callback and the H^2 + U V^T
+    update."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ns_worker, args=(r, world, port, n, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, same, refused, calls in res:
+        assert "error" not in same, same
+        bad = [k for k, v in same.items() if not v]
+        assert not bad, (rank, bad)
+        assert refused and calls > 0
