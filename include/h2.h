@@ -410,7 +410,8 @@ h2_status h2_build_dist(const h2_tree* tree, const h2_sketch* sketch, const h2_e
  * a level converges when every cluster of both sides passes the test.  Operators: sketch
  * H2_S_DENSE_MATRIX (Z via A^T, cuBLAS), H2_S_CALLBACK (called with req->transpose = 0 and 1)
  * or H2_S_DENSE_KERNEL (the built-in kernels are symmetric: Z = K Psi); entry H2_E_BUILTIN,
- * H2_E_CALLBACK or H2_E_DENSE_MATRIX.  One GPU (h2_build_nonsym_dist: sharded).  The result works with h2_matvec (upward pass
+ * H2_E_CALLBACK or H2_E_DENSE_MATRIX.  One GPU; h2_build_nonsym_dist shards it.  The result works
+ * with h2_matvec (upward pass
  * with V, couplings, downward pass with U) and h2_export: H2_X_RANK/SKEL/BASIS/CERT give the row
  * side, H2_X_*_C the column side; D and B are stored for every ORDERED pair (s, b) in (s, b)
  * order, D_{s,b} m_s x m_b, B_{s,b} = K(I~_s, J~_b) k_s x kc_b.  Errors as h2_build. */
