@@ -2447,6 +2447,54 @@ double verify_impl(const h2_matrix& H, const h2_sketch& S, int q, uint64_t seed,
   return a[0] > 0 ? std::sqrt(a[1] / a[0]) : std::sqrt(a[1]);
 }
 
+// The paper's error measure: ||H - K_blk||_2 and ||K_blk||_2 by `iters` power
+// iterations each from the same unit start vector (column 0 of the h2_omega stream (seed, sid)):
+// x <- A x / ||A x||, estimate ||A x||.  Symmetric H and K_blk (A = H - K_blk is symmetric, so
+// ||A x|| for unit x converges to ||A||_2 from below).  Returns (error estimate, norm estimate).
+std::pair<double, double> power2_impl(const h2_matrix& H, const h2_sketch& S, int iters, uint64_t seed, uint32_t sid,
+                                      cudaStream_t st) {
+  const h2_tree& T = *H.tree;
+  const int nleaf = 1 << T.Dl;
+  DArr<double> x, y, part, acc;
+  DArr<int> nf;
+  x.alloc(T.n, st);
+  y.alloc(T.n, st);
+  part.alloc(nleaf, st);
+  acc.alloc(1, st);
+  nf.alloc(1, st);
+  auto norm2 = [&](const double* v) {
+    H2_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), st));
+    H2_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), st));
+    launch_sumsq_leaf(v, T.d_leaf_begin, 0, nleaf, 1, 0, 1, part.p, st);
+    launch_sumsq_total(part.p, nleaf, acc.p, nf.p, st);
+    double a = 0;
+    int bad = 0;
+    H2_CUDA(cudaMemcpyAsync(&a, acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaMemcpyAsync(&bad, nf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaStreamSynchronize(st));
+    if (bad) throw Error(H2_ERR_NONFINITE, "h2_verify_2norm: non-finite vector");
+    return std::sqrt(a);
+  };
+  auto power = [&](bool diff) {
+    launch_omega(seed, sid, 0, T.n, 0, 1, x.p, 1, st);
+    const double n0 = norm2(x.p);
+    launch_scale(x.p, T.n, 1, 1, 1.0 / n0, st);
+    double nu = 0;
+    for (int it = 0; it < iters; ++it) {
+      apply_sketch_op(T, S, x.p, 1, 1, y.p, 1, false, false, st);              // y = K_blk x
+      if (diff) matvec_impl(H, x.p, 1, y.p, 1, 1, 1.0, -1.0, st);              // y = H x - K_blk x
+      nu = norm2(y.p);
+      if (!(nu > 0)) return 0.0;
+      H2_CUDA(cudaMemcpyAsync(x.p, y.p, sizeof(double) * T.n, cudaMemcpyDeviceToDevice, st));
+      launch_scale(x.p, T.n, 1, 1, 1.0 / nu, st);
+    }
+    return nu;
+  };
+  const double e = power(true);
+  const double k = power(false);
+  return {e, k};
+}
+
 }  // namespace
 
 namespace {
@@ -2509,6 +2557,27 @@ h2_status h2_verify(const h2_matrix* H, const h2_sketch* sketch, int32_t ncols, 
                    (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= H->n),
                "h2_verify: bad sketch");
     *err = verify_impl(*H, *sketch, ncols, seed, stream_id, (cudaStream_t)stream);
+    return H2_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+h2_status h2_verify_2norm(const h2_matrix* H, const h2_sketch* sketch, int32_t iters, uint64_t seed,
+                          uint32_t stream_id, void* stream, double* err, double* abs_err, double* knorm) {
+  try {
+    H2_REQUIRE(H && sketch && err, "h2_verify_2norm: NULL argument");
+    H2_REQUIRE(!H->partial, "h2_verify_2norm: distributed matrix: call h2_matrix_allgather first");
+    H2_REQUIRE(!H->nonsym, "h2_verify_2norm: symmetric matrices only");
+    H2_REQUIRE(iters >= 1 && iters <= 1000, "h2_verify_2norm: need 1 <= iters <= 1000");
+    H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
+                   (sketch->kind == H2_S_H2_LOWRANK && sketch->base && !sketch->base->partial) ||
+                   (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= H->n),
+               "h2_verify_2norm: bad sketch");
+    const auto ek = power2_impl(*H, *sketch, iters, seed, stream_id, (cudaStream_t)stream);
+    *err = ek.second > 0 ? ek.first / ek.second : ek.first;
+    if (abs_err) *abs_err = ek.first;
+    if (knorm) *knorm = ek.second;
     return H2_OK;
   } catch (const Error& e) {
     return fail(e);

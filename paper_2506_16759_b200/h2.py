@@ -281,6 +281,21 @@ class H2Matrix:
         check(lib.h2_verify(self._h, C.byref(sk), q, seed, stream_id, _stream(stream), C.byref(e)))
         return e.value
 
+    def verify_2norm(self, kernel=("exp", 0.2), iters=10, seed=1, stream_id=4, dense=None, stream=None):
+        """The paper's error measure (h2_verify_2norm): (||H - K||_2 / ||K||_2,
+        ||H - K||_2, ||K||_2), each 2-norm by ``iters`` power iterations from column 0 of the Omega
+        stream (seed, stream_id); K the built-in kernel or the dense tree-order operator ``dense``."""
+        sk = L.h2_sketch()
+        sk.kern = _kernel(*kernel)
+        if dense is not None:
+            sk.kind, sk.A, sk.ld_A = L.H2_S_DENSE_MATRIX, dense.data_ptr(), dense.stride(0)
+        else:
+            sk.kind = L.H2_S_DENSE_KERNEL
+        r, e, k = C.c_double(), C.c_double(), C.c_double()
+        check(lib.h2_verify_2norm(self._h, C.byref(sk), iters, seed, stream_id, _stream(stream), C.byref(r),
+                                  C.byref(e), C.byref(k)))
+        return r.value, e.value, k.value
+
     def allgather(self, comm, stream=None):
         """Complete a distributed build on every rank (h2_matrix_allgather; collective)."""
         check(lib.h2_matrix_allgather(self._h, C.byref(comm.struct), _stream(stream)))

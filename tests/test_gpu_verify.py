@@ -47,3 +47,31 @@ def test_verify_dense_operator_and_no_retry_when_off():
     ref = A @ P
     direct = (torch.linalg.norm(H.matvec(P) - ref) / torch.linalg.norm(ref)).item()
     assert abs(e - direct) <= 1e-6 * direct
+
+
+@pytest.mark.parametrize("n,tol,s", [(3000, 1e-6, 0.04), (2048, 1e-4, 3.0)])
+def test_power_method_error_matches_oracle_and_dense(n, tol, s):
+    """The paper's error measure (h2_verify_2norm): ||H - K||_2 / ||K||_2 by power
+    iterations.  Checked against oracle/verify.power_error run on the same operators (the CUDA
+    H as a dense matrix, K by plain torch FP64 ops, the same start vector), and against the exact
+    2-norms (the estimates are lower bounds that converge)."""
+    X = uniform_points(n, 3, 8)
+    T = g.Tree(X, 64)
+    H = g.build(T, ("exp", 0.2), tol, tol_safety=s)
+    r, e, k = H.verify_2norm(("exp", 0.2), iters=40, stream_id=4)
+    Xt = torch.from_numpy(X[T.perm]).cuda()
+    K = torch.exp(-torch.sqrt(((Xt[:, None, :] - Xt[None, :, :]) ** 2).sum(-1)) / 0.2)   # no expanded-square
+    Hd = torch.cat([H.matvec(torch.eye(n, dtype=torch.float64, device="cuda")[:, c:c + 64].contiguous())
+                    for c in range(0, n, 64)], dim=1)
+    Kh, Hh = K.cpu().numpy(), Hd.cpu().numpy()
+    x0 = g.omega(n, 1, seed=1, stream_id=4).cpu().numpy()[:, 0]
+    ro, eo, ko = verify.power_error(lambda x: Hh @ x, lambda x: Kh @ x, x0, 40)
+    assert abs(k - ko) <= 1e-10 * ko
+    # ||H - K|| is ~1e-8 ||K||: H x - K x cancels, and the rounding of K x (DMMA sketch vs numpy)
+    # moves the power iterates; the estimates agree to the iteration's own accuracy
+    assert abs(e - eo) <= 1e-3 * eo
+    ex_e = float(np.linalg.norm(Hh - Kh, 2))
+    ex_k = float(np.linalg.norm(Kh, 2))
+    assert e <= ex_e * (1 + 1e-8) and e >= 0.5 * ex_e
+    assert k <= ex_k * (1 + 1e-12) and k >= (1 - 1e-10) * ex_k
+    assert r <= 2 * tol

@@ -39,3 +39,27 @@ def test_estimate_equals_dense_residual_and_retry_reaches_tol():
     # the estimate tracks the true relative error within the probe count's spread
     true = np.linalg.norm(h2.to_dense(H) - K) / np.linalg.norm(K)
     assert 0.2 * true <= e <= 5 * true
+
+
+
+def test_power_method_pins():
+    """O9: the power-method 2-norm never exceeds the exact 2-norm (a Rayleigh-type
+    lower bound), converges to it for a symmetric matrix with a spectral gap, is exactly the 2-norm
+    for a rank-one matrix after two iterations, and the error ratio of an exact H^2 is 0."""
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.standard_normal((60, 60)))
+    lam = np.concatenate([[5.0, -3.0], rng.uniform(-1, 1, 58)])
+    A = (Q * lam) @ Q.T
+    x0 = rng.standard_normal(60)
+    exact = np.linalg.norm(A, 2)
+    for it in (1, 3, 10):
+        assert verify.power_2norm(lambda x: A @ x, x0, it) <= exact * (1 + 1e-12)
+    assert abs(verify.power_2norm(lambda x: A @ x, x0, 200) - exact) <= 1e-10 * exact
+    u = rng.standard_normal(60)
+    R1 = np.outer(u, u)
+    assert abs(verify.power_2norm(lambda x: R1 @ x, x0, 2) - np.linalg.norm(R1, 2)) <= 1e-12 * np.linalg.norm(R1, 2)
+    r, e, k = verify.power_error(lambda x: A @ x, lambda x: A @ x, x0, 5)
+    assert r == 0.0 and e == 0.0 and k > 0
+    E = 1e-3 * ((Q * rng.uniform(-1, 1, 60)) @ Q.T)       # symmetric difference of known norm
+    r, e, k = verify.power_error(lambda x: (A + E) @ x, lambda x: A @ x, x0, 300)
+    assert abs(e - np.linalg.norm(E, 2)) <= 1e-6 * np.linalg.norm(E, 2) and abs(k - exact) <= 1e-10 * exact
