@@ -2,6 +2,8 @@
 #include "alloc.hpp"
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -78,6 +80,12 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
     return b.p;
   }
   void* p = nullptr;
+  static const bool trace_alloc = getenv("H2_TRACE_ALLOC") != nullptr;
+  if (trace_alloc) {
+    auto nx = c.free_.lower_bound(want);
+    fprintf(stderr, "[h2 alloc] miss %.3f GB (next free %.3f GB, %zu free blocks, %.1f GB held)\n", want / 1e9,
+            nx == c.free_.end() ? -1.0 : nx->first / 1e9, c.free_.size(), c.held / 1e9);
+  }
   cudaError_t e = cudaMalloc(&p, want);
   // out of device memory: release as little of the cache as the request needs -- first the
   // smallest free block that covers the deficit (want - the device's free memory), else the
@@ -90,6 +98,7 @@ void* cache_alloc(size_t bytes, cudaStream_t st) {
     cudaMemGetInfo(&fr, &tot);
     const size_t deficit = want > fr ? want - fr + (size_t(64) << 20) : (size_t(64) << 20);
     auto drop = [&](std::multimap<size_t, Block>::iterator it) {
+      if (trace_alloc) fprintf(stderr, "[h2 alloc] drop %.3f GB\n", it->first / 1e9);
       cudaEventSynchronize(it->second.ready);
       cudaEventDestroy(it->second.ready);
       cudaFree(it->second.p);
