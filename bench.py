@@ -389,7 +389,7 @@ def run_ours(args, w, rank, world, local_rank):
     achieved = entries_launch * F_EVAL / (per_launch_ms * 1e-3) / 1e12
     int8_ops = entries_launch * ncol_launch * slices * 2 / (per_launch_ms * 1e-3) / 1e12
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_sketch_tc_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2_sketch_tc_traffic.json")
     if os.path.exists(tpath) and args.workload == "cov3d_256k" and world == 1:
         traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
     # e2e through the public API from host buffers: tree build + H2D + build + D2H of skeletons
