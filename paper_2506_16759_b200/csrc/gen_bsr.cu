@@ -533,6 +533,23 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
       const int main = a.ncols / 64 * 64;
       BsrArgs m = a;
       m.ncols = main;
+      // the tail columns on a second stream, concurrent with the 64-column launch (disjoint output
+      // columns, the same arithmetic: bitwise; the tail's CTAs fill the main launch's last waves):
+      // C2 BSR phase 47.6 -> 44.7 ms (tools/ab_phases.py); H2_BSR_TAIL_STREAM=0 serialises
+      static const int tail_stream = env_int("H2_BSR_TAIL_STREAM", 1);
+      cudaStream_t ts = st;
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      if (tail_stream && main > 0 && a.ncols > main) {
+        static cudaStream_t side[64] = {};
+        int dev = 0;
+        H2_CUDA(cudaGetDevice(&dev));
+        if (!side[dev & 63]) H2_CUDA(cudaStreamCreateWithFlags(&side[dev & 63], cudaStreamNonBlocking));
+        ts = side[dev & 63];
+        H2_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        H2_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+        H2_CUDA(cudaEventRecord(ev0, st));   // everything before this BSR on st
+        H2_CUDA(cudaStreamWaitEvent(ts, ev0, 0));
+      }
       if (main == 0) {
       } else if (v2 == 8) bsr2_go<64, 2, true, 32, 4>(m, alpha, st);
       else if (v2 == 9) bsr2_go<64, 2, true, 16, 4>(m, alpha, st);
@@ -541,8 +558,14 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
         BsrArgs t = a;
         t.c0 = a.c0 + main;
         t.ncols = a.ncols - main;
-        if (v2 == 12) bsr2_go<32, 2, true, 16, 4>(t, alpha, st);   // tail in 32 x 32 warp tiles too
-        else bsr2_go<32, 2, true>(t, alpha, st);
+        if (v2 == 12) bsr2_go<32, 2, true, 16, 4>(t, alpha, ts);   // tail in 32 x 32 warp tiles too
+        else bsr2_go<32, 2, true>(t, alpha, ts);
+        if (ts != st) {
+          H2_CUDA(cudaEventRecord(ev1, ts));
+          H2_CUDA(cudaStreamWaitEvent(st, ev1, 0));
+          H2_CUDA(cudaEventDestroy(ev0));
+          H2_CUDA(cudaEventDestroy(ev1));
+        }
       }
     }
     else wide ? bsr2_go<32, 2, true>(a, alpha, st) : bsr2_go<32, 2, false>(a, alpha, st);
