@@ -21,7 +21,8 @@ def _cases():
     neg = rng.standard_normal((20000, 2))        # negative coordinates, -0.0
     neg[::97, 0] = -0.0
     neg[1::97, 0] = 0.0
-    return {"u3_2^16": (uniform_points(1 << 16, 3, 0), 64), "u2_50000": (uniform_points(50000, 2, 1), 32),
+    return {"u3_2^18_bench": (uniform_points(1 << 18, 3, 0), 64),   # the bench's e2e tree (configs[1])
+            "u3_2^16": (uniform_points(1 << 16, 3, 0), 64), "u2_50000": (uniform_points(50000, 2, 1), 32),
             "u1_9999": (uniform_points(9999, 1, 4), 16), "grid32": (grid_points((32, 32, 32), 1 / 32), 64),
             "dup": (dup, 40), "ties": (half, 50), "signed": (neg, 24)}
 
