@@ -442,12 +442,14 @@ h2_status h2_matvec(const h2_matrix* H, const double* x, int64_t ldx, double* y,
 /* The paper's error measure ("a few iterations of the power method to approximate
  * the 2-norm of the difference between the constructed hierarchical matrix and the provided
  * sampler"): ||H - K_blk||_2 and ||K_blk||_2, each by `iters` power iterations
- * x <- A x / ||A x|| from the same unit start vector (column 0 of the h2_omega stream (seed,
- * stream_id)), estimate ||A x||; both operators symmetric (symmetric H, K_blk = `sketch`, any
- * kind, applied to one column: the FP64 DMMA path for the built-in kernels).  *err = the ratio;
- * abs_err / knorm (may be NULL) the two estimates (each <= the true 2-norm).  1 <= iters <= 1000.
+ * x <- A x / ||A x|| run independently from nvec unit start vectors (columns 0..nvec-1 of the
+ * h2_omega stream (seed, stream_id)) in one block -- the dense sketch costs the same for 1 or 16
+ * columns -- estimate = the largest ||A x|| of the last iteration; both operators symmetric
+ * (symmetric H, K_blk = `sketch`, any kind: the FP64 DMMA path for the built-in kernels).
+ * *err = the ratio; abs_err / knorm (may be NULL) the two estimates (each <= the true 2-norm).
+ * 1 <= iters <= 1000, 1 <= nvec <= 64.
  * Errors: INVALID_ARG (partial or non-symmetric matrix, bad sketch), CUDA, CALLBACK, NONFINITE. */
-h2_status h2_verify_2norm(const h2_matrix* H, const h2_sketch* sketch, int32_t iters, uint64_t seed,
+h2_status h2_verify_2norm(const h2_matrix* H, const h2_sketch* sketch, int32_t iters, int32_t nvec, uint64_t seed,
                           uint32_t stream_id, void* stream, double* err, double* abs_err, double* knorm);
 
 /* A-posteriori error estimate: Om_h = ncols columns of the

@@ -126,7 +126,7 @@ SIGNATURES = {
     "h2_cache_bytes": (C.c_int64, []),
     "h2_cache_trim": (None, []),
     "h2_verify": (C.c_int, [_P, C.POINTER(h2_sketch), C.c_int32, C.c_uint64, C.c_uint32, _P, C.POINTER(C.c_double)]),
-    "h2_verify_2norm": (C.c_int, [_P, C.POINTER(h2_sketch), C.c_int32, C.c_uint64, C.c_uint32, _P,
+    "h2_verify_2norm": (C.c_int, [_P, C.POINTER(h2_sketch), C.c_int32, C.c_int32, C.c_uint64, C.c_uint32, _P,
                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "h2_build_dist": (C.c_int, [_P, C.POINTER(h2_sketch), C.POINTER(h2_entry), C.c_double, C.POINTER(h2_build_opts),
                                 C.POINTER(h2_comm), _P, C.POINTER(_P), C.POINTER(h2_build_stats)]),

@@ -2448,47 +2448,54 @@ double verify_impl(const h2_matrix& H, const h2_sketch& S, int q, uint64_t seed,
 }
 
 // The paper's error measure: ||H - K_blk||_2 and ||K_blk||_2 by `iters` power
-// iterations each from the same unit start vector (column 0 of the h2_omega stream (seed, sid)):
-// x <- A x / ||A x||, estimate ||A x||.  Symmetric H and K_blk (A = H - K_blk is symmetric, so
-// ||A x|| for unit x converges to ||A||_2 from below).  Returns (error estimate, norm estimate).
-std::pair<double, double> power2_impl(const h2_matrix& H, const h2_sketch& S, int iters, uint64_t seed, uint32_t sid,
-                                      cudaStream_t st) {
+// iterations each, run independently from nvec unit start vectors (columns 0..nvec-1 of the h2_omega
+// stream (seed, sid)) side by side -- one sketch call per iteration for all of them, the dense
+// sketch's cost being its kernel evaluations -- x <- A x / ||A x||; the estimate is the largest
+// ||A x|| of the last iteration.  Symmetric H and K_blk (A = H - K_blk symmetric: ||A x|| for unit x
+// converges to ||A||_2 from below).  Returns (error estimate, norm estimate).
+std::pair<double, double> power2_impl(const h2_matrix& H, const h2_sketch& S, int iters, int nvec, uint64_t seed,
+                                      uint32_t sid, cudaStream_t st) {
   const h2_tree& T = *H.tree;
   const int nleaf = 1 << T.Dl;
+  const int q = nvec;
   DArr<double> x, y, part, acc;
   DArr<int> nf;
-  x.alloc(T.n, st);
-  y.alloc(T.n, st);
+  x.alloc(T.n * q, st);
+  y.alloc(T.n * q, st);
   part.alloc(nleaf, st);
-  acc.alloc(1, st);
+  acc.alloc(q, st);
   nf.alloc(1, st);
-  auto norm2 = [&](const double* v) {
-    H2_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), st));
+  std::vector<double> nrm(q);
+  auto norms = [&](const double* v) {   // per-column 2-norms of an n x q row-major block
+    H2_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * q, st));
     H2_CUDA(cudaMemsetAsync(nf.p, 0, sizeof(int), st));
-    launch_sumsq_leaf(v, T.d_leaf_begin, 0, nleaf, 1, 0, 1, part.p, st);
-    launch_sumsq_total(part.p, nleaf, acc.p, nf.p, st);
-    double a = 0;
+    for (int c = 0; c < q; ++c) {
+      launch_sumsq_leaf(v, T.d_leaf_begin, 0, nleaf, q, c, c + 1, part.p, st);
+      launch_sumsq_total(part.p, nleaf, acc.p + c, nf.p, st);
+    }
     int bad = 0;
-    H2_CUDA(cudaMemcpyAsync(&a, acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    H2_CUDA(cudaMemcpyAsync(nrm.data(), acc.p, sizeof(double) * q, cudaMemcpyDeviceToHost, st));
     H2_CUDA(cudaMemcpyAsync(&bad, nf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     H2_CUDA(cudaStreamSynchronize(st));
     if (bad) throw Error(H2_ERR_NONFINITE, "h2_verify_2norm: non-finite vector");
-    return std::sqrt(a);
+    for (double& v : nrm) v = std::sqrt(v);
   };
   auto power = [&](bool diff) {
-    launch_omega(seed, sid, 0, T.n, 0, 1, x.p, 1, st);
-    const double n0 = norm2(x.p);
-    launch_scale(x.p, T.n, 1, 1, 1.0 / n0, st);
-    double nu = 0;
+    launch_omega(seed, sid, 0, T.n, 0, q, x.p, q, st);
+    norms(x.p);
+    for (int c = 0; c < q; ++c) launch_scale(x.p + c, T.n, q, 1, 1.0 / nrm[c], st);
+    double best = 0;
     for (int it = 0; it < iters; ++it) {
-      apply_sketch_op(T, S, x.p, 1, 1, y.p, 1, false, false, st);              // y = K_blk x
-      if (diff) matvec_impl(H, x.p, 1, y.p, 1, 1, 1.0, -1.0, st);              // y = H x - K_blk x
-      nu = norm2(y.p);
-      if (!(nu > 0)) return 0.0;
-      H2_CUDA(cudaMemcpyAsync(x.p, y.p, sizeof(double) * T.n, cudaMemcpyDeviceToDevice, st));
-      launch_scale(x.p, T.n, 1, 1, 1.0 / nu, st);
+      apply_sketch_op(T, S, x.p, q, q, y.p, q, false, false, st);              // y = K_blk x
+      if (diff) matvec_impl(H, x.p, q, y.p, q, q, 1.0, -1.0, st);              // y = H x - K_blk x
+      norms(y.p);
+      best = 0;
+      for (int c = 0; c < q; ++c) best = std::max(best, nrm[c]);
+      if (!(best > 0)) return 0.0;
+      H2_CUDA(cudaMemcpyAsync(x.p, y.p, sizeof(double) * T.n * q, cudaMemcpyDeviceToDevice, st));
+      for (int c = 0; c < q; ++c) launch_scale(x.p + c, T.n, q, 1, nrm[c] > 0 ? 1.0 / nrm[c] : 0.0, st);
     }
-    return nu;
+    return best;
   };
   const double e = power(true);
   const double k = power(false);
@@ -2563,18 +2570,19 @@ h2_status h2_verify(const h2_matrix* H, const h2_sketch* sketch, int32_t ncols, 
   }
 }
 
-h2_status h2_verify_2norm(const h2_matrix* H, const h2_sketch* sketch, int32_t iters, uint64_t seed,
+h2_status h2_verify_2norm(const h2_matrix* H, const h2_sketch* sketch, int32_t iters, int32_t nvec, uint64_t seed,
                           uint32_t stream_id, void* stream, double* err, double* abs_err, double* knorm) {
   try {
     H2_REQUIRE(H && sketch && err, "h2_verify_2norm: NULL argument");
     H2_REQUIRE(!H->partial, "h2_verify_2norm: distributed matrix: call h2_matrix_allgather first");
     H2_REQUIRE(!H->nonsym, "h2_verify_2norm: symmetric matrices only");
-    H2_REQUIRE(iters >= 1 && iters <= 1000, "h2_verify_2norm: need 1 <= iters <= 1000");
+    H2_REQUIRE(iters >= 1 && iters <= 1000 && nvec >= 1 && nvec <= 64,
+               "h2_verify_2norm: need 1 <= iters <= 1000, 1 <= nvec <= 64");
     H2_REQUIRE(sketch->kind == H2_S_DENSE_KERNEL || (sketch->kind == H2_S_CALLBACK && sketch->fn) ||
                    (sketch->kind == H2_S_H2_LOWRANK && sketch->base && !sketch->base->partial) ||
                    (sketch->kind == H2_S_DENSE_MATRIX && sketch->A && sketch->ld_A >= H->n),
                "h2_verify_2norm: bad sketch");
-    const auto ek = power2_impl(*H, *sketch, iters, seed, stream_id, (cudaStream_t)stream);
+    const auto ek = power2_impl(*H, *sketch, iters, nvec, seed, stream_id, (cudaStream_t)stream);
     *err = ek.second > 0 ? ek.first / ek.second : ek.first;
     if (abs_err) *abs_err = ek.first;
     if (knorm) *knorm = ek.second;

@@ -281,10 +281,11 @@ class H2Matrix:
         check(lib.h2_verify(self._h, C.byref(sk), q, seed, stream_id, _stream(stream), C.byref(e)))
         return e.value
 
-    def verify_2norm(self, kernel=("exp", 0.2), iters=10, seed=1, stream_id=4, dense=None, stream=None):
+    def verify_2norm(self, kernel=("exp", 0.2), iters=10, nvec=1, seed=1, stream_id=4, dense=None, stream=None):
         """The paper's error measure (h2_verify_2norm): (||H - K||_2 / ||K||_2,
-        ||H - K||_2, ||K||_2), each 2-norm by ``iters`` power iterations from column 0 of the Omega
-        stream (seed, stream_id); K the built-in kernel or the dense tree-order operator ``dense``."""
+        ||H - K||_2, ||K||_2), each 2-norm by ``iters`` power iterations from columns 0..nvec-1 of
+        the Omega stream (seed, stream_id), the largest estimate; K the built-in kernel or the dense
+        tree-order operator ``dense``."""
         sk = L.h2_sketch()
         sk.kern = _kernel(*kernel)
         if dense is not None:
@@ -292,7 +293,7 @@ class H2Matrix:
         else:
             sk.kind = L.H2_S_DENSE_KERNEL
         r, e, k = C.c_double(), C.c_double(), C.c_double()
-        check(lib.h2_verify_2norm(self._h, C.byref(sk), iters, seed, stream_id, _stream(stream), C.byref(r),
+        check(lib.h2_verify_2norm(self._h, C.byref(sk), iters, nvec, seed, stream_id, _stream(stream), C.byref(r),
                                   C.byref(e), C.byref(k)))
         return r.value, e.value, k.value
 

@@ -75,3 +75,6 @@ def test_power_method_error_matches_oracle_and_dense(n, tol, s):
     assert e <= ex_e * (1 + 1e-8) and e >= 0.5 * ex_e
     assert k <= ex_k * (1 + 1e-12) and k >= (1 - 1e-10) * ex_k
     assert r <= 2 * tol
+    # several start vectors side by side: each column the 1-vector iteration, the best kept
+    r8, e8, k8 = H.verify_2norm(("exp", 0.2), iters=40, nvec=8, stream_id=4)
+    assert e8 >= e * (1 - 1e-12) and e8 <= ex_e * (1 + 1e-8) and abs(k8 - ex_k) <= 1e-10 * ex_k
