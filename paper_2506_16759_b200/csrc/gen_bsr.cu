@@ -1,5 +1,7 @@
 // batchedGen (PAPER.md L212 D blocks, L258 B blocks, L384 batched entry generator) and the
 // non-uniform batched block-sparse-row product batchedBSRGemm (L213, L240-243, L385).
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -540,11 +542,15 @@ static void bsr_launch(const BsrArgs& a, double alpha, cudaStream_t st) {
       cudaStream_t ts = st;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (tail_stream && main > 0 && a.ncols > main) {
+        static std::mutex mu;   // builds may run on several host threads / devices
         static cudaStream_t side[64] = {};
         int dev = 0;
         H2_CUDA(cudaGetDevice(&dev));
-        if (!side[dev & 63]) H2_CUDA(cudaStreamCreateWithFlags(&side[dev & 63], cudaStreamNonBlocking));
-        ts = side[dev & 63];
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!side[dev & 63]) H2_CUDA(cudaStreamCreateWithFlags(&side[dev & 63], cudaStreamNonBlocking));
+          ts = side[dev & 63];
+        }
         H2_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
         H2_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
         H2_CUDA(cudaEventRecord(ev0, st));   // everything before this BSR on st
