@@ -661,26 +661,34 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_full + 8 * buf));
 
       const bool drain = ((it % P::DRAIN) == P::DRAIN - 1) || (it == nch - 1);
-      if (PACK && drain && warp < 4) {
+      // near-field mode: its only drain is the final one (a few chunks per CTA), and every producer
+      // warp has finished -- all NPW / 4 warp quartets drain, each a quarter of the column groups
+      // (the same per-entry arithmetic; the A buffers, idle after the last MMA, hold the hand-off)
+      constexpr int NREP = (nearm && NPW % 4 == 0) ? NPW / 4 : 1;
+      const bool all_drain = NREP > 1 && it == nch - 1;
+      if (PACK && drain && (warp < 4 || all_drain)) {
         mbar_wait(bar_drain, drains & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         // lane 32 w + l: row 32 (w & 1) + l; warps 0-1 hold slices 0-2 (pairs' low halves), warps
         // 2-3 slices 3-5.  Chains (s0..s2) and (s3..s5) as in the other shapes; the high warps hand
         // theirs to the low warps through the coordinate slot of this chunk (consumed, and not
         // refilled before chunk it + 4), 8 columns at a time.
-        const int64_t i = rtile + 32 * (warp & 1) + lane;
-        const bool high = warp >= 2;
-        double* xb = reinterpret_cast<double*>(smem + P::C0 + slot * CBUF) + (32 * (warp & 1) + lane) * 8;
+        const int wq = warp & 3, rep = all_drain ? warp >> 2 : 0;
+        const int i_stride = all_drain ? 8 * NREP : 8;
+        const int64_t i = rtile + 32 * (wq & 1) + lane;
+        const bool high = wq >= 2;
+        double* xb = all_drain ? reinterpret_cast<double*>(smem + P::A0) + rep * 512 + (32 * (wq & 1) + lane) * 8
+                               : reinterpret_cast<double*>(smem + P::C0 + slot * CBUF) + (32 * (warp & 1) + lane) * 8;
         double* y = Yo + (i - row0) * ldy;
 #pragma unroll 1
-        for (int c0 = 0; c0 < NCOL; c0 += 8) {
+        for (int c0 = 8 * rep; c0 < NCOL; c0 += i_stride) {
           double v[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[c] = 0.0;
 #pragma unroll
           for (int p = 0; p < 3; ++p) {
             uint32_t r[8];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(p * NCOL + c0);
+            const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(p * NCOL + c0);
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                            "=r"(r[7])
@@ -694,7 +702,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
 #pragma unroll
             for (int c = 0; c < 8; ++c) xb[c] = v[c];
           }
-          asm volatile("bar.sync 1, 128;\n" ::);
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + rep));
           if (!high && i < row1) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -702,7 +710,7 @@ __global__ void __launch_bounds__(32 * (NPW + 1), 1)
               if (c0 + c < ncols) y[c0 + c] = nearm ? y[c0 + c] - t : drains == 0 ? t : y[c0 + c] + t;
             }
           }
-          asm volatile("bar.sync 1, 128;\n" ::);
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + rep));
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       } else if (PACK7 && drain && warp < 4) {
