@@ -2194,9 +2194,8 @@ bool ensure_near_chunks(const h2_tree* tree) {
     }
   }
   ptr[nleaf] = (int32_t)chunk.size();
-  auto up = [](const void* src, size_t bytes) {
-    void* p = nullptr;
-    H2_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
+  auto up = [](const void* src, size_t bytes) {   // block cache, as every tree array (tree.cpp)
+    void* p = h2::cache_alloc(std::max<size_t>(bytes, 4), nullptr);
     if (bytes) H2_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
     return p;
   };

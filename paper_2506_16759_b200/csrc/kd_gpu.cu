@@ -209,7 +209,7 @@ __global__ void kd_iota_kernel(int* v, int n) {
 // Device KD ordering.  X: host coordinates (n x dim, original order); seg_all: the node ranges of
 // depths 0..Dl-1 concatenated (depth t: 2^t + 1 offsets).  Outputs (cudaMalloc'd, owned by the
 // caller): perm_dev (tree index -> original index), xt / yt / zt (tree order, zero-padded),
-// iota_dev; root_box[6] (host) = the bounding box of all points.
+// iota_dev, from the block cache (free them with cache_free); root_box[6] (host) = the bounding box.
 void kd_order_device(const double* X, int64_t n64, int dim, int Dl, const std::vector<int>& seg_all, int** perm_dev,
                      double** xt, double** yt, double** zt, int** iota_dev, double* root_box, cudaStream_t st) {
   const int n = (int)n64;
@@ -286,11 +286,13 @@ void kd_order_device(const double* X, int64_t n64, int dim, int Dl, const std::v
     H2_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, sk[0], sk[1], val[1], idx, n, 0, bits, st));
     off += (size_t)nseg + 1;
   }
-  H2_CUDA(cudaMalloc(perm_dev, sizeof(int) * (size_t)std::max(n, 1)));
-  H2_CUDA(cudaMalloc(xt, sizeof(double) * (size_t)std::max(n, 1)));
-  H2_CUDA(cudaMalloc(yt, sizeof(double) * (size_t)std::max(n, 1)));
-  H2_CUDA(cudaMalloc(zt, sizeof(double) * (size_t)std::max(n, 1)));
-  H2_CUDA(cudaMalloc(iota_dev, sizeof(int) * (size_t)std::max(n, 1)));
+  // the tree's order arrays come from the block cache (h2_tree::order_cached): no cudaMalloc /
+  // cudaFree per tree (their driver latency varied by 1-20 ms in the end-to-end loop)
+  *perm_dev = static_cast<int*>(cache_alloc(sizeof(int) * (size_t)std::max(n, 1), st));
+  *xt = static_cast<double*>(cache_alloc(sizeof(double) * (size_t)std::max(n, 1), st));
+  *yt = static_cast<double*>(cache_alloc(sizeof(double) * (size_t)std::max(n, 1), st));
+  *zt = static_cast<double*>(cache_alloc(sizeof(double) * (size_t)std::max(n, 1), st));
+  *iota_dev = static_cast<int*>(cache_alloc(sizeof(int) * (size_t)std::max(n, 1), st));
   H2_CUDA(cudaMemcpyAsync(*perm_dev, idx, sizeof(int) * (size_t)n, cudaMemcpyDeviceToDevice, st));
   kd_finish_kernel<<<grid1, 256, 0, st>>>(dX, dim, idx, n, *xt, *yt, *zt, *iota_dev);
   H2_CHECK_LAUNCH();

@@ -11,6 +11,7 @@
 #include <numeric>
 #include <thread>
 
+#include "alloc.hpp"
 #include "common.cuh"
 #include "tree.hpp"
 
@@ -287,11 +288,11 @@ void tree_build_order_gpu(h2_tree& T, const double* X, int64_t n, int dim, int l
   {
     std::vector<int64_t> lb(T.begin[Dl]);
     lb.push_back(n);
-    H2_CUDA(cudaMalloc(&T.d_leaf_begin, lb.size() * sizeof(int64_t)));
+    T.d_leaf_begin = static_cast<int64_t*>(h2::cache_alloc(lb.size() * sizeof(int64_t), nullptr));
     H2_CUDA(cudaMemcpy(T.d_leaf_begin, lb.data(), lb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     std::vector<int32_t> ls(T.begin[Dl].size());
     for (size_t c = 0; c < ls.size(); ++c) ls[c] = (int32_t)(T.end[Dl][c] - T.begin[Dl][c]);
-    H2_CUDA(cudaMalloc(&T.d_leaf_size, std::max<size_t>(ls.size(), 1) * sizeof(int32_t)));
+    T.d_leaf_size = static_cast<int32_t*>(h2::cache_alloc(std::max<size_t>(ls.size(), 1) * sizeof(int32_t), nullptr));
     H2_CUDA(cudaMemcpy(T.d_leaf_size, ls.data(), ls.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   // the bounding-box diagonal as the host computes it (tree-order coordinates, zero-padded to 3D)
@@ -549,9 +550,10 @@ void tree_import_host(h2_tree& T, const h2_tree_desc& D) {
 namespace {
 template <class V>
 typename V::value_type* upload(const V& v) {
-  typename V::value_type* p = nullptr;
+  // the tree's device arrays live in libh2's block cache: no cudaMalloc / cudaFree (device-
+  // synchronising, latency varying by 1-20 ms) per tree once the cache holds the sizes
   size_t bytes = std::max<size_t>(1, v.size()) * sizeof(typename V::value_type);
-  H2_CUDA(cudaMalloc(&p, bytes));
+  auto* p = static_cast<typename V::value_type*>(h2::cache_alloc(bytes, nullptr));
   if (!v.empty()) H2_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(typename V::value_type), cudaMemcpyHostToDevice));
   return p;
 }
@@ -565,11 +567,7 @@ DeviceCSR upload_csr(const PairCSR& C) {
   return d;
 }
 void free_csr(DeviceCSR& d) {
-  cudaFree(d.ptr);
-  cudaFree(d.idx);
-  cudaFree(d.uidx);
-  cudaFree(d.us);
-  cudaFree(d.ub);
+  for (void* p : {(void*)d.ptr, (void*)d.idx, (void*)d.uidx, (void*)d.us, (void*)d.ub}) h2::cache_free(p, nullptr);
   d = DeviceCSR{};
 }
 }  // namespace
@@ -617,18 +615,12 @@ h2_tree::~h2_tree() {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  cudaFree(d_x);
-  cudaFree(d_y);
-  cudaFree(d_z);
-  cudaFree(d_iota);
-  cudaFree(d_perm);
-  cudaFree(d_leaf_begin);
-  cudaFree(d_leaf_size);
-  cudaFree(d_D_off);
+  // every device array of the tree comes from the block cache: back to it, no device sync
+  for (void* p : {(void*)d_x, (void*)d_y, (void*)d_z, (void*)d_iota, (void*)d_perm, (void*)d_leaf_begin,
+                  (void*)d_leaf_size, (void*)d_D_off})
+    h2::cache_free(p, nullptr);
   free_csr(d_near);
   for (auto& f : d_far) free_csr(f);
-  cudaFree(d_nl_ptr);
-  cudaFree(d_nl_chunk);
-  cudaFree(d_nl_mask);
+  for (void* p : {(void*)d_nl_ptr, (void*)d_nl_chunk, (void*)d_nl_mask}) h2::cache_free(p, nullptr);
   cudaSetDevice(prev);
 }

@@ -8,7 +8,7 @@ from synth import uniform_points
 X = uniform_points(1 << 18, 3, 0)
 Xpin = torch.from_numpy(X).pin_memory()
 torch.cuda.synchronize()
-for rep in range(4):
+for rep in range(int(os.environ.get("REPS", 4))):
     t0 = time.perf_counter(); T = g.Tree(Xpin.numpy(), 64, 0.7, asynchronous=True); t1 = time.perf_counter()
     H = g.build(T, ("exp", 0.2), 1e-6); t2 = time.perf_counter()
     torch.cuda.synchronize(); t3 = time.perf_counter()
